@@ -1,0 +1,205 @@
+/* sof_cuda.h — C-ABI of libsof_cuda.so, the B200-native SOF hot path.
+ *
+ * This is the drop-in boundary for the sorted opacity-field evaluator, the
+ * Marching-Tetrahedra mesher and the sorted rasterizer of arXiv 2506.19139.
+ * The reference (/root/reference/proj/include/sof, header-only C++20, CPU) has
+ * no FFI of its own; every entry point below names the reference function it
+ * replaces (file:line under proj/include/sof/). The C++ host API in
+ * include/sof_b200/*.hpp and the Python package paper_2506_19139_b200 both call
+ * only these functions.
+ *
+ * Conventions
+ *   - plain pointers and sizes, no C++ or torch types; host pointers unless the
+ *     name ends in _dev (device pointers on the context's GPU);
+ *   - every function returns an int status: SOF_OK (0) or a negative SOF_E_*;
+ *     sof_last_error(ctx) returns the message (e.g. "non-finite Gaussian
+ *     parameters", precompute.hpp:60-63);
+ *   - arrays: scene pos[3n], scale[3n], rot_wxyz[4n], opacity[n], dc[3n] (activated
+ *     values, GaussianPrimitive gaussian.hpp:12-18); cameras R[9V] row-major
+ *     world-to-view, t[3V], intr[4V] = {fx, fy, cx, cy}, wh[2V] = {width, height},
+ *     nearfar[2V] (Camera camera.hpp:10-21); points xyz[3n]; tets int32[4nt];
+ *   - strategies: bit mask of SOF_TILE_SCHEDULING ... SOF_DEAD_CULL
+ *     (EvalStrategies field_eval.hpp:14-23);
+ *   - counters: uint64[2] = {pairs, point_view_evals} accumulated into by the call
+ *     (EvalCounters field_eval.hpp:25-29, exact reference semantics);
+ *   - a context owns one GPU and all device memory; use it from one host thread
+ *     at a time; variable-size results stay on the device until copied out with
+ *     sof_copy_result.
+ */
+#ifndef SOF_CUDA_H
+#define SOF_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SOF_OK = 0,
+  SOF_E_INVALID = -1, /* bad argument: std::invalid_argument in the reference */
+  SOF_E_CUDA = -2,    /* CUDA runtime error */
+  SOF_E_NCCL = -3,    /* collective error */
+  SOF_E_OOM = -4,     /* device allocation failed */
+  SOF_E_STATE = -5,   /* missing scene / views / tets, or no result of that kind */
+  SOF_E_RUNTIME = -6  /* std::runtime_error in the reference (e.g. "no live Gaussians") */
+};
+
+enum {
+  SOF_TILE_SCHEDULING = 1,
+  SOF_MIN_Z = 2,
+  SOF_EARLY_STOP = 4,
+  SOF_PRUNE = 8,
+  SOF_DEAD_CULL = 16,
+  SOF_ALL_STRATEGIES = 31 /* EvalStrategies::all(), field_eval.hpp:22 */
+};
+
+enum { SOF_DEPTH_MEDIAN = 0, SOF_DEPTH_EXACT = 1 }; /* DepthMode opacity_field.hpp:199 */
+
+/* result kinds for sof_result_count / sof_copy_result */
+enum {
+  SOF_R_EDGES = 1,         /* int32[2E]  CrossingEdge{inside, outside} (marching_tets.hpp:16-19) */
+  SOF_R_EDGE_VERTS = 2,    /* f64[3E]    MarchingResult::vertices (lerp, then refined) */
+  SOF_R_TRIANGLES = 3,     /* int32[3T]  MarchingResult::triangles */
+  SOF_R_MESH_VERTS = 4,    /* f64[3V]    Mesh::vertices after assemble_mesh */
+  SOF_R_MESH_TRIS = 5,     /* int32[3T]  Mesh::triangles after assemble_mesh */
+  SOF_R_GRID_OPACITY = 6,  /* f64[nv]    TetGrid::opacity after label_grid */
+  SOF_R_TILE_OFFSETS = 7,  /* int64[T+1] per-tile list offsets of the last binding */
+  SOF_R_TILE_ENTRIES = 8   /* int32[M]   per-tile Gaussian lists (TileBinding, tiles.hpp:88-92) */
+};
+
+typedef struct sof_ctx sof_ctx;
+
+/* Options of the fused label -> march -> refine -> weld pipeline
+ * (ExtractOptions extract.hpp:12-20 minus the seed/Delaunay producer). */
+typedef struct sof_extract_opts {
+  int strategies;        /* default SOF_ALL_STRATEGIES */
+  int tile_size;         /* default 16 (kDefaultTileSize tiles.hpp:14) */
+  int refine_iterations; /* default 8 */
+  double weld_eps;       /* default 1e-7 (mesh.hpp:38) */
+  double min_area;       /* default 1e-14 (mesh.hpp:38) */
+  int view_begin;        /* views [view_begin, view_end) of this rank; -1/-1 = all */
+  int view_end;
+} sof_extract_opts;
+
+/* Per-stage statistics (ExtractStats extract.hpp:22-33) plus device timings. */
+typedef struct sof_extract_stats {
+  int64_t crossing_edges;
+  int64_t march_triangles;
+  int64_t mesh_vertices;
+  int64_t mesh_triangles;
+  uint64_t pairs;            /* label + refine, reference `pairs` semantics */
+  uint64_t point_view_evals;
+  uint64_t label_pairs;
+  uint64_t refine_pairs;
+  double ms_label;           /* device time per stage (CUDA events) */
+  double ms_march;
+  double ms_refine;
+  double ms_weld;
+  double ms_eval_kernel;     /* summed duration of the opacity-eval kernel launches */
+  int64_t eval_launches;     /* number of opacity-eval kernel launches */
+  int64_t kernel_launches;   /* all kernels launched by the call */
+} sof_extract_stats;
+
+/* ---- context --------------------------------------------------------------- */
+int sof_ctx_create(int device, sof_ctx** out);
+void sof_ctx_destroy(sof_ctx* ctx);
+const char* sof_last_error(const sof_ctx* ctx);
+int sof_version(void);
+/* number of kernels launched on this context so far (instrumentation) */
+int64_t sof_kernel_launches(const sof_ctx* ctx);
+
+/* ---- inputs ----------------------------------------------------------------- */
+/* Replaces the scene half of ViewSet::build (opacity_field.hpp:26-34) and the
+ * view-independent half of precompute (precompute.hpp:57-78): uploads the
+ * Gaussians and computes Sigma^-1, the filtered opacity and E on the device. */
+int sof_set_scene(sof_ctx* ctx, int64_t n, const double* pos, const double* scale,
+                  const double* rot_wxyz, const double* opacity, const double* dc,
+                  double filter_scale);
+/* The cameras of the ViewSet. Per-view preprocessing runs lazily on the device. */
+int sof_set_views(sof_ctx* ctx, int v, const double* R, const double* t, const double* intr,
+                  const int32_t* wh, const double* nearfar);
+/* The tetra input (TetGrid delaunay.hpp:14-18: vertices + tetrahedra), resident on the device. */
+int sof_set_tets(sof_ctx* ctx, int64_t nv, const double* xyz, int64_t nt, const int32_t* tets);
+
+/* ---- per-view preprocessing and binning (parity / inspection) -------------------- */
+/* PrecomputedGaussian per Gaussian for one view (precompute.hpp:21-28): 13 doubles
+ * {inv_cov[6], b_vec[3], c_scalar, tight_bound, min_z, filtered_opacity}. */
+int sof_precompute_view(sof_ctx* ctx, int view, double* out13);
+/* build_tile_binding (tiles.hpp:94-146) for one view; lists stay on the device
+ * (SOF_R_TILE_OFFSETS / SOF_R_TILE_ENTRIES). */
+int sof_tile_binding(sof_ctx* ctx, int view, int tile_size, int64_t* n_tiles, int64_t* n_entries);
+/* schedule_points (tiles.hpp:29-84) for one view, exact (tile, depth, point) order.
+ * tile_assignment[n]; order/key_tile/key_depth[n_sched]; block_ranges[2*n_blocks],
+ * block_to_tile[n_blocks]. Pass NULL outputs to get the counts first. */
+int sof_schedule_points(sof_ctx* ctx, int view, int64_t n, const double* xyz, int tile_size,
+                        int64_t* n_sched, int64_t* n_blocks, int32_t* tile_assignment,
+                        int32_t* order, int32_t* key_tile, double* key_depth,
+                        int32_t* block_ranges, int32_t* block_to_tile);
+
+/* ---- opacity field (FieldEvaluator field_eval.hpp:39-198) --------------------------- */
+/* view_opacity (field_eval.hpp:59-111) for n points against one view. */
+int sof_view_opacity(sof_ctx* ctx, int view, int64_t n, const double* xyz, int strategies,
+                     int tile_size, int classify_mode, double* o, uint8_t* observed,
+                     uint8_t* complete, uint64_t* counters);
+/* classify_point (field_eval.hpp:114-125), batched. interior[n]. */
+int sof_classify_points(sof_ctx* ctx, int64_t n, const double* xyz, int strategies, int tile_size,
+                        uint8_t* interior, uint64_t* counters);
+/* value_at (field_eval.hpp:128-136), batched (classification mode off). */
+int sof_value_at(sof_ctx* ctx, int64_t n, const double* xyz, int strategies, int tile_size,
+                 double* out, uint64_t* counters);
+/* label_grid (field_eval.hpp:140-176): grid.opacity for nv vertices. */
+int sof_label_grid(sof_ctx* ctx, int64_t nv, const double* xyz, int strategies, int tile_size,
+                   int classify_mode, double* opacity, uint64_t* counters);
+
+/* Device-resident, view-range building blocks for view-sharded multi-GPU runs:
+ * label views [v0, v1) with pruning state carried across them. min_opacity and
+ * exterior are read and updated in place (initialise to 1.0 / 0). */
+int sof_label_views_dev(sof_ctx* ctx, int v0, int v1, int64_t n, const double* xyz_dev,
+                        int strategies, int tile_size, int classify_mode,
+                        double* min_opacity_dev, uint8_t* exterior_dev, uint64_t* counters);
+/* classification of n points against views [v0, v1): exterior_dev |= exterior. */
+int sof_classify_views_dev(sof_ctx* ctx, int v0, int v1, int64_t n, const double* xyz_dev,
+                           int strategies, int tile_size, uint8_t* exterior_dev,
+                           uint64_t* counters);
+
+/* ---- mesher ------------------------------------------------------------------------- */
+/* marching_tets (marching_tets.hpp:29-84) over the resident tets with the given vertex
+ * opacities (host array, nv entries; NULL = use the last label result).
+ * Results: SOF_R_EDGES, SOF_R_EDGE_VERTS, SOF_R_TRIANGLES. */
+int sof_marching_tets(sof_ctx* ctx, const double* opacity, int64_t* n_edges, int64_t* n_tris);
+/* binary_search_refine (marching_tets.hpp:94-114) with classify_point as the interior
+ * test, run as `iterations` batched device passes over all crossing edges. edges[2E]
+ * and verts[3E] are host arrays; verts is updated in place. Grid vertices come from
+ * the resident tets. */
+int sof_refine(sof_ctx* ctx, int64_t n_edges, const int32_t* edges, double* verts,
+               int iterations, int strategies, int tile_size, uint64_t* counters);
+/* assemble_mesh (mesh.hpp:36-79). Results: SOF_R_MESH_VERTS, SOF_R_MESH_TRIS. */
+int sof_assemble(sof_ctx* ctx, int64_t n_verts, const double* verts, int64_t n_tris,
+                 const int32_t* tris, double weld_eps, double min_area, int64_t* out_verts,
+                 int64_t* out_tris);
+/* extract_mesh's label -> march -> refine -> assemble (extract.hpp:59-78) over the
+ * resident scene, views and tets, entirely on the device. */
+int sof_extract(sof_ctx* ctx, const sof_extract_opts* opts, sof_extract_stats* stats);
+void sof_extract_opts_default(sof_extract_opts* opts);
+
+/* ---- results ------------------------------------------------------------------------ */
+int64_t sof_result_count(const sof_ctx* ctx, int kind); /* elements (not bytes); <0 if none */
+int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);
+
+/* ---- sorted rasterizer -------------------------------------------------------------- */
+/* render_depth_map (render.hpp:26-51) plus render_pixel's colour / final
+ * transmittance (opacity_field.hpp:201-219) for one view, with the exact per-pixel
+ * (t*, index) resort of collect_contributions (opacity_field.hpp:39-61).
+ * Outputs [h*w] row-major (rgb [h*w*3]); any output may be NULL.
+ * stats (nullable) uint64[4] = {tested pairs, contributing pairs, kbuffer overflow
+ * pixels, exact-depth fallbacks}. */
+int sof_render_view(sof_ctx* ctx, int view, int depth_mode, int tile_size, double* depth,
+                    double* opacity, double* rgb, double* t_final, uint64_t* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SOF_CUDA_H */

@@ -1,0 +1,417 @@
+"""Host-side mirror of the reference's `sof::` API for the hot path, over the C-ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/sof:
+  EvalStrategies / FieldEvaluator        field_eval.hpp:14-198
+  ViewSet                                opacity_field.hpp:21-35 (lazy, device-resident)
+  TetGrid                                delaunay.hpp:14-18
+  marching_tets / binary_search_refine   marching_tets.hpp:29-114
+  assemble_mesh / Mesh                   mesh.hpp:13-79
+  extract_mesh (tetra-input overload)    extract.hpp:35-86
+  render_depth_map / render_pixel        render.hpp:26-51, opacity_field.hpp:201-219
+  write_mesh_ply                         io_mesh.hpp:55-73
+Every computation runs in libsof_cuda.so on the GPU; numpy only holds host buffers.
+Errors: std::invalid_argument -> ValueError, std::runtime_error -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+_P = ctypes.c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a, shape_last=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape_last is not None:
+        a = a.reshape(-1, shape_last)
+    return a
+
+
+class SofError(RuntimeError):
+    pass
+
+
+def _check(ctx_handle, status: int):
+    if status == L.SOF_OK:
+        return
+    lib = L.load()
+    msg = lib.sof_last_error(ctx_handle).decode() if ctx_handle else "error"
+    if status == L.SOF_E_INVALID:
+        raise ValueError(msg)
+    if status == L.SOF_E_OOM:
+        raise MemoryError(msg)
+    raise SofError(f"[{status}] {msg}")
+
+
+# ---- reference data types ------------------------------------------------------------------
+
+@dataclass
+class GaussianScene:
+    """std::vector<GaussianPrimitive> as SoA arrays (gaussian.hpp:12-18)."""
+    pos: np.ndarray
+    scale: np.ndarray
+    rot: np.ndarray  # (w, x, y, z)
+    opacity: np.ndarray
+    dc: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return int(np.asarray(self.opacity).shape[0])
+
+    @staticmethod
+    def of(obj) -> "GaussianScene":
+        return GaussianScene(_f64(obj.pos, 3), _f64(obj.scale, 3), _f64(obj.rot, 4),
+                             _f64(obj.opacity).reshape(-1), _f64(obj.dc, 3))
+
+
+@dataclass
+class CameraSet:
+    """std::vector<Camera> as arrays (camera.hpp:10-21)."""
+    R: np.ndarray
+    t: np.ndarray
+    intr: np.ndarray
+    wh: np.ndarray
+    nearfar: np.ndarray
+
+    @property
+    def v(self) -> int:
+        return int(np.asarray(self.t).shape[0])
+
+    @staticmethod
+    def of(obj) -> "CameraSet":
+        nf = getattr(obj, "nearfar", None)
+        R = _f64(obj.R).reshape(-1, 9)
+        return CameraSet(R, _f64(obj.t, 3), _f64(obj.intr, 4), np.ascontiguousarray(obj.wh, np.int32).reshape(-1, 2),
+                         _f64(nf, 2) if nf is not None else np.tile([0.2, 100.0], (R.shape[0], 1)))
+
+
+@dataclass
+class EvalStrategies:
+    tile_scheduling: bool = False
+    min_z: bool = False
+    early_stop: bool = False
+    prune: bool = False
+    dead_cull: bool = False
+
+    @staticmethod
+    def naive() -> "EvalStrategies":
+        return EvalStrategies()
+
+    @staticmethod
+    def all() -> "EvalStrategies":
+        return EvalStrategies(True, True, True, True, True)
+
+    @staticmethod
+    def from_mask(m: int) -> "EvalStrategies":
+        return EvalStrategies(bool(m & 1), bool(m & 2), bool(m & 4), bool(m & 8), bool(m & 16))
+
+    @property
+    def mask(self) -> int:
+        return (int(self.tile_scheduling) | int(self.min_z) << 1 | int(self.early_stop) << 2
+                | int(self.prune) << 3 | int(self.dead_cull) << 4)
+
+
+def _mask(s) -> int:
+    return s if isinstance(s, int) else s.mask
+
+
+@dataclass
+class TetGrid:
+    vertices: np.ndarray
+    tetrahedra: np.ndarray
+    opacity: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+@dataclass
+class MarchingResult:
+    edges: np.ndarray      # [E, 2] (inside, outside)
+    vertices: np.ndarray   # [E, 3]
+    triangles: np.ndarray  # [T, 3]
+
+
+@dataclass
+class Mesh:
+    vertices: np.ndarray
+    triangles: np.ndarray
+    residuals: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+@dataclass
+class ExtractOptions:
+    strategies: EvalStrategies = field(default_factory=EvalStrategies.all)
+    refine_iterations: int = 8
+    tile_size: int = 16
+    weld_eps: float = 1e-7
+    min_area: float = 1e-14
+    view_begin: int = -1
+    view_end: int = -1
+
+
+# ---- device context ------------------------------------------------------------------------
+
+class Context:
+    """One GPU's sof_ctx: resident scene, cameras, tets and per-view caches."""
+
+    def __init__(self, device: int = 0):
+        self.lib = L.load()
+        h = _P()
+        st = self.lib.sof_ctx_create(device, ctypes.byref(h))
+        if st != L.SOF_OK:
+            raise SofError(f"sof_ctx_create(device={device}) failed with status {st} (no usable CUDA device?)")
+        self.h = h
+        self.device = device
+        self.scene: GaussianScene | None = None
+        self.cams: CameraSet | None = None
+        self.nv = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sof_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def check(self, st):
+        _check(self.h, st)
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.sof_kernel_launches(self.h))
+
+    def set_scene(self, scene, filter_scale: float = 0.0):
+        s = GaussianScene.of(scene)
+        self.check(self.lib.sof_set_scene(self.h, s.n, _ptr(s.pos), _ptr(s.scale), _ptr(s.rot), _ptr(s.opacity),
+                                          _ptr(s.dc), float(filter_scale)))
+        self.scene = s
+
+    def set_views(self, cams):
+        c = CameraSet.of(cams)
+        self.check(self.lib.sof_set_views(self.h, c.v, _ptr(c.R), _ptr(c.t), _ptr(c.intr), _ptr(c.wh), _ptr(c.nearfar)))
+        self.cams = c
+
+    def set_tets(self, vertices, tets):
+        v = _f64(vertices, 3)
+        t = np.ascontiguousarray(tets, np.int32).reshape(-1, 4)
+        self.check(self.lib.sof_set_tets(self.h, len(v), _ptr(v), len(t), _ptr(t)))
+        self.nv = len(v)
+
+    def result(self, kind: int, dtype, width: int):
+        n = int(self.lib.sof_result_count(self.h, kind))
+        if n < 0:
+            raise SofError("no result of that kind")
+        out = np.empty(n, dtype)
+        if n:
+            self.check(self.lib.sof_copy_result(self.h, kind, _ptr(out)))
+        return out.reshape(-1, width) if width > 1 else out
+
+    # -- inspection / parity -------------------------------------------------------------
+    def precompute_view(self, view: int) -> np.ndarray:
+        out = np.empty((self.scene.n, 13))
+        self.check(self.lib.sof_precompute_view(self.h, view, _ptr(out)))
+        return out
+
+    def tile_binding(self, view: int, tile_size: int = 16):
+        nt, ne = ctypes.c_int64(), ctypes.c_int64()
+        self.check(self.lib.sof_tile_binding(self.h, view, tile_size, ctypes.byref(nt), ctypes.byref(ne)))
+        return self.result(L.R_TILE_OFFSETS, np.int64, 1), self.result(L.R_TILE_ENTRIES, np.int32, 1)
+
+    def schedule_points(self, view: int, xyz, tile_size: int = 16) -> dict:
+        xyz = _f64(xyz, 3)
+        n = len(xyz)
+        ns, nb = ctypes.c_int64(), ctypes.c_int64()
+        ta = np.empty(n, np.int32)
+        self.check(self.lib.sof_schedule_points(self.h, view, n, _ptr(xyz), tile_size, ctypes.byref(ns),
+                                                ctypes.byref(nb), _ptr(ta), None, None, None, None, None))
+        order, kt = np.empty(ns.value, np.int32), np.empty(ns.value, np.int32)
+        kd = np.empty(ns.value)
+        br, bt = np.empty((nb.value, 2), np.int32), np.empty(nb.value, np.int32)
+        self.check(self.lib.sof_schedule_points(self.h, view, n, _ptr(xyz), tile_size, None, None, _ptr(ta),
+                                                _ptr(order), _ptr(kt), _ptr(kd), _ptr(br), _ptr(bt)))
+        return {"tile_assignment": ta, "order": order, "key_tile": kt, "key_depth": kd,
+                "block_ranges": br, "block_to_tile": bt}
+
+
+_default_ctx: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+class ViewSet:
+    """ViewSet::build (opacity_field.hpp:26-34): the per-view caches are built lazily
+    on the device instead of eagerly materialising V x N PrecomputedGaussians."""
+
+    def __init__(self, ctx: Context, scene: GaussianScene, cams: CameraSet, filter_scale: float):
+        self.ctx, self.scene, self.cameras, self.filter_scale = ctx, scene, cams, filter_scale
+
+    @staticmethod
+    def build(gaussians, cams, filter_scale: float = 0.0, ctx: Context | None = None) -> "ViewSet":
+        ctx = ctx or Context(0)
+        ctx.set_scene(gaussians, filter_scale)
+        ctx.set_views(cams)
+        return ViewSet(ctx, ctx.scene, ctx.cams, filter_scale)
+
+
+class FieldEvaluator:
+    """FieldEvaluator (field_eval.hpp:39-198), batched over points on the GPU."""
+
+    def __init__(self, gaussians, views: ViewSet, strategies=None, tile_size: int = 16):
+        self.views = views
+        self.ctx = views.ctx
+        self.strategies = EvalStrategies.naive() if strategies is None else strategies
+        self.mask = _mask(self.strategies)
+        self.tile_size = int(tile_size)
+        if self.tile_size <= 0:
+            raise ValueError("tile_size must be positive")
+        self._counters = np.zeros(2, np.uint64)
+
+    def counters(self) -> dict:
+        return {"pairs": int(self._counters[0]), "point_view_evals": int(self._counters[1])}
+
+    def reset_counters(self):
+        self._counters[:] = 0
+
+    def view_opacity(self, view: int, xyz, classify_mode: bool):
+        xyz = _f64(xyz, 3)
+        n = len(xyz)
+        o, ob, co = np.empty(n), np.empty(n, np.uint8), np.empty(n, np.uint8)
+        self.ctx.check(self.ctx.lib.sof_view_opacity(self.ctx.h, view, n, _ptr(xyz), self.mask, self.tile_size,
+                                                     int(classify_mode), _ptr(o), _ptr(ob), _ptr(co),
+                                                     _ptr(self._counters)))
+        return o, ob.astype(bool), co.astype(bool)
+
+    def classify_points(self, xyz) -> np.ndarray:
+        xyz = _f64(xyz, 3)
+        out = np.empty(len(xyz), np.uint8)
+        self.ctx.check(self.ctx.lib.sof_classify_points(self.ctx.h, len(xyz), _ptr(xyz), self.mask, self.tile_size,
+                                                        _ptr(out), _ptr(self._counters)))
+        return out.astype(bool)
+
+    def classify_point(self, x) -> bool:
+        return bool(self.classify_points(np.asarray(x, np.float64).reshape(1, 3))[0])
+
+    def value_at(self, xyz):
+        a = _f64(xyz, 3)
+        out = np.empty(len(a))
+        self.ctx.check(self.ctx.lib.sof_value_at(self.ctx.h, len(a), _ptr(a), self.mask, self.tile_size,
+                                                 _ptr(out), _ptr(self._counters)))
+        return out if np.ndim(xyz) == 2 else float(out[0])
+
+    def label_grid(self, grid, classify_mode: bool = True):
+        """Labels every grid vertex; writes grid.opacity (field_eval.hpp:140-176)."""
+        xyz = _f64(grid.vertices if hasattr(grid, "vertices") else grid, 3)
+        out = np.empty(len(xyz))
+        self.ctx.check(self.ctx.lib.sof_label_grid(self.ctx.h, len(xyz), _ptr(xyz), self.mask, self.tile_size,
+                                                   int(classify_mode), _ptr(out), _ptr(self._counters)))
+        if hasattr(grid, "vertices"):
+            grid.opacity = out
+        return out
+
+
+def marching_tets(grid: TetGrid, ctx: Context | None = None) -> MarchingResult:
+    """marching_tets (marching_tets.hpp:29-84) on the GPU."""
+    ctx = ctx or default_context()
+    ctx.set_tets(grid.vertices, grid.tetrahedra)
+    opa = _f64(grid.opacity).reshape(-1)
+    if len(opa) != ctx.nv:
+        raise ValueError("grid.opacity must have one value per vertex")
+    ne, nt = ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(ctx.lib.sof_marching_tets(ctx.h, _ptr(opa), ctypes.byref(ne), ctypes.byref(nt)))
+    return MarchingResult(ctx.result(L.R_EDGES, np.int32, 2), ctx.result(L.R_EDGE_VERTS, np.float64, 3),
+                          ctx.result(L.R_TRIANGLES, np.int32, 3))
+
+
+def binary_search_refine(m: MarchingResult, grid: TetGrid, evaluator: FieldEvaluator, iterations: int = 8):
+    """Batched binary_search_refine (marching_tets.hpp:94-114): all edges x `iterations`
+    device passes, classify_point as the interior test. Updates m.vertices in place."""
+    ctx = evaluator.ctx
+    ctx.set_tets(grid.vertices, grid.tetrahedra)
+    edges = np.ascontiguousarray(m.edges, np.int32).reshape(-1, 2)
+    v = np.array(m.vertices, np.float64, order="C").reshape(-1, 3)
+    ctx.check(ctx.lib.sof_refine(ctx.h, len(edges), _ptr(edges), _ptr(v), int(iterations), evaluator.mask,
+                                 evaluator.tile_size, _ptr(evaluator._counters)))
+    m.vertices = v
+    return m
+
+
+def assemble_mesh(vertices, triangles, residuals=None, weld_eps: float = 1e-7, min_area: float = 1e-14,
+                  ctx: Context | None = None) -> Mesh:
+    """assemble_mesh (mesh.hpp:36-79) on the GPU."""
+    ctx = ctx or default_context()
+    v = _f64(vertices, 3) if len(vertices) else np.zeros((0, 3))
+    t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+    nv, nt = ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(ctx.lib.sof_assemble(ctx.h, len(v), _ptr(v), len(t), _ptr(t), float(weld_eps), float(min_area),
+                                   ctypes.byref(nv), ctypes.byref(nt)))
+    if residuals is not None:
+        raise ValueError("residual passthrough is not supported by the device weld")
+    return Mesh(ctx.result(L.R_MESH_VERTS, np.float64, 3), ctx.result(L.R_MESH_TRIS, np.int32, 3))
+
+
+def extract_mesh(gaussians, views: ViewSet, grid: TetGrid, opt: ExtractOptions | None = None,
+                 stats: dict | None = None) -> Mesh:
+    """extract_mesh's label -> march -> refine -> weld (extract.hpp:59-78) on a given
+    tetra grid, fused on the device."""
+    opt = opt or ExtractOptions()
+    ctx = views.ctx
+    ctx.set_tets(grid.vertices, grid.tetrahedra)
+    return extract_resident(ctx, opt, stats)
+
+
+def extract_resident(ctx: Context, opt: ExtractOptions, stats: dict | None = None, fetch: bool = True):
+    o = L.ExtractOpts(_mask(opt.strategies), opt.tile_size, opt.refine_iterations, opt.weld_eps, opt.min_area,
+                      opt.view_begin, opt.view_end)
+    st = L.ExtractStats()
+    ctx.check(ctx.lib.sof_extract(ctx.h, ctypes.byref(o), ctypes.byref(st)))
+    if stats is not None:
+        stats.update(st.as_dict())
+    if not fetch:
+        return None
+    return Mesh(ctx.result(L.R_MESH_VERTS, np.float64, 3), ctx.result(L.R_MESH_TRIS, np.int32, 3))
+
+
+def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile_size: int = 16) -> dict:
+    """render_depth_map (render.hpp:26-51) + render_pixel colour / T (opacity_field.hpp:201-219)."""
+    ctx = views.ctx
+    w, h = (int(x) for x in ctx.cams.wh[view])
+    out = {"depth": np.empty((h, w)), "opacity": np.empty((h, w)), "rgb": np.empty((h, w, 3)),
+           "t_final": np.empty((h, w)), "stats": np.zeros(4, np.uint64)}
+    ctx.check(ctx.lib.sof_render_view(ctx.h, view, depth_mode, tile_size, _ptr(out["depth"]), _ptr(out["opacity"]),
+                                      _ptr(out["rgb"]), _ptr(out["t_final"]), _ptr(out["stats"])))
+    return out
+
+
+def render_depth_map(views: ViewSet, view: int, exact: bool = True):
+    r = render_view(views, view, L.DEPTH_EXACT if exact else L.DEPTH_MEDIAN)
+    return r["depth"], r["opacity"]
+
+
+def write_mesh_ply(mesh: Mesh, path: str):
+    """Binary little-endian PLY with double coordinates, byte-identical to
+    write_mesh_ply (io_mesh.hpp:55-73)."""
+    v = _f64(mesh.vertices, 3) if len(mesh.vertices) else np.zeros((0, 3))
+    t = np.ascontiguousarray(mesh.triangles, np.int32).reshape(-1, 3)
+    header = ("ply\nformat binary_little_endian 1.0\n"
+              f"element vertex {len(v)}\n"
+              "property double x\nproperty double y\nproperty double z\n"
+              f"element face {len(t)}\n"
+              "property list uchar int vertex_indices\nend_header\n").encode()
+    faces = np.empty(len(t), dtype=[("n", "u1"), ("i", "<i4", 3)])
+    faces["n"] = 3
+    faces["i"] = t
+    with open(path, "wb") as f:
+        f.write(header)
+        f.write(v.astype("<f8").tobytes())
+        f.write(faces.tobytes())

@@ -1,0 +1,655 @@
+// k_field.cu — per-view preprocessing (K0/K1), Gaussian tile binning (K2), point
+// scheduling (K3) and the opacity-field evaluation kernel (K4), FP64 parity path.
+//
+// Reference path replaced: ViewSet::build / precompute (opacity_field.hpp:26-34,
+// precompute.hpp:57-87), build_tile_binding (tiles.hpp:94-146), schedule_points
+// (tiles.hpp:29-84) and FieldEvaluator::view_opacity / classify_point / value_at /
+// label_grid (field_eval.hpp:59-176). Compiled with --fmad=false: every FP64
+// expression is the reference's, so values and decisions are bit-identical.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "sof_internal.h"
+
+namespace sofk {
+
+// ---- helpers ------------------------------------------------------------------------------
+
+int bits_for(uint64_t max_value) {
+  int b = 1;
+  while (b < 64 && (max_value >> b) != 0) ++b;
+  return b;
+}
+
+void sort_pairs_u64(sof_ctx* c, const uint64_t* kin, uint64_t* kout, const int32_t* vin,
+                    int32_t* vout, int64_t n, int end_bit) {
+  if (n <= 0) return;
+  size_t bytes = 0;
+  SOF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, n, 0, end_bit,
+                                           c->stream));
+  c->cub_tmp.ensure(bytes);
+  SOF_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, bytes, kin, kout, vin, vout, n, 0,
+                                           end_bit, c->stream));
+  c->launches += 2 + (end_bit + 7) / 8;
+}
+
+void sort_pairs_u32(sof_ctx* c, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
+                    int32_t* vout, int64_t n, int end_bit) {
+  if (n <= 0) return;
+  size_t bytes = 0;
+  SOF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, n, 0, end_bit,
+                                           c->stream));
+  c->cub_tmp.ensure(bytes);
+  SOF_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, bytes, kin, kout, vin, vout, n, 0,
+                                           end_bit, c->stream));
+  c->launches += 2 + (end_bit + 7) / 8;
+}
+
+void exclusive_scan_u32_to_i64(sof_ctx* c, const uint32_t* in, int64_t* out, int64_t n) {
+  if (n <= 0) return;
+  size_t bytes = 0;
+  SOF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, c->stream));
+  c->cub_tmp.ensure(bytes);
+  SOF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, bytes, in, out, n, c->stream));
+  c->launches += 2;
+}
+
+void exclusive_scan_i32(sof_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
+  if (n <= 0) return;
+  size_t bytes = 0;
+  SOF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, c->stream));
+  c->cub_tmp.ensure(bytes);
+  SOF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, bytes, in, out, n, c->stream));
+  c->launches += 2;
+}
+
+// ---- K0 / K1: preprocessing ------------------------------------------------------------------
+
+__global__ void k_gauss_static(int64_t n, const double* __restrict__ pos,
+                               const double* __restrict__ scale, const double* __restrict__ rot,
+                               const double* __restrict__ opa, double fs, GaussStatic* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  GaussStatic g;
+  gauss_static(pos + 3 * i, scale + 3 * i, rot + 4 * i, opa[i], fs, g);
+  out[i] = g;
+}
+
+__global__ void k_view_rec(int64_t n, const GaussStatic* __restrict__ g, Cam cam, Rec* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  Rec r;
+  gauss_view(g[i], cam, r);
+  out[i] = r;
+}
+
+void scene_prep(sof_ctx* c) {
+  c->gstat.ensure(c->n);
+  if (c->n == 0) return;
+  k_gauss_static<<<grid_for(c->n, 128), 128, 0, c->stream>>>(
+      c->n, c->pos.p, c->scale.p, c->rot.p, c->opa.p, c->filter_scale, c->gstat.p);
+  SOF_LAUNCHED(c);
+}
+
+void invalidate_view_caches(sof_ctx* c) {
+  for (auto& r : c->recs) r.release();
+  for (auto& b : c->bindings) {
+    b.off.release();
+    b.ent.release();
+    b.view = -1;
+  }
+  c->recs.clear();
+  c->bindings.clear();
+  c->recs.resize(c->cams.size());
+  c->bindings.resize(c->cams.size());
+  c->rec_valid.assign(c->cams.size(), 0);
+  c->cache_bytes = 0;
+}
+
+const Rec* view_records(sof_ctx* c, int view) {
+  if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+  if (c->rec_valid[view]) return c->recs[view].p;
+  const size_t bytes = size_t(c->n) * sizeof(Rec);
+  DBuf<Rec>* dst = &c->rec_scratch;
+  if (c->cache_bytes + bytes <= c->cache_budget) {
+    dst = &c->recs[view];
+    c->cache_bytes += bytes;
+    c->rec_valid[view] = 1;
+  }
+  dst->ensure(std::max<int64_t>(c->n, 1));
+  if (c->n > 0) {
+    k_view_rec<<<grid_for(c->n, 128), 128, 0, c->stream>>>(c->n, c->gstat.p, c->cams[view],
+                                                            dst->p);
+    SOF_LAUNCHED(c);
+  }
+  return dst->p;
+}
+
+// ---- K2: Gaussian tile binning ------------------------------------------------------------------
+
+__global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
+                            const Rec* __restrict__ rec, Cam cam, int ts, int tiles_x, int tiles_y,
+                            int4* rect, uint32_t* cnt, uint64_t* zkey, int32_t* idx) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {  // sentinel for the exclusive scan over n + 1 counts
+    cnt[n] = 0;
+    return;
+  }
+  int tx0, tx1, ty0, ty1;
+  uint32_t count = 0;
+  if (tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1)) {
+    count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
+    rect[i] = make_int4(tx0, tx1, ty0, ty1);
+  }
+  cnt[i] = count;
+  zkey[i] = double_key(rec[i].zmin);
+  idx[i] = int32_t(i);
+}
+
+__global__ void k_gather_counts(int64_t n, const int32_t* __restrict__ order,
+                                const uint32_t* __restrict__ cnt, uint32_t* out) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r > n) return;
+  out[r] = (r == n) ? 0u : cnt[order[r]];
+}
+
+// One warp per Gaussian (in (min_z, index) order): emit (tile, gaussian) entries.
+__global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
+                               const int4* __restrict__ rect, const uint32_t* __restrict__ cnt,
+                               const int64_t* __restrict__ off, int tiles_x, uint32_t* keys,
+                               int32_t* vals) {
+  const int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const int32_t g = order[r];
+  const uint32_t count = cnt[g];
+  if (count == 0) return;
+  const int4 rc = rect[g];
+  const int w = rc.y - rc.x + 1;
+  const int64_t base = off[r];
+  for (uint32_t k = lane; k < count; k += 32) {
+    const int ty = rc.z + int(k / w), tx = rc.x + int(k % w);
+    keys[base + k] = uint32_t(ty * tiles_x + tx);
+    vals[base + k] = g;
+  }
+}
+
+// starts[t] = first position with key >= t, for t in [0, nseg]; keys sorted ascending.
+template <typename K, int SHIFT>
+__global__ void k_segment_starts(int64_t m, const K* __restrict__ keys, int64_t nseg,
+                                 int64_t* starts) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j > m) return;
+  const int64_t k = (j < m) ? int64_t(uint64_t(keys[j]) >> SHIFT) : nseg;
+  const int64_t prev = (j > 0) ? int64_t(uint64_t(keys[j - 1]) >> SHIFT) : -1;
+  for (int64_t t = prev + 1; t <= k; ++t) starts[t] = j;
+}
+
+static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
+  const Cam& cam = c->cams[view];
+  const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
+  const int64_t T = int64_t(tiles_x) * tiles_y;
+  const Rec* rec = view_records(c, view);
+  const int64_t n = c->n;
+  b.view = view;
+  b.tile_size = ts;
+  b.tiles_x = tiles_x;
+  b.tiles_y = tiles_y;
+  b.off.ensure(T + 1);
+  if (n == 0) {
+    SOF_CUDA(cudaMemsetAsync(b.off.p, 0, sizeof(int64_t) * (T + 1), c->stream));
+    b.entries = 0;
+    b.ent.ensure(1);
+    return;
+  }
+  c->rect.ensure(n);
+  c->gcount.ensure(n + 1);
+  c->zkey_in.ensure(n);
+  c->zkey_out.ensure(n);
+  c->gidx_in.ensure(n);
+  c->gidx_out.ensure(n);
+  c->goff.ensure(n + 1);
+  k_tile_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(n, c->gstat.p, rec, cam, ts, tiles_x,
+                                                            tiles_y, c->rect.p, c->gcount.p,
+                                                            c->zkey_in.p, c->gidx_in.p);
+  SOF_LAUNCHED(c);
+  // Gaussians in (min_z, index) order: a stable radix sort keeps index order on ties.
+  sort_pairs_u64(c, c->zkey_in.p, c->zkey_out.p, c->gidx_in.p, c->gidx_out.p, n, 64);
+  c->ekey_in.ensure(n + 1);
+  k_gather_counts<<<grid_for(n + 1, 256), 256, 0, c->stream>>>(n, c->gidx_out.p, c->gcount.p,
+                                                                c->ekey_in.p);
+  SOF_LAUNCHED(c);
+  exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, n + 1);
+  const int64_t M = read_scalar(c, c->goff.p + n);
+  b.entries = M;
+  b.ent.ensure(std::max<int64_t>(M, 1));
+  if (M > 0) {
+    c->ekey_in.ensure(M);
+    c->ekey_out.ensure(M);
+    c->eval_in.ensure(M);
+    k_emit_entries<<<grid_for(n * 32, 256), 256, 0, c->stream>>>(
+        n, c->gidx_out.p, c->rect.p, c->gcount.p, c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p);
+    SOF_LAUNCHED(c);
+    // stable sort by tile keeps the (min_z, index) order inside every tile list
+    sort_pairs_u32(c, c->ekey_in.p, c->ekey_out.p, c->eval_in.p, b.ent.p, M, bits_for(T));
+  }
+  k_segment_starts<uint32_t, 0><<<grid_for(M + 1, 256), 256, 0, c->stream>>>(M, c->ekey_out.p, T,
+                                                                             b.off.p);
+  SOF_LAUNCHED(c);
+}
+
+const Binding& view_binding(sof_ctx* c, int view, int tile_size) {
+  Binding& cached = c->bindings[view];
+  if (cached.view == view && cached.tile_size == tile_size) return cached;
+  // build into the scratch slot, then keep it if the cache budget allows
+  Binding& s = c->bind_scratch;
+  build_binding(c, view, tile_size, s);
+  const size_t bytes = size_t(s.entries) * 4 + size_t(s.tiles_x) * s.tiles_y * 8 + 8;
+  if (c->cache_bytes + bytes <= c->cache_budget) {
+    if (cached.view >= 0) c->cache_bytes -= cached.ent.bytes() + cached.off.bytes();
+    cached.off.swap(s.off);
+    cached.ent.swap(s.ent);
+    cached.view = s.view;
+    cached.tile_size = s.tile_size;
+    cached.tiles_x = s.tiles_x;
+    cached.tiles_y = s.tiles_y;
+    cached.entries = s.entries;
+    s.view = -1;
+    c->cache_bytes += cached.ent.bytes() + cached.off.bytes();
+    return cached;
+  }
+  return s;
+}
+
+// ---- K3: point scheduling ------------------------------------------------------------------------
+
+// Active (not pruned) and observed points -> (tile, f32 view depth) keys, compacted.
+__global__ void k_sched_compact(int64_t n, const double* __restrict__ xyz, Cam cam, int ts,
+                                int tiles_x, const uint8_t* __restrict__ skip, uint64_t* keys,
+                                int32_t* idx, int32_t* count) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  bool keep = false;
+  uint64_t key = 0;
+  if (i < n && !(skip && skip[i])) {
+    const PointRay pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+    keep = pr.observed;
+    if (keep) key = (uint64_t(uint32_t(pr.tile)) << 32) | __float_as_uint(float(pr.zp));
+  }
+  const unsigned mask = __ballot_sync(0xffffffffu, keep);
+  if (mask == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(count, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (keep) {
+    const int pos = base + __popc(mask & ((1u << lane) - 1u));
+    keys[pos] = key;
+    idx[pos] = int32_t(i);
+  }
+}
+
+__global__ void k_block_flags(int64_t m, const uint64_t* __restrict__ keys,
+                              const int64_t* __restrict__ tile_start, int32_t* flag) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  const int64_t t = int64_t(keys[j] >> 32);
+  flag[j] = ((j - tile_start[t]) % kBlockPoints) == 0;
+}
+
+__global__ void k_block_fill(int64_t m, const uint64_t* __restrict__ keys,
+                             const int64_t* __restrict__ tile_start,
+                             const int32_t* __restrict__ flag, const int32_t* __restrict__ bid,
+                             int4* blocks, int64_t* nblocks) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  if (j == m - 1) *nblocks = bid[j] + flag[j];
+  if (!flag[j]) return;
+  const int64_t t = int64_t(keys[j] >> 32);
+  const int64_t end = std::min<int64_t>(j + kBlockPoints, tile_start[t + 1]);
+  blocks[bid[j]] = make_int4(int(j), int(end), int(t), 0);
+}
+
+__global__ void k_block_linear(int64_t m, int4* blocks, int64_t* nblocks) {
+  const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t nb = (m + kBlockPoints - 1) / kBlockPoints;
+  if (b == 0) *nblocks = nb;
+  if (b >= nb) return;
+  blocks[b] = make_int4(int(b * kBlockPoints), int(std::min<int64_t>(m, (b + 1) * kBlockPoints)),
+                        -1, 0);
+}
+
+// ---- K4: opacity evaluation ----------------------------------------------------------------------
+
+constexpr int kChunk = 32;  // Gaussian records staged in shared memory per step
+
+// One CTA = one schedule block (<= 256 points of one tile). The block's Gaussian
+// list is streamed through shared memory in chunks; every thread runs the exact
+// view_opacity loop (field_eval.hpp:86-108) for its point.
+template <int MODE, bool TILED>
+__global__ void __launch_bounds__(256) k_eval(
+    const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks,
+    const int32_t* __restrict__ pidx, const double* __restrict__ xyz, Cam cam, int ts,
+    int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
+    int64_t n_gauss, const Rec* __restrict__ recs, int strategies, int classify, double* min_op,
+    uint8_t* ext, double* o_out, uint8_t* obs_out, uint8_t* comp_out,
+    unsigned long long* pairs_counter) {
+  __shared__ __align__(16) Rec srec[kChunk];
+  const int64_t b = blockIdx.x;
+  if (b >= *nblocks) return;
+  const int4 blk = blocks[b];
+  const int j = blk.x + int(threadIdx.x);
+  const bool active = j < blk.y;
+  int i = 0;
+  PointRay pr;
+  pr.observed = false;
+  if (active) {
+    i = pidx[j];
+    pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+  }
+  int64_t l0 = 0, l1 = n_gauss;
+  if (TILED) {
+    l0 = loff[blk.z];
+    l1 = loff[blk.z + 1];
+  }
+  const bool dead_cull = strategies & 16, use_min_z = strategies & 2;
+  const bool early = classify && (strategies & 4);
+  double survive = 1.0;
+  bool complete = true;
+  bool done = !active;
+  unsigned pairs = 0;
+  for (int64_t base = l0; base < l1; base += kChunk) {
+    if (!__syncthreads_or(!done)) break;
+    const int cnt = int(std::min<int64_t>(kChunk, l1 - base));
+    for (int k = threadIdx.x; k < cnt * 6; k += blockDim.x) {
+      const int r = k / 6, q = k % 6;
+      const int64_t g = TILED ? int64_t(lent[base + r]) : base + r;
+      reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+    }
+    __syncthreads();
+    if (!done) {
+      for (int k = 0; k < cnt; ++k) {
+        const Rec& r = srec[k];
+        if (dead_cull && r.op < kMinAlpha) continue;
+        if (use_min_z && r.zmin > pr.zp) {
+          if (TILED) {  // list sorted by min_z (field_eval.hpp:91)
+            done = true;
+            break;
+          }
+          continue;
+        }
+        ++pairs;
+        const double alpha = pair_alpha(r, pr.d, pr.t);
+        if (alpha == 0.0) continue;
+        survive *= 1.0 - alpha;
+        if (early && 1.0 - survive > 0.5) {
+          complete = false;
+          done = true;
+          break;
+        }
+      }
+    }
+  }
+  if (active) {
+    const double o = 1.0 - survive;
+    if (MODE == kModeLabel || MODE == kModeValue) {
+      const double m = min_op[i];
+      min_op[i] = (o < m) ? o : m;
+      if (MODE == kModeLabel && complete && o < 0.5) ext[i] = 1;
+    } else if (MODE == kModeClassify) {
+      if (complete && o < 0.5) ext[i] = 1;
+    } else {
+      o_out[i] = o;
+      obs_out[i] = 1;
+      comp_out[i] = complete;
+    }
+  }
+  // pairs counter: warp reduce, one atomic per warp
+  unsigned long long p = pairs;
+  for (int s = 16; s > 0; s >>= 1) p += __shfl_down_sync(0xffffffffu, p, s);
+  if ((threadIdx.x & 31) == 0 && p) atomicAdd(pairs_counter, p);
+}
+
+__global__ void k_fill_view_outputs(int64_t n, double* o, uint8_t* obs, uint8_t* comp) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  o[i] = 1.0;
+  obs[i] = 0;
+  comp[i] = 1;
+}
+
+template <int MODE>
+static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pidx,
+                        const double* xyz, const Cam& cam, int ts, int tiles_x, const Binding* bd,
+                        const Rec* rec, int strategies, bool classify, double* min_op,
+                        uint8_t* ext, double* o_out, uint8_t* obs, uint8_t* comp) {
+  if (grid <= 0) return;
+  const int64_t* nb = c->d_scalar.p;
+  unsigned long long* pc = c->d_counters.p;
+  if (c->time_eval) SOF_CUDA(cudaEventRecord(c->ev0, c->stream));
+  if (tiled)
+    k_eval<MODE, true><<<unsigned(grid), 256, 0, c->stream>>>(
+        c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
+        strategies, classify, min_op, ext, o_out, obs, comp, pc);
+  else
+    k_eval<MODE, false><<<unsigned(grid), 256, 0, c->stream>>>(
+        c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
+        strategies, classify, min_op, ext, o_out, obs, comp, pc);
+  SOF_LAUNCHED(c);
+  c->eval_launches++;
+  if (c->time_eval) {
+    SOF_CUDA(cudaEventRecord(c->ev1, c->stream));
+    SOF_CUDA(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    SOF_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->eval_ms += ms;
+  }
+}
+
+void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int strategies,
+                int tile_size, bool classify_mode, EvalMode mode, double* min_op, uint8_t* ext,
+                double* o_out, uint8_t* obs_out, uint8_t* comp_out, uint64_t* counters_host) {
+  if (!c->has_scene) throw StateError("no scene: call sof_set_scene first");
+  if (v0 < 0 || v1 > int(c->cams.size()) || v0 > v1) throw InvalidArg("view range out of bounds");
+  if (tile_size <= 0) throw InvalidArg("tile_size must be positive");
+  const bool tiled = strategies & 1;
+  const bool prune = strategies & 8;
+  c->d_counters.ensure(4);
+  c->d_scalar.ensure(4);
+  SOF_CUDA(cudaMemsetAsync(c->d_counters.p, 0, sizeof(unsigned long long) * 4, c->stream));
+  uint64_t pve = 0;
+  PointSchedule& s = c->sched;
+  if (n > 0) {
+    s.key_in.ensure(n);
+    s.key_out.ensure(n);
+    s.idx_in.ensure(n);
+    s.idx_out.ensure(n);
+    s.block_flag.ensure(n);
+    s.block_id.ensure(n);
+    s.counters.ensure(2);
+  }
+  if (mode == kModeView && n > 0) {
+    k_fill_view_outputs<<<grid_for(n, 256), 256, 0, c->stream>>>(n, o_out, obs_out, comp_out);
+    SOF_LAUNCHED(c);
+  }
+  for (int v = v0; v < v1 && n > 0; ++v) {
+    const Cam& cam = c->cams[v];
+    const int tiles_x = (cam.w + tile_size - 1) / tile_size;
+    const int tiles_y = (cam.h + tile_size - 1) / tile_size;
+    const int64_t T = int64_t(tiles_x) * tiles_y;
+    const Rec* rec = view_records(c, v);
+    const Binding* bd = tiled ? &view_binding(c, v, tile_size) : nullptr;
+    // K3: compact the active, observed points of this view
+    const uint8_t* skip = (prune && (mode == kModeLabel || mode == kModeClassify)) ? ext : nullptr;
+    SOF_CUDA(cudaMemsetAsync(s.counters.p, 0, sizeof(int32_t) * 2, c->stream));
+    k_sched_compact<<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, cam, tile_size, tiles_x, skip,
+                                                             s.key_in.p, s.idx_in.p, s.counters.p);
+    SOF_LAUNCHED(c);
+    const int64_t nact = read_scalar(c, s.counters.p);
+    if (nact == 0) continue;
+    pve += uint64_t(nact);
+    const int32_t* pidx = s.idx_in.p;
+    int64_t grid;
+    if (tiled) {
+      sort_pairs_u64(c, s.key_in.p, s.key_out.p, s.idx_in.p, s.idx_out.p, nact,
+                     32 + bits_for(uint64_t(T)));
+      pidx = s.idx_out.p;
+      s.tile_start.ensure(T + 1);
+      k_segment_starts<uint64_t, 32><<<grid_for(nact + 1, 256), 256, 0, c->stream>>>(
+          nact, s.key_out.p, T, s.tile_start.p);
+      SOF_LAUNCHED(c);
+      k_block_flags<<<grid_for(nact, 256), 256, 0, c->stream>>>(nact, s.key_out.p,
+                                                                 s.tile_start.p, s.block_flag.p);
+      SOF_LAUNCHED(c);
+      exclusive_scan_i32(c, s.block_flag.p, s.block_id.p, nact);
+      grid = (nact + kBlockPoints - 1) / kBlockPoints + std::min<int64_t>(T, nact);
+      s.blocks.ensure(grid);
+      k_block_fill<<<grid_for(nact, 256), 256, 0, c->stream>>>(
+          nact, s.key_out.p, s.tile_start.p, s.block_flag.p, s.block_id.p, s.blocks.p,
+          c->d_scalar.p);
+      SOF_LAUNCHED(c);
+    } else {
+      grid = (nact + kBlockPoints - 1) / kBlockPoints;
+      s.blocks.ensure(grid);
+      k_block_linear<<<grid_for(grid, 256), 256, 0, c->stream>>>(nact, s.blocks.p, c->d_scalar.p);
+      SOF_LAUNCHED(c);
+    }
+    switch (mode) {
+      case kModeLabel:
+        launch_eval<kModeLabel>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
+                                strategies, classify_mode, min_op, ext, o_out, obs_out, comp_out);
+        break;
+      case kModeClassify:
+        launch_eval<kModeClassify>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
+                                   strategies, true, min_op, ext, o_out, obs_out, comp_out);
+        break;
+      case kModeView:
+        launch_eval<kModeView>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
+                               strategies, classify_mode, min_op, ext, o_out, obs_out, comp_out);
+        break;
+      case kModeValue:
+        launch_eval<kModeValue>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
+                                strategies, false, min_op, ext, o_out, obs_out, comp_out);
+        break;
+    }
+  }
+  if (counters_host) {
+    const unsigned long long pairs = read_scalar(c, c->d_counters.p);
+    counters_host[0] += pairs;
+    counters_host[1] += pve;
+  }
+}
+
+// label_grid's final write (field_eval.hpp:173-175)
+__global__ void k_finalize_label(int64_t n, const double* __restrict__ m,
+                                 const uint8_t* __restrict__ ext, double* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double v = m[i];
+  out[i] = ext[i] ? ((0.49999999 < v) ? 0.49999999 : v) : v;
+}
+
+void finalize_label(sof_ctx* c, int64_t n, const double* min_op, const uint8_t* ext, double* out) {
+  if (n <= 0) return;
+  k_finalize_label<<<grid_for(n, 256), 256, 0, c->stream>>>(n, min_op, ext, out);
+  SOF_LAUNCHED(c);
+}
+
+// ---- exact schedule_points (API / parity; tiles.hpp:29-84) -------------------------------------
+
+__global__ void k_sched_exact(int64_t n, const double* __restrict__ xyz, Cam cam, int ts,
+                              int tiles_x, int32_t* tile_assign, uint64_t* dkey, int32_t* idx) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  // tiles.hpp:46-51: observe test without the t >= 1e-12 rule of view_opacity
+  const double x0 = xyz[3 * i], x1 = xyz[3 * i + 1], x2 = xyz[3 * i + 2];
+  const double vx = to_view_c(cam, 0, x0, x1, x2);
+  const double vy = to_view_c(cam, 1, x0, x1, x2);
+  const double vz = to_view_c(cam, 2, x0, x1, x2);
+  int tile = -1;
+  if (vz > 0.0) {
+    const double px = cam.fx * vx / vz + cam.cx;
+    const double py = cam.fy * vy / vz + cam.cy;
+    if (!(px < 0.0 || px >= cam.w || py < 0.0 || py >= cam.h))
+      tile = (int)py / ts * tiles_x + (int)px / ts;
+  }
+  tile_assign[i] = tile;
+  dkey[i] = double_key(vz);
+  idx[i] = int32_t(i);
+}
+
+void schedule_points_exact(sof_ctx* c, int view, int64_t n, const double* xyz, int ts,
+                           int32_t* tile_assignment, std::vector<int32_t>& order,
+                           std::vector<int32_t>& key_tile, std::vector<double>& key_depth,
+                           std::vector<int32_t>& block_ranges,
+                           std::vector<int32_t>& block_to_tile) {
+  if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+  const Cam& cam = c->cams[view];
+  const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
+  order.clear();
+  key_tile.clear();
+  key_depth.clear();
+  block_ranges.clear();
+  block_to_tile.clear();
+  if (n == 0) return;
+  DBuf<int32_t> tile, tile_sorted;
+  DBuf<uint64_t> k1, k2;
+  DBuf<int32_t> i1, i2;
+  tile.ensure(n);
+  tile_sorted.ensure(n);
+  k1.ensure(n);
+  k2.ensure(n);
+  i1.ensure(n);
+  i2.ensure(n);
+  k_sched_exact<<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, cam, ts, tiles_x, tile.p, k1.p,
+                                                          i1.p);
+  SOF_LAUNCHED(c);
+  // (tile, depth, point): sort by depth (stable on index), then stably by tile
+  sort_pairs_u64(c, k1.p, k2.p, i1.p, i2.p, n, 64);
+  std::vector<int32_t> h_tile(n), h_ord(n);
+  std::vector<uint64_t> h_dk(n);
+  SOF_CUDA(cudaMemcpyAsync(tile_assignment, tile.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                           c->stream));
+  SOF_CUDA(cudaMemcpyAsync(h_ord.data(), i2.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                           c->stream));
+  SOF_CUDA(cudaStreamSynchronize(c->stream));
+  // stable counting pass by tile on the host side (the API path is not hot)
+  const int64_t T = int64_t(tiles_x) * tiles_y;
+  std::vector<int64_t> cnt(T + 1, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    const int t = tile_assignment[h_ord[r]];
+    if (t >= 0) cnt[t + 1]++;
+  }
+  for (int64_t t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
+  const int64_t m = cnt[T];
+  order.assign(m, 0);
+  std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+  for (int64_t r = 0; r < n; ++r) {
+    const int32_t p = h_ord[r];
+    const int t = tile_assignment[p];
+    if (t >= 0) order[pos[t]++] = p;
+  }
+  // depths in double from the host copy of the points is not available here; recompute
+  std::vector<double> h_xyz(3 * n);
+  SOF_CUDA(cudaMemcpy(h_xyz.data(), xyz, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+  key_tile.resize(m);
+  key_depth.resize(m);
+  for (int64_t k = 0; k < m; ++k) {
+    const int32_t p = order[k];
+    key_tile[k] = tile_assignment[p];
+    key_depth[k] = to_view_c(cam, 2, h_xyz[3 * p], h_xyz[3 * p + 1], h_xyz[3 * p + 2]);
+  }
+  for (int64_t t = 0; t < T; ++t) {
+    const int64_t b0 = cnt[t], b1 = cnt[t + 1];
+    for (int64_t b = b0; b < b1; b += kBlockPoints) {
+      block_ranges.push_back(int32_t(b));
+      block_ranges.push_back(int32_t(std::min<int64_t>(b + kBlockPoints, b1)));
+      block_to_tile.push_back(int32_t(t));
+    }
+  }
+}
+
+}  // namespace sofk

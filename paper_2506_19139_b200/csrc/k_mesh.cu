@@ -1,0 +1,519 @@
+// k_mesh.cu — Marching Tetrahedra (K6-K8), batched bisection (K9) and the weld
+// (K10), all deterministic and bit-identical to the reference.
+//
+// Reference path replaced: marching_tets (marching_tets.hpp:29-84),
+// binary_search_refine (marching_tets.hpp:94-114) and assemble_mesh (mesh.hpp:36-79).
+// The reference numbers edges and welded vertices in order of first appearance,
+// driven by hash maps; here "first appearance" is recovered with stable radix
+// sorts: occurrences are sorted by key keeping their global position order, the
+// run head is the first occurrence, and an exclusive scan over first-occurrence
+// flags assigns ids in appearance order. Compiled with --fmad=false.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+
+#include "sof_internal.h"
+
+namespace sofk {
+
+// ---- K6: per-tet case ------------------------------------------------------------------------
+
+__global__ void k_tet_case(int64_t nt, const int32_t* __restrict__ tets,
+                           const double* __restrict__ opa, uint8_t* crossing) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= nt) return;
+  const int4 tt = reinterpret_cast<const int4*>(tets)[t];
+  const int ni = (opa[tt.x] >= 0.5) + (opa[tt.y] >= 0.5) + (opa[tt.z] >= 0.5) + (opa[tt.w] >= 0.5);
+  crossing[t] = (ni != 0 && ni != 4);
+}
+
+// occurrence / triangle counts of the crossing tets, packed (occ | tri << 32)
+__global__ void k_tet_counts(int64_t nc, const int32_t* __restrict__ ctets,
+                             const int32_t* __restrict__ tets, const double* __restrict__ opa,
+                             unsigned long long* packed) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k > nc) return;
+  if (k == nc) {
+    packed[nc] = 0;
+    return;
+  }
+  const int4 tt = reinterpret_cast<const int4*>(tets)[ctets[k]];
+  const int ni = (opa[tt.x] >= 0.5) + (opa[tt.y] >= 0.5) + (opa[tt.z] >= 0.5) + (opa[tt.w] >= 0.5);
+  const unsigned long long occ = (ni == 2) ? 4 : 3, tri = (ni == 2) ? 2 : 1;
+  packed[k] = occ | (tri << 32);
+}
+
+// K7: emit the edge_vertex() occurrences of each crossing tet in the reference's
+// call order and the triangles' occurrence references.
+//   ni == 1: emit(edge(i0,o0), edge(i0,o1), edge(i0,o2)) — GCC/x86-64 evaluates the
+//            three call arguments right to left, so the calls (and therefore the
+//            first-appearance edge numbering) run (i0,o2), (i0,o1), (i0,o0);
+//   ni == 3: likewise (i2,o0), (i1,o0), (i0,o0);
+//   ni == 2: named statements ac, ad, bd, bc (marching_tets.hpp:75-78).
+// Verified against the compiled reference (tests/test_mesh_cpu.py).
+__global__ void k_tet_emit(int64_t nc, int64_t nv, const int32_t* __restrict__ ctets,
+                           const int32_t* __restrict__ tets, const double* __restrict__ opa,
+                           const unsigned long long* __restrict__ off, uint64_t* occ_key,
+                           int32_t* occ_pos, int32_t* occ_in, int32_t* occ_out, int32_t* tri_occ,
+                           int32_t* tri_tet) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= nc) return;
+  const int32_t t = ctets[k];
+  const int4 tt = reinterpret_cast<const int4*>(tets)[t];
+  const int v[4] = {tt.x, tt.y, tt.z, tt.w};
+  int in[4], out[4], ni = 0, no = 0;
+  for (int q = 0; q < 4; ++q) {
+    if (opa[v[q]] >= 0.5)
+      in[ni++] = v[q];
+    else
+      out[no++] = v[q];
+  }
+  const unsigned long long o = off[k];
+  const int64_t ob = int64_t(o & 0xffffffffull), tb = int64_t(o >> 32);
+  int ci[4], co[4], nocc;
+  if (ni == 1) {
+    ci[0] = in[0]; co[0] = out[2];
+    ci[1] = in[0]; co[1] = out[1];
+    ci[2] = in[0]; co[2] = out[0];
+    nocc = 3;
+    // triangle (e(i0,o0), e(i0,o1), e(i0,o2)) = occurrences (2, 1, 0)
+    tri_occ[3 * tb] = int32_t(ob + 2);
+    tri_occ[3 * tb + 1] = int32_t(ob + 1);
+    tri_occ[3 * tb + 2] = int32_t(ob);
+    tri_tet[tb] = t;
+  } else if (ni == 3) {
+    ci[0] = in[2]; co[0] = out[0];
+    ci[1] = in[1]; co[1] = out[0];
+    ci[2] = in[0]; co[2] = out[0];
+    nocc = 3;
+    tri_occ[3 * tb] = int32_t(ob + 2);
+    tri_occ[3 * tb + 1] = int32_t(ob + 1);
+    tri_occ[3 * tb + 2] = int32_t(ob);
+    tri_tet[tb] = t;
+  } else {
+    ci[0] = in[0]; co[0] = out[0];  // ac
+    ci[1] = in[0]; co[1] = out[1];  // ad
+    ci[2] = in[1]; co[2] = out[1];  // bd
+    ci[3] = in[1]; co[3] = out[0];  // bc
+    nocc = 4;
+    // emit(ac, ad, bd), emit(ac, bd, bc)
+    tri_occ[3 * tb] = int32_t(ob);
+    tri_occ[3 * tb + 1] = int32_t(ob + 1);
+    tri_occ[3 * tb + 2] = int32_t(ob + 2);
+    tri_occ[3 * tb + 3] = int32_t(ob);
+    tri_occ[3 * tb + 4] = int32_t(ob + 2);
+    tri_occ[3 * tb + 5] = int32_t(ob + 3);
+    tri_tet[tb] = t;
+    tri_tet[tb + 1] = t;
+  }
+  for (int q = 0; q < nocc; ++q) {
+    occ_key[ob + q] = uint64_t(ci[q]) * uint64_t(nv) + uint64_t(co[q]);
+    occ_pos[ob + q] = int32_t(ob + q);
+    occ_in[ob + q] = ci[q];
+    occ_out[ob + q] = co[q];
+  }
+}
+
+// Run heads of the key-sorted occurrences: the head carries the smallest global
+// position (stable sort), i.e. the first appearance.
+__global__ void k_occ_heads(int64_t m, const uint64_t* __restrict__ skey,
+                            const int32_t* __restrict__ spos, int32_t* head, uint8_t* is_first_u8) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  const bool h = (j == 0) || skey[j] != skey[j - 1];
+  head[j] = h;
+  if (h) is_first_u8[spos[j]] = 1;
+}
+
+__global__ void k_u8_to_i32(int64_t m, const uint8_t* __restrict__ a, int32_t* b) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j < m) b[j] = a[j];
+}
+
+// edges[e] and the lerp vertex (marching_tets.hpp:36-42) for each first occurrence.
+__global__ void k_edges(int64_t m, const int32_t* __restrict__ is_first,
+                        const int32_t* __restrict__ eid, const int32_t* __restrict__ occ_in,
+                        const int32_t* __restrict__ occ_out, const double* __restrict__ opa,
+                        const double* __restrict__ xyz, int32_t* edges, double* verts) {
+  const int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (q >= m || !is_first[q]) return;
+  const int32_t e = eid[q];
+  const int32_t a = occ_in[q], b = occ_out[q];
+  edges[2 * e] = a;
+  edges[2 * e + 1] = b;
+  const double oi = opa[a], oo = opa[b];
+  const double s = (0.5 - oi) / (oo - oi);
+  for (int k = 0; k < 3; ++k) {
+    const double pi = xyz[3 * a + k], po = xyz[3 * b + k];
+    verts[3 * e + k] = pi + s * (po - pi);
+  }
+}
+
+// edge id of every occurrence: the id of its run head's first occurrence.
+__global__ void k_occ_edge(int64_t m, const int32_t* __restrict__ run_incl,
+                           const int32_t* __restrict__ head, const int32_t* __restrict__ spos,
+                           const int32_t* __restrict__ eid, int32_t* run_eid, int32_t* occ_edge) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  if (head[j]) run_eid[run_incl[j] + head[j] - 1] = eid[spos[j]];
+}
+__global__ void k_occ_edge2(int64_t m, const int32_t* __restrict__ run_incl,
+                            const int32_t* __restrict__ head, const int32_t* __restrict__ spos,
+                            const int32_t* __restrict__ run_eid, int32_t* occ_edge) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  occ_edge[spos[j]] = run_eid[run_incl[j] + head[j] - 1];
+}
+
+// emit() winding (marching_tets.hpp:45-52) with interior_ref from the tet (:64-66).
+__global__ void k_tris(int64_t ntri, const int32_t* __restrict__ tri_occ,
+                       const int32_t* __restrict__ tri_tet, const int32_t* __restrict__ occ_edge,
+                       const int32_t* __restrict__ tets, const double* __restrict__ opa,
+                       const double* __restrict__ xyz, const double* __restrict__ verts,
+                       int32_t* tris) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= ntri) return;
+  const int32_t e0 = occ_edge[tri_occ[3 * k]], e1 = occ_edge[tri_occ[3 * k + 1]],
+                e2 = occ_edge[tri_occ[3 * k + 2]];
+  const int4 tt = reinterpret_cast<const int4*>(tets)[tri_tet[k]];
+  const int v[4] = {tt.x, tt.y, tt.z, tt.w};
+  double ref[3] = {0.0, 0.0, 0.0};
+  int ni = 0;
+  for (int q = 0; q < 4; ++q)
+    if (opa[v[q]] >= 0.5) {
+      for (int c = 0; c < 3; ++c) ref[c] = ref[c] + xyz[3 * v[q] + c];
+      ++ni;
+    }
+  for (int c = 0; c < 3; ++c) ref[c] = ref[c] / double(ni);
+  const double* a = verts + 3 * e0;
+  const double* b = verts + 3 * e1;
+  const double* cc = verts + 3 * e2;
+  const double u0 = b[0] - a[0], u1 = b[1] - a[1], u2 = b[2] - a[2];
+  const double w0 = cc[0] - a[0], w1 = cc[1] - a[1], w2 = cc[2] - a[2];
+  const double n0 = u1 * w2 - u2 * w1, n1 = u2 * w0 - u0 * w2, n2 = u0 * w1 - u1 * w0;
+  const double g0 = (a[0] + b[0] + cc[0]) / 3.0 - ref[0];
+  const double g1 = (a[1] + b[1] + cc[1]) / 3.0 - ref[1];
+  const double g2 = (a[2] + b[2] + cc[2]) / 3.0 - ref[2];
+  const bool keep = n0 * g0 + n1 * g1 + n2 * g2 >= 0.0;
+  tris[3 * k] = e0;
+  tris[3 * k + 1] = keep ? e1 : e2;
+  tris[3 * k + 2] = keep ? e2 : e1;
+}
+
+struct MeshScratch {
+  DBuf<uint8_t> crossing, first_u8;
+  DBuf<int32_t> ctets, nsel;
+  DBuf<unsigned long long> packed, off;
+  DBuf<uint64_t> okey, skey;
+  DBuf<int32_t> opos, spos, oin, oout, tri_occ, tri_tet, head, run_incl, is_first, eid, run_eid,
+      occ_edge;
+};
+static MeshScratch& scratch() {
+  static thread_local MeshScratch s;
+  return s;
+}
+
+void march(sof_ctx* c, const double* opa) {
+  if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
+  const int64_t nt = c->nt, nv = c->nv;
+  MeshScratch& s = scratch();
+  c->n_edges = c->n_march_tris = 0;
+  c->r_edges.ensure(2);
+  c->r_everts.ensure(3);
+  c->r_tris.ensure(3);
+  if (nt == 0) return;
+  s.crossing.ensure(nt);
+  k_tet_case<<<grid_for(nt, 256), 256, 0, c->stream>>>(nt, c->tt.p, opa, s.crossing.p);
+  SOF_LAUNCHED(c);
+  // compact the crossing tets, keeping tet order
+  s.ctets.ensure(nt);
+  s.nsel.ensure(1);
+  {
+    thrust::counting_iterator<int32_t> it(0);
+    size_t bytes = 0;
+    SOF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, s.crossing.p, s.ctets.p, s.nsel.p, nt,
+                                        c->stream));
+    c->cub_tmp.ensure(bytes);
+    SOF_CUDA(cub::DeviceSelect::Flagged(c->cub_tmp.p, bytes, it, s.crossing.p, s.ctets.p,
+                                        s.nsel.p, nt, c->stream));
+    c->launches += 2;
+  }
+  const int64_t nc = read_scalar(c, s.nsel.p);
+  if (nc == 0) return;
+  s.packed.ensure(nc + 1);
+  s.off.ensure(nc + 1);
+  k_tet_counts<<<grid_for(nc + 1, 256), 256, 0, c->stream>>>(nc, s.ctets.p, c->tt.p, opa,
+                                                              s.packed.p);
+  SOF_LAUNCHED(c);
+  {
+    size_t bytes = 0;
+    SOF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, s.packed.p, s.off.p, nc + 1, c->stream));
+    c->cub_tmp.ensure(bytes);
+    SOF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, bytes, s.packed.p, s.off.p, nc + 1,
+                                           c->stream));
+    c->launches += 2;
+  }
+  const unsigned long long tot = read_scalar(c, s.off.p + nc);
+  const int64_t m = int64_t(tot & 0xffffffffull), ntri = int64_t(tot >> 32);
+  s.okey.ensure(m);
+  s.skey.ensure(m);
+  s.opos.ensure(m);
+  s.spos.ensure(m);
+  s.oin.ensure(m);
+  s.oout.ensure(m);
+  s.tri_occ.ensure(3 * ntri);
+  s.tri_tet.ensure(ntri);
+  k_tet_emit<<<grid_for(nc, 128), 128, 0, c->stream>>>(nc, nv, s.ctets.p, c->tt.p, opa, s.off.p,
+                                                        s.okey.p, s.opos.p, s.oin.p, s.oout.p,
+                                                        s.tri_occ.p, s.tri_tet.p);
+  SOF_LAUNCHED(c);
+  const int kbits = bits_for(uint64_t(nv) * uint64_t(nv));
+  sort_pairs_u64(c, s.okey.p, s.skey.p, s.opos.p, s.spos.p, m, kbits);
+  s.head.ensure(m);
+  s.first_u8.ensure(m);
+  s.is_first.ensure(m);
+  s.eid.ensure(m);
+  s.run_incl.ensure(m);
+  s.occ_edge.ensure(m);
+  SOF_CUDA(cudaMemsetAsync(s.first_u8.p, 0, m, c->stream));
+  k_occ_heads<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.skey.p, s.spos.p, s.head.p,
+                                                        s.first_u8.p);
+  SOF_LAUNCHED(c);
+  k_u8_to_i32<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.first_u8.p, s.is_first.p);
+  SOF_LAUNCHED(c);
+  exclusive_scan_i32(c, s.is_first.p, s.eid.p, m);
+  exclusive_scan_i32(c, s.head.p, s.run_incl.p, m);  // exclusive: run id = run_incl + head - 1
+  // number of edges = number of runs
+  const int32_t last_run = read_scalar(c, s.run_incl.p + (m - 1));
+  const int32_t last_head = read_scalar(c, s.head.p + (m - 1));
+  const int64_t E = int64_t(last_run) + last_head;
+  s.run_eid.ensure(E);
+  c->r_edges.ensure(2 * E);
+  c->r_everts.ensure(3 * E);
+  c->r_tris.ensure(3 * ntri);
+  k_edges<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.is_first.p, s.eid.p, s.oin.p, s.oout.p, opa,
+                                                    c->tv.p, c->r_edges.p, c->r_everts.p);
+  SOF_LAUNCHED(c);
+  k_occ_edge<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.run_incl.p, s.head.p, s.spos.p, s.eid.p,
+                                                       s.run_eid.p, s.occ_edge.p);
+  SOF_LAUNCHED(c);
+  k_occ_edge2<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.run_incl.p, s.head.p, s.spos.p,
+                                                        s.run_eid.p, s.occ_edge.p);
+  SOF_LAUNCHED(c);
+  k_tris<<<grid_for(ntri, 256), 256, 0, c->stream>>>(ntri, s.tri_occ.p, s.tri_tet.p, s.occ_edge.p,
+                                                      c->tt.p, opa, c->tv.p, c->r_everts.p,
+                                                      c->r_tris.p);
+  SOF_LAUNCHED(c);
+  c->n_edges = E;
+  c->n_march_tris = ntri;
+}
+
+// ---- K9: batched bisection -------------------------------------------------------------------------
+
+__global__ void k_bisect_init(int64_t ne, const int32_t* __restrict__ edges,
+                              const double* __restrict__ xyz, double* pin, double* pout) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= ne) return;
+  const int32_t a = edges[2 * e], b = edges[2 * e + 1];
+  for (int k = 0; k < 3; ++k) {
+    pin[3 * e + k] = xyz[3 * a + k];
+    pout[3 * e + k] = xyz[3 * b + k];
+  }
+}
+
+// mid = 0.5 * (p_in + p_out) (marching_tets.hpp:108); also clears the exterior flags.
+__global__ void k_bisect_mid(int64_t ne, const double* __restrict__ pin,
+                             const double* __restrict__ pout, double* mid, uint8_t* ext) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= ne) return;
+  for (int k = 0; k < 3; ++k) mid[3 * e + k] = 0.5 * (pin[3 * e + k] + pout[3 * e + k]);
+  ext[e] = 0;
+}
+
+// (interior(mid) ? p_in : p_out) = mid (marching_tets.hpp:109)
+__global__ void k_bisect_update(int64_t ne, const double* __restrict__ mid,
+                                const uint8_t* __restrict__ ext, double* pin, double* pout) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= ne) return;
+  double* dst = ext[e] ? pout : pin;
+  for (int k = 0; k < 3; ++k) dst[3 * e + k] = mid[3 * e + k];
+}
+
+__global__ void k_bisect_final(int64_t ne, const double* __restrict__ pin,
+                               const double* __restrict__ pout, double* verts) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= ne) return;
+  for (int k = 0; k < 3; ++k) verts[3 * e + k] = 0.5 * (pin[3 * e + k] + pout[3 * e + k]);
+}
+
+void refine(sof_ctx* c, int64_t ne, const int32_t* edges, double* verts, int iterations,
+            int strategies, int tile_size, int v0, int v1, uint64_t* counters) {
+  if (iterations <= 0 || ne == 0) return;  // iterations = 0 keeps the lerp vertices (:100)
+  if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
+  DBuf<double> pin, pout, mid;
+  DBuf<uint8_t> ext;
+  pin.ensure(3 * ne);
+  pout.ensure(3 * ne);
+  mid.ensure(3 * ne);
+  ext.ensure(ne);
+  k_bisect_init<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, edges, c->tv.p, pin.p, pout.p);
+  SOF_LAUNCHED(c);
+  for (int it = 0; it < iterations; ++it) {
+    k_bisect_mid<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, pin.p, pout.p, mid.p, ext.p);
+    SOF_LAUNCHED(c);
+    // classify_point over every view (field_eval.hpp:114-125): exterior iff some view
+    // has observed && complete && O < 0.5; prune skips the rest for that point
+    eval_views(c, v0, v1, ne, mid.p, strategies, tile_size, true, kModeClassify, nullptr, ext.p,
+               nullptr, nullptr, nullptr, counters);
+    k_bisect_update<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, mid.p, ext.p, pin.p, pout.p);
+    SOF_LAUNCHED(c);
+  }
+  k_bisect_final<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, pin.p, pout.p, verts);
+  SOF_LAUNCHED(c);
+}
+
+// ---- K10: weld ------------------------------------------------------------------------------------
+
+__global__ void k_weld_keys(int64_t n, const double* __restrict__ v, double inv, uint64_t* kx,
+                            uint64_t* ky, uint64_t* kz, int32_t* idx) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  // llround(p * inv) (mesh.hpp:57-62); any bijection of the int64 works as a sort key
+  kx[i] = uint64_t(llround(v[3 * i] * inv));
+  ky[i] = uint64_t(llround(v[3 * i + 1] * inv));
+  kz[i] = uint64_t(llround(v[3 * i + 2] * inv));
+  idx[i] = int32_t(i);
+}
+
+__global__ void k_gather_u64(int64_t n, const int32_t* __restrict__ perm,
+                             const uint64_t* __restrict__ src, uint64_t* dst) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j < n) dst[j] = src[perm[j]];
+}
+
+__global__ void k_weld_heads(int64_t n, const int32_t* __restrict__ perm,
+                             const uint64_t* __restrict__ kx, const uint64_t* __restrict__ ky,
+                             const uint64_t* __restrict__ kz, int32_t* head) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= n) return;
+  bool h = j == 0;
+  if (!h) {
+    const int32_t a = perm[j], b = perm[j - 1];
+    h = kx[a] != kx[b] || ky[a] != ky[b] || kz[a] != kz[b];
+  }
+  head[j] = h;
+}
+
+__global__ void k_weld_runfirst(int64_t n, const int32_t* __restrict__ perm,
+                                const int32_t* __restrict__ head, const int32_t* __restrict__ run,
+                                int32_t* run_first) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j < n && head[j]) run_first[run[j]] = perm[j];
+}
+
+__global__ void k_weld_first(int64_t n, const int32_t* __restrict__ perm,
+                             const int32_t* __restrict__ head, const int32_t* __restrict__ run,
+                             const int32_t* __restrict__ run_first, int32_t* first_of,
+                             int32_t* is_first) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= n) return;
+  const int32_t i = perm[j];
+  const int32_t f = run_first[run[j] + head[j] - 1];
+  first_of[i] = f;
+  is_first[i] = (f == i);
+}
+
+__global__ void k_weld_out(int64_t n, const int32_t* __restrict__ is_first,
+                           const int32_t* __restrict__ nid, const double* __restrict__ v,
+                           double* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n || !is_first[i]) return;
+  for (int k = 0; k < 3; ++k) out[3 * nid[i] + k] = v[3 * i + k];
+}
+
+// remap + drop repeated ids / area <= min_area on the welded positions (mesh.hpp:70-77)
+__global__ void k_weld_tris(int64_t nt, const int32_t* __restrict__ tris,
+                            const int32_t* __restrict__ first_of, const int32_t* __restrict__ nid,
+                            const double* __restrict__ wv, double min_area, int32_t* rt,
+                            int32_t* keep) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= nt) return;
+  int32_t r[3];
+  for (int q = 0; q < 3; ++q) r[q] = nid[first_of[tris[3 * k + q]]];
+  bool ok = !(r[0] == r[1] || r[1] == r[2] || r[0] == r[2]);
+  if (ok) {
+    const double* a = wv + 3 * r[0];
+    const double* b = wv + 3 * r[1];
+    const double* cc = wv + 3 * r[2];
+    const double u0 = b[0] - a[0], u1 = b[1] - a[1], u2 = b[2] - a[2];
+    const double w0 = cc[0] - a[0], w1 = cc[1] - a[1], w2 = cc[2] - a[2];
+    const double n0 = u1 * w2 - u2 * w1, n1 = u2 * w0 - u0 * w2, n2 = u0 * w1 - u1 * w0;
+    const double area = 0.5 * sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+    ok = !(area <= min_area);
+  }
+  keep[k] = ok;
+  for (int q = 0; q < 3; ++q) rt[3 * k + q] = r[q];
+}
+
+__global__ void k_compact_tris(int64_t nt, const int32_t* __restrict__ keep,
+                               const int32_t* __restrict__ pos, const int32_t* __restrict__ rt,
+                               int32_t* out) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= nt || !keep[k]) return;
+  for (int q = 0; q < 3; ++q) out[3 * pos[k] + q] = rt[3 * k + q];
+}
+
+void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t* tris,
+              double weld_eps, double min_area) {
+  c->mesh_nv = c->mesh_nt = 0;
+  c->m_verts.ensure(3);
+  c->m_tris.ensure(3);
+  if (n == 0) return;
+  const double inv = 1.0 / weld_eps;
+  DBuf<uint64_t> kx, ky, kz, k1, k2;
+  DBuf<int32_t> p0, p1, head, run, run_first, first_of, is_first, nid;
+  kx.ensure(n); ky.ensure(n); kz.ensure(n); k1.ensure(n); k2.ensure(n);
+  p0.ensure(n); p1.ensure(n); head.ensure(n); run.ensure(n); run_first.ensure(n);
+  first_of.ensure(n); is_first.ensure(n); nid.ensure(n);
+  k_weld_keys<<<grid_for(n, 256), 256, 0, c->stream>>>(n, v, inv, kx.p, ky.p, kz.p, p0.p);
+  SOF_LAUNCHED(c);
+  // LSD over (kx, ky, kz): stable sorts by kz, then ky, then kx; ties keep index order
+  sort_pairs_u64(c, kz.p, k2.p, p0.p, p1.p, n, 64);
+  k_gather_u64<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p1.p, ky.p, k1.p);
+  SOF_LAUNCHED(c);
+  sort_pairs_u64(c, k1.p, k2.p, p1.p, p0.p, n, 64);
+  k_gather_u64<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p0.p, kx.p, k1.p);
+  SOF_LAUNCHED(c);
+  sort_pairs_u64(c, k1.p, k2.p, p0.p, p1.p, n, 64);
+  k_weld_heads<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p1.p, kx.p, ky.p, kz.p, head.p);
+  SOF_LAUNCHED(c);
+  exclusive_scan_i32(c, head.p, run.p, n);
+  k_weld_runfirst<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p1.p, head.p, run.p, run_first.p);
+  SOF_LAUNCHED(c);
+  k_weld_first<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p1.p, head.p, run.p, run_first.p,
+                                                         first_of.p, is_first.p);
+  SOF_LAUNCHED(c);
+  exclusive_scan_i32(c, is_first.p, nid.p, n);
+  const int64_t nout = int64_t(read_scalar(c, nid.p + (n - 1))) + read_scalar(c, is_first.p + (n - 1));
+  c->m_verts.ensure(3 * nout);
+  k_weld_out<<<grid_for(n, 256), 256, 0, c->stream>>>(n, is_first.p, nid.p, v, c->m_verts.p);
+  SOF_LAUNCHED(c);
+  c->mesh_nv = nout;
+  if (nt == 0) return;
+  DBuf<int32_t> rt, keep, pos;
+  rt.ensure(3 * nt);
+  keep.ensure(nt);
+  pos.ensure(nt);
+  k_weld_tris<<<grid_for(nt, 256), 256, 0, c->stream>>>(nt, tris, first_of.p, nid.p, c->m_verts.p,
+                                                          min_area, rt.p, keep.p);
+  SOF_LAUNCHED(c);
+  exclusive_scan_i32(c, keep.p, pos.p, nt);
+  const int64_t ntout = int64_t(read_scalar(c, pos.p + (nt - 1))) + read_scalar(c, keep.p + (nt - 1));
+  c->m_tris.ensure(std::max<int64_t>(3 * ntout, 3));
+  k_compact_tris<<<grid_for(nt, 256), 256, 0, c->stream>>>(nt, keep.p, pos.p, rt.p, c->m_tris.p);
+  SOF_LAUNCHED(c);
+  c->mesh_nt = ntout;
+}
+
+}  // namespace sofk

@@ -1,0 +1,281 @@
+// sof_device.cuh — device-side restatement of the reference's per-(Gaussian, view)
+// and per-(point, Gaussian) arithmetic in FP64, operation for operation.
+//
+// Every expression follows the reference's C++ evaluation order (left-assoc,
+// no contraction; this translation unit is compiled with --fmad=false) and the
+// Eigen-API semantics pinned in oracle/eigen_shim/Eigen/Dense, so the results
+// are bit-identical to the reference compiled against that shim. Each function
+// cites the reference line it restates.
+#pragma once
+
+#include <cstdint>
+
+#include "sof_math.h"
+
+namespace sofk {
+
+constexpr double kMinAlpha = 1.0 / 255.0;  // core.hpp:18
+constexpr double kMaxAlpha = 0.999;        // core.hpp:22
+constexpr double kMinScale = 1e-8;         // gaussian.hpp:20
+constexpr int kBlockPoints = 256;          // kBlockSize tiles.hpp:15
+
+// Camera (camera.hpp:10-21) with the derived centre and tile grid.
+struct Cam {
+  double R[9];  // row-major world-to-view
+  double t[3];
+  double fx, fy, cx, cy;
+  int w, h;
+  double center[3];  // -R^T t (camera.hpp:20), computed on the host in reference order
+};
+
+// Per-(Gaussian, view) record used by the opacity evaluation:
+// PrecomputedGaussian minus tight_bound (precompute.hpp:21-28). 96 B, 16-B aligned.
+struct __align__(16) Rec {
+  double ic[6];  // inv_cov upper triangle xx xy xz yy yz zz
+  double b[3];   // b_vec
+  double c;      // c_scalar
+  double op;     // filtered opacity
+  double zmin;   // min_z
+};
+static_assert(sizeof(Rec) == 96, "record layout");
+
+// View-independent per-Gaussian data (the parts of precompute.hpp:65-75 that do
+// not depend on the camera, hoisted out of the per-view loop).
+struct GaussStatic {
+  double pos[3];
+  double scale[3];
+  double rot[9];   // toRotationMatrix(q)            (gaussian.hpp:24)
+  double cov[9];   // covariance(g) = R S^2 R^T      (gaussian.hpp:23-26)
+  double icf[9];   // full inv_cov (NOT symmetrised: b_vec uses all 9, precompute.hpp:66-72)
+  double op;       // filtered_opacity               (gaussian.hpp:67-73)
+  double E;        // tight_bound, 0 when dead       (gaussian.hpp:60-64)
+};
+
+// ---- L0: Eigen-shim semantics ---------------------------------------------------------
+
+// Quaternion::toRotationMatrix (Eigen formula), q = (w, x, y, z).
+__host__ __device__ inline void quat_to_rot(double w, double x, double y, double z, double* r) {
+  const double tx = 2.0 * x, ty = 2.0 * y, tz = 2.0 * z;
+  const double twx = tx * w, twy = ty * w, twz = tz * w;
+  const double txx = tx * x, txy = ty * x, txz = tz * x;
+  const double tyy = ty * y, tyz = tz * y, tzz = tz * z;
+  r[0] = 1.0 - (tyy + tzz);
+  r[1] = txy - twz;
+  r[2] = txz + twy;
+  r[3] = txy + twz;
+  r[4] = 1.0 - (txx + tzz);
+  r[5] = tyz - twx;
+  r[6] = txz - twy;
+  r[7] = tyz + twx;
+  r[8] = 1.0 - (txx + tyy);
+}
+
+// 3x3 determinant, Eigen's bruteforce_det3 expansion.
+__host__ __device__ inline double det3(const double* m) {
+  const double h0 = m[0] * (m[4] * m[8] - m[5] * m[7]);
+  const double h1 = m[1] * (m[3] * m[8] - m[5] * m[6]);
+  const double h2 = m[2] * (m[3] * m[7] - m[4] * m[6]);
+  return h0 - h1 + h2;
+}
+
+// r * diag(d) * r^T, each entry ((M(i,0) r(j,0) + M(i,1) r(j,1)) + M(i,2) r(j,2)).
+__host__ __device__ inline void r_diag_rt(const double* r, const double* d, double* out) {
+  double m[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) m[3 * i + j] = r[3 * i + j] * d[j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      out[3 * i + j] = m[3 * i] * r[3 * j] + m[3 * i + 1] * r[3 * j + 1] + m[3 * i + 2] * r[3 * j + 2];
+}
+
+// Camera::to_view (camera.hpp:19): R x + t, one component.
+__host__ __device__ inline double to_view_c(const Cam& c, int i, double x0, double x1, double x2) {
+  return c.R[3 * i] * x0 + c.R[3 * i + 1] * x1 + c.R[3 * i + 2] * x2 + c.t[i];
+}
+
+// ---- L1: per-(Gaussian, view) preprocessing ----------------------------------------------
+
+// View-independent half of precompute() (precompute.hpp:65-70) + filtered_opacity
+// (gaussian.hpp:67-73) + tight_bound (gaussian.hpp:60-64).
+__host__ __device__ inline void gauss_static(const double* pos, const double* scale,
+                                             const double* q, double opacity,
+                                             double filter_scale, GaussStatic& g) {
+  for (int k = 0; k < 3; ++k) {
+    g.pos[k] = pos[k];
+    g.scale[k] = scale[k];
+  }
+  quat_to_rot(q[0], q[1], q[2], q[3], g.rot);
+  // covariance(g): r * scale.cwiseProduct(scale).asDiagonal() * r^T  (unclamped scale)
+  const double s2[3] = {scale[0] * scale[0], scale[1] * scale[1], scale[2] * scale[2]};
+  r_diag_rt(g.rot, s2, g.cov);
+  // inv_cov: r * (s.cwiseProduct(s)).cwiseInverse().asDiagonal() * r^T with s = max(scale, 1e-8)
+  double s[3], inv[3];
+  for (int k = 0; k < 3; ++k) {
+    s[k] = (scale[k] < kMinScale) ? kMinScale : scale[k];
+    inv[k] = 1.0 / (s[k] * s[k]);
+  }
+  r_diag_rt(g.rot, inv, g.icf);
+  // filtered_opacity
+  if (filter_scale <= 0.0) {
+    g.op = opacity;
+  } else {
+    const double det = det3(g.cov);
+    double cf[9];
+    for (int k = 0; k < 9; ++k) cf[k] = g.cov[k] + filter_scale * ((k % 4 == 0) ? 1.0 : 0.0);
+    const double det_f = det3(cf);
+    g.op = opacity * sqrt(det / det_f);
+  }
+  // tight_bound(filtered opacity).value_or(0.0)
+  if (g.op < kMinAlpha) {
+    g.E = 0.0;
+  } else {
+    const double v = 2.0 * sof_log(255.0 * g.op);
+    g.E = sqrt((v < 0.0) ? 0.0 : v);
+  }
+}
+
+// View-dependent half of precompute() (precompute.hpp:71-76), diagonal z-extent mode.
+__host__ __device__ inline void gauss_view(const GaussStatic& g, const Cam& cam, Rec& r) {
+  // pc.inv_cov = upper triangle xx xy xz yy yz zz (precompute.hpp:69-70)
+  r.ic[0] = g.icf[0];
+  r.ic[1] = g.icf[1];
+  r.ic[2] = g.icf[2];
+  r.ic[3] = g.icf[4];
+  r.ic[4] = g.icf[5];
+  r.ic[5] = g.icf[8];
+  const double d0 = cam.center[0] - g.pos[0];
+  const double d1 = cam.center[1] - g.pos[1];
+  const double d2 = cam.center[2] - g.pos[2];
+  // b_vec = inv_cov * delta with the full (unsymmetrised) matrix (precompute.hpp:71-72)
+  r.b[0] = g.icf[0] * d0 + g.icf[1] * d1 + g.icf[2] * d2;
+  r.b[1] = g.icf[3] * d0 + g.icf[4] * d1 + g.icf[5] * d2;
+  r.b[2] = g.icf[6] * d0 + g.icf[7] * d1 + g.icf[8] * d2;
+  r.c = d0 * r.b[0] + d1 * r.b[1] + d2 * r.b[2];
+  r.op = g.op;
+  // z_extent_sigma kDiagonal (precompute.hpp:49-55): sqrt((W Sigma W^T)(2,2))
+  double wc[3];
+  for (int j = 0; j < 3; ++j)
+    wc[j] = cam.R[6] * g.cov[j] + cam.R[7] * g.cov[3 + j] + cam.R[8] * g.cov[6 + j];
+  const double czz = wc[0] * cam.R[6] + wc[1] * cam.R[7] + wc[2] * cam.R[8];
+  const double zc = to_view_c(cam, 2, g.pos[0], g.pos[1], g.pos[2]);
+  r.zmin = zc - g.E * sqrt(czz);
+}
+
+// x86-64 cvttsd2si semantics for int(x) (out of range / NaN -> INT_MIN), the
+// reference binary's behaviour for int(std::floor(.)) at tiles.hpp:127-130.
+__host__ __device__ inline int x86_int(double x) {
+  return (x >= -2147483648.0 && x < 2147483648.0) ? (int)x : (int)0x80000000;
+}
+
+// Tile rectangle of one Gaussian's E-scaled OBB (build_tile_binding tiles.hpp:104-133).
+// Returns false when the Gaussian is skipped (E <= 0 or fully off screen).
+__host__ __device__ inline bool tile_rect(const GaussStatic& g, const Cam& cam, int tile_size,
+                                          int tiles_x, int tiles_y, int& tx0, int& tx1, int& ty0,
+                                          int& ty1) {
+  const double r = g.E;
+  if (r <= 0.0) return false;
+  double min_x = 1e300, max_x = -1e300, min_y = 1e300, max_y = -1e300;
+  bool crosses = false;
+  for (int mask = 0; mask < 8; ++mask) {
+    const double l0 = r * g.scale[0] * (double)((mask & 1) ? 1 : -1);
+    const double l1 = r * g.scale[1] * (double)((mask & 2) ? 1 : -1);
+    const double l2 = r * g.scale[2] * (double)((mask & 4) ? 1 : -1);
+    // g.position + rot * local
+    const double p0 = g.pos[0] + (g.rot[0] * l0 + g.rot[1] * l1 + g.rot[2] * l2);
+    const double p1 = g.pos[1] + (g.rot[3] * l0 + g.rot[4] * l1 + g.rot[5] * l2);
+    const double p2 = g.pos[2] + (g.rot[6] * l0 + g.rot[7] * l1 + g.rot[8] * l2);
+    const double vx = to_view_c(cam, 0, p0, p1, p2);
+    const double vy = to_view_c(cam, 1, p0, p1, p2);
+    const double vz = to_view_c(cam, 2, p0, p1, p2);
+    if (vz <= 1e-9) {
+      crosses = true;
+      break;
+    }
+    const double px = cam.fx * vx / vz + cam.cx;
+    const double py = cam.fy * vy / vz + cam.cy;
+    min_x = (px < min_x) ? px : min_x;  // std::min(min_x, px)
+    max_x = (max_x < px) ? px : max_x;  // std::max(max_x, px)
+    min_y = (py < min_y) ? py : min_y;
+    max_y = (max_y < py) ? py : max_y;
+  }
+  tx0 = 0;
+  tx1 = tiles_x - 1;
+  ty0 = 0;
+  ty1 = tiles_y - 1;
+  if (!crosses) {
+    int a = x86_int(floor(min_x)) / tile_size;
+    tx0 = (0 < a) ? a : 0;
+    a = x86_int(floor(max_x)) / tile_size;
+    tx1 = (a < tiles_x - 1) ? a : tiles_x - 1;
+    a = x86_int(floor(min_y)) / tile_size;
+    ty0 = (0 < a) ? a : 0;
+    a = x86_int(floor(max_y)) / tile_size;
+    ty1 = (a < tiles_y - 1) ? a : tiles_y - 1;
+    if (max_x < 0.0 || min_x >= (double)cam.w || max_y < 0.0 || min_y >= (double)cam.h)
+      return false;
+  }
+  return tx0 <= tx1 && ty0 <= ty1;
+}
+
+// ---- L2: per-point ray setup (field_eval.hpp:62-79) -------------------------------------
+
+struct PointRay {
+  double d[3];   // unit direction camera -> x
+  double t;      // |x - o|
+  double zp;     // view-space z of x
+  int tile;      // tile index (valid when observed)
+  bool observed;
+};
+
+__host__ __device__ inline PointRay point_ray(const Cam& cam, double x0, double x1, double x2,
+                                              int tile_size, int tiles_x) {
+  PointRay pr;
+  pr.observed = false;
+  pr.tile = -1;
+  // Camera::observes via project (camera.hpp:23-33)
+  const double vx = to_view_c(cam, 0, x0, x1, x2);
+  const double vy = to_view_c(cam, 1, x0, x1, x2);
+  const double vz = to_view_c(cam, 2, x0, x1, x2);
+  pr.zp = vz;
+  if (vz <= 0.0) return pr;
+  const double px = cam.fx * vx / vz + cam.cx;
+  const double py = cam.fy * vy / vz + cam.cy;
+  if (!(px >= 0.0 && px < (double)cam.w && py >= 0.0 && py < (double)cam.h)) return pr;
+  // ray_through_point (camera.hpp:52-59)
+  const double e0 = x0 - cam.center[0], e1 = x1 - cam.center[1], e2 = x2 - cam.center[2];
+  pr.t = sqrt(e0 * e0 + e1 * e1 + e2 * e2);
+  if (pr.t < 1e-12) return pr;  // field_eval.hpp:67-70
+  pr.d[0] = e0 / pr.t;
+  pr.d[1] = e1 / pr.t;
+  pr.d[2] = e2 / pr.t;
+  pr.tile = (int)py / tile_size * tiles_x + (int)px / tile_size;  // field_eval.hpp:79
+  pr.observed = true;
+  return pr;
+}
+
+// ---- L2: one (point, Gaussian) pair of view_opacity (field_eval.hpp:95-103) ---------------
+// Returns the clamped alpha, or 0 when the pair is skipped (te <= 0 or alpha < 1/255).
+__device__ __forceinline__ double pair_alpha(const Rec& r, const double* d, double t) {
+  const double x = d[0], y = d[1], z = d[2];
+  // abc_cached (precompute.hpp:39-45)
+  const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
+                   2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
+  const double b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
+  const double t_star = -b / (2.0 * a);          // peak_t gaussian.hpp:52
+  const double te = (t < t_star) ? t : t_star;   // std::min(t_star, t)
+  if (te <= 0.0) return 0.0;
+  const double arg = -0.5 * ((a * te + b) * te + r.c);  // eval_1d gaussian.hpp:47-49
+  double alpha = r.op * sof_exp(arg);
+  if (alpha < kMinAlpha) return 0.0;
+  return (kMaxAlpha < alpha) ? kMaxAlpha : alpha;  // std::min(alpha, kMaxAlpha)
+}
+
+// Orderable 64-bit key of a double (ascending), with -0 folded onto +0 so that
+// equal values compare equal as in `min_z != min_z` (tiles.hpp:141).
+__host__ __device__ inline uint64_t double_key(double v) {
+  if (v == 0.0) v = 0.0;
+  const uint64_t u = sof_double_to_bits(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+}  // namespace sofk

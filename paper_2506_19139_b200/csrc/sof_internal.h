@@ -1,0 +1,221 @@
+// sof_internal.h — context, device buffers and stage entry points shared by the
+// translation units of libsof_cuda.so. Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sof_device.cuh"
+
+namespace sofk {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArg : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct OomError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define SOF_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      if (e_ == cudaErrorMemoryAllocation) {                                               \
+        (void)cudaGetLastError();                                                          \
+        throw ::sofk::OomError(std::string("CUDA out of memory at ") + __FILE__ + ":" +   \
+                               std::to_string(__LINE__));                                  \
+      }                                                                                    \
+      throw ::sofk::CudaError(std::string(cudaGetErrorString(e_)) + " at " + __FILE__ +   \
+                              ":" + std::to_string(__LINE__));                             \
+    }                                                                                      \
+  } while (0)
+
+// Grow-only device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  size_t n = 0;    // logical size
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), cap(o.cap), n(o.n) { o.p = nullptr; o.cap = o.n = 0; }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  T* ensure(size_t count) {
+    if (count > cap) {
+      if (p) SOF_CUDA(cudaFree(p));
+      p = nullptr;
+      cap = 0;
+      const size_t want = count + count / 8 + 16;
+      SOF_CUDA(cudaMalloc(&p, want * sizeof(T)));
+      cap = want;
+    }
+    n = count;
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = n = 0;
+  }
+  void swap(DBuf& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(cap, o.cap);
+    std::swap(n, o.n);
+  }
+  size_t bytes() const { return cap * sizeof(T); }
+};
+
+// Per-view Gaussian tile lists (TileBinding tiles.hpp:88-92) resident on the device.
+struct Binding {
+  int view = -1, tile_size = 0, tiles_x = 0, tiles_y = 0;
+  int64_t entries = 0;
+  DBuf<int64_t> off;  // [T + 1]
+  DBuf<int32_t> ent;  // [entries], per tile sorted by (min_z, index)
+};
+
+// Scratch of the per-view point schedule (schedule_points tiles.hpp:29-84).
+struct PointSchedule {
+  DBuf<uint64_t> key_in, key_out;
+  DBuf<int32_t> idx_in, idx_out;
+  DBuf<int64_t> tile_start;  // [T + 1]
+  DBuf<int32_t> block_flag, block_id;
+  DBuf<int4> blocks;         // {start, end, tile, 0}
+  DBuf<int32_t> counters;    // [0] active count, [1] block count
+};
+
+enum EvalMode { kModeLabel = 0, kModeClassify = 1, kModeView = 2, kModeValue = 3 };
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace sofk
+
+struct sof_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // scene
+  int64_t n = 0;
+  double filter_scale = 0.0;
+  bool has_scene = false;
+  sofk::DBuf<double> pos, scale, rot, opa, dc;
+  sofk::DBuf<sofk::GaussStatic> gstat;
+
+  // views
+  std::vector<sofk::Cam> cams;
+
+  // per-view record cache: recs[v] valid when rec_valid[v]
+  std::vector<sofk::DBuf<sofk::Rec>> recs;
+  std::vector<char> rec_valid;
+  std::vector<sofk::Binding> bindings;  // per view (cache keyed by tile size)
+  size_t cache_budget = size_t(96) << 30;  // bytes of HBM the per-view caches may use
+  size_t cache_bytes = 0;
+  sofk::DBuf<sofk::Rec> rec_scratch;      // when the cache budget is exhausted
+  sofk::Binding bind_scratch;
+
+  // binning scratch
+  sofk::DBuf<int4> rect;
+  sofk::DBuf<uint32_t> gcount;
+  sofk::DBuf<uint64_t> zkey_in, zkey_out;
+  sofk::DBuf<int32_t> gidx_in, gidx_out;
+  sofk::DBuf<int64_t> goff;
+  sofk::DBuf<uint32_t> ekey_in, ekey_out;
+  sofk::DBuf<int32_t> eval_in;
+
+  sofk::PointSchedule sched;
+  sofk::DBuf<char> cub_tmp;
+  sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
+  sofk::DBuf<int64_t> d_scalar;               // small device scalars
+
+  // tets
+  int64_t nv = 0, nt = 0;
+  bool has_tets = false;
+  sofk::DBuf<double> tv;
+  sofk::DBuf<int32_t> tt;
+
+  // generic point buffers
+  sofk::DBuf<double> pts;
+  sofk::DBuf<double> min_op, o_view;
+  sofk::DBuf<uint8_t> ext, observed, complete;
+
+  // mesher results
+  int64_t n_edges = -1, n_march_tris = -1, mesh_nv = -1, mesh_nt = -1, grid_n = -1;
+  sofk::DBuf<double> grid_opacity;
+  sofk::DBuf<int32_t> r_edges, r_tris, m_tris;
+  sofk::DBuf<double> r_everts, m_verts;
+  int64_t bind_tiles = -1, bind_entries = -1;
+  int last_binding_view = -1;
+
+  // instrumentation
+  double eval_ms = 0.0;
+  int64_t eval_launches = 0;
+  bool time_eval = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace sofk {
+
+// ---- k_field.cu -------------------------------------------------------------------------
+void scene_prep(sof_ctx* c);
+const Rec* view_records(sof_ctx* c, int view);
+const Binding& view_binding(sof_ctx* c, int view, int tile_size);
+void invalidate_view_caches(sof_ctx* c);
+// Evaluates points xyz_dev[n] against views [v0, v1) in order (field_eval.hpp:59-176).
+void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz_dev, int strategies,
+                int tile_size, bool classify_mode, EvalMode mode, double* min_op, uint8_t* ext,
+                double* o_out, uint8_t* observed_out, uint8_t* complete_out,
+                uint64_t* counters_host);
+void finalize_label(sof_ctx* c, int64_t n, const double* min_op, const uint8_t* ext, double* out);
+void schedule_points_exact(sof_ctx* c, int view, int64_t n, const double* xyz_dev, int tile_size,
+                           int32_t* tile_assignment, std::vector<int32_t>& order,
+                           std::vector<int32_t>& key_tile, std::vector<double>& key_depth,
+                           std::vector<int32_t>& block_ranges, std::vector<int32_t>& block_to_tile);
+
+// ---- k_mesh.cu --------------------------------------------------------------------------
+void march(sof_ctx* c, const double* opacity_dev);
+void refine(sof_ctx* c, int64_t ne, const int32_t* edges_dev, double* verts_dev, int iterations,
+            int strategies, int tile_size, int v0, int v1, uint64_t* counters);
+void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris,
+              const int32_t* tris_dev, double weld_eps, double min_area);
+
+// ---- helpers ----------------------------------------------------------------------------
+inline unsigned grid_for(int64_t n, int block) { return unsigned((n + block - 1) / block); }
+void sort_pairs_u64(sof_ctx* c, const uint64_t* kin, uint64_t* kout, const int32_t* vin,
+                    int32_t* vout, int64_t n, int end_bit);
+void sort_pairs_u32(sof_ctx* c, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
+                    int32_t* vout, int64_t n, int end_bit);
+void exclusive_scan_u32_to_i64(sof_ctx* c, const uint32_t* in, int64_t* out, int64_t n);
+void exclusive_scan_i32(sof_ctx* c, const int32_t* in, int32_t* out, int64_t n);
+int bits_for(uint64_t max_value);
+template <typename T>
+inline T read_scalar(sof_ctx* c, const T* dev) {
+  T h;
+  SOF_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  SOF_CUDA(cudaStreamSynchronize(c->stream));
+  return h;
+}
+#define SOF_LAUNCHED(c)              \
+  do {                               \
+    (c)->launches++;                 \
+    SOF_CUDA(cudaGetLastError());    \
+  } while (0)
+
+}  // namespace sofk

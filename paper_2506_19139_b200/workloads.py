@@ -1,0 +1,224 @@
+"""Synthetic inputs for the benchmark configurations.
+
+Deterministic generators for the tetra input (a jittered Kuhn/Freudenthal lattice)
+and the C2-C5 scenes/cameras. These produce INPUT data only; nothing here is on
+the compute path. The scene generator uses numpy's PCG64 with a fixed seed
+(2506191390 + config index) instead of libstdc++'s mt19937_64 distributions, so
+the same arrays are fed to the GPU path and to the CPU reference.
+"""
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass
+
+import numpy as np
+
+SEED_BASE = 2506191390
+
+# per-config sizes (BASELINE.json configs)
+CONFIGS = {
+    "C1": dict(gaussians=10_000, views=16, width=256, height=256, lattice=45),
+    "C2": dict(gaussians=1_000_000, views=100, width=1920, height=1080, lattice=0),
+    "C3": dict(gaussians=3_000_000, views=200, width=1600, height=1064, lattice=300),
+    "C4": dict(gaussians=5_000_000, views=300, width=1920, height=1080, lattice=345),
+    "C5": dict(gaussians=10_000_000, views=500, width=1600, height=1064, lattice=436),
+}
+
+
+@dataclass
+class Scene:
+    pos: np.ndarray
+    scale: np.ndarray
+    rot: np.ndarray
+    opacity: np.ndarray
+    dc: np.ndarray
+
+    @property
+    def n(self):
+        return len(self.opacity)
+
+
+@dataclass
+class Cams:
+    R: np.ndarray
+    t: np.ndarray
+    intr: np.ndarray
+    wh: np.ndarray
+    nearfar: np.ndarray
+
+    @property
+    def v(self):
+        return len(self.t)
+
+    def subset(self, idx):
+        return Cams(*(np.ascontiguousarray(a[idx]) for a in (self.R, self.t, self.intr, self.wh, self.nearfar)))
+
+
+# ---- tetra input -------------------------------------------------------------------------------
+
+_PERMS = list(itertools.permutations(range(3)))  # xyz, xzy, yxz, yzx, zxy, zyx
+
+
+def _hash3(ids: np.ndarray) -> np.ndarray:
+    """Three deterministic uniforms in [0,1) per id (splitmix64)."""
+    out = np.empty((len(ids), 3))
+    for c in range(3):
+        z = (ids.astype(np.uint64) * np.uint64(3) + np.uint64(c + 1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+        out[:, c] = (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    return out
+
+
+def kuhn_lattice(n: int, lo: float = -2.5, hi: float = 2.5, jitter: float = 0.25):
+    """n^3 vertices (id = i + n (j + n k)), 6 (n-1)^3 tets (per cell the 6 Kuhn
+    permutations in fixed order, each positively oriented), vertices jittered by
+    jitter * cell * (hash3(id) - 0.5)."""
+    cell = (hi - lo) / (n - 1)
+    g = np.arange(n, dtype=np.float64) * cell + lo
+    k, j, i = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    verts = np.stack([g[i.ravel()], g[j.ravel()], g[k.ravel()]], axis=1)
+    ids = np.arange(n ** 3, dtype=np.int64)
+    if jitter:
+        verts += jitter * cell * (_hash3(ids) - 0.5)
+    m = n - 1
+    ck, cj, ci = np.meshgrid(np.arange(m), np.arange(m), np.arange(m), indexing="ij")
+    base = (ci + n * (cj + n * ck)).ravel().astype(np.int64)
+    step = np.array([1, n, n * n], dtype=np.int64)
+    tets = np.empty((len(base), 6, 4), dtype=np.int32)
+    for p, perm in enumerate(_PERMS):
+        v0 = base
+        v1 = v0 + step[perm[0]]
+        v2 = v1 + step[perm[1]]
+        v3 = v2 + step[perm[2]]
+        # even permutations are positively oriented; swap the last two otherwise
+        parity = sum(1 for a in range(3) for b in range(a + 1, 3) if perm[a] > perm[b]) % 2
+        if parity == 0:
+            tets[:, p] = np.stack([v0, v1, v2, v3], 1)
+        else:
+            tets[:, p] = np.stack([v0, v1, v3, v2], 1)
+    return verts, tets.reshape(-1, 4)
+
+
+# ---- cameras --------------------------------------------------------------------------------------
+
+def look_at(eye, target, up, fx, fy, w, h):
+    """camera.hpp:62-79 in numpy (same formula; inputs only)."""
+    eye = np.asarray(eye, float)
+    fwd = np.asarray(target, float) - eye
+    fwd = fwd / np.sqrt(fwd @ fwd)
+    right = np.cross(fwd, up)
+    right = right / np.sqrt(right @ right)
+    down = np.cross(fwd, right)
+    R = np.stack([right, down, fwd])
+    t = -R @ eye
+    return R, t, np.array([fx, fy, w * 0.5, h * 0.5])
+
+
+def orbit_cameras(count: int, width: int, height: int, radius: float = 4.0, focal_scale: float = 0.8) -> Cams:
+    """Golden-spiral band z in [-0.8, 0.8] looking at the origin (test_util.hpp:72-84
+    pattern), f = focal_scale * W."""
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    R = np.empty((count, 3, 3))
+    t = np.empty((count, 3))
+    intr = np.empty((count, 4))
+    for i in range(count):
+        z = 0.8 - 1.6 * (i + 0.5) / count
+        r = np.sqrt(max(0.0, 1.0 - z * z))
+        phi = golden * i
+        eye = radius * np.array([r * np.cos(phi), r * np.sin(phi), z])
+        fwd = -eye / np.linalg.norm(eye)
+        up = np.array([1.0, 0, 0]) if abs(fwd[1]) > 0.9 else np.array([0, 1.0, 0])
+        f = focal_scale * width
+        R[i], t[i], intr[i] = look_at(eye, np.zeros(3), up, f, f, width, height)
+    wh = np.tile(np.array([width, height], np.int32), (count, 1))
+    nf = np.tile([0.2, 100.0], (count, 1))
+    return Cams(R, t, intr, wh, nf)
+
+
+# ---- scenes ----------------------------------------------------------------------------------------
+
+def _rot_z_to(normals: np.ndarray) -> np.ndarray:
+    """Unit quaternions (w,x,y,z) rotating +z onto each normal."""
+    z = np.array([0.0, 0.0, 1.0])
+    axis = np.cross(np.broadcast_to(z, normals.shape), normals)
+    s = np.linalg.norm(axis, axis=1)
+    c = normals @ z
+    half = np.arctan2(s, c) * 0.5
+    axis = np.where(s[:, None] > 1e-12, axis / np.maximum(s, 1e-300)[:, None], np.array([1.0, 0, 0]))
+    return np.concatenate([np.cos(half)[:, None], axis * np.sin(half)[:, None]], axis=1)
+
+
+def synthetic_scene(n: int, config_index: int) -> Scene:
+    """Appendix B: 85% surface Gaussians on 3 spheres + ground plane + 2 boxes,
+    7% unbounded background shell, 8% dead (opacity below 1/255)."""
+    rng = np.random.default_rng(SEED_BASE + config_index)
+    n_bg = int(round(0.07 * n))
+    n_dead = int(round(0.08 * n))
+    n_surf = n - n_bg - n_dead
+    n_on = n_surf + n_dead
+    # surfaces: spheres (centre, radius), plane z=-1 within |x|,|y|<=3, boxes (lo, hi)
+    spheres = [((-0.9, 0.2, 0.0), 0.8), ((0.9, -0.3, 0.3), 0.6), ((0.0, 0.9, -0.4), 0.5)]
+    boxes = [((-1.8, -1.6, -1.0), (-1.0, -0.8, -0.2)), ((1.0, 1.0, -1.0), (1.7, 1.8, 0.1))]
+    areas = [4 * np.pi * r * r for _, r in spheres] + [36.0]
+    for lo, hi in boxes:
+        d = np.subtract(hi, lo)
+        areas.append(2 * (d[0] * d[1] + d[1] * d[2] + d[0] * d[2]))
+    areas = np.array(areas)
+    which = rng.choice(len(areas), size=n_on, p=areas / areas.sum())
+    pos = np.empty((n_on, 3))
+    nrm = np.empty((n_on, 3))
+    for k, (c, r) in enumerate(spheres):
+        m = which == k
+        d = rng.normal(size=(m.sum(), 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        pos[m] = np.asarray(c) + r * d
+        nrm[m] = d
+    m = which == 3
+    pos[m] = np.stack([rng.uniform(-3, 3, m.sum()), rng.uniform(-3, 3, m.sum()), np.full(m.sum(), -1.0)], 1)
+    nrm[m] = (0, 0, 1)
+    for b, (lo, hi) in enumerate(boxes):
+        m = which == 4 + b
+        cnt = m.sum()
+        lo, hi = np.asarray(lo), np.asarray(hi)
+        p = rng.uniform(lo, hi, size=(cnt, 3))
+        face = rng.integers(0, 6, cnt)
+        ax = face // 2
+        side = face % 2
+        p[np.arange(cnt), ax] = np.where(side == 1, hi[ax], lo[ax])
+        nn = np.zeros((cnt, 3))
+        nn[np.arange(cnt), ax] = np.where(side == 1, 1.0, -1.0)
+        pos[m] = p
+        nrm[m] = nn
+    s = 1.5 * np.sqrt(areas.sum() / max(n_on, 1))
+    scale_on = np.tile([s, s, 0.1 * s], (n_on, 1)) * rng.uniform(0.7, 1.3, (n_on, 1))
+    rot_on = _rot_z_to(nrm)
+    opa_on = rng.uniform(0.5, 0.99, n_on)
+    dead = np.zeros(n_on, bool)
+    dead[rng.choice(n_on, n_dead, replace=False)] = True
+    opa_on[dead] = rng.uniform(0.3 / 255, 0.99 / 255, n_dead)
+    # background shell, radius 5..20 (unbounded scene)
+    d = rng.normal(size=(n_bg, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    pos_bg = d * rng.uniform(5, 20, (n_bg, 1))
+    scale_bg = np.repeat(rng.uniform(0.05, 0.5, (n_bg, 1)), 3, axis=1)
+    q = rng.normal(size=(n_bg, 4))
+    rot_bg = q / np.linalg.norm(q, axis=1, keepdims=True)
+    opa_bg = rng.uniform(0.05, 0.6, n_bg)
+    pos = np.concatenate([pos, pos_bg])
+    scale = np.concatenate([scale_on, scale_bg])
+    rot = np.concatenate([rot_on, rot_bg])
+    opa = np.concatenate([opa_on, opa_bg])
+    dc = rng.uniform(0, 1, (n, 3))
+    perm = rng.permutation(n)
+    return Scene(*(np.ascontiguousarray(a[perm]) for a in (pos, scale, rot, opa, dc)))
+
+
+def config_inputs(name: str, lattice: bool = True):
+    cfg = CONFIGS[name]
+    idx = int(name[1:])
+    scene = synthetic_scene(cfg["gaussians"], idx)
+    cams = orbit_cameras(cfg["views"], cfg["width"], cfg["height"])
+    grid = kuhn_lattice(cfg["lattice"]) if (lattice and cfg["lattice"]) else None
+    return scene, cams, grid

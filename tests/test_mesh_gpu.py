@@ -1,0 +1,137 @@
+"""GPU parity of the Marching-Tetrahedra mesher against the compiled reference.
+
+Bit-exact: crossing edges and their numbering (first appearance), lerp and refined
+vertex positions, triangle indices and winding, welded mesh, and the PLY bytes of
+write_mesh_ply (io_mesh.hpp:55-73). Reference: marching_tets.hpp:29-114,
+mesh.hpp:36-79, extract.hpp:59-78.
+"""
+import numpy as np
+import pytest
+
+import paper_2506_19139_b200 as sof
+from paper_2506_19139_b200.workloads import kuhn_lattice
+from oracle.refpy import ALL
+
+pytestmark = pytest.mark.gpu
+
+SINGLE = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1.0]])
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+@pytest.mark.parametrize("opa", [[0.4, 0.4, 0.4, 0.6], [0.4, 0.4, 0.6, 0.6], [0.6, 0.7, 0.8, 0.9],
+                                 [0.1, 0.2, 0.3, 0.4], [0.4, 0.6, 0.4, 0.4], [0.6, 0.6, 0.6, 0.4],
+                                 [0.6, 0.4, 0.6, 0.4], [0.5, 0.4, 0.4, 0.4]])
+def test_single_tet_cases(ref, opa):
+    """MarchingTets.* (test_mesher.cpp:75-101) on every case shape."""
+    grid = sof.TetGrid(SINGLE, np.array([[0, 1, 2, 3]], np.int32), np.array(opa))
+    got = sof.marching_tets(grid)
+    want = ref.marching_tets(SINGLE, grid.tetrahedra, grid.opacity)
+    np.testing.assert_array_equal(got.edges, want["edges"])
+    np.testing.assert_array_equal(bits(got.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(got.triangles, want["triangles"])
+
+
+@pytest.fixture(scope="module")
+def lattice_case(ref):
+    scene = ref.random_scene(55, 40, 1.0)
+    cams = ref.orbit_cameras(5, 4.0, 1.8, 64)
+    verts, tets = kuhn_lattice(14, -1.3, 1.3)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    return scene, cams, rc, views, verts, tets
+
+
+def test_march_random_field(ref, lattice_case):
+    _, _, _, _, verts, tets = lattice_case
+    rng = np.random.default_rng(5)
+    opa = rng.uniform(0.2, 0.8, len(verts))
+    opa[::17] = 0.5  # exact iso-value: inside (>= 0.5), s = 0 lerp
+    got = sof.marching_tets(sof.TetGrid(verts, tets, opa))
+    want = ref.marching_tets(verts, tets, opa)
+    np.testing.assert_array_equal(got.edges, want["edges"])
+    np.testing.assert_array_equal(bits(got.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(got.triangles, want["triangles"])
+
+
+@pytest.mark.parametrize("mask", [31, 0, 9, 27])
+def test_refine_bitexact(lattice_case, mask):
+    scene, cams, rc, views, verts, tets = lattice_case
+    rev = rc.evaluator(mask)
+    opa = rev.label_grid(verts, True)
+    m = sof.marching_tets(sof.TetGrid(verts, tets, opa), ctx=views.ctx)
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.from_mask(mask))
+    rev.reset_counters()
+    want = rev.refine(verts, m.edges, m.vertices, 8)
+    sof.binary_search_refine(m, sof.TetGrid(verts, tets, opa), ev, 8)
+    np.testing.assert_array_equal(bits(m.vertices), bits(want))
+    assert ev.counters() == rev.counters()
+
+
+def test_refine_zero_iterations_keeps_lerp(lattice_case):
+    scene, cams, rc, views, verts, tets = lattice_case
+    opa = rc.evaluator(ALL).label_grid(verts, True)
+    m = sof.marching_tets(sof.TetGrid(verts, tets, opa), ctx=views.ctx)
+    before = m.vertices.copy()
+    sof.binary_search_refine(m, sof.TetGrid(verts, tets, opa), sof.FieldEvaluator(scene, views, sof.EvalStrategies.all()), 0)
+    np.testing.assert_array_equal(bits(m.vertices), bits(before))
+
+
+def test_assemble_weld_and_degenerate(ref):
+    """AssembleMesh.WeldAndDegenerate / EmptyInput (test_mesher.cpp:139-153)."""
+    verts = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1 + 1e-9, 0, 0]], float)
+    tris = np.array([[0, 1, 2], [0, 3, 2], [0, 1, 3]], np.int32)
+    got = sof.assemble_mesh(verts, tris)
+    want = ref.assemble(verts, tris)
+    assert len(got.vertices) == 3 and len(got.triangles) == 2
+    np.testing.assert_array_equal(bits(got.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(got.triangles, want["triangles"])
+    empty = sof.assemble_mesh(np.zeros((0, 3)), np.zeros((0, 3), np.int32))
+    assert len(empty.vertices) == 0 and len(empty.triangles) == 0
+
+
+def test_assemble_random_duplicates(ref):
+    rng = np.random.default_rng(9)
+    base = rng.uniform(-1, 1, (500, 3))
+    verts = np.concatenate([base, base[rng.integers(0, 500, 300)] + rng.normal(0, 2e-8, (300, 3))])
+    verts = verts[rng.permutation(len(verts))]
+    tris = rng.integers(0, len(verts), (2000, 3)).astype(np.int32)
+    got = sof.assemble_mesh(verts, tris)
+    want = ref.assemble(verts, tris)
+    np.testing.assert_array_equal(bits(got.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(got.triangles, want["triangles"])
+
+
+@pytest.mark.parametrize("mask", [31, 0])
+def test_extract_fused_ply_bytes(ref, lattice_case, tmp_path, mask):
+    """The fused device pipeline reproduces extract_mesh's mesh byte for byte
+    (Extract.DeterministicAcrossThreadCounts, test_mesher.cpp:242-257)."""
+    scene, cams, rc, views, verts, tets = lattice_case
+    want = rc.extract_tetgrid(verts, tets, strategies=mask, iterations=8)
+    stats = {}
+    mesh = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets),
+                            sof.ExtractOptions(strategies=sof.EvalStrategies.from_mask(mask)), stats)
+    assert len(want["triangles"]) > 0
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(mesh.triangles, want["triangles"])
+    assert stats["pairs"] == int(want["counters"][0])
+    assert stats["point_view_evals"] == int(want["counters"][1])
+    p1, p2 = str(tmp_path / "gpu.ply"), str(tmp_path / "ref.ply")
+    sof.write_mesh_ply(mesh, p1)
+    ref.write_mesh_ply(want["vertices"], want["triangles"], p2)
+    assert open(p1, "rb").read() == open(p2, "rb").read()
+
+
+def test_extract_delaunay_grid(ref):
+    """The reference's own seeds + Delaunay tetra input (seed_points.hpp, delaunay.hpp)."""
+    scene = ref.random_scene(55, 15, 1.0)
+    cams = ref.orbit_cameras(3, 4.0, 1.8, 64)
+    rc = ref.context(scene, cams)
+    grid = rc.seed_delaunay()
+    full = rc.extract_full(ALL)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    mesh = sof.extract_mesh(scene, views, sof.TetGrid(grid["vertices"], grid["tets"]))
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(full["vertices"]))
+    np.testing.assert_array_equal(mesh.triangles, full["triangles"])
