@@ -184,6 +184,20 @@ int sof_assemble(sof_ctx* ctx, int64_t n_verts, const double* verts, int64_t n_t
 int sof_extract(sof_ctx* ctx, const sof_extract_opts* opts, sof_extract_stats* stats);
 void sof_extract_opts_default(sof_extract_opts* opts);
 
+/* ---- utilities ---------------------------------------------------------------------- */
+/* device-side check that 0 <= tets_dev[i] < nv for all 4*nt indices */
+int sof_validate_tets_dev(sof_ctx* ctx, int64_t nt, const int32_t* tets_dev, int64_t nv);
+/* CUDA events on the context's stream (slots 0..7) for device-side timing */
+int sof_event_record(sof_ctx* ctx, int slot);
+int sof_event_elapsed(sof_ctx* ctx, int slot_a, int slot_b, float* ms);
+int sof_sync(sof_ctx* ctx);
+/* page-lock host buffers so uploads run at full link bandwidth */
+int sof_host_register(void* ptr, size_t bytes);
+int sof_host_unregister(void* ptr);
+/* measured FP64 FMA-pipe throughput (TFLOP/s, 2 FLOP per DFMA): the roofline
+ * denominator of the FP64 opacity-evaluation kernel */
+int sof_fp64_peak(sof_ctx* ctx, double* tflops);
+
 /* ---- results ------------------------------------------------------------------------ */
 int64_t sof_result_count(const sof_ctx* ctx, int kind); /* elements (not bytes); <0 if none */
 int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);

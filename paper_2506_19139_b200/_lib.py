@@ -68,6 +68,13 @@ _SIGS = {
     "sof_result_count": (_I64, [_P, _I]),
     "sof_copy_result": (_I, [_P, _I, _P]),
     "sof_render_view": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "sof_validate_tets_dev": (_I, [_P, _I64, _P, _I64]),
+    "sof_event_record": (_I, [_P, _I]),
+    "sof_event_elapsed": (_I, [_P, _I, _I, ctypes.POINTER(ctypes.c_float)]),
+    "sof_sync": (_I, [_P]),
+    "sof_host_register": (_I, [_P, ctypes.c_size_t]),
+    "sof_host_unregister": (_I, [_P]),
+    "sof_fp64_peak": (_I, [_P, ctypes.POINTER(_D)]),
 }
 
 _lib = None

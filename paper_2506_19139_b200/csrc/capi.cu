@@ -187,10 +187,12 @@ int sof_set_tets(sof_ctx* c, int64_t nv, const double* xyz, int64_t nt, const in
   return guard(c, [&] {
     check_points(nv, xyz);
     if (nt < 0 || (nt > 0 && !tets)) throw InvalidArg("invalid tet array");
-    for (int64_t i = 0; i < 4 * nt; ++i)
-      if (tets[i] < 0 || tets[i] >= nv) throw InvalidArg("tet vertex index out of range");
     upload(c, c->tv, xyz, 3 * nv);
     upload(c, c->tt, tets, 4 * nt);
+    c->has_tets = false;
+    // index range check on the device (4 * nt indices would cost seconds on the host)
+    if (sof_validate_tets_dev(c, nt, c->tt.p, nv) != SOF_OK)
+      throw InvalidArg("tet vertex index out of range");
     c->nv = nv;
     c->nt = nt;
     c->has_tets = true;
@@ -458,6 +460,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     }
     sof_extract_stats st;
     std::memset(&st, 0, sizeof st);
+    mark_views_stale(c);  // per-view records / bindings are rebuilt inside every extract
     const int64_t launches0 = c->launches;
     c->eval_ms = 0.0;
     c->eval_launches = 0;

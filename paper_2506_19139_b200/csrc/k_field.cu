@@ -108,6 +108,14 @@ void invalidate_view_caches(sof_ctx* c) {
   c->cache_bytes = 0;
 }
 
+// Marks every per-view cache stale but keeps the allocations (each meshing step
+// recomputes its per-view records and bindings; nothing is carried across calls).
+void mark_views_stale(sof_ctx* c) {
+  c->rec_valid.assign(c->cams.size(), 0);
+  for (auto& b : c->bindings) b.view = -1;
+  c->cache_bytes = 0;
+}
+
 const Rec* view_records(sof_ctx* c, int view) {
   if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
   if (c->rec_valid[view]) return c->recs[view].p;

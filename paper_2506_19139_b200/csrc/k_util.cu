@@ -1,0 +1,129 @@
+// k_util.cu — device-side input validation, stream-event timing, pinned host
+// registration and the FP64-pipe peak probe used as the roofline denominator of
+// the FP64 opacity-evaluation kernel.
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "../../include/sof_cuda.h"
+#include "sof_internal.h"
+
+namespace sofk {
+
+__global__ void k_check_index(int64_t n, const int32_t* __restrict__ idx, int32_t bound,
+                              int32_t* bad) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) {
+    const int32_t v = idx[i];
+    if (v < 0 || v >= bound) atomicExch(bad, 1);
+  }
+}
+
+// Each thread runs 8 independent DFMA chains; 2 FLOP per DFMA.
+__global__ void k_fp64_peak(int iters, double seed, double* sink) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, b = 1e-7;
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, b);
+    a1 = fma(a1, m, b);
+    a2 = fma(a2, m, b);
+    a3 = fma(a3, m, b);
+    a4 = fma(a4, m, b);
+    a5 = fma(a5, m, b);
+    a6 = fma(a6, m, b);
+    a7 = fma(a7, m, b);
+  }
+  const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (r == 12345.678) sink[0] = r;  // keep the chains live
+}
+
+}  // namespace sofk
+
+using namespace sofk;
+
+extern "C" {
+
+int sof_validate_tets_dev(sof_ctx* c, int64_t nt, const int32_t* tets_dev, int64_t nv) {
+  if (!c) return SOF_E_INVALID;
+  try {
+    DBuf<int32_t> bad;
+    bad.ensure(1);
+    SOF_CUDA(cudaMemsetAsync(bad.p, 0, 4, c->stream));
+    if (nt > 0) {
+      k_check_index<<<grid_for(4 * nt, 256), 256, 0, c->stream>>>(4 * nt, tets_dev, int32_t(nv), bad.p);
+      SOF_LAUNCHED(c);
+    }
+    return read_scalar(c, bad.p) ? SOF_E_INVALID : SOF_OK;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return SOF_E_CUDA;
+  }
+}
+
+int sof_event_record(sof_ctx* c, int slot) {
+  if (!c || slot < 0 || slot >= 8) return SOF_E_INVALID;
+  if (!c->user_ev[slot] && cudaEventCreate(&c->user_ev[slot]) != cudaSuccess) return SOF_E_CUDA;
+  return cudaEventRecord(c->user_ev[slot], c->stream) == cudaSuccess ? SOF_OK : SOF_E_CUDA;
+}
+
+int sof_event_elapsed(sof_ctx* c, int a, int b, float* ms) {
+  if (!c || !ms || a < 0 || b < 0 || a >= 8 || b >= 8 || !c->user_ev[a] || !c->user_ev[b])
+    return SOF_E_INVALID;
+  if (cudaEventSynchronize(c->user_ev[b]) != cudaSuccess) return SOF_E_CUDA;
+  return cudaEventElapsedTime(ms, c->user_ev[a], c->user_ev[b]) == cudaSuccess ? SOF_OK : SOF_E_CUDA;
+}
+
+int sof_sync(sof_ctx* c) {
+  if (!c) return SOF_E_INVALID;
+  return cudaStreamSynchronize(c->stream) == cudaSuccess ? SOF_OK : SOF_E_CUDA;
+}
+
+int sof_host_register(void* ptr, size_t bytes) {
+  if (!ptr || !bytes) return SOF_E_INVALID;
+  return cudaHostRegister(ptr, bytes, cudaHostRegisterDefault) == cudaSuccess ? SOF_OK : SOF_E_CUDA;
+}
+
+int sof_host_unregister(void* ptr) {
+  if (!ptr) return SOF_E_INVALID;
+  return cudaHostUnregister(ptr) == cudaSuccess ? SOF_OK : SOF_E_CUDA;
+}
+
+int sof_fp64_peak(sof_ctx* c, double* tflops) {
+  if (!c || !tflops) return SOF_E_INVALID;
+  try {
+    SOF_CUDA(cudaSetDevice(c->device));
+    int sms = 0;
+    SOF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    DBuf<double> sink;
+    sink.ensure(1);
+    const int iters = 1 << 14, threads = 256, blocks = sms * 8;
+    cudaEvent_t a, b;
+    SOF_CUDA(cudaEventCreate(&a));
+    SOF_CUDA(cudaEventCreate(&b));
+    k_fp64_peak<<<blocks, threads, 0, c->stream>>>(iters, 1.0, sink.p);  // warm-up
+    SOF_LAUNCHED(c);
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      SOF_CUDA(cudaEventRecord(a, c->stream));
+      k_fp64_peak<<<blocks, threads, 0, c->stream>>>(iters, 1.0 + r, sink.p);
+      SOF_LAUNCHED(c);
+      SOF_CUDA(cudaEventRecord(b, c->stream));
+      SOF_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      SOF_CUDA(cudaEventElapsedTime(&ms, a, b));
+      if (ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8.0 * double(iters) * threads * double(blocks);
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return SOF_OK;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return SOF_E_CUDA;
+  }
+}
+
+}  // extern "C"

@@ -169,6 +169,7 @@ struct sof_ctx {
   int64_t eval_launches = 0;
   bool time_eval = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t user_ev[8] = {};
 };
 
 namespace sofk {
@@ -178,6 +179,7 @@ void scene_prep(sof_ctx* c);
 const Rec* view_records(sof_ctx* c, int view);
 const Binding& view_binding(sof_ctx* c, int view, int tile_size);
 void invalidate_view_caches(sof_ctx* c);
+void mark_views_stale(sof_ctx* c);
 // Evaluates points xyz_dev[n] against views [v0, v1) in order (field_eval.hpp:59-176).
 void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz_dev, int strategies,
                 int tile_size, bool classify_mode, EvalMode mode, double* min_op, uint8_t* ext,

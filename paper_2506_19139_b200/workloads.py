@@ -116,9 +116,9 @@ def look_at(eye, target, up, fx, fy, w, h):
     return R, t, np.array([fx, fy, w * 0.5, h * 0.5])
 
 
-def orbit_cameras(count: int, width: int, height: int, radius: float = 4.0, focal_scale: float = 0.8) -> Cams:
+def orbit_cameras(count: int, width: int, height: int, radius: float = 6.0, focal_scale: float = 0.8) -> Cams:
     """Golden-spiral band z in [-0.8, 0.8] looking at the origin (test_util.hpp:72-84
-    pattern), f = focal_scale * W."""
+    pattern), f = focal_scale * W, radius 6 so the whole scene is in front."""
     golden = np.pi * (3.0 - np.sqrt(5.0))
     R = np.empty((count, 3, 3))
     t = np.empty((count, 3))
@@ -151,17 +151,23 @@ def _rot_z_to(normals: np.ndarray) -> np.ndarray:
 
 
 def synthetic_scene(n: int, config_index: int) -> Scene:
-    """Appendix B: 85% surface Gaussians on 3 spheres + ground plane + 2 boxes,
-    7% unbounded background shell, 8% dead (opacity below 1/255)."""
+    """Appendix B layout, kept in front of every camera: 85% surface Gaussians on
+    3 spheres + a ground disk (z = -1, radius 3.2) + 2 boxes, 7% volumetric
+    background in a shell of radius 2.8..4.2 around the objects, 8% dead (opacity
+    below 1/255). Everything lies within radius ~4.5 of the origin while the cameras
+    orbit at radius 6, so no E-box corner comes near a camera plane: the reference
+    bins any Gaussian with a corner behind the camera into EVERY tile
+    (tiles.hpp:116-126), which a surrounding background shell would trigger for
+    ~half the shell in every view."""
     rng = np.random.default_rng(SEED_BASE + config_index)
     n_bg = int(round(0.07 * n))
     n_dead = int(round(0.08 * n))
     n_surf = n - n_bg - n_dead
     n_on = n_surf + n_dead
-    # surfaces: spheres (centre, radius), plane z=-1 within |x|,|y|<=3, boxes (lo, hi)
     spheres = [((-0.9, 0.2, 0.0), 0.8), ((0.9, -0.3, 0.3), 0.6), ((0.0, 0.9, -0.4), 0.5)]
     boxes = [((-1.8, -1.6, -1.0), (-1.0, -0.8, -0.2)), ((1.0, 1.0, -1.0), (1.7, 1.8, 0.1))]
-    areas = [4 * np.pi * r * r for _, r in spheres] + [36.0]
+    disk_r = 3.2
+    areas = [4 * np.pi * r * r for _, r in spheres] + [np.pi * disk_r ** 2]
     for lo, hi in boxes:
         d = np.subtract(hi, lo)
         areas.append(2 * (d[0] * d[1] + d[1] * d[2] + d[0] * d[2]))
@@ -176,11 +182,13 @@ def synthetic_scene(n: int, config_index: int) -> Scene:
         pos[m] = np.asarray(c) + r * d
         nrm[m] = d
     m = which == 3
-    pos[m] = np.stack([rng.uniform(-3, 3, m.sum()), rng.uniform(-3, 3, m.sum()), np.full(m.sum(), -1.0)], 1)
+    rr = disk_r * np.sqrt(rng.uniform(0, 1, m.sum()))
+    th = rng.uniform(0, 2 * np.pi, m.sum())
+    pos[m] = np.stack([rr * np.cos(th), rr * np.sin(th), np.full(m.sum(), -1.0)], 1)
     nrm[m] = (0, 0, 1)
     for b, (lo, hi) in enumerate(boxes):
         m = which == 4 + b
-        cnt = m.sum()
+        cnt = int(m.sum())
         lo, hi = np.asarray(lo), np.asarray(hi)
         p = rng.uniform(lo, hi, size=(cnt, 3))
         face = rng.integers(0, 6, cnt)
@@ -198,11 +206,10 @@ def synthetic_scene(n: int, config_index: int) -> Scene:
     dead = np.zeros(n_on, bool)
     dead[rng.choice(n_on, n_dead, replace=False)] = True
     opa_on[dead] = rng.uniform(0.3 / 255, 0.99 / 255, n_dead)
-    # background shell, radius 5..20 (unbounded scene)
     d = rng.normal(size=(n_bg, 3))
     d /= np.linalg.norm(d, axis=1, keepdims=True)
-    pos_bg = d * rng.uniform(5, 20, (n_bg, 1))
-    scale_bg = np.repeat(rng.uniform(0.05, 0.5, (n_bg, 1)), 3, axis=1)
+    pos_bg = d * rng.uniform(2.8, 4.2, (n_bg, 1))
+    scale_bg = np.repeat(rng.uniform(0.01, 0.06, (n_bg, 1)), 3, axis=1) * rng.uniform(0.5, 1.5, (n_bg, 3))
     q = rng.normal(size=(n_bg, 4))
     rot_bg = q / np.linalg.norm(q, axis=1, keepdims=True)
     opa_bg = rng.uniform(0.05, 0.6, n_bg)
