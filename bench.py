@@ -304,7 +304,9 @@ def main():
                            "l2": "inputs (0.65 GB vertices + 2.6 GB tets + per-view caches) exceed the 126 MB L2"},
                 "meshing_wall_s": ms_step / 1e3, "queries_per_step": queries,
                 "stages_ms": {k: float(np.mean([s[k] for s in stats])) for k in
-                              ("ms_label", "ms_march", "ms_refine", "ms_weld")},
+                              ("ms_label", "ms_march", "ms_refine", "ms_weld", "ms_prep", "ms_sched",
+                               "ms_eval_kernel")},
+                "point_view_evals_per_step": int(np.mean([s["point_view_evals"] for s in stats])),
                 "label_queries_per_s": len(verts) / (np.mean([s["ms_label"] for s in stats]) * 1e-3),
                 "crossing_edges": E, "mesh_vertices": int(last["mesh_vertices"]),
                 "mesh_triangles": int(last["mesh_triangles"]), "pairs_per_step": int(pairs),

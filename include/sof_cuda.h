@@ -100,6 +100,8 @@ typedef struct sof_extract_stats {
   double ms_eval_kernel;     /* summed duration of the opacity-eval kernel launches */
   int64_t eval_launches;     /* number of opacity-eval kernel launches */
   int64_t kernel_launches;   /* all kernels launched by the call */
+  double ms_prep;            /* per-view records + Gaussian tile binning (K1, K2) */
+  double ms_sched;           /* per-view point scheduling (K3) */
 } sof_extract_stats;
 
 /* ---- context --------------------------------------------------------------- */

@@ -462,9 +462,12 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     std::memset(&st, 0, sizeof st);
     mark_views_stale(c);  // per-view records / bindings are rebuilt inside every extract
     const int64_t launches0 = c->launches;
-    c->eval_ms = 0.0;
     c->eval_launches = 0;
     c->time_eval = stats != nullptr;
+    if (c->time_eval) {
+      double drop[kProfKinds];
+      prof_collect(c, drop);  // reset the event pool
+    }
     cudaEvent_t e[5];
     for (auto& x : e) SOF_CUDA(cudaEventCreate(&x));
     const int64_t nv = c->nv;
@@ -508,7 +511,11 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     st.ms_march = ms[1];
     st.ms_refine = ms[2];
     st.ms_weld = ms[3];
-    st.ms_eval_kernel = c->eval_ms;
+    double pms[kProfKinds];
+    prof_collect(c, pms);
+    st.ms_eval_kernel = pms[kProfEval];
+    st.ms_prep = pms[kProfPrep];
+    st.ms_sched = pms[kProfSched];
     st.eval_launches = c->eval_launches;
     st.kernel_launches = c->launches - launches0;
     if (stats) *stats = st;

@@ -93,27 +93,25 @@ void scene_prep(sof_ctx* c) {
   SOF_LAUNCHED(c);
 }
 
-void invalidate_view_caches(sof_ctx* c) {
-  for (auto& r : c->recs) r.release();
-  for (auto& b : c->bindings) {
-    b.off.release();
-    b.ent.release();
-    b.view = -1;
-  }
-  c->recs.clear();
-  c->bindings.clear();
-  c->recs.resize(c->cams.size());
-  c->bindings.resize(c->cams.size());
-  c->rec_valid.assign(c->cams.size(), 0);
-  c->cache_bytes = 0;
-}
-
 // Marks every per-view cache stale but keeps the allocations (each meshing step
 // recomputes its per-view records and bindings; nothing is carried across calls).
 void mark_views_stale(sof_ctx* c) {
   c->rec_valid.assign(c->cams.size(), 0);
   for (auto& b : c->bindings) b.view = -1;
+  c->bind_scratch.view = -1;
   c->cache_bytes = 0;
+}
+
+// New scene or cameras: drop the cached per-view state. Buffers are kept (grow-only)
+// unless the number of views changes, so repeated uploads do not re-allocate HBM.
+void invalidate_view_caches(sof_ctx* c) {
+  if (c->recs.size() != c->cams.size()) {
+    c->recs.clear();
+    c->bindings.clear();
+    c->recs.resize(c->cams.size());
+    c->bindings.resize(c->cams.size());
+  }
+  mark_views_stale(c);
 }
 
 const Rec* view_records(sof_ctx* c, int view) {
@@ -196,21 +194,17 @@ __global__ void k_segment_starts(int64_t m, const K* __restrict__ keys, int64_t 
   for (int64_t t = prev + 1; t <= k; ++t) starts[t] = j;
 }
 
+static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t M, int64_t T,
+                               int tiles_x, int tiles_y);
+
 static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
   const Cam& cam = c->cams[view];
   const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
   const int64_t T = int64_t(tiles_x) * tiles_y;
   const Rec* rec = view_records(c, view);
   const int64_t n = c->n;
-  b.view = view;
-  b.tile_size = ts;
-  b.tiles_x = tiles_x;
-  b.tiles_y = tiles_y;
-  b.off.ensure(T + 1);
   if (n == 0) {
-    SOF_CUDA(cudaMemsetAsync(b.off.p, 0, sizeof(int64_t) * (T + 1), c->stream));
-    b.entries = 0;
-    b.ent.ensure(1);
+    build_binding_tail(c, view, ts, b, 0, T, tiles_x, tiles_y);
     return;
   }
   c->rect.ensure(n);
@@ -232,6 +226,26 @@ static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
   SOF_LAUNCHED(c);
   exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, n + 1);
   const int64_t M = read_scalar(c, c->goff.p + n);
+  if (&b != &c->bind_scratch) {
+    // keep the list resident for the rest of the step if the cache budget allows
+    const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
+    if (c->cache_bytes + bytes > c->cache_budget) {
+      build_binding_tail(c, view, ts, c->bind_scratch, M, T, tiles_x, tiles_y);
+      return;
+    }
+    c->cache_bytes += bytes;
+  }
+  build_binding_tail(c, view, ts, b, M, T, tiles_x, tiles_y);
+}
+
+static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t M, int64_t T,
+                               int tiles_x, int tiles_y) {
+  const int64_t n = c->n;
+  b.view = view;
+  b.tile_size = ts;
+  b.tiles_x = tiles_x;
+  b.tiles_y = tiles_y;
+  b.off.ensure(T + 1);
   b.entries = M;
   b.ent.ensure(std::max<int64_t>(M, 1));
   if (M > 0) {
@@ -252,82 +266,75 @@ static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
 const Binding& view_binding(sof_ctx* c, int view, int tile_size) {
   Binding& cached = c->bindings[view];
   if (cached.view == view && cached.tile_size == tile_size) return cached;
-  // build into the scratch slot, then keep it if the cache budget allows
-  Binding& s = c->bind_scratch;
-  build_binding(c, view, tile_size, s);
-  const size_t bytes = size_t(s.entries) * 4 + size_t(s.tiles_x) * s.tiles_y * 8 + 8;
-  if (c->cache_bytes + bytes <= c->cache_budget) {
-    if (cached.view >= 0) c->cache_bytes -= cached.ent.bytes() + cached.off.bytes();
-    cached.off.swap(s.off);
-    cached.ent.swap(s.ent);
-    cached.view = s.view;
-    cached.tile_size = s.tile_size;
-    cached.tiles_x = s.tiles_x;
-    cached.tiles_y = s.tiles_y;
-    cached.entries = s.entries;
-    s.view = -1;
-    c->cache_bytes += cached.ent.bytes() + cached.off.bytes();
-    return cached;
-  }
-  return s;
+  if (c->bind_scratch.view == view && c->bind_scratch.tile_size == tile_size) return c->bind_scratch;
+  // builds into the per-view slot (kept for the rest of the step) or, past the
+  // cache budget, into the scratch slot
+  build_binding(c, view, tile_size, cached);
+  return (cached.view == view) ? cached : c->bind_scratch;
 }
 
 // ---- K3: point scheduling ------------------------------------------------------------------------
+//
+// Points are grouped by tile with a counting sort (histogram, scan over the T
+// tiles, scatter), then cut into blocks of <= 256 points of one tile
+// (tiles.hpp:61-82). Everything stays on the device: no host synchronisation per
+// view. Order inside a tile is arbitrary; it cannot change any result because
+// every (point, view) evaluation is independent (field_eval.hpp:146-154).
 
-// Active (not pruned) and observed points -> (tile, f32 view depth) keys, compacted.
-__global__ void k_sched_compact(int64_t n, const double* __restrict__ xyz, Cam cam, int ts,
-                                int tiles_x, const uint8_t* __restrict__ skip, uint64_t* keys,
-                                int32_t* idx, int32_t* count) {
+// Warp-aggregated atomicAdd on a per-tile counter: lanes with the same tile elect
+// one leader. Returns the slot of this lane among the lanes that hit `tile`.
+__device__ __forceinline__ int warp_tile_add(int* counters, int tile, bool valid) {
+  const unsigned active = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return 0;
+  const unsigned peers = __match_any_sync(active, tile);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counters + tile, __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  return base + __popc(peers & ((1u << lane) - 1u));
+}
+
+// Per point: tile of the view (-1 when pruned or unobserved), histogram per tile.
+__global__ void k_sched_tile(int64_t n, const double* __restrict__ xyz, Cam cam, int ts,
+                             int tiles_x, bool single_bin, const uint8_t* __restrict__ skip,
+                             int32_t* tile_of, int* tile_cnt) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  bool keep = false;
-  uint64_t key = 0;
+  int tile = -1;
   if (i < n && !(skip && skip[i])) {
     const PointRay pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
-    keep = pr.observed;
-    if (keep) key = (uint64_t(uint32_t(pr.tile)) << 32) | __float_as_uint(float(pr.zp));
+    if (pr.observed) tile = single_bin ? 0 : pr.tile;
   }
-  const unsigned mask = __ballot_sync(0xffffffffu, keep);
-  if (mask == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(mask) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(count, __popc(mask));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (keep) {
-    const int pos = base + __popc(mask & ((1u << lane) - 1u));
-    keys[pos] = key;
-    idx[pos] = int32_t(i);
-  }
+  if (i < n) tile_of[i] = tile;
+  warp_tile_add(tile_cnt, tile, tile >= 0);
 }
 
-__global__ void k_block_flags(int64_t m, const uint64_t* __restrict__ keys,
-                              const int64_t* __restrict__ tile_start, int32_t* flag) {
-  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (j >= m) return;
-  const int64_t t = int64_t(keys[j] >> 32);
-  flag[j] = ((j - tile_start[t]) % kBlockPoints) == 0;
+__global__ void k_sched_scatter(int64_t n, const int32_t* __restrict__ tile_of,
+                                const int* __restrict__ tile_off, int* tile_cur, int32_t* order) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int tile = (i < n) ? tile_of[i] : -1;
+  const int slot = warp_tile_add(tile_cur, tile, tile >= 0);
+  if (tile >= 0) order[tile_off[tile] + slot] = int32_t(i);
 }
 
-__global__ void k_block_fill(int64_t m, const uint64_t* __restrict__ keys,
-                             const int64_t* __restrict__ tile_start,
-                             const int32_t* __restrict__ flag, const int32_t* __restrict__ bid,
+// One thread per tile: blocks per tile; an exclusive scan of these gives block ids.
+__global__ void k_block_counts(int T, const int* __restrict__ tile_off, int* blk_cnt) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > T) return;
+  blk_cnt[t] = (t == T) ? 0 : (tile_off[t + 1] - tile_off[t] + kBlockPoints - 1) / kBlockPoints;
+}
+
+__global__ void k_block_fill(int T, const int* __restrict__ tile_off, const int* __restrict__ blk_off,
                              int4* blocks, int64_t* nblocks) {
-  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (j >= m) return;
-  if (j == m - 1) *nblocks = bid[j] + flag[j];
-  if (!flag[j]) return;
-  const int64_t t = int64_t(keys[j] >> 32);
-  const int64_t end = std::min<int64_t>(j + kBlockPoints, tile_start[t + 1]);
-  blocks[bid[j]] = make_int4(int(j), int(end), int(t), 0);
-}
-
-__global__ void k_block_linear(int64_t m, int4* blocks, int64_t* nblocks) {
-  const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int64_t nb = (m + kBlockPoints - 1) / kBlockPoints;
-  if (b == 0) *nblocks = nb;
-  if (b >= nb) return;
-  blocks[b] = make_int4(int(b * kBlockPoints), int(std::min<int64_t>(m, (b + 1) * kBlockPoints)),
-                        -1, 0);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0) *nblocks = blk_off[T];
+  if (t >= T) return;
+  const int b0 = blk_off[t], b1 = blk_off[t + 1];
+  const int p0 = tile_off[t], p1 = tile_off[t + 1];
+  for (int b = b0; b < b1; ++b) {
+    const int s = p0 + (b - b0) * kBlockPoints;
+    blocks[b] = make_int4(s, min(s + kBlockPoints, p1), t, 0);
+  }
 }
 
 // ---- K4: opacity evaluation ----------------------------------------------------------------------
@@ -416,9 +423,15 @@ __global__ void __launch_bounds__(256) k_eval(
     }
   }
   // pairs counter: warp reduce, one atomic per warp
-  unsigned long long p = pairs;
-  for (int s = 16; s > 0; s >>= 1) p += __shfl_down_sync(0xffffffffu, p, s);
-  if ((threadIdx.x & 31) == 0 && p) atomicAdd(pairs_counter, p);
+  unsigned long long p = pairs, q = active;  // pairs, point_view_evals
+  for (int s = 16; s > 0; s >>= 1) {
+    p += __shfl_down_sync(0xffffffffu, p, s);
+    q += __shfl_down_sync(0xffffffffu, q, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (p) atomicAdd(pairs_counter, p);
+    if (q) atomicAdd(pairs_counter + 1, q);
+  }
 }
 
 __global__ void k_fill_view_outputs(int64_t n, double* o, uint8_t* obs, uint8_t* comp) {
@@ -437,7 +450,7 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
   if (grid <= 0) return;
   const int64_t* nb = c->d_scalar.p;
   unsigned long long* pc = c->d_counters.p;
-  if (c->time_eval) SOF_CUDA(cudaEventRecord(c->ev0, c->stream));
+  const int e0 = prof_mark(c);
   if (tiled)
     k_eval<MODE, true><<<unsigned(grid), 256, 0, c->stream>>>(
         c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
@@ -447,14 +460,8 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
         c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
         strategies, classify, min_op, ext, o_out, obs, comp, pc);
   SOF_LAUNCHED(c);
+  prof_span(c, e0, prof_mark(c), kProfEval);
   c->eval_launches++;
-  if (c->time_eval) {
-    SOF_CUDA(cudaEventRecord(c->ev1, c->stream));
-    SOF_CUDA(cudaEventSynchronize(c->ev1));
-    float ms = 0.f;
-    SOF_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    c->eval_ms += ms;
-  }
 }
 
 void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int strategies,
@@ -468,16 +475,10 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   c->d_counters.ensure(4);
   c->d_scalar.ensure(4);
   SOF_CUDA(cudaMemsetAsync(c->d_counters.p, 0, sizeof(unsigned long long) * 4, c->stream));
-  uint64_t pve = 0;
   PointSchedule& s = c->sched;
   if (n > 0) {
-    s.key_in.ensure(n);
-    s.key_out.ensure(n);
-    s.idx_in.ensure(n);
-    s.idx_out.ensure(n);
-    s.block_flag.ensure(n);
-    s.block_id.ensure(n);
-    s.counters.ensure(2);
+    s.tile_of.ensure(n);
+    s.order.ensure(n);
   }
   if (mode == kModeView && n > 0) {
     k_fill_view_outputs<<<grid_for(n, 256), 256, 0, c->stream>>>(n, o_out, obs_out, comp_out);
@@ -487,44 +488,37 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     const Cam& cam = c->cams[v];
     const int tiles_x = (cam.w + tile_size - 1) / tile_size;
     const int tiles_y = (cam.h + tile_size - 1) / tile_size;
-    const int64_t T = int64_t(tiles_x) * tiles_y;
+    const int T = tiled ? tiles_x * tiles_y : 1;
+    const int p0 = prof_mark(c);
     const Rec* rec = view_records(c, v);
     const Binding* bd = tiled ? &view_binding(c, v, tile_size) : nullptr;
-    // K3: compact the active, observed points of this view
+    const int p1 = prof_mark(c);
+    prof_span(c, p0, p1, kProfPrep);
+    // K3: group the active, observed points of this view by tile (no host sync)
     const uint8_t* skip = (prune && (mode == kModeLabel || mode == kModeClassify)) ? ext : nullptr;
-    SOF_CUDA(cudaMemsetAsync(s.counters.p, 0, sizeof(int32_t) * 2, c->stream));
-    k_sched_compact<<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, cam, tile_size, tiles_x, skip,
-                                                             s.key_in.p, s.idx_in.p, s.counters.p);
+    s.tile_cnt.ensure(2 * (T + 1));
+    s.tile_off.ensure(T + 1);
+    s.blk_cnt.ensure(T + 1);
+    s.blk_off.ensure(T + 1);
+    SOF_CUDA(cudaMemsetAsync(s.tile_cnt.p, 0, sizeof(int) * 2 * (T + 1), c->stream));
+    int* tile_cur = s.tile_cnt.p + (T + 1);
+    k_sched_tile<<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, cam, tile_size, tiles_x, !tiled,
+                                                          skip, s.tile_of.p, s.tile_cnt.p);
     SOF_LAUNCHED(c);
-    const int64_t nact = read_scalar(c, s.counters.p);
-    if (nact == 0) continue;
-    pve += uint64_t(nact);
-    const int32_t* pidx = s.idx_in.p;
-    int64_t grid;
-    if (tiled) {
-      sort_pairs_u64(c, s.key_in.p, s.key_out.p, s.idx_in.p, s.idx_out.p, nact,
-                     32 + bits_for(uint64_t(T)));
-      pidx = s.idx_out.p;
-      s.tile_start.ensure(T + 1);
-      k_segment_starts<uint64_t, 32><<<grid_for(nact + 1, 256), 256, 0, c->stream>>>(
-          nact, s.key_out.p, T, s.tile_start.p);
-      SOF_LAUNCHED(c);
-      k_block_flags<<<grid_for(nact, 256), 256, 0, c->stream>>>(nact, s.key_out.p,
-                                                                 s.tile_start.p, s.block_flag.p);
-      SOF_LAUNCHED(c);
-      exclusive_scan_i32(c, s.block_flag.p, s.block_id.p, nact);
-      grid = (nact + kBlockPoints - 1) / kBlockPoints + std::min<int64_t>(T, nact);
-      s.blocks.ensure(grid);
-      k_block_fill<<<grid_for(nact, 256), 256, 0, c->stream>>>(
-          nact, s.key_out.p, s.tile_start.p, s.block_flag.p, s.block_id.p, s.blocks.p,
-          c->d_scalar.p);
-      SOF_LAUNCHED(c);
-    } else {
-      grid = (nact + kBlockPoints - 1) / kBlockPoints;
-      s.blocks.ensure(grid);
-      k_block_linear<<<grid_for(grid, 256), 256, 0, c->stream>>>(nact, s.blocks.p, c->d_scalar.p);
-      SOF_LAUNCHED(c);
-    }
+    exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, T + 1);
+    k_sched_scatter<<<grid_for(n, 256), 256, 0, c->stream>>>(n, s.tile_of.p, s.tile_off.p, tile_cur,
+                                                             s.order.p);
+    SOF_LAUNCHED(c);
+    k_block_counts<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, s.tile_off.p, s.blk_cnt.p);
+    SOF_LAUNCHED(c);
+    exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, T + 1);
+    const int64_t grid = (n + kBlockPoints - 1) / kBlockPoints + T;
+    s.blocks.ensure(grid);
+    k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, s.tile_off.p, s.blk_off.p, s.blocks.p,
+                                                               c->d_scalar.p);
+    SOF_LAUNCHED(c);
+    prof_span(c, p1, prof_mark(c), kProfSched);
+    const int32_t* pidx = s.order.p;
     switch (mode) {
       case kModeLabel:
         launch_eval<kModeLabel>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
@@ -545,9 +539,11 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     }
   }
   if (counters_host) {
-    const unsigned long long pairs = read_scalar(c, c->d_counters.p);
-    counters_host[0] += pairs;
-    counters_host[1] += pve;
+    unsigned long long h[2];
+    SOF_CUDA(cudaMemcpyAsync(h, c->d_counters.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+    counters_host[0] += h[0];
+    counters_host[1] += h[1];
   }
 }
 

@@ -201,23 +201,10 @@ __global__ void k_tris(int64_t ntri, const int32_t* __restrict__ tri_occ,
   tris[3 * k + 2] = keep ? e2 : e1;
 }
 
-struct MeshScratch {
-  DBuf<uint8_t> crossing, first_u8;
-  DBuf<int32_t> ctets, nsel;
-  DBuf<unsigned long long> packed, off;
-  DBuf<uint64_t> okey, skey;
-  DBuf<int32_t> opos, spos, oin, oout, tri_occ, tri_tet, head, run_incl, is_first, eid, run_eid,
-      occ_edge;
-};
-static MeshScratch& scratch() {
-  static thread_local MeshScratch s;
-  return s;
-}
-
 void march(sof_ctx* c, const double* opa) {
   if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
   const int64_t nt = c->nt, nv = c->nv;
-  MeshScratch& s = scratch();
+  MeshScratch& s = c->ms;
   c->n_edges = c->n_march_tris = 0;
   c->r_edges.ensure(2);
   c->r_everts.ensure(3);
@@ -351,8 +338,11 @@ void refine(sof_ctx* c, int64_t ne, const int32_t* edges, double* verts, int ite
             int strategies, int tile_size, int v0, int v1, uint64_t* counters) {
   if (iterations <= 0 || ne == 0) return;  // iterations = 0 keeps the lerp vertices (:100)
   if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
-  DBuf<double> pin, pout, mid;
-  DBuf<uint8_t> ext;
+  MeshScratch& s = c->ms;
+  DBuf<double>& pin = s.pin;
+  DBuf<double>& pout = s.pout;
+  DBuf<double>& mid = s.mid;
+  DBuf<uint8_t>& ext = s.rext;
   pin.ensure(3 * ne);
   pout.ensure(3 * ne);
   mid.ensure(3 * ne);
@@ -471,8 +461,10 @@ void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t*
   c->m_tris.ensure(3);
   if (n == 0) return;
   const double inv = 1.0 / weld_eps;
-  DBuf<uint64_t> kx, ky, kz, k1, k2;
-  DBuf<int32_t> p0, p1, head, run, run_first, first_of, is_first, nid;
+  MeshScratch& s = c->ms;
+  DBuf<uint64_t>&kx = s.kx, &ky = s.ky, &kz = s.kz, &k1 = s.k1, &k2 = s.k2;
+  DBuf<int32_t>&p0 = s.p0, &p1 = s.p1, &head = s.whead, &run = s.wrun, &run_first = s.wrun_first,
+                 &first_of = s.first_of, &is_first = s.wfirst, &nid = s.nid;
   kx.ensure(n); ky.ensure(n); kz.ensure(n); k1.ensure(n); k2.ensure(n);
   p0.ensure(n); p1.ensure(n); head.ensure(n); run.ensure(n); run_first.ensure(n);
   first_of.ensure(n); is_first.ensure(n); nid.ensure(n);
@@ -501,7 +493,7 @@ void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t*
   SOF_LAUNCHED(c);
   c->mesh_nv = nout;
   if (nt == 0) return;
-  DBuf<int32_t> rt, keep, pos;
+  DBuf<int32_t>&rt = s.rt, &keep = s.keep, &pos = s.pos;
   rt.ensure(3 * nt);
   keep.ensure(nt);
   pos.ensure(nt);

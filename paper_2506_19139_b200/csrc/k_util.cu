@@ -39,6 +39,38 @@ __global__ void k_fp64_peak(int iters, double seed, double* sink) {
   if (r == 12345.678) sink[0] = r;  // keep the chains live
 }
 
+int prof_mark(sof_ctx* c) {
+  if (!c->time_eval) return -1;
+  if (c->evnext == c->evpool.size()) {
+    cudaEvent_t e;
+    SOF_CUDA(cudaEventCreate(&e));
+    c->evpool.push_back(e);
+  }
+  SOF_CUDA(cudaEventRecord(c->evpool[c->evnext], c->stream));
+  return int(c->evnext++);
+}
+
+void prof_span(sof_ctx* c, int a, int b, int kind) {
+  if (a < 0 || b < 0) return;
+  c->span_a.push_back(a);
+  c->span_b.push_back(b);
+  c->span_k.push_back(kind);
+}
+
+void prof_collect(sof_ctx* c, double* ms) {
+  for (int k = 0; k < kProfKinds; ++k) ms[k] = 0.0;
+  if (c->evnext) SOF_CUDA(cudaEventSynchronize(c->evpool[c->evnext - 1]));
+  for (size_t i = 0; i < c->span_a.size(); ++i) {
+    float x = 0.f;
+    SOF_CUDA(cudaEventElapsedTime(&x, c->evpool[c->span_a[i]], c->evpool[c->span_b[i]]));
+    ms[c->span_k[i]] += x;
+  }
+  c->span_a.clear();
+  c->span_b.clear();
+  c->span_k.clear();
+  c->evnext = 0;
+}
+
 }  // namespace sofk
 
 using namespace sofk;
@@ -48,7 +80,7 @@ extern "C" {
 int sof_validate_tets_dev(sof_ctx* c, int64_t nt, const int32_t* tets_dev, int64_t nv) {
   if (!c) return SOF_E_INVALID;
   try {
-    DBuf<int32_t> bad;
+    DBuf<int32_t>& bad = c->ms.nsel;
     bad.ensure(1);
     SOF_CUDA(cudaMemsetAsync(bad.p, 0, 4, c->stream));
     if (nt > 0) {

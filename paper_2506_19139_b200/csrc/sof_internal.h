@@ -90,13 +90,28 @@ struct Binding {
 
 // Scratch of the per-view point schedule (schedule_points tiles.hpp:29-84).
 struct PointSchedule {
-  DBuf<uint64_t> key_in, key_out;
-  DBuf<int32_t> idx_in, idx_out;
-  DBuf<int64_t> tile_start;  // [T + 1]
-  DBuf<int32_t> block_flag, block_id;
+  DBuf<int32_t> tile_of;     // [n] tile of each point in this view, -1 if inactive
+  DBuf<int32_t> order;       // [n] point indices grouped by tile
+  DBuf<int> tile_cnt;        // [2(T + 1)] histogram | scatter cursors
+  DBuf<int> tile_off, blk_cnt, blk_off;  // [T + 1]
   DBuf<int4> blocks;         // {start, end, tile, 0}
-  DBuf<int32_t> counters;    // [0] active count, [1] block count
 };
+
+// Persistent (grow-only) scratch of the mesher stages: no allocation in steady state.
+struct MeshScratch {
+  DBuf<uint8_t> crossing, first_u8;
+  DBuf<int32_t> ctets, nsel;
+  DBuf<unsigned long long> packed, off;
+  DBuf<uint64_t> okey, skey;
+  DBuf<int32_t> opos, spos, oin, oout, tri_occ, tri_tet, head, run_incl, is_first, eid, run_eid,
+      occ_edge;
+  DBuf<double> pin, pout, mid;  // bisection brackets
+  DBuf<uint8_t> rext;
+  DBuf<uint64_t> kx, ky, kz, k1, k2;  // weld
+  DBuf<int32_t> p0, p1, whead, wrun, wrun_first, first_of, wfirst, nid, rt, keep, pos;
+};
+
+enum ProfKind { kProfEval = 0, kProfPrep = 1, kProfSched = 2, kProfKinds = 4 };
 
 enum EvalMode { kModeLabel = 0, kModeClassify = 1, kModeView = 2, kModeValue = 3 };
 
@@ -141,6 +156,7 @@ struct sof_ctx {
   sofk::DBuf<int32_t> eval_in;
 
   sofk::PointSchedule sched;
+  sofk::MeshScratch ms;
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
   sofk::DBuf<int64_t> d_scalar;               // small device scalars
@@ -170,6 +186,10 @@ struct sof_ctx {
   bool time_eval = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t user_ev[8] = {};
+  // event pool for sync-free phase timing (only while time_eval is set)
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  std::vector<int> span_a, span_b, span_k;
 };
 
 namespace sofk {
@@ -197,6 +217,11 @@ void refine(sof_ctx* c, int64_t ne, const int32_t* edges_dev, double* verts_dev,
             int strategies, int tile_size, int v0, int v1, uint64_t* counters);
 void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris,
               const int32_t* tris_dev, double weld_eps, double min_area);
+
+// ---- k_util.cu: phase timing -------------------------------------------------------------
+int prof_mark(sof_ctx* c);                              // -1 when not profiling
+void prof_span(sof_ctx* c, int a, int b, int kind);
+void prof_collect(sof_ctx* c, double* ms_by_kind);      // syncs, sums, resets
 
 // ---- helpers ----------------------------------------------------------------------------
 inline unsigned grid_for(int64_t n, int block) { return unsigned((n + block - 1) / block); }
