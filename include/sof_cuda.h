@@ -102,6 +102,7 @@ typedef struct sof_extract_stats {
   int64_t kernel_launches;   /* all kernels launched by the call */
   double ms_prep;            /* per-view records + Gaussian tile binning (K1, K2) */
   double ms_sched;           /* per-view point scheduling (K3) */
+  uint64_t exact_pairs;      /* pairs the FP32 filter could not certify (evaluated in FP64) */
 } sof_extract_stats;
 
 /* ---- context --------------------------------------------------------------- */
@@ -199,6 +200,10 @@ int sof_host_unregister(void* ptr);
 /* measured FP64 FMA-pipe throughput (TFLOP/s, 2 FLOP per DFMA): the roofline
  * denominator of the FP64 opacity-evaluation kernel */
 int sof_fp64_peak(sof_ctx* ctx, double* tflops);
+
+/* opacity-evaluation kernel: 0 = certified FP32 filter + exact FP64 replay,
+ * 1 = FP64 for every pair (default). Both produce bit-identical results and counters. */
+int sof_set_eval_path(sof_ctx* ctx, int path);
 
 /* ---- results ------------------------------------------------------------------------ */
 int64_t sof_result_count(const sof_ctx* ctx, int kind); /* elements (not bytes); <0 if none */

@@ -37,7 +37,7 @@ class ExtractStats(ctypes.Structure):
                 ("label_pairs", ctypes.c_uint64), ("refine_pairs", ctypes.c_uint64),
                 ("ms_label", _D), ("ms_march", _D), ("ms_refine", _D), ("ms_weld", _D),
                 ("ms_eval_kernel", _D), ("eval_launches", _I64), ("kernel_launches", _I64),
-                ("ms_prep", _D), ("ms_sched", _D)]
+                ("ms_prep", _D), ("ms_sched", _D), ("exact_pairs", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -76,6 +76,7 @@ _SIGS = {
     "sof_host_register": (_I, [_P, ctypes.c_size_t]),
     "sof_host_unregister": (_I, [_P]),
     "sof_fp64_peak": (_I, [_P, ctypes.POINTER(_D)]),
+    "sof_set_eval_path": (_I, [_P, _I]),
 }
 
 _lib = None

@@ -434,6 +434,15 @@ int sof_assemble(sof_ctx* c, int64_t nverts, const double* verts, int64_t ntris,
   });
 }
 
+int sof_set_eval_path(sof_ctx* c, int path) {
+  if (!c || path < 0 || path > 1) return SOF_E_INVALID;
+  if (c->eval_path != path) {
+    c->eval_path = path;
+    sofk::invalidate_view_caches(c);  // the record layout per view depends on the path
+  }
+  return SOF_OK;
+}
+
 void sof_extract_opts_default(sof_extract_opts* o) {
   if (!o) return;
   o->strategies = SOF_ALL_STRATEGIES;
@@ -463,6 +472,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     mark_views_stale(c);  // per-view records / bindings are rebuilt inside every extract
     const int64_t launches0 = c->launches;
     c->eval_launches = 0;
+    c->exact_evals = 0;
     c->time_eval = stats != nullptr;
     if (c->time_eval) {
       double drop[kProfKinds];
@@ -515,6 +525,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     prof_collect(c, pms);
     st.ms_eval_kernel = pms[kProfEval];
     st.ms_prep = pms[kProfPrep];
+    st.exact_pairs = c->exact_evals;
     st.ms_sched = pms[kProfSched];
     st.eval_launches = c->eval_launches;
     st.kernel_launches = c->launches - launches0;

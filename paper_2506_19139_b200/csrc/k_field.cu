@@ -77,12 +77,14 @@ __global__ void k_gauss_static(int64_t n, const double* __restrict__ pos,
   out[i] = g;
 }
 
-__global__ void k_view_rec(int64_t n, const GaussStatic* __restrict__ g, Cam cam, Rec* out) {
+__global__ void k_view_rec(int64_t n, const GaussStatic* __restrict__ g, Cam cam, Rec* out,
+                           RecF* outf) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   Rec r;
   gauss_view(g[i], cam, r);
   out[i] = r;
+  if (outf) outf[i] = make_recf(r);
 }
 
 void scene_prep(sof_ctx* c) {
@@ -107,8 +109,10 @@ void mark_views_stale(sof_ctx* c) {
 void invalidate_view_caches(sof_ctx* c) {
   if (c->recs.size() != c->cams.size()) {
     c->recs.clear();
+    c->recfs.clear();
     c->bindings.clear();
     c->recs.resize(c->cams.size());
+    c->recfs.resize(c->cams.size());
     c->bindings.resize(c->cams.size());
   }
   mark_views_stale(c);
@@ -117,20 +121,29 @@ void invalidate_view_caches(sof_ctx* c) {
 const Rec* view_records(sof_ctx* c, int view) {
   if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
   if (c->rec_valid[view]) return c->recs[view].p;
-  const size_t bytes = size_t(c->n) * sizeof(Rec);
+  const bool with_f = c->eval_path == 0;  // float filter records only for the FP32 path
+  const size_t bytes = size_t(c->n) * (sizeof(Rec) + (with_f ? sizeof(RecF) : 0));
   DBuf<Rec>* dst = &c->rec_scratch;
+  DBuf<RecF>* dstf = &c->recf_scratch;
   if (c->cache_bytes + bytes <= c->cache_budget) {
     dst = &c->recs[view];
+    dstf = &c->recfs[view];
     c->cache_bytes += bytes;
     c->rec_valid[view] = 1;
   }
   dst->ensure(std::max<int64_t>(c->n, 1));
+  if (with_f) dstf->ensure(std::max<int64_t>(c->n, 1));
   if (c->n > 0) {
     k_view_rec<<<grid_for(c->n, 128), 128, 0, c->stream>>>(c->n, c->gstat.p, c->cams[view],
-                                                            dst->p);
+                                                            dst->p, with_f ? dstf->p : nullptr);
     SOF_LAUNCHED(c);
   }
   return dst->p;
+}
+
+// Float filter records of `view`, valid after view_records(c, view).
+const RecF* view_recf(sof_ctx* c, int view) {
+  return c->rec_valid[view] ? c->recfs[view].p : c->recf_scratch.p;
 }
 
 // ---- K2: Gaussian tile binning ------------------------------------------------------------------
@@ -434,6 +447,159 @@ __global__ void __launch_bounds__(256) k_eval(
   }
 }
 
+// FP32-filtered evaluation: same semantics and bit-identical results as k_eval.
+// Per chunk of kChunkF records staged in shared memory (float copies), every
+// thread scans the chunk in FP32 and queues the pairs the certified filter
+// cannot skip (RecF, sof_device.cuh); the queue is then replayed in list order
+// with the exact FP64 pair arithmetic (pair_alpha) reading the FP64 record from
+// global memory. The survive product, early stop and min-z break are exact, and
+// the reference's pair counter is reproduced from per-pair ordinals.
+constexpr int kChunkF = 64;
+
+template <int MODE, bool TILED>
+__global__ void __launch_bounds__(256) k_eval_f32(
+    const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks,
+    const int32_t* __restrict__ pidx, const double* __restrict__ xyz, Cam cam, int ts,
+    int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
+    int64_t n_gauss, const Rec* __restrict__ recs, const RecF* __restrict__ recf, int strategies,
+    int classify, double* min_op, uint8_t* ext, double* o_out, uint8_t* obs_out,
+    uint8_t* comp_out, unsigned long long* counters) {
+  __shared__ __align__(16) RecF sf[kChunkF];
+  __shared__ int32_t sg[kChunkF];
+  __shared__ uint8_t qk[kChunkF][256];  // queued record (chunk index) per thread
+  __shared__ uint8_t qo[kChunkF][256];  // pair ordinal of the queued record in the chunk
+  const int64_t b = blockIdx.x;
+  if (b >= *nblocks) return;
+  const int4 blk = blocks[b];
+  const int tid = threadIdx.x;
+  const int j = blk.x + tid;
+  const bool active = j < blk.y;
+  int i = 0;
+  PointRay pr;
+  pr.observed = false;
+  pr.zp = 0.0;
+  pr.t = 1.0;
+  pr.d[0] = pr.d[1] = pr.d[2] = 0.0;
+  if (active) {
+    i = pidx[j];
+    pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+  }
+  // per-point float monomials of the ray direction (abc_cached precompute.hpp:39-45)
+  const float x = float(pr.d[0]), y = float(pr.d[1]), z = float(pr.d[2]);
+  const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
+  const float tf = float(pr.t);
+  const float zpf = __double2float_rn(pr.zp);
+  int64_t l0 = 0, l1 = n_gauss;
+  if (TILED) {
+    l0 = loff[blk.z];
+    l1 = loff[blk.z + 1];
+  }
+  const bool dead_cull = strategies & 16, use_min_z = strategies & 2;
+  const bool early = classify && (strategies & 4);
+  double survive = 1.0;
+  bool complete = true;
+  bool done = !active;
+  unsigned pairs = 0, exact_evals = 0;
+  for (int64_t base = l0; base < l1; base += kChunkF) {
+    if (!__syncthreads_or(!done)) break;
+    const int cnt = int(min(int64_t(kChunkF), l1 - base));
+    for (int k = tid; k < cnt * 4; k += blockDim.x) {
+      const int r = k >> 2, q = k & 3;
+      const int32_t g = TILED ? lent[base + r] : int32_t(base + r);
+      reinterpret_cast<float4*>(&sf[r])[q] = __ldg(reinterpret_cast<const float4*>(recf + g) + q);
+      if (q == 0) sg[r] = g;
+    }
+    __syncthreads();
+    if (!done) {
+      int qn = 0, np = 0;
+      bool brk = false;
+      for (int k = 0; k < cnt; ++k) {
+        const RecF& r = sf[k];
+        if (dead_cull && (r.flags & 1u)) continue;
+        if (use_min_z) {
+          // exact `min_z > z_point`: float compare, FP64 only on a float tie
+          const bool gt = (r.zmin > zpf) || (r.zmin == zpf && __ldg(&recs[sg[k]].zmin) > pr.zp);
+          if (gt) {
+            if (TILED) {  // list sorted by min_z (field_eval.hpp:91)
+              brk = true;
+              break;
+            }
+            continue;
+          }
+        }
+        ++np;
+        const float bb = fmaf(r.b2[0], x, fmaf(r.b2[1], y, r.b2[2] * z));
+        if (bb >= r.kb) continue;  // b_fp64 >= 0: te <= 0, skipped by the reference
+        const float a = fmaf(r.ic[0], xx, fmaf(r.ic[1], yy, fmaf(r.ic[2], zz,
+                        fmaf(r.ic[3], xy, fmaf(r.ic[4], xz, r.ic[5] * yz)))));
+        bool need = !(a > r.ka);
+        if (!need) {
+          const float ra = __frcp_rn(a);
+          const float tst = -0.5f * bb * ra;
+          const float te = fminf(tst, tf);
+          const float g = fmaf(fmaf(a, te, bb), te, r.c);
+          // |g_f - g_fp64| <= ka te^2 + kb |te| + kc + kb^2 / a (the last term bounds the
+          // second-order effect of the t* error, a (dt*)^2 <= db^2 / (4a))
+          const float s = fmaf(r.ka, te * te, fmaf(r.kb, fabsf(te) + r.kb * ra, r.kc));
+          need = !(g - s > r.gthr);  // otherwise alpha_fp64 < 1/255 for sure
+        }
+        if (need) {
+          qk[qn][tid] = uint8_t(k);
+          qo[qn][tid] = uint8_t(np);
+          ++qn;
+        }
+      }
+      // exact replay of the queued pairs, in list order
+      int stop = -1;
+      for (int q = 0; q < qn; ++q) {
+        const int k = qk[q][tid];
+        const Rec r = recs[sg[k]];
+        ++exact_evals;
+        const double alpha = pair_alpha(r, pr.d, pr.t);
+        if (alpha == 0.0) continue;
+        survive *= 1.0 - alpha;
+        if (early && 1.0 - survive > 0.5) {
+          complete = false;
+          stop = qo[q][tid];
+          break;
+        }
+      }
+      if (stop >= 0) {
+        pairs += unsigned(stop);
+        done = true;
+      } else {
+        pairs += unsigned(np);
+        if (brk) done = true;
+      }
+    }
+  }
+  if (active) {
+    const double o = 1.0 - survive;
+    if (MODE == kModeLabel || MODE == kModeValue) {
+      const double m = min_op[i];
+      min_op[i] = (o < m) ? o : m;
+      if (MODE == kModeLabel && complete && o < 0.5) ext[i] = 1;
+    } else if (MODE == kModeClassify) {
+      if (complete && o < 0.5) ext[i] = 1;
+    } else {
+      o_out[i] = o;
+      obs_out[i] = 1;
+      comp_out[i] = complete;
+    }
+  }
+  unsigned long long p = pairs, q = active, e = exact_evals;
+  for (int s = 16; s > 0; s >>= 1) {
+    p += __shfl_down_sync(0xffffffffu, p, s);
+    q += __shfl_down_sync(0xffffffffu, q, s);
+    e += __shfl_down_sync(0xffffffffu, e, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (p) atomicAdd(counters, p);
+    if (q) atomicAdd(counters + 1, q);
+    if (e) atomicAdd(counters + 2, e);
+  }
+}
+
 __global__ void k_fill_view_outputs(int64_t n, double* o, uint8_t* obs, uint8_t* comp) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
@@ -451,7 +617,17 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
   const int64_t* nb = c->d_scalar.p;
   unsigned long long* pc = c->d_counters.p;
   const int e0 = prof_mark(c);
-  if (tiled)
+  const RecF* recf = view_recf(c, int(&cam - c->cams.data()));
+  if (c->eval_path == 0) {
+    if (tiled)
+      k_eval_f32<MODE, true><<<unsigned(grid), 256, 0, c->stream>>>(
+          c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec, recf,
+          strategies, classify, min_op, ext, o_out, obs, comp, pc);
+    else
+      k_eval_f32<MODE, false><<<unsigned(grid), 256, 0, c->stream>>>(
+          c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec, recf,
+          strategies, classify, min_op, ext, o_out, obs, comp, pc);
+  } else if (tiled)
     k_eval<MODE, true><<<unsigned(grid), 256, 0, c->stream>>>(
         c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
         strategies, classify, min_op, ext, o_out, obs, comp, pc);
@@ -539,11 +715,12 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     }
   }
   if (counters_host) {
-    unsigned long long h[2];
+    unsigned long long h[3];
     SOF_CUDA(cudaMemcpyAsync(h, c->d_counters.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     SOF_CUDA(cudaStreamSynchronize(c->stream));
     counters_host[0] += h[0];
     counters_host[1] += h[1];
+    c->exact_evals += h[2];
   }
 }
 

@@ -39,6 +39,56 @@ struct __align__(16) Rec {
 };
 static_assert(sizeof(Rec) == 96, "record layout");
 
+// FP32 filter record (64 B): a rounded copy of Rec plus error-bound constants.
+// It only decides which pairs are PROVABLY skipped by the reference's tests
+// (te <= 0 at field_eval.hpp:99, alpha < 1/255 at :101); every other pair is
+// evaluated exactly from the FP64 Rec, so results stay bit-identical.
+//   skip if b >= kb                      (then b_fp64 >= 0, i.e. t* <= 0 and te <= 0)
+//   skip if g - (ka te^2 + kb |te| + kc) > gthr, g = (a te + b) te + c
+//                                        (then the FP64 exponent is below log(1/(255 o)))
+// ka, kb, kc bound the float error of a, b, g with a 64-ulp margin.
+struct __align__(16) RecF {
+  float ic[6];   // xx, yy, zz, 2xy, 2xz, 2yz coefficients (off-diagonals doubled)
+  float b2[3];   // 2 * b_vec
+  float c;
+  float gthr;    // 2 log(255 o) + margin (-inf when o == 0)
+  float zmin;    // nearest float of min_z
+  float ka;      // 64 eps * ||Sigma^-1||_F  (bound on |a_f - a|)
+  float kb;      // 64 eps * 2 ||b_vec||_1    (bound on |b_f - b|)
+  float kc;      // 64 eps * |c| + 1e-5
+  uint32_t flags;  // bit 0: dead (filtered opacity < 1/255, exact FP64 compare)
+};
+static_assert(sizeof(RecF) == 64, "float record layout");
+
+constexpr float kEpsMargin = 64.0f * 5.9604645e-8f;  // 64 ulp of 1.0f
+
+__device__ __forceinline__ RecF make_recf(const Rec& r) {
+  RecF f;
+  f.ic[0] = float(r.ic[0]);
+  f.ic[1] = float(r.ic[3]);
+  f.ic[2] = float(r.ic[5]);
+  f.ic[3] = float(2.0 * r.ic[1]);
+  f.ic[4] = float(2.0 * r.ic[2]);
+  f.ic[5] = float(2.0 * r.ic[4]);
+  for (int k = 0; k < 3; ++k) f.b2[k] = float(2.0 * r.b[k]);
+  f.c = float(r.c);
+  const double fro = sqrt(r.ic[0] * r.ic[0] + r.ic[3] * r.ic[3] + r.ic[5] * r.ic[5] +
+                          2.0 * (r.ic[1] * r.ic[1] + r.ic[2] * r.ic[2] + r.ic[4] * r.ic[4]));
+  const double b1 = 2.0 * (fabs(r.b[0]) + fabs(r.b[1]) + fabs(r.b[2]));
+  f.ka = float(double(kEpsMargin) * fro * 1.0001 + 1e-30);
+  f.kb = float(double(kEpsMargin) * b1 * 1.0001 + 1e-30);
+  f.kc = float(double(kEpsMargin) * fabs(r.c) * 1.0001 + 1e-5);
+  if (r.op > 0.0) {
+    const double L = 2.0 * log(255.0 * r.op);
+    f.gthr = float(L + 1e-6 * (1.0 + fabs(L)));
+  } else {
+    f.gthr = -INFINITY;
+  }
+  f.zmin = __double2float_rn(r.zmin);
+  f.flags = (r.op < kMinAlpha) ? 1u : 0u;
+  return f;
+}
+
 // View-independent per-Gaussian data (the parts of precompute.hpp:65-75 that do
 // not depend on the camera, hoisted out of the per-view loop).
 struct GaussStatic {

@@ -143,7 +143,11 @@ struct sof_ctx {
   std::vector<sofk::Binding> bindings;  // per view (cache keyed by tile size)
   size_t cache_budget = size_t(96) << 30;  // bytes of HBM the per-view caches may use
   size_t cache_bytes = 0;
+  std::vector<sofk::DBuf<sofk::RecF>> recfs;
   sofk::DBuf<sofk::Rec> rec_scratch;      // when the cache budget is exhausted
+  sofk::DBuf<sofk::RecF> recf_scratch;
+  int eval_path = 1;                      // 0: FP32 filter + exact FP64 replay, 1: FP64 only
+  uint64_t exact_evals = 0;               // pairs that took the FP64 path (instrumentation)
   sofk::Binding bind_scratch;
 
   // binning scratch
@@ -197,6 +201,7 @@ namespace sofk {
 // ---- k_field.cu -------------------------------------------------------------------------
 void scene_prep(sof_ctx* c);
 const Rec* view_records(sof_ctx* c, int view);
+const RecF* view_recf(sof_ctx* c, int view);
 const Binding& view_binding(sof_ctx* c, int view, int tile_size);
 void invalidate_view_caches(sof_ctx* c);
 void mark_views_stale(sof_ctx* c);
