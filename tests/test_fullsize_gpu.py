@@ -36,7 +36,7 @@ def test_eval_paths_bit_identical(c3):
         st = {}
         mesh = sof.extract_resident(ctx, sof.ExtractOptions(), st)
         out[path] = (mesh, st)
-    ctx.check(ctx.lib.sof_set_eval_path(ctx.h, 0))
+    ctx.check(ctx.lib.sof_set_eval_path(ctx.h, 1))
     (m0, s0), (m1, s1) = out[0], out[1]
     assert len(m0.triangles) > 1000
     np.testing.assert_array_equal(m0.vertices.view(np.uint64), m1.vertices.view(np.uint64))
