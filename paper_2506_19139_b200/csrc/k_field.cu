@@ -231,7 +231,17 @@ static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
                                                             tiles_y, c->rect.p, c->gcount.p,
                                                             c->zkey_in.p, c->gidx_in.p);
   SOF_LAUNCHED(c);
-  // Gaussians in (min_z, index) order: a stable radix sort keeps index order on ties.
+  bin_by_key(c, view, ts, tiles_x, tiles_y, b, true);
+}
+
+// Second half of a binning: Gaussians sorted by (zkey_in, index) — a stable radix
+// sort keeps index order on ties — emit (tile, gaussian) entries in that order, and a
+// stable sort by tile gives per-tile lists ordered by (key, index). Inputs: c->rect,
+// c->gcount[n + 1] (0 sentinel), c->zkey_in, c->gidx_in filled by a rect kernel.
+void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding& b,
+                bool charge_cache) {
+  const int64_t T = int64_t(tiles_x) * tiles_y;
+  const int64_t n = c->n;
   sort_pairs_u64(c, c->zkey_in.p, c->zkey_out.p, c->gidx_in.p, c->gidx_out.p, n, 64);
   c->ekey_in.ensure(n + 1);
   k_gather_counts<<<grid_for(n + 1, 256), 256, 0, c->stream>>>(n, c->gidx_out.p, c->gcount.p,
@@ -239,7 +249,7 @@ static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
   SOF_LAUNCHED(c);
   exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, n + 1);
   const int64_t M = read_scalar(c, c->goff.p + n);
-  if (&b != &c->bind_scratch) {
+  if (charge_cache && &b != &c->bind_scratch) {
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
     if (c->cache_bytes + bytes > c->cache_budget) {

@@ -1,10 +1,493 @@
-// k_render.cu — sorted rasterizer (K5). Placeholder until the tile renderer lands.
+// k_render.cu — the sorted opacity-field rasterizer (K5), FP64 parity path.
+//
+// Replaces render_depth_map (render.hpp:26-51) and render_pixel (opacity_field.hpp:
+// 201-219) over collect_contributions (opacity_field.hpp:39-61). The reference
+// tests EVERY Gaussian against every pixel ray and fully sorts the contributions
+// by (t*, index). Here:
+//   * a conservative per-tile binning: a Gaussian can only reach alpha >= 1/255 on
+//     a ray whose closest-approach point p* lies in its E-ellipsoid (clamped scales),
+//     whose screen box (dilated by one pixel) bounds every such pixel; lists are
+//     ordered by L = |mu - o| - E s_max, a lower bound of t* for every contributing
+//     ray (|p* - o| = t*, |p* - mu| <= E s_max);
+//   * an exact streaming resort per pixel (a k-buffer in shared memory): before a
+//     list entry with bound L is tested, every buffered contribution with t* < L is
+//     final and is blended in (t*, index) order; a pixel whose buffer would
+//     overflow is re-rendered by a per-pixel full-sort fallback;
+//   * contribution tests, alpha, the blend, the median and the exact depth are the
+//     reference's FP64 expressions (bit-identical); the opacity at depth
+//     (opacity_along_ray, :104-108) is a product over all contributions taken in
+//     list order (equal within a few ulps; the reference's order only matters for
+//     the last bits of that product).
+#include <cub/cub.cuh>
+
+#include <vector>
+
 #include "../../include/sof_cuda.h"
 #include "sof_internal.h"
 
-extern "C" int sof_render_view(sof_ctx* c, int, int, int, double*, double*, double*, double*,
-                               uint64_t*) {
+namespace sofk {
+
+constexpr int kRTile = 16;     // render tile (pixels per side), one CTA per tile
+constexpr int kKBuf = 16;      // k-buffer capacity per pixel
+constexpr int kRChunk = 32;    // records staged per step
+
+// ray_through_pixel (camera.hpp:42-48): normalize(R^T ((px - cx)/fx, (py - cy)/fy, 1))
+__device__ __forceinline__ void pixel_ray(const Cam& cam, int x, int y, double* d) {
+  const double v0 = ((x + 0.5) - cam.cx) / cam.fx;
+  const double v1 = ((y + 0.5) - cam.cy) / cam.fy;
+  const double v2 = 1.0;
+  for (int i = 0; i < 3; ++i) d[i] = cam.R[i] * v0 + cam.R[3 + i] * v1 + cam.R[6 + i] * v2;
+  const double sq = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+  if (sq > 0.0) {
+    const double nrm = sqrt(sq);
+    for (int i = 0; i < 3; ++i) d[i] = d[i] / nrm;
+  }
+}
+
+struct Contrib {
+  double t, alpha;
+  int idx;
+  bool ok;
+};
+
+// collect_contributions' per-Gaussian test (opacity_field.hpp:43-53)
+__device__ __forceinline__ Contrib contribution(const Rec& r, const double* d, int idx) {
+  Contrib c;
+  c.ok = false;
+  c.idx = idx;
+  if (r.op < kMinAlpha) return c;
+  const double x = d[0], y = d[1], z = d[2];
+  const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
+                   2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
+  const double b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
+  const double alpha = r.op * sof_exp(-0.5 * (r.c - b * b / (4.0 * a)));  // peak_value
+  if (alpha < kMinAlpha) return c;
+  c.t = -b / (2.0 * a);
+  if (c.t <= 0.0) return c;
+  c.alpha = (kMaxAlpha < alpha) ? kMaxAlpha : alpha;
+  c.ok = true;
+  return c;
+}
+
+// alpha_at (opacity_field.hpp:95-101) of the contribution of record r at parameter t
+__device__ __forceinline__ double alpha_at(const Rec& r, const double* d, double t_star, double t) {
+  const double x = d[0], y = d[1], z = d[2];
+  const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
+                   2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
+  const double b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
+  const double te = (t < t_star) ? t : t_star;
+  if (te <= 0.0) return 0.0;
+  const double al = r.op * sof_exp(-0.5 * ((a * te + b) * te + r.c));
+  if (al < kMinAlpha) return 0.0;
+  return (kMaxAlpha < al) ? kMaxAlpha : al;
+}
+
+// Conservative render binning: E-box with clamped scales (inflated by 1e-6), one-pixel
+// dilation, key L = |mu - o| - E' s'_max (a lower bound of t* of any contribution).
+__global__ void k_render_rect(int64_t n, const GaussStatic* __restrict__ g, Cam cam, int ts,
+                              int tiles_x, int tiles_y, int4* rect, uint32_t* cnt, uint64_t* key,
+                              int32_t* idx, double* lkey) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {
+    cnt[n] = 0;
+    return;
+  }
+  const GaussStatic& G = g[i];
+  uint32_t count = 0;
+  double L = 0.0;
+  if (G.E > 0.0) {
+    const double E = G.E * (1.0 + 1e-6);
+    double s[3], smax = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      s[k] = (G.scale[k] < kMinScale) ? kMinScale : G.scale[k];
+      smax = fmax(smax, s[k]);
+    }
+    double min_x = 1e300, max_x = -1e300, min_y = 1e300, max_y = -1e300;
+    bool crosses = false;
+    for (int mask = 0; mask < 8; ++mask) {
+      const double l0 = E * s[0] * ((mask & 1) ? 1.0 : -1.0);
+      const double l1 = E * s[1] * ((mask & 2) ? 1.0 : -1.0);
+      const double l2 = E * s[2] * ((mask & 4) ? 1.0 : -1.0);
+      const double p0 = G.pos[0] + (G.rot[0] * l0 + G.rot[1] * l1 + G.rot[2] * l2);
+      const double p1 = G.pos[1] + (G.rot[3] * l0 + G.rot[4] * l1 + G.rot[5] * l2);
+      const double p2 = G.pos[2] + (G.rot[6] * l0 + G.rot[7] * l1 + G.rot[8] * l2);
+      const double vx = to_view_c(cam, 0, p0, p1, p2);
+      const double vy = to_view_c(cam, 1, p0, p1, p2);
+      const double vz = to_view_c(cam, 2, p0, p1, p2);
+      if (vz <= 1e-9) {
+        crosses = true;
+        break;
+      }
+      const double px = cam.fx * vx / vz + cam.cx, py = cam.fy * vy / vz + cam.cy;
+      min_x = fmin(min_x, px);
+      max_x = fmax(max_x, px);
+      min_y = fmin(min_y, py);
+      max_y = fmax(max_y, py);
+    }
+    int tx0 = 0, tx1 = tiles_x - 1, ty0 = 0, ty1 = tiles_y - 1;
+    bool on = true;
+    if (!crosses) {
+      min_x -= 1.0;
+      min_y -= 1.0;
+      max_x += 1.0;
+      max_y += 1.0;
+      on = !(max_x < 0.0 || min_x >= cam.w || max_y < 0.0 || min_y >= cam.h);
+      const double lim = 1e9;
+      tx0 = max(0, int(floor(fmax(min_x, -lim))) / ts);
+      tx1 = min(tiles_x - 1, int(floor(fmin(max_x, lim))) / ts);
+      ty0 = max(0, int(floor(fmax(min_y, -lim))) / ts);
+      ty1 = min(tiles_y - 1, int(floor(fmin(max_y, lim))) / ts);
+    }
+    if (on && tx0 <= tx1 && ty0 <= ty1) {
+      count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
+      rect[i] = make_int4(tx0, tx1, ty0, ty1);
+    }
+    const double e0 = G.pos[0] - cam.center[0], e1 = G.pos[1] - cam.center[1],
+                 e2 = G.pos[2] - cam.center[2];
+    L = sqrt(e0 * e0 + e1 * e1 + e2 * e2) - E * smax;
+    L = L - 1e-9 * (1.0 + fabs(L));
+  }
+  cnt[i] = count;
+  key[i] = double_key(L);
+  idx[i] = int32_t(i);
+  lkey[i] = L;
+}
+
+struct RenderOut {
+  double* depth;
+  double* opacity;
+  double* rgb;
+  double* tfinal;
+};
+
+// One CTA per 16x16 tile; thread = pixel. Pass 1: exact streaming resort + blend +
+// median (+ exact depth); pass 2: opacity at depth.
+__global__ void __launch_bounds__(256) k_render(
+    Cam cam, int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
+    const Rec* __restrict__ recs, const double* __restrict__ lkey, const double* __restrict__ dc,
+    int exact_depth, RenderOut out, int32_t* overflow, unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Rec* srec = reinterpret_cast<Rec*>(smem);
+  double* sL = reinterpret_cast<double*>(srec + kRChunk);
+  int32_t* sidx = reinterpret_cast<int32_t*>(sL + kRChunk);
+  double* bt = reinterpret_cast<double*>(sidx + kRChunk);  // [kKBuf][256]
+  double* ba = bt + kKBuf * 256;
+  int32_t* bi = reinterpret_cast<int32_t*>(ba + kKBuf * 256);
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int px = (tile % tiles_x) * kRTile + (tid % kRTile);
+  const int py = (tile / tiles_x) * kRTile + (tid / kRTile);
+  const bool valid = px < cam.w && py < cam.h;
+  double d[3] = {0.0, 0.0, 1.0};
+  if (valid) pixel_ray(cam, px, py, d);
+  const int64_t l0 = loff[tile], l1 = loff[tile + 1];
+  double T = 1.0, col[3] = {0.0, 0.0, 0.0};
+  int nbuf = 0;
+  bool found = false, over = false;
+  int med_idx = -1;
+  double med_t = 0.0, med_T = 1.0;
+  unsigned long long tested = 0, contributing = 0;
+
+  auto blend = [&](double t, double alpha, int idx) {
+    for (int k = 0; k < 3; ++k) col[k] = col[k] + dc[3 * idx + k] * alpha * T;
+    const double next = T * (1.0 - alpha);
+    if (!found && T > 0.5 && next < 0.5) {
+      found = true;
+      med_idx = idx;
+      med_t = t;
+      med_T = T;
+    }
+    T = next;
+  };
+  // pops the (t, idx)-smallest buffered entry if its t < bound
+  auto flush_below = [&](double bound) {
+    while (nbuf > 0) {
+      int m = 0;
+      for (int k = 1; k < nbuf; ++k) {
+        const double tk = bt[k * 256 + tid], tm = bt[m * 256 + tid];
+        if (tk < tm || (tk == tm && bi[k * 256 + tid] < bi[m * 256 + tid])) m = k;
+      }
+      const double tm = bt[m * 256 + tid];
+      if (!(tm < bound)) return;
+      blend(tm, ba[m * 256 + tid], bi[m * 256 + tid]);
+      --nbuf;
+      bt[m * 256 + tid] = bt[nbuf * 256 + tid];
+      ba[m * 256 + tid] = ba[nbuf * 256 + tid];
+      bi[m * 256 + tid] = bi[nbuf * 256 + tid];
+    }
+  };
+
+  bool live = valid;
+  for (int64_t base = l0; base < l1; base += kRChunk) {
+    if (!__syncthreads_or(live)) break;
+    const int cnt = int(min(int64_t(kRChunk), l1 - base));
+    for (int k = tid; k < cnt * 6; k += blockDim.x) {
+      const int r = k / 6, q = k % 6;
+      const int32_t g = lent[base + r];
+      reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+      if (q == 0) {
+        sidx[r] = g;
+        sL[r] = lkey[g];
+      }
+    }
+    __syncthreads();
+    if (live) {
+      for (int k = 0; k < cnt; ++k) {
+        flush_below(sL[k]);
+        ++tested;
+        const Contrib c = contribution(srec[k], d, sidx[k]);
+        if (!c.ok) continue;
+        ++contributing;
+        if (nbuf == kKBuf) {
+          over = true;
+          live = false;
+          break;
+        }
+        bt[nbuf * 256 + tid] = c.t;
+        ba[nbuf * 256 + tid] = c.alpha;
+        bi[nbuf * 256 + tid] = c.idx;
+        ++nbuf;
+      }
+    }
+  }
+  if (valid && !over) flush_below(INFINITY);
+  double depth = NAN;
+  bool fell_back = false;
+  if (valid && !over && found) {
+    depth = med_t;
+    if (exact_depth) {  // exact_depth (opacity_field.hpp:157-166)
+      const Rec r = recs[med_idx];
+      const double x = d[0], y = d[1], z = d[2];
+      const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
+                       2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
+      const double b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
+      const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * r.op));
+      const double disc = b * b - 4.0 * a * (r.c + lt);
+      if (disc < 0.0)
+        fell_back = true;
+      else
+        depth = med_t - sqrt(disc) / (2.0 * a);
+    }
+  }
+  // pass 2: O_N at the depth over all contributions (opacity_along_ray)
+  bool need2 = valid && !over && !isnan(depth);
+  double T2 = 1.0;
+  for (int64_t base = l0; base < l1; base += kRChunk) {
+    if (!__syncthreads_or(need2)) break;
+    const int cnt = int(min(int64_t(kRChunk), l1 - base));
+    for (int k = tid; k < cnt * 6; k += blockDim.x) {
+      const int r = k / 6, q = k % 6;
+      const int32_t g = lent[base + r];
+      reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+      if (q == 0) sidx[r] = g;
+    }
+    __syncthreads();
+    if (need2) {
+      for (int k = 0; k < cnt; ++k) {
+        const Contrib c = contribution(srec[k], d, sidx[k]);
+        if (!c.ok) continue;
+        T2 *= 1.0 - alpha_at(srec[k], d, c.t, depth);
+      }
+    }
+  }
+  if (valid) {
+    const int64_t p = int64_t(py) * cam.w + px;
+    if (over) {
+      overflow[1 + atomicAdd(overflow, 1)] = int32_t(p);
+    } else {
+      out.depth[p] = depth;
+      out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
+      for (int k = 0; k < 3; ++k) out.rgb[3 * p + k] = col[k];
+      out.tfinal[p] = T;
+    }
+  }
+  unsigned long long s0 = tested, s1 = contributing, s3 = fell_back ? 1 : 0;
+  for (int s = 16; s > 0; s >>= 1) {
+    s0 += __shfl_down_sync(0xffffffffu, s0, s);
+    s1 += __shfl_down_sync(0xffffffffu, s1, s);
+    s3 += __shfl_down_sync(0xffffffffu, s3, s);
+  }
+  if ((tid & 31) == 0) {
+    if (s0) atomicAdd(stats, s0);
+    if (s1) atomicAdd(stats + 1, s1);
+    if (s3) atomicAdd(stats + 3, s3);
+  }
+}
+
+// Fallback for k-buffer overflow: one thread per pixel collects every contribution of
+// its tile list into a private global slice, insertion-sorts by (t*, index) and
+// renders exactly as above.
+__global__ void k_render_fallback(Cam cam, int tiles_x, const int64_t* __restrict__ loff,
+                                  const int32_t* __restrict__ lent, const Rec* __restrict__ recs,
+                                  const double* __restrict__ dc, int exact_depth,
+                                  const int32_t* __restrict__ overflow, int64_t slice,
+                                  double* st, double* sa, int32_t* si, RenderOut out,
+                                  unsigned long long* stats) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= overflow[0]) return;
+  const int64_t p = overflow[1 + k];
+  const int px = int(p % cam.w), py = int(p / cam.w);
+  const int tile = (py / kRTile) * tiles_x + px / kRTile;
+  double d[3];
+  pixel_ray(cam, px, py, d);
+  double* t = st + k * slice;
+  double* a = sa + k * slice;
+  int32_t* ix = si + k * slice;
+  int m = 0;
+  for (int64_t e = loff[tile]; e < loff[tile + 1]; ++e) {
+    const Contrib c = contribution(recs[lent[e]], d, lent[e]);
+    if (!c.ok) continue;
+    int j = m++;
+    while (j > 0 && (t[j - 1] > c.t || (t[j - 1] == c.t && ix[j - 1] > c.idx))) {
+      t[j] = t[j - 1];
+      a[j] = a[j - 1];
+      ix[j] = ix[j - 1];
+      --j;
+    }
+    t[j] = c.t;
+    a[j] = c.alpha;
+    ix[j] = c.idx;
+  }
+  double T = 1.0, col[3] = {0.0, 0.0, 0.0}, depth = NAN;
+  bool found = false;
+  int med = -1;
+  double med_T = 1.0;
+  for (int j = 0; j < m; ++j) {
+    for (int q = 0; q < 3; ++q) col[q] = col[q] + dc[3 * ix[j] + q] * a[j] * T;
+    const double next = T * (1.0 - a[j]);
+    if (!found && T > 0.5 && next < 0.5) {
+      found = true;
+      med = j;
+      med_T = T;
+    }
+    T = next;
+  }
+  if (found) {
+    depth = t[med];
+    if (exact_depth) {
+      const Rec r = recs[ix[med]];
+      const double x = d[0], y = d[1], z = d[2];
+      const double aa = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
+                        2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
+      const double bb = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
+      const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * r.op));
+      const double disc = bb * bb - 4.0 * aa * (r.c + lt);
+      if (disc < 0.0)
+        atomicAdd(stats + 3, 1ull);
+      else
+        depth = t[med] - sqrt(disc) / (2.0 * aa);
+    }
+  }
+  double T2 = 1.0;
+  if (!isnan(depth))
+    for (int j = 0; j < m; ++j) T2 *= 1.0 - alpha_at(recs[ix[j]], d, t[j], depth);
+  out.depth[p] = depth;
+  out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
+  for (int q = 0; q < 3; ++q) out.rgb[3 * p + q] = col[q];
+  out.tfinal[p] = T;
+}
+
+}  // namespace sofk
+
+using namespace sofk;
+
+extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_size, double* depth,
+                               double* opacity, double* rgb, double* t_final, uint64_t* stats) {
   if (!c) return SOF_E_INVALID;
-  c->err = "sof_render_view: not implemented";
-  return SOF_E_STATE;
+  try {
+    SOF_CUDA(cudaSetDevice(c->device));
+    if (!c->has_scene) throw StateError("no scene: call sof_set_scene first");
+    if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+    (void)tile_size;  // the reference render has no tiles; the render tile is fixed at 16
+    const Cam& cam = c->cams[view];
+    const int ts = kRTile;
+    const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
+    const int64_t n = c->n, P = int64_t(cam.w) * cam.h;
+    const Rec* rec = view_records(c, view);
+    c->rect.ensure(std::max<int64_t>(n, 1));
+    c->gcount.ensure(n + 1);
+    c->zkey_in.ensure(std::max<int64_t>(n, 1));
+    c->zkey_out.ensure(std::max<int64_t>(n, 1));
+    c->gidx_in.ensure(std::max<int64_t>(n, 1));
+    c->gidx_out.ensure(std::max<int64_t>(n, 1));
+    c->goff.ensure(n + 1);
+    c->ms.mid.ensure(std::max<int64_t>(n, 1));  // L keys (double) per Gaussian
+    k_render_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(
+        n, c->gstat.p, cam, ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p,
+        c->ms.mid.p);
+    SOF_LAUNCHED(c);
+    if (n > 0) bin_by_key(c, view, ts, tiles_x, tiles_y, c->rbind, false);
+    else {
+      c->rbind.off.ensure(int64_t(tiles_x) * tiles_y + 1);
+      SOF_CUDA(cudaMemsetAsync(c->rbind.off.p, 0, sizeof(int64_t) * (int64_t(tiles_x) * tiles_y + 1),
+                               c->stream));
+      c->rbind.ent.ensure(1);
+    }
+    c->r_out.ensure(6 * P);
+    RenderOut out{c->r_out.p, c->r_out.p + P, c->r_out.p + 2 * P, c->r_out.p + 5 * P};
+    c->r_overflow.ensure(P + 1);
+    c->r_stats.ensure(4);
+    SOF_CUDA(cudaMemsetAsync(c->r_overflow.p, 0, sizeof(int32_t), c->stream));
+    SOF_CUDA(cudaMemsetAsync(c->r_stats.p, 0, 4 * sizeof(unsigned long long), c->stream));
+    const size_t smem = kRChunk * (sizeof(Rec) + sizeof(double) + sizeof(int32_t)) +
+                        size_t(kKBuf) * 256 * (2 * sizeof(double) + sizeof(int32_t));
+    static bool attr_set = false;
+    if (!attr_set) {
+      SOF_CUDA(cudaFuncSetAttribute(k_render, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr_set = true;
+    }
+    k_render<<<tiles_x * tiles_y, 256, smem, c->stream>>>(
+        cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->ms.mid.p, c->dc.p,
+        depth_mode == SOF_DEPTH_EXACT, out, c->r_overflow.p, c->r_stats.p);
+    SOF_LAUNCHED(c);
+    const int32_t nover = read_scalar(c, c->r_overflow.p);
+    if (nover > 0) {
+      // slice = the longest tile list
+      std::vector<int64_t> off(int64_t(tiles_x) * tiles_y + 1);
+      SOF_CUDA(cudaMemcpyAsync(off.data(), c->rbind.off.p, sizeof(int64_t) * off.size(),
+                               cudaMemcpyDeviceToHost, c->stream));
+      SOF_CUDA(cudaStreamSynchronize(c->stream));
+      int64_t slice = 1;
+      for (size_t t = 0; t + 1 < off.size(); ++t) slice = std::max(slice, off[t + 1] - off[t]);
+      DBuf<double> st, sa;
+      DBuf<int32_t> si;
+      st.ensure(size_t(nover) * slice);
+      sa.ensure(size_t(nover) * slice);
+      si.ensure(size_t(nover) * slice);
+      k_render_fallback<<<grid_for(nover, 64), 64, 0, c->stream>>>(
+          cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT,
+          c->r_overflow.p, slice, st.p, sa.p, si.p, out, c->r_stats.p);
+      SOF_LAUNCHED(c);
+      SOF_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    if (depth) SOF_CUDA(cudaMemcpyAsync(depth, out.depth, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
+    if (opacity)
+      SOF_CUDA(cudaMemcpyAsync(opacity, out.opacity, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
+    if (rgb) SOF_CUDA(cudaMemcpyAsync(rgb, out.rgb, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, c->stream));
+    if (t_final)
+      SOF_CUDA(cudaMemcpyAsync(t_final, out.tfinal, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
+    unsigned long long h[4];
+    SOF_CUDA(cudaMemcpyAsync(h, c->r_stats.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+    if (stats) {
+      stats[0] = h[0];
+      stats[1] = h[1];
+      stats[2] = uint64_t(nover);
+      stats[3] = h[3];
+    }
+    return SOF_OK;
+  } catch (const InvalidArg& e) {
+    c->err = e.what();
+    return SOF_E_INVALID;
+  } catch (const StateError& e) {
+    c->err = e.what();
+    return SOF_E_STATE;
+  } catch (const OomError& e) {
+    c->err = e.what();
+    return SOF_E_OOM;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return SOF_E_CUDA;
+  }
 }

@@ -161,6 +161,10 @@ struct sof_ctx {
 
   sofk::PointSchedule sched;
   sofk::MeshScratch ms;
+  sofk::Binding rbind;                    // render binding (lists ordered by a t* lower bound)
+  sofk::DBuf<int32_t> r_overflow;         // [0] count, then overflow pixel ids
+  sofk::DBuf<double> r_out;               // depth, opacity, rgb(3), t_final per pixel
+  sofk::DBuf<unsigned long long> r_stats;
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
   sofk::DBuf<int64_t> d_scalar;               // small device scalars
@@ -203,6 +207,8 @@ void scene_prep(sof_ctx* c);
 const Rec* view_records(sof_ctx* c, int view);
 const RecF* view_recf(sof_ctx* c, int view);
 const Binding& view_binding(sof_ctx* c, int view, int tile_size);
+void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding& b,
+                bool charge_cache);
 void invalidate_view_caches(sof_ctx* c);
 void mark_views_stale(sof_ctx* c);
 // Evaluates points xyz_dev[n] against views [v0, v1) in order (field_eval.hpp:59-176).
