@@ -210,7 +210,7 @@ def main():
     if world > 1:
         from paper_2506_19139_b200.sharded import ShardedMesher
         mesher = ShardedMesher(ctx, rank, world)
-        step = lambda st: mesher.extract_resident(opt, st)  # noqa: E731
+        step = lambda st: mesher.extract(sof.ExtractOptions(), st, fetch=False)  # noqa: E731
     else:
         step = lambda st: sof.extract_resident(ctx, opt, st, fetch=False)  # noqa: E731
 
@@ -247,21 +247,27 @@ def main():
     queries = len(verts) + ITER * E
     value = queries / (ms_step * 1e-3)
 
-    # roofline of the dominant kernel (opacity evaluation, FP64 pipe)
-    eval_ms = np.mean([s["ms_eval_kernel"] for s in stats])
-    eval_launches = np.mean([s["eval_launches"] for s in stats])
-    pairs = np.mean([s["pairs"] for s in stats])
-    fp64 = ctypes.c_double()
-    ctx.check(lib.sof_fp64_peak(ctx.h, ctypes.byref(fp64)))
-    achieved = pairs * FLOP_PER_PAIR / (eval_ms * 1e-3) / 1e12
-    traffic = ncu_traffic()
-    roof = {"bound": "fp64", "kernel": "k_eval (opacity evaluation, FP64 parity path)",
-            "achieved": achieved, "peak": fp64.value, "unit": "TFLOP/s", "frac": achieved / fp64.value,
-            "traffic": traffic, "flop_per_pair": FLOP_PER_PAIR,
-            "pairs_per_s": pairs / (eval_ms * 1e-3), "kernel_share_of_step": eval_ms / ms_step,
-            "avg_launch_ms": eval_ms / max(eval_launches, 1),
-            "peak_note": "FP64 FMA-pipe throughput measured in-process (sof_fp64_peak, 2 FLOP/DFMA); "
-                         "MEASURED_PEAKS.json has no FP64 figure"}
+    # roofline of the dominant kernel (opacity evaluation, FP64 pipe); the fused
+    # single-GPU step reports per-launch kernel times, the sharded step does not
+    def mean(k, default=None):
+        vals = [s[k] for s in stats if k in s]
+        return float(np.mean(vals)) if vals else default
+
+    pairs = mean("pairs", mean("rank_pairs", 0.0))
+    roof = None
+    if "ms_eval_kernel" in last:
+        eval_ms = mean("ms_eval_kernel")
+        eval_launches = mean("eval_launches")
+        fp64 = ctypes.c_double()
+        ctx.check(lib.sof_fp64_peak(ctx.h, ctypes.byref(fp64)))
+        achieved = pairs * FLOP_PER_PAIR / (eval_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "kernel": "k_eval (opacity evaluation, FP64 parity path)",
+                "achieved": achieved, "peak": fp64.value, "unit": "TFLOP/s", "frac": achieved / fp64.value,
+                "traffic": ncu_traffic(), "flop_per_pair": FLOP_PER_PAIR,
+                "pairs_per_s": pairs / (eval_ms * 1e-3), "kernel_share_of_step": eval_ms / ms_step,
+                "avg_launch_ms": eval_ms / max(eval_launches, 1),
+                "peak_note": "FP64 FMA-pipe throughput measured in-process (sof_fp64_peak, 2 FLOP/DFMA); "
+                             "MEASURED_PEAKS.json has no FP64 figure"}
 
     # e2e: the public C-ABI with host buffers: upload scene/views/tets, extract, fetch mesh
     e2e = None
@@ -303,11 +309,10 @@ def main():
                            "parallelism": f"views sharded x{world}" if world > 1 else "single GPU",
                            "l2": "inputs (0.65 GB vertices + 2.6 GB tets + per-view caches) exceed the 126 MB L2"},
                 "meshing_wall_s": ms_step / 1e3, "queries_per_step": queries,
-                "stages_ms": {k: float(np.mean([s[k] for s in stats])) for k in
-                              ("ms_label", "ms_march", "ms_refine", "ms_weld", "ms_prep", "ms_sched",
-                               "ms_eval_kernel")},
-                "point_view_evals_per_step": int(np.mean([s["point_view_evals"] for s in stats])),
-                "label_queries_per_s": len(verts) / (np.mean([s["ms_label"] for s in stats]) * 1e-3),
+                "stages_ms": {k: mean(k) for k in ("ms_label", "ms_march", "ms_refine", "ms_weld", "ms_prep",
+                                                   "ms_sched", "ms_eval_kernel") if k in last},
+                "point_view_evals_per_step": int(mean("point_view_evals", mean("rank_point_view_evals", 0))),
+                "label_queries_per_s": (len(verts) / (mean("ms_label") * 1e-3)) if "ms_label" in last else None,
                 "crossing_edges": E, "mesh_vertices": int(last["mesh_vertices"]),
                 "mesh_triangles": int(last["mesh_triangles"]), "pairs_per_step": int(pairs),
                 "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -167,6 +167,31 @@ int sof_classify_views_dev(sof_ctx* ctx, int v0, int v1, int64_t n, const double
                            int strategies, int tile_size, uint8_t* exterior_dev,
                            uint64_t* counters);
 
+/* ---- view-sharded meshing primitives (one process per GPU; the caller runs the
+ * collectives, see paper_2506_19139_b200/sharded.py) ------------------------------------ */
+/* device pointer of the resident tetra vertices (xyz_dev[3 nv]) */
+int sof_tets_vertices_dev(sof_ctx* ctx, const double** xyz_dev, int64_t* nv);
+/* out[i] = exterior[i] ? rank : world — all-reduce MIN gives the first exterior rank */
+int sof_shard_ext_rank_dev(sof_ctx* ctx, int64_t n, const uint8_t* exterior_dev, int rank,
+                           int world, int32_t* out_dev);
+/* min_opacity[i] = +inf where rank > first_exterior_rank[i] (views after the first
+ * exterior view are pruned in the sequential reference, field_eval.hpp:147) */
+int sof_shard_mask_min_dev(sof_ctx* ctx, int64_t n, const int32_t* first_ext_rank_dev, int rank,
+                           double* min_opacity_dev);
+/* label_grid's final write (field_eval.hpp:173-175) into the resident grid opacity */
+int sof_shard_finalize_dev(sof_ctx* ctx, int64_t n, const double* min_opacity_dev,
+                           const int32_t* first_ext_rank_dev, int world);
+/* marching_tets over the resident tets and grid opacity (results stay resident) */
+int sof_march_resident(sof_ctx* ctx, int64_t* n_edges, int64_t* n_tris);
+/* one phase of binary_search_refine over the resident crossing edges:
+ * 0 init brackets, 1 midpoints + classify against views [v0, v1) into exterior_dev
+ * (cleared first), 2 update brackets from exterior_dev, 3 write the final vertices */
+int sof_refine_phase_dev(sof_ctx* ctx, int phase, uint8_t* exterior_dev, int v0, int v1,
+                         int strategies, int tile_size, uint64_t* counters);
+/* assemble_mesh over the resident refined vertices / triangles */
+int sof_assemble_resident(sof_ctx* ctx, double weld_eps, double min_area, int64_t* n_verts,
+                          int64_t* n_tris);
+
 /* ---- mesher ------------------------------------------------------------------------- */
 /* marching_tets (marching_tets.hpp:29-84) over the resident tets with the given vertex
  * opacities (host array, nv entries; NULL = use the last label result).

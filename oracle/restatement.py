@@ -53,6 +53,7 @@ def lib():
         L.sofo_view_opacity.argtypes = [S, C, _I, _I, _I, _I64, _P, _I, _P, _P, _P, _P]
         L.sofo_label_grid.argtypes = [S, C, _I, _I, _I64, _P, _I, _P, _P]
         L.sofo_classify_points.argtypes = [S, C, _I, _I, _I64, _P, _P, _P]
+        L.sofo_label_state.argtypes = [S, C, _I, _I, _I64, _P, _I, _P, _P, _P]
         L.sofo_value_at.argtypes = [S, C, _I, _I, _I64, _P, _P, _P]
         L.sofo_marching_tets.restype = _I64
         L.sofo_marching_tets.argtypes = [_I64, _P, _I64, _P, _P, _P, _P, _P, _P]
@@ -176,6 +177,20 @@ def label_grid(scene, cams, strategies, xyz, classify_mode=True, tile_size=16, f
     lib().sofo_label_grid(ctypes.byref(s), ctypes.byref(c), strategies, tile_size, len(xyz), _p(xyz),
                           int(classify_mode), _p(out), _p(cnt))
     return out, cnt
+
+
+def label_state(scene, cams, strategies, xyz, min_op, ext, classify_mode=True, tile_size=16,
+                filter_scale=0.0):
+    """label_grid's view loop with caller state; min_op (f64) and ext (u8) updated in place."""
+    k = _Keep()
+    s, c = _scene(k, scene, filter_scale), _cams(k, cams)
+    xyz = k.f64(xyz, 3)
+    assert min_op.dtype == np.float64 and ext.dtype == np.uint8 and min_op.flags.c_contiguous
+    cnt = np.zeros(2, np.uint64)
+    if c.v:
+        lib().sofo_label_state(ctypes.byref(s), ctypes.byref(c), strategies, tile_size, len(xyz), _p(xyz),
+                               int(classify_mode), _p(min_op), _p(ext), _p(cnt))
+    return cnt
 
 
 def classify_points(scene, cams, strategies, xyz, tile_size=16, filter_scale=0.0):

@@ -403,6 +403,22 @@ void sofo_label_grid(const sofo_scene* s, const sofo_cams* c, int strategies, in
   eval_free(&e);
 }
 
+void sofo_label_state(const sofo_scene* s, const sofo_cams* c, int strategies, int tile_size,
+                      int64_t nv, const double* xyz, int classify_mode, double* min_op,
+                      uint8_t* ext, uint64_t* counters) {
+  Eval e = eval_make(s, c, strategies, tile_size);
+  for (int v = 0; v < c->v; ++v)
+    for (int64_t i = 0; i < nv; ++i) {
+      if ((strategies & 8) && ext[i]) continue;
+      int ob, co;
+      const double o = view_opacity(&e, v, xyz + 3 * i, classify_mode, &ob, &co, counters);
+      if (!ob) continue;
+      min_op[i] = o < min_op[i] ? o : min_op[i];
+      if (co && o < 0.5) ext[i] = 1;
+    }
+  eval_free(&e);
+}
+
 /* classify_point (field_eval.hpp:114-125) */
 static int classify_point(const Eval* e, const double* x, uint64_t* counters) {
   int interior = 1;

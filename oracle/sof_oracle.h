@@ -52,6 +52,12 @@ void sofo_label_grid(const sofo_scene* s, const sofo_cams* c, int strategies, in
                      int64_t nv, const double* xyz, int classify_mode, double* opacity,
                      uint64_t* counters);
 
+/* label_grid's per-view loop (field_eval.hpp:145-172) over the given cameras with
+ * caller-owned state (min_opacity in/out, exterior in/out), without the final write. */
+void sofo_label_state(const sofo_scene* s, const sofo_cams* c, int strategies, int tile_size,
+                      int64_t nv, const double* xyz, int classify_mode, double* min_opacity,
+                      uint8_t* exterior, uint64_t* counters);
+
 /* classify_point (field_eval.hpp:114-125) and value_at (:128-136), batched. */
 void sofo_classify_points(const sofo_scene* s, const sofo_cams* c, int strategies,
                           int tile_size, int64_t n, const double* xyz, uint8_t* interior,

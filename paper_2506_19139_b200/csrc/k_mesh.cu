@@ -334,33 +334,51 @@ __global__ void k_bisect_final(int64_t ne, const double* __restrict__ pin,
   for (int k = 0; k < 3; ++k) verts[3 * e + k] = 0.5 * (pin[3 * e + k] + pout[3 * e + k]);
 }
 
+// Bisection phases (also driven one by one by the view-sharded path, with an
+// all-reduce of the exterior flags between classify and update).
+void refine_init(sof_ctx* c, int64_t ne, const int32_t* edges) {
+  MeshScratch& s = c->ms;
+  s.pin.ensure(3 * ne);
+  s.pout.ensure(3 * ne);
+  s.mid.ensure(3 * ne);
+  s.rext.ensure(ne);
+  if (ne == 0) return;
+  k_bisect_init<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, edges, c->tv.p, s.pin.p, s.pout.p);
+  SOF_LAUNCHED(c);
+}
+
+void refine_mid(sof_ctx* c, int64_t ne, uint8_t* ext) {
+  if (ne == 0) return;
+  k_bisect_mid<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, c->ms.pin.p, c->ms.pout.p, c->ms.mid.p, ext);
+  SOF_LAUNCHED(c);
+}
+
+void refine_update(sof_ctx* c, int64_t ne, const uint8_t* ext) {
+  if (ne == 0) return;
+  k_bisect_update<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, c->ms.mid.p, ext, c->ms.pin.p, c->ms.pout.p);
+  SOF_LAUNCHED(c);
+}
+
+void refine_final(sof_ctx* c, int64_t ne, double* verts) {
+  if (ne == 0) return;
+  k_bisect_final<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, c->ms.pin.p, c->ms.pout.p, verts);
+  SOF_LAUNCHED(c);
+}
+
 void refine(sof_ctx* c, int64_t ne, const int32_t* edges, double* verts, int iterations,
             int strategies, int tile_size, int v0, int v1, uint64_t* counters) {
   if (iterations <= 0 || ne == 0) return;  // iterations = 0 keeps the lerp vertices (:100)
   if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
-  MeshScratch& s = c->ms;
-  DBuf<double>& pin = s.pin;
-  DBuf<double>& pout = s.pout;
-  DBuf<double>& mid = s.mid;
-  DBuf<uint8_t>& ext = s.rext;
-  pin.ensure(3 * ne);
-  pout.ensure(3 * ne);
-  mid.ensure(3 * ne);
-  ext.ensure(ne);
-  k_bisect_init<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, edges, c->tv.p, pin.p, pout.p);
-  SOF_LAUNCHED(c);
+  refine_init(c, ne, edges);
   for (int it = 0; it < iterations; ++it) {
-    k_bisect_mid<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, pin.p, pout.p, mid.p, ext.p);
-    SOF_LAUNCHED(c);
+    refine_mid(c, ne, c->ms.rext.p);
     // classify_point over every view (field_eval.hpp:114-125): exterior iff some view
     // has observed && complete && O < 0.5; prune skips the rest for that point
-    eval_views(c, v0, v1, ne, mid.p, strategies, tile_size, true, kModeClassify, nullptr, ext.p,
-               nullptr, nullptr, nullptr, counters);
-    k_bisect_update<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, mid.p, ext.p, pin.p, pout.p);
-    SOF_LAUNCHED(c);
+    eval_views(c, v0, v1, ne, c->ms.mid.p, strategies, tile_size, true, kModeClassify, nullptr,
+               c->ms.rext.p, nullptr, nullptr, nullptr, counters);
+    refine_update(c, ne, c->ms.rext.p);
   }
-  k_bisect_final<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, pin.p, pout.p, verts);
-  SOF_LAUNCHED(c);
+  refine_final(c, ne, verts);
 }
 
 // ---- K10: weld ------------------------------------------------------------------------------------

@@ -412,10 +412,10 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     c->gidx_in.ensure(std::max<int64_t>(n, 1));
     c->gidx_out.ensure(std::max<int64_t>(n, 1));
     c->goff.ensure(n + 1);
-    c->ms.mid.ensure(std::max<int64_t>(n, 1));  // L keys (double) per Gaussian
+    c->r_lkey.ensure(std::max<int64_t>(n, 1));  // L keys (double) per Gaussian
     k_render_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(
         n, c->gstat.p, cam, ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p,
-        c->ms.mid.p);
+        c->r_lkey.p);
     SOF_LAUNCHED(c);
     if (n > 0) bin_by_key(c, view, ts, tiles_x, tiles_y, c->rbind, false);
     else {
@@ -438,7 +438,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       attr_set = true;
     }
     k_render<<<tiles_x * tiles_y, 256, smem, c->stream>>>(
-        cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->ms.mid.p, c->dc.p,
+        cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->r_lkey.p, c->dc.p,
         depth_mode == SOF_DEPTH_EXACT, out, c->r_overflow.p, c->r_stats.p);
     SOF_LAUNCHED(c);
     const int32_t nover = read_scalar(c, c->r_overflow.p);

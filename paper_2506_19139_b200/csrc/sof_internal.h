@@ -164,6 +164,7 @@ struct sof_ctx {
   sofk::Binding rbind;                    // render binding (lists ordered by a t* lower bound)
   sofk::DBuf<int32_t> r_overflow;         // [0] count, then overflow pixel ids
   sofk::DBuf<double> r_out;               // depth, opacity, rgb(3), t_final per pixel
+  sofk::DBuf<double> r_lkey;              // per-Gaussian t* lower bound of the render binning
   sofk::DBuf<unsigned long long> r_stats;
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
@@ -226,6 +227,10 @@ void schedule_points_exact(sof_ctx* c, int view, int64_t n, const double* xyz_de
 void march(sof_ctx* c, const double* opacity_dev);
 void refine(sof_ctx* c, int64_t ne, const int32_t* edges_dev, double* verts_dev, int iterations,
             int strategies, int tile_size, int v0, int v1, uint64_t* counters);
+void refine_init(sof_ctx* c, int64_t ne, const int32_t* edges_dev);
+void refine_mid(sof_ctx* c, int64_t ne, uint8_t* ext_dev);
+void refine_update(sof_ctx* c, int64_t ne, const uint8_t* ext_dev);
+void refine_final(sof_ctx* c, int64_t ne, double* verts_dev);
 void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris,
               const int32_t* tris_dev, double weld_eps, double min_area);
 

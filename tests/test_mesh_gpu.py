@@ -135,3 +135,19 @@ def test_extract_delaunay_grid(ref):
     mesh = sof.extract_mesh(scene, views, sof.TetGrid(grid["vertices"], grid["tets"]))
     np.testing.assert_array_equal(bits(mesh.vertices), bits(full["vertices"]))
     np.testing.assert_array_equal(mesh.triangles, full["triangles"])
+
+
+def test_sharded_path_single_rank_matches_fused(ref, lattice_case):
+    """The view-sharded step (sharded.py over the device primitives) on one rank equals
+    the fused sof_extract bit for bit."""
+    import torch
+    from paper_2506_19139_b200.sharded import ShardedMesher
+    scene, cams, rc, views, verts, tets = lattice_case
+    views.ctx.set_tets(verts, tets)
+    fused = sof.extract_resident(views.ctx, sof.ExtractOptions(), {})
+    mesher = ShardedMesher(views.ctx, 0, 1)
+    st = {}
+    mesh = mesher.extract(sof.ExtractOptions(), st)
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(fused.vertices))
+    np.testing.assert_array_equal(mesh.triangles, fused.triangles)
+    torch.cuda.synchronize()
