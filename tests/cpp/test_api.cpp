@@ -1,0 +1,189 @@
+// The reference's own test cases (proj/tests/test_mesher.cpp, test_opacity_field.cpp),
+// rewritten against the drop-in C++ API include/sof_b200/sof.hpp. Compiled and run by
+// tests/test_cpp_api.py (GPU) with the in-repo GoogleTest / Eigen shims.
+#include <gtest/gtest.h>
+
+#include <algorithm>
+#include <random>
+
+#include "sof_b200/sof.hpp"
+
+using namespace sof;
+
+namespace {
+
+TetGrid single_tet(const std::array<double, 4>& opacity) {
+  TetGrid grid;
+  grid.vertices = {Vec3(0, 0, 0), Vec3(1, 0, 0), Vec3(0, 1, 0), Vec3(0, 0, 1)};
+  grid.tetrahedra = {{0, 1, 2, 3}};
+  grid.opacity.assign(opacity.begin(), opacity.end());
+  return grid;
+}
+
+Camera look_at(const Vec3& eye, const Vec3& target, const Vec3& up, double f, int res) {
+  Camera cam;
+  const Vec3 fwd = (target - eye).normalized();
+  const Vec3 right = fwd.cross(up).normalized();
+  const Vec3 down = fwd.cross(right);
+  cam.rotation.row(0) = right.transpose();
+  cam.rotation.row(1) = down.transpose();
+  cam.rotation.row(2) = fwd.transpose();
+  cam.translation = -cam.rotation * eye;
+  cam.fx = cam.fy = f;
+  cam.width = cam.height = res;
+  cam.cx = cam.cy = res * 0.5;
+  return cam;
+}
+
+std::vector<GaussianPrimitive> random_scene(unsigned seed, int count) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> up(-1, 1), us(0.05, 0.25), uo(0.4, 0.95);
+  std::normal_distribution<double> n(0, 1);
+  std::vector<GaussianPrimitive> out(count);
+  for (auto& g : out) {
+    g.position = Vec3(up(rng), up(rng), up(rng));
+    g.scale = Vec3(us(rng), us(rng), us(rng));
+    g.rotation = Quat(n(rng), n(rng), n(rng), n(rng)).normalized();
+    g.opacity = uo(rng);
+  }
+  return out;
+}
+
+TetGrid lattice(int n, double lo, double hi) {
+  TetGrid g;
+  const double h = (hi - lo) / (n - 1);
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) g.vertices.emplace_back(lo + i * h, lo + j * h, lo + k * h);
+  auto id = [n](int i, int j, int k) { return i + n * (j + n * k); };
+  for (int k = 0; k + 1 < n; ++k)
+    for (int j = 0; j + 1 < n; ++j)
+      for (int i = 0; i + 1 < n; ++i) {
+        const int a = id(i, j, k), b = id(i + 1, j, k), c = id(i + 1, j + 1, k), d = id(i + 1, j + 1, k + 1);
+        const int e = id(i, j + 1, k), f = id(i, j + 1, k + 1), gg = id(i, j, k + 1), hh = id(i + 1, j, k + 1);
+        g.tetrahedra.push_back({a, b, c, d});
+        g.tetrahedra.push_back({a, b, hh, d});
+        g.tetrahedra.push_back({a, e, c, d});
+        g.tetrahedra.push_back({a, e, f, d});
+        g.tetrahedra.push_back({a, gg, hh, d});
+        g.tetrahedra.push_back({a, gg, f, d});
+      }
+  return g;
+}
+
+}  // namespace
+
+TEST(MarchingTets, OneInsideCorner) {
+  const auto out = marching_tets(single_tet({0.4, 0.4, 0.4, 0.6}));
+  ASSERT_EQ(out.triangles.size(), 1u);
+  EXPECT_EQ(out.edges.size(), 3u);
+  for (const auto& e : out.edges) EXPECT_EQ(e.inside, 3);
+}
+
+TEST(MarchingTets, TwoInsideQuad) {
+  const auto out = marching_tets(single_tet({0.4, 0.4, 0.6, 0.6}));
+  EXPECT_EQ(out.triangles.size(), 2u);
+  EXPECT_EQ(out.edges.size(), 4u);
+}
+
+TEST(MarchingTets, NoCrossingNoOutput) {
+  EXPECT_TRUE(marching_tets(single_tet({0.6, 0.7, 0.8, 0.9})).triangles.empty());
+  EXPECT_TRUE(marching_tets(single_tet({0.1, 0.2, 0.3, 0.4})).triangles.empty());
+}
+
+TEST(MarchingTets, LinearInterpolation) {
+  const auto out = marching_tets(single_tet({0.4, 0.6, 0.4, 0.4}));
+  ASSERT_EQ(out.edges.size(), 3u);
+  for (size_t i = 0; i < out.edges.size(); ++i) {
+    const Vec3 mid = 0.5 * (Vec3(1, 0, 0) + single_tet({0, 0, 0, 0}).vertices[out.edges[i].outside]);
+    EXPECT_LT((out.vertices[i] - mid).norm(), 1e-12);
+  }
+}
+
+TEST(BinarySearchRefine, BisectionBound) {
+  auto grid = single_tet({0.6, 0.4, 0.4, 0.4});
+  auto out = marching_tets(grid);
+  const double crossing = 0.37;
+  binary_search_refine(out, grid, [&](const Vec3& p) { return p.x() < crossing; }, 8);
+  for (size_t i = 0; i < out.edges.size(); ++i) {
+    if (out.edges[i].outside != 1) continue;
+    EXPECT_NEAR(out.vertices[i].x(), crossing, 1.0 / 256.0);
+  }
+}
+
+TEST(AssembleMesh, WeldAndDegenerate) {
+  const std::vector<Vec3> verts{Vec3(0, 0, 0), Vec3(1, 0, 0), Vec3(0, 1, 0), Vec3(1 + 1e-9, 0, 0)};
+  const std::vector<std::array<int, 3>> tris{{0, 1, 2}, {0, 3, 2}, {0, 1, 3}};
+  const auto mesh = assemble_mesh(verts, tris);
+  EXPECT_EQ(mesh.vertices.size(), 3u);
+  EXPECT_EQ(mesh.triangles.size(), 2u);
+}
+
+TEST(AssembleMesh, EmptyInput) {
+  const auto mesh = assemble_mesh({}, {});
+  EXPECT_TRUE(mesh.vertices.empty());
+  EXPECT_TRUE(mesh.triangles.empty());
+}
+
+TEST(FieldEvaluator, SingleViewMahalanobisBall) {
+  GaussianPrimitive g;
+  g.scale = Vec3(0.3, 0.3, 0.3);
+  const std::vector<GaussianPrimitive> scene{g};
+  const ViewSet views = ViewSet::build(scene, {look_at(Vec3(0, 0, 3), Vec3::Zero(), Vec3(0, 1, 0), 0.4 * 64 * 3.0, 64)});
+  const FieldEvaluator eval(scene, views, EvalStrategies::all());
+  std::mt19937 rng(53);
+  std::uniform_real_distribution<double> u(-0.5, 0.5);
+  const double iso = std::sqrt(2.0 * std::log(2.0));
+  for (int i = 0; i < 200; ++i) {
+    const Vec3 x(u(rng), u(rng), u(rng));
+    const double mahal = x.norm() / 0.3;
+    if (std::abs(mahal - iso) < 0.02) continue;
+    if (views.cameras[0].to_view(x).z() >= 3.0) continue;
+    EXPECT_EQ(eval.classify_point(x), mahal < iso) << x.transpose();
+  }
+}
+
+TEST(FieldEvaluator, StrategiesAgreeAndReducePairs) {
+  const auto scene = random_scene(54, 40);
+  std::vector<Camera> cams;
+  for (int i = 0; i < 4; ++i) {
+    const double a = 2.0 * M_PI * i / 4;
+    cams.push_back(look_at(Vec3(4 * std::cos(a), 4 * std::sin(a), 0.5), Vec3::Zero(), Vec3(0, 0, 1), 60.0, 64));
+  }
+  const ViewSet views = ViewSet::build(scene, cams);
+  TetGrid grid = lattice(12, -1.3, 1.3);
+  const FieldEvaluator naive(scene, views, EvalStrategies::naive());
+  const FieldEvaluator fast(scene, views, EvalStrategies::all());
+  TetGrid g1 = grid, g2 = grid;
+  naive.label_grid(g1, true);
+  fast.label_grid(g2, true);
+  for (size_t i = 0; i < grid.vertices.size(); ++i) EXPECT_EQ(g1.opacity[i] >= 0.5, g2.opacity[i] >= 0.5);
+  EXPECT_GE(naive.counters().pairs, 2 * fast.counters().pairs);
+  ExtractOptions on, off;
+  off.strategies = EvalStrategies::naive();
+  const Mesh m1 = extract_mesh(scene, views, grid, on), m2 = extract_mesh(scene, views, grid, off);
+  ASSERT_EQ(m1.vertices.size(), m2.vertices.size());
+  ASSERT_GT(m1.triangles.size(), 0u);
+  for (size_t i = 0; i < m1.vertices.size(); ++i)
+    EXPECT_LT((m1.vertices[i] - m2.vertices[i]).cwiseAbs().maxCoeff(), 1e-9);
+}
+
+TEST(RenderDepthMap, SingleGaussianDisk) {
+  GaussianPrimitive g;
+  const std::vector<GaussianPrimitive> scene{g};
+  const Camera cam = look_at(Vec3(0, 0, -5), Vec3::Zero(), Vec3(0, 1, 0), 0.4 * 32 * 5.0 / 2.0, 32);
+  const ViewSet views = ViewSet::build(scene, {cam});
+  const auto exact = render_depth_map(views, 0, DepthMode::kExact);
+  const auto median = render_depth_map(views, 0, DepthMode::kMedian);
+  EXPECT_NEAR(exact.depth.at(16, 16), 3.82258, 0.01);
+  EXPECT_NEAR(median.depth.at(16, 16), 5.0, 0.01);
+  for (int y = 0; y < cam.height; ++y)
+    for (int x = 0; x < cam.width; ++x)
+      EXPECT_EQ(is_no_surface(exact.depth.at(x, y)), is_no_surface(median.depth.at(x, y)));
+}
+
+TEST(Errors, NonFiniteScene) {
+  GaussianPrimitive g;
+  g.position = Vec3(0, std::nan(""), 0);
+  EXPECT_THROW(ViewSet::build({g}, {Camera{}}), std::invalid_argument);
+}

@@ -1,0 +1,48 @@
+"""A short C3 meshing run for ncu captures (same scene, lattice and kernels as bench.py,
+with the views subsampled so a profiled run stays short).
+
+    python tools/profile_case.py --views 8 --steps 2
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2506_19139_b200 as sof  # noqa: E402
+from paper_2506_19139_b200.workloads import CONFIGS, kuhn_lattice, orbit_cameras, synthetic_scene  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--views", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--render", action="store_true", help="render one view instead of meshing")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    scene = synthetic_scene(cfg["gaussians"], int(args.config[1:]))
+    cams = orbit_cameras(cfg["views"], cfg["width"], cfg["height"])
+    cams = cams.subset(np.linspace(0, cfg["views"] - 1, args.views).astype(int))
+    ctx = sof.Context(0)
+    ctx.set_scene(scene)
+    ctx.set_views(cams)
+    if args.render:
+        views = sof.ViewSet(ctx, ctx.scene, ctx.cams, 0.0)
+        for _ in range(args.steps):
+            r = sof.render_view(views, 0)
+        print("render stats", r["stats"].tolist())
+        return
+    verts, tets = kuhn_lattice(cfg["lattice"])
+    ctx.set_tets(verts, tets)
+    for _ in range(args.steps):
+        st = {}
+        sof.extract_resident(ctx, sof.ExtractOptions(), st, fetch=False)
+    print({k: st[k] for k in ("ms_label", "ms_refine", "ms_eval_kernel", "pairs", "crossing_edges")})
+
+
+if __name__ == "__main__":
+    main()
