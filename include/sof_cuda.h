@@ -103,6 +103,8 @@ typedef struct sof_extract_stats {
   double ms_prep;            /* per-view records + Gaussian tile binning (K1, K2) */
   double ms_sched;           /* per-view point scheduling (K3) */
   uint64_t exact_pairs;      /* pairs the FP32 filter could not certify (evaluated in FP64) */
+  double host_ms_prep;       /* host time spent issuing per-view prep (incl. its one sync) */
+  double host_ms_sched;      /* host time spent issuing per-view scheduling */
 } sof_extract_stats;
 
 /* ---- context --------------------------------------------------------------- */

@@ -317,8 +317,8 @@ int sof_value_at(sof_ctx* c, int64_t n, const double* xyz, int strategies, int t
     check_points(n, xyz);
     upload(c, c->pts, xyz, 3 * n);
     c->min_op.ensure(std::max<int64_t>(n, 1));
-    std::vector<double> ones(n, 1.0);
-    upload(c, c->min_op, ones.data(), n);
+    fill_f64(c, c->min_op.p, n, 1.0);
+
     eval_views(c, 0, int(c->cams.size()), n, c->pts.p, strategies, tile_size, false, kModeValue,
                c->min_op.p, nullptr, nullptr, nullptr, nullptr, counters);
     download(c, out, c->min_op.p, n);
@@ -336,8 +336,8 @@ int sof_label_grid(sof_ctx* c, int64_t nv, const double* xyz, int strategies, in
     c->min_op.ensure(std::max<int64_t>(nv, 1));
     c->ext.ensure(std::max<int64_t>(nv, 1));
     c->grid_opacity.ensure(std::max<int64_t>(nv, 1));
-    std::vector<double> ones(nv, 1.0);
-    upload(c, c->min_op, ones.data(), nv);
+    fill_f64(c, c->min_op.p, nv, 1.0);
+
     SOF_CUDA(cudaMemsetAsync(c->ext.p, 0, nv, c->stream));
     eval_views(c, 0, int(c->cams.size()), nv, c->pts.p, strategies, tile_size, classify_mode != 0,
                kModeLabel, c->min_op.p, c->ext.p, nullptr, nullptr, nullptr, counters);
@@ -473,6 +473,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     const int64_t launches0 = c->launches;
     c->eval_launches = 0;
     c->exact_evals = 0;
+    c->host_ms[0] = c->host_ms[1] = 0.0;
     c->time_eval = stats != nullptr;
     if (c->time_eval) {
       double drop[kProfKinds];
@@ -487,8 +488,8 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     SOF_CUDA(cudaEventRecord(e[0], c->stream));
     // label_grid (extract.hpp:59-61): classification mode, views in order
     {
-      std::vector<double> ones(nv, 1.0);
-      upload(c, c->min_op, ones.data(), nv);
+      fill_f64(c, c->min_op.p, nv, 1.0);
+
     }
     SOF_CUDA(cudaMemsetAsync(c->ext.p, 0, nv, c->stream));
     uint64_t cl[2] = {0, 0}, cr[2] = {0, 0};
@@ -526,6 +527,8 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     st.ms_eval_kernel = pms[kProfEval];
     st.ms_prep = pms[kProfPrep];
     st.exact_pairs = c->exact_evals;
+    st.host_ms_prep = c->host_ms[0];
+    st.host_ms_sched = c->host_ms[1];
     st.ms_sched = pms[kProfSched];
     st.eval_launches = c->eval_launches;
     st.kernel_launches = c->launches - launches0;

@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 #include "sof_internal.h"
@@ -675,11 +676,14 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     const int tiles_x = (cam.w + tile_size - 1) / tile_size;
     const int tiles_y = (cam.h + tile_size - 1) / tile_size;
     const int T = tiled ? tiles_x * tiles_y : 1;
+    const auto h0 = std::chrono::steady_clock::now();
     const int p0 = prof_mark(c);
     const Rec* rec = view_records(c, v);
     const Binding* bd = tiled ? &view_binding(c, v, tile_size) : nullptr;
     const int p1 = prof_mark(c);
     prof_span(c, p0, p1, kProfPrep);
+    const auto h1 = std::chrono::steady_clock::now();
+    c->host_ms[0] += std::chrono::duration<double, std::milli>(h1 - h0).count();
     // K3: group the active, observed points of this view by tile (no host sync)
     const uint8_t* skip = (prune && (mode == kModeLabel || mode == kModeClassify)) ? ext : nullptr;
     s.tile_cnt.ensure(2 * (T + 1));
@@ -704,6 +708,8 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
                                                                c->d_scalar.p);
     SOF_LAUNCHED(c);
     prof_span(c, p1, prof_mark(c), kProfSched);
+    const auto h2 = std::chrono::steady_clock::now();
+    c->host_ms[1] += std::chrono::duration<double, std::milli>(h2 - h1).count();
     const int32_t* pidx = s.order.p;
     switch (mode) {
       case kModeLabel:

@@ -315,14 +315,16 @@ __global__ void __launch_bounds__(256) k_render(
   }
 }
 
-// Fallback for k-buffer overflow: one thread per pixel collects every contribution of
-// its tile list into a private global slice, insertion-sorts by (t*, index) and
-// renders exactly as above.
+// Fallback for k-buffer overflow: one thread per pixel emits its contributions in
+// exact (t*, index) order by repeated selection passes over its tile list — each pass
+// keeps the kSel smallest keys above the last emitted one — so no per-pixel storage
+// beyond kSel entries is needed however many Gaussians overlap the pixel.
+constexpr int kSel = 32;
+
 __global__ void k_render_fallback(Cam cam, int tiles_x, const int64_t* __restrict__ loff,
                                   const int32_t* __restrict__ lent, const Rec* __restrict__ recs,
                                   const double* __restrict__ dc, int exact_depth,
-                                  const int32_t* __restrict__ overflow, int64_t slice,
-                                  double* st, double* sa, int32_t* si, RenderOut out,
+                                  const int32_t* __restrict__ overflow, RenderOut out,
                                   unsigned long long* stats) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= overflow[0]) return;
@@ -331,42 +333,51 @@ __global__ void k_render_fallback(Cam cam, int tiles_x, const int64_t* __restric
   const int tile = (py / kRTile) * tiles_x + px / kRTile;
   double d[3];
   pixel_ray(cam, px, py, d);
-  double* t = st + k * slice;
-  double* a = sa + k * slice;
-  int32_t* ix = si + k * slice;
-  int m = 0;
-  for (int64_t e = loff[tile]; e < loff[tile + 1]; ++e) {
-    const Contrib c = contribution(recs[lent[e]], d, lent[e]);
-    if (!c.ok) continue;
-    int j = m++;
-    while (j > 0 && (t[j - 1] > c.t || (t[j - 1] == c.t && ix[j - 1] > c.idx))) {
-      t[j] = t[j - 1];
-      a[j] = a[j - 1];
-      ix[j] = ix[j - 1];
-      --j;
-    }
-    t[j] = c.t;
-    a[j] = c.alpha;
-    ix[j] = c.idx;
-  }
-  double T = 1.0, col[3] = {0.0, 0.0, 0.0}, depth = NAN;
+  const int64_t l0 = loff[tile], l1 = loff[tile + 1];
+  double st[kSel], sa[kSel];
+  int si[kSel];
+  double last_t = -INFINITY;
+  int last_i = -1;
+  double T = 1.0, col[3] = {0.0, 0.0, 0.0}, depth = NAN, med_t = 0.0, med_T = 1.0;
   bool found = false;
-  int med = -1;
-  double med_T = 1.0;
-  for (int j = 0; j < m; ++j) {
-    for (int q = 0; q < 3; ++q) col[q] = col[q] + dc[3 * ix[j] + q] * a[j] * T;
-    const double next = T * (1.0 - a[j]);
-    if (!found && T > 0.5 && next < 0.5) {
-      found = true;
-      med = j;
-      med_T = T;
+  int med_idx = -1;
+  for (;;) {
+    int m = 0;
+    for (int64_t e = l0; e < l1; ++e) {
+      const Contrib c = contribution(recs[lent[e]], d, lent[e]);
+      if (!c.ok) continue;
+      if (c.t < last_t || (c.t == last_t && c.idx <= last_i)) continue;  // already emitted
+      if (m == kSel && (c.t > st[m - 1] || (c.t == st[m - 1] && c.idx > si[m - 1]))) continue;
+      int j = (m < kSel) ? m++ : kSel - 1;
+      while (j > 0 && (st[j - 1] > c.t || (st[j - 1] == c.t && si[j - 1] > c.idx))) {
+        st[j] = st[j - 1];
+        sa[j] = sa[j - 1];
+        si[j] = si[j - 1];
+        --j;
+      }
+      st[j] = c.t;
+      sa[j] = c.alpha;
+      si[j] = c.idx;
     }
-    T = next;
+    for (int j = 0; j < m; ++j) {
+      for (int q = 0; q < 3; ++q) col[q] = col[q] + dc[3 * si[j] + q] * sa[j] * T;
+      const double next = T * (1.0 - sa[j]);
+      if (!found && T > 0.5 && next < 0.5) {
+        found = true;
+        med_idx = si[j];
+        med_t = st[j];
+        med_T = T;
+      }
+      T = next;
+    }
+    if (m < kSel) break;
+    last_t = st[m - 1];
+    last_i = si[m - 1];
   }
   if (found) {
-    depth = t[med];
+    depth = med_t;
     if (exact_depth) {
-      const Rec r = recs[ix[med]];
+      const Rec r = recs[med_idx];
       const double x = d[0], y = d[1], z = d[2];
       const double aa = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
                         2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
@@ -376,12 +387,16 @@ __global__ void k_render_fallback(Cam cam, int tiles_x, const int64_t* __restric
       if (disc < 0.0)
         atomicAdd(stats + 3, 1ull);
       else
-        depth = t[med] - sqrt(disc) / (2.0 * aa);
+        depth = med_t - sqrt(disc) / (2.0 * aa);
     }
   }
   double T2 = 1.0;
   if (!isnan(depth))
-    for (int j = 0; j < m; ++j) T2 *= 1.0 - alpha_at(recs[ix[j]], d, t[j], depth);
+    for (int64_t e = l0; e < l1; ++e) {
+      const Rec r = recs[lent[e]];
+      const Contrib c = contribution(r, d, lent[e]);
+      if (c.ok) T2 *= 1.0 - alpha_at(r, d, c.t, depth);
+    }
   out.depth[p] = depth;
   out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
   for (int q = 0; q < 3; ++q) out.rgb[3 * p + q] = col[q];
@@ -443,23 +458,10 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     SOF_LAUNCHED(c);
     const int32_t nover = read_scalar(c, c->r_overflow.p);
     if (nover > 0) {
-      // slice = the longest tile list
-      std::vector<int64_t> off(int64_t(tiles_x) * tiles_y + 1);
-      SOF_CUDA(cudaMemcpyAsync(off.data(), c->rbind.off.p, sizeof(int64_t) * off.size(),
-                               cudaMemcpyDeviceToHost, c->stream));
-      SOF_CUDA(cudaStreamSynchronize(c->stream));
-      int64_t slice = 1;
-      for (size_t t = 0; t + 1 < off.size(); ++t) slice = std::max(slice, off[t + 1] - off[t]);
-      DBuf<double> st, sa;
-      DBuf<int32_t> si;
-      st.ensure(size_t(nover) * slice);
-      sa.ensure(size_t(nover) * slice);
-      si.ensure(size_t(nover) * slice);
       k_render_fallback<<<grid_for(nover, 64), 64, 0, c->stream>>>(
           cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT,
-          c->r_overflow.p, slice, st.p, sa.p, si.p, out, c->r_stats.p);
+          c->r_overflow.p, out, c->r_stats.p);
       SOF_LAUNCHED(c);
-      SOF_CUDA(cudaStreamSynchronize(c->stream));
     }
     if (depth) SOF_CUDA(cudaMemcpyAsync(depth, out.depth, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
     if (opacity)

@@ -39,6 +39,17 @@ __global__ void k_fp64_peak(int iters, double seed, double* sink) {
   if (r == 12345.678) sink[0] = r;  // keep the chains live
 }
 
+__global__ void k_fill_f64(int64_t n, double* p, double v) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+void fill_f64(sof_ctx* c, double* p, int64_t n, double v) {
+  if (n <= 0) return;
+  k_fill_f64<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p, v);
+  SOF_LAUNCHED(c);
+}
+
 int prof_mark(sof_ctx* c) {
   if (!c->time_eval) return -1;
   if (c->evnext == c->evpool.size()) {

@@ -148,6 +148,7 @@ struct sof_ctx {
   sofk::DBuf<sofk::RecF> recf_scratch;
   int eval_path = 1;                      // 0: FP32 filter + exact FP64 replay, 1: FP64 only
   uint64_t exact_evals = 0;               // pairs that took the FP64 path (instrumentation)
+  double host_ms[4] = {0, 0, 0, 0};       // host time in per-view prep / scheduling (instrumentation)
   sofk::Binding bind_scratch;
 
   // binning scratch
@@ -235,6 +236,7 @@ void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris
               const int32_t* tris_dev, double weld_eps, double min_area);
 
 // ---- k_util.cu: phase timing -------------------------------------------------------------
+void fill_f64(sof_ctx* c, double* p, int64_t n, double v);
 int prof_mark(sof_ctx* c);                              // -1 when not profiling
 void prof_span(sof_ctx* c, int a, int b, int kind);
 void prof_collect(sof_ctx* c, double* ms_by_kind);      // syncs, sums, resets

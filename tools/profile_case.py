@@ -41,7 +41,8 @@ def main():
     for _ in range(args.steps):
         st = {}
         sof.extract_resident(ctx, sof.ExtractOptions(), st, fetch=False)
-    print({k: st[k] for k in ("ms_label", "ms_refine", "ms_eval_kernel", "pairs", "crossing_edges")})
+    print({k: st[k] for k in ("ms_label", "ms_refine", "ms_eval_kernel", "ms_prep", "ms_sched", "host_ms_prep",
+                               "host_ms_sched", "pairs", "crossing_edges", "kernel_launches")})
 
 
 if __name__ == "__main__":
