@@ -161,12 +161,52 @@ struct RenderOut {
   double* tfinal;
 };
 
-// One CTA per 16x16 tile; thread = pixel. Pass 1: exact streaming resort + blend +
-// median (+ exact depth); pass 2: opacity at depth.
+// Spill area of the pixels whose k-buffer overflows: a pixel of tile t owns the slice
+// [256 off[t] + lp len(t), +len(t)) of the pool (len(t) bounds its contributions),
+// written in collect mode and later sorted by t* with a segmented radix sort.
+struct Spill {
+  uint64_t* keys;      // double_key(t*)
+  int32_t* vals;       // Gaussian index
+  int64_t* begin;      // [slot] slice begin
+  int64_t* end;        // [slot] slice end (begin + count)
+  int32_t* pixel;      // [slot] pixel id
+  double* state;       // [slot][6] T, col[3], med_t, med_T
+  int32_t* istate;     // [slot][2] med_idx, found
+  int32_t* count;      // number of slots in use
+};
+
+__device__ __forceinline__ double opacity_at_depth(const Rec* __restrict__ recs,
+                                                   const int32_t* __restrict__ lent, int64_t l0,
+                                                   int64_t l1, const double* d, double depth) {
+  double T2 = 1.0;
+  for (int64_t e = l0; e < l1; ++e) {
+    const Rec r = recs[lent[e]];
+    const Contrib c = contribution(r, d, lent[e]);
+    if (c.ok) T2 *= 1.0 - alpha_at(r, d, c.t, depth);
+  }
+  return T2;
+}
+
+__device__ __forceinline__ double exact_depth_at(const Rec& r, const double* d, double med_t,
+                                                 double med_T, bool& fell_back) {
+  // exact_depth (opacity_field.hpp:157-166)
+  const double x = d[0], y = d[1], z = d[2];
+  const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
+                   2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
+  const double b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
+  const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * r.op));
+  const double disc = b * b - 4.0 * a * (r.c + lt);
+  fell_back = disc < 0.0;
+  return fell_back ? med_t : med_t - sqrt(disc) / (2.0 * a);
+}
+
+// One CTA per 16x16 tile; thread = pixel. Pass 1: exact streaming resort (k-buffer)
+// + blend + median (+ exact depth); pass 2: opacity at depth. A pixel whose k-buffer
+// would overflow switches to collect mode and is finished by k_render_finish.
 __global__ void __launch_bounds__(256) k_render(
     Cam cam, int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
     const Rec* __restrict__ recs, const double* __restrict__ lkey, const double* __restrict__ dc,
-    int exact_depth, RenderOut out, int32_t* overflow, unsigned long long* stats) {
+    int exact_depth, RenderOut out, Spill spill, unsigned long long* stats, int tile_base) {
   extern __shared__ __align__(16) unsigned char smem[];
   Rec* srec = reinterpret_cast<Rec*>(smem);
   double* sL = reinterpret_cast<double*>(srec + kRChunk);
@@ -174,7 +214,7 @@ __global__ void __launch_bounds__(256) k_render(
   double* bt = reinterpret_cast<double*>(sidx + kRChunk);  // [kKBuf][256]
   double* ba = bt + kKBuf * 256;
   int32_t* bi = reinterpret_cast<int32_t*>(ba + kKBuf * 256);
-  const int tile = blockIdx.x;
+  const int tile = tile_base + int(blockIdx.x);
   const int tid = threadIdx.x;
   const int px = (tile % tiles_x) * kRTile + (tid % kRTile);
   const int py = (tile / tiles_x) * kRTile + (tid / kRTile);
@@ -182,11 +222,13 @@ __global__ void __launch_bounds__(256) k_render(
   double d[3] = {0.0, 0.0, 1.0};
   if (valid) pixel_ray(cam, px, py, d);
   const int64_t l0 = loff[tile], l1 = loff[tile + 1];
+  const int64_t slice = 256 * (l0 - loff[tile_base]) + int64_t(tid) * (l1 - l0);
   double T = 1.0, col[3] = {0.0, 0.0, 0.0};
   int nbuf = 0;
-  bool found = false, over = false;
+  bool found = false, collect = false;
   int med_idx = -1;
   double med_t = 0.0, med_T = 1.0;
+  int64_t nspill = 0;
   unsigned long long tested = 0, contributing = 0;
 
   auto blend = [&](double t, double alpha, int idx) {
@@ -200,7 +242,6 @@ __global__ void __launch_bounds__(256) k_render(
     }
     T = next;
   };
-  // pops the (t, idx)-smallest buffered entry if its t < bound
   auto flush_below = [&](double bound) {
     while (nbuf > 0) {
       int m = 0;
@@ -217,10 +258,14 @@ __global__ void __launch_bounds__(256) k_render(
       bi[m * 256 + tid] = bi[nbuf * 256 + tid];
     }
   };
+  auto spill_one = [&](double t, int idx) {
+    spill.keys[slice + nspill] = double_key(t);
+    spill.vals[slice + nspill] = idx;
+    ++nspill;
+  };
 
-  bool live = valid;
   for (int64_t base = l0; base < l1; base += kRChunk) {
-    if (!__syncthreads_or(live)) break;
+    if (!__syncthreads_or(valid)) break;
     const int cnt = int(min(int64_t(kRChunk), l1 - base));
     for (int k = tid; k < cnt * 6; k += blockDim.x) {
       const int r = k / 6, q = k % 6;
@@ -232,46 +277,40 @@ __global__ void __launch_bounds__(256) k_render(
       }
     }
     __syncthreads();
-    if (live) {
+    if (valid) {
       for (int k = 0; k < cnt; ++k) {
-        flush_below(sL[k]);
+        if (!collect) flush_below(sL[k]);
         ++tested;
         const Contrib c = contribution(srec[k], d, sidx[k]);
         if (!c.ok) continue;
         ++contributing;
-        if (nbuf == kKBuf) {
-          over = true;
-          live = false;
-          break;
+        if (collect) {
+          spill_one(c.t, c.idx);
+        } else if (nbuf == kKBuf) {
+          // the buffered entries are not final yet: hand them and the rest of the
+          // list to the sort-based finish (blend state so far is kept)
+          collect = true;
+          for (int q = 0; q < nbuf; ++q) spill_one(bt[q * 256 + tid], bi[q * 256 + tid]);
+          nbuf = 0;
+          spill_one(c.t, c.idx);
+        } else {
+          bt[nbuf * 256 + tid] = c.t;
+          ba[nbuf * 256 + tid] = c.alpha;
+          bi[nbuf * 256 + tid] = c.idx;
+          ++nbuf;
         }
-        bt[nbuf * 256 + tid] = c.t;
-        ba[nbuf * 256 + tid] = c.alpha;
-        bi[nbuf * 256 + tid] = c.idx;
-        ++nbuf;
       }
     }
   }
-  if (valid && !over) flush_below(INFINITY);
+  if (valid && !collect) flush_below(INFINITY);
   double depth = NAN;
   bool fell_back = false;
-  if (valid && !over && found) {
+  if (valid && !collect && found) {
     depth = med_t;
-    if (exact_depth) {  // exact_depth (opacity_field.hpp:157-166)
-      const Rec r = recs[med_idx];
-      const double x = d[0], y = d[1], z = d[2];
-      const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
-                       2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
-      const double b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
-      const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * r.op));
-      const double disc = b * b - 4.0 * a * (r.c + lt);
-      if (disc < 0.0)
-        fell_back = true;
-      else
-        depth = med_t - sqrt(disc) / (2.0 * a);
-    }
+    if (exact_depth) depth = exact_depth_at(recs[med_idx], d, med_t, med_T, fell_back);
   }
-  // pass 2: O_N at the depth over all contributions (opacity_along_ray)
-  bool need2 = valid && !over && !isnan(depth);
+  // pass 2 (non-collect pixels): O_N at the depth over all contributions
+  const bool need2 = valid && !collect && !isnan(depth);
   double T2 = 1.0;
   for (int64_t base = l0; base < l1; base += kRChunk) {
     if (!__syncthreads_or(need2)) break;
@@ -293,8 +332,20 @@ __global__ void __launch_bounds__(256) k_render(
   }
   if (valid) {
     const int64_t p = int64_t(py) * cam.w + px;
-    if (over) {
-      overflow[1 + atomicAdd(overflow, 1)] = int32_t(p);
+    if (collect) {
+      const int s = atomicAdd(spill.count, 1);
+      spill.begin[s] = slice;
+      spill.end[s] = slice + nspill;
+      spill.pixel[s] = int32_t(p);
+      double* st = spill.state + 6 * s;
+      st[0] = T;
+      st[1] = col[0];
+      st[2] = col[1];
+      st[3] = col[2];
+      st[4] = med_t;
+      st[5] = med_T;
+      spill.istate[2 * s] = med_idx;
+      spill.istate[2 * s + 1] = found;
     } else {
       out.depth[p] = depth;
       out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
@@ -315,91 +366,62 @@ __global__ void __launch_bounds__(256) k_render(
   }
 }
 
-// Fallback for k-buffer overflow: one thread per pixel emits its contributions in
-// exact (t*, index) order by repeated selection passes over its tile list — each pass
-// keeps the kSel smallest keys above the last emitted one — so no per-pixel storage
-// beyond kSel entries is needed however many Gaussians overlap the pixel.
-constexpr int kSel = 32;
-
-__global__ void k_render_fallback(Cam cam, int tiles_x, const int64_t* __restrict__ loff,
-                                  const int32_t* __restrict__ lent, const Rec* __restrict__ recs,
-                                  const double* __restrict__ dc, int exact_depth,
-                                  const int32_t* __restrict__ overflow, RenderOut out,
-                                  unsigned long long* stats) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= overflow[0]) return;
-  const int64_t p = overflow[1 + k];
+// Resumes the blend of a collect-mode pixel over its t*-sorted spill slice. The sort
+// is stable on a key of t* alone; equal-t* runs are replayed in Gaussian-index order,
+// completing the reference's (t*, index) order (opacity_field.hpp:56-59).
+__global__ void k_render_finish(Cam cam, int tiles_x, const int64_t* __restrict__ loff,
+                                const int32_t* __restrict__ lent, const Rec* __restrict__ recs,
+                                const double* __restrict__ dc, int exact_depth, Spill spill,
+                                const uint64_t* __restrict__ skeys, const int32_t* __restrict__ svals,
+                                RenderOut out, unsigned long long* stats) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= *spill.count) return;
+  const int64_t p = spill.pixel[s];
   const int px = int(p % cam.w), py = int(p / cam.w);
   const int tile = (py / kRTile) * tiles_x + px / kRTile;
   double d[3];
   pixel_ray(cam, px, py, d);
-  const int64_t l0 = loff[tile], l1 = loff[tile + 1];
-  double st[kSel], sa[kSel];
-  int si[kSel];
-  double last_t = -INFINITY;
-  int last_i = -1;
-  double T = 1.0, col[3] = {0.0, 0.0, 0.0}, depth = NAN, med_t = 0.0, med_T = 1.0;
-  bool found = false;
-  int med_idx = -1;
-  for (;;) {
-    int m = 0;
-    for (int64_t e = l0; e < l1; ++e) {
-      const Contrib c = contribution(recs[lent[e]], d, lent[e]);
-      if (!c.ok) continue;
-      if (c.t < last_t || (c.t == last_t && c.idx <= last_i)) continue;  // already emitted
-      if (m == kSel && (c.t > st[m - 1] || (c.t == st[m - 1] && c.idx > si[m - 1]))) continue;
-      int j = (m < kSel) ? m++ : kSel - 1;
-      while (j > 0 && (st[j - 1] > c.t || (st[j - 1] == c.t && si[j - 1] > c.idx))) {
-        st[j] = st[j - 1];
-        sa[j] = sa[j - 1];
-        si[j] = si[j - 1];
-        --j;
-      }
-      st[j] = c.t;
-      sa[j] = c.alpha;
-      si[j] = c.idx;
-    }
-    for (int j = 0; j < m; ++j) {
-      for (int q = 0; q < 3; ++q) col[q] = col[q] + dc[3 * si[j] + q] * sa[j] * T;
-      const double next = T * (1.0 - sa[j]);
+  const double* st = spill.state + 6 * s;
+  double T = st[0], col[3] = {st[1], st[2], st[3]}, med_t = st[4], med_T = st[5];
+  int med_idx = spill.istate[2 * s];
+  bool found = spill.istate[2 * s + 1];
+  const int64_t b = spill.begin[s], e = spill.end[s];
+  int64_t j = b;
+  while (j < e) {
+    int64_t r = j + 1;
+    while (r < e && skeys[r] == skeys[j]) ++r;  // run of equal t*
+    int last = -1;
+    for (int64_t q = j; q < r; ++q) {  // replay the run in index order
+      int nxt = 0x7fffffff;
+      for (int64_t u = j; u < r; ++u)
+        if (svals[u] > last && svals[u] < nxt) nxt = svals[u];
+      last = nxt;
+      const Contrib c = contribution(recs[nxt], d, nxt);
+      for (int k = 0; k < 3; ++k) col[k] = col[k] + dc[3 * nxt + k] * c.alpha * T;
+      const double next = T * (1.0 - c.alpha);
       if (!found && T > 0.5 && next < 0.5) {
         found = true;
-        med_idx = si[j];
-        med_t = st[j];
+        med_idx = nxt;
+        med_t = c.t;
         med_T = T;
       }
       T = next;
     }
-    if (m < kSel) break;
-    last_t = st[m - 1];
-    last_i = si[m - 1];
+    j = r;
   }
+  double depth = NAN;
   if (found) {
     depth = med_t;
     if (exact_depth) {
-      const Rec r = recs[med_idx];
-      const double x = d[0], y = d[1], z = d[2];
-      const double aa = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
-                        2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
-      const double bb = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
-      const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * r.op));
-      const double disc = bb * bb - 4.0 * aa * (r.c + lt);
-      if (disc < 0.0)
-        atomicAdd(stats + 3, 1ull);
-      else
-        depth = med_t - sqrt(disc) / (2.0 * aa);
+      bool fb = false;
+      depth = exact_depth_at(recs[med_idx], d, med_t, med_T, fb);
+      if (fb) atomicAdd(stats + 3, 1ull);
     }
   }
-  double T2 = 1.0;
-  if (!isnan(depth))
-    for (int64_t e = l0; e < l1; ++e) {
-      const Rec r = recs[lent[e]];
-      const Contrib c = contribution(r, d, lent[e]);
-      if (c.ok) T2 *= 1.0 - alpha_at(r, d, c.t, depth);
-    }
+  const double T2 = isnan(depth) ? 1.0 : opacity_at_depth(recs, lent, loff[tile], loff[tile + 1], d, depth);
   out.depth[p] = depth;
   out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
-  for (int q = 0; q < 3; ++q) out.rgb[3 * p + q] = col[q];
+  for (int k = 0; k < 3; ++k) out.rgb[3 * p + k] = col[k];
   out.tfinal[p] = T;
 }
 
@@ -418,6 +440,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     const Cam& cam = c->cams[view];
     const int ts = kRTile;
     const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
+    const int64_t T = int64_t(tiles_x) * tiles_y;
     const int64_t n = c->n, P = int64_t(cam.w) * cam.h;
     const Rec* rec = view_records(c, view);
     c->rect.ensure(std::max<int64_t>(n, 1));
@@ -432,18 +455,27 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
         n, c->gstat.p, cam, ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p,
         c->r_lkey.p);
     SOF_LAUNCHED(c);
-    if (n > 0) bin_by_key(c, view, ts, tiles_x, tiles_y, c->rbind, false);
-    else {
-      c->rbind.off.ensure(int64_t(tiles_x) * tiles_y + 1);
-      SOF_CUDA(cudaMemsetAsync(c->rbind.off.p, 0, sizeof(int64_t) * (int64_t(tiles_x) * tiles_y + 1),
-                               c->stream));
+    if (n > 0) {
+      bin_by_key(c, view, ts, tiles_x, tiles_y, c->rbind, false);
+    } else {
+      c->rbind.off.ensure(T + 1);
+      SOF_CUDA(cudaMemsetAsync(c->rbind.off.p, 0, sizeof(int64_t) * (T + 1), c->stream));
       c->rbind.ent.ensure(1);
+      c->rbind.entries = 0;
     }
     c->r_out.ensure(6 * P);
     RenderOut out{c->r_out.p, c->r_out.p + P, c->r_out.p + 2 * P, c->r_out.p + 5 * P};
-    c->r_overflow.ensure(P + 1);
+    // Spill pool: a pixel of tile t may need len(t) slots, so a band of tiles [t0, t1)
+    // needs 256 (off[t1] - off[t0]). Tiles are rendered in bands whose pool fits both
+    // the 2^31-item limit of the segmented sort and a 24 GB memory cap.
+    std::vector<int64_t> off(T + 1, 0);
+    if (n > 0)
+      SOF_CUDA(cudaMemcpyAsync(off.data(), c->rbind.off.p, sizeof(int64_t) * (T + 1),
+                               cudaMemcpyDeviceToHost, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+    const int64_t cap = std::min<int64_t>((int64_t(1) << 31) - 1, (int64_t(24) << 30) / 24);
+    RenderScratch& rs = c->rs;
     c->r_stats.ensure(4);
-    SOF_CUDA(cudaMemsetAsync(c->r_overflow.p, 0, sizeof(int32_t), c->stream));
     SOF_CUDA(cudaMemsetAsync(c->r_stats.p, 0, 4 * sizeof(unsigned long long), c->stream));
     const size_t smem = kRChunk * (sizeof(Rec) + sizeof(double) + sizeof(int32_t)) +
                         size_t(kKBuf) * 256 * (2 * sizeof(double) + sizeof(int32_t));
@@ -452,17 +484,49 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       SOF_CUDA(cudaFuncSetAttribute(k_render, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       attr_set = true;
     }
-    k_render<<<tiles_x * tiles_y, 256, smem, c->stream>>>(
-        cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->r_lkey.p, c->dc.p,
-        depth_mode == SOF_DEPTH_EXACT, out, c->r_overflow.p, c->r_stats.p);
-    SOF_LAUNCHED(c);
-    const int32_t nover = read_scalar(c, c->r_overflow.p);
-    if (nover > 0) {
-      k_render_fallback<<<grid_for(nover, 64), 64, 0, c->stream>>>(
-          cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT,
-          c->r_overflow.p, out, c->r_stats.p);
+    int64_t nover_total = 0;
+    for (int64_t t0 = 0; t0 < T;) {
+      int64_t t1 = t0 + 1;  // always at least one tile
+      while (t1 < T && 256 * (off[t1 + 1] - off[t0]) <= cap) ++t1;
+      const int64_t pool = std::max<int64_t>(256 * (off[t1] - off[t0]), 1);
+      if (pool > cap) throw InvalidArg("a single render tile's list exceeds the spill pool");
+      const int64_t bpx = (t1 - t0) * 256;
+      rs.keys.ensure(pool);
+      rs.keys2.ensure(pool);
+      rs.vals.ensure(pool);
+      rs.vals2.ensure(pool);
+      rs.begin.ensure(bpx);
+      rs.end.ensure(bpx);
+      rs.pixel.ensure(bpx);
+      rs.state.ensure(6 * bpx);
+      rs.istate.ensure(2 * bpx);
+      rs.count.ensure(1);
+      SOF_CUDA(cudaMemsetAsync(rs.count.p, 0, sizeof(int32_t), c->stream));
+      Spill spill{rs.keys.p, rs.vals.p, rs.begin.p, rs.end.p, rs.pixel.p, rs.state.p, rs.istate.p, rs.count.p};
+      k_render<<<unsigned(t1 - t0), 256, smem, c->stream>>>(
+          cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->r_lkey.p, c->dc.p,
+          depth_mode == SOF_DEPTH_EXACT, out, spill, c->r_stats.p, int(t0));
       SOF_LAUNCHED(c);
+      const int32_t nover = read_scalar(c, rs.count.p);
+      if (nover > 0) {
+        size_t bytes = 0;
+        SOF_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, rs.keys.p, rs.keys2.p, rs.vals.p,
+                                                           rs.vals2.p, pool, nover, rs.begin.p, rs.end.p,
+                                                           c->stream));
+        c->cub_tmp.ensure(bytes);
+        SOF_CUDA(cub::DeviceSegmentedSort::StableSortPairs(c->cub_tmp.p, bytes, rs.keys.p, rs.keys2.p,
+                                                           rs.vals.p, rs.vals2.p, pool, nover, rs.begin.p,
+                                                           rs.end.p, c->stream));
+        c->launches += 3;
+        k_render_finish<<<grid_for(nover, 64), 64, 0, c->stream>>>(
+            cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT,
+            spill, rs.keys2.p, rs.vals2.p, out, c->r_stats.p);
+        SOF_LAUNCHED(c);
+      }
+      nover_total += nover;
+      t0 = t1;
     }
+    const int64_t nover = nover_total;
     if (depth) SOF_CUDA(cudaMemcpyAsync(depth, out.depth, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
     if (opacity)
       SOF_CUDA(cudaMemcpyAsync(opacity, out.opacity, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));

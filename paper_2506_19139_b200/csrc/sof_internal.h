@@ -111,6 +111,14 @@ struct MeshScratch {
   DBuf<int32_t> p0, p1, whead, wrun, wrun_first, first_of, wfirst, nid, rt, keep, pos;
 };
 
+// Render spill pool (k_render.cu): keys / values double-buffered for the segmented sort.
+struct RenderScratch {
+  DBuf<uint64_t> keys, keys2;
+  DBuf<int32_t> vals, vals2, pixel, istate, count;
+  DBuf<int64_t> begin, end;
+  DBuf<double> state;
+};
+
 enum ProfKind { kProfEval = 0, kProfPrep = 1, kProfSched = 2, kProfKinds = 4 };
 
 enum EvalMode { kModeLabel = 0, kModeClassify = 1, kModeView = 2, kModeValue = 3 };
@@ -163,7 +171,7 @@ struct sof_ctx {
   sofk::PointSchedule sched;
   sofk::MeshScratch ms;
   sofk::Binding rbind;                    // render binding (lists ordered by a t* lower bound)
-  sofk::DBuf<int32_t> r_overflow;         // [0] count, then overflow pixel ids
+  sofk::RenderScratch rs;                 // spill pool of k-buffer-overflow pixels
   sofk::DBuf<double> r_out;               // depth, opacity, rgb(3), t_final per pixel
   sofk::DBuf<double> r_lkey;              // per-Gaussian t* lower bound of the render binning
   sofk::DBuf<unsigned long long> r_stats;

@@ -32,9 +32,14 @@ def main():
     ctx.set_views(cams)
     if args.render:
         views = sof.ViewSet(ctx, ctx.scene, ctx.cams, 0.0)
+        import time
         for _ in range(args.steps):
+            t0 = time.perf_counter()
             r = sof.render_view(views, 0)
-        print("render stats", r["stats"].tolist())
+            dt = time.perf_counter() - t0
+        w, h = (int(x) for x in cams.wh[0])
+        print(f"render {w}x{h}: {dt * 1e3:.1f} ms ({w * h / dt / 1e6:.1f} Mpix/s) stats "
+              f"[tested, contributing, sorted-path pixels, exact-depth fallbacks] = {r['stats'].tolist()}")
         return
     verts, tets = kuhn_lattice(cfg["lattice"])
     ctx.set_tets(verts, tets)
