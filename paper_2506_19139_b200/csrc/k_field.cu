@@ -369,7 +369,7 @@ constexpr int kChunk = 32;  // Gaussian records staged in shared memory per step
 // list is streamed through shared memory in chunks; every thread runs the exact
 // view_opacity loop (field_eval.hpp:86-108) for its point.
 template <int MODE, bool TILED>
-__global__ void __launch_bounds__(256) k_eval(
+__global__ void __launch_bounds__(256, 6) k_eval(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks,
     const int32_t* __restrict__ pidx, const double* __restrict__ xyz, Cam cam, int ts,
     int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
@@ -403,8 +403,8 @@ __global__ void __launch_bounds__(256) k_eval(
   for (int64_t base = l0; base < l1; base += kChunk) {
     if (!__syncthreads_or(!done)) break;
     const int cnt = int(std::min<int64_t>(kChunk, l1 - base));
-    for (int k = threadIdx.x; k < cnt * 6; k += blockDim.x) {
-      const int r = k / 6, q = k % 6;
+    for (int k = threadIdx.x; k < cnt * kRecV2; k += blockDim.x) {
+      const int r = k / kRecV2, q = k % kRecV2;
       const int64_t g = TILED ? int64_t(lent[base + r]) : base + r;
       reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
     }

@@ -267,8 +267,8 @@ __global__ void __launch_bounds__(256) k_render(
   for (int64_t base = l0; base < l1; base += kRChunk) {
     if (!__syncthreads_or(valid)) break;
     const int cnt = int(min(int64_t(kRChunk), l1 - base));
-    for (int k = tid; k < cnt * 6; k += blockDim.x) {
-      const int r = k / 6, q = k % 6;
+    for (int k = tid; k < cnt * kRecV2; k += blockDim.x) {
+      const int r = k / kRecV2, q = k % kRecV2;
       const int32_t g = lent[base + r];
       reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
       if (q == 0) {
@@ -315,8 +315,8 @@ __global__ void __launch_bounds__(256) k_render(
   for (int64_t base = l0; base < l1; base += kRChunk) {
     if (!__syncthreads_or(need2)) break;
     const int cnt = int(min(int64_t(kRChunk), l1 - base));
-    for (int k = tid; k < cnt * 6; k += blockDim.x) {
-      const int r = k / 6, q = k % 6;
+    for (int k = tid; k < cnt * kRecV2; k += blockDim.x) {
+      const int r = k / kRecV2, q = k % kRecV2;
       const int32_t g = lent[base + r];
       reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
       if (q == 0) sidx[r] = g;

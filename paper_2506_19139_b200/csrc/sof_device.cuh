@@ -29,15 +29,19 @@ struct Cam {
 };
 
 // Per-(Gaussian, view) record used by the opacity evaluation:
-// PrecomputedGaussian minus tight_bound (precompute.hpp:21-28). 96 B, 16-B aligned.
+// PrecomputedGaussian minus tight_bound (precompute.hpp:21-28), plus the exponent
+// threshold below which alpha < 1/255 is certain. 112 B, 16-B aligned.
 struct __align__(16) Rec {
   double ic[6];  // inv_cov upper triangle xx xy xz yy yz zz
   double b[3];   // b_vec
   double c;      // c_scalar
   double op;     // filtered opacity
   double zmin;   // min_z
+  double thr;    // log(1/(255 op)) - 1e-9 (1 + |.|): exponent < thr => alpha < 1/255
+  double pad;
 };
-static_assert(sizeof(Rec) == 96, "record layout");
+static_assert(sizeof(Rec) == 112, "record layout");
+constexpr int kRecV2 = int(sizeof(Rec) / 16);  // double2 per record
 
 // FP32 filter record (64 B): a rounded copy of Rec plus error-bound constants.
 // It only decides which pairs are PROVABLY skipped by the reference's tests
@@ -209,6 +213,16 @@ __host__ __device__ inline void gauss_view(const GaussStatic& g, const Cam& cam,
   const double czz = wc[0] * cam.R[6] + wc[1] * cam.R[7] + wc[2] * cam.R[8];
   const double zc = to_view_c(cam, 2, g.pos[0], g.pos[1], g.pos[2]);
   r.zmin = zc - g.E * sqrt(czz);
+  // alpha = op exp(arg) < 1/255 whenever arg < log(1/(255 op)); the 1e-9 relative
+  // margin dwarfs the ulp-level error of exp and of the product, so skipping the exp
+  // below thr never changes a decision (field_eval.hpp:100-101, opacity_field.hpp:98-99)
+  if (r.op > 0.0) {
+    const double L = -log(255.0 * r.op);
+    r.thr = L - 1e-9 * (1.0 + fabs(L));
+  } else {
+    r.thr = 1e300;
+  }
+  r.pad = 0.0;
 }
 
 // x86-64 cvttsd2si semantics for int(x) (out of range / NaN -> INT_MIN), the
@@ -311,10 +325,19 @@ __device__ __forceinline__ double pair_alpha(const Rec& r, const double* d, doub
   const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
                    2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
   const double b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
-  const double t_star = -b / (2.0 * a);          // peak_t gaussian.hpp:52
-  const double te = (t < t_star) ? t : t_star;   // std::min(t_star, t)
-  if (te <= 0.0) return 0.0;
+  const double two_a = 2.0 * a;
+  double te;
+  if (a > 0.0 && __fma_rn(two_a, t, b) < 0.0) {
+    // 2 a t + b < 0 exactly (the sign of a correctly rounded fma is exact), so
+    // t* = -b / (2a) > t and min(fl(t*), t) = t: the IEEE division is not needed
+    te = t;
+  } else {
+    const double t_star = -b / two_a;           // peak_t gaussian.hpp:52
+    te = (t < t_star) ? t : t_star;             // std::min(t_star, t)
+    if (te <= 0.0) return 0.0;
+  }
   const double arg = -0.5 * ((a * te + b) * te + r.c);  // eval_1d gaussian.hpp:47-49
+  if (arg < r.thr) return 0.0;                          // alpha < 1/255 certain
   double alpha = r.op * sof_exp(arg);
   if (alpha < kMinAlpha) return 0.0;
   return (kMaxAlpha < alpha) ? kMaxAlpha : alpha;  // std::min(alpha, kMaxAlpha)
