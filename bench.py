@@ -33,10 +33,13 @@ sys.path.insert(0, ROOT)
 
 ITER = 8  # refine_iterations (extract.hpp:16)
 # algorithmic FP64 FLOPs of one evaluated (point, Gaussian) pair of view_opacity
-# (field_eval.hpp:95-103): abc_cached 24 (A: 13 mul + 5 add, B: 4 mul + 2 add),
-# peak_t 2, eval_1d argument 5, alpha 1, survive update 2 -> 34; the exp and the
-# IEEE division are counted as one FLOP each -> 36.
-FLOP_PER_PAIR = 36.0
+# (field_eval.hpp:95-103) as the bit-exact reference arithmetic performs it:
+# abc_cached 24 (A: 13 mul + 5 add, B: 4 mul + 2 add), peak_t 2 + IEEE division ~8,
+# eval_1d argument 5, exp (sof_exp: rint-scaled reduction 6, 13-term Horner 24,
+# reconstruction 2) 32, alpha / clamp / survive 5 -> 76. The kernel
+# skips the division and the exp where it can prove them irrelevant, so this is the
+# algorithmic (reference) work, not the executed instruction count.
+FLOP_PER_PAIR = 76.0
 
 
 def env_int(k, d):
