@@ -101,6 +101,8 @@ int sof_ctx_create(int device, sof_ctx** out) {
     SOF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     SOF_CUDA(cudaEventCreate(&c->ev0));
     SOF_CUDA(cudaEventCreate(&c->ev1));
+    SOF_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    for (auto& e : c->prep_ev) SOF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t free_b = 0, total_b = 0;
     SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
     // per-view record / binding caches may take up to half of the free HBM
@@ -120,6 +122,15 @@ void sof_ctx_destroy(sof_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (auto e : ctx->prep_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : ctx->evpool) cudaEventDestroy(e);
+  for (auto e : ctx->user_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream2) {
+    cudaStreamSynchronize(ctx->stream2);
+    cudaStreamDestroy(ctx->stream2);
+  }
   cudaStream_t s = ctx->stream;
   delete ctx;
   if (s) cudaStreamDestroy(s);

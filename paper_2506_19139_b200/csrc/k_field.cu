@@ -7,6 +7,7 @@
 // label_grid (field_eval.hpp:59-176). Compiled with --fmad=false: every FP64
 // expression is the reference's, so values and decisions are bit-identical.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <chrono>
@@ -101,7 +102,10 @@ void scene_prep(sof_ctx* c) {
 void mark_views_stale(sof_ctx* c) {
   c->rec_valid.assign(c->cams.size(), 0);
   for (auto& b : c->bindings) b.view = -1;
-  c->bind_scratch.view = -1;
+  for (int k = 0; k < 2; ++k) {
+    c->bind_scratch[k].view = -1;
+    c->scratch_view[k] = -1;
+  }
   c->cache_bytes = 0;
 }
 
@@ -122,11 +126,15 @@ void invalidate_view_caches(sof_ctx* c) {
 const Rec* view_records(sof_ctx* c, int view) {
   if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
   if (c->rec_valid[view]) return c->recs[view].p;
+  const int sel = c->scratch_sel;
+  if (c->scratch_view[sel] == view) return c->rec_scratch[sel].p;
   const bool with_f = c->eval_path == 0;  // float filter records only for the FP32 path
   const size_t bytes = size_t(c->n) * (sizeof(Rec) + (with_f ? sizeof(RecF) : 0));
-  DBuf<Rec>* dst = &c->rec_scratch;
-  DBuf<RecF>* dstf = &c->recf_scratch;
+  DBuf<Rec>* dst = &c->rec_scratch[sel];
+  DBuf<RecF>* dstf = &c->recf_scratch[sel];
+  c->scratch_view[sel] = view;
   if (c->cache_bytes + bytes <= c->cache_budget) {
+    c->scratch_view[sel] = -1;
     dst = &c->recs[view];
     dstf = &c->recfs[view];
     c->cache_bytes += bytes;
@@ -144,7 +152,8 @@ const Rec* view_records(sof_ctx* c, int view) {
 
 // Float filter records of `view`, valid after view_records(c, view).
 const RecF* view_recf(sof_ctx* c, int view) {
-  return c->rec_valid[view] ? c->recfs[view].p : c->recf_scratch.p;
+  if (c->rec_valid[view]) return c->recfs[view].p;
+  return c->recf_scratch[c->scratch_view[0] == view ? 0 : 1].p;
 }
 
 // ---- K2: Gaussian tile binning ------------------------------------------------------------------
@@ -250,11 +259,11 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
   SOF_LAUNCHED(c);
   exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, n + 1);
   const int64_t M = read_scalar(c, c->goff.p + n);
-  if (charge_cache && &b != &c->bind_scratch) {
+  if (charge_cache && &b != &c->bind_scratch[0] && &b != &c->bind_scratch[1]) {
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
     if (c->cache_bytes + bytes > c->cache_budget) {
-      build_binding_tail(c, view, ts, c->bind_scratch, M, T, tiles_x, tiles_y);
+      build_binding_tail(c, view, ts, c->bind_scratch[c->scratch_sel], M, T, tiles_x, tiles_y);
       return;
     }
     c->cache_bytes += bytes;
@@ -290,11 +299,13 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
 const Binding& view_binding(sof_ctx* c, int view, int tile_size) {
   Binding& cached = c->bindings[view];
   if (cached.view == view && cached.tile_size == tile_size) return cached;
-  if (c->bind_scratch.view == view && c->bind_scratch.tile_size == tile_size) return c->bind_scratch;
+  for (int k = 0; k < 2; ++k)
+    if (c->bind_scratch[k].view == view && c->bind_scratch[k].tile_size == tile_size)
+      return c->bind_scratch[k];
   // builds into the per-view slot (kept for the rest of the step) or, past the
   // cache budget, into the scratch slot
   build_binding(c, view, tile_size, cached);
-  return (cached.view == view) ? cached : c->bind_scratch;
+  return (cached.view == view) ? cached : c->bind_scratch[c->scratch_sel];
 }
 
 // ---- K3: point scheduling ------------------------------------------------------------------------
@@ -320,25 +331,37 @@ __device__ __forceinline__ int warp_tile_add(int* counters, int tile, bool valid
 }
 
 // Per point: tile of the view (-1 when pruned or unobserved), histogram per tile.
-__global__ void k_sched_tile(int64_t n, const double* __restrict__ xyz, Cam cam, int ts,
-                             int tiles_x, bool single_bin, const uint8_t* __restrict__ skip,
-                             int32_t* tile_of, int* tile_cnt) {
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+// Candidates are all points (cand == nullptr) or a compacted list of the points not
+// yet pruned; tile_of is indexed by candidate slot.
+__global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
+                             const double* __restrict__ xyz, Cam cam, int ts, int tiles_x,
+                             bool single_bin, const uint8_t* __restrict__ skip, int32_t* tile_of,
+                             int* tile_cnt) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   int tile = -1;
-  if (i < n && !(skip && skip[i])) {
-    const PointRay pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
-    if (pr.observed) tile = single_bin ? 0 : pr.tile;
+  if (k < n) {
+    const int64_t i = cand ? cand[k] : k;
+    if (!(skip && skip[i])) {
+      const PointRay pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+      if (pr.observed) tile = single_bin ? 0 : pr.tile;
+    }
+    tile_of[k] = tile;
   }
-  if (i < n) tile_of[i] = tile;
   warp_tile_add(tile_cnt, tile, tile >= 0);
 }
 
-__global__ void k_sched_scatter(int64_t n, const int32_t* __restrict__ tile_of,
+struct NotPruned {
+  const uint8_t* ext;
+  __device__ bool operator()(int32_t i) const { return ext[i] == 0; }
+};
+
+__global__ void k_sched_scatter(int64_t n, const int32_t* __restrict__ cand,
+                                const int32_t* __restrict__ tile_of,
                                 const int* __restrict__ tile_off, int* tile_cur, int32_t* order) {
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int tile = (i < n) ? tile_of[i] : -1;
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int tile = (k < n) ? tile_of[k] : -1;
   const int slot = warp_tile_add(tile_cur, tile, tile >= 0);
-  if (tile >= 0) order[tile_off[tile] + slot] = int32_t(i);
+  if (tile >= 0) order[tile_off[tile] + slot] = cand ? cand[k] : int32_t(k);
 }
 
 // One thread per tile: blocks per tile; an exclusive scan of these gives block ids.
@@ -369,7 +392,7 @@ constexpr int kChunk = 32;  // Gaussian records staged in shared memory per step
 // list is streamed through shared memory in chunks; every thread runs the exact
 // view_opacity loop (field_eval.hpp:86-108) for its point.
 template <int MODE, bool TILED>
-__global__ void __launch_bounds__(256, 6) k_eval(
+__global__ void __launch_bounds__(256, 5) k_eval(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks,
     const int32_t* __restrict__ pidx, const double* __restrict__ xyz, Cam cam, int ts,
     int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
@@ -396,6 +419,8 @@ __global__ void __launch_bounds__(256, 6) k_eval(
   }
   const bool dead_cull = strategies & 16, use_min_z = strategies & 2;
   const bool early = classify && (strategies & 4);
+  const float cu = float(pr.px), cv = float(pr.py);
+  const float cuu = cu * cu, cvv = cv * cv, cuv = cu * cv;
   double survive = 1.0;
   bool complete = true;
   bool done = !active;
@@ -421,6 +446,7 @@ __global__ void __launch_bounds__(256, 6) k_eval(
           continue;
         }
         ++pairs;
+        if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
         const double alpha = pair_alpha(r, pr.d, pr.t);
         if (alpha == 0.0) continue;
         survive *= 1.0 - alpha;
@@ -671,17 +697,44 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     k_fill_view_outputs<<<grid_for(n, 256), 256, 0, c->stream>>>(n, o_out, obs_out, comp_out);
     SOF_LAUNCHED(c);
   }
+  // Per-view preprocessing (K1 records + K2 tile binding) runs on the prep lane
+  // (second stream, own CUB scratch), one view ahead of the evaluation: the host
+  // issues view v's schedule + eval, then prepares view v + 1 (its one size readback
+  // blocks only the host) while the GPU evaluates view v.
+  int64_t ncand = n;      // candidate points of the next view
+  bool use_list = false;  // candidates = s.active[0, ncand) instead of all points
+  const Rec* prep_rec[2] = {nullptr, nullptr};
+  const Binding* prep_bd[2] = {nullptr, nullptr};
+  auto prep_view = [&](int pv) {
+    std::swap(c->stream, c->stream2);
+    c->cub_tmp.swap(c->cub_tmp2);
+    c->scratch_sel = pv & 1;
+    try {
+      const int p0 = prof_mark(c);
+      prep_rec[pv & 1] = view_records(c, pv);
+      prep_bd[pv & 1] = tiled ? &view_binding(c, pv, tile_size) : nullptr;
+      prof_span(c, p0, prof_mark(c), kProfPrep);
+      SOF_CUDA(cudaEventRecord(c->prep_ev[pv & 1], c->stream));
+    } catch (...) {
+      std::swap(c->stream, c->stream2);
+      c->cub_tmp.swap(c->cub_tmp2);
+      throw;
+    }
+    std::swap(c->stream, c->stream2);
+    c->cub_tmp.swap(c->cub_tmp2);
+  };
   for (int v = v0; v < v1 && n > 0; ++v) {
     const Cam& cam = c->cams[v];
     const int tiles_x = (cam.w + tile_size - 1) / tile_size;
     const int tiles_y = (cam.h + tile_size - 1) / tile_size;
     const int T = tiled ? tiles_x * tiles_y : 1;
     const auto h0 = std::chrono::steady_clock::now();
-    const int p0 = prof_mark(c);
-    const Rec* rec = view_records(c, v);
-    const Binding* bd = tiled ? &view_binding(c, v, tile_size) : nullptr;
+    if (v == v0) prep_view(v);
+    // the records / binding of view v were prepared on the prep lane (during view v-1)
+    SOF_CUDA(cudaStreamWaitEvent(c->stream, c->prep_ev[v & 1], 0));
+    const Rec* rec = prep_rec[v & 1];
+    const Binding* bd = prep_bd[v & 1];
     const int p1 = prof_mark(c);
-    prof_span(c, p0, p1, kProfPrep);
     const auto h1 = std::chrono::steady_clock::now();
     c->host_ms[0] += std::chrono::duration<double, std::milli>(h1 - h0).count();
     // K3: group the active, observed points of this view by tile (no host sync)
@@ -692,17 +745,18 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     s.blk_off.ensure(T + 1);
     SOF_CUDA(cudaMemsetAsync(s.tile_cnt.p, 0, sizeof(int) * 2 * (T + 1), c->stream));
     int* tile_cur = s.tile_cnt.p + (T + 1);
-    k_sched_tile<<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, cam, tile_size, tiles_x, !tiled,
-                                                          skip, s.tile_of.p, s.tile_cnt.p);
+    const int32_t* cand = use_list ? s.active.p : nullptr;
+    k_sched_tile<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
+                                                              !tiled, skip, s.tile_of.p, s.tile_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, T + 1);
-    k_sched_scatter<<<grid_for(n, 256), 256, 0, c->stream>>>(n, s.tile_of.p, s.tile_off.p, tile_cur,
-                                                             s.order.p);
+    k_sched_scatter<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, s.tile_of.p, s.tile_off.p,
+                                                                 tile_cur, s.order.p);
     SOF_LAUNCHED(c);
     k_block_counts<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, s.tile_off.p, s.blk_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, T + 1);
-    const int64_t grid = (n + kBlockPoints - 1) / kBlockPoints + T;
+    const int64_t grid = (ncand + kBlockPoints - 1) / kBlockPoints + T;
     s.blocks.ensure(grid);
     k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, s.tile_off.p, s.blk_off.p, s.blocks.p,
                                                                c->d_scalar.p);
@@ -728,6 +782,35 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
         launch_eval<kModeValue>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
                                 strategies, false, min_op, ext, o_out, obs_out, comp_out);
         break;
+    }
+    // drop pruned points from the candidate list now and then (the reference skips them,
+    // field_eval.hpp:147); the list shrinks fast over the first views
+    const int done_views = v - v0 + 1;
+    if (skip && v + 1 < v1 && (done_views <= 4 || done_views % 16 == 0)) {
+      s.active2.ensure(std::max<int64_t>(ncand, 1));
+      s.nsel.ensure(1);
+      size_t bytes = 0;
+      NotPruned pred{ext};
+      if (use_list) {
+        SOF_CUDA(cub::DeviceSelect::If(nullptr, bytes, s.active.p, s.active2.p, s.nsel.p, ncand, pred, c->stream));
+        c->cub_tmp.ensure(bytes);
+        SOF_CUDA(cub::DeviceSelect::If(c->cub_tmp.p, bytes, s.active.p, s.active2.p, s.nsel.p, ncand, pred,
+                                       c->stream));
+      } else {
+        thrust::counting_iterator<int32_t> it(0);
+        SOF_CUDA(cub::DeviceSelect::If(nullptr, bytes, it, s.active2.p, s.nsel.p, ncand, pred, c->stream));
+        c->cub_tmp.ensure(bytes);
+        SOF_CUDA(cub::DeviceSelect::If(c->cub_tmp.p, bytes, it, s.active2.p, s.nsel.p, ncand, pred, c->stream));
+      }
+      c->launches += 2;
+      s.active.swap(s.active2);
+      ncand = read_scalar(c, s.nsel.p);
+      use_list = true;
+    }
+    if (v + 1 < v1) {
+      const auto h3 = std::chrono::steady_clock::now();
+      prep_view(v + 1);
+      c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h3).count();
     }
   }
   if (counters_host) {

@@ -37,10 +37,18 @@ struct __align__(16) Rec {
   double c;      // c_scalar
   double op;     // filtered opacity
   double zmin;   // min_z
-  double thr;    // log(1/(255 op)) - 1e-9 (1 + |.|): exponent < thr => alpha < 1/255
-  double pad;
+  // log(1/(255 op)) - 1e-9 (1 + |.|), rounded toward -inf to float:
+  // exponent < thr => alpha < 1/255
+  float thr;
+  // screen-space conic of the rays that can reach alpha >= 1/255: for the point's
+  // pixel (u, v), g = G00 u^2 + G11 v^2 + G22 + 2 (G01 uv + G02 u + G12 v) equals
+  // a(d) (L - m2_min(d)) for the (unnormalised) ray direction d through (u, v), with
+  // L = 2 log(255 op); g < -gmargin proves m2 > L on the whole ray, i.e. alpha < 1/255
+  // at every te (field_eval.hpp:100-101), so the pair is skipped without FP64 work.
+  float conic[6];  // G00, G11, G22, 2 G01, 2 G02, 2 G12
+  float gmargin;   // 256 ulp x the largest |term| over the image
 };
-static_assert(sizeof(Rec) == 112, "record layout");
+static_assert(sizeof(Rec) == 128, "record layout");
 constexpr int kRecV2 = int(sizeof(Rec) / 16);  // double2 per record
 
 // FP32 filter record (64 B): a rounded copy of Rec plus error-bound constants.
@@ -91,6 +99,17 @@ __device__ __forceinline__ RecF make_recf(const Rec& r) {
   f.zmin = __double2float_rn(r.zmin);
   f.flags = (r.op < kMinAlpha) ? 1u : 0u;
   return f;
+}
+
+// Largest float <= x (round toward -inf), host and device.
+__host__ __device__ inline float float_down(double x) {
+#if defined(__CUDA_ARCH__)
+  return __double2float_rd(x);
+#else
+  float f = (float)x;
+  if ((double)f > x) f = nextafterf(f, -INFINITY);
+  return f;
+#endif
 }
 
 // View-independent per-Gaussian data (the parts of precompute.hpp:65-75 that do
@@ -218,11 +237,55 @@ __host__ __device__ inline void gauss_view(const GaussStatic& g, const Cam& cam,
   // below thr never changes a decision (field_eval.hpp:100-101, opacity_field.hpp:98-99)
   if (r.op > 0.0) {
     const double L = -log(255.0 * r.op);
-    r.thr = L - 1e-9 * (1.0 + fabs(L));
+    r.thr = float_down(L - 1e-9 * (1.0 + fabs(L)));
   } else {
-    r.thr = 1e300;
+    r.thr = INFINITY;
   }
-  r.pad = 0.0;
+  // Screen-space conic (see Rec). Rays through pixel p = (u, v, 1) have direction
+  // d = R^T K^-1 p; with S the symmetric inverse covariance (upper triangle as used by
+  // abc_cached) and L = 2 log(255 op): a(d) (L - m2_min(d)) = d^T (b b^T - (c - L) S) d.
+  if (!(r.op >= kMinAlpha * (1.0 - 1e-9))) {
+    // alpha = op G <= op (1 + 1e-15) < 1/255 for every ray: always skipped
+    for (int k = 0; k < 6; ++k) r.conic[k] = 0.0f;
+    r.conic[2] = -1.0f;
+    r.gmargin = 0.0f;
+  } else {
+    const double L = 2.0 * log(255.0 * r.op);
+    const double S[9] = {r.ic[0], r.ic[1], r.ic[2], r.ic[1], r.ic[3], r.ic[4], r.ic[2], r.ic[4], r.ic[5]};
+    double M[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) M[3 * i + j] = r.b[i] * r.b[j] - (r.c - L) * S[3 * i + j];
+    const double Ki[9] = {1.0 / cam.fx, 0.0, -cam.cx / cam.fx, 0.0, 1.0 / cam.fy, -cam.cy / cam.fy, 0.0, 0.0, 1.0};
+    double A[9];  // R^T K^-1
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        A[3 * i + j] = cam.R[i] * Ki[j] + cam.R[3 + i] * Ki[3 + j] + cam.R[6 + i] * Ki[6 + j];
+    double MA[9], G[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        MA[3 * i + j] = M[3 * i] * A[j] + M[3 * i + 1] * A[3 + j] + M[3 * i + 2] * A[6 + j];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        G[3 * i + j] = A[i] * MA[j] + A[3 + i] * MA[3 + j] + A[6 + i] * MA[6 + j];
+    const double g00 = G[0], g11 = G[4], g22 = G[8];
+    const double g01 = 0.5 * (G[1] + G[3]), g02 = 0.5 * (G[2] + G[6]), g12 = 0.5 * (G[5] + G[7]);
+    r.conic[0] = float(g00);
+    r.conic[1] = float(g11);
+    r.conic[2] = float(g22);
+    r.conic[3] = float(2.0 * g01);
+    r.conic[4] = float(2.0 * g02);
+    r.conic[5] = float(2.0 * g12);
+    const double W = cam.w + 1.0, H = cam.h + 1.0;
+    const double smax = fabs(g00) * W * W + fabs(g11) * H * H + fabs(g22) + 2.0 * fabs(g01) * W * H +
+                        2.0 * fabs(g02) * W + 2.0 * fabs(g12) * H;
+    // 256 ulp of 1.0f: covers the float rounding of the coefficients, of u, v and of
+    // the 6-term evaluation, and the FP64 error of G, with a wide margin
+    r.gmargin = float(smax * (256.0 * 5.9604645e-8) * 1.01 + 1e-30);
+    if (!(r.gmargin < 3.0e38f)) {  // overflow / NaN: never cull
+      for (int k = 0; k < 6; ++k) r.conic[k] = 0.0f;
+      r.gmargin = 3.0e38f;
+    }
+  }
 }
 
 // x86-64 cvttsd2si semantics for int(x) (out of range / NaN -> INT_MIN), the
@@ -287,6 +350,7 @@ struct PointRay {
   double d[3];   // unit direction camera -> x
   double t;      // |x - o|
   double zp;     // view-space z of x
+  double px, py; // pixel coordinates of x (camera.hpp:26)
   int tile;      // tile index (valid when observed)
   bool observed;
 };
@@ -304,6 +368,8 @@ __host__ __device__ inline PointRay point_ray(const Cam& cam, double x0, double 
   if (vz <= 0.0) return pr;
   const double px = cam.fx * vx / vz + cam.cx;
   const double py = cam.fy * vy / vz + cam.cy;
+  pr.px = px;
+  pr.py = py;
   if (!(px >= 0.0 && px < (double)cam.w && py >= 0.0 && py < (double)cam.h)) return pr;
   // ray_through_point (camera.hpp:52-59)
   const double e0 = x0 - cam.center[0], e1 = x1 - cam.center[1], e2 = x2 - cam.center[2];
@@ -337,10 +403,19 @@ __device__ __forceinline__ double pair_alpha(const Rec& r, const double* d, doub
     if (te <= 0.0) return 0.0;
   }
   const double arg = -0.5 * ((a * te + b) * te + r.c);  // eval_1d gaussian.hpp:47-49
-  if (arg < r.thr) return 0.0;                          // alpha < 1/255 certain
+  if (arg < double(r.thr)) return 0.0;                  // alpha < 1/255 certain
   double alpha = r.op * sof_exp(arg);
   if (alpha < kMinAlpha) return 0.0;
   return (kMaxAlpha < alpha) ? kMaxAlpha : alpha;  // std::min(alpha, kMaxAlpha)
+}
+
+// Screen-space cull (Rec::conic): true when the ray through pixel (u, v) provably
+// stays below alpha = 1/255. uu = u*u, vv = v*v, uv = u*v in float.
+__device__ __forceinline__ bool conic_culls(const Rec& r, float u, float v, float uu, float vv,
+                                            float uv) {
+  const float g = fmaf(r.conic[0], uu, fmaf(r.conic[1], vv, fmaf(r.conic[3], uv,
+                  fmaf(r.conic[4], u, fmaf(r.conic[5], v, r.conic[2])))));
+  return g < -r.gmargin;
 }
 
 // Orderable 64-bit key of a double (ascending), with -0 folded onto +0 so that

@@ -95,6 +95,7 @@ struct PointSchedule {
   DBuf<int> tile_cnt;        // [2(T + 1)] histogram | scatter cursors
   DBuf<int> tile_off, blk_cnt, blk_off;  // [T + 1]
   DBuf<int4> blocks;         // {start, end, tile, 0}
+  DBuf<int32_t> active, active2, nsel;  // candidate points (not pruned), compacted
 };
 
 // Persistent (grow-only) scratch of the mesher stages: no allocation in steady state.
@@ -152,12 +153,21 @@ struct sof_ctx {
   size_t cache_budget = size_t(96) << 30;  // bytes of HBM the per-view caches may use
   size_t cache_bytes = 0;
   std::vector<sofk::DBuf<sofk::RecF>> recfs;
-  sofk::DBuf<sofk::Rec> rec_scratch;      // when the cache budget is exhausted
-  sofk::DBuf<sofk::RecF> recf_scratch;
+  // past the cache budget, per-view state goes to one of two scratch slots (ping-pong:
+  // view v + 1 is prepared on the prep stream while view v is evaluated)
+  sofk::DBuf<sofk::Rec> rec_scratch[2];
+  sofk::DBuf<sofk::RecF> recf_scratch[2];
+  sofk::Binding bind_scratch[2];
+  int scratch_view[2] = {-1, -1};
+  int scratch_sel = 0;
   int eval_path = 1;                      // 0: FP32 filter + exact FP64 replay, 1: FP64 only
   uint64_t exact_evals = 0;               // pairs that took the FP64 path (instrumentation)
   double host_ms[4] = {0, 0, 0, 0};       // host time in per-view prep / scheduling (instrumentation)
-  sofk::Binding bind_scratch;
+
+  // prep lane: a second stream (+ its own CUB scratch) for per-view preprocessing
+  cudaStream_t stream2 = nullptr;
+  sofk::DBuf<char> cub_tmp2;
+  cudaEvent_t prep_ev[2] = {nullptr, nullptr};
 
   // binning scratch
   sofk::DBuf<int4> rect;
