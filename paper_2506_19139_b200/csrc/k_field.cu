@@ -343,7 +343,12 @@ __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
     const int64_t i = cand ? cand[k] : k;
     if (!(skip && skip[i])) {
       const PointRay pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
-      if (pr.observed) tile = single_bin ? 0 : pr.tile;
+      // bin = tile x (4x4 cell of pixels inside the tile): points of one cell are
+      // adjacent, so a warp covers a compact screen region (coherent conic culls)
+      if (pr.observed) {
+        const int cs = (ts + 3) / 4;
+        tile = single_bin ? 0 : pr.tile * 16 + (((int)pr.py % ts) / cs) * 4 + ((int)pr.px % ts) / cs;
+      }
     }
     tile_of[k] = tile;
   }
@@ -365,19 +370,22 @@ __global__ void k_sched_scatter(int64_t n, const int32_t* __restrict__ cand,
 }
 
 // One thread per tile: blocks per tile; an exclusive scan of these gives block ids.
-__global__ void k_block_counts(int T, const int* __restrict__ tile_off, int* blk_cnt) {
+// tile_off indexes bins; tile t spans bins [t S, (t + 1) S)
+__global__ void k_block_counts(int T, int S, const int* __restrict__ tile_off, int* blk_cnt) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > T) return;
-  blk_cnt[t] = (t == T) ? 0 : (tile_off[t + 1] - tile_off[t] + kBlockPoints - 1) / kBlockPoints;
+  blk_cnt[t] = (t == T) ? 0
+                        : (tile_off[int64_t(t + 1) * S] - tile_off[int64_t(t) * S] + kBlockPoints - 1) /
+                              kBlockPoints;
 }
 
-__global__ void k_block_fill(int T, const int* __restrict__ tile_off, const int* __restrict__ blk_off,
-                             int4* blocks, int64_t* nblocks) {
+__global__ void k_block_fill(int T, int S, const int* __restrict__ tile_off,
+                             const int* __restrict__ blk_off, int4* blocks, int64_t* nblocks) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t == 0) *nblocks = blk_off[T];
   if (t >= T) return;
   const int b0 = blk_off[t], b1 = blk_off[t + 1];
-  const int p0 = tile_off[t], p1 = tile_off[t + 1];
+  const int p0 = tile_off[int64_t(t) * S], p1 = tile_off[int64_t(t + 1) * S];
   for (int b = b0; b < b1; ++b) {
     const int s = p0 + (b - b0) * kBlockPoints;
     blocks[b] = make_int4(s, min(s + kBlockPoints, p1), t, 0);
@@ -739,26 +747,28 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     c->host_ms[0] += std::chrono::duration<double, std::milli>(h1 - h0).count();
     // K3: group the active, observed points of this view by tile (no host sync)
     const uint8_t* skip = (prune && (mode == kModeLabel || mode == kModeClassify)) ? ext : nullptr;
-    s.tile_cnt.ensure(2 * (T + 1));
-    s.tile_off.ensure(T + 1);
+    const int S = tiled ? 16 : 1;  // bins per tile (4x4 cells)
+    const int64_t NB = int64_t(T) * S;
+    s.tile_cnt.ensure(2 * (NB + 1));
+    s.tile_off.ensure(NB + 1);
     s.blk_cnt.ensure(T + 1);
     s.blk_off.ensure(T + 1);
-    SOF_CUDA(cudaMemsetAsync(s.tile_cnt.p, 0, sizeof(int) * 2 * (T + 1), c->stream));
-    int* tile_cur = s.tile_cnt.p + (T + 1);
+    SOF_CUDA(cudaMemsetAsync(s.tile_cnt.p, 0, sizeof(int) * 2 * (NB + 1), c->stream));
+    int* tile_cur = s.tile_cnt.p + (NB + 1);
     const int32_t* cand = use_list ? s.active.p : nullptr;
     k_sched_tile<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
                                                               !tiled, skip, s.tile_of.p, s.tile_cnt.p);
     SOF_LAUNCHED(c);
-    exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, T + 1);
+    exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);
     k_sched_scatter<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, s.tile_of.p, s.tile_off.p,
                                                                  tile_cur, s.order.p);
     SOF_LAUNCHED(c);
-    k_block_counts<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, s.tile_off.p, s.blk_cnt.p);
+    k_block_counts<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, T + 1);
     const int64_t grid = (ncand + kBlockPoints - 1) / kBlockPoints + T;
     s.blocks.ensure(grid);
-    k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, s.tile_off.p, s.blk_off.p, s.blocks.p,
+    k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_off.p, s.blocks.p,
                                                                c->d_scalar.p);
     SOF_LAUNCHED(c);
     prof_span(c, p1, prof_mark(c), kProfSched);

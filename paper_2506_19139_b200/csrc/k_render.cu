@@ -221,6 +221,10 @@ __global__ void __launch_bounds__(256) k_render(
   const bool valid = px < cam.w && py < cam.h;
   double d[3] = {0.0, 0.0, 1.0};
   if (valid) pixel_ray(cam, px, py, d);
+  // pixel-centre coordinates for the screen-space conic cull (Rec::conic): the ray
+  // direction through (px + 0.5, py + 0.5) is R^T K^-1 (u, v, 1) up to a positive scale
+  const float cu = float(px) + 0.5f, cv = float(py) + 0.5f;
+  const float cuu = cu * cu, cvv = cv * cv, cuv = cu * cv;
   const int64_t l0 = loff[tile], l1 = loff[tile + 1];
   const int64_t slice = 256 * (l0 - loff[tile_base]) + int64_t(tid) * (l1 - l0);
   double T = 1.0, col[3] = {0.0, 0.0, 0.0};
@@ -281,6 +285,7 @@ __global__ void __launch_bounds__(256) k_render(
       for (int k = 0; k < cnt; ++k) {
         if (!collect) flush_below(sL[k]);
         ++tested;
+        if (conic_culls(srec[k], cu, cv, cuu, cvv, cuv)) continue;  // cannot reach 1/255
         const Contrib c = contribution(srec[k], d, sidx[k]);
         if (!c.ok) continue;
         ++contributing;
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(256) k_render(
     __syncthreads();
     if (need2) {
       for (int k = 0; k < cnt; ++k) {
+        if (conic_culls(srec[k], cu, cv, cuu, cvv, cuv)) continue;
         const Contrib c = contribution(srec[k], d, sidx[k]);
         if (!c.ok) continue;
         T2 *= 1.0 - alpha_at(srec[k], d, c.t, depth);
