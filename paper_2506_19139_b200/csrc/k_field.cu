@@ -185,24 +185,49 @@ __global__ void k_gather_counts(int64_t n, const int32_t* __restrict__ order,
   out[r] = (r == n) ? 0u : cnt[order[r]];
 }
 
-// One warp per Gaussian (in (min_z, index) order): emit (tile, gaussian) entries.
+// One thread per Gaussian (in (min_z, index) order) emits its (tile, gaussian)
+// entries; Gaussians covering many tiles (rare) hand the tail to their warp.
 __global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
                                const int4* __restrict__ rect, const uint32_t* __restrict__ cnt,
                                const int64_t* __restrict__ off, int tiles_x, uint32_t* keys,
                                int32_t* vals) {
-  const int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  constexpr uint32_t kOwn = 16;  // entries written by the owning thread
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  if (r >= n) return;
-  const int32_t g = order[r];
-  const uint32_t count = cnt[g];
-  if (count == 0) return;
-  const int4 rc = rect[g];
-  const int w = rc.y - rc.x + 1;
-  const int64_t base = off[r];
-  for (uint32_t k = lane; k < count; k += 32) {
+  int32_t g = -1;
+  uint32_t count = 0;
+  int4 rc = make_int4(0, 0, 0, 0);
+  int64_t base = 0;
+  if (r < n) {
+    g = order[r];
+    count = cnt[g];
+    if (count) {
+      rc = rect[g];
+      base = off[r];
+    }
+  }
+  const int w = max(rc.y - rc.x + 1, 1);
+  for (uint32_t k = 0; k < min(count, kOwn); ++k) {
     const int ty = rc.z + int(k / w), tx = rc.x + int(k % w);
     keys[base + k] = uint32_t(ty * tiles_x + tx);
     vals[base + k] = g;
+  }
+  // large footprints: the warp writes the remaining entries cooperatively
+  unsigned big = __ballot_sync(0xffffffffu, count > kOwn);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const uint32_t bc = __shfl_sync(0xffffffffu, count, src);
+    const int32_t bg = __shfl_sync(0xffffffffu, g, src);
+    const int bx = __shfl_sync(0xffffffffu, rc.x, src), by = __shfl_sync(0xffffffffu, rc.y, src);
+    const int bz = __shfl_sync(0xffffffffu, rc.z, src);
+    const int64_t bb = __shfl_sync(0xffffffffu, base, src);
+    const int bw = by - bx + 1;
+    for (uint32_t k = kOwn + lane; k < bc; k += 32) {
+      const int ty = bz + int(k / bw), tx = bx + int(k % bw);
+      keys[bb + k] = uint32_t(ty * tiles_x + tx);
+      vals[bb + k] = bg;
+    }
   }
 }
 
@@ -285,7 +310,7 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
     c->ekey_in.ensure(M);
     c->ekey_out.ensure(M);
     c->eval_in.ensure(M);
-    k_emit_entries<<<grid_for(n * 32, 256), 256, 0, c->stream>>>(
+    k_emit_entries<<<grid_for(n, 256), 256, 0, c->stream>>>(
         n, c->gidx_out.p, c->rect.p, c->gcount.p, c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p);
     SOF_LAUNCHED(c);
     // stable sort by tile keeps the (min_z, index) order inside every tile list

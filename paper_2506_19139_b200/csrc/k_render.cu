@@ -163,7 +163,7 @@ struct RenderOut {
 
 // Spill area of the pixels whose k-buffer overflows: a pixel of tile t owns the slice
 // [256 off[t] + lp len(t), +len(t)) of the pool (len(t) bounds its contributions),
-// written in collect mode and later sorted by t* with a segmented radix sort.
+// written in collect mode and sorted by (t*, index) inside k_render_finish.
 struct Spill {
   uint64_t* keys;      // double_key(t*)
   int32_t* vals;       // Gaussian index
@@ -174,18 +174,6 @@ struct Spill {
   int32_t* istate;     // [slot][2] med_idx, found
   int32_t* count;      // number of slots in use
 };
-
-__device__ __forceinline__ double opacity_at_depth(const Rec* __restrict__ recs,
-                                                   const int32_t* __restrict__ lent, int64_t l0,
-                                                   int64_t l1, const double* d, double depth) {
-  double T2 = 1.0;
-  for (int64_t e = l0; e < l1; ++e) {
-    const Rec r = recs[lent[e]];
-    const Contrib c = contribution(r, d, lent[e]);
-    if (c.ok) T2 *= 1.0 - alpha_at(r, d, c.t, depth);
-  }
-  return T2;
-}
 
 __device__ __forceinline__ double exact_depth_at(const Rec& r, const double* d, double med_t,
                                                  double med_T, bool& fell_back) {
@@ -372,16 +360,52 @@ __global__ void __launch_bounds__(256) k_render(
   }
 }
 
-// Resumes the blend of a collect-mode pixel over its t*-sorted spill slice. The sort
-// is stable on a key of t* alone; equal-t* runs are replayed in Gaussian-index order,
-// completing the reference's (t*, index) order (opacity_field.hpp:56-59).
-__global__ void k_render_finish(Cam cam, int tiles_x, const int64_t* __restrict__ loff,
-                                const int32_t* __restrict__ lent, const Rec* __restrict__ recs,
-                                const double* __restrict__ dc, int exact_depth, Spill spill,
-                                const uint64_t* __restrict__ skeys, const int32_t* __restrict__ svals,
-                                RenderOut out, unsigned long long* stats) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= *spill.count) return;
+constexpr int kFChunk = 256;  // slice entries a warp sorts at once in shared memory
+constexpr int kFWarps = 8;    // warps (spilled pixels) per finish CTA
+
+__device__ __forceinline__ bool kv_less(uint64_t ka, int32_t va, uint64_t kb, int32_t vb) {
+  return ka < kb || (ka == kb && va < vb);
+}
+
+// Warp-wide bitonic sort of m (a power of two, 32..kFChunk) (key, index) pairs in
+// shared memory, ascending.
+__device__ __forceinline__ void warp_bitonic(uint64_t* k, int32_t* v, int m, int lane) {
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncwarp();
+      for (int i = lane; i < (m >> 1); i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t ka = k[lo], kb = k[hi];
+        const int32_t va = v[lo], vb = v[hi];
+        if (kv_less(kb, vb, ka, va) == up) {
+          k[lo] = kb;
+          k[hi] = ka;
+          v[lo] = vb;
+          v[hi] = va;
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Resumes the blend of a collect-mode pixel (one warp per pixel) over its spill slice
+// in the reference's (t*, index) order (opacity_field.hpp:56-59): the slice is sorted
+// by (double_key(t*), index) in shared memory (slices longer than kFChunk: sorted
+// chunks merged by rank into keys2/vals2); contributions are evaluated lane-parallel
+// and blended serially through shuffles, and O_N at the depth multiplies the
+// tile-list factors in list order (exact: factors of 1 are skipped).
+__global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
+    Cam cam, int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
+    const Rec* __restrict__ recs, const double* __restrict__ dc, int exact_depth, Spill spill,
+    uint64_t* __restrict__ gk2, int32_t* __restrict__ gv2, RenderOut out, unsigned long long* stats) {
+  __shared__ uint64_t sk[kFWarps][kFChunk];
+  __shared__ int32_t sv[kFWarps][kFChunk];
+  constexpr unsigned kAll = 0xffffffffu;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kFWarps + w;
+  if (s >= *spill.count) return;  // warp-uniform
   const int64_t p = spill.pixel[s];
   const int px = int(p % cam.w), py = int(p / cam.w);
   const int tile = (py / kRTile) * tiles_x + px / kRTile;
@@ -391,29 +415,75 @@ __global__ void k_render_finish(Cam cam, int tiles_x, const int64_t* __restrict_
   double T = st[0], col[3] = {st[1], st[2], st[3]}, med_t = st[4], med_T = st[5];
   int med_idx = spill.istate[2 * s];
   bool found = spill.istate[2 * s + 1];
-  const int64_t b = spill.begin[s], e = spill.end[s];
-  int64_t j = b;
-  while (j < e) {
-    int64_t r = j + 1;
-    while (r < e && skeys[r] == skeys[j]) ++r;  // run of equal t*
-    int last = -1;
-    for (int64_t q = j; q < r; ++q) {  // replay the run in index order
-      int nxt = 0x7fffffff;
-      for (int64_t u = j; u < r; ++u)
-        if (svals[u] > last && svals[u] < nxt) nxt = svals[u];
-      last = nxt;
-      const Contrib c = contribution(recs[nxt], d, nxt);
-      for (int k = 0; k < 3; ++k) col[k] = col[k] + dc[3 * nxt + k] * c.alpha * T;
-      const double next = T * (1.0 - c.alpha);
+  const int64_t b = spill.begin[s], n = spill.end[s] - b;
+  uint64_t* K = sk[w];
+  int32_t* V = sv[w];
+  for (int64_t c0 = 0; c0 < n; c0 += kFChunk) {
+    const int cn = int(min(int64_t(kFChunk), n - c0));
+    int m = 32;
+    while (m < cn) m <<= 1;
+    for (int i = lane; i < m; i += 32) {
+      K[i] = i < cn ? spill.keys[b + c0 + i] : ~0ull;
+      V[i] = i < cn ? spill.vals[b + c0 + i] : 0x7fffffff;
+    }
+    warp_bitonic(K, V, m, lane);
+    if (n > kFChunk) {
+      for (int i = lane; i < cn; i += 32) {
+        spill.keys[b + c0 + i] = K[i];
+        spill.vals[b + c0 + i] = V[i];
+      }
+      __syncwarp();
+    }
+  }
+  const int32_t* SV = V;
+  if (n > kFChunk) {
+    // final position = position in own chunk + entries below it in every other chunk
+    for (int64_t i = lane; i < n; i += 32) {
+      const uint64_t ki = spill.keys[b + i];
+      const int32_t vi = spill.vals[b + i];
+      const int64_t own = i / kFChunk;
+      int64_t rank = i - own * kFChunk;
+      for (int64_t c0 = 0; c0 < n; c0 += kFChunk) {
+        if (c0 == own * kFChunk) continue;
+        int lo = 0, hi = int(min(int64_t(kFChunk), n - c0));
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (kv_less(spill.keys[b + c0 + mid], spill.vals[b + c0 + mid], ki, vi)) lo = mid + 1;
+          else hi = mid;
+        }
+        rank += lo;
+      }
+      gk2[b + rank] = ki;
+      gv2[b + rank] = vi;
+    }
+    __syncwarp();
+    SV = gv2 + b;
+  }
+  for (int64_t c0 = 0; c0 < n; c0 += 32) {
+    const int64_t i = c0 + lane;
+    double t = 0.0, al = 0.0, dq[3] = {0.0, 0.0, 0.0};
+    int idx = 0;
+    if (i < n) {
+      idx = SV[i];
+      const Contrib c = contribution(recs[idx], d, idx);
+      t = c.t;
+      al = c.alpha;
+      for (int k = 0; k < 3; ++k) dq[k] = dc[3 * idx + k];
+    }
+    const int cnt = int(min(int64_t(32), n - c0));
+    for (int q = 0; q < cnt; ++q) {
+      const double tq = __shfl_sync(kAll, t, q), aq = __shfl_sync(kAll, al, q);
+      const int iq = __shfl_sync(kAll, idx, q);
+      for (int k = 0; k < 3; ++k) col[k] = col[k] + __shfl_sync(kAll, dq[k], q) * aq * T;
+      const double next = T * (1.0 - aq);
       if (!found && T > 0.5 && next < 0.5) {
         found = true;
-        med_idx = nxt;
-        med_t = c.t;
+        med_idx = iq;
+        med_t = tq;
         med_T = T;
       }
       T = next;
     }
-    j = r;
   }
   double depth = NAN;
   if (found) {
@@ -421,14 +491,38 @@ __global__ void k_render_finish(Cam cam, int tiles_x, const int64_t* __restrict_
     if (exact_depth) {
       bool fb = false;
       depth = exact_depth_at(recs[med_idx], d, med_t, med_T, fb);
-      if (fb) atomicAdd(stats + 3, 1ull);
+      if (fb && lane == 0) atomicAdd(stats + 3, 1ull);
     }
   }
-  const double T2 = isnan(depth) ? 1.0 : opacity_at_depth(recs, lent, loff[tile], loff[tile + 1], d, depth);
-  out.depth[p] = depth;
-  out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
-  for (int k = 0; k < 3; ++k) out.rgb[3 * p + k] = col[k];
-  out.tfinal[p] = T;
+  double T2 = 1.0;
+  if (!isnan(depth)) {
+    const float cu = float(px) + 0.5f, cv = float(py) + 0.5f;
+    const float cuu = cu * cu, cvv = cv * cv, cuv = cu * cv;
+    for (int64_t e0 = loff[tile], l1 = loff[tile + 1]; e0 < l1; e0 += 32) {
+      const int64_t e = e0 + lane;
+      double f = 1.0;
+      if (e < l1) {
+        const int32_t g = lent[e];
+        const Rec& r = recs[g];
+        if (!conic_culls(r, cu, cv, cuu, cvv, cuv)) {
+          const Contrib c = contribution(r, d, g);
+          if (c.ok) f = 1.0 - alpha_at(r, d, c.t, depth);
+        }
+      }
+      unsigned mask = __ballot_sync(kAll, f != 1.0);
+      while (mask) {
+        const int q = __ffs(mask) - 1;
+        mask &= mask - 1;
+        T2 *= __shfl_sync(kAll, f, q);
+      }
+    }
+  }
+  if (lane == 0) {
+    out.depth[p] = depth;
+    out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
+    for (int k = 0; k < 3; ++k) out.rgb[3 * p + k] = col[k];
+    out.tfinal[p] = T;
+  }
 }
 
 }  // namespace sofk
@@ -473,7 +567,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     RenderOut out{c->r_out.p, c->r_out.p + P, c->r_out.p + 2 * P, c->r_out.p + 5 * P};
     // Spill pool: a pixel of tile t may need len(t) slots, so a band of tiles [t0, t1)
     // needs 256 (off[t1] - off[t0]). Tiles are rendered in bands whose pool fits both
-    // the 2^31-item limit of the segmented sort and a 24 GB memory cap.
+    // a 24 GB memory cap (and 32-bit slot counts).
     std::vector<int64_t> off(T + 1, 0);
     if (n > 0)
       SOF_CUDA(cudaMemcpyAsync(off.data(), c->rbind.off.p, sizeof(int64_t) * (T + 1),
@@ -515,16 +609,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       SOF_LAUNCHED(c);
       const int32_t nover = read_scalar(c, rs.count.p);
       if (nover > 0) {
-        size_t bytes = 0;
-        SOF_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, rs.keys.p, rs.keys2.p, rs.vals.p,
-                                                           rs.vals2.p, pool, nover, rs.begin.p, rs.end.p,
-                                                           c->stream));
-        c->cub_tmp.ensure(bytes);
-        SOF_CUDA(cub::DeviceSegmentedSort::StableSortPairs(c->cub_tmp.p, bytes, rs.keys.p, rs.keys2.p,
-                                                           rs.vals.p, rs.vals2.p, pool, nover, rs.begin.p,
-                                                           rs.end.p, c->stream));
-        c->launches += 3;
-        k_render_finish<<<grid_for(nover, 64), 64, 0, c->stream>>>(
+        k_render_finish<<<unsigned((nover + kFWarps - 1) / kFWarps), kFWarps * 32, 0, c->stream>>>(
             cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT,
             spill, rs.keys2.p, rs.vals2.p, out, c->r_stats.p);
         SOF_LAUNCHED(c);

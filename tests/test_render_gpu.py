@@ -85,3 +85,26 @@ def test_render_single_gaussian_disk(ref):
     dm, _ = sof.render_depth_map(views, 0, exact=False)
     assert abs(de[16, 16] - 3.82258) < 0.01 and abs(dm[16, 16] - 5.0) < 0.01
     np.testing.assert_array_equal(np.isnan(de), np.isnan(dm))
+
+
+def test_render_long_spill_slices_with_ties(ref):
+    """~700 contributions per pixel (spill slices longer than the 256-entry shared-memory
+    chunk, merged by rank) with duplicated Gaussians (equal t*: index order breaks ties)."""
+    n = 700
+    rng = np.random.default_rng(11)
+    pos = np.zeros((n, 3))
+    pos[:, 2] = rng.uniform(-1.0, 1.0, n)
+    pos[:, :2] = rng.normal(0, 0.03, (n, 2))
+    scale = np.full((n, 3), 0.35)
+    op = rng.uniform(0.01, 0.05, n)
+    for i in range(1, n, 3):  # duplicates -> ties in t*
+        pos[i] = pos[i - 1]
+        scale[i] = scale[i - 1]
+    scene = Scene(pos, scale, np.tile([1.0, 0, 0, 0], (n, 1)), op, rng.uniform(0, 1, (n, 3)))
+    cams = ref.look_at([0, 0, -4.0], [0, 0, 0], [0, 1, 0], 40.0, 40.0, 20, 20)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    for exact in (True, False):
+        st = []
+        check(rc, views, 0, exact, st)
+        assert st[0][2] > 0 and st[0][1] > 300 * st[0][2]  # long slices took the merge path
