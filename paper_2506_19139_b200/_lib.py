@@ -11,7 +11,7 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsof_cuda.so")
+LIB_PATH = os.environ.get("SOF_LIB_PATH") or os.path.join(PKG, "libsof_cuda.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "sof_cuda.h")
 
 SOF_OK, SOF_E_INVALID, SOF_E_CUDA, SOF_E_NCCL, SOF_E_OOM, SOF_E_STATE, SOF_E_RUNTIME = 0, -1, -2, -3, -4, -5, -6

@@ -17,6 +17,15 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libsof_cuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# tuning experiments: SOF_VARIANT="name:-DKNOB=v ..." builds build/obj_name and
+# libsof_cuda_name.so (loaded with SOF_LIB_PATH); the default build is untouched
+_VARIANT = os.environ.get("SOF_VARIANT", "")
+DEFS: list = []
+if _VARIANT:
+    _name, _, _defs = _VARIANT.partition(":")
+    OBJ = os.path.join(ROOT, "build", "obj_" + _name)
+    LIB = os.path.join(PKG, f"libsof_cuda_{_name}.so")
+    DEFS = _defs.split()
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
@@ -48,7 +57,7 @@ def _compile(src):
     log = os.path.join(OBJ, src.replace(".cu", ".ptxas.txt"))
     if not _stale(o, [s] + _headers()):
         return o
-    cmd = [NVCC] + NVFLAGS + FMAD.get(src, FMAD["default"]) + ["-c", s, "-o", o]
+    cmd = [NVCC] + NVFLAGS + DEFS + FMAD.get(src, FMAD["default"]) + ["-c", s, "-o", o]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)

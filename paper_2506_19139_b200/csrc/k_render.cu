@@ -28,7 +28,10 @@
 namespace sofk {
 
 constexpr int kRTile = 16;     // render tile (pixels per side), one CTA per tile
-constexpr int kKBuf = 16;      // k-buffer capacity per pixel
+#ifndef SOF_KBUF
+#define SOF_KBUF 8
+#endif
+constexpr int kKBuf = SOF_KBUF;  // k-buffer capacity per pixel
 constexpr int kRChunk = 32;    // records staged per step
 
 // ray_through_pixel (camera.hpp:42-48): normalize(R^T ((px - cx)/fx, (py - cy)/fy, 1))
@@ -167,6 +170,7 @@ struct RenderOut {
 struct Spill {
   uint64_t* keys;      // double_key(t*)
   int32_t* vals;       // Gaussian index
+  double* alpha;       // contribution alpha
   int64_t* begin;      // [slot] slice begin
   int64_t* end;        // [slot] slice end (begin + count)
   int32_t* pixel;      // [slot] pixel id
@@ -250,9 +254,10 @@ __global__ void __launch_bounds__(256) k_render(
       bi[m * 256 + tid] = bi[nbuf * 256 + tid];
     }
   };
-  auto spill_one = [&](double t, int idx) {
+  auto spill_one = [&](double t, double alpha, int idx) {
     spill.keys[slice + nspill] = double_key(t);
     spill.vals[slice + nspill] = idx;
+    spill.alpha[slice + nspill] = alpha;
     ++nspill;
   };
 
@@ -278,14 +283,14 @@ __global__ void __launch_bounds__(256) k_render(
         if (!c.ok) continue;
         ++contributing;
         if (collect) {
-          spill_one(c.t, c.idx);
+          spill_one(c.t, c.alpha, c.idx);
         } else if (nbuf == kKBuf) {
           // the buffered entries are not final yet: hand them and the rest of the
           // list to the sort-based finish (blend state so far is kept)
           collect = true;
-          for (int q = 0; q < nbuf; ++q) spill_one(bt[q * 256 + tid], bi[q * 256 + tid]);
+          for (int q = 0; q < nbuf; ++q) spill_one(bt[q * 256 + tid], ba[q * 256 + tid], bi[q * 256 + tid]);
           nbuf = 0;
-          spill_one(c.t, c.idx);
+          spill_one(c.t, c.alpha, c.idx);
         } else {
           bt[nbuf * 256 + tid] = c.t;
           ba[nbuf * 256 + tid] = c.alpha;
@@ -301,28 +306,6 @@ __global__ void __launch_bounds__(256) k_render(
   if (valid && !collect && found) {
     depth = med_t;
     if (exact_depth) depth = exact_depth_at(recs[med_idx], d, med_t, med_T, fell_back);
-  }
-  // pass 2 (non-collect pixels): O_N at the depth over all contributions
-  const bool need2 = valid && !collect && !isnan(depth);
-  double T2 = 1.0;
-  for (int64_t base = l0; base < l1; base += kRChunk) {
-    if (!__syncthreads_or(need2)) break;
-    const int cnt = int(min(int64_t(kRChunk), l1 - base));
-    for (int k = tid; k < cnt * kRecV2; k += blockDim.x) {
-      const int r = k / kRecV2, q = k % kRecV2;
-      const int32_t g = lent[base + r];
-      reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
-      if (q == 0) sidx[r] = g;
-    }
-    __syncthreads();
-    if (need2) {
-      for (int k = 0; k < cnt; ++k) {
-        if (conic_culls(srec[k], cu, cv, cuu, cvv, cuv)) continue;
-        const Contrib c = contribution(srec[k], d, sidx[k]);
-        if (!c.ok) continue;
-        T2 *= 1.0 - alpha_at(srec[k], d, c.t, depth);
-      }
-    }
   }
   if (valid) {
     const int64_t p = int64_t(py) * cam.w + px;
@@ -341,8 +324,7 @@ __global__ void __launch_bounds__(256) k_render(
       spill.istate[2 * s] = med_idx;
       spill.istate[2 * s + 1] = found;
     } else {
-      out.depth[p] = depth;
-      out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
+      out.depth[p] = depth;  // opacity at depth: k_render_opacity
       for (int k = 0; k < 3; ++k) out.rgb[3 * p + k] = col[k];
       out.tfinal[p] = T;
     }
@@ -367,9 +349,9 @@ __device__ __forceinline__ bool kv_less(uint64_t ka, int32_t va, uint64_t kb, in
   return ka < kb || (ka == kb && va < vb);
 }
 
-// Warp-wide bitonic sort of m (a power of two, 32..kFChunk) (key, index) pairs in
-// shared memory, ascending.
-__device__ __forceinline__ void warp_bitonic(uint64_t* k, int32_t* v, int m, int lane) {
+// Warp-wide bitonic sort of m (a power of two, 32..kFChunk) (key, index) pairs (with
+// their alpha) in shared memory, ascending.
+__device__ __forceinline__ void warp_bitonic(uint64_t* k, int32_t* v, double* a, int m, int lane) {
   for (int size = 2; size <= m; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncwarp();
@@ -383,6 +365,9 @@ __device__ __forceinline__ void warp_bitonic(uint64_t* k, int32_t* v, int m, int
           k[hi] = ka;
           v[lo] = vb;
           v[hi] = va;
+          const double aa = a[lo];
+          a[lo] = a[hi];
+          a[hi] = aa;
         }
       }
     }
@@ -391,16 +376,16 @@ __device__ __forceinline__ void warp_bitonic(uint64_t* k, int32_t* v, int m, int
 }
 
 // Resumes the blend of a collect-mode pixel (one warp per pixel) over its spill slice
-// in the reference's (t*, index) order (opacity_field.hpp:56-59): the slice is sorted
-// by (double_key(t*), index) in shared memory (slices longer than kFChunk: sorted
-// chunks merged by rank into keys2/vals2); contributions are evaluated lane-parallel
-// and blended serially through shuffles, and O_N at the depth multiplies the
-// tile-list factors in list order (exact: factors of 1 are skipped).
-__global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
-    Cam cam, int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
-    const Rec* __restrict__ recs, const double* __restrict__ dc, int exact_depth, Spill spill,
-    uint64_t* __restrict__ gk2, int32_t* __restrict__ gv2, RenderOut out, unsigned long long* stats) {
+// in the reference's (t*, index) order (opacity_field.hpp:56-59): the slice's
+// (double_key(t*), index, alpha) entries are sorted in shared memory (slices longer
+// than kFChunk: sorted chunks merged by rank into keys2/vals2/alpha2) and blended
+// serially through shuffles; t* is recovered from its key.
+__global__ void __launch_bounds__(kFWarps * 32, 2) k_render_finish(
+    Cam cam, const Rec* __restrict__ recs, const double* __restrict__ dc, int exact_depth, Spill spill,
+    uint64_t* __restrict__ gk2, int32_t* __restrict__ gv2, double* __restrict__ ga2, RenderOut out,
+    unsigned long long* stats) {
   __shared__ uint64_t sk[kFWarps][kFChunk];
+  __shared__ double sa[kFWarps][kFChunk];
   __shared__ int32_t sv[kFWarps][kFChunk];
   constexpr unsigned kAll = 0xffffffffu;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -408,9 +393,6 @@ __global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
   if (s >= *spill.count) return;  // warp-uniform
   const int64_t p = spill.pixel[s];
   const int px = int(p % cam.w), py = int(p / cam.w);
-  const int tile = (py / kRTile) * tiles_x + px / kRTile;
-  double d[3];
-  pixel_ray(cam, px, py, d);
   const double* st = spill.state + 6 * s;
   double T = st[0], col[3] = {st[1], st[2], st[3]}, med_t = st[4], med_T = st[5];
   int med_idx = spill.istate[2 * s];
@@ -418,6 +400,7 @@ __global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
   const int64_t b = spill.begin[s], n = spill.end[s] - b;
   uint64_t* K = sk[w];
   int32_t* V = sv[w];
+  double* A = sa[w];
   for (int64_t c0 = 0; c0 < n; c0 += kFChunk) {
     const int cn = int(min(int64_t(kFChunk), n - c0));
     int m = 32;
@@ -425,17 +408,21 @@ __global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
     for (int i = lane; i < m; i += 32) {
       K[i] = i < cn ? spill.keys[b + c0 + i] : ~0ull;
       V[i] = i < cn ? spill.vals[b + c0 + i] : 0x7fffffff;
+      A[i] = i < cn ? spill.alpha[b + c0 + i] : 0.0;
     }
-    warp_bitonic(K, V, m, lane);
+    warp_bitonic(K, V, A, m, lane);
     if (n > kFChunk) {
       for (int i = lane; i < cn; i += 32) {
         spill.keys[b + c0 + i] = K[i];
         spill.vals[b + c0 + i] = V[i];
+        spill.alpha[b + c0 + i] = A[i];
       }
       __syncwarp();
     }
   }
+  const uint64_t* SK = K;
   const int32_t* SV = V;
+  const double* SA = A;
   if (n > kFChunk) {
     // final position = position in own chunk + entries below it in every other chunk
     for (int64_t i = lane; i < n; i += 32) {
@@ -455,9 +442,12 @@ __global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
       }
       gk2[b + rank] = ki;
       gv2[b + rank] = vi;
+      ga2[b + rank] = spill.alpha[b + i];
     }
     __syncwarp();
+    SK = gk2 + b;
     SV = gv2 + b;
+    SA = ga2 + b;
   }
   for (int64_t c0 = 0; c0 < n; c0 += 32) {
     const int64_t i = c0 + lane;
@@ -465,9 +455,8 @@ __global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
     int idx = 0;
     if (i < n) {
       idx = SV[i];
-      const Contrib c = contribution(recs[idx], d, idx);
-      t = c.t;
-      al = c.alpha;
+      t = key_double(SK[i]);
+      al = SA[i];
       for (int k = 0; k < 3; ++k) dq[k] = dc[3 * idx + k];
     }
     const int cnt = int(min(int64_t(32), n - c0));
@@ -485,6 +474,8 @@ __global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
       T = next;
     }
   }
+  double d[3];
+  pixel_ray(cam, px, py, d);
   double depth = NAN;
   if (found) {
     depth = med_t;
@@ -494,35 +485,54 @@ __global__ void __launch_bounds__(kFWarps * 32) k_render_finish(
       if (fb && lane == 0) atomicAdd(stats + 3, 1ull);
     }
   }
-  double T2 = 1.0;
-  if (!isnan(depth)) {
-    const float cu = float(px) + 0.5f, cv = float(py) + 0.5f;
-    const float cuu = cu * cu, cvv = cv * cv, cuv = cu * cv;
-    for (int64_t e0 = loff[tile], l1 = loff[tile + 1]; e0 < l1; e0 += 32) {
-      const int64_t e = e0 + lane;
-      double f = 1.0;
-      if (e < l1) {
-        const int32_t g = lent[e];
-        const Rec& r = recs[g];
-        if (!conic_culls(r, cu, cv, cuu, cvv, cuv)) {
-          const Contrib c = contribution(r, d, g);
-          if (c.ok) f = 1.0 - alpha_at(r, d, c.t, depth);
-        }
-      }
-      unsigned mask = __ballot_sync(kAll, f != 1.0);
-      while (mask) {
-        const int q = __ffs(mask) - 1;
-        mask &= mask - 1;
-        T2 *= __shfl_sync(kAll, f, q);
-      }
-    }
-  }
   if (lane == 0) {
     out.depth[p] = depth;
-    out.opacity[p] = isnan(depth) ? 0.0 : 1.0 - T2;
     for (int k = 0; k < 3; ++k) out.rgb[3 * p + k] = col[k];
     out.tfinal[p] = T;
   }
+}
+
+// Pass 2 for every pixel once its depth is known (render_pixel's O_N(depth),
+// opacity_field.hpp:201-219): one CTA per tile multiplies 1 - alpha_at(depth) over the
+// tile's contributions in list order, records staged once per CTA in shared memory.
+__global__ void __launch_bounds__(256) k_render_opacity(Cam cam, int tiles_x,
+                                                        const int64_t* __restrict__ loff,
+                                                        const int32_t* __restrict__ lent,
+                                                        const Rec* __restrict__ recs, RenderOut out) {
+  __shared__ __align__(16) Rec srec[kRChunk];
+  __shared__ int32_t sidx[kRChunk];
+  const int tile = int(blockIdx.x), tid = threadIdx.x;
+  const int px = (tile % tiles_x) * kRTile + (tid % kRTile);
+  const int py = (tile / tiles_x) * kRTile + (tid / kRTile);
+  const bool valid = px < cam.w && py < cam.h;
+  const int64_t p = int64_t(py) * cam.w + px;
+  const double depth = valid ? out.depth[p] : NAN;
+  const bool need = !isnan(depth);
+  double d[3] = {0.0, 0.0, 1.0};
+  if (need) pixel_ray(cam, px, py, d);
+  const float cu = float(px) + 0.5f, cv = float(py) + 0.5f;
+  const float cuu = cu * cu, cvv = cv * cv, cuv = cu * cv;
+  double T2 = 1.0;
+  for (int64_t base = loff[tile], l1 = loff[tile + 1]; base < l1; base += kRChunk) {
+    if (!__syncthreads_or(need)) break;
+    const int cnt = int(min(int64_t(kRChunk), l1 - base));
+    for (int k = tid; k < cnt * kRecV2; k += blockDim.x) {
+      const int r = k / kRecV2, q = k % kRecV2;
+      const int32_t g = lent[base + r];
+      reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+      if (q == 0) sidx[r] = g;
+    }
+    __syncthreads();
+    if (need) {
+      for (int k = 0; k < cnt; ++k) {
+        if (conic_culls(srec[k], cu, cv, cuu, cvv, cuv)) continue;
+        const Contrib c = contribution(srec[k], d, sidx[k]);
+        if (!c.ok) continue;
+        T2 *= 1.0 - alpha_at(srec[k], d, c.t, depth);
+      }
+    }
+  }
+  if (valid) out.opacity[p] = need ? 1.0 - T2 : 0.0;
 }
 
 }  // namespace sofk
@@ -573,7 +583,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       SOF_CUDA(cudaMemcpyAsync(off.data(), c->rbind.off.p, sizeof(int64_t) * (T + 1),
                                cudaMemcpyDeviceToHost, c->stream));
     SOF_CUDA(cudaStreamSynchronize(c->stream));
-    const int64_t cap = std::min<int64_t>((int64_t(1) << 31) - 1, (int64_t(24) << 30) / 24);
+    const int64_t cap = std::min<int64_t>((int64_t(1) << 31) - 1, (int64_t(24) << 30) / 40);
     RenderScratch& rs = c->rs;
     c->r_stats.ensure(4);
     SOF_CUDA(cudaMemsetAsync(c->r_stats.p, 0, 4 * sizeof(unsigned long long), c->stream));
@@ -595,6 +605,8 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       rs.keys2.ensure(pool);
       rs.vals.ensure(pool);
       rs.vals2.ensure(pool);
+      rs.alpha.ensure(pool);
+      rs.alpha2.ensure(pool);
       rs.begin.ensure(bpx);
       rs.end.ensure(bpx);
       rs.pixel.ensure(bpx);
@@ -602,7 +614,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       rs.istate.ensure(2 * bpx);
       rs.count.ensure(1);
       SOF_CUDA(cudaMemsetAsync(rs.count.p, 0, sizeof(int32_t), c->stream));
-      Spill spill{rs.keys.p, rs.vals.p, rs.begin.p, rs.end.p, rs.pixel.p, rs.state.p, rs.istate.p, rs.count.p};
+      Spill spill{rs.keys.p, rs.vals.p, rs.alpha.p, rs.begin.p, rs.end.p, rs.pixel.p, rs.state.p, rs.istate.p, rs.count.p};
       k_render<<<unsigned(t1 - t0), 256, smem, c->stream>>>(
           cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->r_lkey.p, c->dc.p,
           depth_mode == SOF_DEPTH_EXACT, out, spill, c->r_stats.p, int(t0));
@@ -610,12 +622,17 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       const int32_t nover = read_scalar(c, rs.count.p);
       if (nover > 0) {
         k_render_finish<<<unsigned((nover + kFWarps - 1) / kFWarps), kFWarps * 32, 0, c->stream>>>(
-            cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT,
-            spill, rs.keys2.p, rs.vals2.p, out, c->r_stats.p);
+            cam, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT, spill, rs.keys2.p, rs.vals2.p, rs.alpha2.p, out,
+            c->r_stats.p);
         SOF_LAUNCHED(c);
       }
       nover_total += nover;
       t0 = t1;
+    }
+    if (T > 0) {
+      k_render_opacity<<<unsigned(T), 256, 0, c->stream>>>(cam, tiles_x, c->rbind.off.p, c->rbind.ent.p, rec,
+                                                            out);
+      SOF_LAUNCHED(c);
     }
     const int64_t nover = nover_total;
     if (depth) SOF_CUDA(cudaMemcpyAsync(depth, out.depth, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));

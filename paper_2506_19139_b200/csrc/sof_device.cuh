@@ -426,4 +426,9 @@ __host__ __device__ inline uint64_t double_key(double v) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// inverse of double_key
+__host__ __device__ inline double key_double(uint64_t k) {
+  return sof_bits_to_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
+}
+
 }  // namespace sofk

@@ -115,6 +115,7 @@ struct MeshScratch {
 // Render spill pool (k_render.cu): keys / values double-buffered for the segmented sort.
 struct RenderScratch {
   DBuf<uint64_t> keys, keys2;
+  DBuf<double> alpha, alpha2;
   DBuf<int32_t> vals, vals2, pixel, istate, count;
   DBuf<int64_t> begin, end;
   DBuf<double> state;
