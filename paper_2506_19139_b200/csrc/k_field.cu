@@ -420,19 +420,30 @@ __global__ void k_block_fill(int T, int S, const int* __restrict__ tile_off,
 // ---- K4: opacity evaluation ----------------------------------------------------------------------
 
 constexpr int kChunk = 32;  // Gaussian records staged in shared memory per step
+#ifndef SOF_EVAL_MINB
+#define SOF_EVAL_MINB 5
+#endif
 
 // One CTA = one schedule block (<= 256 points of one tile). The block's Gaussian
 // list is streamed through shared memory in chunks; every thread runs the exact
 // view_opacity loop (field_eval.hpp:86-108) for its point.
-template <int MODE, bool TILED>
-__global__ void __launch_bounds__(256, 5) k_eval(
+//
+// FAST (tile lists + min-z + dead cull, the default strategies): the per-record
+// strategy tests leave the inner loop. Dead records (op < 1/255, skipped before the
+// pair counter at field_eval.hpp:89-90) are neutralised in the shared-memory copy —
+// zmin = -inf (never ends the sorted scan) and a conic that always culls — and
+// subtracted from the pair count once per chunk through a dead mask.
+template <int MODE, bool TILED, bool FAST>
+__global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks,
     const int32_t* __restrict__ pidx, const double* __restrict__ xyz, Cam cam, int ts,
     int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
     int64_t n_gauss, const Rec* __restrict__ recs, int strategies, int classify, double* min_op,
     uint8_t* ext, double* o_out, uint8_t* obs_out, uint8_t* comp_out,
     unsigned long long* pairs_counter) {
+  static_assert(!FAST || TILED, "the fast loop relies on min_z-sorted tile lists");
   __shared__ __align__(16) Rec srec[kChunk];
+  __shared__ unsigned s_dead[2];
   const int64_t b = blockIdx.x;
   if (b >= *nblocks) return;
   const int4 blk = blocks[b];
@@ -457,17 +468,59 @@ __global__ void __launch_bounds__(256, 5) k_eval(
   double survive = 1.0;
   bool complete = true;
   bool done = !active;
-  unsigned pairs = 0;
-  for (int64_t base = l0; base < l1; base += kChunk) {
+  unsigned pairs = 0, exact = 0;
+  if (FAST && threadIdx.x < 2) s_dead[threadIdx.x] = 0;  // published by the first barrier
+  int par = 0;
+  for (int64_t base = l0; base < l1; base += kChunk, par ^= 1) {
     if (!__syncthreads_or(!done)) break;
     const int cnt = int(std::min<int64_t>(kChunk, l1 - base));
     for (int k = threadIdx.x; k < cnt * kRecV2; k += blockDim.x) {
       const int r = k / kRecV2, q = k % kRecV2;
       const int64_t g = TILED ? int64_t(lent[base + r]) : base + r;
-      reinterpret_cast<double2*>(&srec[r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+      double2 v = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+      if (FAST && q >= 5 && __ldg(&recs[g].op) < kMinAlpha) {
+        if (q == 5) {  // (op, zmin)
+          v.y = -INFINITY;
+          atomicOr(&s_dead[par], 1u << r);
+        } else if (q == 6) {  // (thr, conic0..2): g = -1
+          float4 f = *reinterpret_cast<float4*>(&v);
+          f.y = 0.0f;
+          f.z = 0.0f;
+          f.w = -1.0f;
+          v = *reinterpret_cast<double2*>(&f);
+        } else {  // (conic3..5, gmargin)
+          v = make_double2(0.0, 0.0);
+        }
+      }
+      reinterpret_cast<double2*>(&srec[r])[q] = v;
     }
+    if (FAST && threadIdx.x == 0) s_dead[par ^ 1] = 0;  // mask of the next chunk
     __syncthreads();
-    if (!done) {
+    if (done) continue;
+    if (FAST) {
+      int k = 0;
+      const Rec* rp = srec;
+      for (; k < cnt; ++k, ++rp) {
+        const Rec& r = *rp;
+        if (r.zmin > pr.zp) {  // list sorted by min_z (field_eval.hpp:91)
+          done = true;
+          break;
+        }
+        if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
+        ++exact;
+        const double alpha = pair_alpha(r, pr.d, pr.t);
+        if (alpha == 0.0) continue;
+        survive *= 1.0 - alpha;
+        if (early && 1.0 - survive > 0.5) {
+          complete = false;
+          done = true;
+          ++k;  // this pair was counted
+          break;
+        }
+      }
+      const unsigned upto = (k >= 32) ? 0xffffffffu : ((1u << k) - 1u);
+      pairs += unsigned(k) - __popc(s_dead[par] & upto);
+    } else {
       for (int k = 0; k < cnt; ++k) {
         const Rec& r = srec[k];
         if (dead_cull && r.op < kMinAlpha) continue;
@@ -480,6 +533,7 @@ __global__ void __launch_bounds__(256, 5) k_eval(
         }
         ++pairs;
         if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
+        ++exact;
         const double alpha = pair_alpha(r, pr.d, pr.t);
         if (alpha == 0.0) continue;
         survive *= 1.0 - alpha;
@@ -506,14 +560,16 @@ __global__ void __launch_bounds__(256, 5) k_eval(
     }
   }
   // pairs counter: warp reduce, one atomic per warp
-  unsigned long long p = pairs, q = active;  // pairs, point_view_evals
+  unsigned long long p = pairs, q = active, e = exact;  // pairs, point_view_evals, FP64 evals
   for (int s = 16; s > 0; s >>= 1) {
     p += __shfl_down_sync(0xffffffffu, p, s);
     q += __shfl_down_sync(0xffffffffu, q, s);
+    e += __shfl_down_sync(0xffffffffu, e, s);
   }
   if ((threadIdx.x & 31) == 0) {
     if (p) atomicAdd(pairs_counter, p);
     if (q) atomicAdd(pairs_counter + 1, q);
+    if (e) atomicAdd(pairs_counter + 2, e);
   }
 }
 
@@ -697,12 +753,16 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
       k_eval_f32<MODE, false><<<unsigned(grid), 256, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec, recf,
           strategies, classify, min_op, ext, o_out, obs, comp, pc);
-  } else if (tiled)
-    k_eval<MODE, true><<<unsigned(grid), 256, 0, c->stream>>>(
+  } else if (tiled && (strategies & 18) == 18)  // min_z + dead cull: the fast loop
+    k_eval<MODE, true, true><<<unsigned(grid), 256, 0, c->stream>>>(
+        c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
+        strategies, classify, min_op, ext, o_out, obs, comp, pc);
+  else if (tiled)
+    k_eval<MODE, true, false><<<unsigned(grid), 256, 0, c->stream>>>(
         c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
         strategies, classify, min_op, ext, o_out, obs, comp, pc);
   else
-    k_eval<MODE, false><<<unsigned(grid), 256, 0, c->stream>>>(
+    k_eval<MODE, false, false><<<unsigned(grid), 256, 0, c->stream>>>(
         c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
         strategies, classify, min_op, ext, o_out, obs, comp, pc);
   SOF_LAUNCHED(c);

@@ -404,7 +404,8 @@ __device__ __forceinline__ double pair_alpha(const Rec& r, const double* d, doub
   }
   const double arg = -0.5 * ((a * te + b) * te + r.c);  // eval_1d gaussian.hpp:47-49
   if (arg < double(r.thr)) return 0.0;                  // alpha < 1/255 certain
-  double alpha = r.op * sof_exp(arg);
+  const double e = (arg >= -700.0 && arg <= 700.0) ? sof_exp_mid(arg) : sof_exp(arg);
+  const double alpha = r.op * e;
   if (alpha < kMinAlpha) return 0.0;
   return (kMaxAlpha < alpha) ? kMaxAlpha : alpha;  // std::min(alpha, kMaxAlpha)
 }

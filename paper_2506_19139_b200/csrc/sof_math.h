@@ -102,6 +102,31 @@ SOF_HD double sof_exp(double x) {
   return SOF_MUL(y, sof_pow2i(ni));
 }
 
+#ifdef __CUDACC__
+// sof_exp's constants in constant memory: the DFMAs of sof_exp_mid take them as
+// c-bank operands instead of materialising each one with two uniform moves.
+static __constant__ double kSofExpC[15] = {
+    1.44269504088896338700e+00, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
+    1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0,
+    1.0 / 40320.0,      1.0 / 5040.0,      1.0 / 720.0,      1.0 / 120.0,     1.0 / 24.0,
+    1.0 / 6.0,          0.5};
+
+/// sof_exp for -700 <= x <= 700 (finite): the same operation sequence without the
+/// special cases, which cannot occur in this range (|n| <= 1010), so the result is
+/// bit-identical to sof_exp(x).
+__device__ __forceinline__ double sof_exp_mid(double x) {
+  const double n = rint(__dmul_rn(x, kSofExpC[0]));
+  double r = __fma_rn(-n, kSofExpC[1], x);
+  r = __fma_rn(-n, kSofExpC[2], r);
+  double q = kSofExpC[3];
+#pragma unroll
+  for (int k = 4; k < 15; ++k) q = __fma_rn(q, r, kSofExpC[k]);
+  const double p = __fma_rn(__dmul_rn(r, r), q, r);
+  const double y = __dadd_rn(1.0, p);
+  return __dmul_rn(y, sof_pow2i((int)n));
+}
+#endif
+
 /// natural log: x = 2^k m with m in [sqrt(2)/2, sqrt(2)), f = m - 1,
 /// s = f / (2 + f), log(1+f) = f - hfsq + s (hfsq + R(s^2)) with the classic
 /// minimax coefficients for R (fdlibm's Lg1..Lg7), k ln2 split hi/lo.

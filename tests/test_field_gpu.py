@@ -127,7 +127,33 @@ def test_filter_scale_and_dead(ref):
         assert_bits(views.ctx.precompute_view(v), rc.precompute()[v])
     pts = np.random.default_rng(3).uniform(-1.2, 1.2, (2000, 3))
     ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
-    assert_bits(ev.label_grid(pts), rc.evaluator(ALL).label_grid(pts))
+    rev = rc.evaluator(ALL)
+    assert_bits(ev.label_grid(pts), rev.label_grid(pts))
+    assert ev.counters() == rev.counters()
+
+
+@pytest.mark.parametrize("mask", [31, 30, 19, 18, 23])
+def test_dead_records_in_fast_loop(ref, mask):
+    """Dead Gaussians (op < 1/255, incl. one ulp-scale below the threshold) inside the
+    min-z-sorted lists: skipped before the pair counter, never ending the scan."""
+    scene = ref.random_scene(29, 400, 1.0)
+    scene.opacity[::5] = 0.002
+    scene.opacity[2::9] = (1.0 / 255.0) * (1.0 - 1e-12)
+    scene.opacity[4::13] = 1.0 / 255.0  # not dead (op < 1/255 is false)
+    cams = ref.orbit_cameras(3, 4.0, 1.8, 48)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    pts = np.random.default_rng(5).uniform(-1.2, 1.2, (3000, 3))
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.from_mask(mask))
+    rev = rc.evaluator(mask)
+    for classify in (False, True):
+        for v in range(cams.v):
+            o, ob, co = ev.view_opacity(v, pts, classify)
+            ro, rob, rco = rev.view_opacity(v, pts, classify)
+            np.testing.assert_array_equal(co, rco.astype(bool))
+            assert_bits(o[ob], ro[rob.astype(bool)], f"mask {mask} view {v}")
+    assert_bits(ev.label_grid(pts), rev.label_grid(pts))
+    assert ev.counters() == rev.counters()
 
 
 def test_single_view_mahalanobis_ball(ref):
