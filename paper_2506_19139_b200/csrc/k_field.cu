@@ -341,18 +341,27 @@ const Binding& view_binding(sof_ctx* c, int view, int tile_size) {
 // view. Order inside a tile is arbitrary; it cannot change any result because
 // every (point, view) evaluation is independent (field_eval.hpp:146-154).
 
-// Warp-aggregated atomicAdd on a per-tile counter: lanes with the same tile elect
-// one leader. Returns the slot of this lane among the lanes that hit `tile`.
-__device__ __forceinline__ int warp_tile_add(int* counters, int tile, bool valid) {
-  const unsigned active = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return 0;
-  const unsigned peers = __match_any_sync(active, tile);
+// Warp-aggregated atomicAdd on a per-bin counter (all 32 lanes call it). Candidates
+// arrive in index order, so equal bins mostly form runs of adjacent lanes: each run
+// is reserved with one atomic by its first lane (shuffle + ballot only; no
+// match.any, whose ADU throughput capped the scheduling kernels). Returns the slot
+// of this lane among the lanes of its run that hit `bin`, offset by the run's base.
+__device__ __forceinline__ int warp_tile_add(int* counters, int bin, bool valid) {
+  constexpr unsigned kAll = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int leader = __ffs(peers) - 1;
+  const int k = valid ? bin : -1;
+  const int prev = __shfl_up_sync(kAll, k, 1);
+  const unsigned bnd = __ballot_sync(kAll, lane == 0 || prev != k);  // run starts
+  const unsigned upto = (2u << lane) - 1u;                            // lanes <= this one
+  const int leader = 31 - __clz(bnd & upto);
   int base = 0;
-  if (lane == leader) base = atomicAdd(counters + tile, __popc(peers));
-  base = __shfl_sync(peers, base, leader);
-  return base + __popc(peers & ((1u << lane) - 1u));
+  if (valid && leader == lane) {
+    const unsigned after = bnd & ~upto;
+    const int end = after ? __ffs(after) - 1 : 32;
+    base = atomicAdd(counters + k, end - lane);
+  }
+  base = __shfl_sync(kAll, base, leader);
+  return base + (lane - leader);
 }
 
 // Per point: tile of the view (-1 when pruned or unobserved), histogram per tile.
