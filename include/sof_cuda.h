@@ -102,9 +102,10 @@ typedef struct sof_extract_stats {
   int64_t kernel_launches;   /* all kernels launched by the call */
   double ms_prep;            /* per-view records + Gaussian tile binning (K1, K2) */
   double ms_sched;           /* per-view point scheduling (K3) */
-  uint64_t exact_pairs;      /* pairs the FP32 filter could not certify (evaluated in FP64) */
+  uint64_t exact_pairs;      /* pairs past the screen-space cull (FP64); 0 unless built with SOF_EVAL_STATS */
   double host_ms_prep;       /* host time spent issuing per-view prep (incl. its one sync) */
   double host_ms_sched;      /* host time spent issuing per-view scheduling */
+  uint64_t contrib_pairs;    /* FP64-evaluated pairs with alpha >= 1/255; 0 unless SOF_EVAL_STATS */
 } sof_extract_stats;
 
 /* ---- context --------------------------------------------------------------- */

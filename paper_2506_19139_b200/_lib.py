@@ -38,7 +38,7 @@ class ExtractStats(ctypes.Structure):
                 ("ms_label", _D), ("ms_march", _D), ("ms_refine", _D), ("ms_weld", _D),
                 ("ms_eval_kernel", _D), ("eval_launches", _I64), ("kernel_launches", _I64),
                 ("ms_prep", _D), ("ms_sched", _D), ("exact_pairs", ctypes.c_uint64),
-                ("host_ms_prep", _D), ("host_ms_sched", _D)]
+                ("host_ms_prep", _D), ("host_ms_sched", _D), ("contrib_pairs", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

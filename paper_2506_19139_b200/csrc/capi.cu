@@ -484,6 +484,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     const int64_t launches0 = c->launches;
     c->eval_launches = 0;
     c->exact_evals = 0;
+    c->contrib_evals = 0;
     c->host_ms[0] = c->host_ms[1] = 0.0;
     c->time_eval = stats != nullptr;
     if (c->time_eval) {
@@ -538,6 +539,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     st.ms_eval_kernel = pms[kProfEval];
     st.ms_prep = pms[kProfPrep];
     st.exact_pairs = c->exact_evals;
+    st.contrib_pairs = c->contrib_evals;
     st.host_ms_prep = c->host_ms[0];
     st.host_ms_sched = c->host_ms[1];
     st.ms_sched = pms[kProfSched];

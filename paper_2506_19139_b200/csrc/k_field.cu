@@ -366,10 +366,11 @@ __device__ __forceinline__ int warp_tile_add(int* counters, int bin, bool valid)
 
 // Per point: tile of the view (-1 when pruned or unobserved), histogram per tile.
 // Candidates are all points (cand == nullptr) or a compacted list of the points not
-// yet pruned; tile_of is indexed by candidate slot.
+// yet pruned; tile_of is indexed by candidate slot. S bins per tile: 16 (4x4 pixel
+// cells) or 1.
 __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
                              const double* __restrict__ xyz, Cam cam, int ts, int tiles_x,
-                             bool single_bin, const uint8_t* __restrict__ skip, int32_t* tile_of,
+                             bool single_bin, int S, const uint8_t* __restrict__ skip, int32_t* tile_of,
                              int* tile_cnt) {
   const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   int tile = -1;
@@ -381,7 +382,9 @@ __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
       // adjacent, so a warp covers a compact screen region (coherent conic culls)
       if (pr.observed) {
         const int cs = (ts + 3) / 4;
-        tile = single_bin ? 0 : pr.tile * 16 + (((int)pr.py % ts) / cs) * 4 + ((int)pr.px % ts) / cs;
+        tile = single_bin ? 0
+               : (S == 16) ? pr.tile * 16 + (((int)pr.py % ts) / cs) * 4 + ((int)pr.px % ts) / cs
+                           : pr.tile;
       }
     }
     tile_of[k] = tile;
@@ -432,6 +435,12 @@ constexpr int kChunk = 32;  // Gaussian records staged in shared memory per step
 #ifndef SOF_EVAL_MINB
 #define SOF_EVAL_MINB 5
 #endif
+// Instrumentation counters of k_eval (pairs evaluated in FP64 / contributing): they
+// cost registers in the hot loop, so they are compiled in only on request
+// (-DSOF_EVAL_STATS=1); the reference's pair counters are always exact.
+#ifndef SOF_EVAL_STATS
+#define SOF_EVAL_STATS 0
+#endif
 
 // One CTA = one schedule block (<= 256 points of one tile). The block's Gaussian
 // list is streamed through shared memory in chunks; every thread runs the exact
@@ -477,7 +486,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
   double survive = 1.0;
   bool complete = true;
   bool done = !active;
-  unsigned pairs = 0, exact = 0;
+  unsigned pairs = 0, exact = 0, contrib = 0;
   if (FAST && threadIdx.x < 2) s_dead[threadIdx.x] = 0;  // published by the first barrier
   int par = 0;
   for (int64_t base = l0; base < l1; base += kChunk, par ^= 1) {
@@ -516,9 +525,10 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
           break;
         }
         if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
-        ++exact;
+        if (SOF_EVAL_STATS) ++exact;
         const double alpha = pair_alpha(r, pr.d, pr.t);
         if (alpha == 0.0) continue;
+        if (SOF_EVAL_STATS) ++contrib;
         survive *= 1.0 - alpha;
         if (early && 1.0 - survive > 0.5) {
           complete = false;
@@ -542,9 +552,10 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
         }
         ++pairs;
         if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
-        ++exact;
+        if (SOF_EVAL_STATS) ++exact;
         const double alpha = pair_alpha(r, pr.d, pr.t);
         if (alpha == 0.0) continue;
+        if (SOF_EVAL_STATS) ++contrib;
         survive *= 1.0 - alpha;
         if (early && 1.0 - survive > 0.5) {
           complete = false;
@@ -569,8 +580,10 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
     }
   }
   // pairs counter: warp reduce, one atomic per warp
-  unsigned long long p = pairs, q = active, e = exact;  // pairs, point_view_evals, FP64 evals
+  // pairs, point_view_evals, FP64 evals, contributing evals
+  unsigned long long p = pairs, q = active, e = exact, w = contrib;
   for (int s = 16; s > 0; s >>= 1) {
+    w += __shfl_down_sync(0xffffffffu, w, s);
     p += __shfl_down_sync(0xffffffffu, p, s);
     q += __shfl_down_sync(0xffffffffu, q, s);
     e += __shfl_down_sync(0xffffffffu, e, s);
@@ -579,6 +592,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
     if (p) atomicAdd(pairs_counter, p);
     if (q) atomicAdd(pairs_counter + 1, q);
     if (e) atomicAdd(pairs_counter + 2, e);
+    if (w) atomicAdd(pairs_counter + 3, w);
   }
 }
 
@@ -841,7 +855,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     c->host_ms[0] += std::chrono::duration<double, std::milli>(h1 - h0).count();
     // K3: group the active, observed points of this view by tile (no host sync)
     const uint8_t* skip = (prune && (mode == kModeLabel || mode == kModeClassify)) ? ext : nullptr;
-    const int S = tiled ? 16 : 1;  // bins per tile (4x4 cells)
+    // bins per tile: 4x4-pixel cells when points are dense enough to fill them (label
+    // grids), else whole tiles (bisection midpoints)
+    const int S = (tiled && ncand >= 1024 * int64_t(T)) ? 16 : 1;
     const int64_t NB = int64_t(T) * S;
     s.tile_cnt.ensure(2 * (NB + 1));
     s.tile_off.ensure(NB + 1);
@@ -851,7 +867,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     int* tile_cur = s.tile_cnt.p + (NB + 1);
     const int32_t* cand = use_list ? s.active.p : nullptr;
     k_sched_tile<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
-                                                              !tiled, skip, s.tile_of.p, s.tile_cnt.p);
+                                                              !tiled, S, skip, s.tile_of.p, s.tile_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);
     k_sched_scatter<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, s.tile_of.p, s.tile_off.p,
@@ -918,12 +934,13 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     }
   }
   if (counters_host) {
-    unsigned long long h[3];
+    unsigned long long h[4];
     SOF_CUDA(cudaMemcpyAsync(h, c->d_counters.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     SOF_CUDA(cudaStreamSynchronize(c->stream));
     counters_host[0] += h[0];
     counters_host[1] += h[1];
     c->exact_evals += h[2];
+    c->contrib_evals += h[3];
   }
 }
 

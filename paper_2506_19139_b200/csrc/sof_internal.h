@@ -163,6 +163,7 @@ struct sof_ctx {
   int scratch_sel = 0;
   int eval_path = 1;                      // 0: FP32 filter + exact FP64 replay, 1: FP64 only
   uint64_t exact_evals = 0;               // pairs that took the FP64 path (instrumentation)
+  uint64_t contrib_evals = 0;             // ... of which contributed (alpha >= 1/255)
   double host_ms[4] = {0, 0, 0, 0};       // host time in per-view prep / scheduling (instrumentation)
 
   // prep lane: a second stream (+ its own CUB scratch) for per-view preprocessing
