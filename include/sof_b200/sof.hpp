@@ -22,6 +22,7 @@
 #include <Eigen/Dense>
 
 #include <array>
+#include <cctype>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -459,6 +460,274 @@ inline DepthMap render_depth_map(const ViewSet& views, size_t view, DepthMode mo
                                 kDefaultTileSize, out.depth.data.data(), out.opacity.data.data(), nullptr,
                                 nullptr, nullptr));
   return out;
+}
+
+// camera.hpp:36-39
+struct Ray {
+  Vec3 origin = Vec3::Zero();
+  Vec3 direction = Vec3(0.0, 0.0, 1.0);  // unit length
+};
+
+// render.hpp:53-56
+struct NormalMap {
+  Grid2D<Vec3> normal;
+  Grid2D<unsigned char> valid;
+};
+
+// normal_from_depth (render.hpp:60-88) with the camera of view `view`; computed on the
+// device, bit-identical to the reference.
+inline NormalMap normal_from_depth(const Grid2D<double>& depth, const ViewSet& views, size_t view) {
+  const Camera& cam = views.cameras.at(view);
+  if (depth.width != cam.width || depth.height != cam.height)
+    throw std::invalid_argument("depth map size does not match the camera");
+  std::vector<double> n(size_t(cam.width) * cam.height * 3);
+  NormalMap out;
+  out.valid = Grid2D<unsigned char>(cam.width, cam.height, 0);
+  detail::check(views.ctx.get(), sof_normal_from_depth(views.ctx.get(), int(view), depth.data.data(), n.data(),
+                                                       out.valid.data.data()));
+  out.normal = Grid2D<Vec3>(cam.width, cam.height, Vec3::Zero());
+  for (size_t i = 0; i < out.normal.data.size(); ++i) out.normal.data[i] = Vec3(n[3 * i], n[3 * i + 1], n[3 * i + 2]);
+  return out;
+}
+
+// gaussian_normal (render.hpp:93-107) of Gaussian `index` of the ViewSet's scene, batched
+// over (index, ray, t) queries; computed on the device.
+inline std::vector<Vec3> gaussian_normals(const ViewSet& views, const std::vector<std::int32_t>& index,
+                                          const std::vector<Ray>& rays, const std::vector<double>& t) {
+  if (index.size() != rays.size() || rays.size() != t.size())
+    throw std::invalid_argument("gaussian_normals: index, rays and t differ in length");
+  std::vector<double> o, d, n(3 * rays.size());
+  for (const Ray& r : rays)
+    for (int k = 0; k < 3; ++k) {
+      o.push_back(r.origin(k));
+      d.push_back(r.direction(k));
+    }
+  detail::check(views.ctx.get(), sof_gaussian_normals(views.ctx.get(), Index(index.size()), index.data(), o.data(),
+                                                      d.data(), t.data(), n.data()));
+  std::vector<Vec3> out;
+  for (size_t i = 0; i < rays.size(); ++i) out.emplace_back(n[3 * i], n[3 * i + 1], n[3 * i + 2]);
+  return out;
+}
+
+inline Vec3 gaussian_normal(const ViewSet& views, std::int32_t index, const Ray& ray, double t) {
+  return gaussian_normals(views, {index}, {ray}, {t}).front();
+}
+
+// ---- float maps (io_maps.hpp:17-84); host-side file IO ------------------------------------
+
+struct FloatMap {
+  int width = 0, height = 0, channels = 1;
+  std::vector<float> data;  // interleaved channels, row-major
+  float& at(int x, int y, int c = 0) { return data[(size_t(y) * width + x) * channels + c]; }
+  float at(int x, int y, int c = 0) const { return data[(size_t(y) * width + x) * channels + c]; }
+};
+
+// "sofmap W H C\n" + raw little-endian float32 payload (byte-identical to the reference).
+inline void write_float_map(const FloatMap& map, const std::string& path) {
+  if (map.data.size() != size_t(map.width) * map.height * map.channels)
+    throw std::runtime_error("float map size mismatch");
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot write float map: " + path);
+  const std::string header = "sofmap " + std::to_string(map.width) + " " + std::to_string(map.height) + " " +
+                             std::to_string(map.channels) + "\n";
+  f.write(header.data(), std::streamsize(header.size()));
+  f.write(reinterpret_cast<const char*>(map.data.data()), std::streamsize(sizeof(float) * map.data.size()));
+}
+
+inline FloatMap read_float_map(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot open float map: " + path);
+  std::string magic;
+  FloatMap map;
+  std::string line;
+  if (!std::getline(f, line)) throw std::runtime_error("malformed float map header");
+  {
+    std::size_t pos = 0;
+    auto next = [&](std::string& tok) {
+      while (pos < line.size() && std::isspace(static_cast<unsigned char>(line[pos]))) ++pos;
+      const std::size_t b = pos;
+      while (pos < line.size() && !std::isspace(static_cast<unsigned char>(line[pos]))) ++pos;
+      tok = line.substr(b, pos - b);
+    };
+    std::string w, h, c;
+    next(magic);
+    next(w);
+    next(h);
+    next(c);
+    try {
+      map.width = std::stoi(w);
+      map.height = std::stoi(h);
+      map.channels = std::stoi(c);
+    } catch (...) {
+      throw std::runtime_error("malformed float map header");
+    }
+  }
+  if (magic != "sofmap" || map.width <= 0 || map.height <= 0 || map.channels <= 0)
+    throw std::runtime_error("malformed float map header");
+  map.data.resize(size_t(map.width) * map.height * map.channels);
+  f.read(reinterpret_cast<char*>(map.data.data()), std::streamsize(sizeof(float) * map.data.size()));
+  if (size_t(f.gcount()) != sizeof(float) * map.data.size()) throw std::runtime_error("truncated float map payload");
+  return map;
+}
+
+// depth + opacity at depth as two float channels
+inline FloatMap depth_to_map(const DepthMap& dm) {
+  FloatMap m{dm.depth.width, dm.depth.height, 2, {}};
+  m.data.reserve(2 * dm.depth.data.size());
+  for (size_t i = 0; i < dm.depth.data.size(); ++i) {
+    m.data.push_back(float(dm.depth.data[i]));
+    m.data.push_back(float(dm.opacity.data[i]));
+  }
+  return m;
+}
+
+inline FloatMap normals_to_map(const NormalMap& nm) {
+  FloatMap m{nm.normal.width, nm.normal.height, 3, {}};
+  m.data.reserve(3 * nm.normal.data.size());
+  for (const Vec3& n : nm.normal.data)
+    for (int k = 0; k < 3; ++k) m.data.push_back(float(n(k)));
+  return m;
+}
+
+// ---- scene files (io_scene.hpp) ---------------------------------------------------------
+
+struct SceneFile {
+  std::vector<GaussianPrimitive> gaussians;
+  std::string source_path;
+};
+
+// parse_scene (io_scene.hpp:54-134): the payload is decoded and activated on the device;
+// throws std::runtime_error with the reference's messages.
+inline SceneFile parse_scene(const std::string& path) {
+  sof_ctx* c = detail::default_ctx().get();
+  Index n = 0;
+  const int st = sof_load_scene_ply(c, path.c_str(), 0.0, &n);
+  if (st != SOF_OK) throw std::runtime_error(sof_last_error(c));
+  std::vector<double> pos(3 * n), scale(3 * n), rot(4 * n), opa(n), dc(3 * n);
+  detail::check(c, sof_get_scene(c, pos.data(), scale.data(), rot.data(), opa.data(), dc.data()));
+  SceneFile out;
+  out.source_path = path;
+  out.gaussians.resize(size_t(n));
+  for (Index i = 0; i < n; ++i) {
+    GaussianPrimitive& g = out.gaussians[size_t(i)];
+    g.position = Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]);
+    g.scale = Vec3(scale[3 * i], scale[3 * i + 1], scale[3 * i + 2]);
+    g.rotation = Quat(rot[4 * i], rot[4 * i + 1], rot[4 * i + 2], rot[4 * i + 3]);
+    g.opacity = opa[size_t(i)];
+    g.dc_color = Vec3(dc[3 * i], dc[3 * i + 1], dc[3 * i + 2]);
+  }
+  return out;
+}
+
+// write_scene (io_scene.hpp:138-181): inverse activations on the device; byte-identical.
+inline void write_scene(const std::vector<GaussianPrimitive>& gaussians, const std::string& path) {
+  sof_ctx* c = detail::default_ctx().get();
+  const size_t n = gaussians.size();
+  std::vector<double> pos(3 * n), scale(3 * n), rot(4 * n), opa(n), dc(3 * n);
+  for (size_t i = 0; i < n; ++i) {
+    const auto& g = gaussians[i];
+    for (int k = 0; k < 3; ++k) {
+      pos[3 * i + k] = g.position(k);
+      scale[3 * i + k] = g.scale(k);
+      dc[3 * i + k] = g.dc_color(k);
+    }
+    rot[4 * i] = g.rotation.w();
+    rot[4 * i + 1] = g.rotation.x();
+    rot[4 * i + 2] = g.rotation.y();
+    rot[4 * i + 3] = g.rotation.z();
+    opa[i] = g.opacity;
+  }
+  detail::check(c, sof_set_scene(c, Index(n), pos.data(), scale.data(), rot.data(), opa.data(), dc.data(), 0.0));
+  const int st = sof_write_scene_ply(c, path.c_str());
+  if (st != SOF_OK) throw std::runtime_error(sof_last_error(c));
+}
+
+// ---- mesh files (io_mesh.hpp:15-120); host-side IO ---------------------------------------
+
+enum class MeshFormat { kObj, kPlyBinary };
+
+// "v %.17g %.17g %.17g" lines then 1-based "f a b c" lines (doubles reload exactly).
+inline void write_mesh_obj(const Mesh& mesh, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot write mesh: " + path);
+  char line[128];
+  for (const Vec3& v : mesh.vertices) {
+    std::snprintf(line, sizeof line, "v %.17g %.17g %.17g\n", v(0), v(1), v(2));
+    out << line;
+  }
+  for (const auto& t : mesh.triangles) out << "f " << t[0] + 1 << " " << t[1] + 1 << " " << t[2] + 1 << "\n";
+}
+
+inline Mesh read_mesh_obj(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open mesh: " + path);
+  Mesh mesh;
+  std::string line;
+  while (std::getline(in, line)) {
+    char tok[64] = {0};
+    int used = 0;
+    if (std::sscanf(line.c_str(), "%63s%n", tok, &used) != 1) continue;
+    if (std::string(tok) == "v") {
+      double x = 0, y = 0, z = 0;
+      std::sscanf(line.c_str() + used, "%lf %lf %lf", &x, &y, &z);
+      mesh.vertices.emplace_back(x, y, z);
+    } else if (std::string(tok) == "f") {
+      int a = 0, b = 0, c = 0;
+      std::sscanf(line.c_str() + used, "%d %d %d", &a, &b, &c);
+      mesh.triangles.push_back({a - 1, b - 1, c - 1});
+    }
+  }
+  return mesh;
+}
+
+inline Mesh read_mesh_ply(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open mesh: " + path);
+  std::string line;
+  if (!std::getline(in, line) || line != "ply") throw std::runtime_error("malformed PLY header: missing magic");
+  long long nv = -1, nf = -1;
+  while (std::getline(in, line)) {
+    char word[64] = {0}, name[64] = {0};
+    long long count = 0;
+    if (std::sscanf(line.c_str(), "%63s", word) != 1) continue;
+    const std::string tok = word;
+    if (tok == "format") {
+      std::sscanf(line.c_str(), "%*s %63s", name);
+      if (std::string(name) != "binary_little_endian")
+        throw std::runtime_error(std::string("unsupported PLY format: ") + name);
+    } else if (tok == "element") {
+      std::sscanf(line.c_str(), "%*s %63s %lld", name, &count);
+      if (std::string(name) == "vertex") nv = count;
+      if (std::string(name) == "face") nf = count;
+    } else if (tok == "end_header") {
+      break;
+    }
+  }
+  if (nv < 0 || nf < 0) throw std::runtime_error("malformed PLY header: incomplete");
+  Mesh mesh;
+  for (long long i = 0; i < nv; ++i) {
+    double xyz[3];
+    in.read(reinterpret_cast<char*>(xyz), sizeof xyz);
+    if (in.gcount() != sizeof xyz) throw std::runtime_error("truncated PLY payload");
+    mesh.vertices.emplace_back(xyz[0], xyz[1], xyz[2]);
+  }
+  for (long long i = 0; i < nf; ++i) {
+    unsigned char k = 0;
+    std::int32_t idx[3];
+    in.read(reinterpret_cast<char*>(&k), 1);
+    if (in.gcount() != 1 || k != 3) throw std::runtime_error("only triangle faces supported");
+    in.read(reinterpret_cast<char*>(idx), sizeof idx);
+    if (in.gcount() != sizeof idx) throw std::runtime_error("truncated PLY payload");
+    mesh.triangles.push_back({idx[0], idx[1], idx[2]});
+  }
+  return mesh;
+}
+
+inline void write_mesh_ply(const Mesh& mesh, const std::string& path);
+
+inline void write_mesh(const Mesh& mesh, const std::string& path, MeshFormat format) {
+  if (format == MeshFormat::kObj) write_mesh_obj(mesh, path);
+  else write_mesh_ply(mesh, path);
 }
 
 // write_mesh_ply (io_mesh.hpp:55-73): byte-identical output.

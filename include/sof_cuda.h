@@ -247,6 +247,40 @@ int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);
 int sof_render_view(sof_ctx* ctx, int view, int depth_mode, int tile_size, double* depth,
                     double* opacity, double* rgb, double* t_final, uint64_t* stats);
 
+/* normal_from_depth (render.hpp:60-88) of the depth map of the last sof_render_view
+ * call for `view`, computed from the device-resident depth (no round trip; the `sof
+ * render` CLI pairs the two, sof_cli.cpp:122-125). normal [h*w*3] (zero where
+ * invalid), valid [h*w]; either may be NULL. SOF_E_STATE if that view was not the
+ * last one rendered. */
+int sof_render_normals(sof_ctx* ctx, int view, double* normal, uint8_t* valid);
+
+/* normal_from_depth (render.hpp:60-88) of a caller-supplied depth map [h*w] (NaN = no
+ * surface, core.hpp:24-26) with view's camera. */
+int sof_normal_from_depth(sof_ctx* ctx, int view, const double* depth, double* normal,
+                          uint8_t* valid);
+
+/* gaussian_normal (render.hpp:93-107) for m queries: Gaussian gidx[k] of the scene, ray
+ * (origin[3k..], dir[3k..]) at parameter t[k] -> out[3k..]. */
+int sof_gaussian_normals(sof_ctx* ctx, int64_t m, const int32_t* gidx, const double* origin,
+                         const double* dir, const double* t, double* out);
+
+/* ---- scene files (io_scene.hpp) ---------------------------------------------------- */
+/* parse_scene (io_scene.hpp:54-134): binary little-endian splatting PLY (x y z,
+ * scale_0..2 log, rot_0..3 wxyz, opacity logit, f_dc_0..2; other properties skipped by
+ * name) decoded and activated on the device straight into the context's scene, as
+ * sof_set_scene would set it (filter_scale as there). *n_out = Gaussians. Errors carry
+ * the reference's messages ("scene contains no Gaussians", "big-endian PLY is not
+ * supported", "missing required property: ...", "truncated PLY payload", "degenerate
+ * rotation quaternion", "non-finite value after activation", "malformed PLY header..."). */
+int sof_load_scene_ply(sof_ctx* ctx, const char* path, double filter_scale, int64_t* n_out);
+
+/* The context's scene as GaussianPrimitive fields (SoA; any pointer may be NULL). */
+int sof_get_scene(sof_ctx* ctx, double* pos, double* scale, double* rot_wxyz, double* opacity, double* dc);
+
+/* write_scene (io_scene.hpp:138-181) of the context's scene: inverse activations on
+ * the device, float32 records; byte-identical to the reference writer. */
+int sof_write_scene_ply(sof_ctx* ctx, const char* path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,7 +24,9 @@
 
 #include "sof/bench.hpp"
 #include "sof/extract.hpp"
+#include "sof/io_maps.hpp"
 #include "sof/io_mesh.hpp"
+#include "sof/io_scene.hpp"
 #include "sof/render.hpp"
 #include "test_util.hpp"
 
@@ -515,6 +517,83 @@ int sofref_write_mesh_ply(long nverts, const double* verts, long ntris, const in
   }
 }
 
+/// write_mesh_obj (io_mesh.hpp:19-29)
+int sofref_write_mesh_obj(long nverts, const double* verts, long ntris, const int32_t* tris, const char* path) {
+  try {
+    Mesh m;
+    m.vertices = to_points(nverts, verts);
+    m.triangles.resize(ntris);
+    for (long i = 0; i < ntris; ++i) m.triangles[i] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+    write_mesh_obj(m, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+/// read_mesh_ply (io_mesh.hpp:75-113) -> bag{vertices f64, triangles int32} or NULL (message in last_error)
+void* sofref_read_mesh_ply(const char* path) {
+  try {
+    const Mesh m = read_mesh_ply(path);
+    auto* bag = new Bag;
+    std::vector<double> v;
+    std::vector<int32_t> t;
+    for (const auto& p : m.vertices)
+      for (int k = 0; k < 3; ++k) v.push_back(p(k));
+    for (const auto& f : m.triangles)
+      for (int k = 0; k < 3; ++k) t.push_back(f[k]);
+    bag->put("vertices", v);
+    bag->put("triangles", t);
+    return bag;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+/// parse_scene (io_scene.hpp:54-134) -> bag{pos, scale, rot (wxyz), opacity, dc} or NULL
+void* sofref_parse_scene(const char* path) {
+  try {
+    const SceneFile sf = parse_scene(path);
+    auto* bag = new Bag;
+    std::vector<double> pos, scale, rot, op, dc;
+    for (const auto& g : sf.gaussians) {
+      for (int k = 0; k < 3; ++k) {
+        pos.push_back(g.position(k));
+        scale.push_back(g.scale(k));
+        dc.push_back(g.dc_color(k));
+      }
+      rot.push_back(g.rotation.w());
+      rot.push_back(g.rotation.x());
+      rot.push_back(g.rotation.y());
+      rot.push_back(g.rotation.z());
+      op.push_back(g.opacity);
+    }
+    bag->put("pos", pos);
+    bag->put("scale", scale);
+    bag->put("rot", rot);
+    bag->put("opacity", op);
+    bag->put("dc", dc);
+    return bag;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+/// write_scene (io_scene.hpp:138-181)
+int sofref_write_scene(int n, const double* pos, const double* scale, const double* rot, const double* opa,
+                       const double* dc, const char* path) {
+  try {
+    write_scene(to_scene(n, pos, scale, rot, opa, dc), path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // ---- render -------------------------------------------------------------------------
 
 /// render_depth_map (render.hpp:26-51) for one view. depth/opacity: [h*w] row-major.
@@ -576,6 +655,59 @@ void sofref_render_pixels(const sofref_ctx* c, int view, int exact, long n, cons
     tfinal[i] = p.transmittance_final;
     ncontrib[i] = int32_t(contribs.size());
   }
+}
+
+/// normal_from_depth (render.hpp:60-88) of a [h*w] depth map for view's camera.
+/// out: normal[3*h*w] (zero where invalid), valid[h*w]
+void sofref_normal_from_depth(const sofref_ctx* c, int view, const double* depth, double* normal,
+                              uint8_t* valid) {
+  const Camera& cam = c->views.cameras[view];
+  Grid2D<double> g(cam.width, cam.height, 0.0);
+  std::memcpy(g.data.data(), depth, sizeof(double) * g.data.size());
+  const NormalMap nm = normal_from_depth(g, cam);
+  for (size_t i = 0; i < nm.normal.data.size(); ++i) {
+    for (int k = 0; k < 3; ++k) normal[3 * i + k] = nm.normal.data[i](k);
+    valid[i] = nm.valid.data[i];
+  }
+}
+
+/// gaussian_normal (render.hpp:93-107) for m (gaussian, ray origin, ray direction, t)
+void sofref_gaussian_normals(const sofref_ctx* c, long m, const int32_t* gidx, const double* o,
+                             const double* d, const double* t, double* out) {
+  for (long k = 0; k < m; ++k) {
+    const Ray ray{Vec3(o[3 * k], o[3 * k + 1], o[3 * k + 2]), Vec3(d[3 * k], d[3 * k + 1], d[3 * k + 2])};
+    const Vec3 n = gaussian_normal(c->gaussians[gidx[k]], ray, t[k]);
+    for (int i = 0; i < 3; ++i) out[3 * k + i] = n(i);
+  }
+}
+
+/// The reference `sof render` per-view output (sof_cli.cpp:122-130): render_depth_map,
+/// normal_from_depth, and the two float maps written by write_float_map.
+void sofref_render_maps(const sofref_ctx* c, int view, int exact, int threads, const char* depth_path,
+                        const char* normal_path) {
+  const Camera& cam = c->views.cameras[view];
+  std::unique_ptr<ThreadPool> pool;
+  if (threads > 0) pool = std::make_unique<ThreadPool>(unsigned(threads));
+  const DepthMap dm = render_depth_map(c->views.caches[view], cam,
+                                       exact ? DepthMode::kExact : DepthMode::kMedian, pool.get());
+  const NormalMap nm = normal_from_depth(dm.depth, cam);
+  write_float_map(depth_to_map(dm), depth_path);
+  write_float_map(normals_to_map(nm), normal_path);
+}
+
+/// write_float_map (io_maps.hpp:30-38) of a raw float buffer; 0 on success, 1 on throw
+int sofref_write_float_map(int w, int h, int ch, const float* data, const char* path) {
+  FloatMap m;
+  m.width = w;
+  m.height = h;
+  m.channels = ch;
+  m.data.assign(data, data + size_t(std::max(w, 0)) * std::max(h, 0) * std::max(ch, 0));
+  try {
+    write_float_map(m, path);
+  } catch (...) {
+    return 1;
+  }
+  return 0;
 }
 
 /// collect_contributions (opacity_field.hpp:39-61) for one pixel ->

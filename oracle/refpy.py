@@ -133,14 +133,32 @@ class RefLib:
         L.sofref_seed_delaunay.argtypes = [_P, _I, _I]
         L.sofref_extract_full.restype = _P
         L.sofref_extract_full.argtypes = [_P, _I, _I, _I, _I]
+        L.sofref_write_mesh_obj.restype = _I
+        L.sofref_write_mesh_obj.argtypes = [_L, _P, _L, _P, ctypes.c_char_p]
+        L.sofref_read_mesh_ply.restype = _P
+        L.sofref_read_mesh_ply.argtypes = [ctypes.c_char_p]
+        L.sofref_parse_scene.restype = _P
+        L.sofref_parse_scene.argtypes = [ctypes.c_char_p]
+        L.sofref_write_scene.restype = _I
+        L.sofref_write_scene.argtypes = [_I, _P, _P, _P, _P, _P, ctypes.c_char_p]
         L.sofref_write_mesh_ply.restype = _I
         L.sofref_write_mesh_ply.argtypes = [_L, _P, _L, _P, ctypes.c_char_p]
         L.sofref_render_depth_map.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
         L.sofref_render_pixels.argtypes = [_P, _I, _I, _L, _P, _P, _P, _P, _P, _P]
+        L.sofref_normal_from_depth.argtypes = [_P, _I, _P, _P, _P]
+        L.sofref_gaussian_normals.argtypes = [_P, _L, _P, _P, _P, _P, _P]
+        L.sofref_render_maps.argtypes = [_P, _I, _I, _I, ctypes.c_char_p, ctypes.c_char_p]
+        L.sofref_write_float_map.argtypes = [_I, _I, _I, _P, ctypes.c_char_p]
+        L.sofref_write_float_map.restype = _I
         L.sofref_collect_contributions.restype = _P
         L.sofref_collect_contributions.argtypes = [_P, _I, _I, _I]
 
     # ---- fixtures ----
+    def write_float_map(self, width: int, height: int, channels: int, data, path: str) -> int:
+        """write_float_map (io_maps.hpp:30-38); returns 1 when the reference throws."""
+        data = np.ascontiguousarray(data, np.float32)
+        return self.lib.sofref_write_float_map(width, height, channels, _ptr(data), path.encode())
+
     def random_scene(self, seed: int, count: int, extent: float = 1.0) -> Scene:
         s = Scene.empty(count)
         self.lib.sofref_random_scene(seed, count, extent, *(_ptr(a) for a in (s.pos, s.scale, s.rot, s.opacity, s.dc)))
@@ -208,6 +226,29 @@ class RefLib:
         verts = np.ascontiguousarray(verts, np.float64)
         tris = np.ascontiguousarray(tris, np.int32)
         if self.lib.sofref_write_mesh_ply(len(verts), _ptr(verts), len(tris), _ptr(tris), path.encode()):
+            raise RuntimeError(self.lib.sofref_last_error().decode())
+
+
+    def write_mesh_obj(self, verts, tris, path: str) -> None:
+        verts = np.ascontiguousarray(verts, np.float64)
+        tris = np.ascontiguousarray(tris, np.int32)
+        if self.lib.sofref_write_mesh_obj(len(verts), _ptr(verts), len(tris), _ptr(tris), path.encode()):
+            raise RuntimeError(self.lib.sofref_last_error().decode())
+
+    def read_mesh_ply(self, path: str):
+        b = self._bag(self.lib.sofref_read_mesh_ply(path.encode()), {"vertices": np.float64, "triangles": np.int32})
+        return b["vertices"].reshape(-1, 3), b["triangles"].reshape(-1, 3)
+
+    def parse_scene(self, path: str) -> Scene:
+        """parse_scene (io_scene.hpp:54-134); RuntimeError with the reference's message."""
+        b = self._bag(self.lib.sofref_parse_scene(path.encode()),
+                      {k: np.float64 for k in ("pos", "scale", "rot", "opacity", "dc")})
+        return Scene(b["pos"].reshape(-1, 3), b["scale"].reshape(-1, 3), b["rot"].reshape(-1, 4), b["opacity"],
+                     b["dc"].reshape(-1, 3))
+
+    def write_scene(self, scene: Scene, path: str) -> None:
+        s = [np.ascontiguousarray(a, np.float64) for a in (scene.pos, scene.scale, scene.rot, scene.opacity, scene.dc)]
+        if self.lib.sofref_write_scene(len(s[3]), *(_ptr(a) for a in s), path.encode()):
             raise RuntimeError(self.lib.sofref_last_error().decode())
 
 
@@ -286,6 +327,24 @@ class RefContext:
         opac = np.zeros((h, w))
         self.ref.lib.sofref_render_depth_map(self.h, view, int(exact), r0, r1, threads, _ptr(depth), _ptr(opac))
         return depth, opac
+
+    def normal_from_depth(self, view: int, depth):
+        w, h = (int(x) for x in self.cams.wh[view])
+        depth = np.ascontiguousarray(depth, np.float64).reshape(h, w)
+        normal, valid = np.zeros((h, w, 3)), np.zeros((h, w), np.uint8)
+        self.ref.lib.sofref_normal_from_depth(self.h, view, _ptr(depth), _ptr(normal), _ptr(valid))
+        return normal, valid
+
+    def gaussian_normals(self, gidx, origin, direction, t):
+        gidx = np.ascontiguousarray(gidx, np.int32)
+        o, d = (np.ascontiguousarray(a, np.float64).reshape(-1, 3) for a in (origin, direction))
+        t = np.ascontiguousarray(t, np.float64)
+        out = np.zeros((len(gidx), 3))
+        self.ref.lib.sofref_gaussian_normals(self.h, len(gidx), *(_ptr(a) for a in (gidx, o, d, t, out)))
+        return out
+
+    def render_maps(self, view: int, depth_path: str, normal_path: str, exact: bool = True, threads: int = 0):
+        self.ref.lib.sofref_render_maps(self.h, view, int(exact), threads, depth_path.encode(), normal_path.encode())
 
     def render_pixels(self, view: int, pix, exact: bool = True) -> dict:
         pix = np.ascontiguousarray(pix, np.int32)

@@ -70,6 +70,12 @@ _SIGS = {
     "sof_result_count": (_I64, [_P, _I]),
     "sof_copy_result": (_I, [_P, _I, _P]),
     "sof_render_view": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "sof_render_normals": (_I, [_P, _I, _P, _P]),
+    "sof_normal_from_depth": (_I, [_P, _I, _P, _P, _P]),
+    "sof_gaussian_normals": (_I, [_P, ctypes.c_int64, _P, _P, _P, _P, _P]),
+    "sof_load_scene_ply": (_I, [_P, ctypes.c_char_p, _D, _P]),
+    "sof_get_scene": (_I, [_P, _P, _P, _P, _P, _P]),
+    "sof_write_scene_ply": (_I, [_P, ctypes.c_char_p]),
     "sof_validate_tets_dev": (_I, [_P, _I64, _P, _I64]),
     "sof_event_record": (_I, [_P, _I]),
     "sof_event_elapsed": (_I, [_P, _I, _I, ctypes.POINTER(ctypes.c_float)]),

@@ -193,6 +193,31 @@ class Context:
                                           _ptr(s.dc), float(filter_scale)))
         self.scene = s
 
+    def load_scene_ply(self, path: str, filter_scale: float = 0.0) -> "GaussianScene":
+        """parse_scene (io_scene.hpp:54-134) decoded and activated on the device into this
+        context's scene; returns the activated parameters."""
+        n = ctypes.c_int64(0)
+        self.scene = None
+        self.check(self.lib.sof_load_scene_ply(self.h, str(path).encode(), float(filter_scale), ctypes.byref(n)))
+        self.scene = self.get_scene(int(n.value))
+        return self.scene
+
+    def get_scene(self, n: int | None = None) -> "GaussianScene":
+        """The context's scene as activated GaussianPrimitive fields (device -> host)."""
+        if n is None:
+            if self.scene is None:
+                raise SofError("no scene: call set_scene or load_scene_ply first")
+            n = self.scene.n
+        s = GaussianScene(np.empty((n, 3)), np.empty((n, 3)), np.empty((n, 4)), np.empty(n), np.empty((n, 3)))
+        self.check(self.lib.sof_get_scene(self.h, _ptr(s.pos), _ptr(s.scale), _ptr(s.rot), _ptr(s.opacity),
+                                          _ptr(s.dc)))
+        return s
+
+    def write_scene_ply(self, path: str):
+        """write_scene (io_scene.hpp:138-181) of this context's scene (inverse activations on
+        the device); byte-identical to the reference writer."""
+        self.check(self.lib.sof_write_scene_ply(self.h, str(path).encode()))
+
     def set_views(self, cams):
         c = CameraSet.of(cams)
         self.check(self.lib.sof_set_views(self.h, c.v, _ptr(c.R), _ptr(c.t), _ptr(c.intr), _ptr(c.wh), _ptr(c.nearfar)))
@@ -382,20 +407,124 @@ def extract_resident(ctx: Context, opt: ExtractOptions, stats: dict | None = Non
     return Mesh(ctx.result(L.R_MESH_VERTS, np.float64, 3), ctx.result(L.R_MESH_TRIS, np.int32, 3))
 
 
-def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile_size: int = 16) -> dict:
-    """render_depth_map (render.hpp:26-51) + render_pixel colour / T (opacity_field.hpp:201-219)."""
+def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile_size: int = 16,
+                normals: bool = False) -> dict:
+    """render_depth_map (render.hpp:26-51) + render_pixel colour / T (opacity_field.hpp:201-219);
+    with normals=True also normal_from_depth (render.hpp:60-88) of the depth, computed on
+    the device from the resident depth map."""
     ctx = views.ctx
     w, h = (int(x) for x in ctx.cams.wh[view])
     out = {"depth": np.empty((h, w)), "opacity": np.empty((h, w)), "rgb": np.empty((h, w, 3)),
            "t_final": np.empty((h, w)), "stats": np.zeros(4, np.uint64)}
     ctx.check(ctx.lib.sof_render_view(ctx.h, view, depth_mode, tile_size, _ptr(out["depth"]), _ptr(out["opacity"]),
                                       _ptr(out["rgb"]), _ptr(out["t_final"]), _ptr(out["stats"])))
+    if normals:
+        out["normal"] = np.empty((h, w, 3))
+        out["normal_valid"] = np.empty((h, w), np.uint8)
+        ctx.check(ctx.lib.sof_render_normals(ctx.h, view, _ptr(out["normal"]), _ptr(out["normal_valid"])))
     return out
 
 
 def render_depth_map(views: ViewSet, view: int, exact: bool = True):
     r = render_view(views, view, L.DEPTH_EXACT if exact else L.DEPTH_MEDIAN)
     return r["depth"], r["opacity"]
+
+
+def normal_from_depth(views: ViewSet, view: int, depth):
+    """normal_from_depth (render.hpp:60-88) of a depth map [h, w] (NaN = no surface) with the
+    camera of `view`. Returns (normal [h, w, 3], valid [h, w] uint8)."""
+    ctx = views.ctx
+    w, h = (int(x) for x in ctx.cams.wh[view])
+    depth = np.ascontiguousarray(depth, np.float64)
+    if depth.shape != (h, w):
+        raise ValueError(f"depth map must be {h}x{w}")
+    normal, valid = np.empty((h, w, 3)), np.empty((h, w), np.uint8)
+    ctx.check(ctx.lib.sof_normal_from_depth(ctx.h, view, _ptr(depth), _ptr(normal), _ptr(valid)))
+    return normal, valid
+
+
+def gaussian_normal(ctx: Context, gidx, origin, direction, t):
+    """gaussian_normal (render.hpp:93-107), batched: Gaussian gidx[k], ray (origin[k],
+    direction[k]) at parameter t[k]."""
+    gidx = np.ascontiguousarray(np.atleast_1d(gidx), np.int32)
+    o = np.ascontiguousarray(origin, np.float64).reshape(-1, 3)
+    d = np.ascontiguousarray(direction, np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(np.atleast_1d(t), np.float64)
+    if not (len(o) == len(d) == len(t) == len(gidx)):
+        raise ValueError("gidx, origin, direction and t must have the same length")
+    out = np.empty((len(gidx), 3))
+    ctx.check(ctx.lib.sof_gaussian_normals(ctx.h, len(gidx), *(_ptr(a) for a in (gidx, o, d, t, out))))
+    return out
+
+
+# ---- float maps (io_maps.hpp) ----------------------------------------------------------------
+
+@dataclass
+class FloatMap:
+    """`channels` interleaved float32 values per pixel, row-major (io_maps.hpp:17-29)."""
+    width: int = 0
+    height: int = 0
+    channels: int = 1
+    data: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+
+
+def write_float_map(m: FloatMap, path: str):
+    """write_float_map (io_maps.hpp:30-38): ASCII header "sofmap W H C\n" then the raw
+    little-endian float32 payload; byte-identical to the reference writer."""
+    data = np.ascontiguousarray(m.data, "<f4").ravel()
+    if data.size != m.width * m.height * m.channels:
+        raise RuntimeError("float map size mismatch")
+    try:
+        f = open(path, "wb")
+    except OSError:
+        raise RuntimeError(f"cannot write float map: {path}") from None
+    with f:
+        f.write(f"sofmap {m.width} {m.height} {m.channels}\n".encode())
+        f.write(data.tobytes())
+
+
+def read_float_map(path: str) -> FloatMap:
+    """read_float_map (io_maps.hpp:40-58), same error messages."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise RuntimeError(f"cannot open float map: {path}") from None
+    with f:
+        line = f.readline()
+        parts = line.decode("latin-1").split()
+        try:
+            magic, w, h, c = parts[0], int(parts[1]), int(parts[2]), int(parts[3])
+        except (IndexError, ValueError):
+            raise RuntimeError("malformed float map header") from None
+        if magic != "sofmap" or w <= 0 or h <= 0 or c <= 0:
+            raise RuntimeError("malformed float map header")
+        payload = f.read(4 * w * h * c)
+        if len(payload) != 4 * w * h * c:
+            raise RuntimeError("truncated float map payload")
+    return FloatMap(w, h, c, np.frombuffer(payload, "<f4").copy())
+
+
+def depth_to_map(depth, opacity) -> FloatMap:
+    """depth_to_map (io_maps.hpp:60-72): channels (depth, opacity at depth) as float32."""
+    depth, opacity = np.asarray(depth, np.float64), np.asarray(opacity, np.float64)
+    h, w = depth.shape
+    return FloatMap(w, h, 2, np.stack([depth, opacity], -1).astype(np.float32).ravel())
+
+
+def normals_to_map(normal) -> FloatMap:
+    """normals_to_map (io_maps.hpp:74-84)."""
+    normal = np.asarray(normal, np.float64)
+    h, w, _ = normal.shape
+    return FloatMap(w, h, 3, normal.astype(np.float32).ravel())
+
+
+def render_maps(views: ViewSet, view: int, depth_path: str, normal_path: str, exact: bool = True):
+    """The per-view output of the reference `sof render` (sof_cli.cpp:122-130): depth +
+    opacity-at-depth map and normal map, rendered and differentiated on the device."""
+    r = render_view(views, view, L.DEPTH_EXACT if exact else L.DEPTH_MEDIAN, normals=True)
+    write_float_map(depth_to_map(r["depth"], r["opacity"]), depth_path)
+    write_float_map(normals_to_map(r["normal"]), normal_path)
+    return r
 
 
 def write_mesh_ply(mesh: Mesh, path: str):
@@ -415,3 +544,99 @@ def write_mesh_ply(mesh: Mesh, path: str):
         f.write(header)
         f.write(v.astype("<f8").tobytes())
         f.write(faces.tobytes())
+
+
+def read_mesh_ply(path: str) -> Mesh:
+    """read_mesh_ply (io_mesh.hpp:75-113), same error messages."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise RuntimeError(f"cannot open mesh: {path}") from None
+    with f:
+        if f.readline().rstrip(b"\n") != b"ply":
+            raise RuntimeError("malformed PLY header: missing magic")
+        nv = nf = -1
+        while True:
+            line = f.readline()
+            if not line:
+                break
+            tk = line.decode("latin-1").split()
+            if not tk:
+                continue
+            if tk[0] == "format" and (len(tk) < 2 or tk[1] != "binary_little_endian"):
+                raise RuntimeError("unsupported PLY format: " + (tk[1] if len(tk) > 1 else ""))
+            if tk[0] == "element" and len(tk) > 2:
+                if tk[1] == "vertex":
+                    nv = int(tk[2])
+                if tk[1] == "face":
+                    nf = int(tk[2])
+            if tk[0] == "end_header":
+                break
+        if nv < 0 or nf < 0:
+            raise RuntimeError("malformed PLY header: incomplete")
+        vb = f.read(24 * nv)
+        if len(vb) != 24 * nv:
+            raise RuntimeError("truncated PLY payload")
+        fb = f.read(13 * nf)
+    faces = np.frombuffer(fb[: 13 * (len(fb) // 13)], dtype=[("n", "u1"), ("i", "<i4", 3)])
+    bad = np.nonzero(faces["n"] != 3)[0]
+    full = len(faces)
+    if len(bad) and bad[0] < full:
+        raise RuntimeError("only triangle faces supported")
+    if full < nf:
+        # a short read: the count byte (if present) is checked before the indices
+        rest = fb[13 * full:]
+        if len(rest) == 0 or rest[0] != 3:
+            raise RuntimeError("only triangle faces supported")
+        raise RuntimeError("truncated PLY payload")
+    return Mesh(np.frombuffer(vb, "<f8").reshape(-1, 3).copy(), faces["i"].astype(np.int32).copy())
+
+
+def write_mesh_obj(mesh: Mesh, path: str):
+    """write_mesh_obj (io_mesh.hpp:19-29): "v %.17g %.17g %.17g" and 1-based faces."""
+    v = _f64(mesh.vertices, 3) if len(mesh.vertices) else np.zeros((0, 3))
+    t = np.ascontiguousarray(mesh.triangles, np.int64).reshape(-1, 3)
+    try:
+        f = open(path, "w", newline="\n")
+    except OSError:
+        raise RuntimeError(f"cannot write mesh: {path}") from None
+    with f:
+        f.writelines("v %.17g %.17g %.17g\n" % (x, y, z) for x, y, z in v.tolist())
+        f.writelines(f"f {a + 1} {b + 1} {c + 1}\n" for a, b, c in t.tolist())
+
+
+def read_mesh_obj(path: str) -> Mesh:
+    """read_mesh_obj (io_mesh.hpp:31-51): v / f records, other lines ignored."""
+    try:
+        f = open(path)
+    except OSError:
+        raise RuntimeError(f"cannot open mesh: {path}") from None
+    vs, ts = [], []
+    with f:
+        for line in f:
+            tk = line.split()
+            if not tk:
+                continue
+            if tk[0] == "v":
+                vs.append([float(x) for x in tk[1:4]])
+            elif tk[0] == "f":
+                ts.append([int(x) - 1 for x in tk[1:4]])
+    return Mesh(np.array(vs, np.float64).reshape(-1, 3), np.array(ts, np.int32).reshape(-1, 3))
+
+
+def write_mesh(mesh: Mesh, path: str, fmt: str = "ply"):
+    """write_mesh (io_mesh.hpp:115-120): fmt "obj" or "ply" (binary)."""
+    (write_mesh_obj if fmt == "obj" else write_mesh_ply)(mesh, path)
+
+
+def parse_scene(path: str, ctx: Context | None = None, filter_scale: float = 0.0) -> GaussianScene:
+    """parse_scene (io_scene.hpp:54-134), decoded and activated on the device of `ctx`
+    (default context), which keeps the scene resident."""
+    return (ctx or default_context()).load_scene_ply(path, filter_scale)
+
+
+def write_scene(scene, path: str, ctx: Context | None = None):
+    """write_scene (io_scene.hpp:138-181) via the device of `ctx`; byte-identical file."""
+    c = ctx or default_context()
+    c.set_scene(scene)
+    c.write_scene_ply(path)

@@ -19,36 +19,6 @@ using namespace sofk;
 
 namespace {
 
-template <typename F>
-int guard(sof_ctx* c, F&& f) {
-  try {
-    if (c) SOF_CUDA(cudaSetDevice(c->device));
-    f();
-    return SOF_OK;
-  } catch (const InvalidArg& e) {
-    if (c) c->err = e.what();
-    return SOF_E_INVALID;
-  } catch (const std::invalid_argument& e) {
-    if (c) c->err = e.what();
-    return SOF_E_INVALID;
-  } catch (const StateError& e) {
-    if (c) c->err = e.what();
-    return SOF_E_STATE;
-  } catch (const OomError& e) {
-    if (c) c->err = e.what();
-    return SOF_E_OOM;
-  } catch (const CudaError& e) {
-    if (c) c->err = e.what();
-    return SOF_E_CUDA;
-  } catch (const std::bad_alloc&) {
-    if (c) c->err = "host allocation failed";
-    return SOF_E_OOM;
-  } catch (const std::exception& e) {
-    if (c) c->err = e.what();
-    return SOF_E_RUNTIME;
-  }
-}
-
 template <typename T>
 void upload(sof_ctx* c, DBuf<T>& dst, const T* src, size_t count) {
   dst.ensure(std::max<size_t>(count, 1));

@@ -535,6 +535,108 @@ __global__ void __launch_bounds__(256) k_render_opacity(Cam cam, int tiles_x,
   if (valid) out.opacity[p] = need ? 1.0 - T2 : 0.0;
 }
 
+// ---- normals (render.hpp:58-107) ---------------------------------------------------------------
+
+// ray_through_pixel(cam, x + 0.5, y + 0.5).origin + depth * direction (render.hpp:64-67)
+__device__ __forceinline__ void backproject(const Cam& cam, int x, int y, double depth, double* p) {
+  double d[3];
+  pixel_ray(cam, x, y, d);
+  for (int i = 0; i < 3; ++i) p[i] = cam.center[i] + depth * d[i];
+}
+
+// normal_from_depth (render.hpp:60-88): forward differences of the back-projected depth
+// map, cross product, camera-facing. One thread per pixel; the last row and column and
+// pixels with a no-surface neighbour stay invalid with a zero normal.
+__global__ void k_normal_from_depth(Cam cam, const double* __restrict__ depth, double* normal,
+                                    uint8_t* valid) {
+  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= int64_t(cam.w) * cam.h) return;
+  const int x = int(p % cam.w), y = int(p / cam.w);
+  double n[3] = {0.0, 0.0, 0.0};
+  uint8_t ok = 0;
+  if (x + 1 < cam.w && y + 1 < cam.h) {
+    const double d00 = depth[p], d10 = depth[p + 1], d01 = depth[p + cam.w];
+    if (!isnan(d00) && !isnan(d10) && !isnan(d01)) {  // is_no_surface (core.hpp:26)
+      double p0[3], p1[3], p2[3], dx[3], dy[3];
+      backproject(cam, x, y, d00, p0);
+      backproject(cam, x + 1, y, d10, p1);
+      backproject(cam, x, y + 1, d01, p2);
+      for (int i = 0; i < 3; ++i) {
+        dx[i] = p1[i] - p0[i];
+        dy[i] = p2[i] - p0[i];
+      }
+      double c[3] = {dx[1] * dy[2] - dx[2] * dy[1], dx[2] * dy[0] - dx[0] * dy[2],
+                     dx[0] * dy[1] - dx[1] * dy[0]};
+      const double len = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+      if (!(len < 1e-14)) {
+        for (int i = 0; i < 3; ++i) c[i] = c[i] / len;
+        double v[3] = {p0[0] - cam.center[0], p0[1] - cam.center[1], p0[2] - cam.center[2]};
+        const double vz = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+        if (vz > 0.0) {
+          const double vn = sqrt(vz);
+          for (int i = 0; i < 3; ++i) v[i] = v[i] / vn;
+        }
+        if (c[0] * v[0] + c[1] * v[1] + c[2] * v[2] > 0.0)
+          for (int i = 0; i < 3; ++i) c[i] = -c[i];
+        for (int i = 0; i < 3; ++i) n[i] = c[i];
+        ok = 1;
+      }
+    }
+  }
+  for (int i = 0; i < 3; ++i) normal[3 * p + i] = n[i];
+  valid[p] = ok;
+}
+
+// gaussian_normal (render.hpp:93-107) for m (Gaussian, ray, t) queries: normalised
+// inv_cov (x - mu) with inv_cov = R diag(1 / max(s, 1e-8)^2) R^T, the shortest-scale
+// axis when it vanishes, flipped to face the camera.
+__global__ void k_gaussian_normal(int64_t m, const int32_t* __restrict__ gidx,
+                                  const double* __restrict__ pos, const double* __restrict__ scale,
+                                  const double* __restrict__ rot, const double* __restrict__ ro,
+                                  const double* __restrict__ rd, const double* __restrict__ tq,
+                                  double* out) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= m) return;
+  const int64_t g = gidx[k];
+  double r[9];
+  quat_to_rot(rot[4 * g], rot[4 * g + 1], rot[4 * g + 2], rot[4 * g + 3], r);
+  double inv[3];
+  for (int i = 0; i < 3; ++i) {
+    const double sc = scale[3 * g + i];
+    const double s = (sc < 1e-8) ? 1e-8 : sc;  // cwiseMax(kMinScale)
+    inv[i] = 1.0 / (s * s);
+  }
+  double m1[9], ic[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) m1[3 * i + j] = r[3 * i + j] * inv[j];  // r * diag
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      ic[3 * i + j] = m1[3 * i] * r[3 * j] + m1[3 * i + 1] * r[3 * j + 1] + m1[3 * i + 2] * r[3 * j + 2];
+  const double t = tq[k];
+  double diff[3];
+  for (int i = 0; i < 3; ++i) diff[i] = (ro[3 * k + i] + t * rd[3 * k + i]) - pos[3 * g + i];
+  double n[3];
+  for (int i = 0; i < 3; ++i) n[i] = ic[3 * i] * diff[0] + ic[3 * i + 1] * diff[1] + ic[3 * i + 2] * diff[2];
+  if (sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]) < 1e-12) {
+    int axis = 0;  // minCoeff(&axis): first minimum of the raw scales
+    double mn = scale[3 * g];
+    for (int i = 1; i < 3; ++i)
+      if (scale[3 * g + i] < mn) {
+        mn = scale[3 * g + i];
+        axis = i;
+      }
+    for (int i = 0; i < 3; ++i) n[i] = r[3 * i + axis];
+  }
+  const double z = n[0] * n[0] + n[1] * n[1] + n[2] * n[2];
+  if (z > 0.0) {
+    const double nn = sqrt(z);
+    for (int i = 0; i < 3; ++i) n[i] = n[i] / nn;
+  }
+  if (n[0] * rd[3 * k] + n[1] * rd[3 * k + 1] + n[2] * rd[3 * k + 2] > 0.0)
+    for (int i = 0; i < 3; ++i) n[i] = -n[i];
+  for (int i = 0; i < 3; ++i) out[3 * k + i] = n[i];
+}
+
 }  // namespace sofk
 
 using namespace sofk;
@@ -634,6 +736,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
                                                             out);
       SOF_LAUNCHED(c);
     }
+    c->r_view = view;
     const int64_t nover = nover_total;
     if (depth) SOF_CUDA(cudaMemcpyAsync(depth, out.depth, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
     if (opacity)
@@ -664,4 +767,70 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     c->err = e.what();
     return SOF_E_CUDA;
   }
+}
+
+extern "C" int sof_render_normals(sof_ctx* c, int view, double* normal, uint8_t* valid) {
+  if (!c) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+    if (c->r_view != view) throw StateError("no render of this view on the device: call sof_render_view first");
+    const Cam& cam = c->cams[view];
+    const int64_t P = int64_t(cam.w) * cam.h;
+    c->r_normal.ensure(std::max<int64_t>(3 * P, 1));
+    c->r_valid.ensure(std::max<int64_t>(P, 1));
+    if (P > 0) {
+      k_normal_from_depth<<<grid_for(P, 256), 256, 0, c->stream>>>(cam, c->r_out.p, c->r_normal.p, c->r_valid.p);
+      SOF_LAUNCHED(c);
+    }
+    if (normal && P) SOF_CUDA(cudaMemcpyAsync(normal, c->r_normal.p, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, c->stream));
+    if (valid && P) SOF_CUDA(cudaMemcpyAsync(valid, c->r_valid.p, P, cudaMemcpyDeviceToHost, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+extern "C" int sof_normal_from_depth(sof_ctx* c, int view, const double* depth, double* normal, uint8_t* valid) {
+  if (!c || !depth) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+    const Cam& cam = c->cams[view];
+    const int64_t P = int64_t(cam.w) * cam.h;
+    c->r_depth_in.ensure(std::max<int64_t>(P, 1));
+    c->r_normal.ensure(std::max<int64_t>(3 * P, 1));
+    c->r_valid.ensure(std::max<int64_t>(P, 1));
+    if (P > 0) {
+      SOF_CUDA(cudaMemcpyAsync(c->r_depth_in.p, depth, sizeof(double) * P, cudaMemcpyHostToDevice, c->stream));
+      k_normal_from_depth<<<grid_for(P, 256), 256, 0, c->stream>>>(cam, c->r_depth_in.p, c->r_normal.p,
+                                                                   c->r_valid.p);
+      SOF_LAUNCHED(c);
+      if (normal) SOF_CUDA(cudaMemcpyAsync(normal, c->r_normal.p, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, c->stream));
+      if (valid) SOF_CUDA(cudaMemcpyAsync(valid, c->r_valid.p, P, cudaMemcpyDeviceToHost, c->stream));
+    }
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+extern "C" int sof_gaussian_normals(sof_ctx* c, int64_t m, const int32_t* gidx, const double* origin,
+                                    const double* dir, const double* t, double* out) {
+  if (!c || m < 0 || (m > 0 && (!gidx || !origin || !dir || !t || !out))) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (!c->has_scene) throw StateError("no scene: call sof_set_scene first");
+    if (m == 0) return;
+    for (int64_t k = 0; k < m; ++k)
+      if (gidx[k] < 0 || gidx[k] >= c->n) throw InvalidArg("gaussian index out of range");
+    DBuf<char>& b = c->r_query;
+    const size_t off_o = 0, off_d = 24 * m, off_t = 48 * m, off_i = 56 * m, off_out = 64 * m;
+    b.ensure(int64_t(off_out + 24 * m));
+    SOF_CUDA(cudaMemcpyAsync(b.p + off_o, origin, 24 * m, cudaMemcpyHostToDevice, c->stream));
+    SOF_CUDA(cudaMemcpyAsync(b.p + off_d, dir, 24 * m, cudaMemcpyHostToDevice, c->stream));
+    SOF_CUDA(cudaMemcpyAsync(b.p + off_t, t, 8 * m, cudaMemcpyHostToDevice, c->stream));
+    SOF_CUDA(cudaMemcpyAsync(b.p + off_i, gidx, 4 * m, cudaMemcpyHostToDevice, c->stream));
+    double* dout = reinterpret_cast<double*>(b.p + off_out);
+    k_gaussian_normal<<<grid_for(m, 256), 256, 0, c->stream>>>(
+        m, reinterpret_cast<const int32_t*>(b.p + off_i), c->pos.p, c->scale.p, c->rot.p,
+        reinterpret_cast<const double*>(b.p + off_o), reinterpret_cast<const double*>(b.p + off_d),
+        reinterpret_cast<const double*>(b.p + off_t), dout);
+    SOF_LAUNCHED(c);
+    SOF_CUDA(cudaMemcpyAsync(out, dout, 24 * m, cudaMemcpyDeviceToHost, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+  });
 }

@@ -11,6 +11,7 @@
 #include <utility>
 #include <vector>
 
+#include "../../include/sof_cuda.h"
 #include "sof_device.cuh"
 
 namespace sofk {
@@ -187,6 +188,11 @@ struct sof_ctx {
   sofk::DBuf<double> r_out;               // depth, opacity, rgb(3), t_final per pixel
   sofk::DBuf<double> r_lkey;              // per-Gaussian t* lower bound of the render binning
   sofk::DBuf<unsigned long long> r_stats;
+  sofk::DBuf<double> r_normal, r_depth_in;  // normal_from_depth output / uploaded depth
+  sofk::DBuf<uint8_t> r_valid;
+  sofk::DBuf<char> r_query;                 // gaussian_normal queries
+  sofk::DBuf<unsigned char> io_bytes;       // scene PLY payload / encoded records
+  int r_view = -1;                          // view whose render is in r_out
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
   sofk::DBuf<int64_t> d_scalar;               // small device scalars
@@ -284,3 +290,38 @@ inline T read_scalar(sof_ctx* c, const T* dev) {
   } while (0)
 
 }  // namespace sofk
+
+namespace sofk {
+// Runs f and maps exceptions to the C-ABI status codes (message in sof_last_error).
+template <typename F>
+inline int guard(sof_ctx* c, F&& f) {
+  try {
+    if (c) SOF_CUDA(cudaSetDevice(c->device));
+    f();
+    return SOF_OK;
+  } catch (const InvalidArg& e) {
+    if (c) c->err = e.what();
+    return SOF_E_INVALID;
+  } catch (const std::invalid_argument& e) {
+    if (c) c->err = e.what();
+    return SOF_E_INVALID;
+  } catch (const StateError& e) {
+    if (c) c->err = e.what();
+    return SOF_E_STATE;
+  } catch (const OomError& e) {
+    if (c) c->err = e.what();
+    return SOF_E_OOM;
+  } catch (const CudaError& e) {
+    if (c) c->err = e.what();
+    return SOF_E_CUDA;
+  } catch (const std::bad_alloc&) {
+    if (c) c->err = "host allocation failed";
+    return SOF_E_OOM;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return SOF_E_RUNTIME;
+  }
+}
+
+}  // namespace sofk
+

@@ -182,6 +182,75 @@ TEST(RenderDepthMap, SingleGaussianDisk) {
       EXPECT_EQ(is_no_surface(exact.depth.at(x, y)), is_no_surface(median.depth.at(x, y)));
 }
 
+TEST(NormalFromDepth, FrontoParallelPlaneAndMaps) {
+  // test_opacity_field.cpp:285-298 with the camera of a ViewSet; then the float maps
+  Camera cam;
+  cam.width = cam.height = 16;
+  cam.cx = cam.cy = 8;
+  cam.fx = cam.fy = 20;
+  const ViewSet views = ViewSet::build({GaussianPrimitive{}}, {cam});
+  Grid2D<double> depth(16, 16, 0.0);
+  for (int y = 0; y < 16; ++y)
+    for (int x = 0; x < 16; ++x) {
+      const Vec3 d = Vec3((x + 0.5 - 8) / 20.0, (y + 0.5 - 8) / 20.0, 1.0).normalized();
+      depth.at(x, y) = 5.0 / d.z();
+    }
+  const NormalMap nm = normal_from_depth(depth, views, 0);
+  ASSERT_TRUE(nm.valid.at(8, 8));
+  EXPECT_TRUE(nm.normal.at(8, 8).isApprox(Vec3(0, 0, -1), 1e-9));
+  EXPECT_FALSE(nm.valid.at(15, 15));
+  const FloatMap fm = normals_to_map(nm);
+  write_float_map(fm, "/tmp/sof_b200_test_normals.sofmap");
+  const FloatMap back = read_float_map("/tmp/sof_b200_test_normals.sofmap");
+  EXPECT_EQ(back.width, 16);
+  EXPECT_EQ(back.channels, 3);
+  EXPECT_EQ(back.data, fm.data);
+  // GaussianNormal.RadialAndFallback (test_opacity_field.cpp:330-340)
+  const Ray ray{Vec3(0, 0, -5), Vec3(0, 0, 1)};
+  EXPECT_TRUE(gaussian_normal(views, 0, ray, 6.0).isApprox(Vec3(0, 0, -1), 1e-12));
+}
+
+TEST(SceneIO, RoundTripAndErrors) {
+  // SceneIO.RoundTrip / RotationsNormalizedOnLoad / MalformedHeaderRejected (test_io.cpp:41-107)
+  std::vector<GaussianPrimitive> scene(20);
+  for (int i = 0; i < 20; ++i) {
+    scene[i].position = Vec3(0.1 * i, -0.2 * i, 0.3);
+    scene[i].scale = Vec3(0.05 + 0.01 * i, 0.2, 0.1);
+    scene[i].rotation = Quat(1, 0.1 * i, 2, 3).normalized();
+    scene[i].opacity = 0.04 * i + 0.01;
+    scene[i].dc_color = Vec3(0.3, 0.5, 0.7);
+  }
+  write_scene(scene, "/tmp/sof_b200_scene.ply");
+  const SceneFile loaded = parse_scene("/tmp/sof_b200_scene.ply");
+  ASSERT_EQ(loaded.gaussians.size(), scene.size());
+  for (size_t i = 0; i < scene.size(); ++i) {
+    EXPECT_LT((scene[i].position - loaded.gaussians[i].position).norm(), 1e-5);
+    EXPECT_NEAR(scene[i].opacity, loaded.gaussians[i].opacity, 1e-6);
+    EXPECT_NEAR(loaded.gaussians[i].rotation.norm(), 1.0, 1e-12);
+  }
+  {
+    std::ofstream f("/tmp/sof_b200_bad.ply");
+    f << "not a ply file\n";
+  }
+  bool threw = false;
+  try {
+    parse_scene("/tmp/sof_b200_bad.ply");
+  } catch (const std::runtime_error& e) {
+    threw = std::string(e.what()).find("malformed PLY header") != std::string::npos;
+  }
+  EXPECT_TRUE(threw);
+  Mesh m;
+  m.vertices = {Vec3(0, 0, 0), Vec3(1, 0, 0), Vec3(0, 1, 0.123456789012345678)};
+  m.triangles = {{0, 1, 2}};
+  write_mesh(m, "/tmp/sof_b200_m.obj", MeshFormat::kObj);
+  write_mesh(m, "/tmp/sof_b200_m.ply", MeshFormat::kPlyBinary);
+  const Mesh a = read_mesh_obj("/tmp/sof_b200_m.obj"), b = read_mesh_ply("/tmp/sof_b200_m.ply");
+  ASSERT_EQ(a.vertices.size(), 3u);
+  EXPECT_EQ(a.vertices[2](2), m.vertices[2](2));
+  EXPECT_EQ(b.vertices[2](2), m.vertices[2](2));
+  EXPECT_EQ(b.triangles[0][2], 2);
+}
+
 TEST(Errors, NonFiniteScene) {
   GaussianPrimitive g;
   g.position = Vec3(0, std::nan(""), 0);

@@ -108,3 +108,116 @@ def test_render_long_spill_slices_with_ties(ref):
         st = []
         check(rc, views, 0, exact, st)
         assert st[0][2] > 0 and st[0][1] > 300 * st[0][2]  # long slices took the merge path
+
+
+# ---- normals (render.hpp:58-107) and the `sof render` outputs (sof_cli.cpp:122-130) ------------
+
+def _plain_cam(w, h, cx, cy, f):
+    from oracle.refpy import Cameras
+    c = Cameras.empty(1)
+    c.R[0] = np.eye(3)
+    c.intr[0] = (f, f, cx, cy)
+    c.wh[0] = (w, h)
+    c.nearfar[0] = (0.2, 100.0)
+    return c
+
+
+def _one_gaussian():
+    return Scene(np.zeros((1, 3)), np.ones((1, 3)), np.array([[1.0, 0, 0, 0]]), np.ones(1), np.zeros((1, 3)))
+
+
+def test_render_normals_bitexact(ref):
+    scene = ref.random_scene(52, 1500, 1.0)
+    cams = ref.orbit_cameras(2, 4.0, 1.8, 48)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    for v in range(cams.v):
+        r = sof.render_view(views, v, sof.DEPTH_EXACT, normals=True)
+        d, _ = rc.render_depth_map(v, True)
+        np.testing.assert_array_equal(bits(r["depth"]), bits(d))
+        n_ref, ok_ref = rc.normal_from_depth(v, d)
+        np.testing.assert_array_equal(r["normal_valid"], ok_ref)
+        np.testing.assert_array_equal(bits(r["normal"]), bits(n_ref))
+        assert ok_ref.sum() > 100
+        # the same from a host depth map
+        n2, ok2 = sof.normal_from_depth(views, v, d)
+        np.testing.assert_array_equal(bits(n2), bits(n_ref))
+        np.testing.assert_array_equal(ok2, ok_ref)
+
+
+def test_normal_from_depth_known_answers(ref):
+    """NormalFromDepth.FrontoParallelPlane / SlantedPlane / IsolatedPixelInvalid
+    (test_opacity_field.cpp:285-327)."""
+    ctx = sof.Context(0)
+    cam = _plain_cam(16, 16, 8, 8, 20)
+    views = sof.ViewSet.build(_one_gaussian(), cam, ctx=ctx)
+    yy, xx = np.mgrid[0:16, 0:16]
+    d = np.stack([(xx + 0.5 - 8) / 20, (yy + 0.5 - 8) / 20, np.ones_like(xx, float)], -1)
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    n, ok = sof.normal_from_depth(views, 0, 5.0 / d[..., 2])
+    assert ok[8, 8] and np.allclose(n[8, 8], (0, 0, -1), atol=1e-9)
+    rc = ref.context(_one_gaussian(), cam)
+    n_ref, ok_ref = rc.normal_from_depth(0, 5.0 / d[..., 2])
+    np.testing.assert_array_equal(bits(n), bits(n_ref))
+    np.testing.assert_array_equal(ok, ok_ref)
+
+    cam = _plain_cam(32, 32, 16, 16, 60)
+    views = sof.ViewSet.build(_one_gaussian(), cam, ctx=ctx)
+    yy, xx = np.mgrid[0:32, 0:32]
+    d = np.stack([(xx + 0.5 - 16) / 60, (yy + 0.5 - 16) / 60, np.ones_like(xx, float)], -1)
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    npl = np.array([0.3, -0.2, -1.0]) / np.linalg.norm([0.3, -0.2, -1.0])
+    n, ok = sof.normal_from_depth(views, 0, -5.0 / (d @ npl))
+    assert ok[16, 16] and np.linalg.norm(n[16, 16] - npl) < 1e-3
+
+    cam = _plain_cam(8, 8, 4, 4, 500)
+    views = sof.ViewSet.build(_one_gaussian(), cam, ctx=ctx)
+    depth = np.full((8, 8), np.nan)
+    depth[3, 3] = 5.0
+    n, ok = sof.normal_from_depth(views, 0, depth)
+    assert ok.sum() == 0 and not n.any()
+
+
+def test_gaussian_normal(ref):
+    """GaussianNormal.RadialAndFallback / AlwaysFacesCamera (test_opacity_field.cpp:330-351)
+    and bit-exact against the reference on random queries."""
+    flat = Scene(np.zeros((2, 3)), np.array([[1.0, 1, 1], [1.0, 1.0, 0.2]]), np.tile([1.0, 0, 0, 0], (2, 1)),
+                 np.ones(2), np.zeros((2, 3)))
+    cam = _plain_cam(16, 16, 8, 8, 20)
+    views = sof.ViewSet.build(flat, cam, ctx=sof.Context(0))
+    o, dvec = np.array([[0, 0, -5.0]]), np.array([[0, 0, 1.0]])
+    n = sof.gaussian_normal(views.ctx, [0], o, dvec, [6.0])
+    assert np.allclose(n[0], (0, 0, -1), atol=1e-12)
+    n = sof.gaussian_normal(views.ctx, [1], o, dvec, [5.0])
+    assert abs(abs(n[0, 2]) - 1.0) < 1e-12 and n[0] @ dvec[0] <= 0.0
+
+    scene = ref.random_scene(27, 300, 1.0)
+    views = sof.ViewSet.build(scene, cam, ctx=sof.Context(0))
+    rc = ref.context(scene, cam)
+    rng = np.random.default_rng(9)
+    m = 2000
+    g = rng.integers(0, 300, m).astype(np.int32)
+    o = np.column_stack([rng.uniform(-2, 2, (m, 2)), np.full(m, -6.0)])
+    dv = np.column_stack([rng.uniform(-0.2, 0.2, (m, 2)), np.ones(m)])
+    dv /= np.linalg.norm(dv, axis=1, keepdims=True)
+    t = rng.uniform(2.0, 8.0, m)
+    got = sof.gaussian_normal(views.ctx, g, o, dv, t)
+    np.testing.assert_array_equal(bits(got), bits(rc.gaussian_normals(g, o, dv, t)))
+    assert (np.einsum("ij,ij->i", got, dv) <= 1e-12).all()
+
+
+def test_render_maps_files_byte_identical(ref, tmp_path):
+    """`sof render` per-view outputs (sof_cli.cpp:122-130): depth + opacity map and
+    normal map files, byte-identical to the reference's."""
+    scene = ref.random_scene(21, 600, 1.0)
+    cams = ref.orbit_cameras(2, 4.0, 1.8, 40)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    for v in range(cams.v):
+        for exact in (True, False):
+            a, b = tmp_path / "a_d.sofmap", tmp_path / "a_n.sofmap"
+            c, d = tmp_path / "b_d.sofmap", tmp_path / "b_n.sofmap"
+            sof.render_maps(views, v, str(a), str(b), exact=exact)
+            rc.render_maps(v, str(c), str(d), exact=exact)
+            assert a.read_bytes() == c.read_bytes()
+            assert b.read_bytes() == d.read_bytes()
