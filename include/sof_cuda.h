@@ -81,6 +81,8 @@ typedef struct sof_extract_opts {
   double min_area;       /* default 1e-14 (mesh.hpp:38) */
   int view_begin;        /* views [view_begin, view_end) of this rank; -1/-1 = all */
   int view_end;
+  int profile;           /* 1: per-kernel device timings (ms_eval_kernel, ms_prep, ...); adds
+                            two events per launch and a host-side collection; default 0 */
 } sof_extract_opts;
 
 /* Per-stage statistics (ExtractStats extract.hpp:22-33) plus device timings. */
@@ -128,6 +130,12 @@ int sof_set_views(sof_ctx* ctx, int v, const double* R, const double* t, const d
                   const int32_t* wh, const double* nearfar);
 /* The tetra input (TetGrid delaunay.hpp:14-18: vertices + tetrahedra), resident on the device. */
 int sof_set_tets(sof_ctx* ctx, int64_t nv, const double* xyz, int64_t nt, const int32_t* tets);
+/* As sof_set_tets, but the tets upload (and their index check) runs on a copy stream
+ * while the next label pass, which needs only the vertices, computes; the marching
+ * stage waits for it. `tets` must stay valid and unchanged until the next sof_extract /
+ * sof_marching_tets returns (pinned memory for the copy to overlap). An out-of-range
+ * index is reported by that call (SOF_E_INVALID). */
+int sof_set_tets_async(sof_ctx* ctx, int64_t nv, const double* xyz, int64_t nt, const int32_t* tets);
 
 /* ---- per-view preprocessing and binning (parity / inspection) -------------------- */
 /* PrecomputedGaussian per Gaussian for one view (precompute.hpp:21-28): 13 doubles

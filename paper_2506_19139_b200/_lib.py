@@ -28,7 +28,7 @@ _I64 = ctypes.c_int64
 
 class ExtractOpts(ctypes.Structure):
     _fields_ = [("strategies", _I), ("tile_size", _I), ("refine_iterations", _I),
-                ("weld_eps", _D), ("min_area", _D), ("view_begin", _I), ("view_end", _I)]
+                ("weld_eps", _D), ("min_area", _D), ("view_begin", _I), ("view_end", _I), ("profile", _I)]
 
 
 class ExtractStats(ctypes.Structure):
@@ -53,6 +53,7 @@ _SIGS = {
     "sof_set_scene": (_I, [_P, _I64, _P, _P, _P, _P, _P, _D]),
     "sof_set_views": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "sof_set_tets": (_I, [_P, _I64, _P, _I64, _P]),
+    "sof_set_tets_async": (_I, [_P, _I64, _P, _I64, _P]),
     "sof_precompute_view": (_I, [_P, _I, _P]),
     "sof_tile_binding": (_I, [_P, _I, _I, _P, _P]),
     "sof_schedule_points": (_I, [_P, _I, _I64, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),

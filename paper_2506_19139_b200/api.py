@@ -153,6 +153,7 @@ class ExtractOptions:
     min_area: float = 1e-14
     view_begin: int = -1
     view_end: int = -1
+    profile: bool = False  # per-kernel device timings in the stats (adds host-side cost)
 
 
 # ---- device context ------------------------------------------------------------------------
@@ -223,10 +224,15 @@ class Context:
         self.check(self.lib.sof_set_views(self.h, c.v, _ptr(c.R), _ptr(c.t), _ptr(c.intr), _ptr(c.wh), _ptr(c.nearfar)))
         self.cams = c
 
-    def set_tets(self, vertices, tets):
+    def set_tets(self, vertices, tets, async_copy: bool = False):
+        """TetGrid vertices + tetrahedra to the device. async_copy: the tets travel on a
+        copy stream during the next label pass (sof_set_tets_async); keep `tets` alive and
+        unchanged until the next extract returns."""
         v = _f64(vertices, 3)
         t = np.ascontiguousarray(tets, np.int32).reshape(-1, 4)
-        self.check(self.lib.sof_set_tets(self.h, len(v), _ptr(v), len(t), _ptr(t)))
+        fn = self.lib.sof_set_tets_async if async_copy else self.lib.sof_set_tets
+        self.check(fn(self.h, len(v), _ptr(v), len(t), _ptr(t)))
+        self._tets_keepalive = t if async_copy else None
         self.nv = len(v)
 
     def result(self, kind: int, dtype, width: int):
@@ -397,7 +403,7 @@ def extract_mesh(gaussians, views: ViewSet, grid: TetGrid, opt: ExtractOptions |
 
 def extract_resident(ctx: Context, opt: ExtractOptions, stats: dict | None = None, fetch: bool = True):
     o = L.ExtractOpts(_mask(opt.strategies), opt.tile_size, opt.refine_iterations, opt.weld_eps, opt.min_area,
-                      opt.view_begin, opt.view_end)
+                      opt.view_begin, opt.view_end, int(opt.profile))
     st = L.ExtractStats()
     ctx.check(ctx.lib.sof_extract(ctx.h, ctypes.byref(o), ctypes.byref(st)))
     if stats is not None:

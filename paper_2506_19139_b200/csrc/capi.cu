@@ -5,6 +5,10 @@
 // k_field.cu / k_mesh.cu / k_render.cu. No compute happens on the host.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -72,6 +76,9 @@ int sof_ctx_create(int device, sof_ctx** out) {
     SOF_CUDA(cudaEventCreate(&c->ev0));
     SOF_CUDA(cudaEventCreate(&c->ev1));
     SOF_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    SOF_CUDA(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
+    SOF_CUDA(cudaEventCreateWithFlags(&c->tets_ev, cudaEventDisableTiming));
+    SOF_CUDA(cudaMallocHost(&c->pinned_scalar, 8 * sizeof(uint64_t)));
     for (auto& e : c->prep_ev) SOF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t free_b = 0, total_b = 0;
     SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -101,6 +108,12 @@ void sof_ctx_destroy(sof_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream2);
     cudaStreamDestroy(ctx->stream2);
   }
+  if (ctx->stream_copy) {
+    cudaStreamSynchronize(ctx->stream_copy);
+    cudaStreamDestroy(ctx->stream_copy);
+  }
+  if (ctx->tets_ev) cudaEventDestroy(ctx->tets_ev);
+  if (ctx->pinned_scalar) cudaFreeHost(ctx->pinned_scalar);
   cudaStream_t s = ctx->stream;
   delete ctx;
   if (s) cudaStreamDestroy(s);
@@ -128,7 +141,7 @@ int sof_set_scene(sof_ctx* c, int64_t n, const double* pos, const double* scale,
     if (dc) upload(c, c->dc, dc, 3 * n);
     else {
       c->dc.ensure(std::max<int64_t>(3 * n, 1));
-      SOF_CUDA(cudaMemsetAsync(c->dc.p, 0, sizeof(double) * 3 * n, c->stream));
+      zero_async(c, c->dc.p, int64_t(sizeof(double)) * 3 * n);
     }
     scene_prep(c);
     c->has_scene = true;
@@ -168,6 +181,9 @@ int sof_set_tets(sof_ctx* c, int64_t nv, const double* xyz, int64_t nt, const in
   return guard(c, [&] {
     check_points(nv, xyz);
     if (nt < 0 || (nt > 0 && !tets)) throw InvalidArg("invalid tet array");
+    if (c->tets_pending) SOF_CUDA(cudaStreamSynchronize(c->stream_copy));
+    c->tets_pending = false;
+    c->up_src = nullptr;  // a not yet issued async upload is dropped
     upload(c, c->tv, xyz, 3 * nv);
     upload(c, c->tt, tets, 4 * nt);
     c->has_tets = false;
@@ -178,6 +194,32 @@ int sof_set_tets(sof_ctx* c, int64_t nv, const double* xyz, int64_t nt, const in
     c->nt = nt;
     c->has_tets = true;
     sync(c);
+  });
+}
+
+int sof_set_tets_async(sof_ctx* c, int64_t nv, const double* xyz, int64_t nt, const int32_t* tets) {
+  if (!c) return SOF_E_INVALID;
+  return guard(c, [&] {
+    check_points(nv, xyz);
+    if (nt < 0 || (nt > 0 && !tets)) throw InvalidArg("invalid tet array");
+    if (nv > INT32_MAX) throw InvalidArg("too many vertices for int32 tet indices");
+    if (c->tets_pending) SOF_CUDA(cudaStreamSynchronize(c->stream_copy));
+    upload(c, c->tv, xyz, 3 * nv);
+    // the tets travel on the copy stream while the label pass (which needs only the
+    // vertices) runs; march waits for them (tets_ready)
+    SOF_CUDA(cudaStreamSynchronize(c->stream));  // c->tt may still be read by earlier work
+    c->tt.ensure(std::max<int64_t>(4 * nt, 1));
+    c->tets_bad.ensure(1);
+    SOF_CUDA(cudaMemsetAsync(c->tets_bad.p, 0, sizeof(int32_t), c->stream_copy));
+    c->up_src = reinterpret_cast<const char*>(tets);
+    c->up_bytes = int64_t(sizeof(int32_t)) * 4 * nt;
+    c->up_done = 0;
+    c->up_nv = nv;
+    c->tets_pending = true;
+    c->nt = nt;
+    pump_upload(c, kUploadChunk);  // the rest is fed by the label pass / tets_ready
+    c->nv = nv;
+    c->has_tets = true;
   });
 }
 
@@ -280,7 +322,7 @@ int sof_classify_points(sof_ctx* c, int64_t n, const double* xyz, int strategies
     check_points(n, xyz);
     upload(c, c->pts, xyz, 3 * n);
     c->ext.ensure(std::max<int64_t>(n, 1));
-    SOF_CUDA(cudaMemsetAsync(c->ext.p, 0, n, c->stream));
+    zero_async(c, c->ext.p, n);
     eval_views(c, 0, int(c->cams.size()), n, c->pts.p, strategies, tile_size, true, kModeClassify,
                nullptr, c->ext.p, nullptr, nullptr, nullptr, counters);
     std::vector<uint8_t> ext(n);
@@ -319,7 +361,7 @@ int sof_label_grid(sof_ctx* c, int64_t nv, const double* xyz, int strategies, in
     c->grid_opacity.ensure(std::max<int64_t>(nv, 1));
     fill_f64(c, c->min_op.p, nv, 1.0);
 
-    SOF_CUDA(cudaMemsetAsync(c->ext.p, 0, nv, c->stream));
+    zero_async(c, c->ext.p, nv);
     eval_views(c, 0, int(c->cams.size()), nv, c->pts.p, strategies, tile_size, classify_mode != 0,
                kModeLabel, c->min_op.p, c->ext.p, nullptr, nullptr, nullptr, counters);
     finalize_label(c, nv, c->min_op.p, c->ext.p, c->grid_opacity.p);
@@ -433,11 +475,19 @@ void sof_extract_opts_default(sof_extract_opts* o) {
   o->min_area = 1e-14;
   o->view_begin = -1;
   o->view_end = -1;
+  o->profile = 0;
 }
 
 int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* stats) {
   if (!c) return SOF_E_INVALID;
   return guard(c, [&] {
+    const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
+    const auto h0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+      if (dbg)
+        std::fprintf(stderr, "  extract %-10s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+    };
     need_views(c);
     if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
     sof_extract_opts o;
@@ -456,7 +506,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     c->exact_evals = 0;
     c->contrib_evals = 0;
     c->host_ms[0] = c->host_ms[1] = 0.0;
-    c->time_eval = stats != nullptr;
+    c->time_eval = stats != nullptr && o.profile != 0;
     if (c->time_eval) {
       double drop[kProfKinds];
       prof_collect(c, drop);  // reset the event pool
@@ -468,26 +518,31 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     c->ext.ensure(std::max<int64_t>(nv, 1));
     c->grid_opacity.ensure(std::max<int64_t>(nv, 1));
     SOF_CUDA(cudaEventRecord(e[0], c->stream));
+    mark("start");
     // label_grid (extract.hpp:59-61): classification mode, views in order
     {
       fill_f64(c, c->min_op.p, nv, 1.0);
 
     }
-    SOF_CUDA(cudaMemsetAsync(c->ext.p, 0, nv, c->stream));
+    zero_async(c, c->ext.p, nv);
     uint64_t cl[2] = {0, 0}, cr[2] = {0, 0};
     eval_views(c, v0, v1, nv, c->tv.p, o.strategies, o.tile_size, true, kModeLabel, c->min_op.p,
                c->ext.p, nullptr, nullptr, nullptr, cl);
     finalize_label(c, nv, c->min_op.p, c->ext.p, c->grid_opacity.p);
     c->grid_n = nv;
     SOF_CUDA(cudaEventRecord(e[1], c->stream));
+    mark("label");
     march(c, c->grid_opacity.p);
     SOF_CUDA(cudaEventRecord(e[2], c->stream));
+    mark("march");
     refine(c, c->n_edges, c->r_edges.p, c->r_everts.p, o.refine_iterations, o.strategies,
            o.tile_size, v0, v1, cr);
     SOF_CUDA(cudaEventRecord(e[3], c->stream));
+    mark("refine");
     assemble(c, c->n_edges, c->r_everts.p, c->n_march_tris, c->r_tris.p, o.weld_eps, o.min_area);
     SOF_CUDA(cudaEventRecord(e[4], c->stream));
     SOF_CUDA(cudaEventSynchronize(e[4]));
+    mark("weld");
     float ms[4];
     for (int k = 0; k < 4; ++k) SOF_CUDA(cudaEventElapsedTime(&ms[k], e[k], e[k + 1]));
     for (auto& x : e) cudaEventDestroy(x);
@@ -504,8 +559,8 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     st.ms_march = ms[1];
     st.ms_refine = ms[2];
     st.ms_weld = ms[3];
-    double pms[kProfKinds];
-    prof_collect(c, pms);
+    double pms[kProfKinds] = {0.0};
+    if (o.profile) prof_collect(c, pms);
     st.ms_eval_kernel = pms[kProfEval];
     st.ms_prep = pms[kProfPrep];
     st.exact_pairs = c->exact_evals;

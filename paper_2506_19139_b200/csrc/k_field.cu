@@ -11,6 +11,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sof_internal.h"
@@ -803,7 +805,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   const bool prune = strategies & 8;
   c->d_counters.ensure(4);
   c->d_scalar.ensure(4);
-  SOF_CUDA(cudaMemsetAsync(c->d_counters.p, 0, sizeof(unsigned long long) * 4, c->stream));
+  zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 4);
   PointSchedule& s = c->sched;
   if (n > 0) {
     s.tile_of.ensure(n);
@@ -839,15 +841,24 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     std::swap(c->stream, c->stream2);
     c->cub_tmp.swap(c->cub_tmp2);
   };
+  const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
+  const auto hd0 = std::chrono::steady_clock::now();
   for (int v = v0; v < v1 && n > 0; ++v) {
+    if (dbg && (v - v0 < 3 || v + 1 == v1))
+      std::fprintf(stderr, "    view %3d issued at %8.2f ms\n", v,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
     const Cam& cam = c->cams[v];
     const int tiles_x = (cam.w + tile_size - 1) / tile_size;
     const int tiles_y = (cam.h + tile_size - 1) / tile_size;
     const int T = tiled ? tiles_x * tiles_y : 1;
     const auto h0 = std::chrono::steady_clock::now();
     if (v == v0) prep_view(v);
+    if (dbg && v == v0)
+      std::fprintf(stderr, "      v0 prepped at %8.2f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
     // the records / binding of view v were prepared on the prep lane (during view v-1)
     SOF_CUDA(cudaStreamWaitEvent(c->stream, c->prep_ev[v & 1], 0));
+
     const Rec* rec = prep_rec[v & 1];
     const Binding* bd = prep_bd[v & 1];
     const int p1 = prof_mark(c);
@@ -863,7 +874,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     s.tile_off.ensure(NB + 1);
     s.blk_cnt.ensure(T + 1);
     s.blk_off.ensure(T + 1);
-    SOF_CUDA(cudaMemsetAsync(s.tile_cnt.p, 0, sizeof(int) * 2 * (NB + 1), c->stream));
+    zero_async(c, s.tile_cnt.p, int64_t(sizeof(int)) * 2 * (NB + 1));
     int* tile_cur = s.tile_cnt.p + (NB + 1);
     const int32_t* cand = use_list ? s.active.p : nullptr;
     k_sched_tile<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
@@ -906,6 +917,10 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     // drop pruned points from the candidate list now and then (the reference skips them,
     // field_eval.hpp:147); the list shrinks fast over the first views
     const int done_views = v - v0 + 1;
+    pump_upload(c, kUploadChunk);  // a pending tets upload advances one chunk per view
+    if (dbg && v == v0)
+      std::fprintf(stderr, "      v0 eval issued at %8.2f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
     if (skip && v + 1 < v1 && (done_views <= 4 || done_views % 16 == 0)) {
       s.active2.ensure(std::max<int64_t>(ncand, 1));
       s.nsel.ensure(1);
@@ -926,6 +941,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
       s.active.swap(s.active2);
       ncand = read_scalar(c, s.nsel.p);
       use_list = true;
+      if (dbg && v == v0)
+        std::fprintf(stderr, "      v0 compacted at %8.2f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
     }
     if (v + 1 < v1) {
       const auto h3 = std::chrono::steady_clock::now();
@@ -933,6 +951,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
       c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h3).count();
     }
   }
+  if (dbg)
+    std::fprintf(stderr, "    all views issued at %8.2f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
   if (counters_host) {
     unsigned long long h[4];
     SOF_CUDA(cudaMemcpyAsync(h, c->d_counters.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));

@@ -202,6 +202,7 @@ __global__ void k_tris(int64_t ntri, const int32_t* __restrict__ tri_occ,
 }
 
 void march(sof_ctx* c, const double* opa) {
+  tets_ready(c);
   if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
   const int64_t nt = c->nt, nv = c->nv;
   MeshScratch& s = c->ms;
@@ -263,7 +264,7 @@ void march(sof_ctx* c, const double* opa) {
   s.eid.ensure(m);
   s.run_incl.ensure(m);
   s.occ_edge.ensure(m);
-  SOF_CUDA(cudaMemsetAsync(s.first_u8.p, 0, m, c->stream));
+  zero_async(c, s.first_u8.p, m);
   k_occ_heads<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.skey.p, s.spos.p, s.head.p,
                                                         s.first_u8.p);
   SOF_LAUNCHED(c);

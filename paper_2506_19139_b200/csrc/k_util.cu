@@ -3,6 +3,10 @@
 // the FP64 opacity-evaluation kernel.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/sof_cuda.h"
@@ -44,6 +48,24 @@ __global__ void k_fill_f64(int64_t n, double* p, double v) {
   if (i < n) p[i] = v;
 }
 
+__global__ void k_zero_words(int64_t n4, uint32_t* p4, int64_t n1, uint8_t* tail) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n4) p4[i] = 0u;
+  if (i < n1) tail[i] = 0;
+}
+
+// cudaMemsetAsync(p, 0, bytes) as a kernel: memsets may be executed by a copy engine
+// and then queue behind a large asynchronous upload (sof_set_tets_async).
+void zero_async(sof_ctx* c, void* p, int64_t bytes) {
+  if (bytes <= 0) return;
+  const bool aligned = (reinterpret_cast<uintptr_t>(p) & 3) == 0;
+  const int64_t n4 = aligned ? bytes / 4 : 0, n1 = bytes - 4 * n4;
+  uint8_t* tail = static_cast<uint8_t*>(p) + 4 * n4;
+  const int64_t n = std::max(n4, n1);
+  k_zero_words<<<grid_for(n, 256), 256, 0, c->stream>>>(n4, static_cast<uint32_t*>(p), n1, tail);
+  SOF_LAUNCHED(c);
+}
+
 void fill_f64(sof_ctx* c, double* p, int64_t n, double v) {
   if (n <= 0) return;
   k_fill_f64<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p, v);
@@ -82,6 +104,43 @@ void prof_collect(sof_ctx* c, double* ms) {
   c->evnext = 0;
 }
 
+void check_tet_indices(sof_ctx* c, cudaStream_t st, int64_t nt, const int32_t* tets_dev, int64_t nv,
+                       int32_t* bad) {
+  k_check_index<<<grid_for(4 * nt, 256), 256, 0, st>>>(4 * nt, tets_dev, int32_t(nv), bad);
+  SOF_LAUNCHED(c);
+}
+
+void pump_upload(sof_ctx* c, int64_t max_bytes) {
+  if (!c->tets_pending || !c->up_src || c->up_done >= c->up_bytes) return;
+  const int64_t n = std::min(max_bytes, c->up_bytes - c->up_done);
+  SOF_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(c->tt.p) + c->up_done, c->up_src + c->up_done, size_t(n),
+                           cudaMemcpyHostToDevice, c->stream_copy));
+  c->up_done += n;
+  if (c->up_done == c->up_bytes) {
+    if (c->nt > 0) check_tet_indices(c, c->stream_copy, c->nt, c->tt.p, c->up_nv, c->tets_bad.p);
+    SOF_CUDA(cudaEventRecord(c->tets_ev, c->stream_copy));
+    c->up_src = nullptr;
+  }
+}
+
+void tets_ready(sof_ctx* c) {
+  if (!c->tets_pending) return;
+  if (c->up_src) pump_upload(c, c->up_bytes - c->up_done);
+  const auto t0 = std::chrono::steady_clock::now();
+  const bool was_done = cudaEventQuery(c->tets_ev) == cudaSuccess;
+  SOF_CUDA(cudaEventSynchronize(c->tets_ev));
+  if (std::getenv("SOF_DEBUG_TETS"))
+    std::fprintf(stderr, "tets_ready: copy %s, waited %.2f ms\n", was_done ? "done" : "pending",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  int32_t bad = 0;
+  SOF_CUDA(cudaMemcpy(&bad, c->tets_bad.p, sizeof bad, cudaMemcpyDeviceToHost));
+  c->tets_pending = false;
+  if (bad) {
+    c->has_tets = false;
+    throw InvalidArg("tet vertex index out of range");
+  }
+}
+
 }  // namespace sofk
 
 using namespace sofk;
@@ -93,7 +152,7 @@ int sof_validate_tets_dev(sof_ctx* c, int64_t nt, const int32_t* tets_dev, int64
   try {
     DBuf<int32_t>& bad = c->ms.nsel;
     bad.ensure(1);
-    SOF_CUDA(cudaMemsetAsync(bad.p, 0, 4, c->stream));
+    zero_async(c, bad.p, 4);
     if (nt > 0) {
       k_check_index<<<grid_for(4 * nt, 256), 256, 0, c->stream>>>(4 * nt, tets_dev, int32_t(nv), bad.p);
       SOF_LAUNCHED(c);

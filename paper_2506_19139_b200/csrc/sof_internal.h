@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -169,6 +170,15 @@ struct sof_ctx {
 
   // prep lane: a second stream (+ its own CUB scratch) for per-view preprocessing
   cudaStream_t stream2 = nullptr;
+  cudaStream_t stream_copy = nullptr;     // sof_set_tets_async: tet upload + index check
+  uint64_t* pinned_scalar = nullptr;      // [8] pinned host slots for small read-backs
+  cudaEvent_t tets_ev = nullptr;          // ... recorded after them
+  bool tets_pending = false;              // march must wait for tets_ev and check the flag
+  // the pending upload, fed to the copy engine in chunks (pump_upload) so that the
+  // memsets CUB issues on the same engine never queue behind gigabytes
+  const char* up_src = nullptr;
+  int64_t up_bytes = 0, up_done = 0, up_nv = 0;
+  sofk::DBuf<int32_t> tets_bad;
   sofk::DBuf<char> cub_tmp2;
   cudaEvent_t prep_ev[2] = {nullptr, nullptr};
 
@@ -251,6 +261,12 @@ void schedule_points_exact(sof_ctx* c, int view, int64_t n, const double* xyz_de
                            std::vector<int32_t>& block_ranges, std::vector<int32_t>& block_to_tile);
 
 // ---- k_mesh.cu --------------------------------------------------------------------------
+// Makes asynchronously uploaded tets usable on c->stream (waits, checks the index flag).
+void tets_ready(sof_ctx* c);
+// Issues up to max_bytes more of a pending sof_set_tets_async upload.
+void pump_upload(sof_ctx* c, int64_t max_bytes);
+constexpr int64_t kUploadChunk = int64_t(64) << 20;
+void check_tet_indices(sof_ctx* c, cudaStream_t st, int64_t nt, const int32_t* tets_dev, int64_t nv, int32_t* bad);
 void march(sof_ctx* c, const double* opacity_dev);
 void refine(sof_ctx* c, int64_t ne, const int32_t* edges_dev, double* verts_dev, int iterations,
             int strategies, int tile_size, int v0, int v1, uint64_t* counters);
@@ -262,6 +278,7 @@ void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris
               const int32_t* tris_dev, double weld_eps, double min_area);
 
 // ---- k_util.cu: phase timing -------------------------------------------------------------
+void zero_async(sof_ctx* c, void* p, int64_t bytes);
 void fill_f64(sof_ctx* c, double* p, int64_t n, double v);
 int prof_mark(sof_ctx* c);                              // -1 when not profiling
 void prof_span(sof_ctx* c, int a, int b, int kind);
@@ -278,9 +295,13 @@ void exclusive_scan_i32(sof_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 int bits_for(uint64_t max_value);
 template <typename T>
 inline T read_scalar(sof_ctx* c, const T* dev) {
-  T h;
-  SOF_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  // through a pinned slot: a pageable read-back is staged by the driver and can queue
+  // behind a large asynchronous upload (sof_set_tets_async)
+  static_assert(sizeof(T) <= sizeof(c->pinned_scalar[0]), "scalar too large");
+  SOF_CUDA(cudaMemcpyAsync(c->pinned_scalar, dev, sizeof(T), cudaMemcpyDeviceToHost, c->stream));
   SOF_CUDA(cudaStreamSynchronize(c->stream));
+  T h;
+  std::memcpy(&h, c->pinned_scalar, sizeof(T));
   return h;
 }
 #define SOF_LAUNCHED(c)              \

@@ -151,3 +151,25 @@ def test_sharded_path_single_rank_matches_fused(ref, lattice_case):
     np.testing.assert_array_equal(bits(mesh.vertices), bits(fused.vertices))
     np.testing.assert_array_equal(mesh.triangles, fused.triangles)
     torch.cuda.synchronize()
+
+
+def test_async_tets_upload(lattice_case):
+    """sof_set_tets_async: the same mesh as the synchronous upload; a bad index is
+    reported by the extract that consumes the tets."""
+    scene, cams, rc, views, verts, tets = lattice_case
+    ctx = views.ctx
+    ctx.set_tets(verts, tets)
+    want = sof.extract_resident(ctx, sof.ExtractOptions(), {})
+    for _ in range(2):  # twice: a pending upload is replaced cleanly
+        ctx.set_tets(verts, tets, async_copy=True)
+    got = sof.extract_resident(ctx, sof.ExtractOptions(), {})
+    np.testing.assert_array_equal(bits(got.vertices), bits(want.vertices))
+    np.testing.assert_array_equal(got.triangles, want.triangles)
+    bad = tets.copy()
+    bad[len(bad) // 2, 1] = len(verts)
+    ctx.set_tets(verts, bad, async_copy=True)
+    with pytest.raises(ValueError, match="out of range"):
+        sof.extract_resident(ctx, sof.ExtractOptions(), {})
+    ctx.set_tets(verts, tets)
+    again = sof.extract_resident(ctx, sof.ExtractOptions(), {})
+    np.testing.assert_array_equal(again.triangles, want.triangles)

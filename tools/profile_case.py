@@ -50,7 +50,7 @@ def main():
     ctx.set_tets(verts, tets)
     for _ in range(args.steps):
         st = {}
-        sof.extract_resident(ctx, sof.ExtractOptions(), st, fetch=False)
+        sof.extract_resident(ctx, sof.ExtractOptions(profile=True), st, fetch=False)
     print({k: st[k] for k in ("ms_label", "ms_refine", "ms_eval_kernel", "ms_prep", "ms_sched", "exact_pairs", "contrib_pairs", "point_view_evals", "host_ms_prep",
                                "host_ms_sched", "pairs", "crossing_edges", "kernel_launches")})
 
