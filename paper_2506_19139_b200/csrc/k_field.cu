@@ -91,6 +91,39 @@ __global__ void k_view_rec(int64_t n, const GaussStatic* __restrict__ g, Cam cam
   if (outf) outf[i] = make_recf(r);
 }
 
+// Per-view binning inputs of k_tile_rect, produced by the record kernel in the same
+// pass over GaussStatic when the binding of the view is built right away.
+struct RectOut {
+  int ts, tiles_x, tiles_y;
+  int4* rect;
+  uint32_t* cnt;
+  uint64_t* zkey;
+  int32_t* idx;
+};
+
+// k_view_rec + k_tile_rect in one pass (one GaussStatic read per Gaussian and view).
+__global__ void k_view_rec_rect(int64_t n, const GaussStatic* __restrict__ g, Cam cam, Rec* out, RectOut ro) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {  // sentinel for the exclusive scan over n + 1 counts
+    ro.cnt[n] = 0;
+    return;
+  }
+  const GaussStatic gs = g[i];
+  Rec r;
+  gauss_view(gs, cam, r);
+  out[i] = r;
+  int tx0, tx1, ty0, ty1;
+  uint32_t count = 0;
+  if (tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1)) {
+    count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
+    ro.rect[i] = make_int4(tx0, tx1, ty0, ty1);
+  }
+  ro.cnt[i] = count;
+  ro.zkey[i] = double_key(r.zmin);
+  ro.idx[i] = int32_t(i);
+}
+
 void scene_prep(sof_ctx* c) {
   c->gstat.ensure(c->n);
   if (c->n == 0) return;
@@ -125,7 +158,10 @@ void invalidate_view_caches(sof_ctx* c) {
   mark_views_stale(c);
 }
 
-const Rec* view_records(sof_ctx* c, int view) {
+// Records of `view` (cached for the step when the budget allows). With ro, a fresh
+// computation also writes the binning inputs (returns true in *rect_done).
+static const Rec* view_records_impl(sof_ctx* c, int view, const RectOut* ro, bool* rect_done) {
+  if (rect_done) *rect_done = false;
   if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
   if (c->rec_valid[view]) return c->recs[view].p;
   const int sel = c->scratch_sel;
@@ -144,13 +180,19 @@ const Rec* view_records(sof_ctx* c, int view) {
   }
   dst->ensure(std::max<int64_t>(c->n, 1));
   if (with_f) dstf->ensure(std::max<int64_t>(c->n, 1));
-  if (c->n > 0) {
+  if (c->n > 0 && ro && !with_f) {
+    k_view_rec_rect<<<grid_for(c->n + 1, 128), 128, 0, c->stream>>>(c->n, c->gstat.p, c->cams[view], dst->p, *ro);
+    SOF_LAUNCHED(c);
+    *rect_done = true;
+  } else if (c->n > 0) {
     k_view_rec<<<grid_for(c->n, 128), 128, 0, c->stream>>>(c->n, c->gstat.p, c->cams[view],
                                                             dst->p, with_f ? dstf->p : nullptr);
     SOF_LAUNCHED(c);
   }
   return dst->p;
 }
+
+const Rec* view_records(sof_ctx* c, int view) { return view_records_impl(c, view, nullptr, nullptr); }
 
 // Float filter records of `view`, valid after view_records(c, view).
 const RecF* view_recf(sof_ctx* c, int view) {
@@ -251,9 +293,9 @@ static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
   const Cam& cam = c->cams[view];
   const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
   const int64_t T = int64_t(tiles_x) * tiles_y;
-  const Rec* rec = view_records(c, view);
   const int64_t n = c->n;
   if (n == 0) {
+    view_records(c, view);
     build_binding_tail(c, view, ts, b, 0, T, tiles_x, tiles_y);
     return;
   }
@@ -264,10 +306,15 @@ static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
   c->gidx_in.ensure(n);
   c->gidx_out.ensure(n);
   c->goff.ensure(n + 1);
-  k_tile_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(n, c->gstat.p, rec, cam, ts, tiles_x,
-                                                            tiles_y, c->rect.p, c->gcount.p,
-                                                            c->zkey_in.p, c->gidx_in.p);
-  SOF_LAUNCHED(c);
+  const RectOut ro{ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p};
+  bool rect_done = false;
+  const Rec* rec = view_records_impl(c, view, &ro, &rect_done);
+  if (!rect_done) {
+    k_tile_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(n, c->gstat.p, rec, cam, ts, tiles_x,
+                                                              tiles_y, c->rect.p, c->gcount.p,
+                                                              c->zkey_in.p, c->gidx_in.p);
+    SOF_LAUNCHED(c);
+  }
   bin_by_key(c, view, ts, tiles_x, tiles_y, b, true);
 }
 
@@ -829,8 +876,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     c->scratch_sel = pv & 1;
     try {
       const int p0 = prof_mark(c);
-      prep_rec[pv & 1] = view_records(c, pv);
+      // binding first: it computes the records in the same pass as the tile rectangles
       prep_bd[pv & 1] = tiled ? &view_binding(c, pv, tile_size) : nullptr;
+      prep_rec[pv & 1] = view_records(c, pv);
       prof_span(c, p0, prof_mark(c), kProfPrep);
       SOF_CUDA(cudaEventRecord(c->prep_ev[pv & 1], c->stream));
     } catch (...) {
