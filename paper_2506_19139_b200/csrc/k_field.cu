@@ -806,6 +806,291 @@ __global__ void k_fill_view_outputs(int64_t n, double* o, uint8_t* obs, uint8_t*
   comp[i] = 1;
 }
 
+// ---- grouped classification (binary_search_refine's classify_point over many views) ---------------
+//
+// The bisection classifies the same midpoints against every view (field_eval.hpp:114-125).
+// Per view the schedule + evaluation is only ~100 us of work, so per-view launches were
+// dominated by launch overhead. Here a group of up to kGroupViews views is scheduled and
+// evaluated at once: bins are (view, tile), every (midpoint, view) item is evaluated
+// exactly as k_eval does, and k_group_fixup then applies the reference's per-point view
+// order: views are visited in order and, under prune, the first exterior view ends the
+// visit (field_eval.hpp:121), so later items of that point neither count pairs nor
+// matter. Items evaluated after a point's first exterior view are wasted work only
+// (a few percent: interior midpoints are evaluated in every view anyway).
+
+constexpr int kGroupViews = 32;
+
+struct GroupTables {
+  int g0, G;
+  int64_t bin_base[kGroupViews + 1];  // first bin of each view of the group
+};
+
+__global__ void k_sched_group(int64_t n, const double* __restrict__ xyz, const Cam* __restrict__ cams, int ts,
+                              GroupTables gt, const uint8_t* __restrict__ skip, int32_t* item_bin, int* bin_cnt) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool live = k < n && !(skip && skip[k]);
+  double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+  if (live) {
+    x0 = xyz[3 * k];
+    x1 = xyz[3 * k + 1];
+    x2 = xyz[3 * k + 2];
+  }
+  for (int j = 0; j < gt.G; ++j) {
+    int bin = -1;
+    if (live) {
+      const Cam& cam = cams[gt.g0 + j];
+      const int tiles_x = (cam.w + ts - 1) / ts;
+      const PointRay pr = point_ray(cam, x0, x1, x2, ts, tiles_x);
+      if (pr.observed) bin = int(gt.bin_base[j]) + pr.tile;
+    }
+    if (k < n) item_bin[int64_t(j) * n + k] = bin;
+    warp_tile_add(bin_cnt, bin, bin >= 0);
+  }
+}
+
+__global__ void k_scatter_group(int64_t n, int G, const int32_t* __restrict__ item_bin,
+                                const int* __restrict__ bin_off, int* bin_cur, int32_t* order) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  for (int j = 0; j < G; ++j) {
+    const int bin = (k < n) ? item_bin[int64_t(j) * n + k] : -1;
+    const int slot = warp_tile_add(bin_cur, bin, bin >= 0);
+    if (bin >= 0) order[bin_off[bin] + slot] = int32_t(int64_t(j) * n + k);
+  }
+}
+
+// k_eval's fast loop (default strategies, classify mode) over the items of a group:
+// block.z is a (view, tile) bin; the view's camera, records and tile lists come from
+// device tables. Writes the per-item pair count and exterior flag.
+__global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
+    const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks, const int32_t* __restrict__ items,
+    int64_t n, const double* __restrict__ xyz, const Cam* __restrict__ cams, int ts, GroupTables gt,
+    const int64_t* const* __restrict__ loffs, const int32_t* const* __restrict__ lents,
+    const Rec* const* __restrict__ recs_v, bool early, uint32_t* item_pairs, uint8_t* item_ext,
+    unsigned long long* counters) {
+  __shared__ __align__(16) Rec srec[kChunk];
+  __shared__ unsigned s_dead[2];
+  const int64_t b = blockIdx.x;
+  if (b >= *nblocks) return;
+  const int4 blk = blocks[b];
+  int j = 0;
+  while (j + 1 < gt.G && gt.bin_base[j + 1] <= blk.z) ++j;
+  const int v = gt.g0 + j;
+  const int tile = blk.z - int(gt.bin_base[j]);
+  const Cam cam = cams[v];
+  const Rec* __restrict__ recs = recs_v[v];
+  const int32_t* __restrict__ lent = lents[v];
+  const int tiles_x = (cam.w + ts - 1) / ts;
+  const int p = blk.x + int(threadIdx.x);
+  const bool active = p < blk.y;
+  int64_t item = 0, k = 0;
+  PointRay pr;
+  pr.observed = false;
+  pr.zp = 0.0;
+  if (active) {
+    item = items[p];
+    k = item - int64_t(j) * n;
+    pr = point_ray(cam, xyz[3 * k], xyz[3 * k + 1], xyz[3 * k + 2], ts, tiles_x);
+  }
+  const int64_t l0 = loffs[v][tile], l1 = loffs[v][tile + 1];
+  const float cu = float(pr.px), cv = float(pr.py);
+  const float cuu = cu * cu, cvv = cv * cv, cuv = cu * cv;
+  double survive = 1.0;
+  bool complete = true;
+  bool done = !active;
+  unsigned pairs = 0, exact = 0, contrib = 0;
+  if (threadIdx.x < 2) s_dead[threadIdx.x] = 0;
+  int par = 0;
+  for (int64_t base = l0; base < l1; base += kChunk, par ^= 1) {
+    if (!__syncthreads_or(!done)) break;
+    const int cnt = int(std::min<int64_t>(kChunk, l1 - base));
+    for (int q8 = threadIdx.x; q8 < cnt * kRecV2; q8 += blockDim.x) {
+      const int r = q8 / kRecV2, q = q8 % kRecV2;
+      const int64_t g = int64_t(lent[base + r]);
+      double2 vv = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+      if (q >= 5 && __ldg(&recs[g].op) < kMinAlpha) {
+        if (q == 5) {
+          vv.y = -INFINITY;
+          atomicOr(&s_dead[par], 1u << r);
+        } else if (q == 6) {
+          float4 f = *reinterpret_cast<float4*>(&vv);
+          f.y = 0.0f;
+          f.z = 0.0f;
+          f.w = -1.0f;
+          vv = *reinterpret_cast<double2*>(&f);
+        } else {
+          vv = make_double2(0.0, 0.0);
+        }
+      }
+      reinterpret_cast<double2*>(&srec[r])[q] = vv;
+    }
+    if (threadIdx.x == 0) s_dead[par ^ 1] = 0;
+    __syncthreads();
+    if (done) continue;
+    int kk = 0;
+    const Rec* rp = srec;
+    for (; kk < cnt; ++kk, ++rp) {
+      const Rec& r = *rp;
+      if (r.zmin > pr.zp) {
+        done = true;
+        break;
+      }
+      if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;
+      if (SOF_EVAL_STATS) ++exact;
+      const double alpha = pair_alpha(r, pr.d, pr.t);
+      if (alpha == 0.0) continue;
+      if (SOF_EVAL_STATS) ++contrib;
+      survive *= 1.0 - alpha;
+      if (early && 1.0 - survive > 0.5) {
+        complete = false;
+        done = true;
+        ++kk;
+        break;
+      }
+    }
+    const unsigned upto = (kk >= 32) ? 0xffffffffu : ((1u << kk) - 1u);
+    pairs += unsigned(kk) - __popc(s_dead[par] & upto);
+  }
+  if (active) {
+    item_pairs[item] = pairs;
+    item_ext[item] = (complete && 1.0 - survive < 0.5) ? 1 : 0;
+  }
+  if (SOF_EVAL_STATS) {
+    unsigned long long e = exact, w = contrib;
+    for (int s = 16; s > 0; s >>= 1) {
+      e += __shfl_down_sync(0xffffffffu, e, s);
+      w += __shfl_down_sync(0xffffffffu, w, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (e) atomicAdd(counters + 2, e);
+      if (w) atomicAdd(counters + 3, w);
+    }
+  }
+}
+
+// The reference's view order per midpoint: counters of every observed view up to the
+// first exterior one (all of them without prune), exterior = any.
+__global__ void k_group_fixup(int64_t n, int G, bool prune, const int32_t* __restrict__ item_bin,
+                              const uint32_t* __restrict__ item_pairs, const uint8_t* __restrict__ item_ext,
+                              uint8_t* ext, unsigned long long* counters) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  unsigned long long pairs = 0, pve = 0;
+  if (k < n && !(prune && ext[k])) {
+    bool ex = false;
+    for (int j = 0; j < G; ++j) {
+      const int64_t it = int64_t(j) * n + k;
+      if (item_bin[it] < 0) continue;  // not observed (or skipped)
+      ++pve;
+      pairs += item_pairs[it];
+      if (item_ext[it]) {
+        ex = true;
+        if (prune) break;
+      }
+    }
+    if (ex) ext[k] = 1;
+  }
+  for (int s = 16; s > 0; s >>= 1) {
+    pairs += __shfl_down_sync(0xffffffffu, pairs, s);
+    pve += __shfl_down_sync(0xffffffffu, pve, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (pairs) atomicAdd(counters, pairs);
+    if (pve) atomicAdd(counters + 1, pve);
+  }
+}
+
+// Bisection classification of n points (ext[k] = exterior) over views [v0, v1) in
+// groups; false when the grouped path does not apply (then eval_views runs per view).
+static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int strategies,
+                             int tile_size, uint8_t* ext, uint64_t* counters_host) {
+  if (c->eval_path != 1 || (strategies & 19) != 19 || n <= 0 || v1 <= v0) return false;
+  if (std::getenv("SOF_NO_GROUPED")) return false;
+  const int V = int(c->cams.size());
+  // every view's records and tile lists must be resident (they are after the label pass
+  // unless the cache budget ran out)
+  for (int v = v0; v < v1; ++v) {
+    const Binding& b = c->bindings[v];
+    if (!c->rec_valid[v] || b.view != v || b.tile_size != tile_size) return false;
+  }
+  const int G = std::min(kGroupViews, v1 - v0);
+  if (int64_t(G) * n >= (int64_t(1) << 31)) return false;
+  std::vector<const void*> ptrs(3 * size_t(V), nullptr);
+  for (int v = v0; v < v1; ++v) {
+    ptrs[v] = c->bindings[v].off.p;
+    ptrs[V + v] = c->bindings[v].ent.p;
+    ptrs[2 * V + v] = c->recs[v].p;
+  }
+  GroupScratch& g = c->grp;
+  g.cams.ensure(V);
+  g.ptrs.ensure(3 * V);
+  SOF_CUDA(cudaMemcpyAsync(g.cams.p, c->cams.data(), sizeof(Cam) * V, cudaMemcpyHostToDevice, c->stream));
+  SOF_CUDA(cudaMemcpyAsync(g.ptrs.p, ptrs.data(), sizeof(void*) * 3 * V, cudaMemcpyHostToDevice, c->stream));
+  g.item_bin.ensure(int64_t(G) * n);
+  g.item_pairs.ensure(int64_t(G) * n);
+  g.item_ext.ensure(int64_t(G) * n);
+  g.order.ensure(int64_t(G) * n);
+  c->d_counters.ensure(4);
+  c->d_scalar.ensure(4);
+  zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 4);
+  const bool prune = strategies & 8, early = strategies & 4;
+  const int64_t* const* loffs = reinterpret_cast<const int64_t* const*>(g.ptrs.p);
+  const int32_t* const* lents = reinterpret_cast<const int32_t* const*>(g.ptrs.p + V);
+  const Rec* const* recs = reinterpret_cast<const Rec* const*>(g.ptrs.p + 2 * V);
+  for (int g0 = v0; g0 < v1; g0 += G) {
+    GroupTables gt;
+    gt.g0 = g0;
+    gt.G = std::min(G, v1 - g0);
+    gt.bin_base[0] = 0;
+    for (int j = 0; j < gt.G; ++j) {
+      const Cam& cam = c->cams[g0 + j];
+      const int64_t T = int64_t((cam.w + tile_size - 1) / tile_size) * ((cam.h + tile_size - 1) / tile_size);
+      gt.bin_base[j + 1] = gt.bin_base[j] + T;
+    }
+    const int64_t NB = gt.bin_base[gt.G];
+    PointSchedule& s = c->sched;
+    s.tile_cnt.ensure(2 * (NB + 1));
+    s.tile_off.ensure(NB + 1);
+    s.blk_cnt.ensure(NB + 1);
+    s.blk_off.ensure(NB + 1);
+    zero_async(c, s.tile_cnt.p, int64_t(sizeof(int)) * 2 * (NB + 1));
+    int* cur = s.tile_cnt.p + (NB + 1);
+    const uint8_t* skip = prune ? ext : nullptr;
+    k_sched_group<<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, g.cams.p, tile_size, gt, skip, g.item_bin.p,
+                                                           s.tile_cnt.p);
+    SOF_LAUNCHED(c);
+    exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);
+    k_scatter_group<<<grid_for(n, 256), 256, 0, c->stream>>>(n, gt.G, g.item_bin.p, s.tile_off.p, cur, g.order.p);
+    SOF_LAUNCHED(c);
+    k_block_counts<<<grid_for(NB + 1, 256), 256, 0, c->stream>>>(int(NB), 1, s.tile_off.p, s.blk_cnt.p);
+    SOF_LAUNCHED(c);
+    exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, NB + 1);
+    const int64_t grid = (int64_t(gt.G) * n + kBlockPoints - 1) / kBlockPoints + NB;
+    s.blocks.ensure(grid);
+    k_block_fill<<<grid_for(NB + 1, 256), 256, 0, c->stream>>>(int(NB), 1, s.tile_off.p, s.blk_off.p, s.blocks.p,
+                                                               c->d_scalar.p);
+    SOF_LAUNCHED(c);
+    const int e0 = prof_mark(c);
+    k_eval_group<<<unsigned(grid), 256, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
+                                                        tile_size, gt, loffs, lents, recs, early, g.item_pairs.p,
+                                                        g.item_ext.p, c->d_counters.p);
+    SOF_LAUNCHED(c);
+    prof_span(c, e0, prof_mark(c), kProfEval);
+    c->eval_launches++;
+    k_group_fixup<<<grid_for(n, 256), 256, 0, c->stream>>>(n, gt.G, prune, g.item_bin.p, g.item_pairs.p,
+                                                           g.item_ext.p, ext, c->d_counters.p);
+    SOF_LAUNCHED(c);
+  }
+  if (counters_host) {
+    unsigned long long h[4];
+    SOF_CUDA(cudaMemcpyAsync(h, c->d_counters.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+    counters_host[0] += h[0];
+    counters_host[1] += h[1];
+    c->exact_evals += h[2];
+    c->contrib_evals += h[3];
+  }
+  return true;
+}
+
 template <int MODE>
 static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pidx,
                         const double* xyz, const Cam& cam, int ts, int tiles_x, const Binding* bd,
@@ -850,6 +1135,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   if (tile_size <= 0) throw InvalidArg("tile_size must be positive");
   const bool tiled = strategies & 1;
   const bool prune = strategies & 8;
+  if (mode == kModeClassify &&
+      classify_grouped(c, v0, v1, n, xyz, strategies, tile_size, ext, counters_host))
+    return;
   c->d_counters.ensure(4);
   c->d_scalar.ensure(4);
   zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 4);

@@ -115,6 +115,15 @@ struct MeshScratch {
 };
 
 // Render spill pool (k_render.cu): keys / values double-buffered for the segmented sort.
+// Grouped bisection classification (k_field.cu classify_grouped).
+struct GroupScratch {
+  DBuf<Cam> cams;                 // [V]
+  DBuf<const void*> ptrs;         // [3V] per-view tile offsets, tile entries, records
+  DBuf<int32_t> item_bin, order;  // [G n]
+  DBuf<uint32_t> item_pairs;      // [G n]
+  DBuf<uint8_t> item_ext;         // [G n]
+};
+
 struct RenderScratch {
   DBuf<uint64_t> keys, keys2;
   DBuf<double> alpha, alpha2;
@@ -194,7 +203,8 @@ struct sof_ctx {
   sofk::PointSchedule sched;
   sofk::MeshScratch ms;
   sofk::Binding rbind;                    // render binding (lists ordered by a t* lower bound)
-  sofk::RenderScratch rs;                 // spill pool of k-buffer-overflow pixels
+  sofk::RenderScratch rs;
+  sofk::GroupScratch grp;                 // spill pool of k-buffer-overflow pixels
   sofk::DBuf<double> r_out;               // depth, opacity, rgb(3), t_final per pixel
   sofk::DBuf<double> r_lkey;              // per-Gaussian t* lower bound of the render binning
   sofk::DBuf<unsigned long long> r_stats;

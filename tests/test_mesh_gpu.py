@@ -104,7 +104,7 @@ def test_assemble_random_duplicates(ref):
     np.testing.assert_array_equal(got.triangles, want["triangles"])
 
 
-@pytest.mark.parametrize("mask", [31, 0])
+@pytest.mark.parametrize("mask", [31, 0, 23, 27, 19])
 def test_extract_fused_ply_bytes(ref, lattice_case, tmp_path, mask):
     """The fused device pipeline reproduces extract_mesh's mesh byte for byte
     (Extract.DeterministicAcrossThreadCounts, test_mesher.cpp:242-257)."""
@@ -173,3 +173,25 @@ def test_async_tets_upload(lattice_case):
     ctx.set_tets(verts, tets)
     again = sof.extract_resident(ctx, sof.ExtractOptions(), {})
     np.testing.assert_array_equal(again.triangles, want.triangles)
+
+
+def test_extract_many_views_grouped_bisection(ref):
+    """More views than one classification group (kGroupViews = 32): the grouped bisection
+    keeps the reference's per-point view order, counters included."""
+    scene = ref.random_scene(57, 60, 1.0)
+    cams = ref.orbit_cameras(70, 4.0, 1.8, 48)
+    verts, tets = kuhn_lattice(12, -1.3, 1.3)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    for mask in (31, 23):
+        want = rc.extract_tetgrid(verts, tets, strategies=mask, iterations=8)
+        stats = {}
+        mesh = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets),
+                                sof.ExtractOptions(strategies=sof.EvalStrategies.from_mask(mask)), stats)
+        assert len(want["triangles"]) > 0
+        np.testing.assert_array_equal(bits(mesh.vertices), bits(want["vertices"]))
+        np.testing.assert_array_equal(mesh.triangles, want["triangles"])
+        assert stats["pairs"] == int(want["counters"][0])
+        assert stats["point_view_evals"] == int(want["counters"][1])
+        # label: one launch per view; bisection: one per 32-view group and iteration
+        assert stats["eval_launches"] == 70 + 8 * 3, stats["eval_launches"]
