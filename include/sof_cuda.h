@@ -136,6 +136,10 @@ int sof_set_tets(sof_ctx* ctx, int64_t nv, const double* xyz, int64_t nt, const 
  * sof_marching_tets returns (pinned memory for the copy to overlap). An out-of-range
  * index is reported by that call (SOF_E_INVALID). */
 int sof_set_tets_async(sof_ctx* ctx, int64_t nv, const double* xyz, int64_t nt, const int32_t* tets);
+/* HBM the per-view records and tile lists of one step may keep resident (default: half
+ * of the free memory at sof_ctx_create). Views past the budget are rebuilt when used,
+ * in two scratch slots. */
+int sof_set_cache_budget(sof_ctx* ctx, int64_t bytes);
 
 /* ---- per-view preprocessing and binning (parity / inspection) -------------------- */
 /* PrecomputedGaussian per Gaussian for one view (precompute.hpp:21-28): 13 doubles

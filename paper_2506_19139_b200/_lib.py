@@ -54,6 +54,7 @@ _SIGS = {
     "sof_set_views": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "sof_set_tets": (_I, [_P, _I64, _P, _I64, _P]),
     "sof_set_tets_async": (_I, [_P, _I64, _P, _I64, _P]),
+    "sof_set_cache_budget": (_I, [_P, _I64]),
     "sof_precompute_view": (_I, [_P, _I, _P]),
     "sof_tile_binding": (_I, [_P, _I, _I, _P, _P]),
     "sof_schedule_points": (_I, [_P, _I, _I64, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -80,6 +80,7 @@ int sof_ctx_create(int device, sof_ctx** out) {
     SOF_CUDA(cudaEventCreateWithFlags(&c->tets_ev, cudaEventDisableTiming));
     SOF_CUDA(cudaMallocHost(&c->pinned_scalar, 8 * sizeof(uint64_t)));
     for (auto& e : c->prep_ev) SOF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->eval_ev) SOF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t free_b = 0, total_b = 0;
     SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
     // per-view record / binding caches may take up to half of the free HBM
@@ -100,6 +101,8 @@ void sof_ctx_destroy(sof_ctx* ctx) {
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   for (auto e : ctx->prep_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : ctx->eval_ev)
     if (e) cudaEventDestroy(e);
   for (auto e : ctx->evpool) cudaEventDestroy(e);
   for (auto e : ctx->user_ev)
@@ -194,6 +197,14 @@ int sof_set_tets(sof_ctx* c, int64_t nv, const double* xyz, int64_t nt, const in
     c->nt = nt;
     c->has_tets = true;
     sync(c);
+  });
+}
+
+int sof_set_cache_budget(sof_ctx* c, int64_t bytes) {
+  if (!c || bytes < 0) return SOF_E_INVALID;
+  return guard(c, [&] {
+    c->cache_budget = size_t(bytes);
+    invalidate_view_caches(c);
   });
 }
 

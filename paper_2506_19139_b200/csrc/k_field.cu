@@ -333,6 +333,7 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
   SOF_LAUNCHED(c);
   exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, n + 1);
   const int64_t M = read_scalar(c, c->goff.p + n);
+  if (std::getenv("SOF_DEBUG_ALLVIEWS")) std::fprintf(stderr, "      binding view %d: M %lld\n", view, (long long)M);
   if (charge_cache && &b != &c->bind_scratch[0] && &b != &c->bind_scratch[1]) {
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
@@ -1163,6 +1164,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     c->cub_tmp.swap(c->cub_tmp2);
     c->scratch_sel = pv & 1;
     try {
+      // scratch slot pv & 1 may still hold the records / tile lists of view pv - 2 (past
+      // the cache budget): wait until its evaluation on the main stream is done
+      SOF_CUDA(cudaStreamWaitEvent(c->stream, c->eval_ev[pv & 1], 0));
       const int p0 = prof_mark(c);
       // binding first: it computes the records in the same pass as the tile rectangles
       prep_bd[pv & 1] = tiled ? &view_binding(c, pv, tile_size) : nullptr;
@@ -1180,9 +1184,10 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
   const auto hd0 = std::chrono::steady_clock::now();
   for (int v = v0; v < v1 && n > 0; ++v) {
-    if (dbg && (v - v0 < 3 || v + 1 == v1))
-      std::fprintf(stderr, "    view %3d issued at %8.2f ms\n", v,
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
+    if (dbg && (v - v0 < 3 || v + 1 == v1 || std::getenv("SOF_DEBUG_ALLVIEWS")))
+      std::fprintf(stderr, "    view %3d issued at %8.2f ms ncand %lld list %d\n", v,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count(),
+                   (long long)ncand, int(use_list));
     const Cam& cam = c->cams[v];
     const int tiles_x = (cam.w + tile_size - 1) / tile_size;
     const int tiles_y = (cam.h + tile_size - 1) / tile_size;
@@ -1250,6 +1255,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
                                 strategies, false, min_op, ext, o_out, obs_out, comp_out);
         break;
     }
+    SOF_CUDA(cudaEventRecord(c->eval_ev[v & 1], c->stream));
     // drop pruned points from the candidate list now and then (the reference skips them,
     // field_eval.hpp:147); the list shrinks fast over the first views
     const int done_views = v - v0 + 1;
@@ -1276,6 +1282,16 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
       c->launches += 2;
       s.active.swap(s.active2);
       ncand = read_scalar(c, s.nsel.p);
+      if (dbg && ncand == 0) {
+        SOF_CUDA(cudaDeviceSynchronize());
+        const int64_t again = read_scalar(c, s.nsel.p);
+        std::vector<uint8_t> hext(std::min<int64_t>(n, 1 << 20));
+        SOF_CUDA(cudaMemcpy(hext.data(), ext, hext.size(), cudaMemcpyDeviceToHost));
+        int64_t ones = 0;
+        for (auto e : hext) ones += e;
+        std::fprintf(stderr, "      compaction after view %d -> 0; re-read %lld; ext ones %lld of %lld (mode %d)\n", v,
+                     (long long)again, (long long)ones, (long long)hext.size(), int(mode));
+      }
       use_list = true;
       if (dbg && v == v0)
         std::fprintf(stderr, "      v0 compacted at %8.2f ms\n",

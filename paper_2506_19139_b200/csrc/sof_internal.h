@@ -179,6 +179,7 @@ struct sof_ctx {
 
   // prep lane: a second stream (+ its own CUB scratch) for per-view preprocessing
   cudaStream_t stream2 = nullptr;
+  cudaEvent_t eval_ev[2] = {nullptr, nullptr};  // end of the eval of views of parity 0 / 1
   cudaStream_t stream_copy = nullptr;     // sof_set_tets_async: tet upload + index check
   uint64_t* pinned_scalar = nullptr;      // [8] pinned host slots for small read-backs
   cudaEvent_t tets_ev = nullptr;          // ... recorded after them

@@ -195,3 +195,23 @@ def test_extract_many_views_grouped_bisection(ref):
         assert stats["point_view_evals"] == int(want["counters"][1])
         # label: one launch per view; bisection: one per 32-view group and iteration
         assert stats["eval_launches"] == 70 + 8 * 3, stats["eval_launches"]
+
+
+@pytest.mark.parametrize("budget", [0, 12_000])
+def test_extract_past_cache_budget(ref, budget):
+    """Views past the record / tile-list cache budget are rebuilt in two scratch slots
+    while earlier views still evaluate (prep stream ahead of the eval stream): same mesh
+    and counters as the reference."""
+    scene = ref.random_scene(61, 40, 1.0)
+    cams = ref.orbit_cameras(40, 4.0, 1.8, 48)
+    verts, tets = kuhn_lattice(12, -1.3, 1.3)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    views.ctx.check(views.ctx.lib.sof_set_cache_budget(views.ctx.h, budget))
+    want = rc.extract_tetgrid(verts, tets, strategies=31, iterations=8)
+    stats = {}
+    mesh = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets), sof.ExtractOptions(), stats)
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(mesh.triangles, want["triangles"])
+    assert stats["pairs"] == int(want["counters"][0])
+    assert stats["point_view_evals"] == int(want["counters"][1])
