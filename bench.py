@@ -113,6 +113,39 @@ def ncu_traffic() -> float | None:
         return None
 
 
+# ---- sorted rasterizer sample (secondary: not the headline metric) -------------------------
+
+def render_sample(device: int, views=(0, 1, 2)):
+    """C2 (1M Gaussians, 1920x1080) exact-depth render of a few views through
+    sof_render_view, device-timed with events; outputs stay on the device."""
+    import paper_2506_19139_b200 as sof
+    from paper_2506_19139_b200.workloads import CONFIGS, orbit_cameras, synthetic_scene
+    cfg = CONFIGS["C2"]
+    scene = synthetic_scene(cfg["gaussians"], 2)
+    cams = orbit_cameras(cfg["views"], cfg["width"], cfg["height"]).subset(np.array(views))
+    ctx = sof.Context(device)
+    ctx.set_scene(scene)
+    ctx.set_views(cams)
+    stats = np.zeros(4, np.uint64)
+    ms, res = ctypes.c_float(), []
+    for v in range(len(views)):
+        ctx.check(ctx.lib.sof_event_record(ctx.h, 0))
+        ctx.check(ctx.lib.sof_render_view(ctx.h, v, sof.DEPTH_EXACT, 16, None, None, None, None, stats.ctypes.data))
+        ctx.check(ctx.lib.sof_event_record(ctx.h, 1))
+        ctx.check(ctx.lib.sof_event_elapsed(ctx.h, 0, 1, ctypes.byref(ms)))
+        res.append((ms.value, stats.copy()))
+    timed = res[1:] if len(res) > 1 else res  # the first view also pays one-time allocations
+    t = float(np.mean([r[0] for r in timed]))
+    tested = float(np.mean([float(r[1][0]) for r in timed]))
+    contrib = float(np.mean([float(r[1][1]) for r in timed]))
+    px = cfg["width"] * cfg["height"]
+    ctx.close()
+    return {"config": "C2: 1M Gaussians, 1920x1080, exact depth + colour + T + opacity at depth, bit-exact",
+            "views_timed": len(timed), "ms_per_view": t, "mpix_per_s": px / (t * 1e-3) / 1e6,
+            "tested_pairs_per_s": tested / (t * 1e-3), "contributing_pairs_per_s": contrib / (t * 1e-3),
+            "sorted_path_pixels": int(np.mean([float(r[1][2]) for r in timed]))}
+
+
 # ---- CPU reference (oracle/_ref): bounded sample -----------------------------------------------
 
 def cpu_reference_sample(scene, cams, verts, sample_views=(0, 1), threads=None, vertex_stride=1):
@@ -180,6 +213,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-render", action="store_true", help="skip the C2 render sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -308,6 +342,13 @@ def main():
         except Exception as e:  # the reference build is absent
             cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    render = None
+    if rank == 0 and world == 1 and not args.no_render:
+        try:
+            render = render_sample(local)
+        except Exception as e:
+            render = {"unavailable": str(e)[:200]}
+
     if rank == 0:
         line = {"metric": "opacity-field point queries/sec", "value": value, "unit": "queries/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -328,7 +369,7 @@ def main():
                 "crossing_edges": E, "mesh_vertices": int(last["mesh_vertices"]),
                 "mesh_triangles": int(last["mesh_triangles"]), "pairs_per_step": int(pairs),
                 "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "clocks": clk.summary()}
+                "render": render, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     for a in host_arrays:
         lib.sof_host_unregister(a.ctypes.data)

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--views", type=int, default=8)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--lattice", type=int, default=0, help="override the config's lattice size")
     ap.add_argument("--render", action="store_true", help="render one view instead of meshing")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -46,7 +47,7 @@ def main():
         print(f"render {w}x{h}: {best:.1f} ms device ({w * h / best / 1e3:.1f} Mpix/s) stats "
               f"[tested, contributing, sorted-path pixels, exact-depth fallbacks] = {stats.tolist()}")
         return
-    verts, tets = kuhn_lattice(cfg["lattice"])
+    verts, tets = kuhn_lattice(args.lattice or cfg["lattice"])
     ctx.set_tets(verts, tets)
     for _ in range(args.steps):
         st = {}
