@@ -589,6 +589,40 @@ inline FloatMap normals_to_map(const NormalMap& nm) {
   return m;
 }
 
+// ---- seed points (seed_points.hpp:15-87), on the device ----------------------------------
+
+enum class BoundingVariant { kStp, kThreeSigma, kStretchedSigma };
+enum class SeedCutoff { kNone, kDeadGaussians };
+enum class SeedProvenance : std::uint8_t { kCenter, kBoundCorner };
+
+struct SeedPointSet {
+  std::vector<Vec3> points;
+  std::vector<SeedProvenance> provenance;
+};
+
+// build_seed_points over the ViewSet's scene (the Gaussians uploaded by ViewSet::build);
+// throws std::runtime_error("no live Gaussians") like the reference.
+inline SeedPointSet build_seed_points(const ViewSet& views, BoundingVariant variant,
+                                      SeedCutoff cutoff = SeedCutoff::kNone, double filter_scale = 0.0) {
+  sof_ctx* c = views.ctx.get();
+  Index n = 0;
+  const int st = sof_seed_points(c, int(variant), int(cutoff), filter_scale, &n);
+  if (st == SOF_E_RUNTIME) throw std::runtime_error(sof_last_error(c));
+  detail::check(c, st);
+  std::vector<double> p(3 * size_t(n));
+  std::vector<std::uint8_t> prov(static_cast<size_t>(n));
+  if (n) {
+    detail::check(c, sof_copy_result(c, SOF_R_SEEDS, p.data()));
+    detail::check(c, sof_copy_result(c, SOF_R_SEED_PROVENANCE, prov.data()));
+  }
+  SeedPointSet out;
+  for (Index i = 0; i < n; ++i) {
+    out.points.emplace_back(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
+    out.provenance.push_back(SeedProvenance(prov[size_t(i)]));
+  }
+  return out;
+}
+
 // ---- scene files (io_scene.hpp) ---------------------------------------------------------
 
 struct SceneFile {

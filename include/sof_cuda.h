@@ -66,7 +66,9 @@ enum {
   SOF_R_MESH_TRIS = 5,     /* int32[3T]  Mesh::triangles after assemble_mesh */
   SOF_R_GRID_OPACITY = 6,  /* f64[nv]    TetGrid::opacity after label_grid */
   SOF_R_TILE_OFFSETS = 7,  /* int64[T+1] per-tile list offsets of the last binding */
-  SOF_R_TILE_ENTRIES = 8   /* int32[M]   per-tile Gaussian lists (TileBinding, tiles.hpp:88-92) */
+  SOF_R_TILE_ENTRIES = 8,  /* int32[M]   per-tile Gaussian lists (TileBinding, tiles.hpp:88-92) */
+  SOF_R_SEEDS = 9,         /* f64[3S]    SeedPointSet::points (seed_points.hpp:24-27) */
+  SOF_R_SEED_PROVENANCE = 10 /* uint8[S] SeedPointSet::provenance: 0 centre, 1 bound corner */
 };
 
 typedef struct sof_ctx sof_ctx;
@@ -275,6 +277,15 @@ int sof_normal_from_depth(sof_ctx* ctx, int view, const double* depth, double* n
  * (origin[3k..], dir[3k..]) at parameter t[k] -> out[3k..]. */
 int sof_gaussian_normals(sof_ctx* ctx, int64_t m, const int32_t* gidx, const double* origin,
                          const double* dir, const double* t, double* out);
+
+/* ---- seed points (seed_points.hpp), the producer of the tetra input ------------------ */
+enum { SOF_SEED_STP = 0, SOF_SEED_THREE_SIGMA = 1, SOF_SEED_STRETCHED_SIGMA = 2 }; /* BoundingVariant */
+enum { SOF_SEED_CUT_NONE = 0, SOF_SEED_CUT_DEAD = 1 };                             /* SeedCutoff */
+/* build_seed_points (seed_points.hpp:41-87) over the context's scene: Gaussian centres
+ * plus the 8 oriented bounding-box corners, deduplicated on the 1e-9 grid in insertion
+ * order, on the device. *n_out = seeds; results SOF_R_SEEDS / SOF_R_SEED_PROVENANCE.
+ * "no live Gaussians" (SOF_E_RUNTIME) when nothing survives. */
+int sof_seed_points(sof_ctx* ctx, int variant, int cutoff, double filter_scale, int64_t* n_out);
 
 /* ---- scene files (io_scene.hpp) ---------------------------------------------------- */
 /* parse_scene (io_scene.hpp:54-134): binary little-endian splatting PLY (x y z,

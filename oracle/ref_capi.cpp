@@ -475,6 +475,23 @@ void* sofref_seed_delaunay(const sofref_ctx* c, int bounding, int cutoff) {
   }
 }
 
+/// build_seed_points (seed_points.hpp:41-87) -> bag{points f64[3S], provenance u8[S]} or NULL
+void* sofref_seed_points(const sofref_ctx* c, int bounding, int cutoff, double filter_scale) {
+  try {
+    const SeedPointSet seeds =
+        build_seed_points(c->gaussians, BoundingVariant(bounding), SeedCutoff(cutoff), filter_scale);
+    auto* bag = new Bag;
+    bag->put_vec3("points", seeds.points);
+    std::vector<uint8_t> prov;
+    for (auto p : seeds.provenance) prov.push_back(uint8_t(p));
+    bag->put("provenance", prov);
+    return bag;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
 /// extract_mesh (extract.hpp:35-86), the full reference pipeline incl. seeds + Delaunay.
 void* sofref_extract_full(sofref_ctx* c, int strategies, int tile_size, int iterations,
                           int threads) {

@@ -129,6 +129,8 @@ class RefLib:
         L.sofref_assemble.argtypes = [_L, _P, _L, _P, _P, _D, _D]
         L.sofref_extract_tetgrid.restype = _P
         L.sofref_extract_tetgrid.argtypes = [_P, _L, _P, _L, _P, _I, _I, _I, _I]
+        L.sofref_seed_points.restype = _P
+        L.sofref_seed_points.argtypes = [_P, _I, _I, ctypes.c_double]
         L.sofref_seed_delaunay.restype = _P
         L.sofref_seed_delaunay.argtypes = [_P, _I, _I]
         L.sofref_extract_full.restype = _P
@@ -295,6 +297,12 @@ class RefContext:
         out = np.empty(len(xyz))
         self.ref.lib.sofref_opacity_at_point(self.h, len(xyz), _ptr(xyz), _ptr(out))
         return out
+
+    def seed_points(self, bounding: int = 0, cutoff: int = 1, filter_scale: float = 0.0):
+        """build_seed_points (seed_points.hpp:41-87) -> (points [S, 3], provenance [S])."""
+        b = self.ref._bag(self.ref.lib.sofref_seed_points(self.h, bounding, cutoff, filter_scale),
+                          {"points": np.float64, "provenance": np.uint8})
+        return b["points"].reshape(-1, 3), b["provenance"]
 
     def seed_delaunay(self, bounding: int = 0, cutoff: int = 1) -> dict:
         b = self.ref._bag(self.ref.lib.sofref_seed_delaunay(self.h, bounding, cutoff),

@@ -19,6 +19,9 @@ TILE_SCHEDULING, MIN_Z, EARLY_STOP, PRUNE, DEAD_CULL = 1, 2, 4, 8, 16
 ALL_STRATEGIES, NAIVE = 31, 0
 DEPTH_MEDIAN, DEPTH_EXACT = 0, 1
 R_EDGES, R_EDGE_VERTS, R_TRIANGLES, R_MESH_VERTS, R_MESH_TRIS, R_GRID_OPACITY, R_TILE_OFFSETS, R_TILE_ENTRIES = range(1, 9)
+R_SEEDS, R_SEED_PROVENANCE = 9, 10
+SEED_STP, SEED_THREE_SIGMA, SEED_STRETCHED_SIGMA = 0, 1, 2
+SEED_CUT_NONE, SEED_CUT_DEAD = 0, 1
 
 _P = ctypes.c_void_p
 _D = ctypes.c_double
@@ -75,6 +78,7 @@ _SIGS = {
     "sof_render_normals": (_I, [_P, _I, _P, _P]),
     "sof_normal_from_depth": (_I, [_P, _I, _P, _P, _P]),
     "sof_gaussian_normals": (_I, [_P, ctypes.c_int64, _P, _P, _P, _P, _P]),
+    "sof_seed_points": (_I, [_P, _I, _I, _D, _P]),
     "sof_load_scene_ply": (_I, [_P, ctypes.c_char_p, _D, _P]),
     "sof_get_scene": (_I, [_P, _P, _P, _P, _P, _P]),
     "sof_write_scene_ply": (_I, [_P, ctypes.c_char_p]),

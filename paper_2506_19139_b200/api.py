@@ -635,6 +635,23 @@ def write_mesh(mesh: Mesh, path: str, fmt: str = "ply"):
     (write_mesh_obj if fmt == "obj" else write_mesh_ply)(mesh, path)
 
 
+@dataclass
+class SeedPointSet:
+    """seed_points.hpp:24-27: points and provenance (0 centre, 1 bounding-box corner)."""
+    points: np.ndarray
+    provenance: np.ndarray
+
+
+def build_seed_points(ctx: Context, variant: int = L.SEED_STP, cutoff: int = L.SEED_CUT_NONE,
+                      filter_scale: float = 0.0) -> SeedPointSet:
+    """build_seed_points (seed_points.hpp:41-87) over ctx's scene, on the device: Gaussian
+    centres + the 8 oriented bounding-box corners, deduplicated on the 1e-9 grid in
+    insertion order. RuntimeError "no live Gaussians" when nothing survives."""
+    n = ctypes.c_int64(0)
+    ctx.check(ctx.lib.sof_seed_points(ctx.h, int(variant), int(cutoff), float(filter_scale), ctypes.byref(n)))
+    return SeedPointSet(ctx.result(L.R_SEEDS, np.float64, 3), ctx.result(L.R_SEED_PROVENANCE, np.uint8, 1).ravel())
+
+
 def parse_scene(path: str, ctx: Context | None = None, filter_scale: float = 0.0) -> GaussianScene:
     """parse_scene (io_scene.hpp:54-134), decoded and activated on the device of `ctx`
     (default context), which keeps the scene resident."""

@@ -585,6 +585,17 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
   });
 }
 
+int sof_seed_points(sof_ctx* c, int variant, int cutoff, double filter_scale, int64_t* n_out) {
+  if (!c) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (!c->has_scene) throw StateError("no scene: call sof_set_scene first");
+    if (variant < 0 || variant > 2 || cutoff < 0 || cutoff > 1) throw InvalidArg("invalid seed options");
+    seed_points(c, variant, cutoff, filter_scale);
+    sync(c);
+    if (n_out) *n_out = c->n_seeds;
+  });
+}
+
 int64_t sof_result_count(const sof_ctx* c, int kind) {
   if (!c) return -1;
   switch (kind) {
@@ -596,6 +607,8 @@ int64_t sof_result_count(const sof_ctx* c, int kind) {
     case SOF_R_GRID_OPACITY: return c->grid_n;
     case SOF_R_TILE_OFFSETS: return c->bind_tiles < 0 ? -1 : c->bind_tiles + 1;
     case SOF_R_TILE_ENTRIES: return c->bind_entries;
+    case SOF_R_SEEDS: return c->n_seeds < 0 ? -1 : 3 * c->n_seeds;
+    case SOF_R_SEED_PROVENANCE: return c->n_seeds;
     default: return -1;
   }
 }
@@ -616,6 +629,8 @@ int sof_copy_result(sof_ctx* c, int kind, void* dst) {
       case SOF_R_GRID_OPACITY: download(c, (double*)dst, c->grid_opacity.p, cnt); break;
       case SOF_R_TILE_OFFSETS: download(c, (int64_t*)dst, c->goff.p, cnt); break;
       case SOF_R_TILE_ENTRIES: download(c, (int32_t*)dst, c->eval_in.p, cnt); break;
+      case SOF_R_SEEDS: download(c, (double*)dst, c->seeds.p, cnt); break;
+      case SOF_R_SEED_PROVENANCE: download(c, (uint8_t*)dst, c->seed_prov.p, cnt); break;
     }
     sync(c);
   });

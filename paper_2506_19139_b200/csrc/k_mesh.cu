@@ -389,9 +389,9 @@ __global__ void k_weld_keys(int64_t n, const double* __restrict__ v, double inv,
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   // llround(p * inv) (mesh.hpp:57-62); any bijection of the int64 works as a sort key
-  kx[i] = uint64_t(llround(v[3 * i] * inv));
-  ky[i] = uint64_t(llround(v[3 * i + 1] * inv));
-  kz[i] = uint64_t(llround(v[3 * i + 2] * inv));
+  kx[i] = uint64_t(x86_llround(v[3 * i] * inv));
+  ky[i] = uint64_t(x86_llround(v[3 * i + 1] * inv));
+  kz[i] = uint64_t(x86_llround(v[3 * i + 2] * inv));
   idx[i] = int32_t(i);
 }
 
@@ -473,13 +473,11 @@ __global__ void k_compact_tris(int64_t nt, const int32_t* __restrict__ keep,
   for (int q = 0; q < 3; ++q) out[3 * pos[k] + q] = rt[3 * k + q];
 }
 
-void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t* tris,
-              double weld_eps, double min_area) {
-  c->mesh_nv = c->mesh_nt = 0;
-  c->m_verts.ensure(3);
-  c->m_tris.ensure(3);
-  if (n == 0) return;
-  const double inv = 1.0 / weld_eps;
+// First-appearance dedup of n points on the grid llround(p * inv) (mesh.hpp:57-68,
+// seed_points.hpp:61-70): leaves in MeshScratch is_first (wfirst), the new id of every
+// first appearance (nid, exclusive scan) and first_of (index of the first point of each
+// point's key); returns the number of distinct keys.
+int64_t dedup_first(sof_ctx* c, int64_t n, const double* v, double inv) {
   MeshScratch& s = c->ms;
   DBuf<uint64_t>&kx = s.kx, &ky = s.ky, &kz = s.kz, &k1 = s.k1, &k2 = s.k2;
   DBuf<int32_t>&p0 = s.p0, &p1 = s.p1, &head = s.whead, &run = s.wrun, &run_first = s.wrun_first,
@@ -506,7 +504,18 @@ void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t*
                                                          first_of.p, is_first.p);
   SOF_LAUNCHED(c);
   exclusive_scan_i32(c, is_first.p, nid.p, n);
-  const int64_t nout = int64_t(read_scalar(c, nid.p + (n - 1))) + read_scalar(c, is_first.p + (n - 1));
+  return int64_t(read_scalar(c, nid.p + (n - 1))) + read_scalar(c, is_first.p + (n - 1));
+}
+
+void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t* tris,
+              double weld_eps, double min_area) {
+  c->mesh_nv = c->mesh_nt = 0;
+  c->m_verts.ensure(3);
+  c->m_tris.ensure(3);
+  if (n == 0) return;
+  MeshScratch& s = c->ms;
+  const int64_t nout = dedup_first(c, n, v, 1.0 / weld_eps);
+  DBuf<int32_t>&first_of = s.first_of, &is_first = s.wfirst, &nid = s.nid;
   c->m_verts.ensure(3 * nout);
   k_weld_out<<<grid_for(n, 256), 256, 0, c->stream>>>(n, is_first.p, nid.p, v, c->m_verts.p);
   SOF_LAUNCHED(c);
@@ -525,6 +534,93 @@ void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t*
   k_compact_tris<<<grid_for(nt, 256), 256, 0, c->stream>>>(nt, keep.p, pos.p, rt.p, c->m_tris.p);
   SOF_LAUNCHED(c);
   c->mesh_nt = ntout;
+}
+
+// ---- seed points (seed_points.hpp:41-87) --------------------------------------------------------
+
+// Candidate seeds in the reference's insertion order: per Gaussian its centre (slot
+// 9 i) then the 8 oriented E-box corners (slots 9 i + 1 + mask); valid = inserted
+// (finite, not cut off, corners only when the radius is positive).
+__global__ void k_seed_candidates(int64_t n, const double* __restrict__ pos, const double* __restrict__ scale,
+                                  const double* __restrict__ rot, const double* __restrict__ opa, double fs,
+                                  int variant, int cutoff, double* pts, uint8_t* prov, int32_t* valid) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  GaussStatic g;
+  gauss_static(pos + 3 * i, scale + 3 * i, rot + 4 * i, opa[i], fs, g);
+  const double eff = g.op;  // filtered_opacity (gaussian.hpp:67-73)
+  const bool cut = cutoff == SOF_SEED_CUT_DEAD && eff < kMinAlpha;
+  const double r = (variant == SOF_SEED_THREE_SIGMA) ? 3.0 : (variant == SOF_SEED_STRETCHED_SIGMA) ? 3.33 : g.E;
+  for (int s = 0; s < 9; ++s) {
+    double p[3];
+    if (s == 0) {
+      for (int k = 0; k < 3; ++k) p[k] = pos[3 * i + k];
+    } else {
+      const int mask = s - 1;
+      const double l[3] = {r * scale[3 * i] * ((mask & 1) ? 1 : -1), r * scale[3 * i + 1] * ((mask & 2) ? 1 : -1),
+                           r * scale[3 * i + 2] * ((mask & 4) ? 1 : -1)};
+      for (int k = 0; k < 3; ++k)
+        p[k] = pos[3 * i + k] + (g.rot[3 * k] * l[0] + g.rot[3 * k + 1] * l[1] + g.rot[3 * k + 2] * l[2]);
+    }
+    const bool ok = !cut && (s == 0 || r > 0.0) && isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]);
+    const int64_t slot = 9 * i + s;
+    for (int k = 0; k < 3; ++k) pts[3 * slot + k] = p[k];
+    prov[slot] = s == 0 ? 0 : 1;
+    valid[slot] = ok;
+  }
+}
+
+__global__ void k_seed_compact(int64_t m, const int32_t* __restrict__ valid, const int32_t* __restrict__ pos,
+                               const double* __restrict__ pts, const uint8_t* __restrict__ prov, double* out,
+                               uint8_t* out_prov) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= m || !valid[k]) return;
+  const int64_t o = pos[k];
+  for (int d = 0; d < 3; ++d) out[3 * o + d] = pts[3 * k + d];
+  out_prov[o] = prov[k];
+}
+
+__global__ void k_seed_out(int64_t n, const int32_t* __restrict__ is_first, const int32_t* __restrict__ nid,
+                           const double* __restrict__ pts, const uint8_t* __restrict__ prov, double* out,
+                           uint8_t* out_prov) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n || !is_first[k]) return;
+  const int64_t o = nid[k];
+  for (int d = 0; d < 3; ++d) out[3 * o + d] = pts[3 * k + d];
+  out_prov[o] = prov[k];
+}
+
+// build_seed_points over the context's scene -> c->seeds / c->seed_prov
+void seed_points(sof_ctx* c, int variant, int cutoff, double filter_scale) {
+  const int64_t n = c->n, m = 9 * n;
+  MeshScratch& s = c->ms;
+  c->n_seeds = 0;
+  s.seed_pts.ensure(std::max<int64_t>(3 * m, 3));
+  s.seed_prov.ensure(std::max<int64_t>(m, 1));
+  s.seed_valid.ensure(std::max<int64_t>(m, 1));
+  s.seed_pos.ensure(std::max<int64_t>(m, 1));
+  if (n > 0) {
+    k_seed_candidates<<<grid_for(n, 128), 128, 0, c->stream>>>(n, c->pos.p, c->scale.p, c->rot.p, c->opa.p,
+                                                               filter_scale, variant, cutoff, s.seed_pts.p,
+                                                               s.seed_prov.p, s.seed_valid.p);
+    SOF_LAUNCHED(c);
+    exclusive_scan_i32(c, s.seed_valid.p, s.seed_pos.p, m);
+  }
+  const int64_t mv = (n > 0) ? int64_t(read_scalar(c, s.seed_pos.p + (m - 1))) + read_scalar(c, s.seed_valid.p + (m - 1))
+                             : 0;
+  if (mv == 0) throw std::runtime_error("no live Gaussians");  // seed_points.hpp:85
+  s.seed_cpts.ensure(3 * mv);
+  s.seed_cprov.ensure(mv);
+  k_seed_compact<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.seed_valid.p, s.seed_pos.p, s.seed_pts.p,
+                                                          s.seed_prov.p, s.seed_cpts.p, s.seed_cprov.p);
+  SOF_LAUNCHED(c);
+  const int64_t nout = dedup_first(c, mv, s.seed_cpts.p, 1e9);  // llround(p * 1e9) keys
+  c->seeds.ensure(3 * nout);
+  c->seed_prov.ensure(nout);
+  k_seed_out<<<grid_for(mv, 256), 256, 0, c->stream>>>(mv, s.wfirst.p, s.nid.p, s.seed_cpts.p, s.seed_cprov.p,
+                                                       c->seeds.p, c->seed_prov.p);
+  SOF_LAUNCHED(c);
+  c->n_seeds = nout;
 }
 
 }  // namespace sofk

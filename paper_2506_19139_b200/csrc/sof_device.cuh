@@ -294,6 +294,14 @@ __host__ __device__ inline int x86_int(double x) {
   return (x >= -2147483648.0 && x < 2147483648.0) ? (int)x : (int)0x80000000;
 }
 
+// glibc x86-64 std::llround: exact for |x| < 2^63; beyond that (and NaN) the result is
+// (long long) x, i.e. cvttsd2si's 0x8000000000000000 for either sign (the reference
+// binary's key at mesh.hpp:57-62 and seed_points.hpp:61-64).
+__host__ __device__ inline long long x86_llround(double x) {
+  return (x > -9223372036854775808.0 && x < 9223372036854775808.0) ? llround(x)
+                                                                   : (long long)0x8000000000000000ull;
+}
+
 // Tile rectangle of one Gaussian's E-scaled OBB (build_tile_binding tiles.hpp:104-133).
 // Returns false when the Gaussian is skipped (E <= 0 or fully off screen).
 __host__ __device__ inline bool tile_rect(const GaussStatic& g, const Cam& cam, int tile_size,

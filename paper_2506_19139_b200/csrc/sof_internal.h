@@ -112,6 +112,9 @@ struct MeshScratch {
   DBuf<uint8_t> rext;
   DBuf<uint64_t> kx, ky, kz, k1, k2;  // weld
   DBuf<int32_t> p0, p1, whead, wrun, wrun_first, first_of, wfirst, nid, rt, keep, pos;
+  DBuf<double> seed_pts, seed_cpts;       // seed candidates / valid ones in order
+  DBuf<uint8_t> seed_prov, seed_cprov;
+  DBuf<int32_t> seed_valid, seed_pos;
 };
 
 // Render spill pool (k_render.cu): keys / values double-buffered for the segmented sort.
@@ -205,7 +208,10 @@ struct sof_ctx {
   sofk::MeshScratch ms;
   sofk::Binding rbind;                    // render binding (lists ordered by a t* lower bound)
   sofk::RenderScratch rs;
-  sofk::GroupScratch grp;                 // spill pool of k-buffer-overflow pixels
+  sofk::GroupScratch grp;
+  sofk::DBuf<double> seeds;               // build_seed_points result
+  sofk::DBuf<uint8_t> seed_prov;
+  int64_t n_seeds = -1;                 // spill pool of k-buffer-overflow pixels
   sofk::DBuf<double> r_out;               // depth, opacity, rgb(3), t_final per pixel
   sofk::DBuf<double> r_lkey;              // per-Gaussian t* lower bound of the render binning
   sofk::DBuf<unsigned long long> r_stats;
@@ -285,6 +291,8 @@ void refine_init(sof_ctx* c, int64_t ne, const int32_t* edges_dev);
 void refine_mid(sof_ctx* c, int64_t ne, uint8_t* ext_dev);
 void refine_update(sof_ctx* c, int64_t ne, const uint8_t* ext_dev);
 void refine_final(sof_ctx* c, int64_t ne, double* verts_dev);
+int64_t dedup_first(sof_ctx* c, int64_t n, const double* v, double inv);
+void seed_points(sof_ctx* c, int variant, int cutoff, double filter_scale);
 void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris,
               const int32_t* tris_dev, double weld_eps, double min_area);
 

@@ -251,6 +251,21 @@ TEST(SceneIO, RoundTripAndErrors) {
   EXPECT_EQ(b.triangles[0][2], 2);
 }
 
+TEST(SeedPoints, CentresAndCorners) {
+  GaussianPrimitive g;  // unit Gaussian, opacity 1: centre + 8 corners at +-E
+  GaussianPrimitive dead;
+  dead.position = Vec3(5, 0, 0);
+  dead.opacity = 0.001;
+  const ViewSet views = ViewSet::build({g, dead}, {Camera{}});
+  const SeedPointSet s = build_seed_points(views, BoundingVariant::kThreeSigma, SeedCutoff::kDeadGaussians);
+  ASSERT_EQ(s.points.size(), 9u);
+  EXPECT_EQ(s.provenance[0], SeedProvenance::kCenter);
+  EXPECT_EQ(s.points[1](0), -3.0);
+  EXPECT_EQ(s.points[8](2), 3.0);
+  const SeedPointSet all = build_seed_points(views, BoundingVariant::kThreeSigma, SeedCutoff::kNone);
+  EXPECT_EQ(all.points.size(), 18u);
+}
+
 TEST(Errors, NonFiniteScene) {
   GaussianPrimitive g;
   g.position = Vec3(0, std::nan(""), 0);

@@ -215,3 +215,19 @@ def test_extract_past_cache_budget(ref, budget):
     np.testing.assert_array_equal(mesh.triangles, want["triangles"])
     assert stats["pairs"] == int(want["counters"][0])
     assert stats["point_view_evals"] == int(want["counters"][1])
+
+
+def test_assemble_overflowing_weld_keys(ref):
+    """llround(p * 1e7) beyond 2^63 is x86's 0x8000000000000000 for either sign in the
+    reference binary (mesh.hpp:57-62): such vertices weld together on that axis."""
+    rng = np.random.default_rng(8)
+    verts = rng.normal(size=(300, 3))
+    verts[::7, 0] = 2e12
+    verts[1::7, 0] = -3e12
+    verts[2::7, 1:] = verts[3::7, 1:][: len(verts[2::7])]
+    verts[3::7, 0] = 5e12
+    tris = rng.integers(0, len(verts), (500, 3)).astype(np.int32)
+    got = sof.assemble_mesh(verts, tris)
+    want = ref.assemble(verts, tris)
+    np.testing.assert_array_equal(bits(got.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(got.triangles, want["triangles"])
