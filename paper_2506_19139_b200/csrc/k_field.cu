@@ -511,6 +511,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
     unsigned long long* pairs_counter) {
   static_assert(!FAST || TILED, "the fast loop relies on min_z-sorted tile lists");
   __shared__ __align__(16) Rec srec[kChunk];
+  __shared__ __align__(16) double s_exp[128];  // sof_exp's table (shared-memory latency)
   __shared__ unsigned s_dead[2];
   const int64_t b = blockIdx.x;
   if (b >= *nblocks) return;
@@ -538,6 +539,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
   bool done = !active;
   unsigned pairs = 0, exact = 0, contrib = 0;
   if (FAST && threadIdx.x < 2) s_dead[threadIdx.x] = 0;  // published by the first barrier
+  if (threadIdx.x < 128) s_exp[threadIdx.x] = kSofExpTabDev[threadIdx.x];
   int par = 0;
   for (int64_t base = l0; base < l1; base += kChunk, par ^= 1) {
     if (!__syncthreads_or(!done)) break;
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
         }
         if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
         if (SOF_EVAL_STATS) ++exact;
-        const double alpha = pair_alpha(r, pr.d, pr.t);
+        const double alpha = pair_alpha(r, pr.d, pr.t, s_exp);
         if (alpha == 0.0) continue;
         if (SOF_EVAL_STATS) ++contrib;
         survive *= 1.0 - alpha;
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
         ++pairs;
         if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
         if (SOF_EVAL_STATS) ++exact;
-        const double alpha = pair_alpha(r, pr.d, pr.t);
+        const double alpha = pair_alpha(r, pr.d, pr.t, s_exp);
         if (alpha == 0.0) continue;
         if (SOF_EVAL_STATS) ++contrib;
         survive *= 1.0 - alpha;
@@ -870,6 +872,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
     unsigned long long* counters) {
   __shared__ __align__(16) Rec srec[kChunk];
   __shared__ unsigned s_dead[2];
+  __shared__ __align__(16) double s_exp[128];
   const int64_t b = blockIdx.x;
   if (b >= *nblocks) return;
   const int4 blk = blocks[b];
@@ -900,6 +903,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
   bool done = !active;
   unsigned pairs = 0, exact = 0, contrib = 0;
   if (threadIdx.x < 2) s_dead[threadIdx.x] = 0;
+  if (threadIdx.x < 128) s_exp[threadIdx.x] = kSofExpTabDev[threadIdx.x];
   int par = 0;
   for (int64_t base = l0; base < l1; base += kChunk, par ^= 1) {
     if (!__syncthreads_or(!done)) break;
@@ -937,7 +941,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
       }
       if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;
       if (SOF_EVAL_STATS) ++exact;
-      const double alpha = pair_alpha(r, pr.d, pr.t);
+      const double alpha = pair_alpha(r, pr.d, pr.t, s_exp);
       if (alpha == 0.0) continue;
       if (SOF_EVAL_STATS) ++contrib;
       survive *= 1.0 - alpha;
