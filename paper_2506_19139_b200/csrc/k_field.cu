@@ -333,7 +333,6 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
   SOF_LAUNCHED(c);
   exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, n + 1);
   const int64_t M = read_scalar(c, c->goff.p + n);
-  if (std::getenv("SOF_DEBUG_ALLVIEWS")) std::fprintf(stderr, "      binding view %d: M %lld\n", view, (long long)M);
   if (charge_cache && &b != &c->bind_scratch[0] && &b != &c->bind_scratch[1]) {
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
@@ -1188,7 +1187,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
   const auto hd0 = std::chrono::steady_clock::now();
   for (int v = v0; v < v1 && n > 0; ++v) {
-    if (dbg && (v - v0 < 3 || v + 1 == v1 || std::getenv("SOF_DEBUG_ALLVIEWS")))
+    if (dbg && (v - v0 < 3 || v + 1 == v1))
       std::fprintf(stderr, "    view %3d issued at %8.2f ms ncand %lld list %d\n", v,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count(),
                    (long long)ncand, int(use_list));
@@ -1198,9 +1197,6 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     const int T = tiled ? tiles_x * tiles_y : 1;
     const auto h0 = std::chrono::steady_clock::now();
     if (v == v0) prep_view(v);
-    if (dbg && v == v0)
-      std::fprintf(stderr, "      v0 prepped at %8.2f ms\n",
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
     // the records / binding of view v were prepared on the prep lane (during view v-1)
     SOF_CUDA(cudaStreamWaitEvent(c->stream, c->prep_ev[v & 1], 0));
 
@@ -1264,9 +1260,6 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     // field_eval.hpp:147); the list shrinks fast over the first views
     const int done_views = v - v0 + 1;
     pump_upload(c, kUploadChunk);  // a pending tets upload advances one chunk per view
-    if (dbg && v == v0)
-      std::fprintf(stderr, "      v0 eval issued at %8.2f ms\n",
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
     if (skip && v + 1 < v1 && (done_views <= 4 || done_views % 16 == 0)) {
       s.active2.ensure(std::max<int64_t>(ncand, 1));
       s.nsel.ensure(1);
@@ -1286,20 +1279,8 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
       c->launches += 2;
       s.active.swap(s.active2);
       ncand = read_scalar(c, s.nsel.p);
-      if (dbg && ncand == 0) {
-        SOF_CUDA(cudaDeviceSynchronize());
-        const int64_t again = read_scalar(c, s.nsel.p);
-        std::vector<uint8_t> hext(std::min<int64_t>(n, 1 << 20));
-        SOF_CUDA(cudaMemcpy(hext.data(), ext, hext.size(), cudaMemcpyDeviceToHost));
-        int64_t ones = 0;
-        for (auto e : hext) ones += e;
-        std::fprintf(stderr, "      compaction after view %d -> 0; re-read %lld; ext ones %lld of %lld (mode %d)\n", v,
-                     (long long)again, (long long)ones, (long long)hext.size(), int(mode));
-      }
       use_list = true;
-      if (dbg && v == v0)
-        std::fprintf(stderr, "      v0 compacted at %8.2f ms\n",
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
+      if (ncand == 0) break;  // every point is pruned: the remaining views skip them all
     }
     if (v + 1 < v1) {
       const auto h3 = std::chrono::steady_clock::now();

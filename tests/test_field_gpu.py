@@ -183,3 +183,23 @@ def test_errors(ref):
         ctx.set_scene(scene)
     with pytest.raises(sof.SofError, match="no scene"):
         sof.FieldEvaluator(None, sof.ViewSet(ctx, None, None, 0.0)).label_grid(np.zeros((3, 3)))
+
+
+def test_label_all_points_pruned_early(ref):
+    """Points that are exterior in the first views are pruned from every later view
+    (field_eval.hpp:147); when the candidate list empties, the remaining views have
+    nothing to evaluate."""
+    scene = ref.random_scene(52, 50, 0.3)
+    cams = ref.orbit_cameras(24, 4.0, 1.8, 32)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    centre0 = -cams.R[0].T @ cams.t[0]
+    # halfway between camera 0 and the scene: exterior in view 0, pruned afterwards
+    pts = 0.5 * centre0 + np.random.default_rng(1).normal(0, 0.05, (500, 3))
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
+    rev = rc.evaluator(ALL)
+    got = ev.label_grid(pts)
+    assert_bits(got, rev.label_grid(pts))
+    assert ev.counters() == rev.counters()
+    # every point exterior in view 0 and never evaluated again
+    assert (got < 0.5).all() and ev.counters()["point_view_evals"] == len(pts)
