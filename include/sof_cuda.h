@@ -247,6 +247,12 @@ int sof_fp64_peak(sof_ctx* ctx, double* tflops);
  * 1 = FP64 for every pair (default). Both produce bit-identical results and counters. */
 int sof_set_eval_path(sof_ctx* ctx, int path);
 
+/* record staging of the FP64 fast loop (default strategies): 0 = every thread loads
+ * 16 B of the chunk (default, fastest on B200), 1 = TMA row gather (cp.async.bulk.tensor
+ * tile::gather4 over the tile's index list into an mbarrier double buffer). Identical
+ * results; an sm_100a implementation choice (the reference has no equivalent). */
+int sof_set_staging(sof_ctx* ctx, int mode);
+
 /* ---- results ------------------------------------------------------------------------ */
 int64_t sof_result_count(const sof_ctx* ctx, int kind); /* elements (not bytes); <0 if none */
 int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);

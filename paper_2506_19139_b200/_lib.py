@@ -90,6 +90,7 @@ _SIGS = {
     "sof_host_unregister": (_I, [_P]),
     "sof_fp64_peak": (_I, [_P, ctypes.POINTER(_D)]),
     "sof_set_eval_path": (_I, [_P, _I]),
+    "sof_set_staging": (_I, [_P, _I]),
     "sof_tets_vertices_dev": (_I, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
     "sof_shard_ext_rank_dev": (_I, [_P, _I64, _P, _I, _I, _P]),
     "sof_shard_mask_min_dev": (_I, [_P, _I64, _P, _I, _P]),

@@ -477,6 +477,12 @@ int sof_set_eval_path(sof_ctx* c, int path) {
   return SOF_OK;
 }
 
+int sof_set_staging(sof_ctx* c, int mode) {
+  if (!c || mode < 0 || mode > 1) return SOF_E_INVALID;
+  c->staging = mode;
+  return SOF_OK;
+}
+
 void sof_extract_opts_default(sof_extract_opts* o) {
   if (!o) return;
   o->strategies = SOF_ALL_STRATEGIES;

@@ -16,6 +16,7 @@
 #include <cstring>
 
 #include "sof_internal.h"
+#include "sof_tma.cuh"
 
 namespace sofk {
 
@@ -99,6 +100,7 @@ struct RectOut {
   uint32_t* cnt;
   uint64_t* zkey;
   int32_t* idx;
+  bool live_only;  // leave dead Gaussians (op < 1/255) out of the lists (see Binding::live)
 };
 
 // k_view_rec + k_tile_rect in one pass (one GaussStatic read per Gaussian and view).
@@ -115,7 +117,7 @@ __global__ void k_view_rec_rect(int64_t n, const GaussStatic* __restrict__ g, Ca
   out[i] = r;
   int tx0, tx1, ty0, ty1;
   uint32_t count = 0;
-  if (tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1)) {
+  if (!(ro.live_only && r.op < kMinAlpha) && tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1)) {
     count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     ro.rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
@@ -204,7 +206,7 @@ const RecF* view_recf(sof_ctx* c, int view) {
 
 __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
                             const Rec* __restrict__ rec, Cam cam, int ts, int tiles_x, int tiles_y,
-                            int4* rect, uint32_t* cnt, uint64_t* zkey, int32_t* idx) {
+                            bool live_only, int4* rect, uint32_t* cnt, uint64_t* zkey, int32_t* idx) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i > n) return;
   if (i == n) {  // sentinel for the exclusive scan over n + 1 counts
@@ -213,7 +215,7 @@ __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
   }
   int tx0, tx1, ty0, ty1;
   uint32_t count = 0;
-  if (tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1)) {
+  if (!(live_only && rec[i].op < kMinAlpha) && tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1)) {
     count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
@@ -289,11 +291,12 @@ __global__ void k_segment_starts(int64_t m, const K* __restrict__ keys, int64_t 
 static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t M, int64_t T,
                                int tiles_x, int tiles_y);
 
-static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
+static void build_binding(sof_ctx* c, int view, int ts, bool live, Binding& b, bool charge) {
   const Cam& cam = c->cams[view];
   const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
   const int64_t T = int64_t(tiles_x) * tiles_y;
   const int64_t n = c->n;
+  b.live = live;
   if (n == 0) {
     view_records(c, view);
     build_binding_tail(c, view, ts, b, 0, T, tiles_x, tiles_y);
@@ -306,16 +309,16 @@ static void build_binding(sof_ctx* c, int view, int ts, Binding& b) {
   c->gidx_in.ensure(n);
   c->gidx_out.ensure(n);
   c->goff.ensure(n + 1);
-  const RectOut ro{ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p};
+  const RectOut ro{ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p, live};
   bool rect_done = false;
   const Rec* rec = view_records_impl(c, view, &ro, &rect_done);
   if (!rect_done) {
     k_tile_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(n, c->gstat.p, rec, cam, ts, tiles_x,
-                                                              tiles_y, c->rect.p, c->gcount.p,
+                                                              tiles_y, live, c->rect.p, c->gcount.p,
                                                               c->zkey_in.p, c->gidx_in.p);
     SOF_LAUNCHED(c);
   }
-  bin_by_key(c, view, ts, tiles_x, tiles_y, b, true);
+  bin_by_key(c, view, ts, tiles_x, tiles_y, b, charge);
 }
 
 // Second half of a binning: Gaussians sorted by (zkey_in, index) — a stable radix
@@ -337,6 +340,7 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
     if (c->cache_bytes + bytes > c->cache_budget) {
+      c->bind_scratch[c->scratch_sel].live = b.live;
       build_binding_tail(c, view, ts, c->bind_scratch[c->scratch_sel], M, T, tiles_x, tiles_y);
       return;
     }
@@ -370,15 +374,18 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
   SOF_LAUNCHED(c);
 }
 
-const Binding& view_binding(sof_ctx* c, int view, int tile_size) {
+const Binding& view_binding(sof_ctx* c, int view, int tile_size, bool live) {
   Binding& cached = c->bindings[view];
-  if (cached.view == view && cached.tile_size == tile_size) return cached;
+  if (cached.view == view && cached.tile_size == tile_size && cached.live == live) return cached;
   for (int k = 0; k < 2; ++k)
-    if (c->bind_scratch[k].view == view && c->bind_scratch[k].tile_size == tile_size)
+    if (c->bind_scratch[k].view == view && c->bind_scratch[k].tile_size == tile_size &&
+        c->bind_scratch[k].live == live)
       return c->bind_scratch[k];
   // builds into the per-view slot (kept for the rest of the step) or, past the
-  // cache budget, into the scratch slot
-  build_binding(c, view, tile_size, cached);
+  // cache budget, into the scratch slot; a resident binding of this view with other
+  // parameters is rebuilt in place (its bytes are already charged to the budget)
+  const bool resident = cached.view == view;
+  build_binding(c, view, tile_size, live, cached, !resident);
   return (cached.view == view) ? cached : c->bind_scratch[c->scratch_sel];
 }
 
@@ -491,27 +498,95 @@ constexpr int kChunk = 32;  // Gaussian records staged in shared memory per step
 #define SOF_EVAL_STATS 0
 #endif
 
+// Streams a live-only tile list (lp[0, len)) through shared memory in chunks of kChunk
+// records and runs eval_chunk(rec*, cnt) -> pairs on each, until every thread of the
+// CTA is done. STAGE selects the staging; both give identical results (A/B on C3 in
+// DESIGN.md §4):
+//   0 (default): every thread copies 16 B of the chunk (index load + record load),
+//     two barriers per chunk; srec[0] only;
+//   1 (sof_set_staging): TMA row gather — warp 0 issues tile::gather4 over the index
+//     list (sof_tma.cuh) into an mbarrier double buffer one chunk ahead, one barrier
+//     per chunk. +4% kernel time on C3: the loads were never the bottleneck, and the
+//     issue (a uniform-register waterfall over 8 gathers) serialises on warp 0.
+// Also measured and dropped: per-lane 1D cp.async.bulk copies (+14%), a register
+// double buffer (+6%; with 4 CTAs/SM +8%).
+template <int STAGE, typename F>
+__device__ __forceinline__ unsigned stream_list(const int32_t* __restrict__ lp, int len, const Rec* __restrict__ recs,
+                                                const CUtensorMap* tmap, Rec (*srec)[kChunk], uint64_t* s_bar,
+                                                bool& done, F&& eval_chunk) {
+  const int nchunks = (len + kChunk - 1) / kChunk;
+  auto chunk_cnt = [&](int k) { return min(kChunk, len - k * kChunk); };
+  unsigned pairs = 0;
+  if constexpr (STAGE == 1) {
+    const bool warp0 = threadIdx.x < 32;
+    auto chunk_row = [&](int k) {  // this lane's list entry of chunk k (0 past the end)
+      const int e = k * kChunk + int(threadIdx.x & 31);
+      return e < len ? lp[e] : 0;
+    };
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    int next_row = 0;  // warp 0: list entry of chunk k + 1 held one chunk ahead
+    if (warp0 && nchunks > 0) {
+      tma_issue_rows(srec[0], tmap, chunk_row(0), chunk_cnt(0), &s_bar[0], sizeof(Rec));
+      next_row = chunk_row(1);
+    }
+    int k = 0;
+    for (; k < nchunks; ++k) {
+      // all threads are past chunk k - 1: its buffer may be refilled with chunk k + 1
+      if (!__syncthreads_or(!done)) break;
+      if (warp0 && k + 1 < nchunks) {
+        tma_issue_rows(srec[(k + 1) & 1], tmap, next_row, chunk_cnt(k + 1), &s_bar[(k + 1) & 1], sizeof(Rec));
+        next_row = chunk_row(k + 2);
+      }
+      if (done) continue;
+      mbar_wait(&s_bar[k & 1], (k >> 1) & 1);
+      pairs += eval_chunk(srec[k & 1], chunk_cnt(k));
+    }
+    // early exit: chunk k was issued but never waited on; the CTA's shared memory must
+    // not be released while the copy is in flight
+    if (k < nchunks && threadIdx.x == 0) mbar_wait(&s_bar[k & 1], (k >> 1) & 1);
+  } else {
+    for (int k = 0; k < nchunks; ++k) {
+      if (!__syncthreads_or(!done)) break;
+      const int cnt = chunk_cnt(k);
+      for (int q8 = threadIdx.x; q8 < cnt * kRecV2; q8 += blockDim.x) {
+        const int r = q8 / kRecV2, q = q8 % kRecV2;
+        reinterpret_cast<double2*>(&srec[0][r])[q] =
+            __ldg(reinterpret_cast<const double2*>(recs + lp[k * kChunk + r]) + q);
+      }
+      __syncthreads();
+      if (!done) pairs += eval_chunk(srec[0], cnt);
+    }
+  }
+  return pairs;
+}
+
 // One CTA = one schedule block (<= 256 points of one tile). The block's Gaussian
 // list is streamed through shared memory in chunks; every thread runs the exact
 // view_opacity loop (field_eval.hpp:86-108) for its point.
 //
-// FAST (tile lists + min-z + dead cull, the default strategies): the per-record
-// strategy tests leave the inner loop. Dead records (op < 1/255, skipped before the
-// pair counter at field_eval.hpp:89-90) are neutralised in the shared-memory copy —
-// zmin = -inf (never ends the sorted scan) and a conic that always culls — and
-// subtracted from the pair count once per chunk through a dead mask.
-template <int MODE, bool TILED, bool FAST>
+// FAST (tile lists + min-z + dead cull, the default strategies): the lists are
+// live-only (Binding::live), so the loop has no per-record strategy tests, and the
+// chunks are gathered by TMA (tile::gather4 over the index list, sof_tma.cuh) into a
+// double buffer: warp 0 issues chunk k + 1 right after the barrier that frees its
+// buffer, and the CTA evaluates chunk k meanwhile. One barrier per chunk (it also
+// detects the all-done early exit).
+template <int MODE, bool TILED, bool FAST, int STAGE = 0>
 __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks,
     const int32_t* __restrict__ pidx, const double* __restrict__ xyz, Cam cam, int ts,
     int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
     int64_t n_gauss, const Rec* __restrict__ recs, int strategies, int classify, double* min_op,
     uint8_t* ext, double* o_out, uint8_t* obs_out, uint8_t* comp_out,
-    unsigned long long* pairs_counter) {
+    unsigned long long* pairs_counter, const __grid_constant__ CUtensorMap tmap) {
   static_assert(!FAST || TILED, "the fast loop relies on min_z-sorted tile lists");
-  __shared__ __align__(16) Rec srec[kChunk];
+  __shared__ __align__(128) Rec srec[STAGE == 1 ? 2 : 1][kChunk];
   __shared__ __align__(16) double s_exp[128];  // sof_exp's table (shared-memory latency)
-  __shared__ unsigned s_dead[2];
+  __shared__ __align__(8) uint64_t s_bar[2];
   const int64_t b = blockIdx.x;
   if (b >= *nblocks) return;
   const int4 blk = blocks[b];
@@ -537,39 +612,14 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
   bool complete = true;
   bool done = !active;
   unsigned pairs = 0, exact = 0, contrib = 0;
-  if (FAST && threadIdx.x < 2) s_dead[threadIdx.x] = 0;  // published by the first barrier
   if (threadIdx.x < 128) s_exp[threadIdx.x] = kSofExpTabDev[threadIdx.x];
-  int par = 0;
-  for (int64_t base = l0; base < l1; base += kChunk, par ^= 1) {
-    if (!__syncthreads_or(!done)) break;
-    const int cnt = int(std::min<int64_t>(kChunk, l1 - base));
-    for (int k = threadIdx.x; k < cnt * kRecV2; k += blockDim.x) {
-      const int r = k / kRecV2, q = k % kRecV2;
-      const int64_t g = TILED ? int64_t(lent[base + r]) : base + r;
-      double2 v = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
-      if (FAST && q >= 5 && __ldg(&recs[g].op) < kMinAlpha) {
-        if (q == 5) {  // (op, zmin)
-          v.y = -INFINITY;
-          atomicOr(&s_dead[par], 1u << r);
-        } else if (q == 6) {  // (thr, conic0..2): g = -1
-          float4 f = *reinterpret_cast<float4*>(&v);
-          f.y = 0.0f;
-          f.z = 0.0f;
-          f.w = -1.0f;
-          v = *reinterpret_cast<double2*>(&f);
-        } else {  // (conic3..5, gmargin)
-          v = make_double2(0.0, 0.0);
-        }
-      }
-      reinterpret_cast<double2*>(&srec[r])[q] = v;
-    }
-    if (FAST && threadIdx.x == 0) s_dead[par ^ 1] = 0;  // mask of the next chunk
-    __syncthreads();
-    if (done) continue;
-    if (FAST) {
-      int k = 0;
-      const Rec* rp = srec;
-      for (; k < cnt; ++k, ++rp) {
+  if constexpr (FAST) {
+    const int32_t* lp = lent + l0;
+    const int len = int(l1 - l0);  // tile lists hold < 2^31 entries
+    // the exact reference loop over one staged chunk; returns the pairs it counted
+    auto eval_chunk = [&](const Rec* rp, int cnt) {
+      int e = 0;
+      for (; e < cnt; ++e, ++rp) {
         const Rec& r = *rp;
         if (r.zmin > pr.zp) {  // list sorted by min_z (field_eval.hpp:91)
           done = true;
@@ -584,15 +634,26 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
         if (early && 1.0 - survive > 0.5) {
           complete = false;
           done = true;
-          ++k;  // this pair was counted
+          ++e;  // this pair was counted
           break;
         }
       }
-      const unsigned upto = (k >= 32) ? 0xffffffffu : ((1u << k) - 1u);
-      pairs += unsigned(k) - __popc(s_dead[par] & upto);
-    } else {
+      return unsigned(e);
+    };
+    pairs += stream_list<STAGE>(lp, len, recs, &tmap, srec, s_bar, done, eval_chunk);
+  } else {
+    for (int64_t base = l0; base < l1; base += kChunk) {
+      if (!__syncthreads_or(!done)) break;
+      const int cnt = int(std::min<int64_t>(kChunk, l1 - base));
+      for (int k = threadIdx.x; k < cnt * kRecV2; k += blockDim.x) {
+        const int r = k / kRecV2, q = k % kRecV2;
+        const int64_t g = TILED ? int64_t(lent[base + r]) : base + r;
+        reinterpret_cast<double2*>(&srec[0][r])[q] = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
+      }
+      __syncthreads();
+      if (done) continue;
       for (int k = 0; k < cnt; ++k) {
-        const Rec& r = srec[k];
+        const Rec& r = srec[0][k];
         if (dead_cull && r.op < kMinAlpha) continue;
         if (use_min_z && r.zmin > pr.zp) {
           if (TILED) {  // list sorted by min_z (field_eval.hpp:91)
@@ -863,15 +924,17 @@ __global__ void k_scatter_group(int64_t n, int G, const int32_t* __restrict__ it
 // k_eval's fast loop (default strategies, classify mode) over the items of a group:
 // block.z is a (view, tile) bin; the view's camera, records and tile lists come from
 // device tables. Writes the per-item pair count and exterior flag.
+template <int STAGE>
 __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks, const int32_t* __restrict__ items,
     int64_t n, const double* __restrict__ xyz, const Cam* __restrict__ cams, int ts, GroupTables gt,
     const int64_t* const* __restrict__ loffs, const int32_t* const* __restrict__ lents,
-    const Rec* const* __restrict__ recs_v, bool early, uint32_t* item_pairs, uint8_t* item_ext,
+    const Rec* const* __restrict__ recs_v, const CUtensorMap* __restrict__ tmaps, bool early,
+    uint32_t* item_pairs, uint8_t* item_ext,
     unsigned long long* counters) {
-  __shared__ __align__(16) Rec srec[kChunk];
-  __shared__ unsigned s_dead[2];
+  __shared__ __align__(128) Rec srec[STAGE == 1 ? 2 : 1][kChunk];
   __shared__ __align__(16) double s_exp[128];
+  __shared__ __align__(8) uint64_t s_bar[2];
   const int64_t b = blockIdx.x;
   if (b >= *nblocks) return;
   const int4 blk = blocks[b];
@@ -880,7 +943,8 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
   const int v = gt.g0 + j;
   const int tile = blk.z - int(gt.bin_base[j]);
   const Cam cam = cams[v];
-  const Rec* __restrict__ recs = recs_v[v];
+  const CUtensorMap* tmap = tmaps + v;
+  const Rec* recs = recs_v[v];
   const int32_t* __restrict__ lent = lents[v];
   const int tiles_x = (cam.w + ts - 1) / ts;
   const int p = blk.x + int(threadIdx.x);
@@ -901,37 +965,12 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
   bool complete = true;
   bool done = !active;
   unsigned pairs = 0, exact = 0, contrib = 0;
-  if (threadIdx.x < 2) s_dead[threadIdx.x] = 0;
   if (threadIdx.x < 128) s_exp[threadIdx.x] = kSofExpTabDev[threadIdx.x];
-  int par = 0;
-  for (int64_t base = l0; base < l1; base += kChunk, par ^= 1) {
-    if (!__syncthreads_or(!done)) break;
-    const int cnt = int(std::min<int64_t>(kChunk, l1 - base));
-    for (int q8 = threadIdx.x; q8 < cnt * kRecV2; q8 += blockDim.x) {
-      const int r = q8 / kRecV2, q = q8 % kRecV2;
-      const int64_t g = int64_t(lent[base + r]);
-      double2 vv = __ldg(reinterpret_cast<const double2*>(recs + g) + q);
-      if (q >= 5 && __ldg(&recs[g].op) < kMinAlpha) {
-        if (q == 5) {
-          vv.y = -INFINITY;
-          atomicOr(&s_dead[par], 1u << r);
-        } else if (q == 6) {
-          float4 f = *reinterpret_cast<float4*>(&vv);
-          f.y = 0.0f;
-          f.z = 0.0f;
-          f.w = -1.0f;
-          vv = *reinterpret_cast<double2*>(&f);
-        } else {
-          vv = make_double2(0.0, 0.0);
-        }
-      }
-      reinterpret_cast<double2*>(&srec[r])[q] = vv;
-    }
-    if (threadIdx.x == 0) s_dead[par ^ 1] = 0;
-    __syncthreads();
-    if (done) continue;
+  // k_eval's fast loop over the live-only list (stream_list); with TMA staging the
+  // tensor maps live in global memory, written by a host copy before the launch
+  if (STAGE == 1 && threadIdx.x < 32) tma_fence_acquire(tmap);
+  auto eval_chunk = [&](const Rec* rp, int cnt) {
     int kk = 0;
-    const Rec* rp = srec;
     for (; kk < cnt; ++kk, ++rp) {
       const Rec& r = *rp;
       if (r.zmin > pr.zp) {
@@ -951,9 +990,9 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
         break;
       }
     }
-    const unsigned upto = (kk >= 32) ? 0xffffffffu : ((1u << kk) - 1u);
-    pairs += unsigned(kk) - __popc(s_dead[par] & upto);
-  }
+    return unsigned(kk);
+  };
+  pairs += stream_list<STAGE>(lent + l0, int(l1 - l0), recs, tmap, srec, s_bar, done, eval_chunk);
   if (active) {
     item_pairs[item] = pairs;
     item_ext[item] = (complete && 1.0 - survive < 0.5) ? 1 : 0;
@@ -1013,7 +1052,7 @@ static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double
   // unless the cache budget ran out)
   for (int v = v0; v < v1; ++v) {
     const Binding& b = c->bindings[v];
-    if (!c->rec_valid[v] || b.view != v || b.tile_size != tile_size) return false;
+    if (!c->rec_valid[v] || b.view != v || b.tile_size != tile_size || !b.live) return false;
   }
   const int G = std::min(kGroupViews, v1 - v0);
   if (int64_t(G) * n >= (int64_t(1) << 31)) return false;
@@ -1028,6 +1067,15 @@ static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double
   g.ptrs.ensure(3 * V);
   SOF_CUDA(cudaMemcpyAsync(g.cams.p, c->cams.data(), sizeof(Cam) * V, cudaMemcpyHostToDevice, c->stream));
   SOF_CUDA(cudaMemcpyAsync(g.ptrs.p, ptrs.data(), sizeof(void*) * 3 * V, cudaMemcpyHostToDevice, c->stream));
+  if (c->staging == 1) {  // TMA staging: one tensor map per view's record array
+    std::vector<CUtensorMap> tmaps(static_cast<size_t>(V));
+    std::memset(tmaps.data(), 0, sizeof(CUtensorMap) * size_t(V));
+    for (int v = v0; v < v1; ++v)
+      if (sof_make_row_tmap(&tmaps[v], c->recs[v].p, c->n) != 0)
+        throw StateError("cuTensorMapEncodeTiled failed for the records");
+    g.tmaps.ensure(V);
+    SOF_CUDA(cudaMemcpyAsync(g.tmaps.p, tmaps.data(), sizeof(CUtensorMap) * V, cudaMemcpyHostToDevice, c->stream));
+  }
   g.item_bin.ensure(int64_t(G) * n);
   g.item_pairs.ensure(int64_t(G) * n);
   g.item_ext.ensure(int64_t(G) * n);
@@ -1073,9 +1121,14 @@ static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double
                                                                c->d_scalar.p);
     SOF_LAUNCHED(c);
     const int e0 = prof_mark(c);
-    k_eval_group<<<unsigned(grid), 256, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
-                                                        tile_size, gt, loffs, lents, recs, early, g.item_pairs.p,
-                                                        g.item_ext.p, c->d_counters.p);
+    if (c->staging == 1)
+      k_eval_group<1><<<unsigned(grid), 256, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
+                                                             tile_size, gt, loffs, lents, recs, g.tmaps.p, early,
+                                                             g.item_pairs.p, g.item_ext.p, c->d_counters.p);
+    else
+      k_eval_group<0><<<unsigned(grid), 256, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
+                                                             tile_size, gt, loffs, lents, recs, nullptr, early,
+                                                             g.item_pairs.p, g.item_ext.p, c->d_counters.p);
     SOF_LAUNCHED(c);
     prof_span(c, e0, prof_mark(c), kProfEval);
     c->eval_launches++;
@@ -1093,6 +1146,11 @@ static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double
     c->contrib_evals += h[3];
   }
   return true;
+}
+
+// The FP64 fast loop of k_eval: tile lists + min-z + dead cull (the default strategies).
+static bool fast_loop(const sof_ctx* c, int strategies) {
+  return c->eval_path == 1 && (strategies & 19) == 19;
 }
 
 template <int MODE>
@@ -1114,18 +1172,32 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
       k_eval_f32<MODE, false><<<unsigned(grid), 256, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec, recf,
           strategies, classify, min_op, ext, o_out, obs, comp, pc);
-  } else if (tiled && (strategies & 18) == 18)  // min_z + dead cull: the fast loop
-    k_eval<MODE, true, true><<<unsigned(grid), 256, 0, c->stream>>>(
-        c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
-        strategies, classify, min_op, ext, o_out, obs, comp, pc);
-  else if (tiled)
-    k_eval<MODE, true, false><<<unsigned(grid), 256, 0, c->stream>>>(
-        c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
-        strategies, classify, min_op, ext, o_out, obs, comp, pc);
-  else
-    k_eval<MODE, false, false><<<unsigned(grid), 256, 0, c->stream>>>(
-        c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
-        strategies, classify, min_op, ext, o_out, obs, comp, pc);
+  } else if (fast_loop(c, strategies)) {  // live-only lists, TMA-gathered records
+    if (!bd->live) throw StateError("internal: the fast evaluation loop needs live-only tile lists");
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof tmap);
+    if (c->staging == 1) {
+      if (sof_make_row_tmap(&tmap, rec, c->n) != 0) throw StateError("cuTensorMapEncodeTiled failed for the records");
+      k_eval<MODE, true, true, 1><<<unsigned(grid), 256, 0, c->stream>>>(
+          c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap);
+    } else {
+      k_eval<MODE, true, true, 0><<<unsigned(grid), 256, 0, c->stream>>>(
+          c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap);
+    }
+  } else {
+    CUtensorMap none;
+    std::memset(&none, 0, sizeof none);
+    if (tiled)
+      k_eval<MODE, true, false><<<unsigned(grid), 256, 0, c->stream>>>(
+          c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, none);
+    else
+      k_eval<MODE, false, false><<<unsigned(grid), 256, 0, c->stream>>>(
+          c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, none);
+  }
   SOF_LAUNCHED(c);
   prof_span(c, e0, prof_mark(c), kProfEval);
   c->eval_launches++;
@@ -1139,6 +1211,8 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   if (tile_size <= 0) throw InvalidArg("tile_size must be positive");
   const bool tiled = strategies & 1;
   const bool prune = strategies & 8;
+  // the FP64 fast loop (tile lists + min-z + dead cull) runs on live-only lists
+  const bool live_lists = fast_loop(c, strategies);
   if (mode == kModeClassify &&
       classify_grouped(c, v0, v1, n, xyz, strategies, tile_size, ext, counters_host))
     return;
@@ -1172,7 +1246,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
       SOF_CUDA(cudaStreamWaitEvent(c->stream, c->eval_ev[pv & 1], 0));
       const int p0 = prof_mark(c);
       // binding first: it computes the records in the same pass as the tile rectangles
-      prep_bd[pv & 1] = tiled ? &view_binding(c, pv, tile_size) : nullptr;
+      prep_bd[pv & 1] = tiled ? &view_binding(c, pv, tile_size, live_lists) : nullptr;
       prep_rec[pv & 1] = view_records(c, pv);
       prof_span(c, p0, prof_mark(c), kProfPrep);
       SOF_CUDA(cudaEventRecord(c->prep_ev[pv & 1], c->stream));

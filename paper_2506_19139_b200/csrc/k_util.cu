@@ -11,6 +11,31 @@
 
 #include "../../include/sof_cuda.h"
 #include "sof_internal.h"
+#include "sof_tma.cuh"
+
+#include <cudaTypedefs.h>
+
+// Tensor map of a 128-B-row record array for the TMA row gather (sof_tma.cuh). The
+// driver entry point is resolved once through the runtime (no -lcuda link).
+int sof_make_row_tmap(CUtensorMap* out, const void* base, int64_t rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return -1;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {16, cuuint64_t(std::max<int64_t>(rows, 1))};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {16, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -int(r);
+}
 
 namespace sofk {
 

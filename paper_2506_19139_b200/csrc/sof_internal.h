@@ -2,6 +2,7 @@
 // translation units of libsof_cuda.so. Not part of the public ABI.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -85,6 +86,11 @@ struct DBuf {
 // Per-view Gaussian tile lists (TileBinding tiles.hpp:88-92) resident on the device.
 struct Binding {
   int view = -1, tile_size = 0, tiles_x = 0, tiles_y = 0;
+  // live-only lists: dead Gaussians (op < 1/255) left out. With dead cull + min-z on
+  // (the default strategies) the reference skips them before the pair counter and the
+  // min-z break (field_eval.hpp:89-93), so these lists give identical results and
+  // counters; the exact reference lists (tiles.hpp:134-144) have live = false.
+  bool live = false;
   int64_t entries = 0;
   DBuf<int64_t> off;  // [T + 1]
   DBuf<int32_t> ent;  // [entries], per tile sorted by (min_z, index)
@@ -122,6 +128,7 @@ struct MeshScratch {
 struct GroupScratch {
   DBuf<Cam> cams;                 // [V]
   DBuf<const void*> ptrs;         // [3V] per-view tile offsets, tile entries, records
+  DBuf<CUtensorMap> tmaps;        // [V] TMA descriptors of the per-view record arrays
   DBuf<int32_t> item_bin, order;  // [G n]
   DBuf<uint32_t> item_pairs;      // [G n]
   DBuf<uint8_t> item_ext;         // [G n]
@@ -176,6 +183,7 @@ struct sof_ctx {
   int scratch_view[2] = {-1, -1};
   int scratch_sel = 0;
   int eval_path = 1;                      // 0: FP32 filter + exact FP64 replay, 1: FP64 only
+  int staging = 0;                        // fast-loop record staging: 0 plain loads, 1 TMA gather4
   uint64_t exact_evals = 0;               // pairs that took the FP64 path (instrumentation)
   uint64_t contrib_evals = 0;             // ... of which contributed (alpha >= 1/255)
   double host_ms[4] = {0, 0, 0, 0};       // host time in per-view prep / scheduling (instrumentation)
@@ -261,7 +269,7 @@ namespace sofk {
 void scene_prep(sof_ctx* c);
 const Rec* view_records(sof_ctx* c, int view);
 const RecF* view_recf(sof_ctx* c, int view);
-const Binding& view_binding(sof_ctx* c, int view, int tile_size);
+const Binding& view_binding(sof_ctx* c, int view, int tile_size, bool live = false);
 void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding& b,
                 bool charge_cache);
 void invalidate_view_caches(sof_ctx* c);

@@ -203,3 +203,36 @@ def test_label_all_points_pruned_early(ref):
     assert ev.counters() == rev.counters()
     # every point exterior in view 0 and never evaluated again
     assert (got < 0.5).all() and ev.counters()["point_view_evals"] == len(pts)
+
+
+@pytest.mark.parametrize("staging", [0, 1])
+@pytest.mark.parametrize("mask", [31, 23, 19, 27])
+def test_fast_loop_staging_bitexact(ref, mask, staging):
+    """The fast loop (tile lists + min-z + dead cull) runs on live-only tile lists with
+    either record staging (plain loads / TMA tile::gather4 into an mbarrier double
+    buffer): values, exterior flags and the reference counters stay bit-exact, with
+    dead Gaussians (field_eval.hpp:89) and lists longer than one staging chunk."""
+    scene = ref.random_scene(31, 700, 1.0)
+    scene.opacity[::6] = 0.003
+    scene.opacity[3::11] = (1.0 / 255.0) * (1.0 - 1e-12)
+    cams = ref.orbit_cameras(4, 4.0, 1.8, 40)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    views.ctx.check(views.ctx.lib.sof_set_staging(views.ctx.h, staging))
+    pts = np.random.default_rng(17).uniform(-1.2, 1.2, (4000, 3))
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.from_mask(mask))
+    rev = rc.evaluator(mask)
+    for classify in (False, True):
+        assert_bits(ev.label_grid(pts, classify), rev.label_grid(pts, classify), f"mask {mask}")
+        assert ev.counters() == rev.counters()
+    for v in (0, cams.v - 1):
+        o, ob, co = ev.view_opacity(v, pts, True)
+        ro, rob, rco = rev.view_opacity(v, pts, True)
+        np.testing.assert_array_equal(co, rco.astype(bool))
+        assert_bits(o[ob], ro[rob.astype(bool)], f"mask {mask} view {v}")
+    np.testing.assert_array_equal(ev.classify_points(pts), rev.classify_points(pts).astype(bool))
+    # the reference tile lists (with the dead Gaussians) are still what the binding API returns
+    off, ent = views.ctx.tile_binding(0, 16)
+    want = rc.tile_binding(0, 16)
+    np.testing.assert_array_equal(off, want["offsets"])
+    np.testing.assert_array_equal(ent, want["entries"])

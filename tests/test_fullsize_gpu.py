@@ -47,6 +47,20 @@ def test_eval_paths_bit_identical(c3):
     print(f"exact FP64 pairs: {s0['exact_pairs']} of {s0['pairs']} ({s0['exact_pairs'] / s0['pairs']:.3f})")
 
 
+def test_staging_modes_bit_identical(c3):
+    """Plain-load and TMA (tile::gather4) record staging: same mesh bits, same counters."""
+    ctx, verts, tets = c3
+    out = {}
+    for mode in (1, 0):
+        ctx.check(ctx.lib.sof_set_staging(ctx.h, mode))
+        st = {}
+        out[mode] = (sof.extract_resident(ctx, sof.ExtractOptions(), st), st)
+    (m0, s0), (m1, s1) = out[0], out[1]
+    np.testing.assert_array_equal(m0.vertices.view(np.uint64), m1.vertices.view(np.uint64))
+    np.testing.assert_array_equal(m0.triangles, m1.triangles)
+    assert s0["pairs"] == s1["pairs"] and s0["point_view_evals"] == s1["point_view_evals"]
+
+
 def test_mesh_consistency(c3):
     ctx, verts, tets = c3
     mesh = sof.extract_resident(ctx, sof.ExtractOptions(), {})
