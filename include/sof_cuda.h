@@ -200,6 +200,20 @@ int sof_shard_finalize_dev(sof_ctx* ctx, int64_t n, const double* min_opacity_de
                            const int32_t* first_ext_rank_dev, int world);
 /* marching_tets over the resident tets and grid opacity (results stay resident) */
 int sof_march_resident(sof_ctx* ctx, int64_t* n_edges, int64_t* n_tris);
+/* Tet-sharded march (one shard of marching_tets, marching_tets.hpp:29-84): the
+ * resident labels marched over the tet range [t0, t1) only; edges are numbered in
+ * first appearance within the range and the triangles reference them. */
+int sof_march_range_resident(sof_ctx* ctx, int64_t t0, int64_t t1, int64_t* n_edges, int64_t* n_tris);
+/* Copies the current march result into caller device buffers: edges [2E] (inside,
+ * outside vertex id), triangles [3T] (edge ids). */
+int sof_march_result_copy_dev(sof_ctx* ctx, int32_t* edges_dst, int32_t* tris_dst);
+/* Merge of `world` shard results gathered on this device in shard order (shard r =
+ * the r-th contiguous tet range): edges_dev = the shards' edge lists concatenated,
+ * tris_dev = their triangles (shard-local edge ids) concatenated. Produces the
+ * whole-grid marching_tets result (same edge numbering, triangles and winding) as
+ * the resident march result. */
+int sof_march_merge_dev(sof_ctx* ctx, int world, const int64_t* edge_counts, const int32_t* edges_dev,
+                        const int64_t* tri_counts, const int32_t* tris_dev, int64_t* n_edges, int64_t* n_tris);
 /* one phase of binary_search_refine over the resident crossing edges:
  * 0 init brackets, 1 midpoints + classify against views [v0, v1) into exterior_dev
  * (cleared first), 2 update brackets from exterior_dev, 3 write the final vertices */

@@ -96,6 +96,9 @@ _SIGS = {
     "sof_shard_mask_min_dev": (_I, [_P, _I64, _P, _I, _P]),
     "sof_shard_finalize_dev": (_I, [_P, _I64, _P, _P, _I]),
     "sof_march_resident": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "sof_march_range_resident": (_I, [_P, _I64, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "sof_march_result_copy_dev": (_I, [_P, _P, _P]),
+    "sof_march_merge_dev": (_I, [_P, _I, _P, _P, _P, _P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "sof_refine_phase_dev": (_I, [_P, _I, _P, _I, _I, _I, _I, _P]),
     "sof_assemble_resident": (_I, [_P, _D, _D, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
 }

@@ -172,6 +172,7 @@ class Context:
         self.scene: GaussianScene | None = None
         self.cams: CameraSet | None = None
         self.nv = 0
+        self.n_tets = 0
 
     def close(self):
         if getattr(self, "h", None):
@@ -234,6 +235,7 @@ class Context:
         self.check(fn(self.h, len(v), _ptr(v), len(t), _ptr(t)))
         self._tets_keepalive = t if async_copy else None
         self.nv = len(v)
+        self.n_tets = len(t)
 
     def result(self, kind: int, dtype, width: int):
         n = int(self.lib.sof_result_count(self.h, kind))

@@ -201,61 +201,47 @@ __global__ void k_tris(int64_t ntri, const int32_t* __restrict__ tri_occ,
   tris[3 * k + 2] = keep ? e2 : e1;
 }
 
-void march(sof_ctx* c, const double* opa) {
-  tets_ready(c);
-  if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
-  const int64_t nt = c->nt, nv = c->nv;
+// ---- tet-sharded march: merge of per-shard results ------------------------------------------------
+
+constexpr int kMaxShards = 64;
+struct ShardOffsets {
+  int world;
+  int64_t edge_off[kMaxShards + 1];  // first gathered edge of each shard
+  int64_t tri_off[kMaxShards + 1];   // first gathered triangle of each shard
+};
+
+// occurrences = the shards' edge lists concatenated in shard (= tet) order
+__global__ void k_shard_occ(int64_t m, int64_t nv, const int32_t* __restrict__ edges, uint64_t* key,
+                            int32_t* pos, int32_t* in, int32_t* out) {
+  const int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (q >= m) return;
+  const int32_t a = edges[2 * q], b = edges[2 * q + 1];
+  key[q] = uint64_t(a) * uint64_t(nv) + uint64_t(b);
+  pos[q] = int32_t(q);
+  in[q] = a;
+  out[q] = b;
+}
+
+// shard-local edge ids of the gathered triangles -> global ids (winding was decided
+// per shard with the same lerp vertices)
+__global__ void k_remap_tris(int64_t ntri, ShardOffsets so, const int32_t* __restrict__ tris_in,
+                             const int32_t* __restrict__ occ_edge, int32_t* tris) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= ntri) return;
+  int r = 0;
+  while (r + 1 < so.world && so.tri_off[r + 1] <= k) ++r;
+  const int64_t eb = so.edge_off[r];
+  for (int q = 0; q < 3; ++q) tris[3 * k + q] = occ_edge[eb + tris_in[3 * k + q]];
+}
+
+// Edge numbering in order of first appearance (marching_tets.hpp:31-44) for the m
+// occurrences in ms.okey / opos / oin / oout (positions = appearance order): a stable
+// key sort puts each edge's first occurrence at its run head; an exclusive scan over
+// first-occurrence flags numbers the edges. Fills r_edges, r_everts (the lerp vertex,
+// :38-41) and ms.occ_edge (edge id of every occurrence); returns the edge count.
+static int64_t number_edges(sof_ctx* c, const double* opa, int64_t m) {
+  const int64_t nv = c->nv;
   MeshScratch& s = c->ms;
-  c->n_edges = c->n_march_tris = 0;
-  c->r_edges.ensure(2);
-  c->r_everts.ensure(3);
-  c->r_tris.ensure(3);
-  if (nt == 0) return;
-  s.crossing.ensure(nt);
-  k_tet_case<<<grid_for(nt, 256), 256, 0, c->stream>>>(nt, c->tt.p, opa, s.crossing.p);
-  SOF_LAUNCHED(c);
-  // compact the crossing tets, keeping tet order
-  s.ctets.ensure(nt);
-  s.nsel.ensure(1);
-  {
-    thrust::counting_iterator<int32_t> it(0);
-    size_t bytes = 0;
-    SOF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, s.crossing.p, s.ctets.p, s.nsel.p, nt,
-                                        c->stream));
-    c->cub_tmp.ensure(bytes);
-    SOF_CUDA(cub::DeviceSelect::Flagged(c->cub_tmp.p, bytes, it, s.crossing.p, s.ctets.p,
-                                        s.nsel.p, nt, c->stream));
-    c->launches += 2;
-  }
-  const int64_t nc = read_scalar(c, s.nsel.p);
-  if (nc == 0) return;
-  s.packed.ensure(nc + 1);
-  s.off.ensure(nc + 1);
-  k_tet_counts<<<grid_for(nc + 1, 256), 256, 0, c->stream>>>(nc, s.ctets.p, c->tt.p, opa,
-                                                              s.packed.p);
-  SOF_LAUNCHED(c);
-  {
-    size_t bytes = 0;
-    SOF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, s.packed.p, s.off.p, nc + 1, c->stream));
-    c->cub_tmp.ensure(bytes);
-    SOF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, bytes, s.packed.p, s.off.p, nc + 1,
-                                           c->stream));
-    c->launches += 2;
-  }
-  const unsigned long long tot = read_scalar(c, s.off.p + nc);
-  const int64_t m = int64_t(tot & 0xffffffffull), ntri = int64_t(tot >> 32);
-  s.okey.ensure(m);
-  s.skey.ensure(m);
-  s.opos.ensure(m);
-  s.spos.ensure(m);
-  s.oin.ensure(m);
-  s.oout.ensure(m);
-  s.tri_occ.ensure(3 * ntri);
-  s.tri_tet.ensure(ntri);
-  k_tet_emit<<<grid_for(nc, 128), 128, 0, c->stream>>>(nc, nv, s.ctets.p, c->tt.p, opa, s.off.p,
-                                                        s.okey.p, s.opos.p, s.oin.p, s.oout.p,
-                                                        s.tri_occ.p, s.tri_tet.p);
-  SOF_LAUNCHED(c);
   const int kbits = bits_for(uint64_t(nv) * uint64_t(nv));
   sort_pairs_u64(c, s.okey.p, s.skey.p, s.opos.p, s.spos.p, m, kbits);
   s.head.ensure(m);
@@ -279,7 +265,6 @@ void march(sof_ctx* c, const double* opa) {
   s.run_eid.ensure(E);
   c->r_edges.ensure(2 * E);
   c->r_everts.ensure(3 * E);
-  c->r_tris.ensure(3 * ntri);
   k_edges<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.is_first.p, s.eid.p, s.oin.p, s.oout.p, opa,
                                                     c->tv.p, c->r_edges.p, c->r_everts.p);
   SOF_LAUNCHED(c);
@@ -289,10 +274,122 @@ void march(sof_ctx* c, const double* opa) {
   k_occ_edge2<<<grid_for(m, 256), 256, 0, c->stream>>>(m, s.run_incl.p, s.head.p, s.spos.p,
                                                         s.run_eid.p, s.occ_edge.p);
   SOF_LAUNCHED(c);
+  return E;
+}
+
+void march(sof_ctx* c, const double* opa) {
+  tets_ready(c);
+  if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
+  march_range(c, opa, 0, c->nt);
+}
+
+// marching_tets over the tet range [t0, t1): edges numbered in first appearance within
+// the range, triangles referencing them (a shard of the tet-sharded march; the whole
+// range is the reference's marching_tets).
+void march_range(sof_ctx* c, const double* opa, int64_t t0, int64_t t1) {
+  tets_ready(c);
+  if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
+  if (t0 < 0 || t1 > c->nt || t0 > t1) throw InvalidArg("tet range out of bounds");
+  const int64_t nt = t1 - t0, nv = c->nv;
+  const int32_t* tets = c->tt.p + 4 * t0;
+  MeshScratch& s = c->ms;
+  c->n_edges = c->n_march_tris = 0;
+  c->r_edges.ensure(2);
+  c->r_everts.ensure(3);
+  c->r_tris.ensure(3);
+  if (nt == 0) return;
+  s.crossing.ensure(nt);
+  k_tet_case<<<grid_for(nt, 256), 256, 0, c->stream>>>(nt, tets, opa, s.crossing.p);
+  SOF_LAUNCHED(c);
+  // compact the crossing tets, keeping tet order
+  s.ctets.ensure(nt);
+  s.nsel.ensure(1);
+  {
+    thrust::counting_iterator<int32_t> it(0);
+    size_t bytes = 0;
+    SOF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, s.crossing.p, s.ctets.p, s.nsel.p, nt,
+                                        c->stream));
+    c->cub_tmp.ensure(bytes);
+    SOF_CUDA(cub::DeviceSelect::Flagged(c->cub_tmp.p, bytes, it, s.crossing.p, s.ctets.p,
+                                        s.nsel.p, nt, c->stream));
+    c->launches += 2;
+  }
+  const int64_t nc = read_scalar(c, s.nsel.p);
+  if (nc == 0) return;
+  s.packed.ensure(nc + 1);
+  s.off.ensure(nc + 1);
+  k_tet_counts<<<grid_for(nc + 1, 256), 256, 0, c->stream>>>(nc, s.ctets.p, tets, opa,
+                                                              s.packed.p);
+  SOF_LAUNCHED(c);
+  {
+    size_t bytes = 0;
+    SOF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, s.packed.p, s.off.p, nc + 1, c->stream));
+    c->cub_tmp.ensure(bytes);
+    SOF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, bytes, s.packed.p, s.off.p, nc + 1,
+                                           c->stream));
+    c->launches += 2;
+  }
+  const unsigned long long tot = read_scalar(c, s.off.p + nc);
+  const int64_t m = int64_t(tot & 0xffffffffull), ntri = int64_t(tot >> 32);
+  s.okey.ensure(m);
+  s.skey.ensure(m);
+  s.opos.ensure(m);
+  s.spos.ensure(m);
+  s.oin.ensure(m);
+  s.oout.ensure(m);
+  s.tri_occ.ensure(3 * ntri);
+  s.tri_tet.ensure(ntri);
+  k_tet_emit<<<grid_for(nc, 128), 128, 0, c->stream>>>(nc, nv, s.ctets.p, tets, opa, s.off.p,
+                                                        s.okey.p, s.opos.p, s.oin.p, s.oout.p,
+                                                        s.tri_occ.p, s.tri_tet.p);
+  SOF_LAUNCHED(c);
+  const int64_t E = number_edges(c, opa, m);
+  c->r_tris.ensure(3 * ntri);
   k_tris<<<grid_for(ntri, 256), 256, 0, c->stream>>>(ntri, s.tri_occ.p, s.tri_tet.p, s.occ_edge.p,
-                                                      c->tt.p, opa, c->tv.p, c->r_everts.p,
+                                                      tets, opa, c->tv.p, c->r_everts.p,
                                                       c->r_tris.p);
   SOF_LAUNCHED(c);
+  c->n_edges = E;
+  c->n_march_tris = ntri;
+}
+
+// Merge of a tet-sharded march (shard r ran march_range over the r-th contiguous tet
+// range): every edge's global first appearance lies in the first shard that contains
+// it, so the global numbering is the first-appearance numbering of the shards' edge
+// lists concatenated in shard order; triangles keep their shard's winding.
+void march_merge(sof_ctx* c, const double* opa, int world, const int64_t* ecount, const int32_t* edges_all,
+                 const int64_t* tcount, const int32_t* tris_all) {
+  if (world < 1 || world > kMaxShards) throw InvalidArg("shard count out of range");
+  if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
+  ShardOffsets so;
+  so.world = world;
+  so.edge_off[0] = so.tri_off[0] = 0;
+  for (int r = 0; r < world; ++r) {
+    if (ecount[r] < 0 || tcount[r] < 0) throw InvalidArg("negative shard count");
+    so.edge_off[r + 1] = so.edge_off[r] + ecount[r];
+    so.tri_off[r + 1] = so.tri_off[r] + tcount[r];
+  }
+  const int64_t m = so.edge_off[world], ntri = so.tri_off[world];
+  MeshScratch& s = c->ms;
+  c->n_edges = c->n_march_tris = 0;
+  c->r_edges.ensure(2);
+  c->r_everts.ensure(3);
+  c->r_tris.ensure(3);
+  if (m == 0) return;
+  s.okey.ensure(m);
+  s.skey.ensure(m);
+  s.opos.ensure(m);
+  s.spos.ensure(m);
+  s.oin.ensure(m);
+  s.oout.ensure(m);
+  k_shard_occ<<<grid_for(m, 256), 256, 0, c->stream>>>(m, c->nv, edges_all, s.okey.p, s.opos.p, s.oin.p, s.oout.p);
+  SOF_LAUNCHED(c);
+  const int64_t E = number_edges(c, opa, m);
+  c->r_tris.ensure(std::max<int64_t>(3 * ntri, 3));
+  if (ntri > 0) {
+    k_remap_tris<<<grid_for(ntri, 256), 256, 0, c->stream>>>(ntri, so, tris_all, s.occ_edge.p, c->r_tris.p);
+    SOF_LAUNCHED(c);
+  }
   c->n_edges = E;
   c->n_march_tris = ntri;
 }

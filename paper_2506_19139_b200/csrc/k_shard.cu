@@ -113,6 +113,39 @@ int sof_march_resident(sof_ctx* c, int64_t* n_edges, int64_t* n_tris) {
   });
 }
 
+int sof_march_range_resident(sof_ctx* c, int64_t t0, int64_t t1, int64_t* n_edges, int64_t* n_tris) {
+  return guarded(c, [&] {
+    if (!c->has_tets || c->grid_n != c->nv) throw StateError("no label result for the resident tets");
+    march_range(c, c->grid_opacity.p, t0, t1);
+    if (n_edges) *n_edges = c->n_edges;
+    if (n_tris) *n_tris = c->n_march_tris;
+  });
+}
+
+int sof_march_result_copy_dev(sof_ctx* c, int32_t* edges_dst, int32_t* tris_dst) {
+  return guarded(c, [&] {
+    if (c->n_edges < 0) throw StateError("no marching result");
+    if (edges_dst && c->n_edges > 0)
+      SOF_CUDA(cudaMemcpyAsync(edges_dst, c->r_edges.p, sizeof(int32_t) * 2 * c->n_edges, cudaMemcpyDeviceToDevice,
+                               c->stream));
+    if (tris_dst && c->n_march_tris > 0)
+      SOF_CUDA(cudaMemcpyAsync(tris_dst, c->r_tris.p, sizeof(int32_t) * 3 * c->n_march_tris,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int sof_march_merge_dev(sof_ctx* c, int world, const int64_t* edge_counts, const int32_t* edges_dev,
+                        const int64_t* tri_counts, const int32_t* tris_dev, int64_t* n_edges, int64_t* n_tris) {
+  return guarded(c, [&] {
+    if (!edge_counts || !tri_counts) throw InvalidArg("null shard counts");
+    if (!c->has_tets || c->grid_n != c->nv) throw StateError("no label result for the resident tets");
+    march_merge(c, c->grid_opacity.p, world, edge_counts, edges_dev, tri_counts, tris_dev);
+    if (n_edges) *n_edges = c->n_edges;
+    if (n_tris) *n_tris = c->n_march_tris;
+  });
+}
+
 int sof_refine_phase_dev(sof_ctx* c, int phase, uint8_t* ext_dev, int v0, int v1, int strategies,
                          int tile_size, uint64_t* counters) {
   return guarded(c, [&] {

@@ -293,6 +293,9 @@ void pump_upload(sof_ctx* c, int64_t max_bytes);
 constexpr int64_t kUploadChunk = int64_t(64) << 20;
 void check_tet_indices(sof_ctx* c, cudaStream_t st, int64_t nt, const int32_t* tets_dev, int64_t nv, int32_t* bad);
 void march(sof_ctx* c, const double* opacity_dev);
+void march_range(sof_ctx* c, const double* opacity_dev, int64_t t0, int64_t t1);
+void march_merge(sof_ctx* c, const double* opacity_dev, int world, const int64_t* ecount, const int32_t* edges_all,
+                 const int64_t* tcount, const int32_t* tris_all);
 void refine(sof_ctx* c, int64_t ne, const int32_t* edges_dev, double* verts_dev, int iterations,
             int strategies, int tile_size, int v0, int v1, uint64_t* counters);
 void refine_init(sof_ctx* c, int64_t ne, const int32_t* edges_dev);

@@ -14,8 +14,13 @@ crosses ranks. Two exchange points reproduce the sequential results exactly:
   rank classifies all midpoints against its views, an all-reduce MAX merges the
   exterior flags, and every rank updates the brackets identically.
 
-Marching Tetrahedra and the weld are replicated (each rank holds the merged labels;
-they are a few milliseconds). The backend performs the per-rank device work
+* Marching Tetrahedra — the tets are split into contiguous ranges: each rank marches
+  its range (edges numbered by first appearance within it), the edge and triangle
+  lists are all-gathered in rank order, and every rank merges them: an edge's global
+  first appearance lies in the first range that contains it, so the global numbering
+  is the first-appearance numbering of the concatenated lists (marching_tets.hpp:31-44).
+
+The bisection brackets and the weld are replicated (each rank holds the merged march). The backend performs the per-rank device work
 (GpuBackend: libsof_cuda.so on CUDA tensors; tests/test_sharded_cpu.py supplies a
 CPU backend to exercise the same protocol over gloo).
 """
@@ -80,6 +85,29 @@ class GpuBackend:
         self.ctx.check(self.ctx.lib.sof_march_resident(self.ctx.h, ctypes.byref(ne), ctypes.byref(nt)))
         return ne.value, nt.value
 
+    def march_range(self, t0, t1):
+        ne, nt = ctypes.c_int64(), ctypes.c_int64()
+        self.ctx.check(self.ctx.lib.sof_march_range_resident(self.ctx.h, t0, t1, ctypes.byref(ne), ctypes.byref(nt)))
+        return ne.value, nt.value
+
+    def march_local(self, ne, nt):
+        """This shard's march result as flat int32 tensors: edges [2 ne], triangles [3 nt]."""
+        t = self.torch
+        edges = t.empty(max(2 * ne, 1), dtype=t.int32, device=self.dev)
+        tris = t.empty(max(3 * nt, 1), dtype=t.int32, device=self.dev)
+        self.ctx.check(self.ctx.lib.sof_march_result_copy_dev(self.ctx.h, self._p(edges), self._p(tris)))
+        return edges[: 2 * ne], tris[: 3 * nt]
+
+    def march_merge(self, edge_counts, edges_all, tri_counts, tris_all):
+        ec, tc = np.asarray(edge_counts, np.int64), np.asarray(tri_counts, np.int64)
+        ne, nt = ctypes.c_int64(), ctypes.c_int64()
+        edges_all, tris_all = edges_all.contiguous(), tris_all.contiguous()
+        self.ctx.check(self.ctx.lib.sof_march_merge_dev(
+            self.ctx.h, len(ec), ec.ctypes.data_as(ctypes.c_void_p), self._p(edges_all),
+            tc.ctypes.data_as(ctypes.c_void_p), self._p(tris_all), ctypes.byref(ne), ctypes.byref(nt)))
+        self.sync()
+        return ne.value, nt.value
+
     def refine_phase(self, phase, ext, v0, v1, strategies, tile_size):
         self.ctx.check(self.ctx.lib.sof_refine_phase_dev(
             self.ctx.h, phase, self._p(ext) if ext is not None else None, v0, v1, strategies, tile_size,
@@ -98,7 +126,8 @@ class GpuBackend:
 class ShardedMesher:
     """label -> march -> 8-step bisection -> weld with views sharded across ranks."""
 
-    def __init__(self, backend_or_ctx, rank: int, world: int, n_views: int | None = None, group=None):
+    def __init__(self, backend_or_ctx, rank: int, world: int, n_views: int | None = None, group=None,
+                 n_tets: int | None = None, shard_tets: bool = True):
         import torch.distributed as dist
         self.dist = dist
         self.b = GpuBackend(backend_or_ctx) if isinstance(backend_or_ctx, Context) else backend_or_ctx
@@ -106,11 +135,44 @@ class ShardedMesher:
         if n_views is None:
             n_views = backend_or_ctx.cams.v
         self.n_views = n_views
+        if n_tets is None:
+            n_tets = backend_or_ctx.n_tets if isinstance(backend_or_ctx, Context) else backend_or_ctx.n_tets
+        self.n_tets, self.shard_tets = n_tets, shard_tets
 
     def _allreduce(self, t, op):
         if self.world > 1:
             self.dist.all_reduce(t, op=op, group=self.group)
             self.b.sync()  # the library runs on its own stream
+
+    def _allgather_v(self, t, n):
+        """All ranks' first n entries of the 1-D tensor t, concatenated in rank order,
+        and the per-rank counts (collectives have no gatherv: pad to the largest)."""
+        import torch
+        dist = self.dist
+        cnt = torch.tensor([n], dtype=torch.int64, device=t.device)
+        cnts = [torch.zeros_like(cnt) for _ in range(self.world)]
+        dist.all_gather(cnts, cnt, group=self.group)
+        counts = [int(x.item()) for x in cnts]
+        buf = torch.zeros(max(max(counts), 1), dtype=t.dtype, device=t.device)
+        buf[:n] = t[:n]
+        outs = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(outs, buf, group=self.group)
+        self.b.sync()
+        return torch.cat([o[:k] for o, k in zip(outs, counts)]), counts
+
+    def _march(self, n_tets: int):
+        """Marching Tetrahedra with the tets split across ranks: rank r marches the r-th
+        contiguous tet range, the edge and triangle lists are gathered in rank (= tet)
+        order, and every rank merges them into the whole-grid numbering
+        (sof_march_merge_dev); identical to a single-rank march."""
+        if self.world == 1 or not self.shard_tets:
+            return self.b.march()
+        t0, t1 = view_range(self.rank, self.world, n_tets)
+        ne, nt = self.b.march_range(t0, t1)
+        edges, tris = self.b.march_local(ne, nt)
+        edges_all, ecnt = self._allgather_v(edges, 2 * ne)
+        tris_all, tcnt = self._allgather_v(tris, 3 * nt)
+        return self.b.march_merge([k // 2 for k in ecnt], edges_all, [k // 3 for k in tcnt], tris_all)
 
     def extract(self, opt: ExtractOptions | None = None, stats: dict | None = None, fetch: bool = True):
         opt = opt or ExtractOptions()
@@ -133,7 +195,7 @@ class ShardedMesher:
             rstar = b.ext_rank(ext, 0, self.world)
         b.finalize(min_op, rstar, self.world)
         label_counters = b.counters.copy()
-        ne, ntri = b.march()
+        ne, ntri = self._march(self.n_tets)
         if opt.refine_iterations > 0 and ne > 0:
             ext_e = b.zeros_u8(ne)
             b.refine_phase(0, None, v0, v1, strategies, opt.tile_size)

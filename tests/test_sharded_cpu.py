@@ -29,7 +29,7 @@ class OracleBackend:
 
     def __init__(self, scene, cams, verts, tets):
         self.scene, self.cams, self.verts, self.tets = scene, cams, verts, tets
-        self.nv = len(verts)
+        self.nv, self.n_tets = len(verts), len(tets)
         self.counters = np.zeros(2, np.uint64)
 
     def sync(self):
@@ -63,6 +63,36 @@ class OracleBackend:
         self.m = R.marching_tets(self.verts, self.tets, self.opacity)
         return len(self.m["edges"]), len(self.m["triangles"])
 
+    def march_range(self, t0, t1):
+        self.m = R.marching_tets(self.verts, self.tets[t0:t1], self.opacity)
+        return len(self.m["edges"]), len(self.m["triangles"])
+
+    def march_local(self, ne, nt):
+        return (torch.from_numpy(self.m["edges"].reshape(-1).copy()),
+                torch.from_numpy(self.m["triangles"].reshape(-1).copy()))
+
+    def march_merge(self, edge_counts, edges_all, tri_counts, tris_all):
+        """Restated merge: first-appearance numbering of the concatenated shard edge
+        lists, lerp vertices (marching_tets.hpp:38-41), shard-local -> global ids."""
+        e = edges_all.numpy().reshape(-1, 2).astype(np.int64)
+        key = e[:, 0] * self.nv + e[:, 1]
+        _, first, inv = np.unique(key, return_index=True, return_inverse=True)
+        order = np.argsort(first, kind="stable")  # unique keys by first appearance
+        gid_of_unique = np.empty_like(order)
+        gid_of_unique[order] = np.arange(len(order))
+        occ_gid = gid_of_unique[inv]
+        edges = e[first[order]].astype(np.int32)
+        o = self.opacity
+        oi, oo = o[edges[:, 0]], o[edges[:, 1]]
+        s = (0.5 - oi) / (oo - oi)
+        pi, po = self.verts[edges[:, 0]], self.verts[edges[:, 1]]
+        verts = pi + s[:, None] * (po - pi)
+        t = tris_all.numpy().reshape(-1, 3)
+        base = np.repeat(np.concatenate([[0], np.cumsum(edge_counts)[:-1]]), tri_counts)
+        tris = occ_gid[t + base[:, None]].astype(np.int32)
+        self.m = {"edges": edges, "vertices": verts, "triangles": tris}
+        return len(edges), len(tris)
+
     def refine_phase(self, phase, ext, v0, v1, strategies, tile_size):
         e = self.m["edges"]
         if phase == 0:
@@ -95,12 +125,13 @@ def _inputs():
     return scene, cams, verts, tets
 
 
-def _worker(rank, world, port, strategies, out):
+def _worker(rank, world, port, strategies, out, shard_tets=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         scene, cams, verts, tets = _inputs()
-        mesher = ShardedMesher(OracleBackend(scene, cams, verts, tets), rank, world, n_views=cams.v)
+        mesher = ShardedMesher(OracleBackend(scene, cams, verts, tets), rank, world, n_views=cams.v,
+                               shard_tets=shard_tets)
         stats = {}
         mesh = mesher.extract(ExtractOptions(strategies=EvalStrategies.from_mask(strategies)), stats)
         out[rank] = (mesh.vertices.copy(), mesh.triangles.copy(), stats)
@@ -114,14 +145,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,strategies", [(2, 31), (3, 31), (2, 23), (2, 0)])
-def test_sharded_extract_matches_sequential(world, strategies):
+@pytest.mark.parametrize("world,strategies,shard_tets", [(2, 31, True), (3, 31, True), (2, 23, True),
+                                                         (2, 0, True), (2, 31, False), (5, 31, True)])
+def test_sharded_extract_matches_sequential(world, strategies, shard_tets):
     scene, cams, verts, tets = _inputs()
     want = R.extract_tetgrid(scene, cams, verts, tets, strategies=strategies, iterations=8)
     assert len(want["triangles"]) > 0
     with mp.Manager() as mgr:
         out = mgr.dict()
-        mp.spawn(_worker, args=(world, _free_port(), strategies, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), strategies, out, shard_tets), nprocs=world, join=True)
         res = dict(out)
     for r in range(world):
         v, t, st = res[r]
