@@ -321,21 +321,117 @@ static void build_binding(sof_ctx* c, int view, int ts, bool live, Binding& b, b
   bin_by_key(c, view, ts, tiles_x, tiles_y, b, charge);
 }
 
-// Second half of a binning: Gaussians sorted by (zkey_in, index) — a stable radix
-// sort keeps index order on ties — emit (tile, gaussian) entries in that order, and a
-// stable sort by tile gives per-tile lists ordered by (key, index). Inputs: c->rect,
-// c->gcount[n + 1] (0 sentinel), c->zkey_in, c->gidx_in filled by a rect kernel.
+__global__ void k_gather_keys(int64_t n, const int32_t* __restrict__ perm, const uint64_t* __restrict__ src,
+                              uint64_t* dst) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j < n) dst[j] = src[perm[j]];
+}
+
+struct HasTiles {
+  const uint32_t* cnt;
+  __device__ bool operator()(int32_t i) const { return cnt[i] != 0; }
+};
+
+// 32-bit order key of a sort key: the double behind the 64-bit key rounded toward
+// -inf to float (monotone, so x < y implies f(x) <= f(y)), -0 folded onto +0.
+__global__ void k_float_keys(int64_t m, const int32_t* __restrict__ idx, const uint64_t* __restrict__ zkey,
+                             uint32_t* fkey) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  float f = __double2float_rd(key_double(zkey[idx[j]]));
+  if (f == 0.0f) f = 0.0f;
+  const uint32_t u = __float_as_uint(f);
+  fkey[j] = (u >> 31) ? ~u : (u | 0x80000000u);
+}
+
+// Runs of equal float keys (in index order after the stable sort) are re-sorted by the
+// full 64-bit key, index breaking ties: the result is the (key, index) order. A run
+// longer than kTieRun sets *overflow (the caller then sorts by the 64-bit keys).
+constexpr int kTieRun = 32;
+__global__ void k_fix_ties(int64_t m, const uint32_t* __restrict__ fk, int32_t* idx,
+                           const uint64_t* __restrict__ zkey, int* overflow) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  const uint32_t f = fk[j];
+  if ((j > 0 && fk[j - 1] == f) || j + 1 >= m || fk[j + 1] != f) return;  // head of a run >= 2 only
+  int64_t e = j + 1;
+  while (e < m && fk[e] == f) {
+    if (++e - j > kTieRun) {
+      atomicExch(overflow, 1);
+      return;
+    }
+  }
+  const int L = int(e - j);
+  uint64_t kk[kTieRun];
+  int32_t ii[kTieRun];
+  for (int q = 0; q < L; ++q) {
+    ii[q] = idx[j + q];
+    kk[q] = zkey[ii[q]];
+  }
+  for (int q = 1; q < L; ++q) {  // insertion sort; indices ascend already, so key ties keep them
+    const uint64_t k = kk[q];
+    const int32_t i = ii[q];
+    int r = q - 1;
+    while (r >= 0 && kk[r] > k) {
+      kk[r + 1] = kk[r];
+      ii[r + 1] = ii[r];
+      --r;
+    }
+    kk[r + 1] = k;
+    ii[r + 1] = i;
+  }
+  for (int q = 0; q < L; ++q) idx[j + q] = ii[q];
+}
+
+// Second half of a binning: the Gaussians with at least one tile (the others emit
+// nothing) in (zkey_in, index) order, their (tile, gaussian) entries emitted in that
+// order, and a stable sort by tile gives per-tile lists ordered by (key, index).
+// Inputs: c->rect, c->gcount[n + 1] (0 sentinel), c->zkey_in filled by a rect kernel.
+//
+// The (key, index) sort: the visible Gaussians are compacted in index order, sorted
+// stably by a 32-bit float rounding of the key (4 radix passes instead of 8), and runs
+// of equal float keys are then re-sorted by the full key (k_fix_ties); runs longer than
+// kTieRun (never seen in practice) fall back to the 64-bit sort.
 void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding& b,
                 bool charge_cache) {
   const int64_t T = int64_t(tiles_x) * tiles_y;
   const int64_t n = c->n;
-  sort_pairs_u64(c, c->zkey_in.p, c->zkey_out.p, c->gidx_in.p, c->gidx_out.p, n, 64);
-  c->ekey_in.ensure(n + 1);
-  k_gather_counts<<<grid_for(n + 1, 256), 256, 0, c->stream>>>(n, c->gidx_out.p, c->gcount.p,
+  // visible Gaussians in index order -> gidx_in[0, m)
+  c->bin_scalar.ensure(2);
+  {
+    size_t bytes = 0;
+    thrust::counting_iterator<int32_t> it(0);
+    HasTiles pred{c->gcount.p};
+    SOF_CUDA(cub::DeviceSelect::If(nullptr, bytes, it, c->gidx_in.p, c->bin_scalar.p, n, pred, c->stream));
+    c->cub_tmp.ensure(bytes);
+    SOF_CUDA(cub::DeviceSelect::If(c->cub_tmp.p, bytes, it, c->gidx_in.p, c->bin_scalar.p, n, pred, c->stream));
+    c->launches += 2;
+  }
+  const int64_t m = read_scalar(c, c->bin_scalar.p);
+  c->bin_m = m;
+  if (m > 0) {
+    uint32_t* fk_in = reinterpret_cast<uint32_t*>(c->zkey_out.p);  // zkey_out: 2 x n u32 of scratch
+    uint32_t* fk_out = fk_in + n;
+    k_float_keys<<<grid_for(m, 256), 256, 0, c->stream>>>(m, c->gidx_in.p, c->zkey_in.p, fk_in);
+    SOF_LAUNCHED(c);
+    sort_pairs_u32(c, fk_in, fk_out, c->gidx_in.p, c->gidx_out.p, m, 32);
+    zero_async(c, c->bin_scalar.p + 1, sizeof(int));
+    k_fix_ties<<<grid_for(m, 256), 256, 0, c->stream>>>(m, fk_out, c->gidx_out.p, c->zkey_in.p,
+                                                         reinterpret_cast<int*>(c->bin_scalar.p + 1));
+    SOF_LAUNCHED(c);
+    if (read_scalar(c, reinterpret_cast<int*>(c->bin_scalar.p + 1))) {  // a long tie run: full sort
+      c->zkey_aux.ensure(m);
+      k_gather_keys<<<grid_for(m, 256), 256, 0, c->stream>>>(m, c->gidx_in.p, c->zkey_in.p, c->zkey_aux.p);
+      SOF_LAUNCHED(c);
+      sort_pairs_u64(c, c->zkey_aux.p, c->zkey_out.p, c->gidx_in.p, c->gidx_out.p, m, 64);
+    }
+  }
+  c->ekey_in.ensure(m + 1);
+  k_gather_counts<<<grid_for(m + 1, 256), 256, 0, c->stream>>>(m, c->gidx_out.p, c->gcount.p,
                                                                 c->ekey_in.p);
   SOF_LAUNCHED(c);
-  exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, n + 1);
-  const int64_t M = read_scalar(c, c->goff.p + n);
+  exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, m + 1);
+  const int64_t M = read_scalar(c, c->goff.p + m);
   if (charge_cache && &b != &c->bind_scratch[0] && &b != &c->bind_scratch[1]) {
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
@@ -363,8 +459,8 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
     c->ekey_in.ensure(M);
     c->ekey_out.ensure(M);
     c->eval_in.ensure(M);
-    k_emit_entries<<<grid_for(n, 256), 256, 0, c->stream>>>(
-        n, c->gidx_out.p, c->rect.p, c->gcount.p, c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p);
+    k_emit_entries<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(
+        c->bin_m, c->gidx_out.p, c->rect.p, c->gcount.p, c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p);
     SOF_LAUNCHED(c);
     // stable sort by tile keeps the (min_z, index) order inside every tile list
     sort_pairs_u32(c, c->ekey_in.p, c->ekey_out.p, c->eval_in.p, b.ent.p, M, bits_for(T));

@@ -206,7 +206,9 @@ struct sof_ctx {
   // binning scratch
   sofk::DBuf<int4> rect;
   sofk::DBuf<uint32_t> gcount;
-  sofk::DBuf<uint64_t> zkey_in, zkey_out;
+  sofk::DBuf<uint64_t> zkey_in, zkey_out, zkey_aux;
+  sofk::DBuf<int64_t> bin_scalar;  // [2] selected count | tie-run overflow flag
+  int64_t bin_m = 0;               // Gaussians with tiles in the current binning
   sofk::DBuf<int32_t> gidx_in, gidx_out;
   sofk::DBuf<int64_t> goff;
   sofk::DBuf<uint32_t> ekey_in, ekey_out;

@@ -236,3 +236,34 @@ def test_fast_loop_staging_bitexact(ref, mask, staging):
     want = rc.tile_binding(0, 16)
     np.testing.assert_array_equal(off, want["offsets"])
     np.testing.assert_array_equal(ent, want["entries"])
+
+
+@pytest.mark.parametrize("group", [5, 40])
+def test_tile_binding_depth_key_ties(ref, group):
+    """The tile lists' (min_z, index) order (tiles.hpp:139-144) survives the 32-bit key
+    sort: clusters of Gaussians whose min_z differ only below float resolution (and some
+    exactly equal) are re-sorted by the full key; clusters longer than the tie-run limit
+    take the 64-bit fallback sort."""
+    scene = ref.random_scene(61, 400, 1.0)
+    rng = np.random.default_rng(group)
+    for g in range(len(scene.opacity) // group):
+        sl = slice(g * group, (g + 1) * group)
+        scene.pos[sl] = scene.pos[g * group]
+        scene.scale[sl] = scene.scale[g * group]
+        scene.rot[sl] = scene.rot[g * group]
+        eps = rng.permutation(group) * 1e-10 * (g % 3)  # g % 3 == 0: exact ties
+        scene.pos[sl, 2] += eps
+    cams = ref.orbit_cameras(3, 4.0, 1.8, 64)
+    rc = ref.context(scene, cams)
+    ctx = sof.Context(0)
+    views = sof.ViewSet.build(scene, cams, ctx=ctx)
+    for v in range(cams.v):
+        off, ent = ctx.tile_binding(v, 16)
+        want = rc.tile_binding(v, 16)
+        np.testing.assert_array_equal(off, want["offsets"])
+        np.testing.assert_array_equal(ent, want["entries"])
+    pts = np.random.default_rng(9).uniform(-1.2, 1.2, (3000, 3))
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
+    rev = rc.evaluator(ALL)
+    assert_bits(ev.label_grid(pts), rev.label_grid(pts))
+    assert ev.counters() == rev.counters()
