@@ -452,6 +452,7 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
   b.tile_size = ts;
   b.tiles_x = tiles_x;
   b.tiles_y = tiles_y;
+  if (M > INT32_MAX) throw InvalidArg("a view's tile lists exceed 2^31 entries");
   b.off.ensure(T + 1);
   b.entries = M;
   b.ent.ensure(std::max<int64_t>(M, 1));
@@ -568,16 +569,21 @@ __global__ void k_block_counts(int T, int S, const int* __restrict__ tile_off, i
                               kBlockPoints;
 }
 
+// Block descriptors {first point, end point, tile, 0}; with the tile lists' offsets
+// (loff) {first point, end point, list begin, list end}, so the evaluation kernel
+// reads its list bounds without a dependent load (lists hold < 2^31 entries).
 __global__ void k_block_fill(int T, int S, const int* __restrict__ tile_off,
-                             const int* __restrict__ blk_off, int4* blocks, int64_t* nblocks) {
+                             const int* __restrict__ blk_off, const int64_t* __restrict__ loff, int4* blocks,
+                             int64_t* nblocks) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t == 0) *nblocks = blk_off[T];
   if (t >= T) return;
   const int b0 = blk_off[t], b1 = blk_off[t + 1];
   const int p0 = tile_off[int64_t(t) * S], p1 = tile_off[int64_t(t + 1) * S];
+  const int z = loff ? int(loff[t]) : t, w = loff ? int(loff[t + 1]) : 0;
   for (int b = b0; b < b1; ++b) {
     const int s = p0 + (b - b0) * kBlockPoints;
-    blocks[b] = make_int4(s, min(s + kBlockPoints, p1), t, 0);
+    blocks[b] = make_int4(s, min(s + kBlockPoints, p1), z, w);
   }
 }
 
@@ -691,15 +697,18 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
   int i = 0;
   PointRay pr;
   pr.observed = false;
+  double m_prev = 0.0;  // min_op[i], loaded up front so its latency hides behind the loop
   if (active) {
     i = pidx[j];
+    if (MODE == kModeLabel || MODE == kModeValue) m_prev = min_op[i];
     pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
   }
   int64_t l0 = 0, l1 = n_gauss;
-  if (TILED) {
-    l0 = loff[blk.z];
-    l1 = loff[blk.z + 1];
+  if (TILED) {  // list bounds carried by the block descriptor (k_block_fill)
+    l0 = blk.z;
+    l1 = blk.w;
   }
+  (void)loff;
   const bool dead_cull = strategies & 16, use_min_z = strategies & 2;
   const bool early = classify && (strategies & 4);
   const float cu = float(pr.px), cv = float(pr.py);
@@ -776,8 +785,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
   if (active) {
     const double o = 1.0 - survive;
     if (MODE == kModeLabel || MODE == kModeValue) {
-      const double m = min_op[i];
-      min_op[i] = (o < m) ? o : m;
+      min_op[i] = (o < m_prev) ? o : m_prev;
       if (MODE == kModeLabel && complete && o < 0.5) ext[i] = 1;
     } else if (MODE == kModeClassify) {
       if (complete && o < 0.5) ext[i] = 1;
@@ -848,9 +856,10 @@ __global__ void __launch_bounds__(256) k_eval_f32(
   const float zpf = __double2float_rn(pr.zp);
   int64_t l0 = 0, l1 = n_gauss;
   if (TILED) {
-    l0 = loff[blk.z];
-    l1 = loff[blk.z + 1];
+    l0 = blk.z;
+    l1 = blk.w;
   }
+  (void)loff;
   const bool dead_cull = strategies & 16, use_min_z = strategies & 2;
   const bool early = classify && (strategies & 4);
   double survive = 1.0;
@@ -1213,7 +1222,8 @@ static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double
     exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, NB + 1);
     const int64_t grid = (int64_t(gt.G) * n + kBlockPoints - 1) / kBlockPoints + NB;
     s.blocks.ensure(grid);
-    k_block_fill<<<grid_for(NB + 1, 256), 256, 0, c->stream>>>(int(NB), 1, s.tile_off.p, s.blk_off.p, s.blocks.p,
+    k_block_fill<<<grid_for(NB + 1, 256), 256, 0, c->stream>>>(int(NB), 1, s.tile_off.p, s.blk_off.p, nullptr,
+                                                               s.blocks.p,
                                                                c->d_scalar.p);
     SOF_LAUNCHED(c);
     const int e0 = prof_mark(c);
@@ -1400,7 +1410,8 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, T + 1);
     const int64_t grid = (ncand + kBlockPoints - 1) / kBlockPoints + T;
     s.blocks.ensure(grid);
-    k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_off.p, s.blocks.p,
+    k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_off.p,
+                                                               tiled ? bd->off.p : nullptr, s.blocks.p,
                                                                c->d_scalar.p);
     SOF_LAUNCHED(c);
     prof_span(c, p1, prof_mark(c), kProfSched);
