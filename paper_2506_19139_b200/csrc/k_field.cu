@@ -20,6 +20,12 @@
 
 namespace sofk {
 
+// threads (= points) per evaluation CTA; the schedule cuts tiles into blocks of this size
+#ifndef SOF_EVAL_THREADS
+#define SOF_EVAL_THREADS 128
+#endif
+constexpr int kEvalThreads = SOF_EVAL_THREADS;
+
 // ---- helpers ------------------------------------------------------------------------------
 
 int bits_for(uint64_t max_value) {
@@ -565,8 +571,8 @@ __global__ void k_block_counts(int T, int S, const int* __restrict__ tile_off, i
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > T) return;
   blk_cnt[t] = (t == T) ? 0
-                        : (tile_off[int64_t(t + 1) * S] - tile_off[int64_t(t) * S] + kBlockPoints - 1) /
-                              kBlockPoints;
+                        : (tile_off[int64_t(t + 1) * S] - tile_off[int64_t(t) * S] + kEvalThreads - 1) /
+                              kEvalThreads;
 }
 
 // Block descriptors {first point, end point, tile, 0}; with the tile lists' offsets
@@ -582,16 +588,19 @@ __global__ void k_block_fill(int T, int S, const int* __restrict__ tile_off,
   const int p0 = tile_off[int64_t(t) * S], p1 = tile_off[int64_t(t + 1) * S];
   const int z = loff ? int(loff[t]) : t, w = loff ? int(loff[t + 1]) : 0;
   for (int b = b0; b < b1; ++b) {
-    const int s = p0 + (b - b0) * kBlockPoints;
-    blocks[b] = make_int4(s, min(s + kBlockPoints, p1), z, w);
+    const int s = p0 + (b - b0) * kEvalThreads;
+    blocks[b] = make_int4(s, min(s + kEvalThreads, p1), z, w);
   }
 }
 
 // ---- K4: opacity evaluation ----------------------------------------------------------------------
 
-constexpr int kChunk = 32;  // Gaussian records staged in shared memory per step
+#ifndef SOF_EVAL_CHUNK
+#define SOF_EVAL_CHUNK 32
+#endif
+constexpr int kChunk = SOF_EVAL_CHUNK;  // Gaussian records staged in shared memory per step
 #ifndef SOF_EVAL_MINB
-#define SOF_EVAL_MINB 5
+#define SOF_EVAL_MINB 10
 #endif
 // Instrumentation counters of k_eval (pairs evaluated in FP64 / contributing): they
 // cost registers in the hot loop, so they are compiled in only on request
@@ -620,6 +629,7 @@ __device__ __forceinline__ unsigned stream_list(const int32_t* __restrict__ lp, 
   auto chunk_cnt = [&](int k) { return min(kChunk, len - k * kChunk); };
   unsigned pairs = 0;
   if constexpr (STAGE == 1) {
+    static_assert(kChunk <= 32, "TMA staging issues one row per lane of warp 0");
     const bool warp0 = threadIdx.x < 32;
     auto chunk_row = [&](int k) {  // this lane's list entry of chunk k (0 past the end)
       const int e = k * kChunk + int(threadIdx.x & 31);
@@ -678,7 +688,7 @@ __device__ __forceinline__ unsigned stream_list(const int32_t* __restrict__ lp, 
 // buffer, and the CTA evaluates chunk k meanwhile. One barrier per chunk (it also
 // detects the all-done early exit).
 template <int MODE, bool TILED, bool FAST, int STAGE = 0>
-__global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
+__global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks,
     const int32_t* __restrict__ pidx, const double* __restrict__ xyz, Cam cam, int ts,
     int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
@@ -717,7 +727,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval(
   bool complete = true;
   bool done = !active;
   unsigned pairs = 0, exact = 0, contrib = 0;
-  if (threadIdx.x < 128) s_exp[threadIdx.x] = kSofExpTabDev[threadIdx.x];
+  for (int q = threadIdx.x; q < 128; q += blockDim.x) s_exp[q] = kSofExpTabDev[q];
   if constexpr (FAST) {
     const int32_t* lp = lent + l0;
     const int len = int(l1 - l0);  // tile lists hold < 2^31 entries
@@ -1030,7 +1040,7 @@ __global__ void k_scatter_group(int64_t n, int G, const int32_t* __restrict__ it
 // block.z is a (view, tile) bin; the view's camera, records and tile lists come from
 // device tables. Writes the per-item pair count and exterior flag.
 template <int STAGE>
-__global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
+__global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks, const int32_t* __restrict__ items,
     int64_t n, const double* __restrict__ xyz, const Cam* __restrict__ cams, int ts, GroupTables gt,
     const int64_t* const* __restrict__ loffs, const int32_t* const* __restrict__ lents,
@@ -1070,7 +1080,7 @@ __global__ void __launch_bounds__(256, SOF_EVAL_MINB) k_eval_group(
   bool complete = true;
   bool done = !active;
   unsigned pairs = 0, exact = 0, contrib = 0;
-  if (threadIdx.x < 128) s_exp[threadIdx.x] = kSofExpTabDev[threadIdx.x];
+  for (int q = threadIdx.x; q < 128; q += blockDim.x) s_exp[q] = kSofExpTabDev[q];
   // k_eval's fast loop over the live-only list (stream_list); with TMA staging the
   // tensor maps live in global memory, written by a host copy before the launch
   if (STAGE == 1 && threadIdx.x < 32) tma_fence_acquire(tmap);
@@ -1220,7 +1230,7 @@ static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double
     k_block_counts<<<grid_for(NB + 1, 256), 256, 0, c->stream>>>(int(NB), 1, s.tile_off.p, s.blk_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, NB + 1);
-    const int64_t grid = (int64_t(gt.G) * n + kBlockPoints - 1) / kBlockPoints + NB;
+    const int64_t grid = (int64_t(gt.G) * n + kEvalThreads - 1) / kEvalThreads + NB;
     s.blocks.ensure(grid);
     k_block_fill<<<grid_for(NB + 1, 256), 256, 0, c->stream>>>(int(NB), 1, s.tile_off.p, s.blk_off.p, nullptr,
                                                                s.blocks.p,
@@ -1228,11 +1238,11 @@ static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double
     SOF_LAUNCHED(c);
     const int e0 = prof_mark(c);
     if (c->staging == 1)
-      k_eval_group<1><<<unsigned(grid), 256, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
+      k_eval_group<1><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
                                                              tile_size, gt, loffs, lents, recs, g.tmaps.p, early,
                                                              g.item_pairs.p, g.item_ext.p, c->d_counters.p);
     else
-      k_eval_group<0><<<unsigned(grid), 256, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
+      k_eval_group<0><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
                                                              tile_size, gt, loffs, lents, recs, nullptr, early,
                                                              g.item_pairs.p, g.item_ext.p, c->d_counters.p);
     SOF_LAUNCHED(c);
@@ -1271,11 +1281,11 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
   const RecF* recf = view_recf(c, int(&cam - c->cams.data()));
   if (c->eval_path == 0) {
     if (tiled)
-      k_eval_f32<MODE, true><<<unsigned(grid), 256, 0, c->stream>>>(
+      k_eval_f32<MODE, true><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec, recf,
           strategies, classify, min_op, ext, o_out, obs, comp, pc);
     else
-      k_eval_f32<MODE, false><<<unsigned(grid), 256, 0, c->stream>>>(
+      k_eval_f32<MODE, false><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec, recf,
           strategies, classify, min_op, ext, o_out, obs, comp, pc);
   } else if (fast_loop(c, strategies)) {  // live-only lists, TMA-gathered records
@@ -1284,11 +1294,11 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
     std::memset(&tmap, 0, sizeof tmap);
     if (c->staging == 1) {
       if (sof_make_row_tmap(&tmap, rec, c->n) != 0) throw StateError("cuTensorMapEncodeTiled failed for the records");
-      k_eval<MODE, true, true, 1><<<unsigned(grid), 256, 0, c->stream>>>(
+      k_eval<MODE, true, true, 1><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
           strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap);
     } else {
-      k_eval<MODE, true, true, 0><<<unsigned(grid), 256, 0, c->stream>>>(
+      k_eval<MODE, true, true, 0><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
           strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap);
     }
@@ -1296,11 +1306,11 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
     CUtensorMap none;
     std::memset(&none, 0, sizeof none);
     if (tiled)
-      k_eval<MODE, true, false><<<unsigned(grid), 256, 0, c->stream>>>(
+      k_eval<MODE, true, false><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
           strategies, classify, min_op, ext, o_out, obs, comp, pc, none);
     else
-      k_eval<MODE, false, false><<<unsigned(grid), 256, 0, c->stream>>>(
+      k_eval<MODE, false, false><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
           strategies, classify, min_op, ext, o_out, obs, comp, pc, none);
   }
@@ -1408,7 +1418,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     k_block_counts<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.blk_cnt.p, s.blk_off.p, T + 1);
-    const int64_t grid = (ncand + kBlockPoints - 1) / kBlockPoints + T;
+    const int64_t grid = (ncand + kEvalThreads - 1) / kEvalThreads + T;
     s.blocks.ensure(grid);
     k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_off.p,
                                                                tiled ? bd->off.p : nullptr, s.blocks.p,
