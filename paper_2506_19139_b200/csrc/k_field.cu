@@ -110,7 +110,11 @@ struct RectOut {
 };
 
 // k_view_rec + k_tile_rect in one pass (one GaussStatic read per Gaussian and view).
-__global__ void k_view_rec_rect(int64_t n, const GaussStatic* __restrict__ g, Cam cam, Rec* out, RectOut ro) {
+#ifndef SOF_REC_MINB
+#define SOF_REC_MINB 1
+#endif
+__global__ void __launch_bounds__(128, SOF_REC_MINB) k_view_rec_rect(int64_t n, const GaussStatic* __restrict__ g,
+                                                                     Cam cam, Rec* out, RectOut ro) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i > n) return;
   if (i == n) {  // sentinel for the exclusive scan over n + 1 counts
@@ -536,14 +540,14 @@ __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
   if (k < n) {
     const int64_t i = cand ? cand[k] : k;
     if (!(skip && skip[i])) {
-      const PointRay pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+      const PointTile pt = point_tile(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
       // bin = tile x (4x4 cell of pixels inside the tile): points of one cell are
       // adjacent, so a warp covers a compact screen region (coherent conic culls)
-      if (pr.observed) {
+      if (pt.tile >= 0) {
         const int cs = (ts + 3) / 4;
         tile = single_bin ? 0
-               : (S == 16) ? pr.tile * 16 + (((int)pr.py % ts) / cs) * 4 + ((int)pr.px % ts) / cs
-                           : pr.tile;
+               : (S == 16) ? pt.tile * 16 + (((int)pt.py % ts) / cs) * 4 + ((int)pt.px % ts) / cs
+                           : pt.tile;
       }
     }
     tile_of[k] = tile;
@@ -556,13 +560,43 @@ struct NotPruned {
   __device__ bool operator()(int32_t i) const { return ext[i] == 0; }
 };
 
+// Scatter pass: kScatterItems warp-contiguous groups of 32 candidates per warp, so
+// that each warp keeps several slot-reserving atomics in flight (the returned base is
+// a long round trip; one item per thread left this kernel latency-bound).
+constexpr int kScatterItems = 4;
 __global__ void k_sched_scatter(int64_t n, const int32_t* __restrict__ cand,
                                 const int32_t* __restrict__ tile_of,
                                 const int* __restrict__ tile_off, int* tile_cur, int32_t* order) {
-  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int tile = (k < n) ? tile_of[k] : -1;
-  const int slot = warp_tile_add(tile_cur, tile, tile >= 0);
-  if (tile >= 0) order[tile_off[tile] + slot] = cand ? cand[k] : int32_t(k);
+  constexpr unsigned kAll = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t k0 = w * (32 * kScatterItems) + lane;
+  int tile[kScatterItems], base[kScatterItems], leader[kScatterItems], off[kScatterItems];
+  for (int q = 0; q < kScatterItems; ++q) {
+    const int64_t k = k0 + 32 * q;
+    tile[q] = (k < n) ? tile_of[k] : -1;
+  }
+  for (int q = 0; q < kScatterItems; ++q) {  // reserve: one atomic per run of equal bins
+    const int t = tile[q];
+    const int prev = __shfl_up_sync(kAll, t, 1);
+    const unsigned bnd = __ballot_sync(kAll, lane == 0 || prev != t);
+    const unsigned upto = (2u << lane) - 1u;
+    leader[q] = 31 - __clz(bnd & upto);
+    base[q] = 0;
+    if (t >= 0 && leader[q] == lane) {
+      const unsigned after = bnd & ~upto;
+      const int end = after ? __ffs(after) - 1 : 32;
+      base[q] = atomicAdd(tile_cur + t, end - lane);
+    }
+    off[q] = (t >= 0) ? tile_off[t] : 0;
+  }
+  for (int q = 0; q < kScatterItems; ++q) {
+    const int b = __shfl_sync(kAll, base[q], leader[q]);
+    if (tile[q] >= 0) {
+      const int64_t k = k0 + 32 * q;
+      order[off[q] + b + (lane - leader[q])] = cand ? cand[k] : int32_t(k);
+    }
+  }
 }
 
 // One thread per tile: blocks per tile; an exclusive scan of these gives block ids.
@@ -1412,7 +1446,8 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
                                                               !tiled, S, skip, s.tile_of.p, s.tile_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);
-    k_sched_scatter<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, s.tile_of.p, s.tile_off.p,
+    k_sched_scatter<<<grid_for((ncand + kScatterItems - 1) / kScatterItems, 256), 256, 0, c->stream>>>(
+        ncand, cand, s.tile_of.p, s.tile_off.p,
                                                                  tile_cur, s.order.p);
     SOF_LAUNCHED(c);
     k_block_counts<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_cnt.p);

@@ -391,6 +391,37 @@ __host__ __device__ inline PointRay point_ray(const Cam& cam, double x0, double 
   return pr;
 }
 
+// point_ray's observed flag and tile only (the scheduler's per-view pass): the same
+// projection and tests, with `t < 1e-12` (field_eval.hpp:67-70) decided on the squared
+// distance outside a relative guard band of 1e-10 around 1e-24 — sqrt and rounding are
+// monotone, so outside the band the comparison cannot differ — and by the exact sqrt
+// inside it.
+struct PointTile {
+  double px, py;
+  int tile;  // -1 when not observed
+};
+__device__ __forceinline__ PointTile point_tile(const Cam& cam, double x0, double x1, double x2, int tile_size,
+                                                int tiles_x) {
+  PointTile pt;
+  pt.tile = -1;
+  pt.px = pt.py = 0.0;
+  const double vx = to_view_c(cam, 0, x0, x1, x2);
+  const double vy = to_view_c(cam, 1, x0, x1, x2);
+  const double vz = to_view_c(cam, 2, x0, x1, x2);
+  if (vz <= 0.0) return pt;
+  const double px = cam.fx * vx / vz + cam.cx;
+  const double py = cam.fy * vy / vz + cam.cy;
+  pt.px = px;
+  pt.py = py;
+  if (!(px >= 0.0 && px < (double)cam.w && py >= 0.0 && py < (double)cam.h)) return pt;
+  const double e0 = x0 - cam.center[0], e1 = x1 - cam.center[1], e2 = x2 - cam.center[2];
+  const double s2 = e0 * e0 + e1 * e1 + e2 * e2;
+  const bool near = (s2 < 1e-24 * (1.0 - 1e-10)) ? true : (s2 > 1e-24 * (1.0 + 1e-10)) ? false : (sqrt(s2) < 1e-12);
+  if (near) return pt;
+  pt.tile = (int)py / tile_size * tiles_x + (int)px / tile_size;
+  return pt;
+}
+
 // ---- L2: one (point, Gaussian) pair of view_opacity (field_eval.hpp:95-103) ---------------
 // Returns the clamped alpha, or 0 when the pair is skipped (te <= 0 or alpha < 1/255).
 __device__ __forceinline__ double pair_alpha(const Rec& r, const double* d, double t,
