@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
         }
         if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
         if (SOF_EVAL_STATS) ++exact;
-        const double alpha = pair_alpha(r, pr.d, pr.t, s_exp);
+        const double alpha = pair_alpha(r, pr.d, pr.t, SofExpSmem{smem_u32(s_exp)});
         if (alpha == 0.0) continue;
         if (SOF_EVAL_STATS) ++contrib;
         survive *= 1.0 - alpha;
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
         ++pairs;
         if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
         if (SOF_EVAL_STATS) ++exact;
-        const double alpha = pair_alpha(r, pr.d, pr.t, s_exp);
+        const double alpha = pair_alpha(r, pr.d, pr.t, SofExpSmem{smem_u32(s_exp)});
         if (alpha == 0.0) continue;
         if (SOF_EVAL_STATS) ++contrib;
         survive *= 1.0 - alpha;
@@ -1128,7 +1128,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
       }
       if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;
       if (SOF_EVAL_STATS) ++exact;
-      const double alpha = pair_alpha(r, pr.d, pr.t, s_exp);
+      const double alpha = pair_alpha(r, pr.d, pr.t, SofExpSmem{smem_u32(s_exp)});
       if (alpha == 0.0) continue;
       if (SOF_EVAL_STATS) ++contrib;
       survive *= 1.0 - alpha;

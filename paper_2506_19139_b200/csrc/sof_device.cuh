@@ -12,6 +12,10 @@
 
 #include "sof_math.h"
 
+#ifndef SOF_EXP_CBANK
+#define SOF_EXP_CBANK 1
+#endif
+
 namespace sofk {
 
 constexpr double kMinAlpha = 1.0 / 255.0;  // core.hpp:18
@@ -424,8 +428,9 @@ __device__ __forceinline__ PointTile point_tile(const Cam& cam, double x0, doubl
 
 // ---- L2: one (point, Gaussian) pair of view_opacity (field_eval.hpp:95-103) ---------------
 // Returns the clamped alpha, or 0 when the pair is skipped (te <= 0 or alpha < 1/255).
+template <typename Tab = const double*>
 __device__ __forceinline__ double pair_alpha(const Rec& r, const double* d, double t,
-                                             const double* exp_tab = kSofExpTabDev) {
+                                             Tab exp_tab = kSofExpTabDev) {
   const double x = d[0], y = d[1], z = d[2];
   // abc_cached (precompute.hpp:39-45)
   const double a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z +
@@ -444,7 +449,11 @@ __device__ __forceinline__ double pair_alpha(const Rec& r, const double* d, doub
   }
   const double arg = -0.5 * ((a * te + b) * te + r.c);  // eval_1d gaussian.hpp:47-49
   if (arg < double(r.thr)) return 0.0;                  // alpha < 1/255 certain
-  const double e = (arg >= -700.0 && arg <= 700.0) ? sof_exp_mid(arg, exp_tab) : sof_exp(arg);
+#if SOF_EXP_CBANK
+  const double e = (arg >= -700.0 && arg <= 700.0) ? sof_exp_mid_cb(arg, exp_tab) : sof_exp(arg);
+#else
+  const double e = (arg >= -700.0 && arg <= 700.0) ? sof_exp_mid(arg, exp_tab) : sof_exp(arg);  // generic table
+#endif
   const double alpha = r.op * e;
   if (alpha < kMinAlpha) return 0.0;
   return (kMaxAlpha < alpha) ? kMaxAlpha : alpha;  // std::min(alpha, kMaxAlpha)

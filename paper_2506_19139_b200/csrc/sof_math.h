@@ -201,6 +201,41 @@ __device__ __forceinline__ double sof_exp_mid(double x, const double* tab = kSof
   const double y = __dadd_rn(t.x, __fma_rn(t.x, p, t.y));
   return __dmul_rn(y, sof_pow2i(k >> 6));
 }
+
+/// sof_exp_mid with its coefficients in the constant bank: every DFMA / DMUL takes its
+/// constant as a c[bank][offset] operand instead of materialising a 64-bit immediate
+/// through uniform-register moves (fewer issue slots per evaluation). Same operations,
+/// same bits.
+static __constant__ double kSofExpC[8] = {0x1.71547652b82fep+6, 0x1.62e42fefa0000p-7, 0x1.cf79abc9e3b3ap-46,
+                                          1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5};
+/// the (hi, lo) table entry j: from a generic pointer, or from a shared-memory copy
+/// addressed by its 32-bit shared-window address (no generic->shared conversion per use)
+struct SofExpSmem {
+  uint32_t addr;
+};
+__device__ __forceinline__ double2 sof_exp_entry(const double* tab, int j) {
+  return reinterpret_cast<const double2*>(tab)[j];
+}
+__device__ __forceinline__ double2 sof_exp_entry(SofExpSmem tab, int j) {
+  double2 t;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(t.x), "=d"(t.y) : "r"(tab.addr + 16u * uint32_t(j)));
+  return t;
+}
+template <typename Tab>
+__device__ __forceinline__ double sof_exp_mid_cb(double x, Tab tab) {
+  const double kd = rint(__dmul_rn(x, kSofExpC[0]));
+  const int k = (int)kd;
+  double r = __fma_rn(-kd, kSofExpC[1], x);
+  r = __fma_rn(-kd, kSofExpC[2], r);
+  double q = __fma_rn(r, kSofExpC[3], kSofExpC[4]);
+  q = __fma_rn(q, r, kSofExpC[5]);
+  q = __fma_rn(q, r, kSofExpC[6]);
+  q = __fma_rn(q, r, kSofExpC[7]);
+  const double p = __fma_rn(__dmul_rn(r, r), q, r);
+  const double2 t = sof_exp_entry(tab, k & 63);  // (hi, lo)
+  const double y = __dadd_rn(t.x, __fma_rn(t.x, p, t.y));
+  return __dmul_rn(y, sof_pow2i(k >> 6));
+}
 #endif
 
 /// natural log: x = 2^k m with m in [sqrt(2)/2, sqrt(2)), f = m - 1,
