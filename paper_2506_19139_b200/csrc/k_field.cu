@@ -1192,17 +1192,43 @@ __global__ void k_group_fixup(int64_t n, int G, bool prune, const int32_t* __res
 
 // Bisection classification of n points (ext[k] = exterior) over views [v0, v1) in
 // groups; false when the grouped path does not apply (then eval_views runs per view).
+static bool view_resident(const sof_ctx* c, int v, int tile_size) {
+  const Binding& b = c->bindings[v];
+  return c->rec_valid[v] && b.view == v && b.tile_size == tile_size && b.live;
+}
+
+static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int strategies,
+                                 int tile_size, uint8_t* ext, uint64_t* counters_host);
+
+// Classification over views [v0, v1) in view order: maximal runs of views whose records
+// and live tile lists are resident go through the grouped kernels, the other views
+// (past the cache budget) through the per-view path. Processing stays in view order, so
+// pruning and the counters follow the reference's sequential visit (field_eval.hpp:114-125).
 static bool classify_grouped(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int strategies,
                              int tile_size, uint8_t* ext, uint64_t* counters_host) {
   if (c->eval_path != 1 || (strategies & 19) != 19 || n <= 0 || v1 <= v0) return false;
   if (std::getenv("SOF_NO_GROUPED")) return false;
-  const int V = int(c->cams.size());
-  // every view's records and tile lists must be resident (they are after the label pass
-  // unless the cache budget ran out)
-  for (int v = v0; v < v1; ++v) {
-    const Binding& b = c->bindings[v];
-    if (!c->rec_valid[v] || b.view != v || b.tile_size != tile_size || !b.live) return false;
+  bool run = false;  // at least two consecutive resident views
+  for (int v = v0; v + 1 < v1 && !run; ++v) run = view_resident(c, v, tile_size) && view_resident(c, v + 1, tile_size);
+  if (!run) return false;
+  for (int v = v0; v < v1;) {
+    int e = v;
+    while (e < v1 && view_resident(c, e, tile_size)) ++e;
+    if (e > v && classify_grouped_run(c, v, e, n, xyz, strategies, tile_size, ext, counters_host)) {
+      v = e;
+      continue;
+    }
+    const int stop = (e > v) ? e : v + 1;  // a run the grouped path declined, or one view
+    for (; v < stop; ++v)
+      eval_views(c, v, v + 1, n, xyz, strategies, tile_size, true, kModeClassify, nullptr, ext, nullptr, nullptr,
+                 nullptr, counters_host);
   }
+  return true;
+}
+
+static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int strategies,
+                                 int tile_size, uint8_t* ext, uint64_t* counters_host) {
+  const int V = int(c->cams.size());
   const int G = std::min(kGroupViews, v1 - v0);
   if (int64_t(G) * n >= (int64_t(1) << 31)) return false;
   std::vector<const void*> ptrs(3 * size_t(V), nullptr);
