@@ -531,6 +531,9 @@ __device__ __forceinline__ int warp_tile_add(int* counters, int bin, bool valid)
 // Candidates are all points (cand == nullptr) or a compacted list of the points not
 // yet pruned; tile_of is indexed by candidate slot. S bins per tile: 16 (4x4 pixel
 // cells) or 1.
+// TS: the tile size when it is the default 16 (shifts and masks instead of integer
+// divisions by a runtime value), 0 for any other tile size.
+template <int TS>
 __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
                              const double* __restrict__ xyz, Cam cam, int ts, int tiles_x,
                              bool single_bin, int S, const uint8_t* __restrict__ skip, int32_t* tile_of,
@@ -540,14 +543,20 @@ __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
   if (k < n) {
     const int64_t i = cand ? cand[k] : k;
     if (!(skip && skip[i])) {
-      const PointTile pt = point_tile(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+      const PointTile pt = point_tile<TS>(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
       // bin = tile x (4x4 cell of pixels inside the tile): points of one cell are
       // adjacent, so a warp covers a compact screen region (coherent conic culls)
       if (pt.tile >= 0) {
-        const int cs = (ts + 3) / 4;
-        tile = single_bin ? 0
-               : (S == 16) ? pt.tile * 16 + (((int)pt.py % ts) / cs) * 4 + ((int)pt.px % ts) / cs
-                           : pt.tile;
+        if (single_bin) {
+          tile = 0;
+        } else if (S != 16) {
+          tile = pt.tile;
+        } else if (TS == 16) {  // px, py >= 0 here, so shifts are the divisions
+          tile = pt.tile * 16 + ((((int)pt.py) & 15) >> 2) * 4 + ((((int)pt.px) & 15) >> 2);
+        } else {
+          const int cs = (ts + 3) / 4;
+          tile = pt.tile * 16 + (((int)pt.py % ts) / cs) * 4 + ((int)pt.px % ts) / cs;
+        }
       }
     }
     tile_of[k] = tile;
@@ -1037,6 +1046,7 @@ struct GroupTables {
   int64_t bin_base[kGroupViews + 1];  // first bin of each view of the group
 };
 
+template <int TS>  // 16: the default tile size as a compile-time constant (see k_sched_tile)
 __global__ void k_sched_group(int64_t n, const double* __restrict__ xyz, const Cam* __restrict__ cams, int ts,
                               GroupTables gt, const uint8_t* __restrict__ skip, int32_t* item_bin, int* bin_cnt) {
   const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -1051,9 +1061,9 @@ __global__ void k_sched_group(int64_t n, const double* __restrict__ xyz, const C
     int bin = -1;
     if (live) {
       const Cam& cam = cams[gt.g0 + j];
-      const int tiles_x = (cam.w + ts - 1) / ts;
-      const PointRay pr = point_ray(cam, x0, x1, x2, ts, tiles_x);
-      if (pr.observed) bin = int(gt.bin_base[j]) + pr.tile;
+      const int tiles_x = (TS == 16) ? (cam.w + 15) >> 4 : (cam.w + ts - 1) / ts;
+      const PointTile pt = point_tile<TS>(cam, x0, x1, x2, ts, tiles_x);
+      if (pt.tile >= 0) bin = int(gt.bin_base[j]) + pt.tile;
     }
     if (k < n) item_bin[int64_t(j) * n + k] = bin;
     warp_tile_add(bin_cnt, bin, bin >= 0);
@@ -1281,7 +1291,11 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
     zero_async(c, s.tile_cnt.p, int64_t(sizeof(int)) * 2 * (NB + 1));
     int* cur = s.tile_cnt.p + (NB + 1);
     const uint8_t* skip = prune ? ext : nullptr;
-    k_sched_group<<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, g.cams.p, tile_size, gt, skip, g.item_bin.p,
+    if (tile_size == 16)
+      k_sched_group<16><<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, g.cams.p, tile_size, gt, skip, g.item_bin.p,
+                                                           s.tile_cnt.p);
+    else
+      k_sched_group<0><<<grid_for(n, 256), 256, 0, c->stream>>>(n, xyz, g.cams.p, tile_size, gt, skip, g.item_bin.p,
                                                            s.tile_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);
@@ -1468,8 +1482,12 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     zero_async(c, s.tile_cnt.p, int64_t(sizeof(int)) * 2 * (NB + 1));
     int* tile_cur = s.tile_cnt.p + (NB + 1);
     const int32_t* cand = use_list ? s.active.p : nullptr;
-    k_sched_tile<<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
-                                                              !tiled, S, skip, s.tile_of.p, s.tile_cnt.p);
+    if (tile_size == 16)
+      k_sched_tile<16><<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
+                                                                    !tiled, S, skip, s.tile_of.p, s.tile_cnt.p);
+    else
+      k_sched_tile<0><<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
+                                                                   !tiled, S, skip, s.tile_of.p, s.tile_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);
     k_sched_scatter<<<grid_for((ncand + kScatterItems - 1) / kScatterItems, 256), 256, 0, c->stream>>>(

@@ -404,6 +404,7 @@ struct PointTile {
   double px, py;
   int tile;  // -1 when not observed
 };
+template <int TS = 0>  // TS = 16: the default tile size as a compile-time constant
 __device__ __forceinline__ PointTile point_tile(const Cam& cam, double x0, double x1, double x2, int tile_size,
                                                 int tiles_x) {
   PointTile pt;
@@ -422,7 +423,8 @@ __device__ __forceinline__ PointTile point_tile(const Cam& cam, double x0, doubl
   const double s2 = e0 * e0 + e1 * e1 + e2 * e2;
   const bool near = (s2 < 1e-24 * (1.0 - 1e-10)) ? true : (s2 > 1e-24 * (1.0 + 1e-10)) ? false : (sqrt(s2) < 1e-12);
   if (near) return pt;
-  pt.tile = (int)py / tile_size * tiles_x + (int)px / tile_size;
+  pt.tile = (TS == 16) ? ((int)py >> 4) * tiles_x + ((int)px >> 4)  // px, py >= 0: shifts = divisions
+                       : (int)py / tile_size * tiles_x + (int)px / tile_size;
   return pt;
 }
 
