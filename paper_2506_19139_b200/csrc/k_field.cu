@@ -262,11 +262,17 @@ __global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
       base = off[r];
     }
   }
-  const int w = max(rc.y - rc.x + 1, 1);
-  for (uint32_t k = 0; k < min(count, kOwn); ++k) {
-    const int ty = rc.z + int(k / w), tx = rc.x + int(k % w);
-    keys[base + k] = uint32_t(ty * tiles_x + tx);
-    vals[base + k] = g;
+  {  // row-major walk of the first kOwn tiles of the rectangle (no divisions)
+    const uint32_t own = min(count, kOwn);
+    int tx = rc.x, ty = rc.z;
+    for (uint32_t k = 0; k < own; ++k) {
+      keys[base + k] = uint32_t(ty * tiles_x + tx);
+      vals[base + k] = g;
+      if (++tx > rc.y) {
+        tx = rc.x;
+        ++ty;
+      }
+    }
   }
   // large footprints: the warp writes the remaining entries cooperatively
   unsigned big = __ballot_sync(0xffffffffu, count > kOwn);
@@ -361,9 +367,14 @@ constexpr int kTieRun = 32;
 __global__ void k_fix_ties(int64_t m, const uint32_t* __restrict__ fk, int32_t* idx,
                            const uint64_t* __restrict__ zkey, int* overflow) {
   const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint32_t f = (j < m) ? fk[j] : 0u;
+  // neighbours through the warp (one load per element); the warp's edge lanes load theirs
+  uint32_t prev = __shfl_up_sync(0xffffffffu, f, 1), next = __shfl_down_sync(0xffffffffu, f, 1);
   if (j >= m) return;
-  const uint32_t f = fk[j];
-  if ((j > 0 && fk[j - 1] == f) || j + 1 >= m || fk[j + 1] != f) return;  // head of a run >= 2 only
+  if (lane == 0) prev = (j > 0) ? fk[j - 1] : ~f;
+  if (lane == 31 || j + 1 >= m) next = (j + 1 < m) ? fk[j + 1] : ~f;
+  if ((j > 0 && prev == f) || j + 1 >= m || next != f) return;  // head of a run >= 2 only
   int64_t e = j + 1;
   while (e < m && fk[e] == f) {
     if (++e - j > kTieRun) {

@@ -380,7 +380,10 @@ __device__ __forceinline__ void warp_bitonic(uint64_t* k, int32_t* v, double* a,
 // (double_key(t*), index, alpha) entries are sorted in shared memory (slices longer
 // than kFChunk: sorted chunks merged by rank into keys2/vals2/alpha2) and blended
 // serially through shuffles; t* is recovered from its key.
-__global__ void __launch_bounds__(kFWarps * 32, 2) k_render_finish(
+#ifndef SOF_FIN_MINB
+#define SOF_FIN_MINB 3
+#endif
+__global__ void __launch_bounds__(kFWarps * 32, SOF_FIN_MINB) k_render_finish(
     Cam cam, const Rec* __restrict__ recs, const double* __restrict__ dc, int exact_depth, Spill spill,
     uint64_t* __restrict__ gk2, int32_t* __restrict__ gv2, double* __restrict__ ga2, RenderOut out,
     unsigned long long* stats) {
