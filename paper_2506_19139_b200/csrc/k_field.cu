@@ -175,7 +175,11 @@ void invalidate_view_caches(sof_ctx* c) {
 static const Rec* view_records_impl(sof_ctx* c, int view, const RectOut* ro, bool* rect_done) {
   if (rect_done) *rect_done = false;
   if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
-  if (c->rec_valid[view]) return c->recs[view].p;
+  if (c->rec_valid[view] == 1) return c->recs[view].p;
+  if (c->rec_valid[view] == 2) {  // a truncated bisection cache: not the full records
+    c->rec_valid[view] = 0;
+    c->bindings[view].view = -1;
+  }
   const int sel = c->scratch_sel;
   if (c->scratch_view[sel] == view) return c->rec_scratch[sel].p;
   const bool with_f = c->eval_path == 0;  // float filter records only for the FP32 path
@@ -208,7 +212,7 @@ const Rec* view_records(sof_ctx* c, int view) { return view_records_impl(c, view
 
 // Float filter records of `view`, valid after view_records(c, view).
 const RecF* view_recf(sof_ctx* c, int view) {
-  if (c->rec_valid[view]) return c->recfs[view].p;
+  if (c->rec_valid[view] == 1) return c->recfs[view].p;
   return c->recf_scratch[c->scratch_view[0] == view ? 0 : 1].p;
 }
 
@@ -308,6 +312,7 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
                                int tiles_x, int tiles_y);
 
 static void build_binding(sof_ctx* c, int view, int ts, bool live, Binding& b, bool charge) {
+  b.trunc = false;
   const Cam& cam = c->cams[view];
   const int tiles_x = (cam.w + ts - 1) / ts, tiles_y = (cam.h + ts - 1) / ts;
   const int64_t T = int64_t(tiles_x) * tiles_y;
@@ -458,6 +463,7 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
     if (c->cache_bytes + bytes > c->cache_budget) {
       c->bind_scratch[c->scratch_sel].live = b.live;
+      c->bind_scratch[c->scratch_sel].trunc = false;
       build_binding_tail(c, view, ts, c->bind_scratch[c->scratch_sel], M, T, tiles_x, tiles_y);
       return;
     }
@@ -494,7 +500,12 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
 
 const Binding& view_binding(sof_ctx* c, int view, int tile_size, bool live) {
   Binding& cached = c->bindings[view];
-  if (cached.view == view && cached.tile_size == tile_size && cached.live == live) return cached;
+  if (cached.view == view && cached.tile_size == tile_size && cached.live == live && !cached.trunc) return cached;
+  if (cached.trunc) {  // a truncated bisection cache is rebuilt as a full binding
+    cached.view = -1;
+    cached.trunc = false;
+    if (c->rec_valid[view] == 2) c->rec_valid[view] = 0;
+  }
   for (int k = 0; k < 2; ++k)
     if (c->bind_scratch[k].view == view && c->bind_scratch[k].tile_size == tile_size &&
         c->bind_scratch[k].live == live)
@@ -1267,7 +1278,7 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
     std::vector<CUtensorMap> tmaps(static_cast<size_t>(V));
     std::memset(tmaps.data(), 0, sizeof(CUtensorMap) * size_t(V));
     for (int v = v0; v < v1; ++v)
-      if (sof_make_row_tmap(&tmaps[v], c->recs[v].p, c->n) != 0)
+      if (sof_make_row_tmap(&tmaps[v], c->recs[v].p, c->bindings[v].trunc ? c->bindings[v].rows : c->n) != 0)
         throw StateError("cuTensorMapEncodeTiled failed for the records");
     g.tmaps.ensure(V);
     SOF_CUDA(cudaMemcpyAsync(g.tmaps.p, tmaps.data(), sizeof(CUtensorMap) * V, cudaMemcpyHostToDevice, c->stream));
@@ -1352,6 +1363,203 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
 // The FP64 fast loop of k_eval: tile lists + min-z + dead cull (the default strategies).
 static bool fast_loop(const sof_ctx* c, int strategies) {
   return c->eval_path == 1 && (strategies & 19) == 19;
+}
+
+// ---- bisection cache for views past the record budget -----------------------------------------
+//
+// binary_search_refine (marching_tets.hpp:94-114) classifies midpoints that always lie on
+// their crossing edge's segment [p_in, p_out]. In a view, such a point's list scan
+// stops at the first entry with min_z > its view depth (field_eval.hpp:90-93), so tile
+// t only ever reads the prefix of its list with min_z <= zmax(t), zmax(t) = the largest
+// endpoint depth over the segments whose projection can reach tile t. For views whose
+// records and lists did not fit the cache during the label pass, the lists are built
+// once, truncated to those prefixes (a midpoint's scan over the prefix makes exactly
+// the reference's pairs, breaks and early stops: the entry after the prefix has
+// min_z > zmax(t) >= the point's depth), and their records compacted — small enough to
+// stay resident for all iterations, so the grouped kernels serve every view instead of
+// re-binning a view per iteration.
+
+// per tile: ordered key of the largest depth a midpoint in the tile can have (0: none)
+__global__ void k_segment_zmax(int64_t ne, const int32_t* __restrict__ edges, const double* __restrict__ xyz,
+                               Cam cam, int ts, int tiles_x, int tiles_y, unsigned long long* zmax,
+                               int* bail) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= ne) return;
+  const int32_t a = edges[2 * e], b = edges[2 * e + 1];
+  double z[2], px[2], py[2];
+  const int32_t v[2] = {a, b};
+  for (int q = 0; q < 2; ++q) {
+    const double x0 = xyz[3 * v[q]], x1 = xyz[3 * v[q] + 1], x2 = xyz[3 * v[q] + 2];
+    z[q] = to_view_c(cam, 2, x0, x1, x2);
+    if (z[q] > 1e-6) {
+      px[q] = cam.fx * to_view_c(cam, 0, x0, x1, x2) / z[q] + cam.cx;
+      py[q] = cam.fy * to_view_c(cam, 1, x0, x1, x2) / z[q] + cam.cy;
+    }
+  }
+  if (z[0] <= 0.0 && z[1] <= 0.0) return;  // the whole segment is behind: never observed
+  if (z[0] <= 1e-6 || z[1] <= 1e-6) {       // crosses (or touches) the camera plane
+    atomicExch(bail, 1);
+    return;
+  }
+  // tile box of the projected segment, dilated by one tile against rounding of the
+  // midpoints' own projections
+  const double lo_x = fmin(px[0], px[1]), hi_x = fmax(px[0], px[1]);
+  const double lo_y = fmin(py[0], py[1]), hi_y = fmax(py[0], py[1]);
+  if (hi_x < -double(ts) || hi_y < -double(ts) || lo_x > double(cam.w + ts) || lo_y > double(cam.h + ts)) return;
+  const int tx0 = max(0, int(floor(fmax(lo_x, -2.0 * ts) / ts)) - 1);
+  const int ty0 = max(0, int(floor(fmax(lo_y, -2.0 * ts) / ts)) - 1);
+  const int tx1 = min(tiles_x - 1, int(floor(fmin(hi_x, double(cam.w + 2 * ts)) / ts)) + 1);
+  const int ty1 = min(tiles_y - 1, int(floor(fmin(hi_y, double(cam.h + 2 * ts)) / ts)) + 1);
+  if (int64_t(tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 4096) {  // a long screen segment: keep the full lists
+    atomicExch(bail, 1);
+    return;
+  }
+  const double zm = fmax(z[0], z[1]);
+  const unsigned long long key = double_key(zm + 1e-9 * (1.0 + zm));
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) atomicMax(zmax + int64_t(ty) * tiles_x + tx, key);
+}
+
+// per tile: length of the list prefix with min_z <= zmax(t) (lists sorted by (min_z, index))
+__global__ void k_trunc_len(int64_t T, const int64_t* __restrict__ off, const int32_t* __restrict__ ent,
+                            const Rec* __restrict__ rec, const unsigned long long* __restrict__ zmax,
+                            int64_t* len) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t > T) return;
+  if (t == T) {
+    len[T] = 0;
+    return;
+  }
+  const unsigned long long zk = zmax[t];
+  int64_t lo = off[t], hi = off[t + 1];
+  if (zk == 0) {
+    len[t] = 0;
+    return;
+  }
+  const double zm = key_double(zk);
+  const int64_t l0 = lo;
+  while (lo < hi) {  // first entry with min_z > zm
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (rec[ent[mid]].zmin > zm)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  len[t] = lo - l0;
+}
+
+// one warp per tile: mark the Gaussians of the kept prefixes
+__global__ void k_trunc_mark(int64_t T, const int64_t* __restrict__ off, const int32_t* __restrict__ ent,
+                             const int64_t* __restrict__ len, uint8_t* used) {
+  const int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = off[t], L = len[t];
+  for (int64_t k = lane; k < L; k += 32) used[ent[b + k]] = 1;
+}
+
+// compact row of every used Gaussian; copy its record
+__global__ void k_trunc_rows(int64_t n, const uint8_t* __restrict__ used, const int32_t* __restrict__ pos,
+                             const Rec* __restrict__ rec, Rec* out) {
+  const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (g >= n || !used[g]) return;
+  out[pos[g]] = rec[g];
+}
+
+// one warp per tile: the kept prefix, entries remapped to compact rows
+__global__ void k_trunc_emit(int64_t T, const int64_t* __restrict__ off, const int32_t* __restrict__ ent,
+                             const int64_t* __restrict__ toff, const int32_t* __restrict__ pos, int32_t* out) {
+  const int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = off[t], ob = toff[t], L = toff[t + 1] - ob;
+  for (int64_t k = lane; k < L; k += 32) out[ob + k] = pos[ent[b + k]];
+}
+
+__global__ void k_u8_to_i32_f(int64_t n, const uint8_t* __restrict__ a, int32_t* b) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j < n) b[j] = a[j];
+}
+
+void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* edges, int strategies,
+                        int tile_size) {
+  if (!fast_loop(c, strategies) || ne <= 0 || c->n <= 0 || std::getenv("SOF_NO_BISECT_CACHE")) return;
+  if (!c->has_tets) return;
+  const int64_t n = c->n;
+  DBuf<unsigned long long> zmax;
+  DBuf<int64_t> len, toff;
+  DBuf<uint8_t> used;
+  DBuf<int32_t> flag, pos;
+  DBuf<int> bail;
+  for (int v = v0; v < v1; ++v) {
+    if (view_resident(c, v, tile_size)) continue;
+    const Cam& cam = c->cams[v];
+    const int tiles_x = (cam.w + tile_size - 1) / tile_size, tiles_y = (cam.h + tile_size - 1) / tile_size;
+    const int64_t T = int64_t(tiles_x) * tiles_y;
+    // tiles and depths the midpoints can reach (needs no records)
+    zmax.ensure(T);
+    bail.ensure(1);
+    zero_async(c, zmax.p, sizeof(unsigned long long) * T);
+    zero_async(c, bail.p, sizeof(int));
+    k_segment_zmax<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, edges, c->tv.p, cam, tile_size, tiles_x, tiles_y,
+                                                             zmax.p, bail.p);
+    SOF_LAUNCHED(c);
+    if (read_scalar(c, bail.p)) continue;  // this view keeps the per-view path
+    // full live lists + records of the view (scratch slot), then the truncation
+    const Binding& full = view_binding(c, v, tile_size, true);
+    const Rec* rec = view_records(c, v);
+    // the budget had room after all: the view is cached in full (or half of it is, and
+    // the per-view path serves it); never truncate into the buffers being read
+    if (&full == &c->bindings[v] || rec == c->recs[v].p) continue;
+    len.ensure(T + 1);
+    toff.ensure(T + 1);
+    k_trunc_len<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, full.off.p, full.ent.p, rec, zmax.p, len.p);
+    SOF_LAUNCHED(c);
+    {
+      size_t bytes = 0;
+      SOF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, len.p, toff.p, T + 1, c->stream));
+      c->cub_tmp.ensure(bytes);
+      SOF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, bytes, len.p, toff.p, T + 1, c->stream));
+      c->launches += 2;
+    }
+    used.ensure(n);
+    zero_async(c, used.p, n);
+    k_trunc_mark<<<grid_for(T * 32, 256), 256, 0, c->stream>>>(T, full.off.p, full.ent.p, len.p, used.p);
+    SOF_LAUNCHED(c);
+    flag.ensure(n + 1);
+    pos.ensure(n + 1);
+    k_u8_to_i32_f<<<grid_for(n, 256), 256, 0, c->stream>>>(n, used.p, flag.p);
+    SOF_LAUNCHED(c);
+    zero_async(c, flag.p + n, sizeof(int32_t));
+    exclusive_scan_i32(c, flag.p, pos.p, n + 1);
+    const int64_t L = read_scalar(c, toff.p + T);
+    const int64_t R = read_scalar(c, pos.p + n);
+    // room for it? (the full caches of the resident views stay; leave headroom)
+    size_t free_b = 0, total_b = 0;
+    SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t need = size_t(R) * sizeof(Rec) + size_t(L) * 4 + size_t(T + 1) * 8;
+    Binding& b = c->bindings[v];
+    const size_t have = c->recs[v].bytes() + b.ent.bytes() + b.off.bytes();
+    if (need > have && need - have + (size_t(8) << 30) > free_b) break;  // out of memory: per-view path from here
+    c->recs[v].ensure(std::max<int64_t>(R, 1));
+    k_trunc_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(n, used.p, pos.p, rec, c->recs[v].p);
+    SOF_LAUNCHED(c);
+    b.off.ensure(T + 1);
+    SOF_CUDA(cudaMemcpyAsync(b.off.p, toff.p, sizeof(int64_t) * (T + 1), cudaMemcpyDeviceToDevice, c->stream));
+    b.ent.ensure(std::max<int64_t>(L, 1));
+    k_trunc_emit<<<grid_for(T * 32, 256), 256, 0, c->stream>>>(T, full.off.p, full.ent.p, toff.p, pos.p, b.ent.p);
+    SOF_LAUNCHED(c);
+    b.view = v;
+    b.tile_size = tile_size;
+    b.tiles_x = tiles_x;
+    b.tiles_y = tiles_y;
+    b.live = true;
+    b.trunc = true;
+    b.rows = R;
+    b.entries = L;
+    c->rec_valid[v] = 2;
+    SOF_CUDA(cudaStreamSynchronize(c->stream));  // the scratch slot is reused by the next view
+  }
 }
 
 template <int MODE>

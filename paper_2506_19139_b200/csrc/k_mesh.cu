@@ -468,6 +468,7 @@ void refine(sof_ctx* c, int64_t ne, const int32_t* edges, double* verts, int ite
   if (iterations <= 0 || ne == 0) return;  // iterations = 0 keeps the lerp vertices (:100)
   if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
   refine_init(c, ne, edges);
+  bisect_cache_views(c, v0, v1, ne, edges, strategies, tile_size);  // views past the record budget
   for (int it = 0; it < iterations; ++it) {
     refine_mid(c, ne, c->ms.rext.p);
     // classify_point over every view (field_eval.hpp:114-125): exterior iff some view

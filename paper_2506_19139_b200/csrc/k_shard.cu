@@ -152,7 +152,10 @@ int sof_refine_phase_dev(sof_ctx* c, int phase, uint8_t* ext_dev, int v0, int v1
     if (c->n_edges < 0) throw StateError("no marching result");
     const int64_t ne = c->n_edges;
     switch (phase) {
-      case 0: refine_init(c, ne, c->r_edges.p); break;
+      case 0:
+        refine_init(c, ne, c->r_edges.p);
+        bisect_cache_views(c, v0, v1, ne, c->r_edges.p, strategies, tile_size);
+        break;
       case 1:
         refine_mid(c, ne, ext_dev);
         if (ne > 0)

@@ -91,6 +91,10 @@ struct Binding {
   // min-z break (field_eval.hpp:89-93), so these lists give identical results and
   // counters; the exact reference lists (tiles.hpp:134-144) have live = false.
   bool live = false;
+  // bisection cache (bisect_cache_views): every list truncated to the depths the
+  // bisection midpoints can reach, entries are rows of a compact record array
+  bool trunc = false;
+  int64_t rows = 0;  // compact record rows (trunc only)
   int64_t entries = 0;
   DBuf<int64_t> off;  // [T + 1]
   DBuf<int32_t> ent;  // [entries], per tile sorted by (min_z, index)
@@ -294,6 +298,8 @@ void tets_ready(sof_ctx* c);
 void pump_upload(sof_ctx* c, int64_t max_bytes);
 constexpr int64_t kUploadChunk = int64_t(64) << 20;
 void check_tet_indices(sof_ctx* c, cudaStream_t st, int64_t nt, const int32_t* tets_dev, int64_t nv, int32_t* bad);
+void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* edges_dev, int strategies,
+                        int tile_size);
 void march(sof_ctx* c, const double* opacity_dev);
 void march_range(sof_ctx* c, const double* opacity_dev, int64_t t0, int64_t t1);
 void march_merge(sof_ctx* c, const double* opacity_dev, int world, const int64_t* ecount, const int32_t* edges_all,

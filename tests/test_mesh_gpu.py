@@ -267,3 +267,28 @@ def test_tet_sharded_march_merge(lattice_case, world):
     np.testing.assert_array_equal(got[0], want[0])
     np.testing.assert_array_equal(bits(got[1]), bits(want[1]))
     np.testing.assert_array_equal(got[2], want[2])
+
+
+@pytest.mark.parametrize("dist", [4.0, 1.0])
+def test_bisection_cache_truncated_lists(ref, dist):
+    """Views past the cache budget get bisection caches: tile lists truncated to the
+    depths the midpoints can reach, with compact records (bisect_cache_views). Same mesh
+    and exact counters as the reference; with cameras inside the lattice (dist 1.0) some
+    crossing edges reach the camera plane and those views keep the per-view path."""
+    scene = ref.random_scene(63, 60, 1.0)
+    cams = ref.orbit_cameras(12, dist, 1.8, 48)
+    verts, tets = kuhn_lattice(12, -1.3, 1.3)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    views.ctx.check(views.ctx.lib.sof_set_cache_budget(views.ctx.h, 0))
+    want = rc.extract_tetgrid(verts, tets, strategies=31, iterations=8)
+    assert len(want["triangles"]) > 0
+    stats = {}
+    mesh = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets), sof.ExtractOptions(), stats)
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(mesh.triangles, want["triangles"])
+    assert stats["pairs"] == int(want["counters"][0])
+    assert stats["point_view_evals"] == int(want["counters"][1])
+    # a second extract on the same context (caches rebuilt) still matches
+    mesh2 = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets), sof.ExtractOptions(), {})
+    np.testing.assert_array_equal(mesh2.triangles, want["triangles"])
