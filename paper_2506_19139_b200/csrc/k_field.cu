@@ -1491,8 +1491,25 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
   DBuf<uint8_t> used;
   DBuf<int32_t> flag, pos;
   DBuf<int> bail;
+  const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  int n_res = 0, n_trunc = 0, n_bail = 0, n_alias = 0;
+  struct Report {  // debug summary on every exit path
+    bool on;
+    const int *res, *trunc, *bail, *alias;
+    std::chrono::steady_clock::time_point t0;
+    ~Report() {
+      if (on)
+        std::fprintf(stderr, "bisect_cache_views: resident %d truncated %d bailed %d full %d, %.1f ms\n", *res,
+                     *trunc, *bail, *alias,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } report{dbg, &n_res, &n_trunc, &n_bail, &n_alias, h0};
   for (int v = v0; v < v1; ++v) {
-    if (view_resident(c, v, tile_size)) continue;
+    if (view_resident(c, v, tile_size)) {
+      ++n_res;
+      continue;
+    }
     const Cam& cam = c->cams[v];
     const int tiles_x = (cam.w + tile_size - 1) / tile_size, tiles_y = (cam.h + tile_size - 1) / tile_size;
     const int64_t T = int64_t(tiles_x) * tiles_y;
@@ -1504,13 +1521,19 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     k_segment_zmax<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, edges, c->tv.p, cam, tile_size, tiles_x, tiles_y,
                                                              zmax.p, bail.p);
     SOF_LAUNCHED(c);
-    if (read_scalar(c, bail.p)) continue;  // this view keeps the per-view path
+    if (read_scalar(c, bail.p)) {  // this view keeps the per-view path
+      ++n_bail;
+      continue;
+    }
     // full live lists + records of the view (scratch slot), then the truncation
     const Binding& full = view_binding(c, v, tile_size, true);
     const Rec* rec = view_records(c, v);
     // the budget had room after all: the view is cached in full (or half of it is, and
     // the per-view path serves it); never truncate into the buffers being read
-    if (&full == &c->bindings[v] || rec == c->recs[v].p) continue;
+    if (&full == &c->bindings[v] || rec == c->recs[v].p) {
+      ++n_alias;
+      continue;
+    }
     len.ensure(T + 1);
     toff.ensure(T + 1);
     k_trunc_len<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, full.off.p, full.ent.p, rec, zmax.p, len.p);
@@ -1540,7 +1563,12 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     const size_t need = size_t(R) * sizeof(Rec) + size_t(L) * 4 + size_t(T + 1) * 8;
     Binding& b = c->bindings[v];
     const size_t have = c->recs[v].bytes() + b.ent.bytes() + b.off.bytes();
-    if (need > have && need - have + (size_t(8) << 30) > free_b) break;  // out of memory: per-view path from here
+    if (need > have && need - have + (size_t(2) << 30) > free_b) {  // out of memory: per-view path from here
+      if (std::getenv("SOF_DEBUG_HOST"))
+        std::fprintf(stderr, "bisect_cache_views: out of memory at view %d (free %.1f GB, need %.2f GB)\n", v,
+                     free_b / 1e9, need / 1e9);
+      break;
+    }
     c->recs[v].ensure(std::max<int64_t>(R, 1));
     k_trunc_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(n, used.p, pos.p, rec, c->recs[v].p);
     SOF_LAUNCHED(c);
@@ -1558,6 +1586,7 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     b.rows = R;
     b.entries = L;
     c->rec_valid[v] = 2;
+    ++n_trunc;
     SOF_CUDA(cudaStreamSynchronize(c->stream));  // the scratch slot is reused by the next view
   }
 }
