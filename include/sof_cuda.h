@@ -324,6 +324,37 @@ int sof_get_scene(sof_ctx* ctx, double* pos, double* scale, double* rot_wxyz, do
  * the device, float32 records; byte-identical to the reference writer. */
 int sof_write_scene_ply(sof_ctx* ctx, const char* path);
 
+
+/* ---- training losses (losses.hpp) --------------------------------------
+ * Batched over rays: ray r owns samples [off[r], off[r + 1]) (off[0] = 0, nrays + 1
+ * entries). One call evaluates the reference's per-ray function for every ray with the
+ * same operation order (per-ray losses and per-sample gradients bit-identical). Host
+ * buffers in and out. */
+/* distortion_loss (losses.hpp:54-107): loss[nrays], d_alpha / d_t [S] (d_alpha only
+ * when attach_w) */
+int sof_distortion_loss(sof_ctx* ctx, int64_t nrays, const int64_t* off, const double* alpha, const double* t,
+                        double near_plane, double far_plane, int attach_w, double* loss, double* d_alpha,
+                        double* d_t);
+/* extent_loss (losses.hpp:152-179): loss / skipped per ray, gradients per sample */
+int sof_extent_loss(sof_ctx* ctx, int64_t nrays, const int64_t* off, const double* w, const double* a,
+                    const double* b, const double* c, const double* bound, double near_plane, double far_plane,
+                    double* loss, int32_t* skipped, double* d_a, double* d_b, double* d_c, double* d_w);
+/* depth_normal_loss (losses.hpp:119-133): normals [3S], pixel_normals [3 nrays] */
+int sof_depth_normal_loss(sof_ctx* ctx, int64_t nrays, const int64_t* off, const double* w, const double* normals,
+                          const double* pixel_normals, double* loss, double* d_w, double* d_n);
+/* opacity_supervision_loss (losses.hpp:195-229): contribs = 6 doubles per sample in the
+ * ray's sorted order (t*, alpha, a, b, c, opacity); depth per ray (NaN = no surface) */
+int sof_opacity_supervision_loss(sof_ctx* ctx, int64_t nrays, const int64_t* off, const double* contribs,
+                                 const double* depth, double* loss, double* field_value, uint8_t* defined,
+                                 double* d_alpha);
+/* normal_smoothness_loss (losses.hpp:247-293): row-major W x H maps, xyz / rgb triples;
+ * per_channel selects ImageGradientMode::kPerChannel */
+int sof_normal_smoothness_loss(sof_ctx* ctx, int width, int height, const double* normals, const uint8_t* valid,
+                               const double* image, int per_channel, double* loss, int64_t* pixels_used,
+                               double* d_normal);
+/* l1_rgb_loss (losses.hpp:305-312) over `pixels` rgb triples */
+int sof_l1_rgb_loss(sof_ctx* ctx, int64_t pixels, const double* rendered, const double* reference, double* loss);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,7 @@
 #include "sof/io_maps.hpp"
 #include "sof/io_mesh.hpp"
 #include "sof/io_scene.hpp"
+#include "sof/losses.hpp"
 #include "sof/render.hpp"
 #include "test_util.hpp"
 
@@ -753,6 +754,112 @@ void* sofref_collect_contributions(const sofref_ctx* c, int view, int px, int py
   bag->put("c", cc);
   bag->put("opacity", op);
   return bag;
+}
+
+
+// ---- training losses (losses.hpp), one reference call per ray / image ---------
+
+void sofref_distortion_loss(long nrays, const int64_t* off, const double* alpha, const double* t, double near_plane,
+                            double far_plane, int attach_w, double* loss, double* d_alpha, double* d_t) {
+  for (long r = 0; r < nrays; ++r) {
+    std::vector<DistortionSample> s;
+    for (int64_t i = off[r]; i < off[r + 1]; ++i) s.push_back({alpha[i], t[i]});
+    const auto out = distortion_loss(s, near_plane, far_plane, attach_w != 0);
+    loss[r] = out.loss;
+    for (size_t k = 0; k < s.size(); ++k) {
+      d_t[off[r] + k] = out.d_t[k];
+      if (attach_w) d_alpha[off[r] + k] = out.d_alpha[k];
+    }
+  }
+}
+
+void sofref_extent_loss(long nrays, const int64_t* off, const double* w, const double* a, const double* b,
+                        const double* c, const double* bound, double near_plane, double far_plane, double* loss,
+                        int32_t* skipped, double* d_a, double* d_b, double* d_c, double* d_w) {
+  for (long r = 0; r < nrays; ++r) {
+    std::vector<ExtentSample> s;
+    for (int64_t i = off[r]; i < off[r + 1]; ++i) s.push_back({w[i], a[i], b[i], c[i], bound[i]});
+    const auto out = extent_loss(s, near_plane, far_plane);
+    loss[r] = out.loss;
+    skipped[r] = out.skipped;
+    for (size_t k = 0; k < s.size(); ++k) {
+      d_a[off[r] + k] = out.d_a[k];
+      d_b[off[r] + k] = out.d_b[k];
+      d_c[off[r] + k] = out.d_c[k];
+      d_w[off[r] + k] = out.d_w[k];
+    }
+  }
+}
+
+void sofref_depth_normal_loss(long nrays, const int64_t* off, const double* w, const double* normals,
+                              const double* pixel_normals, double* loss, double* d_w, double* d_n) {
+  for (long r = 0; r < nrays; ++r) {
+    std::vector<double> ws;
+    std::vector<Vec3> ns;
+    for (int64_t i = off[r]; i < off[r + 1]; ++i) {
+      ws.push_back(w[i]);
+      ns.push_back(Vec3(normals[3 * i], normals[3 * i + 1], normals[3 * i + 2]));
+    }
+    const Vec3 pn(pixel_normals[3 * r], pixel_normals[3 * r + 1], pixel_normals[3 * r + 2]);
+    const auto out = depth_normal_loss(ws, ns, pn);
+    loss[r] = out.loss;
+    for (size_t k = 0; k < ws.size(); ++k) {
+      d_w[off[r] + k] = out.d_w[k];
+      for (int q = 0; q < 3; ++q) d_n[3 * (off[r] + k) + q] = out.d_n[k](q);
+    }
+  }
+}
+
+void sofref_opacity_supervision_loss(long nrays, const int64_t* off, const double* contribs, const double* depth,
+                                     double* loss, double* field, uint8_t* defined, double* d_alpha) {
+  for (long r = 0; r < nrays; ++r) {
+    std::vector<RayContribution> cs;
+    for (int64_t i = off[r]; i < off[r + 1]; ++i) {
+      RayContribution rc;
+      rc.gaussian_index = int(i - off[r]);
+      rc.t_star = contribs[6 * i];
+      rc.alpha = contribs[6 * i + 1];
+      rc.a = contribs[6 * i + 2];
+      rc.b = contribs[6 * i + 3];
+      rc.c = contribs[6 * i + 4];
+      rc.opacity = contribs[6 * i + 5];
+      cs.push_back(rc);
+    }
+    const auto out = opacity_supervision_loss(cs, depth[r]);
+    loss[r] = out.loss;
+    field[r] = out.field_value;
+    defined[r] = out.defined ? 1 : 0;
+    for (size_t k = 0; k < cs.size(); ++k) d_alpha[off[r] + k] = out.defined ? out.d_alpha[k] : 0.0;
+  }
+}
+
+void sofref_normal_smoothness_loss(int width, int height, const double* normals, const uint8_t* valid,
+                                   const double* image, int per_channel, double* loss, int64_t* used,
+                                   double* d_normal) {
+  NormalMap nm;
+  nm.normal = Grid2D<Vec3>(width, height, Vec3::Zero());
+  nm.valid = Grid2D<unsigned char>(width, height, 0);
+  Grid2D<Vec3> img(width, height, Vec3::Zero());
+  for (size_t p = 0; p < size_t(width) * height; ++p) {
+    nm.normal.data[p] = Vec3(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]);
+    nm.valid.data[p] = valid[p];
+    img.data[p] = Vec3(image[3 * p], image[3 * p + 1], image[3 * p + 2]);
+  }
+  const auto out = normal_smoothness_loss(nm, img, per_channel ? ImageGradientMode::kPerChannel
+                                                               : ImageGradientMode::kLuminance);
+  *loss = out.loss;
+  *used = out.pixels_used;
+  for (size_t p = 0; p < size_t(width) * height; ++p)
+    for (int q = 0; q < 3; ++q) d_normal[3 * p + q] = out.d_normal.data[p](q);
+}
+
+double sofref_l1_rgb_loss(long pixels, const double* a, const double* b) {
+  Grid2D<Vec3> ga(int(pixels), 1, Vec3::Zero()), gb(int(pixels), 1, Vec3::Zero());
+  for (long p = 0; p < pixels; ++p) {
+    ga.data[p] = Vec3(a[3 * p], a[3 * p + 1], a[3 * p + 2]);
+    gb.data[p] = Vec3(b[3 * p], b[3 * p + 1], b[3 * p + 2]);
+  }
+  return l1_rgb_loss(ga, gb);
 }
 
 }  // extern "C"

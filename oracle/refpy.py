@@ -91,6 +91,13 @@ class RefLib:
         self.lib = ctypes.CDLL(path)
         L = self.lib
         L.sofref_last_error.restype = ctypes.c_char_p
+        L.sofref_distortion_loss.argtypes = [_L, _P, _P, _P, _D, _D, _I, _P, _P, _P]
+        L.sofref_extent_loss.argtypes = [_L] + [_P] * 6 + [_D, _D] + [_P] * 6
+        L.sofref_depth_normal_loss.argtypes = [_L] + [_P] * 7
+        L.sofref_opacity_supervision_loss.argtypes = [_L] + [_P] * 7
+        L.sofref_normal_smoothness_loss.argtypes = [_I, _I, _P, _P, _P, _I, _P, _P, _P]
+        L.sofref_l1_rgb_loss.restype = _D
+        L.sofref_l1_rgb_loss.argtypes = [_L, _P, _P]
         L.sofref_exp_probe.restype = _D
         L.sofref_exp_probe.argtypes = [_D]
         L.sofref_log_probe.restype = _D
@@ -253,6 +260,61 @@ class RefLib:
         if self.lib.sofref_write_scene(len(s[3]), *(_ptr(a) for a in s), path.encode()):
             raise RuntimeError(self.lib.sofref_last_error().decode())
 
+
+    # ---- training losses (losses.hpp), per ray through the unmodified reference -----------
+    def distortion_loss(self, off, alpha, t, near, far, attach_w=True):
+        o = np.ascontiguousarray(off, np.int64)
+        a, tt = np.ascontiguousarray(alpha, np.float64), np.ascontiguousarray(t, np.float64)
+        R, S = len(o) - 1, int(o[-1])
+        loss, da, dt = np.empty(R), np.zeros(S), np.empty(S)
+        self.lib.sofref_distortion_loss(R, _ptr(o), _ptr(a), _ptr(tt), near, far, int(attach_w), _ptr(loss),
+                                        _ptr(da), _ptr(dt))
+        return {"loss": loss, "d_alpha": da if attach_w else None, "d_t": dt}
+
+    def extent_loss(self, off, w, a, b, c, bound, near, far):
+        o = np.ascontiguousarray(off, np.int64)
+        arrs = [np.ascontiguousarray(x, np.float64) for x in (w, a, b, c, bound)]
+        R, S = len(o) - 1, int(o[-1])
+        loss, skipped = np.empty(R), np.empty(R, np.int32)
+        g = [np.empty(S) for _ in range(4)]
+        self.lib.sofref_extent_loss(R, _ptr(o), *(_ptr(x) for x in arrs), near, far, _ptr(loss), _ptr(skipped),
+                                    *(_ptr(x) for x in g))
+        return {"loss": loss, "skipped": skipped, "d_a": g[0], "d_b": g[1], "d_c": g[2], "d_w": g[3]}
+
+    def depth_normal_loss(self, off, w, normals, pixel_normals):
+        o = np.ascontiguousarray(off, np.int64)
+        ww = np.ascontiguousarray(w, np.float64)
+        nn = np.ascontiguousarray(normals, np.float64).reshape(-1, 3)
+        pn = np.ascontiguousarray(pixel_normals, np.float64).reshape(-1, 3)
+        R, S = len(o) - 1, int(o[-1])
+        loss, dw, dn = np.empty(R), np.empty(S), np.empty((S, 3))
+        self.lib.sofref_depth_normal_loss(R, _ptr(o), _ptr(ww), _ptr(nn), _ptr(pn), _ptr(loss), _ptr(dw), _ptr(dn))
+        return {"loss": loss, "d_w": dw, "d_n": dn}
+
+    def opacity_supervision_loss(self, off, contribs, depth):
+        o = np.ascontiguousarray(off, np.int64)
+        rc = np.ascontiguousarray(contribs, np.float64).reshape(-1, 6)
+        dep = np.ascontiguousarray(depth, np.float64)
+        R, S = len(o) - 1, int(o[-1])
+        loss, fv, defined, da = np.empty(R), np.empty(R), np.empty(R, np.uint8), np.empty(S)
+        self.lib.sofref_opacity_supervision_loss(R, _ptr(o), _ptr(rc), _ptr(dep), _ptr(loss), _ptr(fv),
+                                                 _ptr(defined), _ptr(da))
+        return {"loss": loss, "field_value": fv, "defined": defined.astype(bool), "d_alpha": da}
+
+    def normal_smoothness_loss(self, normals, valid, image, per_channel=False):
+        n = np.ascontiguousarray(normals, np.float64)
+        img = np.ascontiguousarray(image, np.float64)
+        v = np.ascontiguousarray(valid, np.uint8)
+        H, W = v.shape
+        loss, used, dn = np.zeros(1), np.zeros(1, np.int64), np.empty((H, W, 3))
+        self.lib.sofref_normal_smoothness_loss(W, H, _ptr(n), _ptr(v), _ptr(img), int(per_channel), _ptr(loss),
+                                               _ptr(used), _ptr(dn))
+        return {"loss": float(loss[0]), "pixels_used": int(used[0]), "d_normal": dn}
+
+    def l1_rgb_loss(self, rendered, reference):
+        a = np.ascontiguousarray(rendered, np.float64).reshape(-1, 3)
+        b = np.ascontiguousarray(reference, np.float64).reshape(-1, 3)
+        return float(self.lib.sofref_l1_rgb_loss(len(a), _ptr(a), _ptr(b)))
 
 class RefContext:
     """ViewSet::build over (scene, cameras) held by the reference library."""

@@ -11,5 +11,7 @@ from .api import (CameraSet, Context, EvalStrategies, ExtractOptions, FieldEvalu
                   normal_from_depth, normals_to_map, parse_scene, read_float_map, read_mesh_obj, read_mesh_ply,
                   render_depth_map, render_maps, render_view, write_float_map, write_mesh, write_mesh_obj,
                   write_mesh_ply, write_scene)
+from .api import (LossWeights, depth_normal_loss, distortion_loss, extent_loss, l1_rgb_loss, normal_smoothness_loss,
+                  opacity_supervision_loss, total_loss)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -91,6 +91,12 @@ _SIGS = {
     "sof_fp64_peak": (_I, [_P, ctypes.POINTER(_D)]),
     "sof_set_eval_path": (_I, [_P, _I]),
     "sof_set_staging": (_I, [_P, _I]),
+    "sof_distortion_loss": (_I, [_P, _I64, _P, _P, _P, _D, _D, _I, _P, _P, _P]),
+    "sof_extent_loss": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P, _P]),
+    "sof_depth_normal_loss": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "sof_opacity_supervision_loss": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "sof_normal_smoothness_loss": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
+    "sof_l1_rgb_loss": (_I, [_P, _I64, _P, _P, _P]),
     "sof_tets_vertices_dev": (_I, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
     "sof_shard_ext_rank_dev": (_I, [_P, _I64, _P, _I, _I, _P]),
     "sof_shard_mask_min_dev": (_I, [_P, _I64, _P, _I, _P]),

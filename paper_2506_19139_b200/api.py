@@ -665,3 +665,109 @@ def write_scene(scene, path: str, ctx: Context | None = None):
     c = ctx or default_context()
     c.set_scene(scene)
     c.write_scene_ply(path)
+
+
+# ---- training losses (losses.hpp) ------------------------------------------------
+# Batched over rays in CSR form: ray r owns samples [off[r], off[r + 1]). Each returns the
+# reference's per-ray results (losses.hpp names and fields), computed on the device.
+
+def _off(off):
+    o = np.ascontiguousarray(off, np.int64)
+    if o.ndim != 1 or len(o) < 1:
+        raise ValueError("offsets must be a 1-D array of nrays + 1 entries")
+    return o
+
+
+def distortion_loss(ctx: Context, off, alpha, t, near: float, far: float, attach_w: bool = True) -> dict:
+    """distortion_loss (losses.hpp:54-107): loss per ray, d_alpha / d_t per sample."""
+    o = _off(off)
+    a, tt = _f64(alpha), _f64(t)
+    R, S = len(o) - 1, int(o[-1])
+    loss, da, dt = np.empty(R), np.zeros(S), np.empty(S)
+    ctx.check(ctx.lib.sof_distortion_loss(ctx.h, R, _ptr(o), _ptr(a), _ptr(tt), near, far, int(attach_w), _ptr(loss),
+                                          _ptr(da), _ptr(dt)))
+    return {"loss": loss, "d_alpha": da if attach_w else None, "d_t": dt}
+
+
+def extent_loss(ctx: Context, off, w, a, b, c, bound, near: float, far: float) -> dict:
+    """extent_loss (losses.hpp:152-179)."""
+    o = _off(off)
+    arrs = [_f64(x) for x in (w, a, b, c, bound)]
+    R, S = len(o) - 1, int(o[-1])
+    loss, skipped = np.empty(R), np.empty(R, np.int32)
+    g = [np.empty(S) for _ in range(4)]
+    ctx.check(ctx.lib.sof_extent_loss(ctx.h, R, _ptr(o), *(_ptr(x) for x in arrs), near, far, _ptr(loss),
+                                      _ptr(skipped), *(_ptr(x) for x in g)))
+    return {"loss": loss, "skipped": skipped, "d_a": g[0], "d_b": g[1], "d_c": g[2], "d_w": g[3]}
+
+
+def depth_normal_loss(ctx: Context, off, w, normals, pixel_normals) -> dict:
+    """depth_normal_loss (losses.hpp:119-133)."""
+    o = _off(off)
+    ww, nn, pn = _f64(w), _f64(normals, 3), _f64(pixel_normals, 3)
+    R, S = len(o) - 1, int(o[-1])
+    loss, dw, dn = np.empty(R), np.empty(S), np.empty((S, 3))
+    ctx.check(ctx.lib.sof_depth_normal_loss(ctx.h, R, _ptr(o), _ptr(ww), _ptr(nn), _ptr(pn), _ptr(loss), _ptr(dw),
+                                            _ptr(dn)))
+    return {"loss": loss, "d_w": dw, "d_n": dn}
+
+
+def opacity_supervision_loss(ctx: Context, off, contribs, depth) -> dict:
+    """opacity_supervision_loss (losses.hpp:195-229); contribs: (S, 6) = t*, alpha, a, b, c,
+    opacity per sample in each ray's sorted order; depth per ray (NaN = no surface)."""
+    o = _off(off)
+    rc, dep = _f64(contribs, 6), _f64(depth)
+    R, S = len(o) - 1, int(o[-1])
+    loss, fv, defined, da = np.empty(R), np.empty(R), np.empty(R, np.uint8), np.empty(S)
+    ctx.check(ctx.lib.sof_opacity_supervision_loss(ctx.h, R, _ptr(o), _ptr(rc), _ptr(dep), _ptr(loss), _ptr(fv),
+                                                   _ptr(defined), _ptr(da)))
+    return {"loss": loss, "field_value": fv, "defined": defined.astype(bool), "d_alpha": da}
+
+
+def normal_smoothness_loss(ctx: Context, normals, valid, image, per_channel: bool = False) -> dict:
+    """normal_smoothness_loss (losses.hpp:247-293); normals / image (H, W, 3), valid (H, W)."""
+    n = np.ascontiguousarray(normals, np.float64)
+    img = np.ascontiguousarray(image, np.float64)
+    v = np.ascontiguousarray(valid, np.uint8)
+    H, W = v.shape
+    if n.shape != (H, W, 3) or img.shape != (H, W, 3):
+        raise SofError("normal map and image resolution mismatch")
+    loss, used, dn = ctypes.c_double(), ctypes.c_int64(), np.empty((H, W, 3))
+    ctx.check(ctx.lib.sof_normal_smoothness_loss(ctx.h, W, H, _ptr(n), _ptr(v), _ptr(img), int(per_channel),
+                                                 ctypes.byref(loss), ctypes.byref(used), _ptr(dn)))
+    return {"loss": loss.value, "pixels_used": used.value, "d_normal": dn}
+
+
+def l1_rgb_loss(ctx: Context, rendered, reference) -> float:
+    """l1_rgb_loss (losses.hpp:305-312)."""
+    a = _f64(rendered, 3)
+    b = _f64(reference, 3)
+    if a.shape != b.shape:
+        raise SofError("image resolution mismatch")
+    out = ctypes.c_double()
+    ctx.check(ctx.lib.sof_l1_rgb_loss(ctx.h, len(a), _ptr(a), _ptr(b), ctypes.byref(out)))
+    return out.value
+
+
+@dataclass
+class LossWeights:
+    """LossWeights (losses.hpp:12-25)."""
+    lambda_dist_unbounded: float = 100.0
+    lambda_dist_bounded: float = 1000.0
+    lambda_normal: float = 0.05
+    lambda_ext: float = 0.1
+    lambda_opa: float = 0.04
+    lambda_smooth: float = 0.01
+    activation_iteration: int = 15000
+
+    def lambda_dist(self, scene_bounded: bool) -> float:
+        return self.lambda_dist_bounded if scene_bounded else self.lambda_dist_unbounded
+
+
+def total_loss(terms: dict, weights: LossWeights, iteration: int, scene_bounded: bool) -> float:
+    """total_loss (losses.hpp:315-324): auxiliary terms gated by the activation iteration."""
+    if iteration < weights.activation_iteration:
+        return terms["rgb"]
+    return (terms["rgb"] + weights.lambda_dist(scene_bounded) * terms["distortion"] +
+            weights.lambda_normal * terms["normal"] + weights.lambda_ext * terms["extent"] +
+            weights.lambda_opa * terms["opacity"] + weights.lambda_smooth * terms["smoothness"])

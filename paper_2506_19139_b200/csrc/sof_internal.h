@@ -211,6 +211,7 @@ struct sof_ctx {
   sofk::DBuf<int4> rect;
   sofk::DBuf<uint32_t> gcount;
   sofk::DBuf<uint64_t> zkey_in, zkey_out, zkey_aux;
+  sofk::DBuf<char> loss_buf;       // batched training-loss inputs / outputs (k_loss.cu)
   sofk::DBuf<int64_t> bin_scalar;  // [2] selected count | tie-run overflow flag
   int64_t bin_m = 0;               // Gaussians with tiles in the current binning
   sofk::DBuf<int32_t> gidx_in, gidx_out;
