@@ -75,7 +75,15 @@ int sof_ctx_create(int device, sof_ctx** out) {
     SOF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     SOF_CUDA(cudaEventCreate(&c->ev0));
     SOF_CUDA(cudaEventCreate(&c->ev1));
-    SOF_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    {
+      // the prep lane (per-view records + binning for the next view) runs at the highest
+      // priority: its CTAs are dispatched ahead of the evaluation's pending CTAs, so the
+      // next view's lists are ready before the current evaluation drains
+      int lo = 0, hi = 0;
+      SOF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const int prio = std::getenv("SOF_PREP_PRIORITY_OFF") ? lo : hi;
+      SOF_CUDA(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio));
+    }
     SOF_CUDA(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
     SOF_CUDA(cudaEventCreateWithFlags(&c->tets_ev, cudaEventDisableTiming));
     SOF_CUDA(cudaMallocHost(&c->pinned_scalar, 8 * sizeof(uint64_t)));
