@@ -141,7 +141,12 @@ class ShardedMesher:
 
     def _allreduce(self, t, op):
         if self.world > 1:
-            self.dist.all_reduce(t, op=op, group=self.group)
+            if t.is_cuda and self.dist.get_backend(self.group) == "gloo":  # host collective
+                h = t.cpu()
+                self.dist.all_reduce(h, op=op, group=self.group)
+                t.copy_(h)
+            else:
+                self.dist.all_reduce(t, op=op, group=self.group)
             self.b.sync()  # the library runs on its own stream
 
     def _allgather_v(self, t, n):
@@ -149,16 +154,19 @@ class ShardedMesher:
         and the per-rank counts (collectives have no gatherv: pad to the largest)."""
         import torch
         dist = self.dist
-        cnt = torch.tensor([n], dtype=torch.int64, device=t.device)
+        # gloo gathers host tensors only (NCCL gathers device tensors in place)
+        stage = t.is_cuda and dist.get_backend(self.group) == "gloo"
+        dev = torch.device("cpu") if stage else t.device
+        cnt = torch.tensor([n], dtype=torch.int64, device=dev)
         cnts = [torch.zeros_like(cnt) for _ in range(self.world)]
         dist.all_gather(cnts, cnt, group=self.group)
         counts = [int(x.item()) for x in cnts]
-        buf = torch.zeros(max(max(counts), 1), dtype=t.dtype, device=t.device)
-        buf[:n] = t[:n]
+        buf = torch.zeros(max(max(counts), 1), dtype=t.dtype, device=dev)
+        buf[:n] = t[:n].to(dev)
         outs = [torch.empty_like(buf) for _ in range(self.world)]
         dist.all_gather(outs, buf, group=self.group)
         self.b.sync()
-        return torch.cat([o[:k] for o, k in zip(outs, counts)]), counts
+        return torch.cat([o[:k] for o, k in zip(outs, counts)]).to(t.device), counts
 
     def _march(self, n_tets: int):
         """Marching Tetrahedra with the tets split across ranks: rank r marches the r-th
