@@ -83,26 +83,6 @@ __device__ __forceinline__ void tma_issue_rows(void* dst, const CUtensorMap* tma
   if (lane < n4) tma_gather4(static_cast<char*>(dst) + size_t(lane) * 4 * row_bytes, tmap, r0, r1, r2, r3, bar);
 }
 
-// 1D bulk copy (no tensor map): `bytes` from global src to shared dst, completion on bar.
-__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// Warp-level issue of one chunk with per-lane 1D bulk copies of one row each.
-__device__ __forceinline__ void bulk_issue_rows(void* dst, const char* base, int my_row, int cnt, uint64_t* bar,
-                                                uint32_t row_bytes) {
-  const int lane = threadIdx.x & 31;
-  if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(cnt) * row_bytes);
-  __syncwarp();
-  if (lane < cnt)
-    bulk_copy_g2s(static_cast<char*>(dst) + size_t(lane) * row_bytes, base + size_t(my_row) * row_bytes, row_bytes,
-                  bar);
-}
-
 }  // namespace sofk
 
 // Host: a {16 x 8 B, rows} tensor map over a record array (128-B rows).
