@@ -785,4 +785,196 @@ inline void write_mesh_ply(const Mesh& mesh, const std::string& path) {
   }
 }
 
+
+// ---- training losses (losses.hpp), evaluated on the device --------------
+// Same types and signatures as the reference; each call is one ray / one image of the
+// batched C-ABI entry points (sof_*_loss), bit-identical to the reference.
+
+// losses.hpp:12-25
+struct LossWeights {
+  double lambda_dist_unbounded = 100.0;
+  double lambda_dist_bounded = 1000.0;
+  double lambda_normal = 0.05;
+  double lambda_ext = 0.1;
+  double lambda_opa = 0.04;
+  double lambda_smooth = 0.01;
+  int activation_iteration = 15000;
+  double lambda_dist(bool scene_bounded) const { return scene_bounded ? lambda_dist_bounded : lambda_dist_unbounded; }
+};
+
+// opacity_field.hpp:13-19
+struct RayContribution {
+  int gaussian_index = -1;
+  double t_star = 0.0;
+  double alpha = 0.0;
+  double a = 0.0, b = 0.0, c = 0.0;
+  double opacity = 0.0;
+};
+
+struct DistortionSample {  // losses.hpp:44-47
+  double alpha = 0.0;
+  double t = 0.0;
+};
+struct DistortionResult {  // losses.hpp:49-53
+  double loss = 0.0;
+  std::vector<double> d_alpha;
+  std::vector<double> d_t;
+};
+
+inline DistortionResult distortion_loss(const std::vector<DistortionSample>& samples, double near, double far,
+                                        bool attach_w = true) {
+  const size_t n = samples.size();
+  std::vector<double> a(n), t(n);
+  for (size_t i = 0; i < n; ++i) {
+    a[i] = samples[i].alpha;
+    t[i] = samples[i].t;
+  }
+  const int64_t off[2] = {0, int64_t(n)};
+  DistortionResult out;
+  out.d_t.assign(n, 0.0);
+  if (attach_w) out.d_alpha.assign(n, 0.0);
+  sof_ctx* c = detail::default_ctx().get();
+  detail::check(c, sof_distortion_loss(c, 1, off, a.data(), t.data(), near, far, attach_w ? 1 : 0, &out.loss,
+                                       attach_w ? out.d_alpha.data() : nullptr, out.d_t.data()));
+  return out;
+}
+
+struct DepthNormalResult {  // losses.hpp:113-117
+  double loss = 0.0;
+  std::vector<double> d_w;
+  std::vector<Vec3> d_n;
+};
+
+inline DepthNormalResult depth_normal_loss(const std::vector<double>& w, const std::vector<Vec3>& normals,
+                                           const Vec3& pixel_normal) {
+  const size_t n = w.size();
+  const std::vector<double> nf = detail::flat(normals);
+  const double pn[3] = {pixel_normal(0), pixel_normal(1), pixel_normal(2)};
+  const int64_t off[2] = {0, int64_t(n)};
+  DepthNormalResult out;
+  out.d_w.assign(n, 0.0);
+  std::vector<double> dn(3 * n);
+  sof_ctx* c = detail::default_ctx().get();
+  detail::check(c, sof_depth_normal_loss(c, 1, off, w.data(), nf.data(), pn, &out.loss, out.d_w.data(), dn.data()));
+  out.d_n = detail::unflat(dn);
+  return out;
+}
+
+struct ExtentSample {  // losses.hpp:141-145
+  double w = 0.0;
+  double a = 0.0, b = 0.0, c = 0.0;
+  double bound = 0.0;
+};
+struct ExtentResult {  // losses.hpp:147-151
+  double loss = 0.0;
+  std::vector<double> d_a, d_b, d_c, d_w;
+  int skipped = 0;
+};
+
+inline ExtentResult extent_loss(const std::vector<ExtentSample>& samples, double near, double far) {
+  const size_t n = samples.size();
+  std::vector<double> w(n), a(n), b(n), cc(n), e(n);
+  for (size_t i = 0; i < n; ++i) {
+    w[i] = samples[i].w;
+    a[i] = samples[i].a;
+    b[i] = samples[i].b;
+    cc[i] = samples[i].c;
+    e[i] = samples[i].bound;
+  }
+  const int64_t off[2] = {0, int64_t(n)};
+  ExtentResult out;
+  out.d_a.assign(n, 0.0);
+  out.d_b.assign(n, 0.0);
+  out.d_c.assign(n, 0.0);
+  out.d_w.assign(n, 0.0);
+  int32_t skipped = 0;
+  sof_ctx* c = detail::default_ctx().get();
+  detail::check(c, sof_extent_loss(c, 1, off, w.data(), a.data(), b.data(), cc.data(), e.data(), near, far,
+                                   &out.loss, &skipped, out.d_a.data(), out.d_b.data(), out.d_c.data(),
+                                   out.d_w.data()));
+  out.skipped = skipped;
+  return out;
+}
+
+struct OpacitySupervisionResult {  // losses.hpp:188-193
+  double loss = 0.0;
+  double field_value = 0.0;
+  bool defined = false;
+  std::vector<double> d_alpha;
+};
+
+inline OpacitySupervisionResult opacity_supervision_loss(const std::vector<RayContribution>& contribs,
+                                                         double depth) {
+  const size_t n = contribs.size();
+  std::vector<double> rc(6 * n);
+  for (size_t i = 0; i < n; ++i) {
+    const RayContribution& r = contribs[i];
+    const double v[6] = {r.t_star, r.alpha, r.a, r.b, r.c, r.opacity};
+    for (int k = 0; k < 6; ++k) rc[6 * i + k] = v[k];
+  }
+  const int64_t off[2] = {0, int64_t(n)};
+  OpacitySupervisionResult out;
+  std::vector<double> da(n, 0.0);
+  uint8_t defined = 0;
+  sof_ctx* c = detail::default_ctx().get();
+  detail::check(c, sof_opacity_supervision_loss(c, 1, off, rc.data(), &depth, &out.loss, &out.field_value,
+                                                &defined, da.data()));
+  out.defined = defined != 0;
+  if (out.defined) out.d_alpha = da;  // the reference fills d_alpha only for a defined loss
+  return out;
+}
+
+enum class ImageGradientMode { kLuminance, kPerChannel };  // losses.hpp:235
+
+struct NormalSmoothnessResult {  // losses.hpp:237-241
+  double loss = 0.0;
+  Grid2D<Vec3> d_normal;
+  int pixels_used = 0;
+};
+
+inline NormalSmoothnessResult normal_smoothness_loss(const NormalMap& normals, const Grid2D<Vec3>& image,
+                                                     ImageGradientMode mode = ImageGradientMode::kLuminance) {
+  if (normals.normal.width != image.width || normals.normal.height != image.height)
+    throw std::invalid_argument("normal map and image resolution mismatch");
+  const std::vector<double> nf = detail::flat(normals.normal.data), imf = detail::flat(image.data);
+  NormalSmoothnessResult out;
+  std::vector<double> dn(nf.size());
+  int64_t used = 0;
+  sof_ctx* c = detail::default_ctx().get();
+  detail::check(c, sof_normal_smoothness_loss(c, image.width, image.height, nf.data(), normals.valid.data.data(),
+                                              imf.data(), mode == ImageGradientMode::kPerChannel ? 1 : 0,
+                                              &out.loss, &used, dn.data()));
+  out.pixels_used = int(used);
+  out.d_normal = Grid2D<Vec3>(image.width, image.height, Vec3::Zero());
+  out.d_normal.data = detail::unflat(dn);
+  return out;
+}
+
+struct LossTerms {  // losses.hpp:297-304
+  double rgb = 0.0;
+  double distortion = 0.0;
+  double normal = 0.0;
+  double extent = 0.0;
+  double opacity = 0.0;
+  double smoothness = 0.0;
+};
+
+inline double l1_rgb_loss(const Grid2D<Vec3>& rendered, const Grid2D<Vec3>& reference) {
+  if (rendered.width != reference.width || rendered.height != reference.height)
+    throw std::invalid_argument("image resolution mismatch");
+  const std::vector<double> a = detail::flat(rendered.data), b = detail::flat(reference.data);
+  double loss = 0.0;
+  sof_ctx* c = detail::default_ctx().get();
+  detail::check(c, sof_l1_rgb_loss(c, int64_t(rendered.data.size()), a.data(), b.data(), &loss));
+  return loss;
+}
+
+// total_loss (losses.hpp:315-324): the weighted sum of already evaluated terms
+inline double total_loss(const LossTerms& terms, const LossWeights& weights, int iteration, bool scene_bounded) {
+  if (iteration < weights.activation_iteration) return terms.rgb;
+  return terms.rgb + weights.lambda_dist(scene_bounded) * terms.distortion + weights.lambda_normal * terms.normal +
+         weights.lambda_ext * terms.extent + weights.lambda_opa * terms.opacity +
+         weights.lambda_smooth * terms.smoothness;
+}
+
 }  // namespace sof

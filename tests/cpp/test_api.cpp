@@ -271,3 +271,108 @@ TEST(Errors, NonFiniteScene) {
   g.position = Vec3(0, std::nan(""), 0);
   EXPECT_THROW(ViewSet::build({g}, {Camera{}}), std::invalid_argument);
 }
+
+// ---- training losses: the reference's tests/test_losses.cpp cases ----------------
+
+namespace {
+double ndc_inverse(double d, double near, double far) { return far * near / (far - d * (far - near)); }
+}  // namespace
+
+TEST(Distortion, ConstantDepthIsZero) {
+  const double t = ndc_inverse(0.5, 0.2, 100.0);
+  const auto res = distortion_loss({{0.3, t}, {0.4, t}, {0.2, t}}, 0.2, 100.0);
+  EXPECT_NEAR(res.loss, 0.0, 1e-15);
+  for (double g : res.d_t) EXPECT_NEAR(g, 0.0, 1e-12);
+}
+
+TEST(Distortion, TwoSampleExample) {
+  const double t1 = ndc_inverse(0.2, 0.2, 100.0);
+  const double t2 = ndc_inverse(0.8, 0.2, 100.0);
+  const auto res = distortion_loss({{0.5, t1}, {1.0, t2}}, 0.2, 100.0);
+  EXPECT_NEAR(res.loss, 0.18, 1e-12);
+}
+
+TEST(Distortion, DetachFlagDropsAlphaGradients) {
+  const auto res = distortion_loss({{0.5, 1.0}, {0.5, 2.0}}, 0.2, 100.0, false);
+  EXPECT_TRUE(res.d_alpha.empty());
+  EXPECT_EQ(res.d_t.size(), 2u);
+}
+
+TEST(DepthNormal, Examples) {
+  const Vec3 N(0, 0, 1);
+  EXPECT_NEAR(depth_normal_loss({1.0}, {N}, N).loss, 0.0, 1e-15);
+  EXPECT_NEAR(depth_normal_loss({1.0}, {Vec3(0, 0, -1)}, N).loss, 2.0, 1e-12);
+  EXPECT_NEAR(depth_normal_loss({0.5, 0.25}, {N, Vec3(1, 0, 0)}, N).loss, 0.25, 1e-12);
+}
+
+TEST(Extent, PlugInExample) {
+  ExtentSample s;
+  s.w = 1.0;
+  s.a = 1.0;
+  s.b = -10.0;
+  s.c = 25.0;
+  s.bound = std::sqrt(2.0 * std::log(255.0));  // tight_bound(1.0)
+  const auto res = extent_loss({s}, 0.2, 100.0);
+  EXPECT_EQ(res.skipped, 0);
+  EXPECT_NEAR(res.loss, 0.026686, 1e-5);
+}
+
+TEST(Extent, EmptyVisibleSegmentSkipped) {
+  ExtentSample s;
+  s.w = 1.0;
+  s.a = 1.0;
+  s.b = -10.0;
+  s.c = 25.0;
+  s.bound = 0.0;
+  const auto res = extent_loss({s}, 0.2, 100.0);
+  EXPECT_EQ(res.skipped, 1);
+  EXPECT_NEAR(res.loss, 0.0, 1e-15);
+}
+
+TEST(OpacitySupervision, NoSurfaceIsZero) {
+  RayContribution rc;  // tu::flat_contribution(0.2, 3.0)
+  rc.gaussian_index = 0;
+  rc.t_star = 3.0;
+  rc.alpha = 0.2;
+  rc.a = 1.0;
+  rc.b = -6.0;
+  rc.c = 9.0;
+  rc.opacity = 0.2;
+  const auto res = opacity_supervision_loss({rc}, kNoSurface);
+  EXPECT_FALSE(res.defined);
+  EXPECT_DOUBLE_EQ(res.loss, 0.0);
+}
+
+TEST(NormalSmoothness, ConstantMapIsZero) {
+  NormalMap nm;
+  nm.normal = Grid2D<Vec3>(8, 8, Vec3(0, 0, -1));
+  nm.valid = Grid2D<unsigned char>(8, 8, 1);
+  const Grid2D<Vec3> image(8, 8, Vec3(0.5, 0.5, 0.5));
+  EXPECT_NEAR(normal_smoothness_loss(nm, image).loss, 0.0, 1e-15);
+}
+
+TEST(NormalSmoothness, FlatImageEqualsTotalVariation) {
+  NormalMap nm;
+  nm.normal = Grid2D<Vec3>(4, 4, Vec3(0, 0, -1));
+  nm.valid = Grid2D<unsigned char>(4, 4, 1);
+  for (int y = 0; y < 4; ++y)
+    for (int x = 2; x < 4; ++x) nm.normal.at(x, y) = Vec3(0, 0, 1);
+  const Grid2D<Vec3> image(4, 4, Vec3(0.5, 0.5, 0.5));
+  EXPECT_NEAR(normal_smoothness_loss(nm, image).loss, 3.0 * 2.0 / 9.0, 1e-12);
+}
+
+TEST(TotalLoss, GatingAndWeights) {
+  LossWeights w;
+  LossTerms terms;
+  terms.rgb = 0.5;
+  terms.distortion = terms.normal = terms.extent = terms.opacity = terms.smoothness = 1.0;
+  EXPECT_DOUBLE_EQ(total_loss(terms, w, 14999, false), 0.5);
+  EXPECT_DOUBLE_EQ(total_loss(terms, w, 15000, false), 0.5 + 100.0 + 0.05 + 0.1 + 0.04 + 0.01);
+  EXPECT_DOUBLE_EQ(total_loss(terms, w, 15000, true), 0.5 + 1000.0 + 0.05 + 0.1 + 0.04 + 0.01);
+}
+
+TEST(L1Rgb, MeanAbsoluteError) {
+  Grid2D<Vec3> a(2, 1, Vec3(0.5, 0.5, 0.5));
+  Grid2D<Vec3> b(2, 1, Vec3(0.25, 0.5, 0.5));
+  EXPECT_NEAR(l1_rgb_loss(a, b), 0.25 * 2 / 6.0, 1e-12);
+}
