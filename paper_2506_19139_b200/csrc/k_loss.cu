@@ -302,6 +302,10 @@ size_t pad(size_t b) { return (b + 255) & ~size_t(255); }
 
 void sync(sof_ctx* c) { SOF_CUDA(cudaStreamSynchronize(c->stream)); }
 
+void need(bool ok, const char* what) {
+  if (!ok) throw InvalidArg(what);
+}
+
 void check_off(int64_t nrays, const int64_t* off) {
   if (nrays < 0 || (nrays > 0 && !off)) throw InvalidArg("invalid ray offsets");
   if (nrays > 0 && off[0] != 0) throw InvalidArg("ray offsets must start at 0");
@@ -320,6 +324,7 @@ int sof_distortion_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const dou
     check_off(nrays, off);
     if (!(far_plane > near_plane)) throw InvalidArg("far must exceed near");
     const int64_t S = nrays ? off[nrays] : 0;
+    need(S == 0 || (alpha && t), "null sample arrays");
     c->loss_buf.ensure(pad(8 * (nrays + 1)) + pad(8 * size_t(S)) * 7 + pad(8 * nrays) + 4096);
     size_t at = 0;
     int64_t* doff = dev_copy(c, c->loss_buf, at, off, nrays + 1);
@@ -349,6 +354,7 @@ int sof_extent_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const double*
   return guard(c, [&] {
     check_off(nrays, off);
     const int64_t S = nrays ? off[nrays] : 0;
+    need(S == 0 || (w && a && b && cc && bound), "null sample arrays");
     c->loss_buf.ensure(pad(8 * (nrays + 1)) + pad(8 * size_t(S)) * 9 + pad(8 * nrays) + pad(4 * nrays) + 4096);
     size_t at = 0;
     int64_t* doff = dev_copy(c, c->loss_buf, at, off, nrays + 1);
@@ -383,6 +389,8 @@ int sof_depth_normal_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const d
   return guard(c, [&] {
     check_off(nrays, off);
     const int64_t S = nrays ? off[nrays] : 0;
+    need(S == 0 || (w && normals), "null sample arrays");
+    need(nrays == 0 || pixel_normals, "null pixel normals");
     c->loss_buf.ensure(pad(8 * (nrays + 1)) + pad(8 * size_t(S)) * 8 + pad(24 * nrays) + pad(8 * nrays) + 4096);
     size_t at = 0;
     int64_t* doff = dev_copy(c, c->loss_buf, at, off, nrays + 1);
@@ -409,6 +417,8 @@ int sof_opacity_supervision_loss(sof_ctx* c, int64_t nrays, const int64_t* off, 
   return guard(c, [&] {
     check_off(nrays, off);
     const int64_t S = nrays ? off[nrays] : 0;
+    need(S == 0 || contribs, "null contributions");
+    need(nrays == 0 || depth, "null depths");
     c->loss_buf.ensure(pad(8 * (nrays + 1)) + pad(48 * size_t(S)) + pad(8 * size_t(S)) + pad(8 * nrays) * 3 +
                        pad(nrays) + 4096);
     size_t at = 0;
@@ -437,6 +447,7 @@ int sof_normal_smoothness_loss(sof_ctx* c, int width, int height, const double* 
   return guard(c, [&] {
     if (width < 0 || height < 0) throw InvalidArg("invalid image size");
     const int64_t P = int64_t(width) * height;
+    need(P == 0 || (normals && valid && image), "null maps");
     c->loss_buf.ensure(pad(24 * size_t(P)) * 5 + pad(8 * size_t(P)) + pad(size_t(P)) * 2 + 4096);
     size_t at = 0;
     double* dn = dev_copy(c, c->loss_buf, at, normals, 3 * P);
