@@ -244,7 +244,9 @@ int sof_extract(sof_ctx* ctx, const sof_extract_opts* opts, sof_extract_stats* s
 void sof_extract_opts_default(sof_extract_opts* opts);
 
 /* ---- utilities ---------------------------------------------------------------------- */
-/* device-side check that 0 <= tets_dev[i] < nv for all 4*nt indices */
+/* device-side check that 0 <= tets_dev[i] < nv for all 4*nt indices (tets_dev: a
+ * 16-byte aligned device array, as cudaMalloc returns; SOF_E_INVALID when it is not or an
+ * index is out of range) */
 int sof_validate_tets_dev(sof_ctx* ctx, int64_t nt, const int32_t* tets_dev, int64_t nv);
 /* CUDA events on the context's stream (slots 0..7) for device-side timing */
 int sof_event_record(sof_ctx* ctx, int slot);

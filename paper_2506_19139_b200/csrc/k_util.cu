@@ -39,13 +39,15 @@ int sof_make_row_tmap(CUtensorMap* out, const void* base, int64_t rows) {
 
 namespace sofk {
 
-__global__ void k_check_index(int64_t n, const int32_t* __restrict__ idx, int32_t bound,
-                              int32_t* bad) {
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) {
-    const int32_t v = idx[i];
-    if (v < 0 || v >= bound) atomicExch(bad, 1);
+// Tet index range check, one 16-B tet per load, one flag write per warp at most.
+__global__ void k_check_tets(int64_t nt, const int4* __restrict__ tets, int32_t bound, int32_t* bad) {
+  bool b = false;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < nt; t += int64_t(gridDim.x) * blockDim.x) {
+    const int4 q = tets[t];
+    b |= (unsigned(q.x) >= unsigned(bound)) | (unsigned(q.y) >= unsigned(bound)) | (unsigned(q.z) >= unsigned(bound)) |
+         (unsigned(q.w) >= unsigned(bound));
   }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
 }
 
 // Each thread runs 8 independent DFMA chains; 2 FLOP per DFMA.
@@ -131,7 +133,8 @@ void prof_collect(sof_ctx* c, double* ms) {
 
 void check_tet_indices(sof_ctx* c, cudaStream_t st, int64_t nt, const int32_t* tets_dev, int64_t nv,
                        int32_t* bad) {
-  k_check_index<<<grid_for(4 * nt, 256), 256, 0, st>>>(4 * nt, tets_dev, int32_t(nv), bad);
+  k_check_tets<<<std::min<int64_t>(grid_for(nt, 256), 148 * 16), 256, 0, st>>>(
+      nt, reinterpret_cast<const int4*>(tets_dev), int32_t(nv), bad);
   SOF_LAUNCHED(c);
 }
 
@@ -174,12 +177,17 @@ extern "C" {
 
 int sof_validate_tets_dev(sof_ctx* c, int64_t nt, const int32_t* tets_dev, int64_t nv) {
   if (!c) return SOF_E_INVALID;
+  if (nt > 0 && (!tets_dev || (reinterpret_cast<uintptr_t>(tets_dev) & 15))) {
+    c->err = "tets_dev must be a 16-byte aligned device array of 4 * nt indices";
+    return SOF_E_INVALID;
+  }
   try {
     DBuf<int32_t>& bad = c->ms.nsel;
     bad.ensure(1);
     zero_async(c, bad.p, 4);
     if (nt > 0) {
-      k_check_index<<<grid_for(4 * nt, 256), 256, 0, c->stream>>>(4 * nt, tets_dev, int32_t(nv), bad.p);
+      k_check_tets<<<std::min<int64_t>(grid_for(nt, 256), 148 * 16), 256, 0, c->stream>>>(
+          nt, reinterpret_cast<const int4*>(tets_dev), int32_t(nv), bad.p);
       SOF_LAUNCHED(c);
     }
     return read_scalar(c, bad.p) ? SOF_E_INVALID : SOF_OK;
