@@ -348,6 +348,46 @@ __global__ void k_gather_keys(int64_t n, const int32_t* __restrict__ perm, const
   if (j < n) dst[j] = src[perm[j]];
 }
 
+// Bisection-cache binning (bisect_cache_views): a Gaussian enters tile t only when
+// t is reachable by a crossing-edge segment and its min_z <= zmax(t) (ordered keys),
+// i.e. exactly the entries of the full list's prefix that the bisection can read.
+__device__ __forceinline__ bool tile_wanted(const unsigned long long* zmax, int64_t t, unsigned long long zk) {
+  return zmax[t] >= zk;  // zmax 0: no segment reaches t (every key is >= 1)
+}
+
+__global__ void k_filter_counts(int64_t n, const int4* __restrict__ rect, const uint64_t* __restrict__ zkey,
+                                const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* cnt) {
+  const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (g >= n || cnt[g] == 0) return;
+  const int4 rc = rect[g];
+  const unsigned long long zk = zkey[g];
+  uint32_t k = 0;
+  for (int ty = rc.z; ty <= rc.w; ++ty)
+    for (int tx = rc.x; tx <= rc.y; ++tx) k += tile_wanted(zmax, int64_t(ty) * tiles_x + tx, zk);
+  cnt[g] = k;
+}
+
+__global__ void k_emit_filtered(int64_t n, const int32_t* __restrict__ order, const int4* __restrict__ rect,
+                                const int64_t* __restrict__ off, const uint64_t* __restrict__ zkey,
+                                const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* keys,
+                                int32_t* vals) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  const int32_t g = order[r];
+  const int4 rc = rect[g];
+  const unsigned long long zk = zkey[g];
+  int64_t o = off[r];
+  for (int ty = rc.z; ty <= rc.w; ++ty)
+    for (int tx = rc.x; tx <= rc.y; ++tx) {
+      const int64_t t = int64_t(ty) * tiles_x + tx;
+      if (tile_wanted(zmax, t, zk)) {
+        keys[o] = uint32_t(t);
+        vals[o] = g;
+        ++o;
+      }
+    }
+}
+
 struct HasTiles {
   const uint32_t* cnt;
   __device__ bool operator()(int32_t i) const { return cnt[i] != 0; }
@@ -422,6 +462,11 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
                 bool charge_cache) {
   const int64_t T = int64_t(tiles_x) * tiles_y;
   const int64_t n = c->n;
+  if (c->bin_zmax) {  // bisection-cache binning: only the reachable (tile, depth) entries
+    k_filter_counts<<<grid_for(n, 256), 256, 0, c->stream>>>(n, c->rect.p, c->zkey_in.p, c->bin_zmax, tiles_x,
+                                                             c->gcount.p);
+    SOF_LAUNCHED(c);
+  }
   // visible Gaussians in index order -> gidx_in[0, m)
   c->bin_scalar.ensure(2);
   {
@@ -487,8 +532,13 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
     c->ekey_in.ensure(M);
     c->ekey_out.ensure(M);
     c->eval_in.ensure(M);
-    k_emit_entries<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(
-        c->bin_m, c->gidx_out.p, c->rect.p, c->gcount.p, c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p);
+    if (c->bin_zmax)
+      k_emit_filtered<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(c->bin_m, c->gidx_out.p, c->rect.p, c->goff.p,
+                                                                       c->zkey_in.p, c->bin_zmax, tiles_x,
+                                                                       c->ekey_in.p, c->eval_in.p);
+    else
+      k_emit_entries<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(
+          c->bin_m, c->gidx_out.p, c->rect.p, c->gcount.p, c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p);
     SOF_LAUNCHED(c);
     // stable sort by tile keeps the (min_z, index) order inside every tile list
     sort_pairs_u32(c, c->ekey_in.p, c->ekey_out.p, c->eval_in.p, b.ent.p, M, bits_for(T));
@@ -1491,20 +1541,30 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
   DBuf<uint8_t> used;
   DBuf<int32_t> flag, pos;
   DBuf<int> bail;
+  size_t free_b = size_t(-1);
   const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
   const auto h0 = std::chrono::steady_clock::now();
   int n_res = 0, n_trunc = 0, n_bail = 0, n_alias = 0;
+  double ph[4] = {0, 0, 0, 0};  // debug: host ms in zmax, binning, truncation, memory check
+  auto tick = [&]() { return std::chrono::steady_clock::now(); };
+  auto ms_since = [&](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(tick() - t).count();
+  };
   struct Report {  // debug summary on every exit path
     bool on;
     const int *res, *trunc, *bail, *alias;
     std::chrono::steady_clock::time_point t0;
+    const double* ph;
     ~Report() {
       if (on)
-        std::fprintf(stderr, "bisect_cache_views: resident %d truncated %d bailed %d full %d, %.1f ms\n", *res,
-                     *trunc, *bail, *alias,
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        std::fprintf(stderr,
+                     "bisect_cache_views: resident %d truncated %d bailed %d full %d, %.1f ms (zmax %.1f, binning %.1f, "
+                     "truncation %.1f, memory %.1f)\n",
+                     *res, *trunc, *bail, *alias,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), ph[0],
+                     ph[1], ph[2], ph[3]);
     }
-  } report{dbg, &n_res, &n_trunc, &n_bail, &n_alias, h0};
+  } report{dbg, &n_res, &n_trunc, &n_bail, &n_alias, h0, ph};
   for (int v = v0; v < v1; ++v) {
     if (view_resident(c, v, tile_size)) {
       ++n_res;
@@ -1514,6 +1574,7 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     const int tiles_x = (cam.w + tile_size - 1) / tile_size, tiles_y = (cam.h + tile_size - 1) / tile_size;
     const int64_t T = int64_t(tiles_x) * tiles_y;
     // tiles and depths the midpoints can reach (needs no records)
+    auto t0 = tick();
     zmax.ensure(T);
     bail.ensure(1);
     zero_async(c, zmax.p, sizeof(unsigned long long) * T);
@@ -1521,16 +1582,33 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     k_segment_zmax<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, edges, c->tv.p, cam, tile_size, tiles_x, tiles_y,
                                                              zmax.p, bail.p);
     SOF_LAUNCHED(c);
-    if (read_scalar(c, bail.p)) {  // this view keeps the per-view path
+    const bool bailed = read_scalar(c, bail.p);
+    ph[0] += ms_since(t0);
+    t0 = tick();
+    if (bailed) {  // this view keeps the per-view path
       ++n_bail;
       continue;
     }
-    // full live lists + records of the view (scratch slot), then the truncation
-    const Binding& full = view_binding(c, v, tile_size, true);
+    // the view's records and its lists restricted to the reachable (tile, depth)
+    // entries, built in the scratch slot, then compacted below
+    Binding& full = c->bind_scratch[c->scratch_sel];
+    c->bin_zmax = zmax.p;
+    try {
+      build_binding(c, v, tile_size, true, full, false);
+    } catch (...) {
+      c->bin_zmax = nullptr;
+      full.view = -1;
+      throw;
+    }
+    c->bin_zmax = nullptr;
+    full.view = -1;  // a filtered binding is never served as the view's lists
     const Rec* rec = view_records(c, v);
-    // the budget had room after all: the view is cached in full (or half of it is, and
-    // the per-view path serves it); never truncate into the buffers being read
-    if (&full == &c->bindings[v] || rec == c->recs[v].p) {
+    if (dbg) SOF_CUDA(cudaStreamSynchronize(c->stream));
+    ph[1] += ms_since(t0);
+    t0 = tick();
+    // the budget had room after all: the records are cached in full (the per-view path
+    // serves the view); never truncate into the buffers being read
+    if (rec == c->recs[v].p) {
       ++n_alias;
       continue;
     }
@@ -1557,19 +1635,29 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     exclusive_scan_i32(c, flag.p, pos.p, n + 1);
     const int64_t L = read_scalar(c, toff.p + T);
     const int64_t R = read_scalar(c, pos.p + n);
-    // room for it? (the full caches of the resident views stay; leave headroom)
-    size_t free_b = 0, total_b = 0;
-    SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    ph[2] += ms_since(t0);
+    t0 = tick();
+    // room for it? (the full caches of the resident views stay; leave headroom). Free
+    // memory is queried once per call and tracked across the views' new allocations.
+    if (free_b == size_t(-1)) {
+      size_t total_b = 0;
+      SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    }
     const size_t need = size_t(R) * sizeof(Rec) + size_t(L) * 4 + size_t(T + 1) * 8;
     Binding& b = c->bindings[v];
     const size_t have = c->recs[v].bytes() + b.ent.bytes() + b.off.bytes();
-    if (need > have && need - have + (size_t(2) << 30) > free_b) {  // out of memory: per-view path from here
-      if (std::getenv("SOF_DEBUG_HOST"))
-        std::fprintf(stderr, "bisect_cache_views: out of memory at view %d (free %.1f GB, need %.2f GB)\n", v,
-                     free_b / 1e9, need / 1e9);
-      break;
+    if (need > have) {
+      if (need - have + (size_t(2) << 30) > free_b) {  // out of memory: per-view path from here
+        if (std::getenv("SOF_DEBUG_HOST"))
+          std::fprintf(stderr, "bisect_cache_views: out of memory at view %d (free %.1f GB, need %.2f GB)\n", v,
+                       free_b / 1e9, need / 1e9);
+        break;
+      }
+      free_b -= need;  // upper bound of what the ensures below allocate
     }
     c->recs[v].ensure(std::max<int64_t>(R, 1));
+    ph[3] += ms_since(t0);
+    t0 = tick();
     k_trunc_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(n, used.p, pos.p, rec, c->recs[v].p);
     SOF_LAUNCHED(c);
     b.off.ensure(T + 1);
@@ -1588,6 +1676,7 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     c->rec_valid[v] = 2;
     ++n_trunc;
     SOF_CUDA(cudaStreamSynchronize(c->stream));  // the scratch slot is reused by the next view
+    ph[2] += ms_since(t0);
   }
 }
 

@@ -214,6 +214,7 @@ struct sof_ctx {
   sofk::DBuf<char> loss_buf;       // batched training-loss inputs / outputs (k_loss.cu)
   sofk::DBuf<int64_t> bin_scalar;  // [2] selected count | tie-run overflow flag
   int64_t bin_m = 0;               // Gaussians with tiles in the current binning
+  const unsigned long long* bin_zmax = nullptr;  // bisection-cache binning filter (per tile)
   sofk::DBuf<int32_t> gidx_in, gidx_out;
   sofk::DBuf<int64_t> goff;
   sofk::DBuf<uint32_t> ekey_in, ekey_out;
