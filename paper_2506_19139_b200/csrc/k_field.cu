@@ -1111,7 +1111,10 @@ __global__ void k_fill_view_outputs(int64_t n, double* o, uint8_t* obs, uint8_t*
 // matter. Items evaluated after a point's first exterior view are wasted work only
 // (a few percent: interior midpoints are evaluated in every view anyway).
 
-constexpr int kGroupViews = 32;
+#ifndef SOF_GROUP_VIEWS
+#define SOF_GROUP_VIEWS 32
+#endif
+constexpr int kGroupViews = SOF_GROUP_VIEWS;  // views scheduled and evaluated per grouped launch
 
 struct GroupTables {
   int g0, G;
