@@ -1539,11 +1539,12 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
   if (!fast_loop(c, strategies) || ne <= 0 || c->n <= 0 || std::getenv("SOF_NO_BISECT_CACHE")) return;
   if (!c->has_tets) return;
   const int64_t n = c->n;
-  DBuf<unsigned long long> zmax;
-  DBuf<int64_t> len, toff;
-  DBuf<uint8_t> used;
-  DBuf<int32_t> flag, pos;
-  DBuf<int> bail;
+  BisectScratch& bs = c->bis;  // kept across calls (no per-refine allocations)
+  DBuf<unsigned long long>& zmax = bs.zmax;
+  DBuf<int64_t>&len = bs.len, &toff = bs.toff;
+  DBuf<uint8_t>& used = bs.used;
+  DBuf<int32_t>&flag = bs.flag, &pos = bs.pos;
+  DBuf<int>& bail = bs.bail;
   size_t free_b = size_t(-1);
   const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
   const auto h0 = std::chrono::steady_clock::now();

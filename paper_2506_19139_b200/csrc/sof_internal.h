@@ -138,6 +138,15 @@ struct GroupScratch {
   DBuf<uint8_t> item_ext;         // [G n]
 };
 
+// Scratch of bisect_cache_views (per-tile zmax, truncated list offsets, row maps).
+struct BisectScratch {
+  DBuf<unsigned long long> zmax;
+  DBuf<int64_t> len, toff;
+  DBuf<uint8_t> used;
+  DBuf<int32_t> flag, pos;
+  DBuf<int> bail;
+};
+
 struct RenderScratch {
   DBuf<uint64_t> keys, keys2;
   DBuf<double> alpha, alpha2;
@@ -215,6 +224,7 @@ struct sof_ctx {
   sofk::DBuf<int64_t> bin_scalar;  // [2] selected count | tie-run overflow flag
   int64_t bin_m = 0;               // Gaussians with tiles in the current binning
   const unsigned long long* bin_zmax = nullptr;  // bisection-cache binning filter (per tile)
+  sofk::BisectScratch bis;
   sofk::DBuf<int32_t> gidx_in, gidx_out;
   sofk::DBuf<int64_t> goff;
   sofk::DBuf<uint32_t> ekey_in, ekey_out;
