@@ -694,10 +694,9 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     SOF_CUDA(cudaMemsetAsync(c->r_stats.p, 0, 4 * sizeof(unsigned long long), c->stream));
     const size_t smem = kRChunk * (sizeof(Rec) + sizeof(double) + sizeof(int32_t)) +
                         size_t(kKBuf) * 256 * (2 * sizeof(double) + sizeof(int32_t));
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (!c->render_attr_set) {  // a per-device function attribute: set once per context
       SOF_CUDA(cudaFuncSetAttribute(k_render, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr_set = true;
+      c->render_attr_set = true;
     }
     int64_t nover_total = 0;
     for (int64_t t0 = 0; t0 < T;) {

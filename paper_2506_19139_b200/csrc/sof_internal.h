@@ -225,6 +225,7 @@ struct sof_ctx {
   int64_t bin_m = 0;               // Gaussians with tiles in the current binning
   const unsigned long long* bin_zmax = nullptr;  // bisection-cache binning filter (per tile)
   sofk::BisectScratch bis;
+  bool render_attr_set = false;  // k_render's dynamic shared-memory limit set on this device
   sofk::DBuf<int32_t> gidx_in, gidx_out;
   sofk::DBuf<int64_t> goff;
   sofk::DBuf<uint32_t> ekey_in, ekey_out;
