@@ -797,9 +797,6 @@ __device__ __forceinline__ unsigned stream_list(const int32_t* __restrict__ lp, 
 // against the chunk's last record rules the break out for the whole chunk; otherwise a
 // binary search finds it. The loop then runs up to that index without per-record min_z
 // tests (same pairs, same break, fewer instructions on the culled path).
-#ifndef SOF_CHUNK_LIMIT
-#define SOF_CHUNK_LIMIT 1
-#endif
 __device__ __forceinline__ int chunk_limit(const Rec* rp, int cnt, double zp, bool& brk) {
   brk = false;
   if (cnt <= 0 || !(rp[cnt - 1].zmin > zp)) return cnt;
@@ -813,6 +810,46 @@ __device__ __forceinline__ int chunk_limit(const Rec* rp, int cnt, double zp, bo
   }
   brk = true;
   return lo;
+}
+
+// The reference loop (field_eval.hpp:86-108) over one staged chunk of a live-only,
+// min_z-sorted list: records up to the chunk's break are culled by the screen-space conic
+// or evaluated exactly by eval_one (which returns true on the early stop). Returns the
+// pairs counted; sets done at the min-z break or the early stop. SOF_PAIR_CULL tests two
+// records' conics per step (both culled: one branch for the pair).
+#ifndef SOF_PAIR_CULL
+#define SOF_PAIR_CULL 1
+#endif
+template <typename F>
+__device__ __forceinline__ unsigned scan_chunk(const Rec* rp, int cnt, double zp, float cu, float cv, float cuu,
+                                               float cvv, float cuv, bool& done, F&& eval_one) {
+  bool brk;
+  const int lim = chunk_limit(rp, cnt, zp, brk);
+  int e = 0;
+#if SOF_PAIR_CULL
+  for (; e + 1 < lim; e += 2) {
+    const bool c0 = conic_culls(rp[e], cu, cv, cuu, cvv, cuv);
+    const bool c1 = conic_culls(rp[e + 1], cu, cv, cuu, cvv, cuv);
+    if (c0 && c1) continue;
+    if (!c0 && eval_one(rp[e])) {
+      done = true;
+      return unsigned(e + 1);
+    }
+    if (!c1 && eval_one(rp[e + 1])) {
+      done = true;
+      return unsigned(e + 2);
+    }
+  }
+#endif
+  for (; e < lim; ++e) {
+    if (conic_culls(rp[e], cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
+    if (eval_one(rp[e])) {
+      done = true;
+      return unsigned(e + 1);  // this pair was counted
+    }
+  }
+  if (brk) done = true;  // the record at lim ends the sorted scan (not counted)
+  return unsigned(lim);
 }
 
 // One CTA = one schedule block (<= 256 points of one tile). The block's Gaussian
@@ -870,37 +907,20 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
     const int32_t* lp = lent + l0;
     const int len = int(l1 - l0);  // tile lists hold < 2^31 entries
     // the exact reference loop over one staged chunk; returns the pairs it counted
-    auto eval_chunk = [&](const Rec* rp, int cnt) {
-      int e = 0;
-#if SOF_CHUNK_LIMIT
-      bool brk;
-      const int lim = chunk_limit(rp, cnt, pr.zp, brk);
-      for (; e < lim; ++e, ++rp) {
-        const Rec& r = *rp;
-#else
-      const bool brk = false;
-      for (; e < cnt; ++e, ++rp) {
-        const Rec& r = *rp;
-        if (r.zmin > pr.zp) {  // list sorted by min_z (field_eval.hpp:91)
-          done = true;
-          break;
-        }
-#endif
-        if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
-        if (SOF_EVAL_STATS) ++exact;
-        const double alpha = pair_alpha(r, pr.d, pr.t, SofExpSmem{smem_u32(s_exp)});
-        if (alpha == 0.0) continue;
-        if (SOF_EVAL_STATS) ++contrib;
-        survive *= 1.0 - alpha;
-        if (early && 1.0 - survive > 0.5) {
-          complete = false;
-          done = true;
-          ++e;  // this pair was counted
-          return unsigned(e);
-        }
+    auto eval_one = [&](const Rec& r) {
+      if (SOF_EVAL_STATS) ++exact;
+      const double alpha = pair_alpha(r, pr.d, pr.t, SofExpSmem{smem_u32(s_exp)});
+      if (alpha == 0.0) return false;
+      if (SOF_EVAL_STATS) ++contrib;
+      survive *= 1.0 - alpha;
+      if (early && 1.0 - survive > 0.5) {
+        complete = false;
+        return true;
       }
-      if (brk) done = true;  // the record at e ends the sorted scan (not counted)
-      return unsigned(e);
+      return false;
+    };
+    auto eval_chunk = [&](const Rec* rp, int cnt) {
+      return scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, eval_one);
     };
     pairs += stream_list<STAGE>(lp, len, recs, &tmap, srec, s_bar, done, eval_chunk);
   } else {
@@ -1235,37 +1255,20 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
   // k_eval's fast loop over the live-only list (stream_list); with TMA staging the
   // tensor maps live in global memory, written by a host copy before the launch
   if (STAGE == 1 && threadIdx.x < 32) tma_fence_acquire(tmap);
-  auto eval_chunk = [&](const Rec* rp, int cnt) {
-    int kk = 0;
-#if SOF_CHUNK_LIMIT
-    bool brk;
-    const int lim = chunk_limit(rp, cnt, pr.zp, brk);
-    for (; kk < lim; ++kk, ++rp) {
-      const Rec& r = *rp;
-#else
-    const bool brk = false;
-    for (; kk < cnt; ++kk, ++rp) {
-      const Rec& r = *rp;
-      if (r.zmin > pr.zp) {
-        done = true;
-        break;
-      }
-#endif
-      if (conic_culls(r, cu, cv, cuu, cvv, cuv)) continue;
-      if (SOF_EVAL_STATS) ++exact;
-      const double alpha = pair_alpha(r, pr.d, pr.t, SofExpSmem{smem_u32(s_exp)});
-      if (alpha == 0.0) continue;
-      if (SOF_EVAL_STATS) ++contrib;
-      survive *= 1.0 - alpha;
-      if (early && 1.0 - survive > 0.5) {
-        complete = false;
-        done = true;
-        ++kk;
-        return unsigned(kk);
-      }
+  auto eval_one = [&](const Rec& r) {
+    if (SOF_EVAL_STATS) ++exact;
+    const double alpha = pair_alpha(r, pr.d, pr.t, SofExpSmem{smem_u32(s_exp)});
+    if (alpha == 0.0) return false;
+    if (SOF_EVAL_STATS) ++contrib;
+    survive *= 1.0 - alpha;
+    if (early && 1.0 - survive > 0.5) {
+      complete = false;
+      return true;
     }
-    if (brk) done = true;
-    return unsigned(kk);
+    return false;
+  };
+  auto eval_chunk = [&](const Rec* rp, int cnt) {
+    return scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, eval_one);
   };
   pairs += stream_list<STAGE>(lent + l0, int(l1 - l0), recs, tmap, srec, s_bar, done, eval_chunk);
   if (active) {
