@@ -24,6 +24,7 @@
 
 #include "sof/bench.hpp"
 #include "sof/extract.hpp"
+#include "sof/io_camera.hpp"
 #include "sof/io_maps.hpp"
 #include "sof/io_mesh.hpp"
 #include "sof/io_scene.hpp"
@@ -544,6 +545,32 @@ int sofref_write_mesh_obj(long nverts, const double* verts, long ntris, const in
     for (long i = 0; i < ntris; ++i) m.triangles[i] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
     write_mesh_obj(m, path);
     return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+/// save_cameras (io_camera.hpp:65-87)
+int sofref_save_cameras(int v, const double* R, const double* t, const double* intr, const int* wh,
+                        const double* nf, const char* path) {
+  try {
+    save_cameras(to_cams(v, R, t, intr, wh, nf), path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+/// load_cameras (io_camera.hpp:17-63): the camera count (arrays filled when it fits `cap`),
+/// or -1 with the reference's message.
+int sofref_load_cameras(const char* path, int cap, double* R, double* t, double* intr, int* wh,
+                        double* nf) {
+  try {
+    const auto c = load_cameras(path);
+    if ((int)c.size() <= cap) from_cams(c, R, t, intr, wh, nf);
+    return (int)c.size();
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

@@ -152,6 +152,10 @@ class RefLib:
         L.sofref_write_scene.argtypes = [_I, _P, _P, _P, _P, _P, ctypes.c_char_p]
         L.sofref_write_mesh_ply.restype = _I
         L.sofref_write_mesh_ply.argtypes = [_L, _P, _L, _P, ctypes.c_char_p]
+        L.sofref_save_cameras.restype = _I
+        L.sofref_save_cameras.argtypes = [_I, _P, _P, _P, _P, _P, ctypes.c_char_p]
+        L.sofref_load_cameras.restype = _I
+        L.sofref_load_cameras.argtypes = [ctypes.c_char_p, _I, _P, _P, _P, _P, _P]
         L.sofref_render_depth_map.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
         L.sofref_render_pixels.argtypes = [_P, _I, _I, _L, _P, _P, _P, _P, _P, _P]
         L.sofref_normal_from_depth.argtypes = [_P, _I, _P, _P, _P]
@@ -237,6 +241,22 @@ class RefLib:
         if self.lib.sofref_write_mesh_ply(len(verts), _ptr(verts), len(tris), _ptr(tris), path.encode()):
             raise RuntimeError(self.lib.sofref_last_error().decode())
 
+
+    def save_cameras(self, R, t, intr, wh, nearfar, path: str) -> None:
+        a = [np.ascontiguousarray(x, np.float64) for x in (R, t, intr)]
+        wh = np.ascontiguousarray(wh, np.int32)
+        nf = np.ascontiguousarray(nearfar, np.float64)
+        if self.lib.sofref_save_cameras(len(a[1]), *(_ptr(x) for x in a), _ptr(wh), _ptr(nf), path.encode()):
+            raise RuntimeError(self.lib.sofref_last_error().decode())
+
+    def load_cameras(self, path: str):
+        """(R [V, 9], t [V, 3], intr [V, 4], wh [V, 2], nearfar [V, 2])."""
+        v = self.lib.sofref_load_cameras(path.encode(), 0, None, None, None, None, None)
+        if v < 0:
+            raise RuntimeError(self.lib.sofref_last_error().decode())
+        out = (np.empty((v, 9)), np.empty((v, 3)), np.empty((v, 4)), np.empty((v, 2), np.int32), np.empty((v, 2)))
+        self.lib.sofref_load_cameras(path.encode(), v, *(_ptr(x) for x in out))
+        return out
 
     def write_mesh_obj(self, verts, tris, path: str) -> None:
         verts = np.ascontiguousarray(verts, np.float64)

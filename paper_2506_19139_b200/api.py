@@ -637,6 +637,71 @@ def write_mesh(mesh: Mesh, path: str, fmt: str = "ply"):
     (write_mesh_obj if fmt == "obj" else write_mesh_ply)(mesh, path)
 
 
+_CAM_REQUIRED = ("width", "height", "fx", "fy", "cx", "cy", "rotation", "translation")
+
+
+def load_cameras(path: str) -> CameraSet:
+    """load_cameras (io_camera.hpp:17-63): {"cameras": [{width, height, fx, fy, cx, cy,
+    rotation (9, row-major world-to-view), translation (3), near?, far?}, ...]}, with the
+    reference's checks and messages (RuntimeError)."""
+    import json
+    try:
+        f = open(path)
+    except OSError:
+        raise RuntimeError(f"cannot open camera file: {path}") from None
+    with f:
+        try:
+            root = json.load(f)
+        except ValueError as e:
+            raise RuntimeError(f"camera schema error: {e}") from None
+    if not isinstance(root, dict) or not isinstance(root.get("cameras"), list):
+        raise RuntimeError("camera schema error: missing field 'cameras'")
+    v = len(root["cameras"])
+    R, t, intr = np.empty((v, 9)), np.empty((v, 3)), np.empty((v, 4))
+    wh, nf = np.empty((v, 2), np.int32), np.tile([0.2, 100.0], (v, 1))  # camera.hpp:16-17
+    for k, jc in enumerate(root["cameras"]):
+        for req in _CAM_REQUIRED:
+            if req not in jc:
+                raise RuntimeError(f"camera schema error: missing field '{req}'")
+        wh[k] = int(jc["width"]), int(jc["height"])
+        intr[k] = [float(jc[n]) for n in ("fx", "fy", "cx", "cy")]
+        r, tt = jc["rotation"], jc["translation"]
+        if not isinstance(r, list) or len(r) != 9:
+            raise RuntimeError("camera schema error: rotation must have 9 entries")
+        if not isinstance(tt, list) or len(tt) != 3:
+            raise RuntimeError("camera schema error: translation must have 3 entries")
+        R[k], t[k] = [float(x) for x in r], [float(x) for x in tt]
+        if "near" in jc:
+            nf[k, 0] = float(jc["near"])
+        if "far" in jc:
+            nf[k, 1] = float(jc["far"])
+        m = R[k].reshape(3, 3)
+        if np.abs(m @ m.T - np.eye(3)).max() > 1e-6:
+            raise RuntimeError("degenerate rotation: not orthonormal")
+        if wh[k, 0] <= 0 or wh[k, 1] <= 0 or intr[k, 0] <= 0.0 or intr[k, 1] <= 0.0:
+            raise RuntimeError("camera schema error: non-positive intrinsics")
+    return CameraSet(R, t, intr, wh, nf)
+
+
+def save_cameras(cams, path: str):
+    """save_cameras (io_camera.hpp:65-87): the same JSON document nlohmann::json::dump(2)
+    writes (keys sorted, 2-space indent, shortest round-trip doubles), plus a newline."""
+    import json
+    c = CameraSet.of(cams)
+    out = []
+    for k in range(c.v):
+        fx, fy, cx, cy = (float(x) for x in c.intr[k])
+        out.append({"width": int(c.wh[k, 0]), "height": int(c.wh[k, 1]), "fx": fx, "fy": fy, "cx": cx, "cy": cy,
+                    "rotation": [float(x) for x in c.R[k]], "translation": [float(x) for x in c.t[k]],
+                    "near": float(c.nearfar[k, 0]), "far": float(c.nearfar[k, 1])})
+    try:
+        f = open(path, "w", newline="\n")
+    except OSError:
+        raise RuntimeError(f"cannot write camera file: {path}") from None
+    with f:
+        f.write(json.dumps({"cameras": out}, indent=2, sort_keys=True) + "\n")
+
+
 @dataclass
 class SeedPointSet:
     """seed_points.hpp:24-27: points and provenance (0 centre, 1 bounding-box corner)."""

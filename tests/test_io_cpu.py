@@ -57,3 +57,48 @@ def test_mesh_ply_errors(ref, tmp_path):
         with pytest.raises(RuntimeError) as ours:
             sof.read_mesh_ply(str(p))
         assert str(ours.value) == str(theirs.value), name
+
+
+# ---- camera JSON (io_camera.hpp:17-87; tests/test_io.cpp:109-140) ----------------------------
+
+def test_cameras_save_byte_identical_and_round_trip(ref, tmp_path):
+    c = ref.orbit_cameras(3, 4.0, 1.8)  # the reference test's CameraIO.RoundTrip cameras
+    c.nearfar[0] = 0.5, 50.0
+    ours, theirs = tmp_path / "a.json", tmp_path / "b.json"
+    sof.save_cameras(c, str(ours))
+    ref.save_cameras(c.R, c.t, c.intr, c.wh, c.nearfar, str(theirs))
+    assert ours.read_bytes() == theirs.read_bytes()
+    got = sof.load_cameras(str(theirs))
+    want = ref.load_cameras(str(ours))
+    for a, b in zip((got.R, got.t, got.intr, got.wh, got.nearfar), want):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(got.R, c.R.reshape(-1, 9))
+    np.testing.assert_array_equal(got.nearfar, c.nearfar)
+
+
+def test_cameras_defaults_and_errors(ref, tmp_path):
+    p = tmp_path / "c.json"
+    p.write_text('{"cameras": [{"width": 4, "height": 5, "fx": 1, "fy": 2, "cx": 2, "cy": 2,'
+                 ' "rotation": [1,0,0,0,1,0,0,0,1], "translation": [0,0,1]}]}')
+    got, want = sof.load_cameras(str(p)), ref.load_cameras(str(p))
+    for a, b in zip((got.R, got.t, got.intr, got.wh, got.nearfar), want):
+        np.testing.assert_array_equal(a, b)
+    cases = {
+        '{"cameras": [{"width": 4, "height": 4, "fx": 1, "fy": 1, "cx": 2, "cy": 2,'
+        ' "rotation": [1,0,0,0,1,0,0,0,1]}]}': "missing field 'translation'",
+        '{"cameras": [{"width": 4, "height": 4, "fx": 1, "fy": 1, "cx": 2, "cy": 2,'
+        ' "rotation": [2,0,0,0,1,0,0,0,1], "translation": [0,0,0]}]}': "degenerate rotation",
+        '{"cameras": [{"width": 4, "height": 4, "fx": 1, "fy": 1, "cx": 2, "cy": 2,'
+        ' "rotation": [1,0,0,0,1,0,0,0], "translation": [0,0,0]}]}': "rotation must have 9 entries",
+        '{"cameras": [{"width": 0, "height": 4, "fx": 1, "fy": 1, "cx": 2, "cy": 2,'
+        ' "rotation": [1,0,0,0,1,0,0,0,1], "translation": [0,0,0]}]}': "non-positive intrinsics",
+        '{"views": []}': "missing field 'cameras'",
+        '{"cameras": [': "camera schema error",
+    }
+    for text, msg in cases.items():
+        p.write_text(text)
+        for load in (sof.load_cameras, ref.load_cameras):
+            with pytest.raises(RuntimeError, match=msg):
+                load(str(p))
+    with pytest.raises(RuntimeError, match="cannot open camera file"):
+        sof.load_cameras(str(tmp_path / "absent.json"))
