@@ -713,6 +713,9 @@ __global__ void k_block_fill(int T, int S, const int* __restrict__ tile_off,
 #ifndef SOF_EVAL_CHUNK
 #define SOF_EVAL_CHUNK 32
 #endif
+// strategies bit set by eval_views when the schedule was built one view ahead: the
+// evaluation re-reads the pruned flag of each scheduled point
+constexpr int kRecheckPruned = 1 << 8;
 constexpr int kChunk = SOF_EVAL_CHUNK;  // Gaussian records staged in shared memory per step
 #ifndef SOF_EVAL_MINB
 #define SOF_EVAL_MINB 10
@@ -878,7 +881,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
   if (b >= *nblocks) return;
   const int4 blk = blocks[b];
   const int j = blk.x + int(threadIdx.x);
-  const bool active = j < blk.y;
+  bool active = j < blk.y;
   int i = 0;
   PointRay pr;
   pr.observed = false;
@@ -886,7 +889,11 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
   if (active) {
     i = pidx[j];
     if (MODE == kModeLabel || MODE == kModeValue) m_prev = min_op[i];
+    // the schedule is built one view ahead (eval_views): a point the previous view's
+    // evaluation pruned may still be listed; the reference skips it (field_eval.hpp:147)
+    const bool pruned = (MODE == kModeLabel || MODE == kModeClassify) && (strategies & kRecheckPruned) && ext[i];
     pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+    active = !pruned;
   }
   int64_t l0 = 0, l1 = n_gauss;
   if (TILED) {  // list bounds carried by the block descriptor (k_block_fill)
@@ -1015,7 +1022,7 @@ __global__ void __launch_bounds__(256) k_eval_f32(
   const int4 blk = blocks[b];
   const int tid = threadIdx.x;
   const int j = blk.x + tid;
-  const bool active = j < blk.y;
+  bool active = j < blk.y;
   int i = 0;
   PointRay pr;
   pr.observed = false;
@@ -1024,7 +1031,11 @@ __global__ void __launch_bounds__(256) k_eval_f32(
   pr.d[0] = pr.d[1] = pr.d[2] = 0.0;
   if (active) {
     i = pidx[j];
-    pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+    // schedule built one view ahead: skip points pruned since (as k_eval)
+    if ((MODE == kModeLabel || MODE == kModeClassify) && (strategies & kRecheckPruned) && ext[i])
+      active = false;
+    else
+      pr = point_ray(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
   }
   // per-point float monomials of the ray direction (abc_cached precompute.hpp:39-45)
   const float x = float(pr.d[0]), y = float(pr.d[1]), z = float(pr.d[2]);
@@ -1734,7 +1745,7 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
                         const Rec* rec, int strategies, bool classify, double* min_op,
                         uint8_t* ext, double* o_out, uint8_t* obs, uint8_t* comp) {
   if (grid <= 0) return;
-  const int64_t* nb = c->d_scalar.p;
+  const int64_t* nb = c->sched.nblocks.p;
   unsigned long long* pc = c->d_counters.p;
   const int e0 = prof_mark(c);
   const RecF* recf = view_recf(c, int(&cam - c->cams.data()));
@@ -1795,67 +1806,39 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   c->d_scalar.ensure(4);
   zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 4);
   PointSchedule& s = c->sched;
-  if (n > 0) {
-    s.tile_of.ensure(n);
-    s.order.ensure(n);
-  }
   if (mode == kModeView && n > 0) {
     k_fill_view_outputs<<<grid_for(n, 256), 256, 0, c->stream>>>(n, o_out, obs_out, comp_out);
     SOF_LAUNCHED(c);
   }
-  // Per-view preprocessing (K1 records + K2 tile binding) runs on the prep lane
-  // (second stream, own CUB scratch), one view ahead of the evaluation: the host
-  // issues view v's schedule + eval, then prepares view v + 1 (its one size readback
-  // blocks only the host) while the GPU evaluates view v.
+  // Per-view preprocessing (K1 records + K2 tile binding + K3 point schedule) runs on
+  // the prep lane (second stream, own CUB scratch), one view ahead of the evaluation:
+  // the host issues view v's evaluation, then prepares view v + 1 (its one size
+  // readback blocks only the host) while the GPU evaluates view v.
   int64_t ncand = n;      // candidate points of the next view
   bool use_list = false;  // candidates = s.active[0, ncand) instead of all points
   const Rec* prep_rec[2] = {nullptr, nullptr};
   const Binding* prep_bd[2] = {nullptr, nullptr};
-  auto prep_view = [&](int pv) {
-    std::swap(c->stream, c->stream2);
-    c->cub_tmp.swap(c->cub_tmp2);
-    c->scratch_sel = pv & 1;
-    try {
-      // scratch slot pv & 1 may still hold the records / tile lists of view pv - 2 (past
-      // the cache budget): wait until its evaluation on the main stream is done
-      SOF_CUDA(cudaStreamWaitEvent(c->stream, c->eval_ev[pv & 1], 0));
-      const int p0 = prof_mark(c);
-      // binding first: it computes the records in the same pass as the tile rectangles
-      prep_bd[pv & 1] = tiled ? &view_binding(c, pv, tile_size, live_lists) : nullptr;
-      prep_rec[pv & 1] = view_records(c, pv);
-      prof_span(c, p0, prof_mark(c), kProfPrep);
-      SOF_CUDA(cudaEventRecord(c->prep_ev[pv & 1], c->stream));
-    } catch (...) {
-      std::swap(c->stream, c->stream2);
-      c->cub_tmp.swap(c->cub_tmp2);
-      throw;
-    }
-    std::swap(c->stream, c->stream2);
-    c->cub_tmp.swap(c->cub_tmp2);
-  };
-  const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
-  const auto hd0 = std::chrono::steady_clock::now();
-  for (int v = v0; v < v1 && n > 0; ++v) {
-    if (dbg && (v - v0 < 3 || v + 1 == v1))
-      std::fprintf(stderr, "    view %3d issued at %8.2f ms ncand %lld list %d\n", v,
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count(),
-                   (long long)ncand, int(use_list));
-    const Cam& cam = c->cams[v];
+  const uint8_t* skip = (prune && (mode == kModeLabel || mode == kModeClassify)) ? ext : nullptr;
+  // SOF_SCHED_LOOKAHEAD: build view v + 1's schedule on the prep lane during view v's
+  // evaluation (off the critical path; the evaluation then re-checks the pruned flags).
+  // Default off: 1.3% faster per C3 step, but the evaluation kernel then shares the SMs
+  // with the scheduler for its whole span.
+  const bool lookahead = std::getenv("SOF_SCHED_LOOKAHEAD") != nullptr;
+  const int eval_strategies = strategies | ((lookahead && skip) ? kRecheckPruned : 0);
+  int64_t sched_grid[2] = {0, 0};  // evaluation grid of the schedule built for view pv
+  auto sched_view = [&](int pv) {
+    const Cam& cam = c->cams[pv];
     const int tiles_x = (cam.w + tile_size - 1) / tile_size;
     const int tiles_y = (cam.h + tile_size - 1) / tile_size;
     const int T = tiled ? tiles_x * tiles_y : 1;
-    const auto h0 = std::chrono::steady_clock::now();
-    if (v == v0) prep_view(v);
-    // the records / binding of view v were prepared on the prep lane (during view v-1)
-    SOF_CUDA(cudaStreamWaitEvent(c->stream, c->prep_ev[v & 1], 0));
-
-    const Rec* rec = prep_rec[v & 1];
-    const Binding* bd = prep_bd[v & 1];
     const int p1 = prof_mark(c);
     const auto h1 = std::chrono::steady_clock::now();
-    c->host_ms[0] += std::chrono::duration<double, std::milli>(h1 - h0).count();
-    // K3: group the active, observed points of this view by tile (no host sync)
-    const uint8_t* skip = (prune && (mode == kModeLabel || mode == kModeClassify)) ? ext : nullptr;
+    // K3: group the active, observed points of this view by tile (no host sync). The
+    // pruned flags may still change under the previous view's evaluation: a point
+    // pruned after this pass is skipped by the evaluation kernel itself.
+    s.tile_of.ensure(n);
+    s.order.ensure(n);
+    s.nblocks.ensure(1);
     // bins per tile: 4x4-pixel cells when points are dense enough to fill them (label
     // grids), else whole tiles (bisection midpoints)
     const int S = (tiled && ncand >= 1024 * int64_t(T)) ? 16 : 1;
@@ -1876,8 +1859,7 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);
     k_sched_scatter<<<grid_for((ncand + kScatterItems - 1) / kScatterItems, 256), 256, 0, c->stream>>>(
-        ncand, cand, s.tile_of.p, s.tile_off.p,
-                                                                 tile_cur, s.order.p);
+        ncand, cand, s.tile_of.p, s.tile_off.p, tile_cur, s.order.p);
     SOF_LAUNCHED(c);
     k_block_counts<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_cnt.p);
     SOF_LAUNCHED(c);
@@ -1885,29 +1867,83 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     const int64_t grid = (ncand + kEvalThreads - 1) / kEvalThreads + T;
     s.blocks.ensure(grid);
     k_block_fill<<<grid_for(T + 1, 256), 256, 0, c->stream>>>(T, S, s.tile_off.p, s.blk_off.p,
-                                                               tiled ? bd->off.p : nullptr, s.blocks.p,
-                                                               c->d_scalar.p);
+                                                               tiled ? prep_bd[pv & 1]->off.p : nullptr, s.blocks.p,
+                                                               s.nblocks.p);
     SOF_LAUNCHED(c);
+    sched_grid[pv & 1] = grid;
     prof_span(c, p1, prof_mark(c), kProfSched);
-    const auto h2 = std::chrono::steady_clock::now();
-    c->host_ms[1] += std::chrono::duration<double, std::milli>(h2 - h1).count();
+    c->host_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();
+  };
+  auto prep_view = [&](int pv) {
+    std::swap(c->stream, c->stream2);
+    c->cub_tmp.swap(c->cub_tmp2);
+    c->scratch_sel = pv & 1;
+    try {
+      // scratch slot pv & 1 may still hold the records / tile lists of view pv - 2 (past
+      // the cache budget): wait until its evaluation on the main stream is done
+      SOF_CUDA(cudaStreamWaitEvent(c->stream, c->eval_ev[pv & 1], 0));
+      const int p0 = prof_mark(c);
+      // binding first: it computes the records in the same pass as the tile rectangles
+      prep_bd[pv & 1] = tiled ? &view_binding(c, pv, tile_size, live_lists) : nullptr;
+      prep_rec[pv & 1] = view_records(c, pv);
+      prof_span(c, p0, prof_mark(c), kProfPrep);
+      // K3 for view pv into the other schedule buffers (view pv - 1's evaluation reads
+      // the current ones); pv - 2's evaluation, which read them, is done (event above)
+      if (lookahead) {
+        s.swap_view_buffers(c->sched_alt);
+        sched_view(pv);
+      }
+      SOF_CUDA(cudaEventRecord(c->prep_ev[pv & 1], c->stream));
+    } catch (...) {
+      std::swap(c->stream, c->stream2);
+      c->cub_tmp.swap(c->cub_tmp2);
+      throw;
+    }
+    std::swap(c->stream, c->stream2);
+    c->cub_tmp.swap(c->cub_tmp2);
+  };
+  const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
+  const auto hd0 = std::chrono::steady_clock::now();
+  for (int v = v0; v < v1 && n > 0; ++v) {
+    if (dbg && (v - v0 < 3 || v + 1 == v1))
+      std::fprintf(stderr, "    view %3d issued at %8.2f ms ncand %lld list %d\n", v,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count(),
+                   (long long)ncand, int(use_list));
+    const Cam& cam = c->cams[v];
+    const int tiles_x = (cam.w + tile_size - 1) / tile_size;
+    const auto h0 = std::chrono::steady_clock::now();
+    if (v == v0) {
+      // the prep lane's first two views reuse buffers of earlier main-stream work
+      SOF_CUDA(cudaEventRecord(c->eval_ev[0], c->stream));
+      SOF_CUDA(cudaEventRecord(c->eval_ev[1], c->stream));
+      prep_view(v);
+    }
+    // the records, binding and schedule of view v were prepared on the prep lane
+    // (during view v - 1's evaluation)
+    SOF_CUDA(cudaStreamWaitEvent(c->stream, c->prep_ev[v & 1], 0));
+    c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    if (!lookahead) sched_view(v);  // on the main stream, after view v - 1's evaluation
+
+    const Rec* rec = prep_rec[v & 1];
+    const Binding* bd = prep_bd[v & 1];
+    const int64_t grid = sched_grid[v & 1];
     const int32_t* pidx = s.order.p;
     switch (mode) {
       case kModeLabel:
         launch_eval<kModeLabel>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
-                                strategies, classify_mode, min_op, ext, o_out, obs_out, comp_out);
+                                eval_strategies, classify_mode, min_op, ext, o_out, obs_out, comp_out);
         break;
       case kModeClassify:
         launch_eval<kModeClassify>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
-                                   strategies, true, min_op, ext, o_out, obs_out, comp_out);
+                                   eval_strategies, true, min_op, ext, o_out, obs_out, comp_out);
         break;
       case kModeView:
         launch_eval<kModeView>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
-                               strategies, classify_mode, min_op, ext, o_out, obs_out, comp_out);
+                               eval_strategies, classify_mode, min_op, ext, o_out, obs_out, comp_out);
         break;
       case kModeValue:
         launch_eval<kModeValue>(c, tiled, grid, pidx, xyz, cam, tile_size, tiles_x, bd, rec,
-                                strategies, false, min_op, ext, o_out, obs_out, comp_out);
+                                eval_strategies, false, min_op, ext, o_out, obs_out, comp_out);
         break;
     }
     SOF_CUDA(cudaEventRecord(c->eval_ev[v & 1], c->stream));

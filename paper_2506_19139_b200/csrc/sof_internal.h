@@ -108,6 +108,19 @@ struct PointSchedule {
   DBuf<int> tile_off, blk_cnt, blk_off;  // [T + 1]
   DBuf<int4> blocks;         // {start, end, tile, 0}
   DBuf<int32_t> active, active2, nsel;  // candidate points (not pruned), compacted
+  DBuf<int64_t> nblocks;                // [1] block count (read by the evaluation kernel)
+  // the per-view buffers (not the candidate lists): the schedule of view v + 1 is built
+  // on the prep lane while view v's evaluation reads the other set
+  void swap_view_buffers(PointSchedule& o) noexcept {
+    tile_of.swap(o.tile_of);
+    order.swap(o.order);
+    tile_cnt.swap(o.tile_cnt);
+    tile_off.swap(o.tile_off);
+    blk_cnt.swap(o.blk_cnt);
+    blk_off.swap(o.blk_off);
+    blocks.swap(o.blocks);
+    nblocks.swap(o.nblocks);
+  }
 };
 
 // Persistent (grow-only) scratch of the mesher stages: no allocation in steady state.
@@ -232,6 +245,7 @@ struct sof_ctx {
   sofk::DBuf<int32_t> eval_in;
 
   sofk::PointSchedule sched;
+  sofk::PointSchedule sched_alt;          // second set of per-view schedule buffers
   sofk::MeshScratch ms;
   sofk::Binding rbind;                    // render binding (lists ordered by a t* lower bound)
   sofk::RenderScratch rs;

@@ -95,6 +95,22 @@ def test_label_grid_bitexact(case, mask, classify):
     assert ev.counters() == rev.counters()
 
 
+@pytest.mark.parametrize("mask", [8, 12, 15, 24, 31])
+def test_label_grid_sched_lookahead_bitexact(case, mask, monkeypatch):
+    """Schedule of view v + 1 built on the prep lane during view v's evaluation
+    (SOF_SCHED_LOOKAHEAD): pruned points re-checked by the kernel, values and the
+    reference counters unchanged."""
+    scene, cams, rc, views, pts = case
+    monkeypatch.setenv("SOF_SCHED_LOOKAHEAD", "1")
+    for classify in (True, False):
+        ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.from_mask(mask))
+        rev = rc.evaluator(mask)
+        assert_bits(ev.label_grid(pts, classify), rev.label_grid(pts, classify), f"mask {mask}")
+        assert ev.counters() == rev.counters()
+        np.testing.assert_array_equal(ev.classify_points(pts), rev.classify_points(pts).astype(bool))
+        assert ev.counters() == rev.counters()
+
+
 @pytest.mark.parametrize("mask", [0, 31, 8, 12, 19])
 def test_classify_and_value_at(case, mask):
     scene, cams, rc, views, pts = case

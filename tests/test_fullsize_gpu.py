@@ -61,6 +61,24 @@ def test_staging_modes_bit_identical(c3):
     assert s0["pairs"] == s1["pairs"] and s0["point_view_evals"] == s1["point_view_evals"]
 
 
+def test_sched_lookahead_bit_identical(c3, monkeypatch):
+    """Schedule built one view ahead on the prep lane (SOF_SCHED_LOOKAHEAD; the evaluation
+    re-checks the pruned flags) vs on the main stream: same mesh bits, same counters."""
+    ctx, verts, tets = c3
+    out = {}
+    for on in (True, False):
+        if on:
+            monkeypatch.setenv("SOF_SCHED_LOOKAHEAD", "1")
+        else:
+            monkeypatch.delenv("SOF_SCHED_LOOKAHEAD", raising=False)
+        st = {}
+        out[on] = (sof.extract_resident(ctx, sof.ExtractOptions(), st), st)
+    (m0, s0), (m1, s1) = out[False], out[True]
+    np.testing.assert_array_equal(m0.vertices.view(np.uint64), m1.vertices.view(np.uint64))
+    np.testing.assert_array_equal(m0.triangles, m1.triangles)
+    assert s0["pairs"] == s1["pairs"] and s0["point_view_evals"] == s1["point_view_evals"]
+
+
 def test_mesh_consistency(c3):
     ctx, verts, tets = c3
     mesh = sof.extract_resident(ctx, sof.ExtractOptions(), {})
