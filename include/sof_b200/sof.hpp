@@ -21,13 +21,16 @@
 
 #include <Eigen/Dense>
 
+#include <algorithm>
 #include <array>
+#include <charconv>
 #include <cctype>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <fstream>
 #include <functional>
+#include <iterator>
 #include <limits>
 #include <memory>
 #include <stdexcept>
@@ -690,6 +693,237 @@ inline void write_mesh_obj(const Mesh& mesh, const std::string& path) {
     out << line;
   }
   for (const auto& t : mesh.triangles) out << "f " << t[0] + 1 << " " << t[1] + 1 << " " << t[2] + 1 << "\n";
+}
+
+// ---- camera JSON (io_camera.hpp:17-87) ---------------------------------------------------------
+// The reference reads and writes it with nlohmann::json; this is a small reader for the
+// same documents and a writer that emits what nlohmann's dump(2) emits (keys sorted,
+// two-space indent, shortest round-trip doubles with a ".0" on integral values).
+namespace detail {
+struct JsonValue {
+  enum Kind { kNull, kBool, kNumber, kString, kArray, kObject } kind = kNull;
+  double number = 0.0;
+  std::string str;
+  std::vector<JsonValue> items;
+  std::vector<std::pair<std::string, JsonValue>> members;
+  const JsonValue* get(const std::string& key) const {
+    for (const auto& m : members)
+      if (m.first == key) return &m.second;
+    return nullptr;
+  }
+};
+
+class JsonReader {
+ public:
+  explicit JsonReader(const std::string& text) : s_(text) {}
+  JsonValue document() {
+    JsonValue v = value();
+    skip();
+    if (i_ != s_.size()) fail("trailing characters");
+    return v;
+  }
+
+ private:
+  [[noreturn]] void fail(const char* what) const {
+    throw std::runtime_error(std::string("camera schema error: parse error at byte ") + std::to_string(i_) +
+                             ": " + what);
+  }
+  void skip() {
+    while (i_ < s_.size() && std::isspace(static_cast<unsigned char>(s_[i_]))) ++i_;
+  }
+  bool eat(char ch) {
+    skip();
+    if (i_ < s_.size() && s_[i_] == ch) {
+      ++i_;
+      return true;
+    }
+    return false;
+  }
+  void word(const char* w) {
+    for (; *w; ++w, ++i_)
+      if (i_ >= s_.size() || s_[i_] != *w) fail("invalid literal");
+  }
+  std::string string() {
+    if (!eat('"')) fail("expected a string");
+    std::string out;
+    while (true) {
+      if (i_ >= s_.size()) fail("unterminated string");
+      const char ch = s_[i_++];
+      if (ch == '"') return out;
+      if (ch == '\\') {
+        if (i_ >= s_.size()) fail("unterminated string");
+        const char e = s_[i_++];
+        if (e == 'u') {  // keys and values of this schema are ASCII; keep the code unit
+          if (i_ + 4 > s_.size()) fail("bad escape");
+          out += char(std::stoi(s_.substr(i_, 4), nullptr, 16) & 0x7f);
+          i_ += 4;
+        } else {
+          out += (e == 'n') ? '\n' : (e == 't') ? '\t' : (e == 'r') ? '\r' : (e == 'b') ? '\b' : (e == 'f') ? '\f' : e;
+        }
+      } else {
+        out += ch;
+      }
+    }
+  }
+  JsonValue value() {
+    skip();
+    if (i_ >= s_.size()) fail("unexpected end of input");
+    JsonValue v;
+    const char ch = s_[i_];
+    if (ch == '{') {
+      ++i_;
+      v.kind = JsonValue::kObject;
+      if (eat('}')) return v;
+      do {
+        std::string k = string();
+        if (!eat(':')) fail("expected ':'");
+        v.members.emplace_back(std::move(k), value());
+      } while (eat(','));
+      if (!eat('}')) fail("expected '}'");
+    } else if (ch == '[') {
+      ++i_;
+      v.kind = JsonValue::kArray;
+      if (eat(']')) return v;
+      do v.items.push_back(value());
+      while (eat(','));
+      if (!eat(']')) fail("expected ']'");
+    } else if (ch == '"') {
+      v.kind = JsonValue::kString;
+      v.str = string();
+    } else if (ch == 't' || ch == 'f') {
+      v.kind = JsonValue::kBool;
+      v.number = ch == 't';
+      word(ch == 't' ? "true" : "false");
+    } else if (ch == 'n') {
+      word("null");
+    } else {
+      v.kind = JsonValue::kNumber;
+      const char* b = s_.data() + i_;
+      const auto r = std::from_chars(b, s_.data() + s_.size(), v.number);
+      if (r.ec != std::errc()) fail("invalid number");
+      i_ += size_t(r.ptr - b);
+    }
+    return v;
+  }
+  const std::string& s_;
+  size_t i_ = 0;
+};
+
+inline double json_number(const JsonValue& v, const char* key) {
+  if (v.kind != JsonValue::kNumber && v.kind != JsonValue::kBool)
+    throw std::runtime_error(std::string("camera schema error: '") + key + "' must be a number");
+  return v.number;
+}
+
+// nlohmann::json's double formatting (shortest round trip; ".0" on integral values;
+// exponent form below 1e-4 and from 1e16 on, with at least two exponent digits)
+inline std::string json_double(double x) {
+  if (!std::isfinite(x)) return "null";
+  if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof buf, x, std::chars_format::scientific);
+  std::string sci(buf, r.ptr);
+  std::string sign;
+  if (sci[0] == '-') {
+    sign = "-";
+    sci.erase(0, 1);
+  }
+  const size_t epos = sci.find('e');
+  std::string digits = sci.substr(0, epos);
+  digits.erase(std::remove(digits.begin(), digits.end(), '.'), digits.end());
+  const int k = int(digits.size());
+  const int n = std::stoi(sci.substr(epos + 1)) + 1;  // x = 0.d1..dk x 10^n
+  std::string out;
+  if (k <= n && n <= 15) {
+    out = digits + std::string(size_t(n - k), '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    out = digits.substr(0, size_t(n)) + "." + digits.substr(size_t(n));
+  } else if (-4 < n && n <= 0) {
+    out = "0." + std::string(size_t(-n), '0') + digits;
+  } else {
+    const int e = n - 1;
+    out = digits.substr(0, 1) + (k > 1 ? "." + digits.substr(1) : std::string()) + "e" + (e < 0 ? "-" : "+") +
+          (std::abs(e) < 10 ? "0" : "") + std::to_string(std::abs(e));
+  }
+  return sign + out;
+}
+}  // namespace detail
+
+/// load_cameras (io_camera.hpp:17-63): the same schema, checks and messages.
+inline std::vector<Camera> load_cameras(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open camera file: " + path);
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  const detail::JsonValue root = detail::JsonReader(text).document();
+  const detail::JsonValue* list = root.get("cameras");
+  if (!list || list->kind != detail::JsonValue::kArray)
+    throw std::runtime_error("camera schema error: missing field 'cameras'");
+  std::vector<Camera> out;
+  for (const auto& jc : list->items) {
+    for (const char* req : {"width", "height", "fx", "fy", "cx", "cy", "rotation", "translation"})
+      if (!jc.get(req)) throw std::runtime_error(std::string("camera schema error: missing field '") + req + "'");
+    Camera cam;
+    cam.width = int(detail::json_number(*jc.get("width"), "width"));
+    cam.height = int(detail::json_number(*jc.get("height"), "height"));
+    cam.fx = detail::json_number(*jc.get("fx"), "fx");
+    cam.fy = detail::json_number(*jc.get("fy"), "fy");
+    cam.cx = detail::json_number(*jc.get("cx"), "cx");
+    cam.cy = detail::json_number(*jc.get("cy"), "cy");
+    const auto& r = *jc.get("rotation");
+    const auto& t = *jc.get("translation");
+    if (r.kind != detail::JsonValue::kArray || r.items.size() != 9)
+      throw std::runtime_error("camera schema error: rotation must have 9 entries");
+    if (t.kind != detail::JsonValue::kArray || t.items.size() != 3)
+      throw std::runtime_error("camera schema error: translation must have 3 entries");
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) cam.rotation(i, j) = detail::json_number(r.items[size_t(i * 3 + j)], "rotation");
+    for (int i = 0; i < 3; ++i) cam.translation[i] = detail::json_number(t.items[size_t(i)], "translation");
+    if (const auto* v = jc.get("near")) cam.near = detail::json_number(*v, "near");
+    if (const auto* v = jc.get("far")) cam.far = detail::json_number(*v, "far");
+    if ((cam.rotation * cam.rotation.transpose() - Mat3::Identity()).cwiseAbs().maxCoeff() > 1e-6)
+      throw std::runtime_error("degenerate rotation: not orthonormal");
+    if (cam.width <= 0 || cam.height <= 0 || cam.fx <= 0.0 || cam.fy <= 0.0)
+      throw std::runtime_error("camera schema error: non-positive intrinsics");
+    out.push_back(cam);
+  }
+  return out;
+}
+
+/// save_cameras (io_camera.hpp:65-87): byte-identical to the reference's file.
+inline void save_cameras(const std::vector<Camera>& cameras, const std::string& path) {
+  using detail::json_double;
+  std::string s = "{\n  \"cameras\": [";
+  if (cameras.empty()) s += "]";
+  for (size_t k = 0; k < cameras.size(); ++k) {
+    const Camera& c = cameras[k];
+    auto arr = [&](const double* v, int n) {
+      std::string a = "[\n";
+      for (int i = 0; i < n; ++i) a += "        " + json_double(v[i]) + (i + 1 < n ? ",\n" : "\n");
+      return a + "      ]";
+    };
+    double r[9], t[3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) r[i * 3 + j] = c.rotation(i, j);
+    for (int i = 0; i < 3; ++i) t[i] = c.translation[i];
+    s += (k ? ",\n" : "\n");
+    s += "    {\n";  // keys in std::map order, as nlohmann::json stores them
+    s += "      \"cx\": " + json_double(c.cx) + ",\n";
+    s += "      \"cy\": " + json_double(c.cy) + ",\n";
+    s += "      \"far\": " + json_double(c.far) + ",\n";
+    s += "      \"fx\": " + json_double(c.fx) + ",\n";
+    s += "      \"fy\": " + json_double(c.fy) + ",\n";
+    s += "      \"height\": " + std::to_string(c.height) + ",\n";
+    s += "      \"near\": " + json_double(c.near) + ",\n";
+    s += "      \"rotation\": " + arr(r, 9) + ",\n";
+    s += "      \"translation\": " + arr(t, 3) + ",\n";
+    s += "      \"width\": " + std::to_string(c.width) + "\n";
+    s += "    }";
+    if (k + 1 == cameras.size()) s += "\n  ]";
+  }
+  s += "\n}\n";
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot write camera file: " + path);
+  out << s;
 }
 
 inline Mesh read_mesh_obj(const std::string& path) {

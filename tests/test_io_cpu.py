@@ -102,3 +102,55 @@ def test_cameras_defaults_and_errors(ref, tmp_path):
                 load(str(p))
     with pytest.raises(RuntimeError, match="cannot open camera file"):
         sof.load_cameras(str(tmp_path / "absent.json"))
+
+
+def _cpp_camera_io(tmp_path):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "camera_io")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"), "-I",
+                        os.path.join(root, "oracle", "eigen_shim"), os.path.join(root, "tests", "cpp", "camera_io.cpp"),
+                        "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return lambda a, b: subprocess.run([exe, a, b], capture_output=True, text=True)
+
+
+def test_cpp_cameras_round_trip_byte_identical(ref, tmp_path):
+    """C++ drop-in load_cameras + save_cameras reproduce the reference's file byte for byte."""
+    run = _cpp_camera_io(tmp_path)
+    c = ref.orbit_cameras(5, 4.0, 1.8)
+    c.nearfar[0] = 0.5, 50.0
+    c.intr[1] = 1e-05, 123456.789, 0.1, 3.0
+    c.t[2] = -0.0, 1e20, 2.5e-7
+    a, b = tmp_path / "a.json", tmp_path / "b.json"
+    ref.save_cameras(c.R, c.t, c.intr, c.wh, c.nearfar, str(a))
+    r = run(str(a), str(b))
+    assert r.returncode == 0, r.stdout
+    assert b.read_bytes() == a.read_bytes()
+    e, f = tmp_path / "e.json", tmp_path / "f.json"
+    e.write_text('{"cameras": []}')
+    ref.save_cameras(np.zeros((0, 9)), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 2), np.int32),
+                     np.zeros((0, 2)), str(f))
+    assert run(str(e), str(b)).returncode == 0 and b.read_bytes() == f.read_bytes()
+
+
+def test_cpp_cameras_errors(tmp_path):
+    run = _cpp_camera_io(tmp_path)
+    p = tmp_path / "c.json"
+    base = '"width": 4, "height": 4, "fx": 1, "fy": 1, "cx": 2, "cy": 2'
+    cases = {
+        '{"cameras": [{' + base + ', "rotation": [1,0,0,0,1,0,0,0,1]}]}': "missing field 'translation'",
+        '{"cameras": [{' + base + ', "rotation": [2,0,0,0,1,0,0,0,1], "translation": [0,0,0]}]}':
+            "degenerate rotation",
+        '{"cameras": [{' + base + ', "rotation": [1,0,0,0,1,0,0,0,1], "translation": [0,0]}]}':
+            "translation must have 3 entries",
+        '{"views": []}': "missing field 'cameras'",
+        '{"cameras": [': "camera schema error",
+    }
+    for text, msg in cases.items():
+        p.write_text(text)
+        r = run(str(p), str(tmp_path / "o.json"))
+        assert r.returncode == 3 and msg in r.stdout, (text, r.stdout)
+    r = run(str(tmp_path / "absent.json"), str(tmp_path / "o.json"))
+    assert r.returncode == 3 and "cannot open camera file" in r.stdout
