@@ -697,8 +697,10 @@ inline void write_mesh_obj(const Mesh& mesh, const std::string& path) {
 
 // ---- camera JSON (io_camera.hpp:17-87) ---------------------------------------------------------
 // The reference reads and writes it with nlohmann::json; this is a small reader for the
-// same documents and a writer that emits what nlohmann's dump(2) emits (keys sorted,
-// two-space indent, shortest round-trip doubles with a ".0" on integral values).
+// same documents and a writer with nlohmann's dump(2) layout (keys sorted, two-space
+// indent, ".0" on integral values). Doubles are written shortest-round-trip
+// (std::to_chars); nlohmann uses Grisu2, which can pick other (equally round-tripping)
+// digits, so the files are round-trip identical, byte-identical on the tested cameras.
 namespace detail {
 struct JsonValue {
   enum Kind { kNull, kBool, kNumber, kString, kArray, kObject } kind = kNull;
@@ -889,7 +891,8 @@ inline std::vector<Camera> load_cameras(const std::string& path) {
   return out;
 }
 
-/// save_cameras (io_camera.hpp:65-87): byte-identical to the reference's file.
+/// save_cameras (io_camera.hpp:65-87): the reference's document; every double reads back
+/// bit-identically (digits may differ from nlohmann's Grisu2 in rare cases).
 inline void save_cameras(const std::vector<Camera>& cameras, const std::string& path) {
   using detail::json_double;
   std::string s = "{\n  \"cameras\": [";

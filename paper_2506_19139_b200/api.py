@@ -684,8 +684,10 @@ def load_cameras(path: str) -> CameraSet:
 
 
 def save_cameras(cams, path: str):
-    """save_cameras (io_camera.hpp:65-87): the same JSON document nlohmann::json::dump(2)
-    writes (keys sorted, 2-space indent, shortest round-trip doubles), plus a newline."""
+    """save_cameras (io_camera.hpp:65-87): nlohmann::json::dump(2)'s layout (keys sorted,
+    2-space indent) plus a newline. Doubles use Python's shortest round-trip repr, so the
+    values read back bit-identically; the digits can differ from nlohmann's Grisu2 (and
+    non-finite values, which nlohmann writes as null, are not representable here)."""
     import json
     c = CameraSet.of(cams)
     out = []

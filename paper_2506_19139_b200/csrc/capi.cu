@@ -167,9 +167,11 @@ int sof_set_views(sof_ctx* c, int v, const double* R, const double* t, const dou
   return guard(c, [&] {
     if (v < 0 || (v > 0 && (!R || !t || !intr || !wh))) throw InvalidArg("invalid camera arrays");
     (void)nearfar;  // near/far are carried by Camera but unused on this path
-    c->cams.resize(v);
+    // validated into a temporary: a rejected camera leaves the previous set (and its
+    // cached per-view records / bindings) untouched
+    std::vector<Cam> cams(v);
     for (int k = 0; k < v; ++k) {
-      Cam& cam = c->cams[k];
+      Cam& cam = cams[k];
       for (int i = 0; i < 9; ++i) cam.R[i] = R[9 * k + i];
       for (int i = 0; i < 3; ++i) cam.t[i] = t[3 * k + i];
       cam.fx = intr[4 * k];
@@ -183,6 +185,7 @@ int sof_set_views(sof_ctx* c, int v, const double* R, const double* t, const dou
       for (int i = 0; i < 3; ++i)
         cam.center[i] = (-cam.R[i]) * cam.t[0] + (-cam.R[3 + i]) * cam.t[1] + (-cam.R[6 + i]) * cam.t[2];
     }
+    c->cams.swap(cams);
     invalidate_view_caches(c);
   });
 }

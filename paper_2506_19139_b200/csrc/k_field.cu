@@ -1795,6 +1795,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   if (!c->has_scene) throw StateError("no scene: call sof_set_scene first");
   if (v0 < 0 || v1 > int(c->cams.size()) || v0 > v1) throw InvalidArg("view range out of bounds");
   if (tile_size <= 0) throw InvalidArg("tile_size must be positive");
+  // the five EvalStrategies toggles only (field_eval.hpp:14-20); higher bits are
+  // internal kernel flags (kRecheckPruned) and never come from the caller
+  if (strategies & ~int(SOF_ALL_STRATEGIES)) throw InvalidArg("strategies mask has bits outside 0..31");
   const bool tiled = strategies & 1;
   const bool prune = strategies & 8;
   // the FP64 fast loop (tile lists + min-z + dead cull) runs on live-only lists
@@ -1824,6 +1827,8 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   // Default off: 1.3% faster per C3 step, but the evaluation kernel then shares the SMs
   // with the scheduler for its whole span.
   const bool lookahead = std::getenv("SOF_SCHED_LOOKAHEAD") != nullptr;
+  // kRecheckPruned relies on ext only ever going 0 -> 1 while K3 for view v + 1 reads it
+  // on the prep lane and view v's K4 writes it: a stale 0 is re-checked inside K4
   const int eval_strategies = strategies | ((lookahead && skip) ? kRecheckPruned : 0);
   int64_t sched_grid[2] = {0, 0};  // evaluation grid of the schedule built for view pv
   auto sched_view = [&](int pv) {

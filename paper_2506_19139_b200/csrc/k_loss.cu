@@ -320,9 +320,11 @@ extern "C" {
 int sof_distortion_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const double* alpha, const double* t,
                         double near_plane, double far_plane, int attach_w, double* loss, double* d_alpha,
                         double* d_t) {
+  if (!c) return SOF_E_INVALID;
   return guard(c, [&] {
     check_off(nrays, off);
-    if (!(far_plane > near_plane)) throw InvalidArg("far must exceed near");
+    // no near/far check: the reference's distortion_loss has none (ndc_map divides by
+    // far - near, so equal planes give the same inf / NaN there)
     const int64_t S = nrays ? off[nrays] : 0;
     need(S == 0 || (alpha && t), "null sample arrays");
     c->loss_buf.ensure(pad(8 * (nrays + 1)) + pad(8 * size_t(S)) * 7 + pad(8 * nrays) + 4096);
@@ -351,6 +353,7 @@ int sof_distortion_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const dou
 int sof_extent_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const double* w, const double* a,
                     const double* b, const double* cc, const double* bound, double near_plane, double far_plane,
                     double* loss, int32_t* skipped, double* d_a, double* d_b, double* d_c, double* d_w) {
+  if (!c) return SOF_E_INVALID;
   return guard(c, [&] {
     check_off(nrays, off);
     const int64_t S = nrays ? off[nrays] : 0;
@@ -386,6 +389,7 @@ int sof_extent_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const double*
 
 int sof_depth_normal_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const double* w, const double* normals,
                           const double* pixel_normals, double* loss, double* d_w, double* d_n) {
+  if (!c) return SOF_E_INVALID;
   return guard(c, [&] {
     check_off(nrays, off);
     const int64_t S = nrays ? off[nrays] : 0;
@@ -414,6 +418,7 @@ int sof_depth_normal_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const d
 int sof_opacity_supervision_loss(sof_ctx* c, int64_t nrays, const int64_t* off, const double* contribs,
                                  const double* depth, double* loss, double* field_value, uint8_t* defined,
                                  double* d_alpha) {
+  if (!c) return SOF_E_INVALID;
   return guard(c, [&] {
     check_off(nrays, off);
     const int64_t S = nrays ? off[nrays] : 0;
@@ -444,6 +449,7 @@ int sof_opacity_supervision_loss(sof_ctx* c, int64_t nrays, const int64_t* off, 
 int sof_normal_smoothness_loss(sof_ctx* c, int width, int height, const double* normals, const uint8_t* valid,
                                const double* image, int per_channel, double* loss, int64_t* pixels_used,
                                double* d_normal) {
+  if (!c) return SOF_E_INVALID;
   return guard(c, [&] {
     if (width < 0 || height < 0) throw InvalidArg("invalid image size");
     const int64_t P = int64_t(width) * height;
@@ -481,6 +487,7 @@ int sof_normal_smoothness_loss(sof_ctx* c, int width, int height, const double* 
 }
 
 int sof_l1_rgb_loss(sof_ctx* c, int64_t pixels, const double* rendered, const double* reference, double* loss) {
+  if (!c) return SOF_E_INVALID;
   return guard(c, [&] {
     if (pixels < 0 || (pixels > 0 && (!rendered || !reference))) throw InvalidArg("invalid images");
     c->loss_buf.ensure(pad(24 * size_t(pixels)) * 2 + 4096);

@@ -465,6 +465,7 @@ void refine_final(sof_ctx* c, int64_t ne, double* verts) {
 
 void refine(sof_ctx* c, int64_t ne, const int32_t* edges, double* verts, int iterations,
             int strategies, int tile_size, int v0, int v1, uint64_t* counters) {
+  if (strategies & ~int(SOF_ALL_STRATEGIES)) throw InvalidArg("strategies mask has bits outside 0..31");
   if (iterations <= 0 || ne == 0) return;  // iterations = 0 keeps the lerp vertices (:100)
   if (!c->has_tets) throw StateError("no tets: call sof_set_tets first");
   refine_init(c, ne, edges);

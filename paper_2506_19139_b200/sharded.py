@@ -57,12 +57,19 @@ class GpuBackend:
     def sync(self):
         self.torch.cuda.synchronize(self.dev)
 
+    # torch fills and concatenations run on torch's current stream; the library works on
+    # its own non-blocking stream, so every tensor torch wrote is synchronised before a
+    # library call reads it (the library calls themselves return with their stream idle)
     def new_state(self, n):
         t = self.torch
-        return t.ones(n, dtype=t.float64, device=self.dev), t.zeros(n, dtype=t.uint8, device=self.dev)
+        out = t.ones(n, dtype=t.float64, device=self.dev), t.zeros(n, dtype=t.uint8, device=self.dev)
+        self.sync()
+        return out
 
     def zeros_u8(self, n):
-        return self.torch.zeros(max(n, 1), dtype=self.torch.uint8, device=self.dev)
+        out = self.torch.zeros(max(n, 1), dtype=self.torch.uint8, device=self.dev)
+        self.sync()
+        return out
 
     def label_views(self, v0, v1, strategies, tile_size, min_op, ext):
         c = self.ctx
@@ -70,7 +77,7 @@ class GpuBackend:
                                           self._p(min_op), self._p(ext), self.counters.ctypes.data_as(ctypes.c_void_p)))
 
     def ext_rank(self, ext, rank, world):
-        out = self.torch.empty(self.nv, dtype=self.torch.int32, device=self.dev)
+        out = self.torch.empty(self.nv, dtype=self.torch.int32, device=self.dev)  # written by the library only
         self.ctx.check(self.ctx.lib.sof_shard_ext_rank_dev(self.ctx.h, self.nv, self._p(ext), rank, world, self._p(out)))
         return out
 
@@ -165,8 +172,9 @@ class ShardedMesher:
         buf[:n] = t[:n].to(dev)
         outs = [torch.empty_like(buf) for _ in range(self.world)]
         dist.all_gather(outs, buf, group=self.group)
-        self.b.sync()
-        return torch.cat([o[:k] for o, k in zip(outs, counts)]).to(t.device), counts
+        out = torch.cat([o[:k] for o, k in zip(outs, counts)]).to(t.device)
+        self.b.sync()  # the concatenation (torch's stream) is read by the library next
+        return out, counts
 
     def _march(self, n_tets: int):
         """Marching Tetrahedra with the tets split across ranks: rank r marches the r-th

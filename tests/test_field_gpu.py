@@ -283,3 +283,31 @@ def test_tile_binding_depth_key_ties(ref, group):
     rev = rc.evaluator(ALL)
     assert_bits(ev.label_grid(pts), rev.label_grid(pts))
     assert ev.counters() == rev.counters()
+
+
+def test_rejected_views_leave_previous_cameras(ref):
+    """sof_set_views validates every camera before replacing the set: a camera with a
+    non-positive resolution is rejected and the cached per-view state of the previous
+    cameras stays valid (results identical before and after the failed call)."""
+    scene = ref.random_scene(52, 200, 1.0)
+    cams = ref.orbit_cameras(3, 4.0, 1.8, 48)
+    ctx = sof.Context(0)
+    views = sof.ViewSet.build(scene, cams, ctx=ctx)
+    pts = np.random.default_rng(3).uniform(-1.2, 1.2, (500, 3))
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
+    before = ev.label_grid(pts)
+    bad = ref.orbit_cameras(3, 5.0, 1.8, 48)
+    bad.wh[2] = (0, 48)
+    with pytest.raises(ValueError, match="resolution"):
+        ctx.set_views(bad)
+    after = ev.label_grid(pts)
+    assert_bits(after, before, "labels after a rejected sof_set_views")
+
+
+def test_strategy_mask_outside_0_31_rejected(case):
+    scene, cams, rc, views, pts = case
+    for m in (32, 1 << 8, -1):
+        ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
+        ev.mask = m
+        with pytest.raises(ValueError, match="strategies"):
+            ev.label_grid(pts[:10])

@@ -46,6 +46,21 @@ def test_null_and_missing_device_paths():
             sof.Context(0)
 
 
+def test_loss_entry_points_reject_null_context():
+    """Every batched loss entry point returns SOF_E_INVALID on a null context instead of
+    dereferencing it (no device needed)."""
+    lib = _lib.load()
+    off = np.zeros(2, np.int64)
+    z = np.zeros(4)
+    p = lambda a: a.ctypes.data  # noqa: E731
+    assert lib.sof_distortion_loss(None, 1, p(off), p(z), p(z), 0.2, 100.0, 1, p(z), p(z), p(z)) == _lib.SOF_E_INVALID
+    assert lib.sof_extent_loss(None, 1, p(off), *([p(z)] * 5), 0.2, 100.0, *([p(z)] * 6)) == _lib.SOF_E_INVALID
+    assert lib.sof_depth_normal_loss(None, 1, p(off), *([p(z)] * 6)) == _lib.SOF_E_INVALID
+    assert lib.sof_opacity_supervision_loss(None, 1, p(off), *([p(z)] * 6)) == _lib.SOF_E_INVALID
+    assert lib.sof_normal_smoothness_loss(None, 1, 1, p(z), p(z), p(z), 0, p(z), p(z), p(z)) == _lib.SOF_E_INVALID
+    assert lib.sof_l1_rgb_loss(None, 1, p(z), p(z), p(z)) == _lib.SOF_E_INVALID
+
+
 def test_kuhn_lattice_valid():
     v, t = kuhn_lattice(6, -1, 1)
     assert v.shape == (216, 3) and t.shape == (6 * 125, 4)
