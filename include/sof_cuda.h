@@ -275,13 +275,18 @@ int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);
 
 /* ---- sorted rasterizer -------------------------------------------------------------- */
 /* render_depth_map (render.hpp:26-51) plus render_pixel's colour / final
- * transmittance (opacity_field.hpp:201-219) for one view, with the exact per-pixel
- * (t*, index) resort of collect_contributions (opacity_field.hpp:39-61).
- * Outputs [h*w] row-major (rgb [h*w*3]); any output may be NULL.
- * stats (nullable) uint64[4] = {tested pairs, contributing pairs, kbuffer overflow
- * pixels, exact-depth fallbacks}. */
+ * transmittance / accumulated opacity (opacity_field.hpp:192-219) for one view, with the
+ * exact per-pixel (t*, index) sort of collect_contributions (opacity_field.hpp:39-61);
+ * every output bit-identical. Outputs [h*w] row-major (rgb [h*w*3]); any may be NULL.
+ * stats (nullable) uint64[4] = {tested (pixel, list entry) pairs, contributions, pixels
+ * with more than 1024 contributions (CTA-wide sort), exact-depth fallbacks}. */
 int sof_render_view(sof_ctx* ctx, int view, int depth_mode, int tile_size, double* depth,
                     double* opacity, double* rgb, double* t_final, uint64_t* stats);
+
+/* Scratch budget (bytes) of one render band: a frame whose per-pixel contribution slices
+ * (40 B per candidate) exceed it is rendered in bands of tiles. 0 restores the default
+ * (24 GiB). An sm_100a implementation knob; results do not depend on it. */
+int sof_set_render_pool(sof_ctx* ctx, int64_t bytes);
 
 /* normal_from_depth (render.hpp:60-88) of the depth map of the last sof_render_view
  * call for `view`, computed from the device-resident depth (no round trip; the `sof

@@ -436,13 +436,26 @@ class RefContext:
     def render_maps(self, view: int, depth_path: str, normal_path: str, exact: bool = True, threads: int = 0):
         self.ref.lib.sofref_render_maps(self.h, view, int(exact), threads, depth_path.encode(), normal_path.encode())
 
-    def render_pixels(self, view: int, pix, exact: bool = True) -> dict:
+    def render_pixels(self, view: int, pix, exact: bool = True, threads: int = 1) -> dict:
+        """collect_contributions + render_pixel per pixel. threads > 1 splits the pixels
+        over host threads (ctypes releases the GIL; the reference call is const)."""
         pix = np.ascontiguousarray(pix, np.int32)
         n = len(pix)
         out = {"color": np.empty((n, 3)), "depth": np.empty(n), "acc": np.empty(n), "tfinal": np.empty(n),
                "ncontrib": np.empty(n, np.int32)}
-        self.ref.lib.sofref_render_pixels(self.h, view, int(exact), n, _ptr(pix), *(_ptr(out[k]) for k in
-                                          ("color", "depth", "acc", "tfinal", "ncontrib")))
+
+        def run(a, b):
+            if b > a:
+                self.ref.lib.sofref_render_pixels(self.h, view, int(exact), b - a, _ptr(pix[a:b]),
+                                                  *(_ptr(out[k][a:b]) for k in
+                                                    ("color", "depth", "acc", "tfinal", "ncontrib")))
+        if threads <= 1 or n < 2 * threads:
+            run(0, n)
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            cuts = np.linspace(0, n, 4 * threads + 1).astype(int)
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(lambda k: run(cuts[k], cuts[k + 1]), range(len(cuts) - 1)))
         return out
 
     def collect_contributions(self, view: int, px: int, py: int) -> dict:

@@ -160,12 +160,23 @@ struct BisectScratch {
   DBuf<int> bail;
 };
 
+// Sorted rasterizer scratch (k_render.cu): per-view render binning, per-pixel slices of
+// contributions and their sorted order.
 struct RenderScratch {
-  DBuf<uint64_t> keys, keys2;
-  DBuf<double> alpha, alpha2;
-  DBuf<int32_t> vals, vals2, pixel, istate, count;
-  DBuf<int64_t> begin, end;
-  DBuf<double> state;
+  DBuf<int4> rect;                // [n] tile rectangle per Gaussian
+  DBuf<uint32_t> gcnt;            // [n] tiles per Gaussian
+  DBuf<uint32_t> tile_cnt;        // [T] entries per tile (histogram) | scatter cursors
+  DBuf<int64_t> tile_off;         // [T + 1]
+  DBuf<int32_t> ent;              // [entries] Gaussian ids grouped by tile (any order inside)
+  DBuf<int32_t> big;              // Gaussians (binning) / pixels (sort) handled cooperatively
+  DBuf<int32_t> big_cnt;          // [4] counts of those lists
+  DBuf<uint32_t> pcnt;            // [T * 256] per-pixel bound (conic-passing records)
+  DBuf<uint32_t> ncon;            // [T * 256] per-pixel contributions
+  DBuf<int64_t> poff;             // [T * 256 + 1] slice offsets (tile-major pixel order)
+  DBuf<int64_t> band_off;         // [T + 1] slice offset of each tile's first pixel
+  DBuf<double> et, ea, eA, eB;    // per contribution: t*, alpha, a, b (opacity_field.hpp:13-19)
+  DBuf<int32_t> ei;               // Gaussian index
+  DBuf<char> rrec;                // [n] per-view render records (k_render.cu RRec, 128 B)
 };
 
 enum ProfKind { kProfEval = 0, kProfPrep = 1, kProfSched = 2, kProfKinds = 4 };
@@ -238,7 +249,6 @@ struct sof_ctx {
   int64_t bin_m = 0;               // Gaussians with tiles in the current binning
   const unsigned long long* bin_zmax = nullptr;  // bisection-cache binning filter (per tile)
   sofk::BisectScratch bis;
-  bool render_attr_set = false;  // k_render's dynamic shared-memory limit set on this device
   sofk::DBuf<int32_t> gidx_in, gidx_out;
   sofk::DBuf<int64_t> goff;
   sofk::DBuf<uint32_t> ekey_in, ekey_out;
@@ -247,21 +257,22 @@ struct sof_ctx {
   sofk::PointSchedule sched;
   sofk::PointSchedule sched_alt;          // second set of per-view schedule buffers
   sofk::MeshScratch ms;
-  sofk::Binding rbind;                    // render binding (lists ordered by a t* lower bound)
   sofk::RenderScratch rs;
   sofk::GroupScratch grp;
   sofk::DBuf<double> seeds;               // build_seed_points result
   sofk::DBuf<uint8_t> seed_prov;
   int64_t n_seeds = -1;                 // spill pool of k-buffer-overflow pixels
   sofk::DBuf<double> r_out;               // depth, opacity, rgb(3), t_final per pixel
-  sofk::DBuf<double> r_lkey;              // per-Gaussian t* lower bound of the render binning
   sofk::DBuf<unsigned long long> r_stats;
   sofk::DBuf<double> r_normal, r_depth_in;  // normal_from_depth output / uploaded depth
   sofk::DBuf<uint8_t> r_valid;
   sofk::DBuf<char> r_query;                 // gaussian_normal queries
   sofk::DBuf<unsigned char> io_bytes;       // scene PLY payload / encoded records
   int r_view = -1;                          // view whose render is in r_out
+  int64_t r_bands = 0;                      // tile bands of the last render
+  int64_t render_pool = int64_t(24) << 30;  // scratch budget of one render band (bytes)
   sofk::DBuf<char> cub_tmp;
+  sofk::DBuf<char> scan_tmp;                 // block totals of the hand-written scans (k_scan.cu)
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
   sofk::DBuf<int64_t> d_scalar;               // small device scalars
 
@@ -357,6 +368,10 @@ void sort_pairs_u32(sof_ctx* c, const uint32_t* kin, uint32_t* kout, const int32
                     int32_t* vout, int64_t n, int end_bit);
 void exclusive_scan_u32_to_i64(sof_ctx* c, const uint32_t* in, int64_t* out, int64_t n);
 void exclusive_scan_i32(sof_ctx* c, const int32_t* in, int32_t* out, int64_t n);
+// hand-written scans (k_scan.cu) on c->stream: out[0..n] exclusive, out[n] = total
+void scan_u32_i64(sof_ctx* c, const uint32_t* in, int64_t* out, int64_t n);
+void scan_i32_i32(sof_ctx* c, const int32_t* in, int32_t* out, int64_t n);
+void scan_i64_i64(sof_ctx* c, const int64_t* in, int64_t* out, int64_t n);
 int bits_for(uint64_t max_value);
 template <typename T>
 inline T read_scalar(sof_ctx* c, const T* dev) {
