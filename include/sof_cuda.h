@@ -279,12 +279,17 @@ int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);
  * exact per-pixel (t*, index) sort of collect_contributions (opacity_field.hpp:39-61);
  * every output bit-identical. Outputs [h*w] row-major (rgb [h*w*3]); any may be NULL.
  * stats (nullable) uint64[4] = {tested (pixel, list entry) pairs, contributions, pixels
- * with more than 1024 contributions (CTA-wide sort), exact-depth fallbacks}. */
+ * with more than 256 contributions (CTA-wide sort), exact-depth fallbacks}. */
 int sof_render_view(sof_ctx* ctx, int view, int depth_mode, int tile_size, double* depth,
                     double* opacity, double* rgb, double* t_final, uint64_t* stats);
 
+/* Per-pixel contribution counts [h*w] of the last sof_render_view of `view` (the length
+ * of each pixel's collect_contributions list, opacity_field.hpp:39-61). SOF_E_STATE if
+ * that view was not the last one rendered. */
+int sof_render_counts(sof_ctx* ctx, int view, uint32_t* counts);
+
 /* Scratch budget (bytes) of one render band: a frame whose per-pixel contribution slices
- * (40 B per candidate) exceed it is rendered in bands of tiles. 0 restores the default
+ * (16 B per candidate) exceed it is rendered in bands of tiles. 0 restores the default
  * (24 GiB). An sm_100a implementation knob; results do not depend on it. */
 int sof_set_render_pool(sof_ctx* ctx, int64_t bytes);
 

@@ -77,6 +77,7 @@ _SIGS = {
     "sof_render_view": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "sof_render_normals": (_I, [_P, _I, _P, _P]),
     "sof_set_render_pool": (_I, [_P, _I64]),
+    "sof_render_counts": (_I, [_P, _I, _P]),
     "sof_normal_from_depth": (_I, [_P, _I, _P, _P, _P]),
     "sof_gaussian_normals": (_I, [_P, ctypes.c_int64, _P, _P, _P, _P, _P]),
     "sof_seed_points": (_I, [_P, _I, _I, _D, _P]),

@@ -416,7 +416,7 @@ def extract_resident(ctx: Context, opt: ExtractOptions, stats: dict | None = Non
 
 
 def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile_size: int = 16,
-                normals: bool = False) -> dict:
+                normals: bool = False, counts: bool = False) -> dict:
     """render_depth_map (render.hpp:26-51) + render_pixel colour / T (opacity_field.hpp:201-219);
     with normals=True also normal_from_depth (render.hpp:60-88) of the depth, computed on
     the device from the resident depth map."""
@@ -426,6 +426,9 @@ def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile
            "t_final": np.empty((h, w)), "stats": np.zeros(4, np.uint64)}
     ctx.check(ctx.lib.sof_render_view(ctx.h, view, depth_mode, tile_size, _ptr(out["depth"]), _ptr(out["opacity"]),
                                       _ptr(out["rgb"]), _ptr(out["t_final"]), _ptr(out["stats"])))
+    if counts:  # per-pixel contribution counts (len(collect_contributions))
+        out["counts"] = np.empty((h, w), np.uint32)
+        ctx.check(ctx.lib.sof_render_counts(ctx.h, view, _ptr(out["counts"])))
     if normals:
         out["normal"] = np.empty((h, w, 3))
         out["normal_valid"] = np.empty((h, w), np.uint8)

@@ -45,10 +45,8 @@ constexpr int kRTile = 16;                // render tile (pixels per side), one 
 constexpr int kRPix = kRTile * kRTile;    // 256 pixels per tile
 constexpr int kRChunk = 32;               // records staged per step
 constexpr int kBigTiles = 64;             // Gaussians covering more tiles are binned by a CTA
-constexpr int kSortCap = 1024;            // slice length sorted by one warp in shared memory
-constexpr int kSortSlotBits = 10;         // log2(kSortCap)
-constexpr int kSortWarps = 4;
-constexpr int kEntryBytes = 4 * 8 + 4;  // et, ea, eA, eB, ei
+constexpr int kSortWarps = 8;
+constexpr int kEntryBytes = 16;  // REnt
 
 // Pixel of local index l (0..255) in a tile: warp w = l / 32 covers an 8 x 4 block.
 __device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int l, int& x, int& y) {
@@ -382,26 +380,29 @@ __global__ void __launch_bounds__(kRPix) k_rcount(Cam cam, int tiles_x, const in
 
 // ---- R2: FP64 contribution tests -----------------------------------------------------------------
 
-// The contributions of pixel q occupy [poff[q] - base, + ncon[q]) of each array (SoA);
-// R3 sorts them in place by (t*, index).
-struct REntries {
-  double* t;      // t* (peak_t)
-  double* alpha;  // clamped peak alpha
-  double* a;      // A (abc_cached)
-  double* b;      // B
-  int32_t* idx;   // Gaussian index
+// One contribution of a pixel ray (RayContribution, opacity_field.hpp:13-19, reduced to
+// what the sort and the blend cannot recompute cheaply): t* and the Gaussian index are
+// the sort key (:56-59); pos is the record's position in the tile list. A, B and alpha
+// are recomputed from the record in R4 with the same expressions (same bits). The
+// contributions of pixel q occupy [poff[q] - base, + ncon[q]); R3 sorts them in place.
+struct __align__(16) REnt {
+  double t;
+  int32_t pos;
+  int32_t idx;
 };
+static_assert(sizeof(REnt) == 16, "entry layout");
 
 __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0, const int64_t* __restrict__ toff,
                                                  const int32_t* __restrict__ ent, const RRec* __restrict__ recs,
-                                                 const int64_t* __restrict__ poff, int64_t base, REntries E,
+                                                 const int64_t* __restrict__ poff, int64_t base, REnt* E,
                                                  uint32_t* ncon, unsigned long long* stats) {
   __shared__ __align__(16) RRec srec[kRChunk];
   __shared__ int32_t sidx[kRChunk];
   __shared__ double sray[3][kRPix];
   __shared__ int64_t sbase[kRPix];
   __shared__ int scur[kRPix];
-  __shared__ uint16_t queue[kRPix / 32][32 * kRChunk];
+  __shared__ uint16_t queue[kRPix * kRChunk];
+  __shared__ int swarp[kRPix / 32];
   __shared__ __align__(16) double s_exp[128];
   const int tile = tile0 + int(blockIdx.x), l = threadIdx.x, w = l >> 5, lane = l & 31;
   int x, y;
@@ -435,7 +436,8 @@ __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0
         const float4* f = reinterpret_cast<const float4*>(&srec[k]) + 6;
         if (!rcull(f[0], f[1], cu, cv)) mask |= 1u << k;
       }
-    // compact the warp's surviving (pixel, record) pairs into its queue
+    // compact the CTA's surviving (pixel, record) pairs into one queue: warp prefix sums,
+    // then the warps' offsets, so the FP64 work is spread over all 256 threads
     const int np = __popc(mask);
     int at = np;
 #pragma unroll
@@ -443,27 +445,35 @@ __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0
       const int u = __shfl_up_sync(0xffffffffu, at, s);
       if (lane >= s) at += u;
     }
-    const int total = __shfl_sync(0xffffffffu, at, 31);
-    at -= np;
+    if (lane == 31) swarp[w] = at;
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < kRPix / 32; ++k) {
+      const int c = swarp[k];
+      before += (k < w) ? c : 0;
+      total += c;
+    }
+    at += before - np;
     while (mask) {
       const int k = __ffs(mask) - 1;
       mask &= mask - 1;
-      queue[w][at++] = uint16_t((lane << 5) | k);
+      queue[at++] = uint16_t((l << 5) | k);
     }
-    __syncwarp();
-    // FP64 tests on every lane
-    for (int qi = lane; qi < total; qi += 32) {
-      const int v = queue[w][qi];
-      const int pl = (w << 5) | (v >> 5), k = v & 31;
+    __syncthreads();
+    // FP64 tests on every thread
+    for (int qi = l; qi < total; qi += kRPix) {
+      const int v = queue[qi];
+      const int pl = v >> 5, k = v & 31;
       const double d[3] = {sray[0][pl], sray[1][pl], sray[2][pl]};
       double t_star, alpha, a, b;
       if (contribution(srec[k], d, tab, t_star, alpha, a, b)) {
         const int64_t o = sbase[pl] + atomicAdd(&scur[pl], 1);
-        E.t[o] = t_star;
-        E.alpha[o] = alpha;
-        E.a[o] = a;
-        E.b[o] = b;
-        E.idx[o] = sidx[k];
+        REnt e;
+        e.t = t_star;
+        e.pos = int32_t(b0 - l0) + k;
+        e.idx = sidx[k];
+        E[o] = e;
       }
     }
     __syncthreads();
@@ -476,155 +486,304 @@ __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0
 }
 
 // ---- R3: per-pixel sort by (t*, index), in place ---------------------------------------------------
+//
+// A pixel's contributions are sorted by 64-bit keys held in registers: t* > 0, so its bit
+// pattern orders like the value, and k = ((bits(t*) - bits(min t*)) << 9) | slot is an
+// exact key of t* whenever the slice's t* span is below 2^55 ulps (checked; a wider span
+// takes the exact fallback). Keys equal above the slot bits are equal t* values, ordered
+// by Gaussian index afterwards (rare). The bitonic network runs on NT threads x E keys in
+// the striped layout (position i = NT e + tid): partners within a warp exchange through
+// shuffles, partners in another warp through shared memory, partners in the same thread
+// in registers. Only 8 bytes move per key and stage (sorting the 16-byte entries
+// themselves was shared-memory-bandwidth bound); the entries are permuted once at the end.
 
-__device__ __forceinline__ bool entry_less(const double* __restrict__ t, const int32_t* __restrict__ idx, int64_t a,
-                                           int64_t b) {
-  const double ta = t[a], tb = t[b];
-  return ta < tb || (ta == tb && idx[a] < idx[b]);
+__device__ __forceinline__ bool rent_less(const REnt& a, const REnt& b) {
+  return a.t < b.t || (a.t == b.t && a.idx < b.idx);
 }
 
-// Ascending sort of m (power of two, 32..kSortCap) keys in shared memory by one warp:
-// the bitonic network in its "flip" form (every compare-exchange puts the smaller key at
-// the lower position), so +inf padding stays at the end.
-__device__ __forceinline__ void warp_sort_keys(uint64_t* k, int m, int lane) {
-  for (int size = 2; size <= m; size <<= 1) {
-    const int h = size >> 1;
-    __syncwarp();
-    for (int i = lane; i < (m >> 1); i += 32) {  // flip: i against its mirror in the block
-      const int lo = (i / h) * size + (i % h), hi = (i / h) * size + size - 1 - (i % h);
-      const uint64_t a = k[lo], b = k[hi];
-      if (b < a) {
-        k[lo] = b;
-        k[hi] = a;
+__device__ __forceinline__ REnt rent_pad() {
+  REnt e;
+  e.t = INFINITY;
+  e.pos = 0;
+  e.idx = INT_MAX;
+  return e;
+}
+
+// 16-byte moves of an entry (one LDS/STS/LDG/STG.128 each)
+__device__ __forceinline__ REnt ld_rent(const REnt* p) {
+  const int4 v = *reinterpret_cast<const int4*>(p);
+  REnt e;
+  e.t = __hiloint2double(v.y, v.x);
+  e.pos = v.z;
+  e.idx = v.w;
+  return e;
+}
+__device__ __forceinline__ void st_rent(REnt* p, const REnt& e) {
+  *reinterpret_cast<int4*>(p) = make_int4(__double2loint(e.t), __double2hiint(e.t), e.pos, e.idx);
+}
+
+// Warp-private barrier: a named barrier (bar.sync id, 32) per warp, so the per-pixel loop
+// needs no proof of warp convergence (__syncwarp there compiles to the slow collective
+// form). NT == 32: warp w's barrier; otherwise the CTA barrier.
+template <int NT>
+__device__ __forceinline__ void sorter_sync(int w) {
+  if (NT == 32) asm volatile("bar.sync %0, 32;" ::"r"(w + 1) : "memory");
+  else __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  const uint32_t lo = __shfl_xor_sync(0xffffffffu, uint32_t(v), m);
+  const uint32_t hi = __shfl_xor_sync(0xffffffffu, uint32_t(v >> 32), m);
+  return (uint64_t(hi) << 32) | lo;
+}
+
+// in-thread stage: elements e and e + ES (ES < E, compile time)
+template <int NT, int E, int ES>
+__device__ __forceinline__ void keys_inthread(uint64_t (&k)[E], int size, int tid) {
+  if constexpr (ES < E) {
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if ((e & ES) == 0) {
+        const bool asc = ((NT * e + tid) & size) == 0;
+        const uint64_t a = k[e], b = k[e + ES];
+        const bool sw = asc ? (b < a) : (a < b);
+        k[e] = sw ? b : a;
+        k[e + ES] = sw ? a : b;
       }
-    }
-    for (int stride = size >> 2; stride > 0; stride >>= 1) {
-      __syncwarp();
-      for (int i = lane; i < (m >> 1); i += 32) {
-        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const uint64_t a = k[lo], b = k[hi];
-        if (b < a) {
-          k[lo] = b;
-          k[hi] = a;
+  }
+}
+
+// ascending bitonic sort of NT x E keys (position i = NT e + tid); xb: NT x E u64 scratch
+template <int NT, int E>
+__device__ __forceinline__ void sort_keys(uint64_t (&k)[E], int tid, int w, uint64_t* xb) {
+  constexpr int M = NT * E;
+  const int lane = tid & 31;
+#pragma unroll 1
+  for (int lg = 1; (1 << lg) <= M; ++lg) {
+    const int size = 1 << lg;
+#pragma unroll 1
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= NT) {
+        const int es = stride / NT;
+        if (es == 1) keys_inthread<NT, E, 1>(k, size, tid);
+        else if (es == 2) keys_inthread<NT, E, 2>(k, size, tid);
+        else if (es == 4) keys_inthread<NT, E, 4>(k, size, tid);
+        else if (es == 8) keys_inthread<NT, E, 8>(k, size, tid);
+      } else if (stride < 32) {
+        const bool lower = (lane & stride) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t p = shfl_xor_u64(k[e], stride);
+          const bool take_min = lower == (((NT * e + tid) & size) == 0);
+          k[e] = take_min ? (p < k[e] ? p : k[e]) : (k[e] < p ? p : k[e]);
         }
+      } else {  // partner thread in another warp: exchange through shared memory
+#pragma unroll
+        for (int e = 0; e < E; ++e) xb[NT * e + tid] = k[e];
+        sorter_sync<NT>(w);
+        const bool lower = (tid & stride) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t p = xb[(NT * e + tid) ^ stride];
+          const bool take_min = lower == (((NT * e + tid) & size) == 0);
+          k[e] = take_min ? (p < k[e] ? p : k[e]) : (k[e] < p ? p : k[e]);
+        }
+        sorter_sync<NT>(w);
       }
     }
   }
-  __syncwarp();
 }
 
-// Permutes one field of a slice in place: f[i] = f[perm[i]] for i < n (staged in K).
-template <typename T>
-__device__ __forceinline__ void apply_perm(T* f, const uint16_t* perm, uint64_t* K, int n, int lane) {
-  for (int i = lane; i < n; i += 32) {
-    T v = f[perm[i]];
-    uint64_t u = 0;
-    memcpy(&u, &v, sizeof(T));
-    K[i] = u;
-  }
-  __syncwarp();
-  for (int i = lane; i < n; i += 32) {
-    T v;
-    const uint64_t u = K[i];
-    memcpy(&v, &u, sizeof(T));
-    f[i] = v;
-  }
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(kSortWarps * 32) k_rsort(int64_t q0, int64_t nq, const int64_t* __restrict__ poff,
-                                                          int64_t base, const uint32_t* __restrict__ ncon,
-                                                          REntries E, int32_t* big, int32_t* big_cnt) {
-  __shared__ uint64_t sk[kSortWarps][kSortCap];
-  __shared__ uint16_t sp[kSortWarps][kSortCap];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* K = sk[w];
-  uint16_t* perm = sp[w];
-  for (int64_t qq = int64_t(blockIdx.x) * kSortWarps + w; qq < nq; qq += int64_t(gridDim.x) * kSortWarps) {
-    const int64_t q = q0 + qq;
-    const int n = int(ncon[q]);
-    if (n <= 1) continue;
-    if (n > kSortCap) {
-      if (lane == 0) {
-        big[atomicAdd(big_cnt, 1)] = int32_t(q);
-        atomicAdd(big_cnt + 1, 1);  // frame total (stats)
-      }
-      continue;
+// Sorts S[0, n) (n <= NT E) in place. buf: NT E x 16 B of shared memory. Returns false
+// (nothing changed) when the t* span does not fit the 55-bit key.
+template <int NT, int E>
+__device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int tid, int w, void* buf,
+                                                uint64_t* red) {
+  constexpr int M = NT * E;
+  constexpr uint64_t kSlot = 511u;
+  static_assert(M <= 4096, "slot bits");
+  constexpr int SB = (M <= 512) ? 9 : 12;  // slot bits
+  constexpr uint64_t kLow = (uint64_t(1) << SB) - 1;
+  (void)kSlot;
+  uint64_t tb[E];
+  uint64_t lo = ~uint64_t(0), hi = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = NT * e + tid;
+    tb[e] = (i < n) ? uint64_t(__double_as_longlong(S[i].t)) : 0;
+    if (i < n) {
+      lo = min(lo, tb[e]);
+      hi = max(hi, tb[e]);
     }
-    const int64_t o = poff[q] - base;
-    int m = 32;
-    while (m < n) m <<= 1;
-    double* T = E.t + o;
-    int32_t* I = E.idx + o;
-    // t* > 0: its bit pattern orders like the value; the low bits carry the slot
-    constexpr uint64_t kLow = (uint64_t(1) << kSortSlotBits) - 1;
-    for (int i = lane; i < m; i += 32)
-      K[i] = (i < n) ? ((uint64_t(__double_as_longlong(T[i])) & ~kLow) | uint64_t(i)) : ~uint64_t(0);
-    warp_sort_keys(K, m, lane);
-    // keys equal above the slot bits are ordered exactly by (t*, index) — rare
-    bool tie = false;
-    for (int i = lane; i + 1 < n; i += 32) tie |= (K[i] >> kSortSlotBits) == (K[i + 1] >> kSortSlotBits);
-    if (__any_sync(0xffffffffu, tie) && lane == 0) {
-      for (int i = 1; i < n; ++i) {  // insertion sort: only equal-prefix runs move
-        const uint64_t v = K[i];
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    lo = min(lo, shfl_xor_u64(lo, s));
+    hi = max(hi, shfl_xor_u64(hi, s));
+  }
+  if (NT > 32) {  // across the warps of the CTA
+    if ((tid & 31) == 0) {
+      red[2 * (tid >> 5)] = lo;
+      red[2 * (tid >> 5) + 1] = hi;
+    }
+    __syncthreads();
+    for (int k = 0; k < NT / 32; ++k) {
+      lo = min(lo, red[2 * k]);
+      hi = max(hi, red[2 * k + 1]);
+    }
+    __syncthreads();
+  }
+  if (hi - lo >= (uint64_t(1) << (64 - SB))) return false;
+  uint64_t k[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = NT * e + tid;
+    k[e] = (i < n) ? (((tb[e] - lo) << SB) | uint64_t(i)) : ~uint64_t(0);
+  }
+  uint64_t* xb = static_cast<uint64_t*>(buf);
+  sort_keys<NT, E>(k, tid, w, xb);
+  // equal t* at neighbouring positions: order by Gaussian index (rare)
+#pragma unroll
+  for (int e = 0; e < E; ++e) xb[NT * e + tid] = k[e];
+  sorter_sync<NT>(w);
+  bool tie = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = NT * e + tid;
+    if (i + 1 < n && (xb[i] >> SB) == (xb[i + 1] >> SB)) tie = true;
+  }
+  const bool any_tie = (NT == 32) ? __any_sync(0xffffffffu, tie) : __syncthreads_or(tie);
+  if (any_tie) {
+    if (tid == 0)
+      for (int i = 1; i < n; ++i) {  // insertion sort on the index inside equal-t* runs
+        const uint64_t v = xb[i];
         int j = i - 1;
-        while (j >= 0 && entry_less(T, I, int64_t(v & kLow), int64_t(K[j] & kLow))) {
-          K[j + 1] = K[j];
+        while (j >= 0 && (xb[j] >> SB) == (v >> SB) && S[v & kLow].idx < S[xb[j] & kLow].idx) {
+          xb[j + 1] = xb[j];
           --j;
         }
-        K[j + 1] = v;
+        xb[j + 1] = v;
       }
+    sorter_sync<NT>(w);
+#pragma unroll
+    for (int e = 0; e < E; ++e) k[e] = xb[NT * e + tid];
+  }
+  sorter_sync<NT>(w);
+  // permute the entries through shared memory
+  REnt* stage = static_cast<REnt*>(buf);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = NT * e + tid;
+    if (i < n) st_rent(stage + i, ld_rent(S + (k[e] & kLow)));
+  }
+  sorter_sync<NT>(w);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = NT * e + tid;
+    if (i < n) st_rent(S + i, ld_rent(stage + i));
+  }
+  sorter_sync<NT>(w);
+  return true;
+}
+
+__device__ __forceinline__ void swap_rent(REnt* S, int64_t a, int64_t b) {
+  const REnt t = ld_rent(S + a);
+  st_rent(S + a, ld_rent(S + b));
+  st_rent(S + b, t);
+}
+
+// Exact fallback for one CTA (any n): the flip-bitonic network directly on the entries in
+// global memory (positions >= n act as +inf: compare-exchanges touching them are no-ops).
+__device__ void sort_slice_global(REnt* S, int64_t n) {
+  int64_t m = 1;
+  while (m < n) m <<= 1;
+  for (int64_t size = 2; size <= m; size <<= 1) {
+    const int64_t h = size >> 1;
+    for (int64_t i = threadIdx.x; i < (m >> 1); i += blockDim.x) {
+      const int64_t lo = (i / h) * size + (i % h), hi = (i / h) * size + size - 1 - (i % h);
+      if (hi < n && rent_less(ld_rent(S + hi), ld_rent(S + lo))) swap_rent(S, lo, hi);
     }
-    __syncwarp();
-    for (int i = lane; i < n; i += 32) perm[i] = uint16_t(K[i] & kLow);
-    __syncwarp();
-    apply_perm(T, perm, K, n, lane);
-    apply_perm(E.alpha + o, perm, K, n, lane);
-    apply_perm(E.a + o, perm, K, n, lane);
-    apply_perm(E.b + o, perm, K, n, lane);
-    apply_perm(I, perm, K, n, lane);
+    __syncthreads();
+    for (int64_t stride = size >> 2; stride > 0; stride >>= 1) {
+      for (int64_t i = threadIdx.x; i < (m >> 1); i += blockDim.x) {
+        const int64_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        if (hi < n && rent_less(ld_rent(S + hi), ld_rent(S + lo))) swap_rent(S, lo, hi);
+      }
+      __syncthreads();
+    }
   }
 }
 
-// Slices longer than kSortCap (rare): one CTA per pixel runs the flip-bitonic network on
-// the slice itself in global memory (exact (t*, index) comparisons, all five fields
-// swapped); positions >= n act as +inf, so compare-exchanges touching them are no-ops.
-__device__ __forceinline__ void swap_entries(REntries& E, int64_t a, int64_t b) {
-  double t;
-  t = E.t[a], E.t[a] = E.t[b], E.t[b] = t;
-  t = E.alpha[a], E.alpha[a] = E.alpha[b], E.alpha[b] = t;
-  t = E.a[a], E.a[a] = E.a[b], E.a[b] = t;
-  t = E.b[a], E.b[a] = E.b[b], E.b[b] = t;
-  const int32_t i = E.idx[a];
-  E.idx[a] = E.idx[b];
-  E.idx[b] = i;
+constexpr int kWarpSortCap = 256;   // one warp: 8 keys per lane, 4 KB of shared memory
+constexpr int kCtaSortCap = 4096;   // one CTA of 256: 16 keys per thread, 64 KB
+
+// One warp per pixel (grid-stride over the band's pixels), 8 warps per CTA.
+__global__ void __launch_bounds__(kSortWarps * 32, 4) k_rsort(int64_t q0, int64_t nq, const int64_t* __restrict__ poff,
+                                                             int64_t base, const uint32_t* __restrict__ ncon, REnt* E,
+                                                             int32_t* big, int32_t* big_cnt) {
+  __shared__ __align__(16) REnt sbuf[kSortWarps][kWarpSortCap];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t step = int64_t(gridDim.x) * kSortWarps;
+  int64_t qq = int64_t(blockIdx.x) * kSortWarps + w;
+  int n = (qq < nq) ? int(ncon[q0 + qq]) : 0;
+  int64_t o = (qq < nq) ? poff[q0 + qq] : 0;
+  for (; qq < nq; qq += step) {
+    const int64_t q = q0 + qq;
+    const int cn = n;
+    REnt* S = E + (o - base);
+    if (qq + step < nq) {  // the next pixel's count and offset, in flight during this sort
+      n = int(ncon[q + step]);
+      o = poff[q + step];
+    }
+    if (cn <= 1) continue;
+    bool done = false;
+    if (cn <= 32) done = sort_slice_keys<32, 1>(S, cn, lane, w, sbuf[w], nullptr);
+    else if (cn <= 64) done = sort_slice_keys<32, 2>(S, cn, lane, w, sbuf[w], nullptr);
+    else if (cn <= 128) done = sort_slice_keys<32, 4>(S, cn, lane, w, sbuf[w], nullptr);
+    else if (cn <= 256) done = sort_slice_keys<32, 8>(S, cn, lane, w, sbuf[w], nullptr);
+    if (!done && lane == 0) {  // longer slices, or a t* span past the 55-bit key
+      big[atomicAdd(big_cnt, 1)] = int32_t(q);
+      atomicAdd(big_cnt + 1, 1);  // frame total (stats)
+    }
+  }
 }
 
-__global__ void __launch_bounds__(512) k_rsort_big(const int64_t* __restrict__ poff, int64_t base,
-                                                   const uint32_t* __restrict__ ncon, REntries E,
+// The queued slices up to 512 entries (or with a t* span past the warp sort's key): one
+// warp per pixel with 8 KB of shared memory; longer ones go to the CTA sort.
+__global__ void __launch_bounds__(kSortWarps * 32) k_rsort_mid(const int64_t* __restrict__ poff, int64_t base,
+                                                               const uint32_t* __restrict__ ncon, REnt* E,
+                                                               const int32_t* __restrict__ big,
+                                                               const int32_t* __restrict__ big_cnt, int32_t* huge,
+                                                               int32_t* huge_cnt) {
+  extern __shared__ __align__(16) unsigned char sdyn[];  // kSortWarps x 512 x 16 B
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = *big_cnt;
+  for (int bi = blockIdx.x * kSortWarps + w; bi < nb; bi += gridDim.x * kSortWarps) {
+    const int64_t q = big[bi];
+    const int n = int(ncon[q]);
+    REnt* S = E + (poff[q] - base);
+    const bool done = (n <= 512) && sort_slice_keys<32, 16>(S, n, lane, w, sdyn + w * 512 * 16, nullptr);
+    if (!done && lane == 0) huge[atomicAdd(huge_cnt, 1)] = int32_t(q);
+  }
+}
+
+// Slices past 512 entries (rare): one CTA of 256 per pixel.
+__global__ void __launch_bounds__(256) k_rsort_big(const int64_t* __restrict__ poff, int64_t base,
+                                                   const uint32_t* __restrict__ ncon, REnt* E,
                                                    const int32_t* __restrict__ big, const int32_t* __restrict__ big_cnt) {
+  extern __shared__ __align__(16) unsigned char sdyn[];  // kCtaSortCap x 16 B
+  __shared__ uint64_t red[16];
   const int nb = *big_cnt;
   for (int bi = blockIdx.x; bi < nb; bi += gridDim.x) {
     const int64_t q = big[bi];
     const int64_t n = ncon[q];
-    const int64_t o = poff[q] - base;
-    int64_t m = 1;
-    while (m < n) m <<= 1;
-    for (int64_t size = 2; size <= m; size <<= 1) {
-      const int64_t h = size >> 1;
-      for (int64_t i = threadIdx.x; i < (m >> 1); i += blockDim.x) {
-        const int64_t lo = (i / h) * size + (i % h), hi = (i / h) * size + size - 1 - (i % h);
-        if (hi < n && entry_less(E.t, E.idx, o + hi, o + lo)) swap_entries(E, o + lo, o + hi);
-      }
-      __syncthreads();
-      for (int64_t stride = size >> 2; stride > 0; stride >>= 1) {
-        for (int64_t i = threadIdx.x; i < (m >> 1); i += blockDim.x) {
-          const int64_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-          if (hi < n && entry_less(E.t, E.idx, o + hi, o + lo)) swap_entries(E, o + lo, o + hi);
-        }
-        __syncthreads();
-      }
-    }
+    REnt* S = E + (poff[q] - base);
+    bool done = false;
+    const int t = threadIdx.x;
+    if (n <= 1024) done = sort_slice_keys<256, 4>(S, int(n), t, 0, sdyn, red);
+    else if (n <= 4096) done = sort_slice_keys<256, 16>(S, int(n), t, 0, sdyn, red);
+    if (!done) sort_slice_global(S, n);
+    __syncthreads();
   }
 }
 
@@ -637,83 +796,207 @@ struct RenderOut {
   double* tfinal;
 };
 
-// One thread per pixel over its sorted slice (sequential reads).
-__global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile0, const int64_t* __restrict__ poff,
-                                                  int64_t base, const uint32_t* __restrict__ ncon, REntries E,
-                                                  const RRec* __restrict__ recs, const double* __restrict__ dc,
-                                                  int exact_depth, RenderOut out, unsigned long long* stats) {
+
+// The fields of one list record the blend reads (RRec's FP64 part + the DC colour),
+// staged per tile in shared memory as 7 double2 rows.
+struct BRec {
+  double ic[6], b[3], c, op, dc[3];
+  float thr;
+};
+constexpr int kBlendCap = 640;  // records staged per tile (74 KB); later list positions read global memory
+constexpr int kBlendSmem = kBlendCap * (7 * 16 + 4);
+
+__device__ __forceinline__ BRec brec_global(const RRec* __restrict__ recs, const double* __restrict__ dc, int g) {
+  const double2* r = reinterpret_cast<const double2*>(recs + g);
+  BRec o;
+  double2 v = __ldg(r + 0);
+  o.ic[0] = v.x, o.ic[1] = v.y;
+  v = __ldg(r + 1);
+  o.ic[2] = v.x, o.ic[3] = v.y;
+  v = __ldg(r + 2);
+  o.ic[4] = v.x, o.ic[5] = v.y;
+  v = __ldg(r + 3);
+  o.b[0] = v.x, o.b[1] = v.y;
+  v = __ldg(r + 4);
+  o.b[2] = v.x, o.c = v.y;
+  v = __ldg(r + 5);
+  o.op = v.x;
+  o.thr = __ldg(&recs[g].thr);
+  for (int k = 0; k < 3; ++k) o.dc[k] = __ldg(dc + 3 * g + k);
+  return o;
+}
+
+__device__ __forceinline__ BRec brec_smem(const double2* row, const float* thr, int pos) {
+  const double2* r = row + 7 * pos;
+  BRec o;
+  double2 v = r[0];
+  o.ic[0] = v.x, o.ic[1] = v.y;
+  v = r[1];
+  o.ic[2] = v.x, o.ic[3] = v.y;
+  v = r[2];
+  o.ic[4] = v.x, o.ic[5] = v.y;
+  v = r[3];
+  o.b[0] = v.x, o.b[1] = v.y;
+  v = r[4];
+  o.b[2] = v.x, o.c = v.y;
+  v = r[5];
+  o.op = v.x, o.dc[0] = v.y;
+  v = r[6];
+  o.dc[1] = v.x, o.dc[2] = v.y;
+  o.thr = thr[pos];
+  return o;
+}
+
+// A, B of abc_cached (precompute.hpp:39-45) for the record and the pixel ray
+__device__ __forceinline__ void rec_ab(const BRec& r, const double* d, double& a, double& b) {
+  const double x = d[0], y = d[1], z = d[2];
+  a = r.ic[0] * x * x + r.ic[3] * y * y + r.ic[5] * z * z + 2.0 * (r.ic[1] * x * y + r.ic[2] * x * z + r.ic[4] * y * z);
+  b = 2.0 * (x * r.b[0] + y * r.b[1] + z * r.b[2]);
+}
+
+// alpha_at(rc, depth) (opacity_field.hpp:95-101) for a contribution whose A, B are known
+template <typename Tab>
+__device__ __forceinline__ double alpha_at_depth(const BRec& r, double a, double b, double ts, double depth, Tab tab) {
+  const double te = (depth < ts) ? depth : ts;  // std::min(t*, t)
+  if (!(te > 0.0)) return 0.0;
+  const double arg = -0.5 * ((a * te + b) * te + r.c);  // eval_1d gaussian.hpp:47-49
+  if (arg < double(r.thr)) return 0.0;                   // alpha < 1/255 certain
+  const double al = r.op * exp_any(arg, tab);
+  if (al < kMinAlpha) return 0.0;
+  return (kMaxAlpha < al) ? kMaxAlpha : al;
+}
+
+// One thread per pixel over its sorted slice; the tile list's records (up to kBlendCap)
+// staged in shared memory and addressed by the entry's list position. The contribution's
+// A, B and alpha are recomputed with the exact expressions R2 used. Phase A blends
+// (render_pixel :204-210) up to the median (find_median :129-141); phase B fixes the
+// depth (exact_depth :157-166) and takes the opacity product of opacity_along_ray
+// (:104-108) over the prefix up to the median; phase C blends the rest and extends the
+// product in the same pass. Lanes leave phase A at different entries, but every phase is
+// one loop per lane, so the warp never serialises one lane's prefix after another's.
+__global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile0, const int64_t* __restrict__ toff,
+                                                  const int32_t* __restrict__ ent, const int64_t* __restrict__ poff,
+                                                  int64_t base, const uint32_t* __restrict__ ncon,
+                                                  const REnt* __restrict__ E, const RRec* __restrict__ recs,
+                                                  const double* __restrict__ dc, int exact_depth, RenderOut out,
+                                                  unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char sdyn[];
+  double2* srow = reinterpret_cast<double2*>(sdyn);                     // [kBlendCap][7]
+  float* sthr = reinterpret_cast<float*>(srow + 7 * kBlendCap);        // [kBlendCap]
   __shared__ __align__(16) double s_exp[128];
-  for (int k = threadIdx.x; k < 128; k += blockDim.x) s_exp[k] = kSofExpTabDev[k];
+  const int tile = tile0 + int(blockIdx.x), l = threadIdx.x;
+  for (int k = l; k < 128; k += blockDim.x) s_exp[k] = kSofExpTabDev[k];
+  const int64_t l0 = toff[tile];
+  const int len = int(min(int64_t(kBlendCap), toff[tile + 1] - l0));
+  for (int k = l; k < len * 7; k += kRPix) {
+    const int r = k / 7, qq = k % 7;
+    const int32_t g = ent[l0 + r];
+    double2 v;
+    if (qq < 5) {
+      v = __ldg(reinterpret_cast<const double2*>(recs + g) + qq);
+    } else if (qq == 5) {
+      v = make_double2(__ldg(&recs[g].op), __ldg(dc + 3 * g));
+      sthr[r] = __ldg(&recs[g].thr);
+    } else {
+      v = make_double2(__ldg(dc + 3 * g + 1), __ldg(dc + 3 * g + 2));
+    }
+    srow[k] = v;
+  }
   __syncthreads();
   const SofExpSmem tab{smem_u32(s_exp)};
-  const int tile = tile0 + int(blockIdx.x), l = threadIdx.x;
   int x, y;
   tile_pixel(tile, tiles_x, l, x, y);
   if (!(x < cam.w && y < cam.h)) return;
   const int64_t q = int64_t(tile) * kRPix + l;
   const int n = int(ncon[q]);
-  const int64_t o = poff[q] - base;
-  const double* __restrict__ Tt = E.t + o;
-  const double* __restrict__ Ta = E.alpha + o;
-  const double* __restrict__ TA = E.a + o;
-  const double* __restrict__ TB = E.b + o;
-  const int32_t* __restrict__ Ti = E.idx + o;
-  // render_pixel (opacity_field.hpp:201-210) + find_median (:129-141) in one pass
+  const REnt* __restrict__ S = E + (poff[q] - base);
+  double d[3];
+  pixel_ray(cam, x, y, d);
+  auto rec = [&](const REnt& e) { return (e.pos < kBlendCap) ? brec_smem(srow, sthr, e.pos) : brec_global(recs, dc, e.idx); };
   double T = 1.0, col[3] = {0.0, 0.0, 0.0};
-  int med = -1;
-  double med_T = 1.0;
-  for (int j = 0; j < n; ++j) {
-    const double alpha = Ta[j];
-    const int32_t g = Ti[j];
-    for (int k = 0; k < 3; ++k) col[k] = col[k] + __ldg(dc + 3 * g + k) * alpha * T;
-    const double next = T * (1.0 - alpha);
-    if (med < 0 && T > 0.5 && next < 0.5) {
-      med = j;
-      med_T = T;
+  auto blend = [&](const BRec& r, double& a, double& b) {
+    rec_ab(r, d, a, b);
+    const double arg = -0.5 * (r.c - b * b / (4.0 * a));  // peak_value gaussian.hpp:54-56
+    const double al = r.op * exp_any(arg, tab);
+    const double alpha = (kMaxAlpha < al) ? kMaxAlpha : al;
+    for (int k = 0; k < 3; ++k) col[k] = col[k] + r.dc[k] * alpha * T;
+    return alpha;
+  };
+  // phase A (entries fetched four at a time: one memory latency per group)
+  int j = 0, med = -1;
+  double med_T = 1.0, ma = 0.0, mb = 0.0, mc = 0.0, mop = 0.0;
+  while (j < n && med < 0) {
+    REnt g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) g[u] = (j + u < n) ? ld_rent(S + j + u) : rent_pad();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (med < 0 && j < n) {
+        const BRec r = rec(g[u]);
+        double a, b;
+        const double alpha = blend(r, a, b);
+        const double next = T * (1.0 - alpha);
+        if (T > 0.5 && next < 0.5) {
+          med = j;
+          med_T = T;
+          ma = a;
+          mb = b;
+          mc = r.c;
+          mop = r.op;
+        }
+        T = next;
+        ++j;
+      }
     }
-    T = next;
   }
-  double depth = NAN;
+  // phase B
+  double depth = NAN, T2 = 1.0;
   if (med >= 0) {
-    const double med_t = Tt[med];
-    depth = med_t;      // median_depth (:143-147)
+    const double mt = S[med].t;
+    depth = mt;         // median_depth (:143-147)
     if (exact_depth) {  // exact_depth (:157-166)
-      const RRec& r = recs[Ti[med]];
-      const double a = TA[med], b = TB[med];
-      const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * r.op));
-      const double disc = b * b - 4.0 * a * (r.c + lt);
+      const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * mop));
+      const double disc = mb * mb - 4.0 * ma * (mc + lt);
       if (disc < 0.0) {
         atomicAdd(stats + 3, 1ull);
       } else {
-        depth = med_t - sqrt(disc) / (2.0 * a);
+        depth = mt - sqrt(disc) / (2.0 * ma);
       }
+    }
+    for (int i = 0; i <= med; i += 4) {
+      REnt g[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) g[u] = (i + u <= med) ? ld_rent(S + i + u) : rent_pad();
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u <= med) {
+          const BRec r = rec(g[u]);
+          double a, b;
+          rec_ab(r, d, a, b);
+          T2 *= 1.0 - alpha_at_depth(r, a, b, g[u].t, depth, tab);
+        }
     }
   }
-  // accumulated opacity = opacity_along_ray(contribs, depth) (:104-108, 216-217)
-  double acc = 0.0;
-  if (!isnan(depth)) {
-    double T2 = 1.0;
-    for (int j = 0; j < n; ++j) {
-      const double ts = Tt[j];
-      const double te = (depth < ts) ? depth : ts;  // alpha_at :95-101, std::min(t*, t)
-      double al = 0.0;
-      if (te > 0.0) {
-        const RRec* r = recs + Ti[j];
-        const double a = TA[j], b = TB[j];
-        const double arg = -0.5 * ((a * te + b) * te + __ldg(&r->c));  // eval_1d gaussian.hpp:47-49
-        if (!(arg < double(__ldg(&r->thr)))) {                         // else alpha < 1/255 certain
-          al = __ldg(&r->op) * exp_any(arg, tab);
-          if (al < kMinAlpha) al = 0.0;
-          else if (kMaxAlpha < al) al = kMaxAlpha;
-        }
+  // phase C
+  while (j < n) {
+    REnt g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) g[u] = (j + u < n) ? ld_rent(S + j + u) : rent_pad();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j < n) {
+        const BRec r = rec(g[u]);
+        double a, b;
+        const double alpha = blend(r, a, b);
+        if (med >= 0) T2 *= 1.0 - alpha_at_depth(r, a, b, g[u].t, depth, tab);
+        T = T * (1.0 - alpha);
+        ++j;
       }
-      T2 *= 1.0 - al;
     }
-    acc = 1.0 - T2;
   }
   const int64_t p = int64_t(y) * cam.w + x;
   out.depth[p] = depth;
-  out.opacity[p] = acc;
+  out.opacity[p] = (med >= 0 && !isnan(depth)) ? 1.0 - T2 : 0.0;  // accumulated opacity (:216-217)
   for (int k = 0; k < 3; ++k) out.rgb[3 * p + k] = col[k];
   out.tfinal[p] = T;
 }
@@ -722,6 +1005,15 @@ __global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile
 __global__ void k_tile_slice_off(int64_t T, const int64_t* __restrict__ poff, int64_t* out) {
   const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (t <= T) out[t] = poff[t * kRPix];
+}
+
+// per-pixel contribution counts of the last render, image order (diagnostics / tests)
+__global__ void k_rcounts_image(Cam cam, int tiles_x, int64_t Q, const uint32_t* __restrict__ ncon, uint32_t* out) {
+  const int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (q >= Q) return;
+  int x, y;
+  tile_pixel(int(q / kRPix), tiles_x, int(q % kRPix), x, y);
+  if (x < cam.w && y < cam.h) out[int64_t(y) * cam.w + x] = ncon[q];
 }
 
 // ---- normals (render.hpp:58-107) ---------------------------------------------------------------
@@ -851,6 +1143,12 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     if (T > INT32_MAX / kRPix) throw InvalidArg("image too large");
     RenderScratch& rs = c->rs;
     cudaStream_t st = c->stream;
+    if (!rs.attr_set) {  // the sorts' 64 KB of dynamic shared memory (per device)
+      SOF_CUDA(cudaFuncSetAttribute(k_rsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSortCap * 16));
+      SOF_CUDA(cudaFuncSetAttribute(k_rsort_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortWarps * 512 * 16));
+      SOF_CUDA(cudaFuncSetAttribute(k_rblend, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlendSmem));
+      rs.attr_set = true;
+    }
     rs.big_cnt.ensure(4);  // [0] big Gaussians (binning), [1] big pixels (band), [2] big pixels (frame)
     SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p, 0, 4 * sizeof(int32_t), st));
     c->r_stats.ensure(4);
@@ -861,10 +1159,10 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     SOF_CUDA(cudaMemsetAsync(rs.tile_cnt.p, 0, sizeof(uint32_t) * T, st));
     rs.rrec.ensure(std::max<int64_t>(n, 1) * sizeof(RRec));
     RRec* rec = reinterpret_cast<RRec*>(rs.rrec.p);
+    rs.big.ensure(std::max<int64_t>(n, 2 * Q));
     if (n > 0) {
       rs.rect.ensure(n);
       rs.gcnt.ensure(n);
-      rs.big.ensure(std::max<int64_t>(n, Q));
       k_rrec<<<grid_for(n, 128), 128, 0, st>>>(n, c->gstat.p, cam, rec);
       k_rrect<<<grid_for(n, 128), 128, 0, st>>>(n, c->gstat.p, rec, cam, tiles_x, tiles_y, rs.rect.p, rs.gcnt.p);
       c->launches += 1;
@@ -918,24 +1216,27 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
         e1 = toff[t1];
       }
       const int64_t ne = std::max<int64_t>(e1 - e0, 1);
-      rs.et.ensure(ne);
-      rs.ea.ensure(ne);
-      rs.eA.ensure(ne);
-      rs.eB.ensure(ne);
-      rs.ei.ensure(ne);
-      REntries E{rs.et.p, rs.ea.p, rs.eA.p, rs.eB.p, rs.ei.p};
+      rs.ent16.ensure(ne * sizeof(REnt));
+      REnt* E = reinterpret_cast<REnt*>(rs.ent16.p);
       const unsigned nt = unsigned(t1 - t0);
       k_rtest<<<nt, kRPix, 0, st>>>(cam, tiles_x, int(t0), rs.tile_off.p, rs.ent.p, rec, rs.poff.p, e0, E,
                                     rs.ncon.p, c->r_stats.p);
       SOF_LAUNCHED(c);
       SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p + 1, 0, sizeof(int32_t), st));
+      SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p + 3, 0, sizeof(int32_t), st));
       const int64_t nq = int64_t(nt) * kRPix;
-      const unsigned sort_grid = unsigned(std::min<int64_t>((nq + kSortWarps - 1) / kSortWarps, 148 * 32));
-      k_rsort<<<sort_grid, kSortWarps * 32, 0, st>>>(t0 * kRPix, nq, rs.poff.p, e0, rs.ncon.p, E, rs.big.p,
+      const unsigned sort_grid = unsigned(std::min<int64_t>((nq + kSortWarps - 1) / kSortWarps, 148 * 8));
+      // big list: rs.big[0, n) for the binning, then reused for the sort queues
+      int32_t* qmid = rs.big.p;
+      int32_t* qhuge = rs.big.p + nq;
+      k_rsort<<<sort_grid, kSortWarps * 32, 0, st>>>(t0 * kRPix, nq, rs.poff.p, e0, rs.ncon.p, E, qmid,
                                                       rs.big_cnt.p + 1);
-      k_rsort_big<<<148, 512, 0, st>>>(rs.poff.p, e0, rs.ncon.p, E, rs.big.p, rs.big_cnt.p + 1);
-      k_rblend<<<nt, kRPix, 0, st>>>(cam, tiles_x, int(t0), rs.poff.p, e0, rs.ncon.p, E, rec, c->dc.p,
-                                     depth_mode == SOF_DEPTH_EXACT, out, c->r_stats.p);
+      k_rsort_mid<<<148 * 2, kSortWarps * 32, kSortWarps * 512 * 16, st>>>(rs.poff.p, e0, rs.ncon.p, E, qmid,
+                                                                          rs.big_cnt.p + 1, qhuge, rs.big_cnt.p + 3);
+      k_rsort_big<<<148, 256, kCtaSortCap * 16, st>>>(rs.poff.p, e0, rs.ncon.p, E, qhuge, rs.big_cnt.p + 3);
+      k_rblend<<<nt, kRPix, kBlendSmem, st>>>(cam, tiles_x, int(t0), rs.tile_off.p, rs.ent.p, rs.poff.p, e0,
+                                               rs.ncon.p, E, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT, out,
+                                               c->r_stats.p);
       c->launches += 3;
       SOF_CUDA(cudaGetLastError());
       ++nbands;
@@ -943,6 +1244,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     }
     c->r_view = view;
     c->r_bands = nbands;
+    c->r_Q = Q;
     if (depth) SOF_CUDA(cudaMemcpyAsync(depth, out.depth, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
     if (opacity) SOF_CUDA(cudaMemcpyAsync(opacity, out.opacity, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
     if (rgb) SOF_CUDA(cudaMemcpyAsync(rgb, out.rgb, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, st));
@@ -955,10 +1257,27 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       SOF_CUDA(cudaStreamSynchronize(st));
       stats[0] = h[0];  // tested (pixel, list entry) pairs
       stats[1] = h[1];  // contributions
-      stats[2] = uint64_t(nbig);  // pixels whose slice took the CTA-wide sort (> 1024 contributions)
+      stats[2] = uint64_t(nbig);  // pixels whose slice took the CTA-wide sort (> kWarpSortCap contributions)
       stats[3] = h[3];  // exact-depth fallbacks (negative discriminant)
     }
     SOF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+extern "C" int sof_render_counts(sof_ctx* c, int view, uint32_t* counts) {
+  if (!c || !counts) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+    if (c->r_view != view) throw StateError("no render of this view on the device: call sof_render_view first");
+    const Cam& cam = c->cams[view];
+    const int tiles_x = (cam.w + kRTile - 1) / kRTile;
+    const int64_t P = int64_t(cam.w) * cam.h;
+    DBuf<uint32_t>& o = c->rs.pcnt;  // the bounds are no longer needed after the render
+    o.ensure(std::max<int64_t>(P, 1));
+    k_rcounts_image<<<grid_for(c->r_Q, 256), 256, 0, c->stream>>>(cam, tiles_x, c->r_Q, c->rs.ncon.p, o.p);
+    SOF_LAUNCHED(c);
+    SOF_CUDA(cudaMemcpyAsync(counts, o.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, c->stream));
+    SOF_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -174,8 +174,8 @@ struct RenderScratch {
   DBuf<uint32_t> ncon;            // [T * 256] per-pixel contributions
   DBuf<int64_t> poff;             // [T * 256 + 1] slice offsets (tile-major pixel order)
   DBuf<int64_t> band_off;         // [T + 1] slice offset of each tile's first pixel
-  DBuf<double> et, ea, eA, eB;    // per contribution: t*, alpha, a, b (opacity_field.hpp:13-19)
-  DBuf<int32_t> ei;               // Gaussian index
+  DBuf<char> ent16;               // per contribution: REnt {t*, list position, Gaussian index}
+  bool attr_set = false;          // k_rsort_big's dynamic shared-memory limit set
   DBuf<char> rrec;                // [n] per-view render records (k_render.cu RRec, 128 B)
 };
 
@@ -270,6 +270,7 @@ struct sof_ctx {
   sofk::DBuf<unsigned char> io_bytes;       // scene PLY payload / encoded records
   int r_view = -1;                          // view whose render is in r_out
   int64_t r_bands = 0;                      // tile bands of the last render
+  int64_t r_Q = 0;                          // tile-major pixel slots of the last render
   int64_t render_pool = int64_t(24) << 30;  // scratch budget of one render band (bytes)
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<char> scan_tmp;                 // block totals of the hand-written scans (k_scan.cu)

@@ -98,8 +98,9 @@ def test_c1_render_all_views(c1):
     yy, xx = np.mgrid[0:h, 0:w]
     pix = np.stack([xx.ravel(), yy.ravel()], 1).astype(np.int32)
     for v in range(cams.v):
-        r = sof.render_view(views, v, sof.DEPTH_EXACT)
+        r = sof.render_view(views, v, sof.DEPTH_EXACT, counts=True)
         ref_px = rc.render_pixels(v, pix, True, threads=THREADS)
+        np.testing.assert_array_equal(r["counts"].ravel(), ref_px["ncontrib"])
         assert_bits(r["rgb"].reshape(-1, 3), ref_px["color"], f"view {v} colour")
         assert_bits(r["t_final"].ravel(), ref_px["tfinal"], f"view {v} T")
         assert_bits(r["depth"].ravel(), ref_px["depth"], f"view {v} depth")
@@ -124,13 +125,14 @@ def test_c2_render_rows(c2, view):
     scene, cams, rc = c2
     ctx = sof.Context(0)
     views = sof.ViewSet.build(scene, cams, ctx=ctx)
-    r = sof.render_view(views, view, sof.DEPTH_EXACT)
+    r = sof.render_view(views, view, sof.DEPTH_EXACT, counts=True)
     w = int(cams.wh[view, 0])
     rows = C2_ROWS if view == 0 else C2_ROWS[1::3]
     pix = np.array([(x, y) for y in rows for x in range(w)], np.int32)
     want = rc.render_pixels(view, pix, True, threads=THREADS)
     ys, xs = pix[:, 1], pix[:, 0]
-    assert want["ncontrib"].max() > 100  # deep pixels (the k-buffer / sort path)
+    assert want["ncontrib"].max() > 100  # deep pixels
+    np.testing.assert_array_equal(r["counts"][ys, xs], want["ncontrib"])
     assert_bits(r["rgb"][ys, xs], want["color"], "colour")
     assert_bits(r["t_final"][ys, xs], want["tfinal"], "T")
     assert_bits(r["depth"][ys, xs], want["depth"], "depth")
