@@ -95,6 +95,12 @@ struct __align__(16) RRec {
 static_assert(sizeof(RRec) == 128, "render record layout");
 constexpr int kRRecV2 = int(sizeof(RRec) / 16);
 
+// The fields of one list record the blend reads (RRec's FP64 part + the DC colour),
+// staged per tile in shared memory as 7 double2 rows.
+struct BRec {
+  double ic[6], b[3], c, op, dc[3];
+  float thr;
+};
 __device__ __forceinline__ float float_up(double x) { return __double2float_ru(x); }
 
 __device__ void render_conic(const Rec& r, const Cam& cam, RRec& q) {
@@ -191,8 +197,8 @@ __device__ __forceinline__ double exp_any(double x, Tab tab) {
 
 // collect_contributions' per-Gaussian test (opacity_field.hpp:43-53) with the
 // RayContribution fields it keeps: t*, the clamped peak alpha, and A, B of abc_cached.
-template <typename Tab>
-__device__ __forceinline__ bool contribution(const RRec& r, const double* d, Tab tab, double& t_star,
+template <typename Tab, typename R>
+__device__ __forceinline__ bool contribution(const R& r, const double* d, Tab tab, double& t_star,
                                              double& alpha, double& a, double& b) {
   if (r.op < kMinAlpha) return false;  // :44
   const double x = d[0], y = d[1], z = d[2];
@@ -396,7 +402,12 @@ __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0
                                                  const int32_t* __restrict__ ent, const RRec* __restrict__ recs,
                                                  const int64_t* __restrict__ poff, int64_t base, REnt* E,
                                                  uint32_t* ncon, unsigned long long* stats) {
-  __shared__ __align__(16) RRec srec[kRChunk];
+  // the chunk's records: conic floats as rows (every lane reads the same record: a
+  // broadcast), FP64 fields as columns (lanes of the FP64 phase read different records:
+  // consecutive words, no bank conflicts; 128-byte rows would put every record's field in
+  // the same bank)
+  __shared__ __align__(16) float4 sc[kRChunk][2];
+  __shared__ double sd[11][kRChunk];
   __shared__ int32_t sidx[kRChunk];
   __shared__ double sray[3][kRPix];
   __shared__ int64_t sbase[kRPix];
@@ -425,17 +436,23 @@ __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0
     for (int k = l; k < cnt * kRRecV2; k += kRPix) {
       const int r = k / kRRecV2, qq = k % kRRecV2;
       const int32_t g = ent[b0 + r];
-      reinterpret_cast<double2*>(&srec[r])[qq] = __ldg(reinterpret_cast<const double2*>(recs + g) + qq);
-      if (qq == 0) sidx[r] = g;
+      const double2 v = __ldg(reinterpret_cast<const double2*>(recs + g) + qq);
+      if (qq < 5) {
+        sd[2 * qq][r] = v.x;
+        sd[2 * qq + 1][r] = v.y;
+      } else if (qq == 5) {
+        sd[10][r] = v.x;  // op
+        sidx[r] = g;
+      } else {
+        sc[r][qq - 6] = *reinterpret_cast<const float4*>(&v);
+      }
     }
     __syncthreads();
     // this lane's pixel: which of the chunk's records survive the cull
     uint32_t mask = 0;
     if (valid)
-      for (int k = 0; k < cnt; ++k) {
-        const float4* f = reinterpret_cast<const float4*>(&srec[k]) + 6;
-        if (!rcull(f[0], f[1], cu, cv)) mask |= 1u << k;
-      }
+      for (int k = 0; k < cnt; ++k)
+        if (!rcull(sc[k][0], sc[k][1], cu, cv)) mask |= 1u << k;
     // compact the CTA's surviving (pixel, record) pairs into one queue: warp prefix sums,
     // then the warps' offsets, so the FP64 work is spread over all 256 threads
     const int np = __popc(mask);
@@ -466,8 +483,14 @@ __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0
       const int v = queue[qi];
       const int pl = v >> 5, k = v & 31;
       const double d[3] = {sray[0][pl], sray[1][pl], sray[2][pl]};
+      BRec r;
+      for (int f = 0; f < 6; ++f) r.ic[f] = sd[f][k];
+      for (int f = 0; f < 3; ++f) r.b[f] = sd[6 + f][k];
+      r.c = sd[9][k];
+      r.op = sd[10][k];
+      r.thr = sc[k][0].x;
       double t_star, alpha, a, b;
-      if (contribution(srec[k], d, tab, t_star, alpha, a, b)) {
+      if (contribution(r, d, tab, t_star, alpha, a, b)) {
         const int64_t o = sbase[pl] + atomicAdd(&scur[pl], 1);
         REnt e;
         e.t = t_star;
@@ -537,23 +560,27 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   return (uint64_t(hi) << 32) | lo;
 }
 
-// in-thread stage: elements e and e + ES (ES < E, compile time)
-template <int NT, int E, int ES>
+// in-thread stage: elements e and e + ES (ES < E, compile time), position i = E tid + e
+template <int E, int ES>
 __device__ __forceinline__ void keys_inthread(uint64_t (&k)[E], int size, int tid) {
   if constexpr (ES < E) {
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if ((e & ES) == 0) {
-        const bool asc = ((NT * e + tid) & size) == 0;
+        const bool asc = ((E * tid + e) & size) == 0;
         const uint64_t a = k[e], b = k[e + ES];
-        const bool sw = asc ? (b < a) : (a < b);
+        const bool sw = (b < a) == asc;  // keys are distinct (equal only as padding)
         k[e] = sw ? b : a;
         k[e + ES] = sw ? a : b;
       }
   }
 }
 
-// ascending bitonic sort of NT x E keys (position i = NT e + tid); xb: NT x E u64 scratch
+// Ascending bitonic sort of NT x E keys in the blocked layout (position i = E tid + e):
+// strides below E are compare-exchanges inside a thread, larger ones pair element e of
+// threads tid and tid ^ (stride / E) — through shuffles inside a warp, through shared
+// memory (xb: NT x E u64) across warps. Small strides, the most frequent in the network,
+// thus cost no data movement.
 template <int NT, int E>
 __device__ __forceinline__ void sort_keys(uint64_t (&k)[E], int tid, int w, uint64_t* xb) {
   constexpr int M = NT * E;
@@ -563,53 +590,53 @@ __device__ __forceinline__ void sort_keys(uint64_t (&k)[E], int tid, int w, uint
     const int size = 1 << lg;
 #pragma unroll 1
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride >= NT) {
-        const int es = stride / NT;
-        if (es == 1) keys_inthread<NT, E, 1>(k, size, tid);
-        else if (es == 2) keys_inthread<NT, E, 2>(k, size, tid);
-        else if (es == 4) keys_inthread<NT, E, 4>(k, size, tid);
-        else if (es == 8) keys_inthread<NT, E, 8>(k, size, tid);
-      } else if (stride < 32) {
-        const bool lower = (lane & stride) == 0;
+      if (stride < E) {
+        if (stride == 1) keys_inthread<E, 1>(k, size, tid);
+        else if (stride == 2) keys_inthread<E, 2>(k, size, tid);
+        else if (stride == 4) keys_inthread<E, 4>(k, size, tid);
+        else if (stride == 8) keys_inthread<E, 8>(k, size, tid);
+      } else {
+        const int ts = stride / E;  // partner thread distance
+        const bool lower = (tid & ts) == 0;
+        if (ts < 32) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint64_t p = shfl_xor_u64(k[e], stride);
-          const bool take_min = lower == (((NT * e + tid) & size) == 0);
-          k[e] = take_min ? (p < k[e] ? p : k[e]) : (k[e] < p ? p : k[e]);
+          for (int e = 0; e < E; ++e) {
+            const uint64_t p = shfl_xor_u64(k[e], ts);
+            const bool take_min = lower == (((E * tid + e) & size) == 0);
+            k[e] = ((p < k[e]) == take_min) ? p : k[e];  // distinct keys (equal only as padding)
+          }
+        } else {  // partner thread in another warp: exchange through shared memory
+#pragma unroll
+          for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
+          sorter_sync<NT>(w);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const uint64_t p = xb[E * (tid ^ ts) + e];
+            const bool take_min = lower == (((E * tid + e) & size) == 0);
+            k[e] = ((p < k[e]) == take_min) ? p : k[e];
+          }
+          sorter_sync<NT>(w);
         }
-      } else {  // partner thread in another warp: exchange through shared memory
-#pragma unroll
-        for (int e = 0; e < E; ++e) xb[NT * e + tid] = k[e];
-        sorter_sync<NT>(w);
-        const bool lower = (tid & stride) == 0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint64_t p = xb[(NT * e + tid) ^ stride];
-          const bool take_min = lower == (((NT * e + tid) & size) == 0);
-          k[e] = take_min ? (p < k[e] ? p : k[e]) : (k[e] < p ? p : k[e]);
-        }
-        sorter_sync<NT>(w);
       }
     }
   }
+  (void)lane;
 }
 
 // Sorts S[0, n) (n <= NT E) in place. buf: NT E x 16 B of shared memory. Returns false
-// (nothing changed) when the t* span does not fit the 55-bit key.
+// (nothing changed) when the t* span does not fit the key.
 template <int NT, int E>
 __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int tid, int w, void* buf,
                                                 uint64_t* red) {
   constexpr int M = NT * E;
-  constexpr uint64_t kSlot = 511u;
   static_assert(M <= 4096, "slot bits");
   constexpr int SB = (M <= 512) ? 9 : 12;  // slot bits
   constexpr uint64_t kLow = (uint64_t(1) << SB) - 1;
-  (void)kSlot;
   uint64_t tb[E];
   uint64_t lo = ~uint64_t(0), hi = 0;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = NT * e + tid;
+    const int i = E * tid + e;
     tb[e] = (i < n) ? uint64_t(__double_as_longlong(S[i].t)) : 0;
     if (i < n) {
       lo = min(lo, tb[e]);
@@ -637,19 +664,19 @@ __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int
   uint64_t k[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = NT * e + tid;
+    const int i = E * tid + e;
     k[e] = (i < n) ? (((tb[e] - lo) << SB) | uint64_t(i)) : ~uint64_t(0);
   }
   uint64_t* xb = static_cast<uint64_t*>(buf);
   sort_keys<NT, E>(k, tid, w, xb);
   // equal t* at neighbouring positions: order by Gaussian index (rare)
 #pragma unroll
-  for (int e = 0; e < E; ++e) xb[NT * e + tid] = k[e];
+  for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
   sorter_sync<NT>(w);
   bool tie = false;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = NT * e + tid;
+    const int i = E * tid + e;
     if (i + 1 < n && (xb[i] >> SB) == (xb[i + 1] >> SB)) tie = true;
   }
   const bool any_tie = (NT == 32) ? __any_sync(0xffffffffu, tie) : __syncthreads_or(tie);
@@ -666,22 +693,18 @@ __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int
       }
     sorter_sync<NT>(w);
 #pragma unroll
-    for (int e = 0; e < E; ++e) k[e] = xb[NT * e + tid];
+    for (int e = 0; e < E; ++e) k[e] = xb[E * tid + e];
   }
   sorter_sync<NT>(w);
   // permute the entries through shared memory
   REnt* stage = static_cast<REnt*>(buf);
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = NT * e + tid;
+    const int i = E * tid + e;
     if (i < n) st_rent(stage + i, ld_rent(S + (k[e] & kLow)));
   }
   sorter_sync<NT>(w);
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = NT * e + tid;
-    if (i < n) st_rent(S + i, ld_rent(stage + i));
-  }
+  for (int i = tid; i < n; i += NT) st_rent(S + i, ld_rent(stage + i));  // coalesced
   sorter_sync<NT>(w);
   return true;
 }
@@ -797,14 +820,8 @@ struct RenderOut {
 };
 
 
-// The fields of one list record the blend reads (RRec's FP64 part + the DC colour),
-// staged per tile in shared memory as 7 double2 rows.
-struct BRec {
-  double ic[6], b[3], c, op, dc[3];
-  float thr;
-};
 constexpr int kBlendCap = 640;  // records staged per tile (74 KB); later list positions read global memory
-constexpr int kBlendSmem = kBlendCap * (7 * 16 + 4);
+constexpr int kBlendSmem = kBlendCap * (14 * 8 + 4);
 
 __device__ __forceinline__ BRec brec_global(const RRec* __restrict__ recs, const double* __restrict__ dc, int g) {
   const double2* r = reinterpret_cast<const double2*>(recs + g);
@@ -826,23 +843,16 @@ __device__ __forceinline__ BRec brec_global(const RRec* __restrict__ recs, const
   return o;
 }
 
-__device__ __forceinline__ BRec brec_smem(const double2* row, const float* thr, int pos) {
-  const double2* r = row + 7 * pos;
+// staged columns: sd[f * kBlendCap + pos], f = ic0..5, b0..2, c, op, dc0..2 (lanes read
+// different records: consecutive words, no bank conflicts)
+constexpr int kBlendF = 14;
+__device__ __forceinline__ BRec brec_smem(const double* sd, const float* thr, int pos) {
   BRec o;
-  double2 v = r[0];
-  o.ic[0] = v.x, o.ic[1] = v.y;
-  v = r[1];
-  o.ic[2] = v.x, o.ic[3] = v.y;
-  v = r[2];
-  o.ic[4] = v.x, o.ic[5] = v.y;
-  v = r[3];
-  o.b[0] = v.x, o.b[1] = v.y;
-  v = r[4];
-  o.b[2] = v.x, o.c = v.y;
-  v = r[5];
-  o.op = v.x, o.dc[0] = v.y;
-  v = r[6];
-  o.dc[1] = v.x, o.dc[2] = v.y;
+  for (int f = 0; f < 6; ++f) o.ic[f] = sd[f * kBlendCap + pos];
+  for (int f = 0; f < 3; ++f) o.b[f] = sd[(6 + f) * kBlendCap + pos];
+  o.c = sd[9 * kBlendCap + pos];
+  o.op = sd[10 * kBlendCap + pos];
+  for (int f = 0; f < 3; ++f) o.dc[f] = sd[(11 + f) * kBlendCap + pos];
   o.thr = thr[pos];
   return o;
 }
@@ -881,26 +891,29 @@ __global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile
                                                   const double* __restrict__ dc, int exact_depth, RenderOut out,
                                                   unsigned long long* stats) {
   extern __shared__ __align__(16) unsigned char sdyn[];
-  double2* srow = reinterpret_cast<double2*>(sdyn);                     // [kBlendCap][7]
-  float* sthr = reinterpret_cast<float*>(srow + 7 * kBlendCap);        // [kBlendCap]
+  double* scol = reinterpret_cast<double*>(sdyn);                      // [kBlendF][kBlendCap]
+  float* sthr = reinterpret_cast<float*>(scol + kBlendF * kBlendCap);  // [kBlendCap]
   __shared__ __align__(16) double s_exp[128];
   const int tile = tile0 + int(blockIdx.x), l = threadIdx.x;
   for (int k = l; k < 128; k += blockDim.x) s_exp[k] = kSofExpTabDev[k];
   const int64_t l0 = toff[tile];
   const int len = int(min(int64_t(kBlendCap), toff[tile + 1] - l0));
-  for (int k = l; k < len * 7; k += kRPix) {
-    const int r = k / 7, qq = k % 7;
+  for (int k = l; k < len * 8; k += kRPix) {
+    const int r = k >> 3, qq = k & 7;
     const int32_t g = ent[l0 + r];
-    double2 v;
     if (qq < 5) {
-      v = __ldg(reinterpret_cast<const double2*>(recs + g) + qq);
+      const double2 v = __ldg(reinterpret_cast<const double2*>(recs + g) + qq);
+      scol[(2 * qq) * kBlendCap + r] = v.x;
+      scol[(2 * qq + 1) * kBlendCap + r] = v.y;
     } else if (qq == 5) {
-      v = make_double2(__ldg(&recs[g].op), __ldg(dc + 3 * g));
+      scol[10 * kBlendCap + r] = __ldg(&recs[g].op);
       sthr[r] = __ldg(&recs[g].thr);
+    } else if (qq == 6) {
+      scol[11 * kBlendCap + r] = __ldg(dc + 3 * g);
+      scol[12 * kBlendCap + r] = __ldg(dc + 3 * g + 1);
     } else {
-      v = make_double2(__ldg(dc + 3 * g + 1), __ldg(dc + 3 * g + 2));
+      scol[13 * kBlendCap + r] = __ldg(dc + 3 * g + 2);
     }
-    srow[k] = v;
   }
   __syncthreads();
   const SofExpSmem tab{smem_u32(s_exp)};
@@ -912,7 +925,7 @@ __global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile
   const REnt* __restrict__ S = E + (poff[q] - base);
   double d[3];
   pixel_ray(cam, x, y, d);
-  auto rec = [&](const REnt& e) { return (e.pos < kBlendCap) ? brec_smem(srow, sthr, e.pos) : brec_global(recs, dc, e.idx); };
+  auto rec = [&](const REnt& e) { return (e.pos < kBlendCap) ? brec_smem(scol, sthr, e.pos) : brec_global(recs, dc, e.idx); };
   double T = 1.0, col[3] = {0.0, 0.0, 0.0};
   auto blend = [&](const BRec& r, double& a, double& b) {
     rec_ab(r, d, a, b);
