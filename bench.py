@@ -32,14 +32,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ITER = 8  # refine_iterations (extract.hpp:16)
-# algorithmic FP64 FLOPs of one evaluated (point, Gaussian) pair of view_opacity
-# (field_eval.hpp:95-103) as the bit-exact reference arithmetic performs it:
-# abc_cached 24 (A: 13 mul + 5 add, B: 4 mul + 2 add), peak_t 2 + IEEE division ~8,
-# eval_1d argument 5, exp (sof_exp: rint-scaled reduction 6, 13-term Horner 24,
-# reconstruction 2) 32, alpha / clamp / survive 5 -> 76. The kernel
-# skips the division and the exp where it can prove them irrelevant, so this is the
-# algorithmic (reference) work, not the executed instruction count.
-FLOP_PER_PAIR = 76.0
+# Algorithmic FP64 FLOPs of one evaluated (point, Gaussian) pair of view_opacity
+# (field_eval.hpp:95-103) as the reference arithmetic performs it (no contraction):
+# abc_cached A 18 (13 mul + 5 add), B 6, 2a 1, the division t* = -b / 2a ~8 (Newton
+# sequence), eval_1d's exponent 5, exp 18 (sof_exp: rint-scaled reduction 1 mul + 2 fma,
+# degree-6 polynomial 4 fma + 1 mul + 1 fma, table reconstruction 1 fma + 1 add, scaling
+# 1 mul; fma = 2 FLOP), alpha 1, survive 2 -> 59. The kernel skips the
+# division and the exp where it can prove them irrelevant, so this is the reference's work,
+# not the executed instruction count.
+FLOP_PER_PAIR = 59.0
+# SURVEY.md §8(d) issue roofline of an FP32 fast path: 148 SM x 4 warp-instr/clk x 32 x
+# 1.965 GHz / 21 issue slots per pair (reported beside the FP64-pipe fraction)
+ISSUE_PAIRS_PER_S = 148 * 4 * 32 * 1.965e9 / 21
+# render (K5) issue roofline, §8(d): 17 issue slots per tested (pixel, Gaussian) pair
+RENDER_TESTED_PAIRS_PER_S = 148 * 4 * 32 * 1.965e9 / 17
 
 
 def env_int(k, d):
@@ -104,20 +110,24 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "fallback": True}
 
 
-def ncu_traffic() -> float | None:
-    """dram bytes per launch of the opacity-eval kernel from the committed ncu capture."""
+def ncu_k_eval() -> dict:
+    """dram bytes per launch and pipe utilisation of the opacity-eval kernel from the
+    committed ncu capture (profiles/k_eval_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "k_eval_traffic.json")
     try:
-        return float(json.load(open(p))["dram_bytes_per_launch"])
+        return json.load(open(p))
     except Exception:
-        return None
+        return {}
 
 
 # ---- sorted rasterizer sample (secondary: not the headline metric) -------------------------
 
-def render_sample(device: int, views=(0, 1, 2)):
+def render_sample(device: int, views=(0, 1, 2), rows=(135, 540, 945), threads=None):
     """C2 (1M Gaussians, 1920x1080) exact-depth render of a few views through
-    sof_render_view, device-timed with events; outputs stay on the device."""
+    sof_render_view, device-timed with events (outputs stay on the device), then a CPU
+    baseline and a parity check on the same rows: the reference's collect_contributions +
+    render_pixel (oracle/_ref, ThreadPool-like host threads) for every pixel of `rows` of
+    view 0, compared bit for bit (colour, T, depth, opacity, contribution counts)."""
     import paper_2506_19139_b200 as sof
     from paper_2506_19139_b200.workloads import CONFIGS, orbit_cameras, synthetic_scene
     cfg = CONFIGS["C2"]
@@ -128,7 +138,7 @@ def render_sample(device: int, views=(0, 1, 2)):
     ctx.set_views(cams)
     stats = np.zeros(4, np.uint64)
     ms, res = ctypes.c_float(), []
-    for rep in range(2):  # pass 0 warms up (spill-pool and binning allocations), pass 1 is timed
+    for rep in range(2):  # pass 0 warms up (scratch allocations), pass 1 is timed
         for v in range(len(views)):
             ctx.check(ctx.lib.sof_event_record(ctx.h, 0))
             ctx.check(ctx.lib.sof_render_view(ctx.h, v, sof.DEPTH_EXACT, 16, None, None, None, None,
@@ -137,26 +147,79 @@ def render_sample(device: int, views=(0, 1, 2)):
             ctx.check(ctx.lib.sof_event_elapsed(ctx.h, 0, 1, ctypes.byref(ms)))
             if rep == 1:
                 res.append((ms.value, stats.copy()))
-    timed = res
-    t = float(np.mean([r[0] for r in timed]))
-    tested = float(np.mean([float(r[1][0]) for r in timed]))
-    contrib = float(np.mean([float(r[1][1]) for r in timed]))
+    t = float(np.mean([r[0] for r in res]))
+    tested = float(np.mean([float(r[1][0]) for r in res]))
+    contrib = float(np.mean([float(r[1][1]) for r in res]))
     px = cfg["width"] * cfg["height"]
+    out = {"config": "C2: 1M Gaussians, 1920x1080, exact depth + colour + T + opacity at depth",
+           "views_timed": len(res), "ms_per_view": t, "mpix_per_s": px / (t * 1e-3) / 1e6,
+           "tested_pairs_per_s": tested / (t * 1e-3), "contributing_pairs_per_s": contrib / (t * 1e-3),
+           "contributions_per_pixel": contrib / px,
+           "roofline": {"bound": "issue", "kernel": "K5 (R1-R4, whole render)", "achieved": tested / (t * 1e-3),
+                        "peak": RENDER_TESTED_PAIRS_PER_S, "unit": "tested pairs/s",
+                        "frac": tested / (t * 1e-3) / RENDER_TESTED_PAIRS_PER_S,
+                        "note": "SURVEY.md 8(d): 17 issue slots per tested (pixel, Gaussian) pair"}}
+    # the rows of view 0 on the device, then on the CPU reference
+    full = sof.render_view(sof.ViewSet(ctx, ctx.scene, ctx.cams, 0.0), 0, sof.DEPTH_EXACT, counts=True)
     ctx.close()
-    return {"config": "C2: 1M Gaussians, 1920x1080, exact depth + colour + T + opacity at depth, bit-exact",
-            "views_timed": len(timed), "ms_per_view": t, "mpix_per_s": px / (t * 1e-3) / 1e6,
-            "tested_pairs_per_s": tested / (t * 1e-3), "contributing_pairs_per_s": contrib / (t * 1e-3),
-            "sorted_path_pixels": int(np.mean([float(r[1][2]) for r in timed]))}
+    try:
+        from oracle import refpy
+        ref = refpy.RefLib()
+        threads = threads or len(os.sched_getaffinity(0))
+        rc = ref.context(scene, cams.subset(np.array([0])))
+        w = cfg["width"]
+        pix = np.array([(x, y) for y in rows for x in range(w)], np.int32)
+        t0 = time.perf_counter()
+        want = rc.render_pixels(0, pix, True, threads=threads)
+        dt = time.perf_counter() - t0
+        ys, xs = pix[:, 1], pix[:, 0]
+        bad = {k: int((full[kk][ys, xs].reshape(len(pix), -1).view(np.uint64) !=
+                       want[k].reshape(len(pix), -1).view(np.uint64)).any(axis=1).sum())
+               for k, kk in (("color", "rgb"), ("tfinal", "t_final"), ("depth", "depth"), ("acc", "opacity"))}
+        bad["counts"] = int((full["counts"][ys, xs] != want["ncontrib"]).sum())
+        out["parity"] = {"pixels": len(pix), "rows": list(rows), "mismatched_pixels": bad,
+                         "bit_identical": all(v == 0 for v in bad.values())}
+        cpu_mpix = len(pix) / dt / 1e6
+        out["cpu_baseline"] = {"value": cpu_mpix, "unit": "Mpix/s", "cores": threads, "kind": "reference",
+                               "sample": f"reference collect_contributions + render_pixel over {len(pix)} pixels "
+                                         f"(rows {list(rows)} of view 0), {dt:.1f} s"}
+    except Exception as e:  # the reference build is absent
+        out["parity"] = {"unavailable": str(e)[:200]}
+        out["cpu_baseline"] = {"value": None, "unit": "Mpix/s", "cores": 0, "kind": "reference",
+                               "sample": f"unavailable: {e}"[:200]}
+    return out
 
 
 # ---- CPU reference (oracle/_ref): bounded sample -----------------------------------------------
 
-def cpu_reference_sample(scene, cams, verts, sample_views=(0, 1), threads=None, vertex_stride=1):
-    """The reference's own FieldEvaluator (all strategies) on a 2-view ViewSet:
-    ViewSet::build + FieldEvaluator ctor (tile bindings) + label_grid over the
-    vertices with ThreadPool(threads). Returns seconds and the per-view-query rate
-    extrapolated linearly to all V views (pruning makes later views cheaper, so
-    this is an upper bound on CPU time)."""
+def crossing_edge_sample(verts, labels, n_lattice, count, seed=0):
+    """Up to `count` lattice edges (x, y and z neighbours) whose endpoints are on
+    opposite sides of the level set of `labels`, oriented (inside, outside)."""
+    inside = labels >= 0.5
+    rng = np.random.default_rng(seed)
+    out = []
+    for step in (1, n_lattice, n_lattice * n_lattice):
+        i = np.arange(len(verts) - step)
+        i = i[inside[i] != inside[i + step]]
+        if step == 1:
+            i = i[(i % n_lattice) != n_lattice - 1]
+        elif step == n_lattice:
+            i = i[(i // n_lattice) % n_lattice != n_lattice - 1]
+        a, b = i, i + step
+        e = np.where(inside[a][:, None], np.stack([a, b], 1), np.stack([b, a], 1))
+        out.append(e)
+    e = np.concatenate(out)
+    return e[rng.permutation(len(e))[:count]].astype(np.int64)
+
+
+def cpu_reference_sample(scene, cams, verts, n_lattice, edges_total, sample_views=(0, 1), threads=None,
+                         vertex_stride=1, refine_edges=10_000):
+    """The reference's own code (oracle/_ref, all strategies) on a ViewSet of
+    `sample_views`: ViewSet::build + FieldEvaluator ctor (tile bindings) + label_grid over
+    the vertices with ThreadPool(threads), then binary_search_refine (8 iterations, the
+    serial classify_point callback as in extract_mesh) over `refine_edges` crossing
+    lattice edges of that label. Per-query times are scaled by V / k views, and the
+    label and bisection queries are combined in the step's own mix (N_v + 8 E)."""
     from oracle import refpy
     ref = refpy.RefLib()
     threads = threads or len(os.sched_getaffinity(0))
@@ -165,12 +228,39 @@ def cpu_reference_sample(scene, cams, verts, sample_views=(0, 1), threads=None, 
     t0 = time.perf_counter()
     rc = ref.context(scene, sub)
     ev = rc.evaluator(refpy.ALL)
-    ev.label_grid(xyz, True, threads)
-    dt = time.perf_counter() - t0
+    labels = ev.label_grid(xyz, True, threads)
+    t_label = time.perf_counter() - t0
+    out = {"seconds_label": t_label, "threads": threads, "views": len(sample_views), "vertices": len(xyz),
+           "labels": labels, "pairs": ev.counters()["pairs"], "evaluator": ev, "context": rc}
     k = len(sample_views)
-    per_query = dt * (cams.v / k) / len(xyz)
-    return {"seconds": dt, "queries_per_s": 1.0 / per_query, "threads": threads, "views": k,
-            "vertices": len(xyz), "pairs": ev.counters()["pairs"]}
+    per_label_query = t_label * (cams.v / k) / len(xyz)
+    out["label_queries_per_s"] = 1.0 / per_label_query
+    if vertex_stride == 1 and refine_edges > 0:
+        e = crossing_edge_sample(xyz, labels, n_lattice, refine_edges)
+        used, inv = np.unique(e.ravel(), return_inverse=True)
+        ev2 = rc.evaluator(refpy.ALL)
+        sub_xyz = np.ascontiguousarray(xyz[used])
+        sub_e = inv.reshape(-1, 2).astype(np.int32)
+        t1 = time.perf_counter()
+        ev2.refine(sub_xyz, sub_e, 0.5 * (sub_xyz[sub_e[:, 0]] + sub_xyz[sub_e[:, 1]]), ITER)
+        t_ref = time.perf_counter() - t1
+        per_bisect_query = t_ref * (cams.v / k) / (ITER * len(e))
+        out.update(seconds_refine=t_ref, refine_edges=len(e), bisection_queries_per_s=1.0 / per_bisect_query)
+        q_label, q_bis = len(xyz), ITER * edges_total
+        out["queries_per_s"] = (q_label + q_bis) / (q_label * per_label_query + q_bis * per_bisect_query)
+    else:
+        out["queries_per_s"] = out["label_queries_per_s"]
+    return out
+
+
+def describe_cpu(r, V):
+    s = (f"reference label_grid (all strategies, ThreadPool({r['threads']})) over {r['vertices']} lattice vertices "
+         f"with views {{0,1}} incl. ViewSet::build + tile bindings ({r['seconds_label']:.1f} s)")
+    if "seconds_refine" in r:
+        s += (f" + binary_search_refine (8 iterations, serial classify_point) of {r['refine_edges']} crossing "
+              f"edges ({r['seconds_refine']:.1f} s); per-query times x{V // r['views']} in views, "
+              f"combined as N_v label + 8 E bisection queries")
+    return s
 
 
 def run_reference(args):
@@ -182,21 +272,19 @@ def run_reference(args):
     scene, cams, _ = config_inputs(args.config, lattice=False)
     verts, _ = kuhn_lattice(cfg["lattice"]) if cfg["lattice"] else (None, None)
     for _ in range(args.warmup):  # warm-up: a small sample (threads, page cache)
-        cpu_reference_sample(scene, cams, verts, vertex_stride=64)
+        cpu_reference_sample(scene, cams, verts, cfg["lattice"], cfg["edges"], vertex_stride=64, refine_edges=0)
     vals, secs = [], []
     for _ in range(args.steps):
-        r = cpu_reference_sample(scene, cams, verts)
+        r = cpu_reference_sample(scene, cams, verts, cfg["lattice"], cfg["edges"])
         vals.append(r["queries_per_s"])
-        secs.append(r["seconds"])
+        secs.append(r["seconds_label"] + r.get("seconds_refine", 0.0))
     v = float(np.median(vals))
-    sample = (f"reference label_grid (all strategies, ThreadPool({r['threads']})) over all {r['vertices']} "
-              f"lattice vertices with views {{0,1}} incl. ViewSet::build + tile bindings, "
-              f"{np.median(secs):.1f} s/step, extrapolated x{cams.v // 2} in views")
+    sample = describe_cpu(r, cams.v) + f", {np.median(secs):.1f} s/step"
     line = {"metric": "opacity-field point queries/sec", "value": v, "unit": "queries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(secs)) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: meshing step (label + 8-step bisection queries)",
+            "config": {"workload": f"{args.config}: meshing step (label + {ITER}-step bisection queries)",
                        "gaussians": cfg["gaussians"], "views": cfg["views"],
                        "resolution": [cfg["width"], cfg["height"]], "lattice": cfg["lattice"]},
             "cpu_baseline": {"value": v, "unit": "queries/s", "cores": r["threads"], "kind": "reference",
@@ -204,6 +292,41 @@ def run_reference(args):
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def c3_parity(device, scene, cams, verts, n_lattice, cpu_run, classify_points=10_000):
+    """Parity of the benchmark configuration itself, outside the timed region: the GPU
+    label over views {0, 1} of every lattice vertex against the reference's label_grid on
+    the same 2-view ViewSet (the cpu_baseline run above: values bit for bit, pairs and
+    point-view counters equal), and classify_point on a 10^4-point sample (crossing-edge
+    midpoints and uniform points) against the reference's classify_point."""
+    import paper_2506_19139_b200 as sof
+    want = cpu_run["labels"]
+    rev = cpu_run["evaluator"]
+    sub = cams.subset([0, 1])
+    ctx = sof.Context(device)
+    views = sof.ViewSet.build(scene, sub, ctx=ctx)
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
+    got = ev.label_grid(verts)
+    label_bad = int((got.view(np.uint64) != want.view(np.uint64)).sum())
+    label_counters = ev.counters() == rev.counters()
+    e = crossing_edge_sample(verts, want, n_lattice, classify_points // 2, seed=1)
+    rng = np.random.default_rng(2)
+    mid = np.concatenate([0.5 * (verts[e[:, 0]] + verts[e[:, 1]]),
+                          rng.uniform(verts.min(0), verts.max(0), (classify_points - len(e), 3))])
+    ev.reset_counters()
+    rev.reset_counters()
+    g = ev.classify_points(mid)
+    r = rev.classify_points(mid).astype(bool)
+    cls_bad = int((g != r).sum())
+    cls_counters = ev.counters() == rev.counters()
+    ctx.close()
+    return {"label_views01": {"vertices": int(len(verts)), "mismatched_values": label_bad,
+                              "counters_equal": bool(label_counters), "pairs": int(rev.counters()["pairs"] or 0)},
+            "classify_sample": {"points": int(len(mid)), "crossing_edge_midpoints": int(len(e)),
+                                "mismatched": cls_bad, "counters_equal": bool(cls_counters)},
+            "reference": "oracle/_ref (reference headers compiled in place)",
+            "bit_identical": label_bad == 0 and cls_bad == 0 and label_counters and cls_counters}
 
 
 # ---- ours ---------------------------------------------------------------------------------------
@@ -316,13 +439,19 @@ def main():
         fp64 = ctypes.c_double()
         ctx.check(lib.sof_fp64_peak(ctx.h, ctypes.byref(fp64)))
         achieved = pairs * FLOP_PER_PAIR / (eval_ms * 1e-3) / 1e12
+        nk = ncu_k_eval()
+        pps = pairs / (eval_ms * 1e-3)
         roof = {"bound": "fp64", "kernel": "k_eval (opacity evaluation, FP64 parity path)",
                 "achieved": achieved, "peak": fp64.value, "unit": "TFLOP/s", "frac": achieved / fp64.value,
-                "traffic": ncu_traffic(), "flop_per_pair": FLOP_PER_PAIR,
-                "pairs_per_s": pairs / (eval_ms * 1e-3), "kernel_share_of_step": eval_ms / prof_step_ms,
+                "traffic": nk.get("dram_bytes_per_launch"), "flop_per_pair": FLOP_PER_PAIR,
+                "pairs_per_s": pps, "kernel_share_of_step": eval_ms / prof_step_ms,
                 "avg_launch_ms": eval_ms / max(eval_launches, 1),
+                "issue_roofline_frac": pps / ISSUE_PAIRS_PER_S,
+                "ncu_fp64_pipe_active": nk.get("fp64_pipe_active_pct"),
+                "ncu_issue_active": nk.get("issue_active_pct"),
                 "peak_note": "FP64 FMA-pipe throughput measured in-process (sof_fp64_peak, 2 FLOP/DFMA); "
-                             "MEASURED_PEAKS.json has no FP64 figure"}
+                             "MEASURED_PEAKS.json has no FP64 figure. issue_roofline_frac: pairs/s against "
+                             "SURVEY.md 8(d)'s FP32 fast-path issue roofline (1.77e12 pairs/s)"}
 
     # e2e: the public C-ABI with host buffers: upload scene/views/tets, extract, fetch mesh
     e2e = None
@@ -343,13 +472,14 @@ def main():
         e2e = {"value": queries / float(np.median(times)), "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.median(times)) * 1e3}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    cpu, cpu_run = None, None
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_sample(scene, cams, verts)
-            cpu = {"value": r["queries_per_s"], "unit": "queries/s", "cores": r["threads"], "kind": "reference",
-                   "sample": f"reference label_grid over all {r['vertices']} vertices with views {{0,1}} "
-                             f"(incl. ViewSet::build + bindings), {r['seconds']:.1f} s, extrapolated x{V // 2} in views"}
+            cpu_run = cpu_reference_sample(scene, cams, verts, cfg["lattice"], E)
+            cpu = {"value": cpu_run["queries_per_s"], "unit": "queries/s", "cores": cpu_run["threads"],
+                   "kind": "reference", "sample": describe_cpu(cpu_run, V)}
+            if world > 1:
+                cpu["note"] = "measured on rank 0's host cores once; the same CPU job for every N"
         except Exception as e:  # the reference build is absent
             cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -379,6 +509,10 @@ def main():
     for a in host_arrays:
         lib.sof_host_unregister(a.ctypes.data)
     ctx.close()  # the render sample gets the whole device (the meshing cache holds ~half of HBM)
+    ok = True
+    if rank == 0 and cpu_run is not None:
+        line["parity"] = c3_parity(local, scene, cams, verts, cfg["lattice"], cpu_run)
+        ok = line["parity"].get("bit_identical", True)
     if rank == 0:
         render = None
         if world == 1 and not args.no_render:
@@ -387,9 +521,14 @@ def main():
             except Exception as e:
                 render = {"unavailable": str(e)[:200]}
         line["render"] = render
+        if render and render.get("parity", {}).get("bit_identical") is False:
+            ok = False
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+    if not ok:
+        print("PARITY FAILURE: the GPU results differ from the reference (see the parity objects)", file=sys.stderr)
+        return 3
     return 0
 
 

@@ -269,6 +269,28 @@ int sof_set_eval_path(sof_ctx* ctx, int path);
  * results; an sm_100a implementation choice (the reference has no equivalent). */
 int sof_set_staging(sof_ctx* ctx, int mode);
 
+/* ---- multi-GPU: a communicator owned by the context -------------
+ * One process per GPU. Rank 0 draws a unique id (an ncclUniqueId, 128 bytes), every rank
+ * receives it out of band (e.g. torch.distributed's broadcast) and calls sof_comm_init on
+ * its context. From then on sof_extract runs the sharded meshing step on the library
+ * stream: views split over the ranks for the label pass and the bisection (MIN / MAX
+ * all-reduces merge them exactly), tets split for Marching Tetrahedra (all-gathered
+ * edge / triangle lists merged into the whole-grid numbering), weld replicated; every rank
+ * ends with the same mesh, identical to the single-GPU one. Counters in the stats are the
+ * rank's own. NCCL is resolved at run time (libnccl.so.2); SOF_E_NCCL when absent. */
+#define SOF_COMM_ID_BYTES 128
+int sof_comm_unique_id(void* id_out /* SOF_COMM_ID_BYTES */);
+int sof_comm_init(sof_ctx* ctx, const void* id /* from rank 0's sof_comm_unique_id */, int nranks, int rank);
+/* Joins n contexts of ONE process (same device) into an in-process communicator whose
+ * collectives are device-side reductions between the contexts' buffers. Each context must
+ * then be driven from its own host thread (the collectives rendezvous on the host). For
+ * testing the sharded protocol with several ranks where only one GPU exists. */
+int sof_comm_init_local(sof_ctx* const* ctxs, int n);
+/* nranks / rank of the context (1 / 0 without a communicator); returns 0 = none,
+ * 1 = NCCL, 2 = in-process, <0 on error. */
+int sof_comm_info(const sof_ctx* ctx, int* nranks, int* rank);
+int sof_comm_destroy(sof_ctx* ctx);
+
 /* ---- results ------------------------------------------------------------------------ */
 int64_t sof_result_count(const sof_ctx* ctx, int kind); /* elements (not bytes); <0 if none */
 int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);

@@ -22,6 +22,7 @@ R_EDGES, R_EDGE_VERTS, R_TRIANGLES, R_MESH_VERTS, R_MESH_TRIS, R_GRID_OPACITY, R
 R_SEEDS, R_SEED_PROVENANCE = 9, 10
 SEED_STP, SEED_THREE_SIGMA, SEED_STRETCHED_SIGMA = 0, 1, 2
 SEED_CUT_NONE, SEED_CUT_DEAD = 0, 1
+SOF_COMM_ID_BYTES = 128
 
 _P = ctypes.c_void_p
 _D = ctypes.c_double
@@ -78,6 +79,11 @@ _SIGS = {
     "sof_render_normals": (_I, [_P, _I, _P, _P]),
     "sof_set_render_pool": (_I, [_P, _I64]),
     "sof_render_counts": (_I, [_P, _I, _P]),
+    "sof_comm_unique_id": (_I, [_P]),
+    "sof_comm_init": (_I, [_P, _P, _I, _I]),
+    "sof_comm_init_local": (_I, [_P, _I]),
+    "sof_comm_info": (_I, [_P, _P, _P]),
+    "sof_comm_destroy": (_I, [_P]),
     "sof_normal_from_depth": (_I, [_P, _I, _P, _P, _P]),
     "sof_gaussian_normals": (_I, [_P, ctypes.c_int64, _P, _P, _P, _P, _P]),
     "sof_seed_points": (_I, [_P, _I, _I, _D, _P]),

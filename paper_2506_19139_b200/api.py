@@ -246,6 +246,39 @@ class Context:
             self.check(self.lib.sof_copy_result(self.h, kind, _ptr(out)))
         return out.reshape(-1, width) if width > 1 else out
 
+    # -- multi-GPU: the context's communicator (include/sof_cuda.h, sof_comm_*) ------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """A fresh NCCL unique id (rank 0 draws it, every rank receives it out of band)."""
+        lib = L.load()
+        buf = ctypes.create_string_buffer(L.SOF_COMM_ID_BYTES)
+        st = lib.sof_comm_unique_id(buf)
+        if st != L.SOF_OK:
+            raise SofError(f"sof_comm_unique_id failed with status {st} (NCCL unavailable?)")
+        return buf.raw
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        """Attach an NCCL communicator: sof_extract then runs the sharded meshing step."""
+        buf = ctypes.create_string_buffer(bytes(uid), L.SOF_COMM_ID_BYTES)
+        self.check(self.lib.sof_comm_init(self.h, buf, int(nranks), int(rank)))
+
+    @staticmethod
+    def comm_init_local(ctxs) -> None:
+        """Join contexts of this process (one device) into an in-process communicator;
+        drive each from its own thread afterwards (tests of the sharded protocol)."""
+        arr = (_P * len(ctxs))(*[c.h for c in ctxs])
+        st = L.load().sof_comm_init_local(arr, len(ctxs))
+        if st != L.SOF_OK:
+            raise SofError(f"sof_comm_init_local failed with status {st}")
+
+    def comm_info(self) -> tuple[str, int, int]:
+        n, r = ctypes.c_int(), ctypes.c_int()
+        kind = self.lib.sof_comm_info(self.h, ctypes.byref(n), ctypes.byref(r))
+        return {0: "none", 1: "nccl", 2: "local"}.get(kind, "error"), n.value, r.value
+
+    def comm_destroy(self):
+        self.check(self.lib.sof_comm_destroy(self.h))
+
     # -- inspection / parity -------------------------------------------------------------
     def precompute_view(self, view: int) -> np.ndarray:
         out = np.empty((self.scene.n, 13))

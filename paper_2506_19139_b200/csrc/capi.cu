@@ -106,6 +106,7 @@ void sof_ctx_destroy(sof_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  sofk::comm_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   for (auto e : ctx->prep_ev)
@@ -547,27 +548,30 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     c->grid_opacity.ensure(std::max<int64_t>(nv, 1));
     SOF_CUDA(cudaEventRecord(e[0], c->stream));
     mark("start");
-    // label_grid (extract.hpp:59-61): classification mode, views in order
-    {
-      fill_f64(c, c->min_op.p, nv, 1.0);
-
-    }
-    zero_async(c, c->ext.p, nv);
     uint64_t cl[2] = {0, 0}, cr[2] = {0, 0};
-    eval_views(c, v0, v1, nv, c->tv.p, o.strategies, o.tile_size, true, kModeLabel, c->min_op.p,
-               c->ext.p, nullptr, nullptr, nullptr, cl);
-    finalize_label(c, nv, c->min_op.p, c->ext.p, c->grid_opacity.p);
-    c->grid_n = nv;
-    SOF_CUDA(cudaEventRecord(e[1], c->stream));
-    mark("label");
-    march(c, c->grid_opacity.p);
-    SOF_CUDA(cudaEventRecord(e[2], c->stream));
-    mark("march");
-    refine(c, c->n_edges, c->r_edges.p, c->r_everts.p, o.refine_iterations, o.strategies,
-           o.tile_size, v0, v1, cr);
-    SOF_CUDA(cudaEventRecord(e[3], c->stream));
-    mark("refine");
-    assemble(c, c->n_edges, c->r_everts.p, c->n_march_tris, c->r_tris.p, o.weld_eps, o.min_area);
+    if (c->comm) {
+      // multi-GPU: this rank's share of the views and tets, collectives on the stream
+      extract_sharded(c, o, v0, v1, cl, cr, e);
+      mark("sharded");
+    } else {
+      // label_grid (extract.hpp:59-61): classification mode, views in order
+      fill_f64(c, c->min_op.p, nv, 1.0);
+      zero_async(c, c->ext.p, nv);
+      eval_views(c, v0, v1, nv, c->tv.p, o.strategies, o.tile_size, true, kModeLabel, c->min_op.p,
+                 c->ext.p, nullptr, nullptr, nullptr, cl);
+      finalize_label(c, nv, c->min_op.p, c->ext.p, c->grid_opacity.p);
+      c->grid_n = nv;
+      SOF_CUDA(cudaEventRecord(e[1], c->stream));
+      mark("label");
+      march(c, c->grid_opacity.p);
+      SOF_CUDA(cudaEventRecord(e[2], c->stream));
+      mark("march");
+      refine(c, c->n_edges, c->r_edges.p, c->r_everts.p, o.refine_iterations, o.strategies,
+             o.tile_size, v0, v1, cr);
+      SOF_CUDA(cudaEventRecord(e[3], c->stream));
+      mark("refine");
+      assemble(c, c->n_edges, c->r_everts.p, c->n_march_tris, c->r_tris.p, o.weld_eps, o.min_area);
+    }
     SOF_CUDA(cudaEventRecord(e[4], c->stream));
     SOF_CUDA(cudaEventSynchronize(e[4]));
     mark("weld");

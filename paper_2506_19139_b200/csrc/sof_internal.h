@@ -30,6 +30,10 @@ struct StateError : std::runtime_error {
 struct OomError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Comm;  // k_comm.cu: the context's communicator (NCCL, or in-process for tests)
 
 #define SOF_CUDA(call)                                                                     \
   do {                                                                                     \
@@ -275,6 +279,9 @@ struct sof_ctx {
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<char> scan_tmp;                 // block totals of the hand-written scans (k_scan.cu)
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
+  sofk::Comm* comm = nullptr;                 // multi-GPU: owned communicator (sof_comm_init)
+  sofk::DBuf<int32_t> shard_i32, shard_send, shard_recv, shard_all;  // sharded-step scratch
+  sofk::DBuf<int64_t> shard_i64;
   sofk::DBuf<int64_t> d_scalar;               // small device scalars
 
   // tets
@@ -354,6 +361,12 @@ void seed_points(sof_ctx* c, int variant, int cutoff, double filter_scale);
 void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris,
               const int32_t* tris_dev, double weld_eps, double min_area);
 
+// ---- k_comm.cu ----------------------------------------------------------------------------
+void comm_destroy(sof_ctx* c);
+// the view- / tet-sharded label -> march -> refine -> weld with c->comm (records ev[1..3])
+void extract_sharded(sof_ctx* c, const sof_extract_opts& o, int vb, int ve, uint64_t* cl, uint64_t* cr,
+                     cudaEvent_t* ev);
+
 // ---- k_util.cu: phase timing -------------------------------------------------------------
 void zero_async(sof_ctx* c, void* p, int64_t bytes);
 void fill_f64(sof_ctx* c, double* p, int64_t n, double v);
@@ -413,6 +426,9 @@ inline int guard(sof_ctx* c, F&& f) {
   } catch (const OomError& e) {
     if (c) c->err = e.what();
     return SOF_E_OOM;
+  } catch (const NcclError& e) {
+    if (c) c->err = e.what();
+    return SOF_E_NCCL;
   } catch (const CudaError& e) {
     if (c) c->err = e.what();
     return SOF_E_CUDA;

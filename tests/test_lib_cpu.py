@@ -61,6 +61,21 @@ def test_loss_entry_points_reject_null_context():
     assert lib.sof_l1_rgb_loss(None, 1, p(z), p(z), p(z)) == _lib.SOF_E_INVALID
 
 
+def test_comm_entry_points_without_device():
+    """The communicator ABI: null checks, and a unique id from NCCL (resolved at run time)
+    or a clean SOF_E_NCCL where no NCCL library exists."""
+    lib = _lib.load()
+    assert lib.sof_comm_info(None, None, None) == _lib.SOF_E_INVALID
+    assert lib.sof_comm_init(None, None, 1, 0) == _lib.SOF_E_INVALID
+    assert lib.sof_comm_init_local(None, 0) == _lib.SOF_E_INVALID
+    assert lib.sof_comm_unique_id(None) == _lib.SOF_E_INVALID
+    buf = ctypes.create_string_buffer(_lib.SOF_COMM_ID_BYTES)
+    st = lib.sof_comm_unique_id(buf)
+    assert st in (_lib.SOF_OK, _lib.SOF_E_NCCL)
+    if st == _lib.SOF_OK:
+        assert any(buf.raw)
+
+
 def test_kuhn_lattice_valid():
     v, t = kuhn_lattice(6, -1, 1)
     assert v.shape == (216, 3) and t.shape == (6 * 125, 4)
