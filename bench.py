@@ -357,7 +357,10 @@ def main():
     if backend == "gloo" and local >= torch.cuda.device_count():
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    if world > 1:
+    # SOF_BENCH_COMM=1 (under torchrun) attaches the library communicator even at one rank,
+    # so the multi-GPU code path can be exercised where only one GPU exists
+    force_comm = os.environ.get("SOF_BENCH_COMM") == "1" and "RANK" in os.environ
+    if world > 1 or force_comm:
         import torch.distributed as dist
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -377,16 +380,27 @@ def main():
     ctx.set_scene(scene)
     ctx.set_views(cams)
     ctx.set_tets(verts, tets)
-    opt = sof.ExtractOptions(view_begin=v0, view_end=v1)
-    if world > 1:
+    opt = sof.ExtractOptions()
+    comm_kind = "single GPU"
+    if (world > 1 or force_comm) and backend == "nccl":
+        # the library owns the communicator: rank 0 draws the NCCL id, torch.distributed
+        # only carries it; sof_extract then shards views and tets with NCCL collectives on
+        # the library stream (k_comm.cu)
+        obj = [sof.Context.comm_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        ctx.comm_init(obj[0], world, rank)
+        comm_kind = f"library NCCL communicator, views and tets sharded x{world}"
+        step = lambda st: sof.extract_resident(ctx, opt, st, fetch=False)  # noqa: E731
+    elif world > 1:  # SOF_DIST_BACKEND=gloo: ranks may share a GPU; host-driven protocol (sharded.py)
         from paper_2506_19139_b200.sharded import ShardedMesher
         mesher = ShardedMesher(ctx, rank, world)
+        comm_kind = f"host protocol over gloo, views sharded x{world}"
         step = lambda st: mesher.extract(sof.ExtractOptions(), st, fetch=False)  # noqa: E731
     else:
         step = lambda st: sof.extract_resident(ctx, opt, st, fetch=False)  # noqa: E731
 
     def barrier():
-        if world > 1:
+        if world > 1 or force_comm:
             torch.distributed.barrier()
         ctx.check(lib.sof_sync(ctx.h))
         torch.cuda.synchronize()
@@ -411,9 +425,8 @@ def main():
     # one more step with per-kernel device timings, outside the timed region, for the
     # roofline (the timed steps run without the per-launch events)
     prof_stats = {}
-    if world == 1:
-        sof.extract_resident(ctx, sof.ExtractOptions(view_begin=v0, view_end=v1, profile=True), prof_stats,
-                             fetch=False)
+    if world == 1 or backend == "nccl":
+        sof.extract_resident(ctx, sof.ExtractOptions(profile=True), prof_stats, fetch=False)
     if world > 1:
         t = torch.tensor([total_ms], device="cuda" if backend == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -455,7 +468,7 @@ def main():
 
     # e2e: the public C-ABI with host buffers: upload scene/views/tets, extract, fetch mesh
     e2e = None
-    if args.e2e_steps > 0 and world == 1:
+    if args.e2e_steps > 0 and (world == 1 or backend == "nccl"):
         h2d = sum(a.nbytes for a in host_arrays) + cams.R.nbytes + cams.t.nbytes + cams.intr.nbytes + cams.wh.nbytes
         times, d2h = [], 0
         for k in range(args.e2e_steps + 1):
@@ -464,13 +477,21 @@ def main():
             ctx.set_scene(scene)
             ctx.set_views(cams)
             ctx.set_tets(verts, tets, async_copy=True)  # tets upload overlaps the label pass
-            mesh = sof.extract_resident(ctx, opt, {}, fetch=True)
+            # every rank holds the merged mesh; rank 0 delivers it to the host
+            mesh = sof.extract_resident(ctx, opt, {}, fetch=(rank == 0))
             dt = time.perf_counter() - t0
-            d2h = mesh.vertices.nbytes + mesh.triangles.nbytes
+            if world > 1:  # the job ends when the slowest rank is done
+                tt = torch.tensor([dt], device="cuda")
+                torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+                dt = float(tt.item())
+            if mesh is not None:
+                d2h = mesh.vertices.nbytes + mesh.triangles.nbytes
             if k > 0:
                 times.append(dt)
-        e2e = {"value": queries / float(np.median(times)), "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.median(times)) * 1e3}
+        # job totals: every rank uploads the inputs, rank 0 downloads the mesh
+        e2e = {"value": queries / float(np.median(times)), "unit": "queries/s",
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(np.median(times)) * 1e3}
 
     cpu, cpu_run = None, None
     if rank == 0 and not args.no_cpu_baseline:
@@ -492,7 +513,7 @@ def main():
                 "config": {"workload": f"{args.config}: meshing step (label + march + {ITER}-step bisection + weld)",
                            "gaussians": cfg["gaussians"], "views": V, "resolution": [cfg["width"], cfg["height"]],
                            "lattice": cfg["lattice"], "tets": int(len(tets)), "vertices": int(len(verts)),
-                           "parallelism": f"views sharded x{world}" if world > 1 else "single GPU",
+                           "parallelism": comm_kind,
                            "l2": f"inputs ({verts.nbytes / 1e9:.2f} GB vertices + {tets.nbytes / 1e9:.2f} GB tets + "
                                  f"per-view records of {cfg['gaussians'] * 128 / 1e9:.2f} GB) exceed the 126 MB L2"},
                 "meshing_wall_s": ms_step / 1e3, "queries_per_step": queries,
@@ -524,7 +545,7 @@ def main():
         if render and render.get("parity", {}).get("bit_identical") is False:
             ok = False
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or force_comm:
         torch.distributed.destroy_process_group()
     if not ok:
         print("PARITY FAILURE: the GPU results differ from the reference (see the parity objects)", file=sys.stderr)
