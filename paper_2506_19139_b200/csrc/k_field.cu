@@ -106,7 +106,8 @@ struct RectOut {
   uint32_t* cnt;
   uint64_t* zkey;
   int32_t* idx;
-  bool live_only;  // leave dead Gaussians (op < 1/255) out of the lists (see Binding::live)
+  bool live_only;   // leave dead Gaussians (op < 1/255) out of the lists (see Binding::live)
+  uint8_t* behind;  // live_only: 1 for gauss_behind Gaussians (counted, not listed)
 };
 
 // k_view_rec + k_tile_rect in one pass (one GaussStatic read per Gaussian and view).
@@ -127,7 +128,10 @@ __global__ void __launch_bounds__(128, SOF_REC_MINB) k_view_rec_rect(int64_t n, 
   out[i] = r;
   int tx0, tx1, ty0, ty1;
   uint32_t count = 0;
-  if (!(ro.live_only && r.op < kMinAlpha) && tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1)) {
+  const bool behind = ro.live_only && r.op >= kMinAlpha && gauss_behind(gs, cam, r.c);
+  if (ro.live_only) ro.behind[i] = behind;
+  if (!(ro.live_only && (r.op < kMinAlpha || behind)) &&
+      tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1)) {
     count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     ro.rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
@@ -220,7 +224,8 @@ const RecF* view_recf(sof_ctx* c, int view) {
 
 __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
                             const Rec* __restrict__ rec, Cam cam, int ts, int tiles_x, int tiles_y,
-                            bool live_only, int4* rect, uint32_t* cnt, uint64_t* zkey, int32_t* idx) {
+                            bool live_only, int4* rect, uint32_t* cnt, uint64_t* zkey, int32_t* idx,
+                            uint8_t* behind_out) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i > n) return;
   if (i == n) {  // sentinel for the exclusive scan over n + 1 counts
@@ -229,7 +234,10 @@ __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
   }
   int tx0, tx1, ty0, ty1;
   uint32_t count = 0;
-  if (!(live_only && rec[i].op < kMinAlpha) && tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1)) {
+  const bool behind = live_only && rec[i].op >= kMinAlpha && gauss_behind(g[i], cam, rec[i].c);
+  if (live_only) behind_out[i] = behind;
+  if (!(live_only && (rec[i].op < kMinAlpha || behind)) &&
+      tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1)) {
     count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
@@ -330,13 +338,14 @@ static void build_binding(sof_ctx* c, int view, int ts, bool live, Binding& b, b
   c->gidx_in.ensure(n);
   c->gidx_out.ensure(n);
   c->goff.ensure(n + 1);
-  const RectOut ro{ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p, live};
+  c->gbehind.ensure(n);
+  const RectOut ro{ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p, live, c->gbehind.p};
   bool rect_done = false;
   const Rec* rec = view_records_impl(c, view, &ro, &rect_done);
   if (!rect_done) {
     k_tile_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(n, c->gstat.p, rec, cam, ts, tiles_x,
                                                               tiles_y, live, c->rect.p, c->gcount.p,
-                                                              c->zkey_in.p, c->gidx_in.p);
+                                                              c->zkey_in.p, c->gidx_in.p, c->gbehind.p);
     SOF_LAUNCHED(c);
   }
   bin_by_key(c, view, ts, tiles_x, tiles_y, b, charge);
@@ -519,6 +528,31 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
 
 static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t M, int64_t T,
                                int tiles_x, int tiles_y) {
+
+  // (on the binding that is served: the view's cache or a scratch slot)
+  b.nb = 0;
+  if (b.live && c->n > 0) {  // the behind Gaussians: (min_z key, index) order, index order kept on ties
+    size_t bytes = 0;
+    thrust::counting_iterator<int32_t> it(0);
+    const uint8_t* flags = c->gbehind.p;
+    const int64_t n = c->n;
+    c->zkey_aux.ensure(n);
+    int32_t* sel = reinterpret_cast<int32_t*>(c->zkey_aux.p);  // n int32 of scratch
+    SOF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, sel, c->bin_scalar.p + 1, n, c->stream));
+    c->cub_tmp.ensure(bytes);
+    SOF_CUDA(cub::DeviceSelect::Flagged(c->cub_tmp.p, bytes, it, flags, sel, c->bin_scalar.p + 1, n, c->stream));
+    c->launches += 2;
+    const int64_t nb = read_scalar(c, c->bin_scalar.p + 1);
+    b.nb = nb;
+    if (nb > 0) {
+      b.bkey.ensure(2 * nb);
+      b.bidx.ensure(2 * nb);
+      k_gather_keys<<<grid_for(nb, 256), 256, 0, c->stream>>>(nb, sel, c->zkey_in.p, b.bkey.p + nb);
+      SOF_LAUNCHED(c);
+      SOF_CUDA(cudaMemcpyAsync(b.bidx.p + nb, sel, sizeof(int32_t) * nb, cudaMemcpyDeviceToDevice, c->stream));
+      sort_pairs_u64(c, b.bkey.p + nb, b.bkey.p, b.bidx.p + nb, b.bidx.p, nb, 64);  // stable: index order on ties
+    }
+  }
   const int64_t n = c->n;
   b.view = view;
   b.tile_size = ts;
@@ -823,9 +857,10 @@ __device__ __forceinline__ int chunk_limit(const Rec* rp, int cnt, double zp, bo
 #ifndef SOF_PAIR_CULL
 #define SOF_PAIR_CULL 1
 #endif
+// stop: the chunk position of the record at which the early stop happened (else -1).
 template <typename F>
 __device__ __forceinline__ unsigned scan_chunk(const Rec* rp, int cnt, double zp, float cu, float cv, float cuu,
-                                               float cvv, float cuv, bool& done, F&& eval_one) {
+                                               float cvv, float cuv, bool& done, int& stop, F&& eval_one) {
   bool brk;
   const int lim = chunk_limit(rp, cnt, zp, brk);
   int e = 0;
@@ -836,10 +871,12 @@ __device__ __forceinline__ unsigned scan_chunk(const Rec* rp, int cnt, double zp
     if (c0 && c1) continue;
     if (!c0 && eval_one(rp[e])) {
       done = true;
+      stop = e;
       return unsigned(e + 1);
     }
     if (!c1 && eval_one(rp[e + 1])) {
       done = true;
+      stop = e + 1;
       return unsigned(e + 2);
     }
   }
@@ -848,11 +885,38 @@ __device__ __forceinline__ unsigned scan_chunk(const Rec* rp, int cnt, double zp
     if (conic_culls(rp[e], cu, cv, cuu, cvv, cuv)) continue;  // alpha < 1/255 for sure
     if (eval_one(rp[e])) {
       done = true;
+      stop = e;
       return unsigned(e + 1);  // this pair was counted
     }
   }
   if (brk) done = true;  // the record at lim ends the sorted scan (not counted)
   return unsigned(lim);
+}
+
+// The view's behind Gaussians (Binding::nb), sorted by (min_z key, index).
+struct Behind {
+  const uint64_t* key;
+  const int32_t* idx;
+  int64_t n;
+};
+
+// Pairs the reference counts for the behind Gaussians of a point's scan: every one of
+// them precedes any min-z break (min_z < 0 < z_point) and none contributes, so all are
+// counted, unless the scan stopped early (classify mode, field_eval.hpp:104-107) at a
+// listed entry (stop_key, stop_idx) that precedes some of them in the (min_z, index)
+// order: then only those before it.
+__device__ __forceinline__ unsigned behind_pairs(const Behind& bh, bool stopped, uint64_t stop_key,
+                                                 int32_t stop_idx) {
+  if (bh.n == 0) return 0;
+  if (!stopped) return unsigned(bh.n);
+  int64_t lo = 0, hi = bh.n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const uint64_t k = __ldg(bh.key + mid);
+    if (k < stop_key || (k == stop_key && __ldg(bh.idx + mid) < stop_idx)) lo = mid + 1;
+    else hi = mid;
+  }
+  return unsigned(lo);
 }
 
 // One CTA = one schedule block (<= 256 points of one tile). The block's Gaussian
@@ -872,7 +936,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
     int tiles_x, const int64_t* __restrict__ loff, const int32_t* __restrict__ lent,
     int64_t n_gauss, const Rec* __restrict__ recs, int strategies, int classify, double* min_op,
     uint8_t* ext, double* o_out, uint8_t* obs_out, uint8_t* comp_out,
-    unsigned long long* pairs_counter, const __grid_constant__ CUtensorMap tmap) {
+    unsigned long long* pairs_counter, const __grid_constant__ CUtensorMap tmap, Behind bh) {
   static_assert(!FAST || TILED, "the fast loop relies on min_z-sorted tile lists");
   __shared__ __align__(128) Rec srec[STAGE == 1 ? 2 : 1][kChunk];
   __shared__ __align__(16) double s_exp[128];  // sof_exp's table (shared-memory latency)
@@ -926,10 +990,20 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
       }
       return false;
     };
+    int chunk_no = 0, stop = -1;
+    uint64_t stop_key = 0;
+    int32_t stop_idx = 0;
     auto eval_chunk = [&](const Rec* rp, int cnt) {
-      return scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, eval_one);
+      const unsigned p = scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, stop, eval_one);
+      if (stop >= 0 && bh.n > 0) {  // where the early stop happened, for behind_pairs
+        stop_key = double_key(rp[stop].zmin);
+        stop_idx = lp[chunk_no * kChunk + stop];
+      }
+      ++chunk_no;
+      return p;
     };
     pairs += stream_list<STAGE>(lp, len, recs, &tmap, srec, s_bar, done, eval_chunk);
+    if (active) pairs += behind_pairs(bh, stop >= 0, stop_key, stop_idx);
   } else {
     for (int64_t base = l0; base < l1; base += kChunk) {
       if (!__syncthreads_or(!done)) break;
@@ -1228,7 +1302,8 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
     const int64_t* const* __restrict__ loffs, const int32_t* const* __restrict__ lents,
     const Rec* const* __restrict__ recs_v, const CUtensorMap* __restrict__ tmaps, bool early,
     uint32_t* item_pairs, uint8_t* item_ext,
-    unsigned long long* counters) {
+    unsigned long long* counters, const uint64_t* const* __restrict__ bkeys,
+    const int32_t* const* __restrict__ bidxs, const int64_t* __restrict__ nbeh) {
   __shared__ __align__(128) Rec srec[STAGE == 1 ? 2 : 1][kChunk];
   __shared__ __align__(16) double s_exp[128];
   __shared__ __align__(8) uint64_t s_bar[2];
@@ -1278,10 +1353,22 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
     }
     return false;
   };
+  const Behind bh{bkeys[v], bidxs[v], nbeh[v]};
+  const int32_t* lp = lent + l0;
+  int chunk_no = 0, stop = -1;
+  uint64_t stop_key = 0;
+  int32_t stop_idx = 0;
   auto eval_chunk = [&](const Rec* rp, int cnt) {
-    return scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, eval_one);
+    const unsigned p = scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, stop, eval_one);
+    if (stop >= 0 && bh.n > 0) {
+      stop_key = double_key(rp[stop].zmin);
+      stop_idx = lp[chunk_no * kChunk + stop];
+    }
+    ++chunk_no;
+    return p;
   };
-  pairs += stream_list<STAGE>(lent + l0, int(l1 - l0), recs, tmap, srec, s_bar, done, eval_chunk);
+  pairs += stream_list<STAGE>(lp, int(l1 - l0), recs, tmap, srec, s_bar, done, eval_chunk);
+  if (active) pairs += behind_pairs(bh, stop >= 0, stop_key, stop_idx);
   if (active) {
     item_pairs[item] = pairs;
     item_ext[item] = (complete && 1.0 - survive < 0.5) ? 1 : 0;
@@ -1371,17 +1458,24 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
   const int V = int(c->cams.size());
   const int G = std::min(kGroupViews, v1 - v0);
   if (int64_t(G) * n >= (int64_t(1) << 31)) return false;
-  std::vector<const void*> ptrs(3 * size_t(V), nullptr);
+  std::vector<const void*> ptrs(5 * size_t(V), nullptr);
+  std::vector<int64_t> nbeh(size_t(V), 0);
   for (int v = v0; v < v1; ++v) {
-    ptrs[v] = c->bindings[v].off.p;
-    ptrs[V + v] = c->bindings[v].ent.p;
+    const Binding& bd = c->bindings[v];
+    ptrs[v] = bd.off.p;
+    ptrs[V + v] = bd.ent.p;
     ptrs[2 * V + v] = c->recs[v].p;
+    ptrs[3 * V + v] = bd.nb ? bd.bkey.p : nullptr;
+    ptrs[4 * V + v] = bd.nb ? bd.bidx.p : nullptr;
+    nbeh[v] = bd.nb;
   }
   GroupScratch& g = c->grp;
   g.cams.ensure(V);
-  g.ptrs.ensure(3 * V);
+  g.ptrs.ensure(5 * V);
+  g.nbeh.ensure(V);
   SOF_CUDA(cudaMemcpyAsync(g.cams.p, c->cams.data(), sizeof(Cam) * V, cudaMemcpyHostToDevice, c->stream));
-  SOF_CUDA(cudaMemcpyAsync(g.ptrs.p, ptrs.data(), sizeof(void*) * 3 * V, cudaMemcpyHostToDevice, c->stream));
+  SOF_CUDA(cudaMemcpyAsync(g.ptrs.p, ptrs.data(), sizeof(void*) * 5 * V, cudaMemcpyHostToDevice, c->stream));
+  SOF_CUDA(cudaMemcpyAsync(g.nbeh.p, nbeh.data(), sizeof(int64_t) * V, cudaMemcpyHostToDevice, c->stream));
   if (c->staging == 1) {  // TMA staging: one tensor map per view's record array
     std::vector<CUtensorMap> tmaps(static_cast<size_t>(V));
     std::memset(tmaps.data(), 0, sizeof(CUtensorMap) * size_t(V));
@@ -1402,6 +1496,8 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
   const int64_t* const* loffs = reinterpret_cast<const int64_t* const*>(g.ptrs.p);
   const int32_t* const* lents = reinterpret_cast<const int32_t* const*>(g.ptrs.p + V);
   const Rec* const* recs = reinterpret_cast<const Rec* const*>(g.ptrs.p + 2 * V);
+  const uint64_t* const* bkeys = reinterpret_cast<const uint64_t* const*>(g.ptrs.p + 3 * V);
+  const int32_t* const* bidxs = reinterpret_cast<const int32_t* const*>(g.ptrs.p + 4 * V);
   for (int g0 = v0; g0 < v1; g0 += G) {
     GroupTables gt;
     gt.g0 = g0;
@@ -1444,11 +1540,13 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
     if (c->staging == 1)
       k_eval_group<1><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
                                                              tile_size, gt, loffs, lents, recs, g.tmaps.p, early,
-                                                             g.item_pairs.p, g.item_ext.p, c->d_counters.p);
+                                                             g.item_pairs.p, g.item_ext.p, c->d_counters.p, bkeys,
+                                                             bidxs, g.nbeh.p);
     else
       k_eval_group<0><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
                                                              tile_size, gt, loffs, lents, recs, nullptr, early,
-                                                             g.item_pairs.p, g.item_ext.p, c->d_counters.p);
+                                                             g.item_pairs.p, g.item_ext.p, c->d_counters.p, bkeys,
+                                                             bidxs, g.nbeh.p);
     SOF_LAUNCHED(c);
     prof_span(c, e0, prof_mark(c), kProfEval);
     c->eval_launches++;
@@ -1582,6 +1680,12 @@ __global__ void k_trunc_emit(int64_t T, const int64_t* __restrict__ off, const i
   const int lane = threadIdx.x & 31;
   const int64_t b = off[t], ob = toff[t], L = toff[t + 1] - ob;
   for (int64_t k = lane; k < L; k += 32) out[ob + k] = pos[ent[b + k]];
+}
+
+__global__ void k_rows_of(int64_t nb, const int32_t* __restrict__ gidx, const int32_t* __restrict__ pos,
+                          int32_t* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < nb) out[i] = pos[gidx[i]] - 1;
 }
 
 __global__ void k_u8_to_i32_f(int64_t n, const uint8_t* __restrict__ a, int32_t* b) {
@@ -1724,6 +1828,17 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     b.ent.ensure(std::max<int64_t>(L, 1));
     k_trunc_emit<<<grid_for(T * 32, 256), 256, 0, c->stream>>>(T, full.off.p, full.ent.p, toff.p, pos.p, b.ent.p);
     SOF_LAUNCHED(c);
+    // the behind Gaussians, their indices in row space: rows keep the Gaussian order and
+    // a behind Gaussian has no row, so (pos[g] - 1 < row of the stop entry) is exactly
+    // (g < its Gaussian index) for behind_pairs' tie-break
+    b.nb = full.nb;
+    if (b.nb > 0) {
+      b.bkey.ensure(b.nb);
+      b.bidx.ensure(b.nb);
+      SOF_CUDA(cudaMemcpyAsync(b.bkey.p, full.bkey.p, sizeof(uint64_t) * b.nb, cudaMemcpyDeviceToDevice, c->stream));
+      k_rows_of<<<grid_for(b.nb, 256), 256, 0, c->stream>>>(b.nb, full.bidx.p, pos.p, b.bidx.p);
+      SOF_LAUNCHED(c);
+    }
     b.view = v;
     b.tile_size = tile_size;
     b.tiles_x = tiles_x;
@@ -1760,17 +1875,18 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
           strategies, classify, min_op, ext, o_out, obs, comp, pc);
   } else if (fast_loop(c, strategies)) {  // live-only lists, TMA-gathered records
     if (!bd->live) throw StateError("internal: the fast evaluation loop needs live-only tile lists");
+    const Behind bh{bd->bkey.p, bd->bidx.p, bd->nb};
     CUtensorMap tmap;
     std::memset(&tmap, 0, sizeof tmap);
     if (c->staging == 1) {
       if (sof_make_row_tmap(&tmap, rec, c->n) != 0) throw StateError("cuTensorMapEncodeTiled failed for the records");
       k_eval<MODE, true, true, 1><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
-          strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap);
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap, bh);
     } else {
       k_eval<MODE, true, true, 0><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
-          strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap);
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, tmap, bh);
     }
   } else {
     CUtensorMap none;
@@ -1778,11 +1894,11 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
     if (tiled)
       k_eval<MODE, true, false><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
-          strategies, classify, min_op, ext, o_out, obs, comp, pc, none);
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, none, Behind{nullptr, nullptr, 0});
     else
       k_eval<MODE, false, false><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
-          strategies, classify, min_op, ext, o_out, obs, comp, pc, none);
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, none, Behind{nullptr, nullptr, 0});
   }
   SOF_LAUNCHED(c);
   prof_span(c, e0, prof_mark(c), kProfEval);

@@ -356,6 +356,31 @@ __host__ __device__ inline bool tile_rect(const GaussStatic& g, const Cam& cam, 
   return tx0 <= tx1 && ty0 <= ty1;
 }
 
+// A live Gaussian lying behind the camera in Mahalanobis terms: its centre at view depth
+// zc < 0 and zc^2 >= s_z^2 (E^2 (1 + 1e-4) + 1e-4), s_z^2 the clamped-scale covariance's
+// variance along the view axis (so every point at view z >= 0 has squared Mahalanobis
+// distance q >= zc^2 / s_z^2 from it). Consequences, all exact:
+//  * the reference binds it to every tile (a box centred behind the plane has a corner at
+//    z <= 1e-9, tiles.hpp:116-126) with min_z < zc < 0, ahead of every other entry with
+//    min_z > 0 and of any min-z break (field_eval.hpp:90-93);
+//  * along a point ray (view z >= 0 for te >= 0) alpha = op exp(-q / 2) stays below
+//    (1 / 255) exp(-5e-5): the pair is counted (:94) and contributes nothing (:99-101);
+//    c <= 1e10 keeps the FP64 evaluation error of q far below that margin.
+// The fast evaluation loop therefore leaves these out of the tile lists and counts them
+// (Binding::nb).
+__host__ __device__ inline bool gauss_behind(const GaussStatic& g, const Cam& cam, double c_scalar) {
+  if (!(g.E > 0.0) || !(c_scalar <= 1e10)) return false;
+  const double zc = to_view_c(cam, 2, g.pos[0], g.pos[1], g.pos[2]);
+  if (!(zc < 0.0)) return false;
+  double czz = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    const double w = cam.R[6] * g.rot[k] + cam.R[7] * g.rot[3 + k] + cam.R[8] * g.rot[6 + k];  // (W R)_zk
+    const double sk = (g.scale[k] < kMinScale) ? kMinScale : g.scale[k];
+    czz += w * w * sk * sk;
+  }
+  return zc * zc >= czz * (g.E * g.E * (1.0 + 1e-4) + 1e-4) * (1.0 + 1e-12);
+}
+
 // ---- L2: per-point ray setup (field_eval.hpp:62-79) -------------------------------------
 
 struct PointRay {

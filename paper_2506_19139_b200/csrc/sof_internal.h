@@ -102,6 +102,12 @@ struct Binding {
   int64_t entries = 0;
   DBuf<int64_t> off;  // [T + 1]
   DBuf<int32_t> ent;  // [entries], per tile sorted by (min_z, index)
+  // live lists only: the gauss_behind Gaussians (sof_device.cuh), which the reference
+  // lists in every tile ahead of everything else and which never contribute: left out of
+  // the lists, sorted by (min_z key, index) here, and counted by the evaluation
+  int64_t nb = 0;
+  DBuf<uint64_t> bkey;  // double_key(min_z)
+  DBuf<int32_t> bidx;
 };
 
 // Scratch of the per-view point schedule (schedule_points tiles.hpp:29-84).
@@ -148,7 +154,8 @@ struct MeshScratch {
 // Grouped bisection classification (k_field.cu classify_grouped).
 struct GroupScratch {
   DBuf<Cam> cams;                 // [V]
-  DBuf<const void*> ptrs;         // [3V] per-view tile offsets, tile entries, records
+  DBuf<const void*> ptrs;         // [5V] per-view tile offsets, tile entries, records, behind keys / indices
+  DBuf<int64_t> nbeh;             // [V] behind counts
   DBuf<CUtensorMap> tmaps;        // [V] TMA descriptors of the per-view record arrays
   DBuf<int32_t> item_bin, order;  // [G n]
   DBuf<uint32_t> item_pairs;      // [G n]
@@ -247,6 +254,7 @@ struct sof_ctx {
   // binning scratch
   sofk::DBuf<int4> rect;
   sofk::DBuf<uint32_t> gcount;
+  sofk::DBuf<uint8_t> gbehind;     // per Gaussian: gauss_behind (live bindings)
   sofk::DBuf<uint64_t> zkey_in, zkey_out, zkey_aux;
   sofk::DBuf<char> loss_buf;       // batched training-loss inputs / outputs (k_loss.cu)
   sofk::DBuf<int64_t> bin_scalar;  // [2] selected count | tie-run overflow flag

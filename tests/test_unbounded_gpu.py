@@ -1,0 +1,81 @@
+"""Appendix B's unbounded layout with the cameras INSIDE the background shell.
+
+About half of the shell lies behind every camera; the reference binds those Gaussians
+to every tile (tiles.hpp:116-126) ahead of all other entries, and counts them as pairs
+for every evaluated point (field_eval.hpp:94) although they never contribute. The fast
+evaluation loop leaves them out of the tile lists and counts them (gauss_behind,
+Binding::nb, behind_pairs in k_field.cu); the extraction must still equal the
+reference's mesh byte for byte with identical pair / point-view counters — in the label
+pass, the per-view bisection and the truncated bisection caches.
+"""
+import numpy as np
+import pytest
+
+import paper_2506_19139_b200 as sof
+from paper_2506_19139_b200.workloads import kuhn_lattice, orbit_cameras, unbounded_scene
+from oracle.refpy import Cameras, Scene
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def case(ref):
+    c = orbit_cameras(8, 64, 48, radius=4.0)
+    s = unbounded_scene(4000, 5, c)
+    scene = Scene(s.pos, s.scale, s.rot, s.opacity, s.dc)
+    cams = Cameras(c.R, c.t, c.intr, c.wh, c.nearfar)
+    verts, tets = kuhn_lattice(16)
+    rc = ref.context(scene, cams)
+    # behind the cameras in Mahalanobis terms: centre depth beyond the bound
+    zc = np.einsum("vj,nj->vn", cams.R[:, 2, :], s.pos) + cams.t[:, 2:3]
+    assert (zc < -1.0).sum(axis=1).min() > 50  # shell Gaussians behind every camera
+    return scene, cams, verts, tets, rc
+
+
+@pytest.mark.parametrize("budget", [None, 0])
+@pytest.mark.parametrize("mask", [31, 27, 23])
+def test_unbounded_extract_matches_reference(case, tmp_path, mask, budget):
+    scene, cams, verts, tets, rc = case
+    want = rc.extract_tetgrid(verts, tets, strategies=mask, iterations=8)
+    assert len(want["triangles"]) > 100
+    ctx = sof.Context(0)
+    views = sof.ViewSet.build(scene, cams, ctx=ctx)
+    if budget is not None:  # bisection through truncated caches
+        ctx.check(ctx.lib.sof_set_cache_budget(ctx.h, budget))
+    st = {}
+    mesh = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets),
+                            sof.ExtractOptions(strategies=sof.EvalStrategies.from_mask(mask)), st)
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(want["vertices"]))
+    np.testing.assert_array_equal(mesh.triangles, want["triangles"])
+    assert st["pairs"] == int(want["counters"][0])
+    assert st["point_view_evals"] == int(want["counters"][1])
+    ctx.close()
+
+
+@pytest.mark.parametrize("classify", [True, False])
+def test_unbounded_label_and_views(case, classify):
+    """label_grid in both modes and view_opacity per view (early stop and value mode)."""
+    from oracle.refpy import ALL
+    scene, cams, verts, tets, rc = case
+    rev = rc.evaluator(ALL)
+    want = rev.label_grid(verts, classify)
+    ctx = sof.Context(0)
+    views = sof.ViewSet.build(scene, cams, ctx=ctx)
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
+    got = ev.label_grid(verts, classify)
+    np.testing.assert_array_equal(bits(got), bits(want))
+    assert ev.counters() == rev.counters()
+    for v in range(cams.v):
+        rev.reset_counters()
+        ev.reset_counters()
+        o, ob, co = ev.view_opacity(v, verts[::7], classify)
+        wo, wob, wco = rev.view_opacity(v, verts[::7], classify)
+        np.testing.assert_array_equal(bits(o), bits(wo))
+        np.testing.assert_array_equal(ob, wob.astype(bool))
+        np.testing.assert_array_equal(co, wco.astype(bool))
+        assert ev.counters() == rev.counters()
+    ctx.close()
