@@ -13,10 +13,11 @@
 //    V x N PrecomputedGaussian (opacity_field.hpp:26-34 would need 62 GB at 3M x 200);
 //    per-view preprocessing is lazy on the device.
 //  * FieldEvaluator methods accept batches (std::vector<Vec3>) besides single points.
-//  * extract_mesh gains the tetra-input overload (the seeds + Delaunay producer,
-//    seed_points.hpp / delaunay.hpp, is out of scope); binary_search_refine gains the
-//    batched overload taking the evaluator; the std::function overload keeps the
-//    reference's host loop for arbitrary user predicates.
+//  * extract_mesh keeps the reference signature (seeds on the device, the reference's
+//    Delaunay tet list from sof_tetrahedralize, then the fused device pipeline) and
+//    gains a tetra-input overload; binary_search_refine and level_set_residuals gain
+//    batched overloads taking the evaluator (the refine adds its counters into it); the
+//    std::function overloads keep the reference's host loops for arbitrary predicates.
 #pragma once
 
 #include <Eigen/Dense>
@@ -24,6 +25,7 @@
 #include <algorithm>
 #include <array>
 #include <charconv>
+#include <chrono>
 #include <cctype>
 #include <cmath>
 #include <cstdint>
@@ -313,6 +315,11 @@ class FieldEvaluator {
     return c;
   }
   void reset_counters() const { counters_[0] = counters_[1] = 0; }
+  // the batched refine's classify passes count like classify_point calls (field_eval.hpp:178-181)
+  void add_counters(std::uint64_t pairs, std::uint64_t point_view_evals) const {
+    counters_[0] += pairs;
+    counters_[1] += point_view_evals;
+  }
 
   sof_ctx* ctx() const { return views_->ctx.get(); }
   int tile_size() const { return tile_size_; }
@@ -373,68 +380,138 @@ inline RefineStats binary_search_refine(MarchingResult& m, const TetGrid& grid,
   detail::check(c, sof_refine(c, Index(m.edges.size()), e.data(), v.data(), iterations,
                               eval.strategies().mask(), eval.tile_size(), cnt));
   m.vertices = detail::unflat(v);
-  return {};
+  eval.add_counters(cnt[0], cnt[1]);
+  return RefineStats{};  // no bracket re-check: bracket_lost stays 0 (verify_brackets=false)
+}
+
+// level_set_residuals (marching_tets.hpp:117-124), reference host loop around any value query.
+inline std::vector<double> level_set_residuals(const MarchingResult& m,
+                                               const std::function<double(const Vec3&)>& value) {
+  std::vector<double> out(m.vertices.size());
+  for (size_t i = 0; i < m.vertices.size(); ++i) out[i] = std::abs(value(m.vertices[i]) - 0.5);
+  return out;
+}
+
+// Batched overload: one device value_at pass over all vertices (pass the NAIVE evaluator
+// for the exact field values extract.hpp:66-69 asks for).
+inline std::vector<double> level_set_residuals(const MarchingResult& m, const FieldEvaluator& exact) {
+  std::vector<double> out = exact.value_at(m.vertices);
+  for (double& r : out) r = std::abs(r - 0.5);
+  return out;
 }
 
 // assemble_mesh (mesh.hpp:36-79) on the GPU.
 inline Mesh assemble_mesh(const std::vector<Vec3>& vertices, const std::vector<std::array<int, 3>>& triangles,
                           const std::vector<double>* residuals = nullptr, double weld_eps = 1e-7,
                           double min_area = 1e-14) {
-  if (residuals) throw std::invalid_argument("residual passthrough is not supported by the device weld");
+  if (residuals && residuals->size() != vertices.size())
+    throw std::invalid_argument("residuals must have one value per vertex");
   sof_ctx* c = detail::default_ctx().get();
   const std::vector<double> v = detail::flat(vertices);
   std::vector<int32_t> t(3 * triangles.size());
   for (size_t i = 0; i < triangles.size(); ++i)
     for (int k = 0; k < 3; ++k) t[3 * i + k] = triangles[i][k];
   int64_t nv = 0, nt = 0;
-  detail::check(c, sof_assemble(c, Index(vertices.size()), v.data(), Index(triangles.size()), t.data(),
-                                weld_eps, min_area, &nv, &nt));
-  return detail::fetch_mesh(c);
+  detail::check(c, sof_assemble_residuals(c, Index(vertices.size()), v.data(), residuals ? residuals->data() : nullptr,
+                                          Index(triangles.size()), t.data(), weld_eps, min_area, &nv, &nt));
+  Mesh m = detail::fetch_mesh(c);
+  if (residuals) m.residuals = detail::result<double>(c, SOF_R_MESH_RESIDUALS);
+  return m;
 }
 
-// extract.hpp:12-33 (seeds / Delaunay fields dropped: the tetra input is given)
+// delaunay_tetrahedralize (delaunay.hpp:52-142): the reference's Bowyer-Watson tet list,
+// bit for bit (sof_tetrahedralize, the host stage of the tetra-input producer).
+inline TetGrid delaunay_tetrahedralize(const std::vector<Vec3>& points, sof_ctx* c = nullptr) {
+  if (!c) c = detail::default_ctx().get();
+  const std::vector<double> p = detail::flat(points);
+  int64_t nt = 0;
+  detail::check(c, sof_tetrahedralize(c, Index(points.size()), p.data(), &nt));
+  const std::vector<int32_t> t = detail::result<int32_t>(c, SOF_R_TETS);
+  TetGrid grid;
+  grid.vertices = points;
+  grid.tetrahedra.resize(t.size() / 4);
+  for (size_t i = 0; i < grid.tetrahedra.size(); ++i)
+    grid.tetrahedra[i] = {t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]};
+  return grid;
+}
+
+enum class BoundingVariant { kStp, kThreeSigma, kStretchedSigma };  // seed_points.hpp:15
+enum class SeedCutoff { kNone, kDeadGaussians };                     // seed_points.hpp:17
+enum class SeedProvenance : std::uint8_t { kCenter, kBoundCorner };
+
+struct SeedPointSet;
+inline SeedPointSet build_seed_points(const ViewSet& views, BoundingVariant variant, SeedCutoff cutoff,
+                                      double filter_scale);
+
+// extract.hpp:12-20
 struct ExtractOptions {
+  BoundingVariant bounding = BoundingVariant::kStp;
+  SeedCutoff cutoff = SeedCutoff::kDeadGaussians;
   EvalStrategies strategies = EvalStrategies::all();
   int refine_iterations = 8;
   int tile_size = kDefaultTileSize;
   double filter_scale = 0.0;
+  bool compute_residuals = false;  // needs exact field values, extra cost
 };
 
+// extract.hpp:22-33 (+ seconds_weld: the device weld is timed separately)
 struct ExtractStats {
+  size_t seed_points = 0;
   size_t tetrahedra = 0;
   size_t crossing_edges = 0;
   EvalCounters counters;
   RefineStats refine;
+  double seconds_seed = 0.0;
+  double seconds_delaunay = 0.0;
   double seconds_label = 0.0;
   double seconds_march = 0.0;
   double seconds_refine = 0.0;
   double seconds_weld = 0.0;
 };
 
-// extract_mesh with the tetra input given: label -> march -> refine -> weld on the GPU.
-inline Mesh extract_mesh(const std::vector<GaussianPrimitive>& /*gaussians*/, const ViewSet& views,
-                         const TetGrid& grid, const ExtractOptions& opt = {}, ExtractStats* stats = nullptr) {
-  sof_ctx* c = views.ctx.get();
-  detail::upload_tets(c, grid);
+namespace detail {
+// label -> march -> refine (-> residuals) -> weld over the resident tets, fused on the device
+inline Mesh extract_resident(sof_ctx* c, size_t n_tets, const ExtractOptions& opt, ExtractStats* stats) {
   sof_extract_opts o;
   sof_extract_opts_default(&o);
   o.strategies = opt.strategies.mask();
   o.tile_size = opt.tile_size;
   o.refine_iterations = opt.refine_iterations;
+  o.compute_residuals = opt.compute_residuals ? 1 : 0;
   sof_extract_stats st{};
-  detail::check(c, sof_extract(c, &o, &st));
+  check(c, sof_extract(c, &o, &st));
   if (stats) {
-    stats->tetrahedra = grid.tetrahedra.size();
+    stats->tetrahedra = n_tets;
     stats->crossing_edges = size_t(st.crossing_edges);
     stats->counters.pairs = st.pairs;
     stats->counters.point_view_evals = st.point_view_evals;
+    stats->refine = RefineStats{};
     stats->seconds_label = st.ms_label * 1e-3;
     stats->seconds_march = st.ms_march * 1e-3;
     stats->seconds_refine = st.ms_refine * 1e-3;
     stats->seconds_weld = st.ms_weld * 1e-3;
   }
-  return detail::fetch_mesh(c);
+  Mesh m = fetch_mesh(c);
+  if (opt.compute_residuals) m.residuals = result<double>(c, SOF_R_MESH_RESIDUALS);
+  return m;
 }
+}  // namespace detail
+
+// extract_mesh with the tetra input given: label -> march -> refine -> weld on the GPU.
+inline Mesh extract_mesh(const std::vector<GaussianPrimitive>& /*gaussians*/, const ViewSet& views,
+                         const TetGrid& grid, const ExtractOptions& opt = {}, ExtractStats* stats = nullptr) {
+  sof_ctx* c = views.ctx.get();
+  detail::upload_tets(c, grid);
+  return detail::extract_resident(c, grid.tetrahedra.size(), opt, stats);
+}
+
+// extract_mesh (extract.hpp:35-86) with the reference's signature: the seeds
+// (build_seed_points, device) and their Delaunay tetrahedralization (host, the
+// reference's tet list exactly) feed the fused device pipeline. `gaussians` must be the
+// scene the ViewSet was built from (it is resident on the device); the pool argument is
+// accepted and ignored (the GPU grid replaces it).
+inline Mesh extract_mesh(const std::vector<GaussianPrimitive>& gaussians, const ViewSet& views,
+                         const ExtractOptions& opt, ExtractStats* stats = nullptr, const void* /*pool*/ = nullptr);
 
 // render.hpp:10-24
 template <typename T>
@@ -593,10 +670,8 @@ inline FloatMap normals_to_map(const NormalMap& nm) {
 }
 
 // ---- seed points (seed_points.hpp:15-87), on the device ----------------------------------
+// (BoundingVariant / SeedCutoff / SeedProvenance are declared with ExtractOptions above)
 
-enum class BoundingVariant { kStp, kThreeSigma, kStretchedSigma };
-enum class SeedCutoff { kNone, kDeadGaussians };
-enum class SeedProvenance : std::uint8_t { kCenter, kBoundCorner };
 
 struct SeedPointSet {
   std::vector<Vec3> points;
@@ -624,6 +699,28 @@ inline SeedPointSet build_seed_points(const ViewSet& views, BoundingVariant vari
     out.provenance.push_back(SeedProvenance(prov[size_t(i)]));
   }
   return out;
+}
+
+inline Mesh extract_mesh(const std::vector<GaussianPrimitive>& gaussians, const ViewSet& views,
+                         const ExtractOptions& opt, ExtractStats* stats, const void* /*pool*/) {
+  using clock = std::chrono::steady_clock;
+  auto seconds = [](clock::time_point a, clock::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  if (gaussians.size() != size_t(sof_scene_size(views.ctx.get())))
+    throw std::invalid_argument("extract_mesh: gaussians differ from the ViewSet's scene");
+  sof_ctx* c = views.ctx.get();
+  const auto t0 = clock::now();
+  const SeedPointSet seeds = build_seed_points(views, opt.bounding, opt.cutoff, opt.filter_scale);
+  const auto t1 = clock::now();
+  const TetGrid grid = delaunay_tetrahedralize(seeds.points, c);
+  const auto t2 = clock::now();
+  detail::upload_tets(c, grid);
+  Mesh m = detail::extract_resident(c, grid.tetrahedra.size(), opt, stats);
+  if (stats) {
+    stats->seed_points = seeds.points.size();
+    stats->seconds_seed = seconds(t0, t1);
+    stats->seconds_delaunay = seconds(t1, t2);
+  }
+  return m;
 }
 
 // ---- scene files (io_scene.hpp) ---------------------------------------------------------

@@ -68,7 +68,9 @@ enum {
   SOF_R_TILE_OFFSETS = 7,  /* int64[T+1] per-tile list offsets of the last binding */
   SOF_R_TILE_ENTRIES = 8,  /* int32[M]   per-tile Gaussian lists (TileBinding, tiles.hpp:88-92) */
   SOF_R_SEEDS = 9,         /* f64[3S]    SeedPointSet::points (seed_points.hpp:24-27) */
-  SOF_R_SEED_PROVENANCE = 10 /* uint8[S] SeedPointSet::provenance: 0 centre, 1 bound corner */
+  SOF_R_SEED_PROVENANCE = 10, /* uint8[S] SeedPointSet::provenance: 0 centre, 1 bound corner */
+  SOF_R_MESH_RESIDUALS = 11,  /* f64[V] Mesh::residuals (mesh.hpp:16), when computed */
+  SOF_R_TETS = 12             /* int32[4T] the tets of the last sof_tetrahedralize */
 };
 
 typedef struct sof_ctx sof_ctx;
@@ -85,6 +87,9 @@ typedef struct sof_extract_opts {
   int view_end;
   int profile;           /* 1: per-kernel device timings (ms_eval_kernel, ms_prep, ...); adds
                             two events per launch and a host-side collection; default 0 */
+  int compute_residuals; /* ExtractOptions::compute_residuals (extract.hpp:19,65-72): per mesh
+                            vertex |value_at - 0.5| with naive strategies, carried through the
+                            weld (result SOF_R_MESH_RESIDUALS); default 0 */
 } sof_extract_opts;
 
 /* Per-stage statistics (ExtractStats extract.hpp:22-33) plus device timings. */
@@ -119,6 +124,8 @@ const char* sof_last_error(const sof_ctx* ctx);
 int sof_version(void);
 /* number of kernels launched on this context so far (instrumentation) */
 int64_t sof_kernel_launches(const sof_ctx* ctx);
+/* Gaussians of the resident scene; -1 before sof_set_scene. */
+int64_t sof_scene_size(const sof_ctx* ctx);
 
 /* ---- inputs ----------------------------------------------------------------- */
 /* Replaces the scene half of ViewSet::build (opacity_field.hpp:26-34) and the
@@ -238,6 +245,12 @@ int sof_refine(sof_ctx* ctx, int64_t n_edges, const int32_t* edges, double* vert
 int sof_assemble(sof_ctx* ctx, int64_t n_verts, const double* verts, int64_t n_tris,
                  const int32_t* tris, double weld_eps, double min_area, int64_t* out_verts,
                  int64_t* out_tris);
+/* assemble_mesh with its residual passthrough (mesh.hpp:36-79, :66): residuals[nverts]
+ * (nullable) are carried to the welded vertices (first appearance); result kind
+ * SOF_R_MESH_RESIDUALS. */
+int sof_assemble_residuals(sof_ctx* ctx, int64_t nverts, const double* verts, const double* residuals,
+                           int64_t ntris, const int32_t* tris, double weld_eps, double min_area,
+                           int64_t* out_verts, int64_t* out_tris);
 /* extract_mesh's label -> march -> refine -> assemble (extract.hpp:59-78) over the
  * resident scene, views and tets, entirely on the device. */
 int sof_extract(sof_ctx* ctx, const sof_extract_opts* opts, sof_extract_stats* stats);
@@ -290,6 +303,15 @@ int sof_comm_init_local(sof_ctx* const* ctxs, int n);
  * 1 = NCCL, 2 = in-process, <0 on error. */
 int sof_comm_info(const sof_ctx* ctx, int* nranks, int* rank);
 int sof_comm_destroy(sof_ctx* ctx);
+
+/* ---- the tetra-input producer ------------------------------------ */
+/* delaunay_tetrahedralize (delaunay.hpp:52-142) of n points on the HOST: the reference's
+ * incremental Bowyer-Watson (same enclosing tetrahedron, in-circumsphere slack, cavity
+ * re-closing order and arithmetic), so the tet list — and the mesh numbering MT derives
+ * from it — is the reference's. O(n^2): small seed sets. *n_tets = T; tets via
+ * sof_copy_result(SOF_R_TETS). Errors: "need at least 4 points", "degenerate (coplanar)
+ * point set". */
+int sof_tetrahedralize(sof_ctx* ctx, int64_t n, const double* pts, int64_t* n_tets);
 
 /* ---- results ------------------------------------------------------------------------ */
 int64_t sof_result_count(const sof_ctx* ctx, int kind); /* elements (not bytes); <0 if none */

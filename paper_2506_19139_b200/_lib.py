@@ -19,7 +19,7 @@ TILE_SCHEDULING, MIN_Z, EARLY_STOP, PRUNE, DEAD_CULL = 1, 2, 4, 8, 16
 ALL_STRATEGIES, NAIVE = 31, 0
 DEPTH_MEDIAN, DEPTH_EXACT = 0, 1
 R_EDGES, R_EDGE_VERTS, R_TRIANGLES, R_MESH_VERTS, R_MESH_TRIS, R_GRID_OPACITY, R_TILE_OFFSETS, R_TILE_ENTRIES = range(1, 9)
-R_SEEDS, R_SEED_PROVENANCE = 9, 10
+R_SEEDS, R_SEED_PROVENANCE, R_MESH_RESIDUALS, R_TETS = 9, 10, 11, 12
 SEED_STP, SEED_THREE_SIGMA, SEED_STRETCHED_SIGMA = 0, 1, 2
 SEED_CUT_NONE, SEED_CUT_DEAD = 0, 1
 SOF_COMM_ID_BYTES = 128
@@ -32,7 +32,8 @@ _I64 = ctypes.c_int64
 
 class ExtractOpts(ctypes.Structure):
     _fields_ = [("strategies", _I), ("tile_size", _I), ("refine_iterations", _I),
-                ("weld_eps", _D), ("min_area", _D), ("view_begin", _I), ("view_end", _I), ("profile", _I)]
+                ("weld_eps", _D), ("min_area", _D), ("view_begin", _I), ("view_end", _I), ("profile", _I),
+                ("compute_residuals", _I)]
 
 
 class ExtractStats(ctypes.Structure):
@@ -52,6 +53,7 @@ _SIGS = {
     "sof_version": (_I, []),
     "sof_last_error": (ctypes.c_char_p, [_P]),
     "sof_kernel_launches": (_I64, [_P]),
+    "sof_scene_size": (_I64, [_P]),
     "sof_ctx_create": (_I, [_I, ctypes.POINTER(_P)]),
     "sof_ctx_destroy": (None, [_P]),
     "sof_set_scene": (_I, [_P, _I64, _P, _P, _P, _P, _P, _D]),
@@ -71,6 +73,8 @@ _SIGS = {
     "sof_marching_tets": (_I, [_P, _P, _P, _P]),
     "sof_refine": (_I, [_P, _I64, _P, _P, _I, _I, _I, _P]),
     "sof_assemble": (_I, [_P, _I64, _P, _I64, _P, _D, _D, _P, _P]),
+    "sof_assemble_residuals": (_I, [_P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P]),
+    "sof_tetrahedralize": (_I, [_P, _I64, _P, ctypes.POINTER(_I64)]),
     "sof_extract": (_I, [_P, ctypes.POINTER(ExtractOpts), ctypes.POINTER(ExtractStats)]),
     "sof_extract_opts_default": (None, [ctypes.POINTER(ExtractOpts)]),
     "sof_result_count": (_I64, [_P, _I]),

@@ -154,6 +154,7 @@ class ExtractOptions:
     view_begin: int = -1
     view_end: int = -1
     profile: bool = False  # per-kernel device timings in the stats (adds host-side cost)
+    compute_residuals: bool = False  # extract.hpp:19,65-72: |exact value_at - 0.5| per mesh vertex
 
 
 # ---- device context ------------------------------------------------------------------------
@@ -418,34 +419,54 @@ def assemble_mesh(vertices, triangles, residuals=None, weld_eps: float = 1e-7, m
     ctx = ctx or default_context()
     v = _f64(vertices, 3) if len(vertices) else np.zeros((0, 3))
     t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+    r = None if residuals is None else _f64(residuals).reshape(-1)
+    if r is not None and len(r) != len(v):
+        raise ValueError("one residual per vertex")
     nv, nt = ctypes.c_int64(), ctypes.c_int64()
-    ctx.check(ctx.lib.sof_assemble(ctx.h, len(v), _ptr(v), len(t), _ptr(t), float(weld_eps), float(min_area),
-                                   ctypes.byref(nv), ctypes.byref(nt)))
-    if residuals is not None:
-        raise ValueError("residual passthrough is not supported by the device weld")
-    return Mesh(ctx.result(L.R_MESH_VERTS, np.float64, 3), ctx.result(L.R_MESH_TRIS, np.int32, 3))
+    ctx.check(ctx.lib.sof_assemble_residuals(ctx.h, len(v), _ptr(v), _ptr(r), len(t), _ptr(t), float(weld_eps),
+                                             float(min_area), ctypes.byref(nv), ctypes.byref(nt)))
+    res = ctx.result(L.R_MESH_RESIDUALS, np.float64, 1) if r is not None else np.zeros(0)
+    return Mesh(ctx.result(L.R_MESH_VERTS, np.float64, 3), ctx.result(L.R_MESH_TRIS, np.int32, 3), res)
 
 
-def extract_mesh(gaussians, views: ViewSet, grid: TetGrid, opt: ExtractOptions | None = None,
-                 stats: dict | None = None) -> Mesh:
-    """extract_mesh's label -> march -> refine -> weld (extract.hpp:59-78) on a given
-    tetra grid, fused on the device."""
+def delaunay_tetrahedralize(points, ctx: Context | None = None) -> TetGrid:
+    """delaunay_tetrahedralize (delaunay.hpp:52-142): the reference's Bowyer-Watson tet
+    list (host stage of the tetra-input producer, sof_tetrahedralize)."""
+    ctx = ctx or default_context()
+    p = _f64(points, 3)
+    nt = ctypes.c_int64()
+    ctx.check(ctx.lib.sof_tetrahedralize(ctx.h, len(p), _ptr(p), ctypes.byref(nt)))
+    return TetGrid(p.copy(), ctx.result(L.R_TETS, np.int32, 4), np.zeros(len(p)))
+
+
+def extract_mesh(gaussians, views: ViewSet, grid: TetGrid | None = None, opt: ExtractOptions | None = None,
+                 stats: dict | None = None, bounding: int = L.SEED_STP, cutoff: int = L.SEED_CUT_DEAD) -> Mesh:
+    """extract_mesh (extract.hpp:35-86). With `grid`: label -> march -> refine -> weld on
+    the given tetra input, fused on the device. Without: the reference's own producer
+    first — build_seed_points (device) and delaunay_tetrahedralize (host), with the
+    reference's defaults (BoundingVariant::kStp, SeedCutoff::kDeadGaussians)."""
     opt = opt or ExtractOptions()
     ctx = views.ctx
+    if grid is None:
+        seeds = build_seed_points(ctx, bounding, cutoff, views.filter_scale)
+        grid = delaunay_tetrahedralize(seeds.points, ctx)
+        if stats is not None:
+            stats.update(seed_points=len(seeds.points), tetrahedra=len(grid.tetrahedra))
     ctx.set_tets(grid.vertices, grid.tetrahedra)
     return extract_resident(ctx, opt, stats)
 
 
 def extract_resident(ctx: Context, opt: ExtractOptions, stats: dict | None = None, fetch: bool = True):
     o = L.ExtractOpts(_mask(opt.strategies), opt.tile_size, opt.refine_iterations, opt.weld_eps, opt.min_area,
-                      opt.view_begin, opt.view_end, int(opt.profile))
+                      opt.view_begin, opt.view_end, int(opt.profile), int(opt.compute_residuals))
     st = L.ExtractStats()
     ctx.check(ctx.lib.sof_extract(ctx.h, ctypes.byref(o), ctypes.byref(st)))
     if stats is not None:
         stats.update(st.as_dict())
     if not fetch:
         return None
-    return Mesh(ctx.result(L.R_MESH_VERTS, np.float64, 3), ctx.result(L.R_MESH_TRIS, np.int32, 3))
+    res = ctx.result(L.R_MESH_RESIDUALS, np.float64, 1) if opt.compute_residuals else np.zeros(0)
+    return Mesh(ctx.result(L.R_MESH_VERTS, np.float64, 3), ctx.result(L.R_MESH_TRIS, np.int32, 3), res)
 
 
 def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile_size: int = 16,

@@ -58,6 +58,8 @@ const char* sof_last_error(const sof_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 int64_t sof_kernel_launches(const sof_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int64_t sof_scene_size(const sof_ctx* ctx) { return ctx && ctx->has_scene ? ctx->n : -1; }
+
 int sof_ctx_create(int device, sof_ctx** out) {
   if (!out) return SOF_E_INVALID;
   *out = nullptr;
@@ -480,6 +482,28 @@ int sof_assemble(sof_ctx* c, int64_t nverts, const double* verts, int64_t ntris,
   });
 }
 
+int sof_assemble_residuals(sof_ctx* c, int64_t nverts, const double* verts, const double* residuals,
+                           int64_t ntris, const int32_t* tris, double weld_eps, double min_area, int64_t* out_verts,
+                           int64_t* out_tris) {
+  if (!c) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (nverts < 0 || ntris < 0 || (nverts && !verts) || (ntris && !tris))
+      throw InvalidArg("invalid mesh arrays");
+    for (int64_t i = 0; i < 3 * ntris; ++i)
+      if (tris[i] < 0 || tris[i] >= nverts) throw InvalidArg("triangle index out of range");
+    if (!(weld_eps > 0.0)) throw InvalidArg("weld_eps must be positive");
+    DBuf<double> dv, dr;
+    DBuf<int32_t> dt;
+    upload(c, dv, verts, 3 * nverts);
+    upload(c, dt, tris, 3 * ntris);
+    if (residuals) upload(c, dr, residuals, nverts);
+    assemble(c, nverts, dv.p, ntris, dt.p, weld_eps, min_area, residuals ? dr.p : nullptr);
+    sync(c);
+    if (out_verts) *out_verts = c->mesh_nv;
+    if (out_tris) *out_tris = c->mesh_nt;
+  });
+}
+
 int sof_set_eval_path(sof_ctx* c, int path) {
   if (!c || path < 0 || path > 1) return SOF_E_INVALID;
   if (c->eval_path != path) {
@@ -505,6 +529,7 @@ void sof_extract_opts_default(sof_extract_opts* o) {
   o->view_begin = -1;
   o->view_end = -1;
   o->profile = 0;
+  o->compute_residuals = 0;
 }
 
 int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* stats) {
@@ -570,7 +595,8 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
              o.tile_size, v0, v1, cr);
       SOF_CUDA(cudaEventRecord(e[3], c->stream));
       mark("refine");
-      assemble(c, c->n_edges, c->r_everts.p, c->n_march_tris, c->r_tris.p, o.weld_eps, o.min_area);
+      const double* res = o.compute_residuals ? level_set_residuals(c, o, v0, v1) : nullptr;
+      assemble(c, c->n_edges, c->r_everts.p, c->n_march_tris, c->r_tris.p, o.weld_eps, o.min_area, res);
     }
     SOF_CUDA(cudaEventRecord(e[4], c->stream));
     SOF_CUDA(cudaEventSynchronize(e[4]));
@@ -630,6 +656,8 @@ int64_t sof_result_count(const sof_ctx* c, int kind) {
     case SOF_R_TILE_ENTRIES: return c->bind_entries;
     case SOF_R_SEEDS: return c->n_seeds < 0 ? -1 : 3 * c->n_seeds;
     case SOF_R_SEED_PROVENANCE: return c->n_seeds;
+    case SOF_R_MESH_RESIDUALS: return c->mesh_nres;
+    case SOF_R_TETS: return int64_t(c->delaunay_tets.size());
     default: return -1;
   }
 }
@@ -652,6 +680,8 @@ int sof_copy_result(sof_ctx* c, int kind, void* dst) {
       case SOF_R_TILE_ENTRIES: download(c, (int32_t*)dst, c->eval_in.p, cnt); break;
       case SOF_R_SEEDS: download(c, (double*)dst, c->seeds.p, cnt); break;
       case SOF_R_SEED_PROVENANCE: download(c, (uint8_t*)dst, c->seed_prov.p, cnt); break;
+      case SOF_R_MESH_RESIDUALS: download(c, (double*)dst, c->m_res.p, cnt); break;
+      case SOF_R_TETS: std::memcpy(dst, c->delaunay_tets.data(), sizeof(int32_t) * cnt); break;
     }
     sync(c);
   });

@@ -336,7 +336,13 @@ void extract_sharded(sof_ctx* c, const sof_extract_opts& o, int vb, int ve, uint
     refine_final(c, ne, c->r_everts.p);
   }
   SOF_CUDA(cudaEventRecord(ev[3], st));
-  assemble(c, c->n_edges, c->r_everts.p, c->n_march_tris, c->r_tris.p, o.weld_eps, o.min_area);
+  const double* res = nullptr;
+  if (o.compute_residuals) {  // value_at = min over views: this rank's views, MIN-reduced
+    double* val = level_set_values(c, o, v0, v1);
+    comm.allreduce(val, c->n_edges, kF64, kMin, st);
+    res = residuals_from_values(c, val);
+  }
+  assemble(c, c->n_edges, c->r_everts.p, c->n_march_tris, c->r_tris.p, o.weld_eps, o.min_area, res);
 }
 
 }  // namespace sofk

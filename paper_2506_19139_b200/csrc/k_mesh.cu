@@ -540,6 +540,13 @@ __global__ void k_weld_out(int64_t n, const int32_t* __restrict__ is_first,
   for (int k = 0; k < 3; ++k) out[3 * nid[i] + k] = v[3 * i + k];
 }
 
+// the residual of the first appearance of each welded vertex (mesh.hpp:63-67)
+__global__ void k_weld_res(int64_t n, const int32_t* __restrict__ is_first, const int32_t* __restrict__ nid,
+                           const double* __restrict__ r, double* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n && is_first[i]) out[nid[i]] = r[i];
+}
+
 // remap + drop repeated ids / area <= min_area on the welded positions (mesh.hpp:70-77)
 __global__ void k_weld_tris(int64_t nt, const int32_t* __restrict__ tris,
                             const int32_t* __restrict__ first_of, const int32_t* __restrict__ nid,
@@ -607,8 +614,9 @@ int64_t dedup_first(sof_ctx* c, int64_t n, const double* v, double inv) {
 }
 
 void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t* tris,
-              double weld_eps, double min_area) {
+              double weld_eps, double min_area, const double* residuals) {
   c->mesh_nv = c->mesh_nt = 0;
+  c->mesh_nres = residuals ? 0 : -1;
   c->m_verts.ensure(3);
   c->m_tris.ensure(3);
   if (n == 0) return;
@@ -619,6 +627,12 @@ void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t*
   k_weld_out<<<grid_for(n, 256), 256, 0, c->stream>>>(n, is_first.p, nid.p, v, c->m_verts.p);
   SOF_LAUNCHED(c);
   c->mesh_nv = nout;
+  if (residuals) {  // out.residuals.push_back((*residuals)[i]) on first appearance (mesh.hpp:66)
+    c->m_res.ensure(std::max<int64_t>(nout, 1));
+    k_weld_res<<<grid_for(n, 256), 256, 0, c->stream>>>(n, is_first.p, nid.p, residuals, c->m_res.p);
+    SOF_LAUNCHED(c);
+    c->mesh_nres = nout;
+  }
   if (nt == 0) return;
   DBuf<int32_t>&rt = s.rt, &keep = s.keep, &pos = s.pos;
   rt.ensure(3 * nt);
@@ -633,6 +647,39 @@ void assemble(sof_ctx* c, int64_t n, const double* v, int64_t nt, const int32_t*
   k_compact_tris<<<grid_for(nt, 256), 256, 0, c->stream>>>(nt, keep.p, pos.p, rt.p, c->m_tris.p);
   SOF_LAUNCHED(c);
   c->mesh_nt = ntout;
+}
+
+// ---- level_set_residuals (marching_tets.hpp:117-123) ------------------------------------------
+
+__global__ void k_abs_minus_half(int64_t n, const double* __restrict__ v, double* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = fabs(v[i] - 0.5);  // std::abs(value(x) - 0.5)
+}
+
+// value_at (field_eval.hpp:128-136) with EvalStrategies::naive() — the `exact` evaluator of
+// extract.hpp:66-67 — at the refined edge vertices, over views [v0, v1).
+double* level_set_values(sof_ctx* c, const sof_extract_opts& o, int v0, int v1) {
+  const int64_t ne = c->n_edges;
+  c->res_in.ensure(std::max<int64_t>(2 * ne, 2));
+  fill_f64(c, c->res_in.p, ne, 1.0);
+  if (ne > 0)
+    eval_views(c, v0, v1, ne, c->r_everts.p, /*EvalStrategies::naive()*/ 0, o.tile_size, false, kModeValue, c->res_in.p, nullptr,
+               nullptr, nullptr, nullptr, nullptr);
+  return c->res_in.p;
+}
+
+double* residuals_from_values(sof_ctx* c, const double* values) {
+  const int64_t ne = c->n_edges;
+  double* out = c->res_in.p + ne;
+  if (ne > 0) {
+    k_abs_minus_half<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, values, out);
+    SOF_LAUNCHED(c);
+  }
+  return out;
+}
+
+double* level_set_residuals(sof_ctx* c, const sof_extract_opts& o, int v0, int v1) {
+  return residuals_from_values(c, level_set_values(c, o, v0, v1));
 }
 
 // ---- seed points (seed_points.hpp:41-87) --------------------------------------------------------

@@ -305,6 +305,9 @@ struct sof_ctx {
 
   // mesher results
   int64_t n_edges = -1, n_march_tris = -1, mesh_nv = -1, mesh_nt = -1, grid_n = -1;
+  int64_t mesh_nres = -1;                // residuals of the last weld (-1: none)
+  std::vector<int32_t> delaunay_tets;    // sof_tetrahedralize result (host, 4 per tet)
+  sofk::DBuf<double> m_res, res_in;      // welded / pre-weld residuals
   sofk::DBuf<double> grid_opacity;
   sofk::DBuf<int32_t> r_edges, r_tris, m_tris;
   sofk::DBuf<double> r_everts, m_verts;
@@ -365,9 +368,14 @@ void refine_mid(sof_ctx* c, int64_t ne, uint8_t* ext_dev);
 void refine_update(sof_ctx* c, int64_t ne, const uint8_t* ext_dev);
 void refine_final(sof_ctx* c, int64_t ne, double* verts_dev);
 int64_t dedup_first(sof_ctx* c, int64_t n, const double* v, double inv);
+// extract_mesh's residuals (extract.hpp:65-72): naive value_at at the refined vertices over
+// views [v0, v1), then |value - 0.5|; pointers into c->res_in
+double* level_set_values(sof_ctx* c, const sof_extract_opts& o, int v0, int v1);
+double* residuals_from_values(sof_ctx* c, const double* values);
+double* level_set_residuals(sof_ctx* c, const sof_extract_opts& o, int v0, int v1);
 void seed_points(sof_ctx* c, int variant, int cutoff, double filter_scale);
 void assemble(sof_ctx* c, int64_t nverts, const double* verts_dev, int64_t ntris,
-              const int32_t* tris_dev, double weld_eps, double min_area);
+              const int32_t* tris_dev, double weld_eps, double min_area, const double* residuals_dev = nullptr);
 
 // ---- k_comm.cu ----------------------------------------------------------------------------
 void comm_destroy(sof_ctx* c);

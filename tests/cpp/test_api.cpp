@@ -376,3 +376,91 @@ TEST(L1Rgb, MeanAbsoluteError) {
   Grid2D<Vec3> b(2, 1, Vec3(0.25, 0.5, 0.5));
   EXPECT_NEAR(l1_rgb_loss(a, b), 0.25 * 2 / 6.0, 1e-12);
 }
+
+TEST(AssembleMesh, ResidualPassthrough) {
+  // mesh.hpp:66: a welded vertex keeps the residual of its first appearance
+  const std::vector<Vec3> verts{Vec3(0, 0, 0), Vec3(1, 0, 0), Vec3(0, 1, 0), Vec3(1 + 1e-9, 0, 0)};
+  const std::vector<std::array<int, 3>> tris{{0, 1, 2}, {0, 3, 2}};
+  const std::vector<double> res{0.1, 0.2, 0.3, 0.4};
+  const auto mesh = assemble_mesh(verts, tris, &res);
+  ASSERT_EQ(mesh.vertices.size(), 3u);
+  ASSERT_EQ(mesh.residuals.size(), 3u);
+  EXPECT_EQ(mesh.residuals[0], 0.1);
+  EXPECT_EQ(mesh.residuals[1], 0.2);
+  EXPECT_EQ(mesh.residuals[2], 0.3);
+  const std::vector<double> bad{0.1};
+  EXPECT_THROW(assemble_mesh(verts, tris, &bad), std::invalid_argument);
+}
+
+TEST(Delaunay, ErrorsLikeTheReference) {
+  EXPECT_THROW(delaunay_tetrahedralize({Vec3(0, 0, 0), Vec3(1, 0, 0), Vec3(0, 1, 0)}), std::invalid_argument);
+  EXPECT_THROW(delaunay_tetrahedralize({Vec3(0, 0, 0), Vec3(1, 0, 0), Vec3(0, 1, 0), Vec3(1, 1, 0)}),
+               std::invalid_argument);
+  const TetGrid g = delaunay_tetrahedralize({Vec3(0, 0, 0), Vec3(1, 0, 0), Vec3(0, 1, 0), Vec3(0, 0, 1)});
+  ASSERT_EQ(g.tetrahedra.size(), 1u);
+}
+
+TEST(ExtractMesh, ReferenceSignatureWithResiduals) {
+  // extract.hpp:35-86: seeds -> Delaunay -> label -> march -> refine -> residuals -> weld
+  const auto scene = random_scene(57, 25);
+  std::vector<Camera> cams;
+  for (int i = 0; i < 4; ++i) {
+    const double a = 2.0 * M_PI * i / 4;
+    cams.push_back(look_at(Vec3(4 * std::cos(a), 4 * std::sin(a), 0.5), Vec3::Zero(), Vec3(0, 0, 1), 60.0, 64));
+  }
+  const ViewSet views = ViewSet::build(scene, cams);
+  ExtractOptions opt;
+  opt.compute_residuals = true;
+  ExtractStats st;
+  const Mesh m = extract_mesh(scene, views, opt, &st);
+  ASSERT_GT(m.triangles.size(), 0u);
+  ASSERT_EQ(m.residuals.size(), m.vertices.size());
+  for (double r : m.residuals) EXPECT_LT(r, 0.5);
+  EXPECT_GT(st.seed_points, 0u);
+  EXPECT_GT(st.tetrahedra, 0u);
+  EXPECT_GT(st.crossing_edges, 0u);
+  EXPECT_GT(st.counters.pairs, 0u);
+  // the same mesh through the explicit producer + the tetra-input overload
+  const SeedPointSet seeds = build_seed_points(views, opt.bounding, opt.cutoff, opt.filter_scale);
+  ASSERT_EQ(seeds.points.size(), st.seed_points);
+  const TetGrid grid = delaunay_tetrahedralize(seeds.points);
+  ASSERT_EQ(grid.tetrahedra.size(), st.tetrahedra);
+  const Mesh m2 = extract_mesh(scene, views, grid, opt);
+  ASSERT_EQ(m2.vertices.size(), m.vertices.size());
+  for (size_t i = 0; i < m.vertices.size(); ++i) {
+    EXPECT_EQ(m.vertices[i], m2.vertices[i]);
+    EXPECT_EQ(m.residuals[i], m2.residuals[i]);
+  }
+  EXPECT_THROW(extract_mesh(std::vector<GaussianPrimitive>(3), views, opt), std::invalid_argument);
+}
+
+TEST(BinarySearchRefine, BatchedAddsCountersAndMatchesHostLoop) {
+  const auto scene = random_scene(58, 20);
+  std::vector<Camera> cams;
+  for (int i = 0; i < 3; ++i) {
+    const double a = 2.0 * M_PI * i / 3;
+    cams.push_back(look_at(Vec3(4 * std::cos(a), 4 * std::sin(a), 0.5), Vec3::Zero(), Vec3(0, 0, 1), 60.0, 64));
+  }
+  const ViewSet views = ViewSet::build(scene, cams);
+  TetGrid grid = lattice(8, -1.3, 1.3);
+  const FieldEvaluator eval(scene, views, EvalStrategies::all());
+  eval.label_grid(grid, true);
+  MarchingResult a = marching_tets(grid);
+  ASSERT_GT(a.edges.size(), 0u);
+  MarchingResult b = a;
+  const EvalCounters before = eval.counters();
+  const RefineStats rs = binary_search_refine(a, grid, eval, 8);
+  EXPECT_EQ(rs.bracket_lost, 0u);
+  const EvalCounters after = eval.counters();
+  EXPECT_GT(after.pairs, before.pairs);
+  EXPECT_GT(after.point_view_evals, before.point_view_evals);
+  const FieldEvaluator host(scene, views, EvalStrategies::all());
+  binary_search_refine(b, grid, [&](const Vec3& x) { return host.classify_point(x); }, 8);
+  for (size_t i = 0; i < a.vertices.size(); ++i) EXPECT_EQ(a.vertices[i], b.vertices[i]);
+  // the batched residuals equal the host loop over value_at
+  const FieldEvaluator exact(scene, views, EvalStrategies::naive());
+  const auto r1 = level_set_residuals(a, exact);
+  const auto r2 = level_set_residuals(a, [&](const Vec3& x) { return exact.value_at(x); });
+  ASSERT_EQ(r1.size(), a.vertices.size());
+  for (size_t i = 0; i < r1.size(); ++i) EXPECT_EQ(r1[i], r2[i]);
+}

@@ -88,3 +88,35 @@ def test_local_ranks_match_reference(case, world, mask):
     assert all(s["label_pairs"] < int(want["counters"][0]) for s in stats)
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_local_ranks_residuals(case, world):
+    """compute_residuals on the sharded step: the per-view |T-0.5| values are MIN-reduced
+    across the view shards, then every rank welds the same residuals as one context."""
+    scene, cams, verts, tets, rc = case
+    opt = sof.ExtractOptions(compute_residuals=True)
+    one = make_ctx(scene, cams, verts, tets)
+    want = sof.extract_resident(one, opt, {})
+    assert len(want.residuals) == len(want.vertices) > 0
+    ctxs = [make_ctx(scene, cams, verts, tets) for _ in range(world)]
+    sof.Context.comm_init_local(ctxs)
+    meshes, errors = [None] * world, []
+
+    def run(r):
+        try:
+            meshes[r] = sof.extract_resident(ctxs[r], opt, {})
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    assert not errors, errors
+    for m in meshes:
+        np.testing.assert_array_equal(bits(m.vertices), bits(want.vertices))
+        np.testing.assert_array_equal(bits(m.residuals), bits(want.residuals))
+    for c in ctxs + [one]:
+        c.close()

@@ -292,3 +292,60 @@ def test_bisection_cache_truncated_lists(ref, dist):
     # a second extract on the same context (caches rebuilt) still matches
     mesh2 = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets), sof.ExtractOptions(), {})
     np.testing.assert_array_equal(mesh2.triangles, want["triangles"])
+
+
+@pytest.mark.parametrize("mask", [31, 23])
+def test_extract_residuals(ref, lattice_case, mask):
+    """ExtractOptions::compute_residuals (extract.hpp:65-72): level_set_residuals with the
+    naive exact evaluator at the refined vertices, carried through the weld (mesh.hpp:66);
+    every residual bit-identical to the reference's."""
+    from oracle.refpy import NAIVE
+    scene, cams, rc, views, verts, tets = lattice_case
+    want = rc.extract_tetgrid(verts, tets, strategies=mask, iterations=8)
+    exact = rc.evaluator(NAIVE)
+    res = np.abs(exact.value_at(want["refined"]) - 0.5)
+    wmesh = ref.assemble(want["refined"], want["march_triangles"], res)
+    mesh = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets),
+                            sof.ExtractOptions(strategies=sof.EvalStrategies.from_mask(mask), compute_residuals=True))
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(wmesh["vertices"]))
+    np.testing.assert_array_equal(mesh.triangles, wmesh["triangles"])
+    assert len(mesh.residuals) == len(mesh.vertices) > 0
+    np.testing.assert_array_equal(bits(mesh.residuals), bits(wmesh["residuals"]))
+    # the stand-alone weld with a residual passthrough
+    m2 = sof.assemble_mesh(want["refined"], want["march_triangles"], residuals=res, ctx=views.ctx)
+    np.testing.assert_array_equal(bits(m2.residuals), bits(wmesh["residuals"]))
+
+
+@pytest.mark.parametrize("seed, count", [(55, 15), (56, 30)])
+def test_extract_mesh_reference_signature(ref, seed, count, tmp_path):
+    """extract_mesh(gaussians, views, opt) (extract.hpp:35-86) with its own producer:
+    build_seed_points on the device, delaunay_tetrahedralize on the host (sof_tetrahedralize,
+    the reference's Bowyer-Watson tet list exactly), then the device pipeline; the PLY
+    bytes equal the reference's extract_mesh."""
+    scene = ref.random_scene(seed, count, 1.0)
+    cams = ref.orbit_cameras(3, 4.0, 1.8, 64)
+    rc = ref.context(scene, cams)
+    grid_ref = rc.seed_delaunay(bounding=0, cutoff=1)
+    full = rc.extract_full(ALL)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    seeds = sof.build_seed_points(views.ctx, sof.SEED_STP, sof.SEED_CUT_DEAD)
+    grid = sof.delaunay_tetrahedralize(seeds.points, views.ctx)
+    np.testing.assert_array_equal(bits(grid.vertices), bits(grid_ref["vertices"]))
+    np.testing.assert_array_equal(grid.tetrahedra, grid_ref["tets"])
+    st = {}
+    mesh = sof.extract_mesh(scene, views, opt=sof.ExtractOptions(), stats=st)
+    assert st["tetrahedra"] == len(grid_ref["tets"])
+    np.testing.assert_array_equal(bits(mesh.vertices), bits(full["vertices"]))
+    np.testing.assert_array_equal(mesh.triangles, full["triangles"])
+    p1, p2 = str(tmp_path / "gpu.ply"), str(tmp_path / "ref.ply")
+    sof.write_mesh_ply(mesh, p1)
+    ref.write_mesh_ply(full["vertices"], full["triangles"], p2)
+    assert open(p1, "rb").read() == open(p2, "rb").read()
+
+
+def test_tetrahedralize_errors(ref):
+    ctx = sof.Context(0)
+    with pytest.raises(ValueError, match="need at least 4 points"):
+        sof.delaunay_tetrahedralize(np.zeros((3, 3)), ctx)
+    with pytest.raises(ValueError, match="degenerate"):
+        sof.delaunay_tetrahedralize(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0], [2, 3, 0.0]]), ctx)
