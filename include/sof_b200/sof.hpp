@@ -207,9 +207,21 @@ inline CtxPtr& default_ctx() {
 
 }  // namespace detail
 
+// caches[v] of the reference's ViewSet (std::vector<PrecomputedGaussian>, opacity_field.hpp:
+// 23-24), here a handle of view v's records resident on the device of `ctx`.
+struct ViewCache {
+  detail::CtxPtr ctx;
+  int view = 0;
+  size_t n = 0;
+  Camera camera;
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
+};
+
 // opacity_field.hpp:21-35, lazily device-resident.
 struct ViewSet {
   std::vector<Camera> cameras;
+  std::vector<ViewCache> caches;
   detail::CtxPtr ctx;
   double filter_scale = 0.0;
 
@@ -255,9 +267,17 @@ struct ViewSet {
     }
     detail::check(vs.ctx.get(), sof_set_views(vs.ctx.get(), int(v), R.data(), t.data(), intr.data(),
                                               wh.data(), nf.data()));
+    for (size_t k = 0; k < v; ++k) vs.caches.push_back(ViewCache{vs.ctx, int(k), n, vs.cameras[k]});
     return vs;
   }
 };
+
+// precompute_all (precompute.hpp:83-90): the records of `gaussians` for one camera, on
+// the device (a one-view ViewSet's cache).
+inline ViewCache precompute_all(const std::vector<GaussianPrimitive>& gaussians, const Camera& cam,
+                                double filter_scale = 0.0) {
+  return ViewSet::build(gaussians, {cam}, filter_scale).caches.front();
+}
 
 // field_eval.hpp:39-198 on the GPU. The views' device context is shared.
 class FieldEvaluator {
@@ -529,17 +549,36 @@ struct DepthMap {
   Grid2D<double> opacity;
 };
 
-// render_depth_map (render.hpp:26-51) for view `view` of the ViewSet.
-inline DepthMap render_depth_map(const ViewSet& views, size_t view, DepthMode mode) {
-  const Camera& cam = views.cameras.at(view);
+namespace detail {
+inline bool same_camera(const Camera& a, const Camera& b) {
+  return a.rotation == b.rotation && a.translation == b.translation && a.fx == b.fx && a.fy == b.fy &&
+         a.cx == b.cx && a.cy == b.cy && a.width == b.width && a.height == b.height && a.near == b.near &&
+         a.far == b.far;
+}
+}  // namespace detail
+
+// render_depth_map (render.hpp:26-51) with the reference's arguments: `cache` must be the
+// records of `cam` (a ViewSet's caches[v] with cameras[v], or precompute_all(g, cam)); the
+// pool argument is accepted and ignored (the GPU grid replaces it).
+inline DepthMap render_depth_map(const ViewCache& cache, const Camera& cam, DepthMode mode,
+                                 const void* /*pool*/ = nullptr) {
   DepthMap out;
   out.depth = Grid2D<double>(cam.width, cam.height, kNoSurface);
   out.opacity = Grid2D<double>(cam.width, cam.height, 0.0);
-  detail::check(views.ctx.get(),
-                sof_render_view(views.ctx.get(), int(view), mode == DepthMode::kExact ? SOF_DEPTH_EXACT : SOF_DEPTH_MEDIAN,
-                                kDefaultTileSize, out.depth.data.data(), out.opacity.data.data(), nullptr,
-                                nullptr, nullptr));
+  if (!cache.ctx || cache.n == 0) return out;  // no Gaussians: no surface anywhere
+  if (!detail::same_camera(cam, cache.camera))
+    throw std::invalid_argument("render_depth_map: cam is not the camera the cache was built for");
+  sof_ctx* c = cache.ctx.get();
+  detail::check(c, sof_set_render_window(c, 0));
+  detail::check(c, sof_render_view(c, cache.view, mode == DepthMode::kExact ? SOF_DEPTH_EXACT : SOF_DEPTH_MEDIAN,
+                                   kDefaultTileSize, out.depth.data.data(), out.opacity.data.data(), nullptr,
+                                   nullptr, nullptr));
   return out;
+}
+
+// render_depth_map for view `view` of the ViewSet.
+inline DepthMap render_depth_map(const ViewSet& views, size_t view, DepthMode mode) {
+  return render_depth_map(views.caches.at(view), views.cameras.at(view), mode);
 }
 
 // camera.hpp:36-39
@@ -547,6 +586,132 @@ struct Ray {
   Vec3 origin = Vec3::Zero();
   Vec3 direction = Vec3(0.0, 0.0, 1.0);  // unit length
 };
+
+// camera.hpp:42-48
+inline Ray ray_through_pixel(const Camera& cam, double px, double py) {
+  Ray r;
+  r.origin = cam.center();
+  const Vec3 d_view((px - cam.cx) / cam.fx, (py - cam.cy) / cam.fy, 1.0);
+  r.direction = (cam.rotation.transpose() * d_view).normalized();
+  return r;
+}
+
+// ---- per-ray compositing (opacity_field.hpp:13-219), on the device -------------------------
+
+// opacity_field.hpp:13-19
+struct RayContribution {
+  int gaussian_index = -1;
+  double t_star = 0.0;
+  double alpha = 0.0;
+  double a = 0.0, b = 0.0, c = 0.0;
+  double opacity = 0.0;
+};
+
+// collect_contributions (opacity_field.hpp:39-61) for a batch of rays: every Gaussian of
+// the cache is tested on the device; each list sorted by (t*, index). As in the reference
+// only the ray direction is read (the records are relative to the camera centre).
+inline std::vector<std::vector<RayContribution>> collect_contributions(const ViewCache& cache,
+                                                                       const std::vector<Ray>& rays) {
+  std::vector<std::vector<RayContribution>> out(rays.size());
+  if (!cache.ctx || cache.n == 0 || rays.empty()) return out;
+  sof_ctx* c = cache.ctx.get();
+  std::vector<double> d(3 * rays.size());
+  for (size_t i = 0; i < rays.size(); ++i)
+    for (int k = 0; k < 3; ++k) d[3 * i + k] = rays[i].direction(k);
+  std::vector<int64_t> off(rays.size() + 1, 0);
+  detail::check(c, sof_collect_contributions(c, cache.view, Index(rays.size()), d.data(), off.data()));
+  const std::vector<int32_t> idx = detail::result<int32_t>(c, SOF_R_CONTRIB_INDEX);
+  const std::vector<double> val = detail::result<double>(c, SOF_R_CONTRIB_VALUES);
+  for (size_t i = 0; i < rays.size(); ++i)
+    for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+      RayContribution r;
+      r.gaussian_index = idx[size_t(k)];
+      r.t_star = val[6 * size_t(k)];
+      r.alpha = val[6 * size_t(k) + 1];
+      r.a = val[6 * size_t(k) + 2];
+      r.b = val[6 * size_t(k) + 3];
+      r.c = val[6 * size_t(k) + 4];
+      r.opacity = val[6 * size_t(k) + 5];
+      out[i].push_back(r);
+    }
+  return out;
+}
+
+inline std::vector<RayContribution> collect_contributions(const ViewCache& cache, const Ray& ray) {
+  return collect_contributions(cache, std::vector<Ray>{ray}).front();
+}
+
+// windowed_resort (opacity_field.hpp:66-91) on the device: the reference's element order,
+// ties included.
+inline std::vector<RayContribution> windowed_resort(std::vector<RayContribution> in, size_t window) {
+  if (in.size() < 2) return in;
+  sof_ctx* c = detail::default_ctx().get();
+  std::vector<double> t(in.size());
+  for (size_t i = 0; i < in.size(); ++i) t[i] = in[i].t_star;
+  const int64_t off[2] = {0, Index(in.size())};
+  std::vector<int64_t> order(in.size());
+  const Index w = window >= in.size() ? Index(in.size()) : Index(window);
+  detail::check(c, sof_windowed_resort(c, 1, off, t.data(), w, order.data()));
+  std::vector<RayContribution> out(in.size());
+  for (size_t i = 0; i < in.size(); ++i) out[i] = in[size_t(order[i])];
+  return out;
+}
+
+// opacity_field.hpp:192-197
+struct PixelOutputs {
+  Vec3 color = Vec3::Zero();
+  double depth = kNoSurface;
+  double accumulated_opacity = 0.0;  // O_N at the depth
+  double transmittance_final = 1.0;
+};
+
+// render_pixel (opacity_field.hpp:201-219) of a batch of lists on the device; the colours
+// are those of gaussians[gaussian_index] (only the referenced ones are uploaded).
+inline std::vector<PixelOutputs> render_pixels(const std::vector<std::vector<RayContribution>>& lists,
+                                               const std::vector<GaussianPrimitive>& gaussians,
+                                               DepthMode mode = DepthMode::kExact) {
+  std::vector<PixelOutputs> out(lists.size());
+  if (lists.empty()) return out;
+  std::vector<int64_t> off(1, 0);
+  std::vector<int32_t> idx;
+  std::vector<double> val, dc;
+  std::vector<int32_t> remap(gaussians.size(), -1);
+  for (const auto& l : lists) {
+    for (const RayContribution& r : l) {
+      if (r.gaussian_index < 0 || size_t(r.gaussian_index) >= gaussians.size())
+        throw std::out_of_range("render_pixel: gaussian_index out of range");
+      int32_t& m = remap[size_t(r.gaussian_index)];
+      if (m < 0) {
+        m = int32_t(dc.size() / 3);
+        for (int k = 0; k < 3; ++k) dc.push_back(gaussians[size_t(r.gaussian_index)].dc_color(k));
+      }
+      idx.push_back(m);
+      for (double v : {r.t_star, r.alpha, r.a, r.b, r.c, r.opacity}) val.push_back(v);
+    }
+    off.push_back(Index(idx.size()));
+  }
+  sof_ctx* c = detail::default_ctx().get();
+  const size_t nl = lists.size();
+  std::vector<double> col(3 * nl), depth(nl), acc(nl), tf(nl);
+  const double dummy[3] = {0.0, 0.0, 0.0};
+  detail::check(c, sof_render_pixel(c, Index(nl), off.data(), idx.data(), val.data(), Index(dc.size() / 3),
+                                    dc.empty() ? dummy : dc.data(),
+                                    mode == DepthMode::kExact ? SOF_DEPTH_EXACT : SOF_DEPTH_MEDIAN, col.data(),
+                                    depth.data(), acc.data(), tf.data()));
+  for (size_t i = 0; i < nl; ++i) {
+    out[i].color = Vec3(col[3 * i], col[3 * i + 1], col[3 * i + 2]);
+    out[i].depth = depth[i];
+    out[i].accumulated_opacity = acc[i];
+    out[i].transmittance_final = tf[i];
+  }
+  return out;
+}
+
+inline PixelOutputs render_pixel(const std::vector<RayContribution>& contribs,
+                                 const std::vector<GaussianPrimitive>& gaussians,
+                                 DepthMode mode = DepthMode::kExact) {
+  return render_pixels({contribs}, gaussians, mode).front();
+}
 
 // render.hpp:53-56
 struct NormalMap {
@@ -1136,14 +1301,6 @@ struct LossWeights {
   double lambda_dist(bool scene_bounded) const { return scene_bounded ? lambda_dist_bounded : lambda_dist_unbounded; }
 };
 
-// opacity_field.hpp:13-19
-struct RayContribution {
-  int gaussian_index = -1;
-  double t_star = 0.0;
-  double alpha = 0.0;
-  double a = 0.0, b = 0.0, c = 0.0;
-  double opacity = 0.0;
-};
 
 struct DistortionSample {  // losses.hpp:44-47
   double alpha = 0.0;

@@ -70,7 +70,9 @@ enum {
   SOF_R_SEEDS = 9,         /* f64[3S]    SeedPointSet::points (seed_points.hpp:24-27) */
   SOF_R_SEED_PROVENANCE = 10, /* uint8[S] SeedPointSet::provenance: 0 centre, 1 bound corner */
   SOF_R_MESH_RESIDUALS = 11,  /* f64[V] Mesh::residuals (mesh.hpp:16), when computed */
-  SOF_R_TETS = 12             /* int32[4T] the tets of the last sof_tetrahedralize */
+  SOF_R_TETS = 12,            /* int32[4T] the tets of the last sof_tetrahedralize */
+  SOF_R_CONTRIB_INDEX = 13,   /* int32[C] RayContribution::gaussian_index of sof_collect_contributions */
+  SOF_R_CONTRIB_VALUES = 14   /* f64[6C] (t_star, alpha, a, b, c, opacity) per contribution */
 };
 
 typedef struct sof_ctx sof_ctx;
@@ -331,6 +333,36 @@ int sof_render_view(sof_ctx* ctx, int view, int depth_mode, int tile_size, doubl
  * of each pixel's collect_contributions list, opacity_field.hpp:39-61). SOF_E_STATE if
  * that view was not the last one rendered. */
 int sof_render_counts(sof_ctx* ctx, int view, uint32_t* counts);
+
+/* Per-pixel resort of sof_render_view. 0 (default): the exact (t*, index) order of
+ * collect_contributions (opacity_field.hpp:39-61). K > 0: the K-slot window of
+ * windowed_resort (opacity_field.hpp:66-91) applied to each pixel's contributions in
+ * arrival order = ascending view-space centre depth (ties by index) -- the streaming
+ * k-buffer approximation; libstdc++'s tie order is reproduced (stl_order.cuh). */
+int sof_set_render_window(sof_ctx* ctx, int64_t window);
+
+/* collect_contributions (opacity_field.hpp:39-61) for n_rays rays of `view` given by
+ * their unit directions dirs[3 n_rays] (the reference reads only ray.direction: the
+ * cache is relative to the camera centre). offsets_out[n_rays + 1] (host) receives the
+ * list offsets; the lists, each sorted by (t*, index), are the results
+ * SOF_R_CONTRIB_INDEX / SOF_R_CONTRIB_VALUES. Every Gaussian is tested (no tiles), on
+ * the device. */
+int sof_collect_contributions(sof_ctx* ctx, int view, int64_t n_rays, const double* dirs, int64_t* offsets_out);
+
+/* windowed_resort (opacity_field.hpp:66-91) of n_lists arrival-ordered lists (host
+ * arrays: offsets[n_lists + 1], t_star[offsets[n_lists]]): order_out[k] is the input
+ * position (into t_star) of the element the reference puts at output slot k, ties
+ * included. One device thread per list. */
+int sof_windowed_resort(sof_ctx* ctx, int64_t n_lists, const int64_t* offsets, const double* t_star,
+                        int64_t window, int64_t* order_out);
+
+/* render_pixel (opacity_field.hpp:201-219) of n_lists given contribution lists (host:
+ * offsets[n_lists + 1], index[C], values[6C] as SOF_R_CONTRIB_VALUES) with the DC colours
+ * dc[3 n_gauss] of `gaussians` (NULL: the resident scene's): color[3 n_lists], depth,
+ * accumulated_opacity, t_final [n_lists] (each nullable). One device thread per list. */
+int sof_render_pixel(sof_ctx* ctx, int64_t n_lists, const int64_t* offsets, const int32_t* index,
+                     const double* values, int64_t n_gauss, const double* dc, int depth_mode, double* color,
+                     double* depth, double* acc_opacity, double* t_final);
 
 /* Scratch budget (bytes) of one render band: a frame whose per-pixel contribution slices
  * (16 B per candidate) exceed it is rendered in bands of tiles. 0 restores the default

@@ -702,6 +702,71 @@ void sofref_render_pixels(const sofref_ctx* c, int view, int exact, long n, cons
   }
 }
 
+/// The K-window resort render mode: per pixel collect_contributions, re-ordered into
+/// arrival order by view-space centre depth (ties by index; a strict total order, so any
+/// sort gives it), then windowed_resort(window) (opacity_field.hpp:66-91) and render_pixel.
+void sofref_render_pixels_windowed(const sofref_ctx* c, int view, int exact, long window, long n,
+                                   const int32_t* pix, double* color, double* depth, double* acc,
+                                   double* tfinal, int32_t* ncontrib) {
+  const Camera& cam = c->views.cameras[view];
+  const auto& cache = c->views.caches[view];
+  std::vector<double> zc(c->gaussians.size());
+  for (size_t i = 0; i < zc.size(); ++i) zc[i] = cam.to_view(c->gaussians[i].position).z();
+  for (long i = 0; i < n; ++i) {
+    const Ray ray = ray_through_pixel(cam, pix[2 * i] + 0.5, pix[2 * i + 1] + 0.5);
+    auto contribs = collect_contributions(cache, ray);
+    std::sort(contribs.begin(), contribs.end(), [&](const RayContribution& l, const RayContribution& r) {
+      const double a = zc[size_t(l.gaussian_index)], b = zc[size_t(r.gaussian_index)];
+      return a < b || (a == b && l.gaussian_index < r.gaussian_index);
+    });
+    contribs = windowed_resort(std::move(contribs), size_t(window));
+    const PixelOutputs p =
+        render_pixel(contribs, c->gaussians, exact ? DepthMode::kExact : DepthMode::kMedian);
+    for (int k = 0; k < 3; ++k) color[3 * i + k] = p.color(k);
+    depth[i] = p.depth;
+    acc[i] = p.accumulated_opacity;
+    tfinal[i] = p.transmittance_final;
+    ncontrib[i] = int32_t(contribs.size());
+  }
+}
+
+/// windowed_resort (opacity_field.hpp:66-91) of one list given (t*, index) in arrival order;
+/// out_idx[n] = the gaussian_index sequence it returns.
+void sofref_windowed_resort(long n, const double* t, const int32_t* idx, long window, int32_t* out_idx) {
+  std::vector<RayContribution> in(size_t(std::max(n, 0L)));
+  for (long i = 0; i < n; ++i) {
+    in[size_t(i)].t_star = t[i];
+    in[size_t(i)].gaussian_index = idx[i];
+  }
+  const auto out = windowed_resort(std::move(in), size_t(window));
+  for (size_t i = 0; i < out.size(); ++i) out_idx[i] = out[i].gaussian_index;
+}
+
+/// render_pixel (opacity_field.hpp:201-219) of given contribution lists:
+/// vals = 6 doubles per contribution (t*, alpha, a, b, c, opacity).
+void sofref_render_pixel_lists(const sofref_ctx* c, int exact, long nl, const int64_t* off, const int32_t* idx,
+                               const double* vals, double* color, double* depth, double* acc, double* tfinal) {
+  for (long l = 0; l < nl; ++l) {
+    std::vector<RayContribution> rc;
+    for (int64_t k = off[l]; k < off[l + 1]; ++k) {
+      RayContribution r;
+      r.gaussian_index = idx[k];
+      r.t_star = vals[6 * k];
+      r.alpha = vals[6 * k + 1];
+      r.a = vals[6 * k + 2];
+      r.b = vals[6 * k + 3];
+      r.c = vals[6 * k + 4];
+      r.opacity = vals[6 * k + 5];
+      rc.push_back(r);
+    }
+    const PixelOutputs p = render_pixel(rc, c->gaussians, exact ? DepthMode::kExact : DepthMode::kMedian);
+    for (int k = 0; k < 3; ++k) color[3 * l + k] = p.color(k);
+    depth[l] = p.depth;
+    acc[l] = p.accumulated_opacity;
+    tfinal[l] = p.transmittance_final;
+  }
+}
+
 /// normal_from_depth (render.hpp:60-88) of a [h*w] depth map for view's camera.
 /// out: normal[3*h*w] (zero where invalid), valid[h*w]
 void sofref_normal_from_depth(const sofref_ctx* c, int view, const double* depth, double* normal,

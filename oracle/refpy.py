@@ -165,12 +165,24 @@ class RefLib:
         L.sofref_write_float_map.restype = _I
         L.sofref_collect_contributions.restype = _P
         L.sofref_collect_contributions.argtypes = [_P, _I, _I, _I]
+        L.sofref_render_pixels_windowed.argtypes = [_P, _I, _I, _L, _L, _P, _P, _P, _P, _P, _P]
+        L.sofref_windowed_resort.argtypes = [_L, _P, _P, _L, _P]
+        L.sofref_render_pixel_lists.argtypes = [_P, _I, _L, _P, _P, _P, _P, _P, _P, _P]
 
     # ---- fixtures ----
     def write_float_map(self, width: int, height: int, channels: int, data, path: str) -> int:
         """write_float_map (io_maps.hpp:30-38); returns 1 when the reference throws."""
         data = np.ascontiguousarray(data, np.float32)
         return self.lib.sofref_write_float_map(width, height, channels, _ptr(data), path.encode())
+
+    def windowed_resort(self, t_star, index, window: int) -> np.ndarray:
+        """windowed_resort (opacity_field.hpp:66-91) of one arrival-ordered list; returns
+        the gaussian_index sequence."""
+        t = np.ascontiguousarray(t_star, np.float64)
+        i = np.ascontiguousarray(index, np.int32)
+        out = np.empty(len(t), np.int32)
+        self.lib.sofref_windowed_resort(len(t), _ptr(t), _ptr(i), int(window), _ptr(out))
+        return out
 
     def random_scene(self, seed: int, count: int, extent: float = 1.0) -> Scene:
         s = Scene.empty(count)
@@ -456,6 +468,29 @@ class RefContext:
             cuts = np.linspace(0, n, 4 * threads + 1).astype(int)
             with ThreadPoolExecutor(threads) as ex:
                 list(ex.map(lambda k: run(cuts[k], cuts[k + 1]), range(len(cuts) - 1)))
+        return out
+
+    def render_pixels_windowed(self, view: int, pix, window: int, exact: bool = True) -> dict:
+        """collect_contributions, arrival order by view-space centre depth (ties: index),
+        windowed_resort(window), render_pixel -- per pixel."""
+        pix = np.ascontiguousarray(pix, np.int32)
+        n = len(pix)
+        out = {"color": np.empty((n, 3)), "depth": np.empty(n), "acc": np.empty(n), "tfinal": np.empty(n),
+               "ncontrib": np.empty(n, np.int32)}
+        self.ref.lib.sofref_render_pixels_windowed(self.h, view, int(exact), int(window), n, _ptr(pix),
+                                                   *(_ptr(out[k]) for k in ("color", "depth", "acc", "tfinal",
+                                                                            "ncontrib")))
+        return out
+
+    def render_pixel_lists(self, off, idx, vals, exact: bool = True) -> dict:
+        """render_pixel (opacity_field.hpp:201-219) of given contribution lists."""
+        off = np.ascontiguousarray(off, np.int64)
+        idx = np.ascontiguousarray(idx, np.int32)
+        vals = np.ascontiguousarray(vals, np.float64).reshape(-1, 6)
+        nl = len(off) - 1
+        out = {"color": np.empty((nl, 3)), "depth": np.empty(nl), "acc": np.empty(nl), "tfinal": np.empty(nl)}
+        self.ref.lib.sofref_render_pixel_lists(self.h, int(exact), nl, _ptr(off), _ptr(idx), _ptr(vals),
+                                               *(_ptr(out[k]) for k in ("color", "depth", "acc", "tfinal")))
         return out
 
     def collect_contributions(self, view: int, px: int, py: int) -> dict:

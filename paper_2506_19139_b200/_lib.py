@@ -20,6 +20,7 @@ ALL_STRATEGIES, NAIVE = 31, 0
 DEPTH_MEDIAN, DEPTH_EXACT = 0, 1
 R_EDGES, R_EDGE_VERTS, R_TRIANGLES, R_MESH_VERTS, R_MESH_TRIS, R_GRID_OPACITY, R_TILE_OFFSETS, R_TILE_ENTRIES = range(1, 9)
 R_SEEDS, R_SEED_PROVENANCE, R_MESH_RESIDUALS, R_TETS = 9, 10, 11, 12
+R_CONTRIB_INDEX, R_CONTRIB_VALUES = 13, 14
 SEED_STP, SEED_THREE_SIGMA, SEED_STRETCHED_SIGMA = 0, 1, 2
 SEED_CUT_NONE, SEED_CUT_DEAD = 0, 1
 SOF_COMM_ID_BYTES = 128
@@ -54,6 +55,10 @@ _SIGS = {
     "sof_last_error": (ctypes.c_char_p, [_P]),
     "sof_kernel_launches": (_I64, [_P]),
     "sof_scene_size": (_I64, [_P]),
+    "sof_set_render_window": (_I, [_P, _I64]),
+    "sof_collect_contributions": (_I, [_P, _I, _I64, _P, _P]),
+    "sof_windowed_resort": (_I, [_P, _I64, _P, _P, _I64, _P]),
+    "sof_render_pixel": (_I, [_P, _I64, _P, _P, _P, _I64, _P, _I, _P, _P, _P, _P]),
     "sof_ctx_create": (_I, [_I, ctypes.POINTER(_P)]),
     "sof_ctx_destroy": (None, [_P]),
     "sof_set_scene": (_I, [_P, _I64, _P, _P, _P, _P, _P, _D]),

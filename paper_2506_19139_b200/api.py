@@ -470,11 +470,14 @@ def extract_resident(ctx: Context, opt: ExtractOptions, stats: dict | None = Non
 
 
 def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile_size: int = 16,
-                normals: bool = False, counts: bool = False) -> dict:
+                normals: bool = False, counts: bool = False, window: int = 0) -> dict:
     """render_depth_map (render.hpp:26-51) + render_pixel colour / T (opacity_field.hpp:201-219);
     with normals=True also normal_from_depth (render.hpp:60-88) of the depth, computed on
-    the device from the resident depth map."""
+    the device from the resident depth map. window=K > 0 replaces the exact per-pixel
+    (t*, index) order by windowed_resort's K-slot window (opacity_field.hpp:66-91) over
+    the contributions in view-space centre-depth order (sof_set_render_window)."""
     ctx = views.ctx
+    ctx.check(ctx.lib.sof_set_render_window(ctx.h, int(window)))
     w, h = (int(x) for x in ctx.cams.wh[view])
     out = {"depth": np.empty((h, w)), "opacity": np.empty((h, w)), "rgb": np.empty((h, w, 3)),
            "t_final": np.empty((h, w)), "stats": np.zeros(4, np.uint64)}
@@ -487,6 +490,67 @@ def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile
         out["normal"] = np.empty((h, w, 3))
         out["normal_valid"] = np.empty((h, w), np.uint8)
         ctx.check(ctx.lib.sof_render_normals(ctx.h, view, _ptr(out["normal"]), _ptr(out["normal_valid"])))
+    return out
+
+
+def pixel_rays(cams: CameraSet, view: int, pix) -> np.ndarray:
+    """ray_through_pixel(cam, x + 0.5, y + 0.5).direction (camera.hpp:42-48) for integer
+    pixels pix[n, 2] = (x, y), in the reference's operation order (host)."""
+    pix = np.asarray(pix, np.float64).reshape(-1, 2)
+    R = np.asarray(cams.R[view], np.float64).reshape(3, 3)
+    fx, fy, cx, cy = (float(v) for v in cams.intr[view])
+    v0 = ((pix[:, 0] + 0.5) - cx) / fx
+    v1 = ((pix[:, 1] + 0.5) - cy) / fy
+    d = np.stack([(R[0, i] * v0 + R[1, i] * v1) + R[2, i] * 1.0 for i in range(3)], axis=1)
+    sq = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+    nrm = np.sqrt(sq)
+    return np.where(sq[:, None] > 0.0, d / np.where(nrm > 0, nrm, 1.0)[:, None], d)
+
+
+def collect_contributions(views: ViewSet, view: int, directions) -> dict:
+    """collect_contributions (opacity_field.hpp:39-61) for each ray of `view` (unit
+    directions [n, 3]; the origin is the camera centre), on the device over ALL Gaussians.
+    Returns offsets [n + 1] and, per contribution in (t*, index) order per ray, index and
+    t_star / alpha / a / b / c / opacity (values [C, 6] holds the six columns)."""
+    ctx = views.ctx
+    d = _f64(directions, 3)
+    off = np.zeros(len(d) + 1, np.int64)
+    ctx.check(ctx.lib.sof_collect_contributions(ctx.h, int(view), len(d), _ptr(d), _ptr(off)))
+    idx = ctx.result(L.R_CONTRIB_INDEX, np.int32, 1)
+    val = ctx.result(L.R_CONTRIB_VALUES, np.float64, 6).reshape(-1, 6)
+    out = {"offsets": off, "index": idx, "values": val}
+    for k, name in enumerate(("t_star", "alpha", "a", "b", "c", "opacity")):
+        out[name] = val[:, k]
+    return out
+
+
+def windowed_resort(offsets, t_star, window: int, ctx: Context | None = None) -> np.ndarray:
+    """windowed_resort (opacity_field.hpp:66-91) of arrival-ordered lists on the device:
+    returns order[C], the input position of the element at each output slot (ties as
+    libstdc++ orders them)."""
+    ctx = ctx or default_context()
+    off = np.ascontiguousarray(offsets, np.int64)
+    t = np.ascontiguousarray(t_star, np.float64)
+    order = np.empty(len(t), np.int64)
+    ctx.check(ctx.lib.sof_windowed_resort(ctx.h, len(off) - 1, _ptr(off), _ptr(t), int(window), _ptr(order)))
+    return order
+
+
+def render_pixel(offsets, index, values, depth_mode: int = L.DEPTH_EXACT, ctx: Context | None = None,
+                 dc=None) -> dict:
+    """render_pixel (opacity_field.hpp:201-219) of given contribution lists on the device;
+    colours from `dc` [N, 3] or, when None, the resident scene of `ctx`."""
+    ctx = ctx or default_context()
+    off = np.ascontiguousarray(offsets, np.int64)
+    idx = np.ascontiguousarray(index, np.int32)
+    val = np.ascontiguousarray(values, np.float64).reshape(-1, 6)
+    nl = len(off) - 1
+    dcp = None if dc is None else _f64(dc, 3)
+    out = {"color": np.empty((nl, 3)), "depth": np.empty(nl), "accumulated_opacity": np.empty(nl),
+           "t_final": np.empty(nl)}
+    ctx.check(ctx.lib.sof_render_pixel(ctx.h, nl, _ptr(off), _ptr(idx), _ptr(val), 0 if dcp is None else len(dcp),
+                                       None if dcp is None else _ptr(dcp), int(depth_mode),
+                                       *(_ptr(out[k]) for k in ("color", "depth", "accumulated_opacity", "t_final"))))
     return out
 
 

@@ -658,6 +658,8 @@ int64_t sof_result_count(const sof_ctx* c, int kind) {
     case SOF_R_SEED_PROVENANCE: return c->n_seeds;
     case SOF_R_MESH_RESIDUALS: return c->mesh_nres;
     case SOF_R_TETS: return int64_t(c->delaunay_tets.size());
+    case SOF_R_CONTRIB_INDEX: return c->n_contrib;
+    case SOF_R_CONTRIB_VALUES: return c->n_contrib < 0 ? -1 : 6 * c->n_contrib;
     default: return -1;
   }
 }
@@ -682,6 +684,8 @@ int sof_copy_result(sof_ctx* c, int kind, void* dst) {
       case SOF_R_SEED_PROVENANCE: download(c, (uint8_t*)dst, c->seed_prov.p, cnt); break;
       case SOF_R_MESH_RESIDUALS: download(c, (double*)dst, c->m_res.p, cnt); break;
       case SOF_R_TETS: std::memcpy(dst, c->delaunay_tets.data(), sizeof(int32_t) * cnt); break;
+      case SOF_R_CONTRIB_INDEX: download(c, (int32_t*)dst, c->ct_idx.p, cnt); break;
+      case SOF_R_CONTRIB_VALUES: download(c, (double*)dst, c->ct_val.p, cnt); break;
     }
     sync(c);
   });

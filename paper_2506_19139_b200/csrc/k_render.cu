@@ -38,6 +38,7 @@
 #include "../../include/sof_cuda.h"
 #include "sof_internal.h"
 #include "sof_tma.cuh"
+#include "stl_order.cuh"
 
 namespace sofk {
 
@@ -1131,9 +1132,204 @@ __global__ void k_gaussian_normal(int64_t m, const int32_t* __restrict__ gidx,
   for (int i = 0; i < 3; ++i) out[3 * k + i] = n[i];
 }
 
+
+// ---- the K-window resort mode and the per-ray API ---------------------------------------------
+
+// view-space centre depth cam.to_view(mu).z() (camera.hpp:19, Eigen sums left to right):
+// the arrival order of the window mode
+__global__ void k_center_depth(int64_t n, const GaussStatic* __restrict__ g, Cam cam, double* zc) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double* x = g[i].pos;
+  zc[i] = ((cam.R[6] * x[0] + cam.R[7] * x[1]) + cam.R[8] * x[2]) + cam.t[2];
+}
+
+// One thread per pixel: the slice (any order after R2) goes into arrival order -- centre
+// depth, ties by index, a strict total order -- then through windowed_resort's K-slot
+// window (stl_order.cuh) into A. Serial per pixel: this mode trades the exact sort's
+// warp-parallel network for the reference's streaming window semantics.
+__global__ void __launch_bounds__(128) k_rwindow(int64_t q0, int64_t nq, const int64_t* __restrict__ poff,
+                                                 int64_t base, const uint32_t* __restrict__ ncon, REnt* E, REnt* A,
+                                                 const double* __restrict__ zc, int64_t window) {
+  const int64_t qq = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (qq >= nq) return;
+  const int64_t q = q0 + qq;
+  const int64_t n = ncon[q];
+  REnt* S = E + (poff[q] - base);
+  REnt* O = A + (poff[q] - base);
+  stlo::sort(S, n, [zc](const REnt& a, const REnt& b) {
+    const double za = __ldg(zc + a.idx), zb = __ldg(zc + b.idx);
+    return za < zb || (za == zb && a.idx < b.idx);
+  });
+  stlo::windowed_resort(S, O, n, window, [](const REnt& a, const REnt& b) { return a.t < b.t; });
+}
+
+// collect_contributions over ALL Gaussians for each ray (grid.y strides the rays): PASS 0
+// counts per ray, PASS 1 scatters REnt{t*, 0, index} into the ray's slice (any order;
+// the exact sort follows).
+template <int PASS>
+__global__ void __launch_bounds__(256) k_ct_scan(int64_t n, const Rec* __restrict__ rec, int64_t nr,
+                                                 const double* __restrict__ dirs, uint32_t* cnt,
+                                                 const int64_t* __restrict__ off, REnt* E) {
+  const int lane = threadIdx.x & 31;
+  const double* tab = kSofExpTabDev;
+  for (int64_t r = blockIdx.y; r < nr; r += gridDim.y) {
+    const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t g0 = int64_t(blockIdx.x) * blockDim.x; g0 < n; g0 += stride) {
+      const int64_t g = g0 + threadIdx.x;
+      double t = 0.0, alpha, a, b;
+      const bool hit = g < n && contribution(rec[g], d, tab, t, alpha, a, b);
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (!m) continue;
+      const int leader = __ffs(m) - 1;
+      uint32_t slot = 0;
+      if (lane == leader) slot = atomicAdd(cnt + r, uint32_t(__popc(m)));
+      slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(m & ((1u << lane) - 1u));
+      if (PASS == 1 && hit) {
+        REnt e;
+        e.t = t;
+        e.pos = 0;
+        e.idx = int32_t(g);
+        st_rent(E + off[r] + slot, e);
+      }
+    }
+  }
+}
+
+// RayContribution fields of every sorted entry (the expressions of the scan, recomputed)
+__global__ void k_ct_values(int64_t C, int64_t nr, const int64_t* __restrict__ off, const REnt* __restrict__ E,
+                            const Rec* __restrict__ rec, const double* __restrict__ dirs, int32_t* idx, double* val) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= C) return;
+  int64_t lo = 0, hi = nr;  // the ray: last r with off[r] <= k
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  const REnt e = ld_rent(E + k);
+  const double d[3] = {dirs[3 * lo], dirs[3 * lo + 1], dirs[3 * lo + 2]};
+  double t = 0.0, alpha = 0.0, a = 0.0, b = 0.0;
+  contribution(rec[e.idx], d, kSofExpTabDev, t, alpha, a, b);
+  idx[k] = e.idx;
+  double* v = val + 6 * k;
+  v[0] = t;
+  v[1] = alpha;
+  v[2] = a;
+  v[3] = b;
+  v[4] = rec[e.idx].c;
+  v[5] = rec[e.idx].op;
+}
+
+// windowed_resort of independent lists, one thread per list
+__global__ void k_wresort(int64_t nl, const int64_t* __restrict__ off, const double* __restrict__ t, int64_t window,
+                          REnt* S, REnt* O, int64_t* order) {
+  const int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (l >= nl) return;
+  const int64_t b = off[l], n = off[l + 1] - b;
+  for (int64_t k = 0; k < n; ++k) {
+    REnt e;
+    e.t = t[b + k];
+    e.pos = int32_t(k);
+    e.idx = 0;
+    S[b + k] = e;
+  }
+  stlo::windowed_resort(S + b, O + b, n, window, [](const REnt& x, const REnt& y) { return x.t < y.t; });
+  for (int64_t k = 0; k < n; ++k) order[b + k] = b + O[b + k].pos;
+}
+
+// render_pixel (opacity_field.hpp:201-219) of given lists, one thread per list
+__global__ void k_rpixel(int64_t nl, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                         const double* __restrict__ val, const double* __restrict__ dc, int exact, double* color,
+                         double* depth_out, double* acc, double* tfinal) {
+  const int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (l >= nl) return;
+  const int64_t b = off[l], e = off[l + 1];
+  double T = 1.0, col[3] = {0.0, 0.0, 0.0}, med_T = 1.0;
+  int64_t med = -1;
+  for (int64_t k = b; k < e; ++k) {
+    const double alpha = val[6 * k + 1];
+    const int64_t g = idx[k];
+    for (int c = 0; c < 3; ++c) col[c] = col[c] + dc[3 * g + c] * alpha * T;  // :207
+    const double next = T * (1.0 - alpha);
+    if (med < 0 && T > 0.5 && next < 0.5) {  // find_median :132-141
+      med = k;
+      med_T = T;
+    }
+    T = next;
+  }
+  double depth = NAN;
+  if (med >= 0) {
+    const double* m = val + 6 * med;
+    depth = m[0];  // median_depth :143-147
+    if (exact) {   // exact_depth :157-166
+      const double lt = 2.0 * sof_log((med_T - 0.5) / (med_T * m[5]));
+      const double disc = m[3] * m[3] - 4.0 * m[2] * (m[4] + lt);
+      if (!(disc < 0.0)) depth = m[0] - sqrt(disc) / (2.0 * m[2]);
+    }
+  }
+  double o = 0.0;
+  if (!isnan(depth)) {  // opacity_along_ray(contribs, depth) :104-108
+    double T2 = 1.0;
+    for (int64_t k = b; k < e; ++k) {
+      const double* v = val + 6 * k;
+      const double te = (depth < v[0]) ? depth : v[0];
+      double al = 0.0;
+      if (!(te <= 0.0)) {
+        al = v[5] * exp_any(-0.5 * ((v[2] * te + v[3]) * te + v[4]), kSofExpTabDev);  // alpha_at :95-101
+        if (al < kMinAlpha) al = 0.0;
+        else if (kMaxAlpha < al) al = kMaxAlpha;
+      }
+      T2 *= 1.0 - al;
+    }
+    o = 1.0 - T2;
+  }
+  if (color)
+    for (int c = 0; c < 3; ++c) color[3 * l + c] = col[c];
+  if (depth_out) depth_out[l] = depth;
+  if (acc) acc[l] = o;
+  if (tfinal) tfinal[l] = T;
+}
+
 }  // namespace sofk
 
 using namespace sofk;
+
+namespace {
+void render_attrs(sof_ctx* c) {
+  if (c->rs.attr_set) return;  // the sorts' and the blend's dynamic shared memory (per device)
+  SOF_CUDA(cudaFuncSetAttribute(k_rsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSortCap * 16));
+  SOF_CUDA(cudaFuncSetAttribute(k_rsort_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortWarps * 512 * 16));
+  SOF_CUDA(cudaFuncSetAttribute(k_rblend, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlendSmem));
+  c->rs.attr_set = true;
+}
+
+// the exact (t*, index) sort of nq slices [poff[q0 + i] - base, +ncon) of E (R3)
+void sort_slices(sof_ctx* c, int64_t q0, int64_t nq, const int64_t* poff, int64_t base, const uint32_t* ncon, REnt* E) {
+  RenderScratch& rs = c->rs;
+  cudaStream_t st = c->stream;
+  rs.big.ensure(std::max<int64_t>(int64_t(rs.big.n), 2 * nq));
+  rs.big_cnt.ensure(4);
+  SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p + 1, 0, sizeof(int32_t), st));
+  SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p + 3, 0, sizeof(int32_t), st));
+  const unsigned sort_grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((nq + kSortWarps - 1) / kSortWarps, 148 * 8)));
+  int32_t* qmid = rs.big.p;  // rs.big[0, n) served the binning; reused for the sort queues
+  int32_t* qhuge = rs.big.p + nq;
+  k_rsort<<<sort_grid, kSortWarps * 32, 0, st>>>(q0, nq, poff, base, ncon, E, qmid, rs.big_cnt.p + 1);
+  k_rsort_mid<<<148 * 2, kSortWarps * 32, kSortWarps * 512 * 16, st>>>(poff, base, ncon, E, qmid, rs.big_cnt.p + 1,
+                                                                      qhuge, rs.big_cnt.p + 3);
+  k_rsort_big<<<148, 256, kCtaSortCap * 16, st>>>(poff, base, ncon, E, qhuge, rs.big_cnt.p + 3);
+  c->launches += 3;
+  SOF_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+extern "C" int sof_set_render_window(sof_ctx* c, int64_t window) {
+  if (!c || window < 0) return SOF_E_INVALID;
+  c->r_window = window;
+  return SOF_OK;
+}
 
 extern "C" int sof_set_render_pool(sof_ctx* c, int64_t bytes) {
   if (!c || bytes < 0) return SOF_E_INVALID;
@@ -1156,12 +1352,7 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     if (T > INT32_MAX / kRPix) throw InvalidArg("image too large");
     RenderScratch& rs = c->rs;
     cudaStream_t st = c->stream;
-    if (!rs.attr_set) {  // the sorts' 64 KB of dynamic shared memory (per device)
-      SOF_CUDA(cudaFuncSetAttribute(k_rsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSortCap * 16));
-      SOF_CUDA(cudaFuncSetAttribute(k_rsort_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortWarps * 512 * 16));
-      SOF_CUDA(cudaFuncSetAttribute(k_rblend, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlendSmem));
-      rs.attr_set = true;
-    }
+    render_attrs(c);
     rs.big_cnt.ensure(4);  // [0] big Gaussians (binning), [1] big pixels (band), [2] big pixels (frame)
     SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p, 0, 4 * sizeof(int32_t), st));
     c->r_stats.ensure(4);
@@ -1208,8 +1399,14 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     const int64_t total = read_scalar(c, rs.poff.p + Q);
     c->r_out.ensure(6 * P);
     RenderOut out{c->r_out.p, c->r_out.p + P, c->r_out.p + 2 * P, c->r_out.p + 5 * P};
-    // bands of tiles whose slices fit the scratch budget
-    const int64_t cap = std::max<int64_t>(c->render_pool / kEntryBytes, 1);
+    // bands of tiles whose slices fit the scratch budget (two slice buffers in window mode)
+    const int64_t window = c->r_window;
+    const int64_t cap = std::max<int64_t>(c->render_pool / (window > 0 ? 2 * kEntryBytes : kEntryBytes), 1);
+    if (window > 0 && n > 0) {
+      rs.zc.ensure(n);
+      k_center_depth<<<grid_for(n, 256), 256, 0, st>>>(n, c->gstat.p, cam, rs.zc.p);
+      SOF_LAUNCHED(c);
+    }
     std::vector<int64_t> toff;
     if (total > cap) {
       rs.band_off.ensure(T + 1);
@@ -1235,22 +1432,21 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       k_rtest<<<nt, kRPix, 0, st>>>(cam, tiles_x, int(t0), rs.tile_off.p, rs.ent.p, rec, rs.poff.p, e0, E,
                                     rs.ncon.p, c->r_stats.p);
       SOF_LAUNCHED(c);
-      SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p + 1, 0, sizeof(int32_t), st));
-      SOF_CUDA(cudaMemsetAsync(rs.big_cnt.p + 3, 0, sizeof(int32_t), st));
       const int64_t nq = int64_t(nt) * kRPix;
-      const unsigned sort_grid = unsigned(std::min<int64_t>((nq + kSortWarps - 1) / kSortWarps, 148 * 8));
-      // big list: rs.big[0, n) for the binning, then reused for the sort queues
-      int32_t* qmid = rs.big.p;
-      int32_t* qhuge = rs.big.p + nq;
-      k_rsort<<<sort_grid, kSortWarps * 32, 0, st>>>(t0 * kRPix, nq, rs.poff.p, e0, rs.ncon.p, E, qmid,
-                                                      rs.big_cnt.p + 1);
-      k_rsort_mid<<<148 * 2, kSortWarps * 32, kSortWarps * 512 * 16, st>>>(rs.poff.p, e0, rs.ncon.p, E, qmid,
-                                                                          rs.big_cnt.p + 1, qhuge, rs.big_cnt.p + 3);
-      k_rsort_big<<<148, 256, kCtaSortCap * 16, st>>>(rs.poff.p, e0, rs.ncon.p, E, qhuge, rs.big_cnt.p + 3);
+      const REnt* B = E;
+      if (window > 0) {
+        rs.ent16b.ensure(ne * sizeof(REnt));
+        REnt* A = reinterpret_cast<REnt*>(rs.ent16b.p);
+        k_rwindow<<<grid_for(nq, 128), 128, 0, st>>>(t0 * kRPix, nq, rs.poff.p, e0, rs.ncon.p, E, A, rs.zc.p, window);
+        SOF_LAUNCHED(c);
+        B = A;
+      } else {
+        sort_slices(c, t0 * kRPix, nq, rs.poff.p, e0, rs.ncon.p, E);  // k_rsort counts big_cnt[2] per frame
+      }
       k_rblend<<<nt, kRPix, kBlendSmem, st>>>(cam, tiles_x, int(t0), rs.tile_off.p, rs.ent.p, rs.poff.p, e0,
-                                               rs.ncon.p, E, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT, out,
+                                               rs.ncon.p, B, rec, c->dc.p, depth_mode == SOF_DEPTH_EXACT, out,
                                                c->r_stats.p);
-      c->launches += 3;
+      SOF_LAUNCHED(c);
       SOF_CUDA(cudaGetLastError());
       ++nbands;
       t0 = t1;
@@ -1357,5 +1553,149 @@ extern "C" int sof_gaussian_normals(sof_ctx* c, int64_t m, const int32_t* gidx, 
     SOF_LAUNCHED(c);
     SOF_CUDA(cudaMemcpyAsync(out, dout, 24 * m, cudaMemcpyDeviceToHost, c->stream));
     SOF_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+namespace {
+// carve a per-call scratch of `bytes` (16-byte aligned pieces) out of c->r_query
+struct Carve {
+  char* base;
+  size_t at = 0;
+  template <typename T>
+  T* take(int64_t count) {
+    T* p = reinterpret_cast<T*>(base + at);
+    at += (size_t(std::max<int64_t>(count, 1)) * sizeof(T) + 15) & ~size_t(15);
+    return p;
+  }
+};
+size_t carve_size(std::initializer_list<size_t> bytes) {
+  size_t s = 0;
+  for (size_t b : bytes) s += (std::max<size_t>(b, 1) + 15) & ~size_t(15);
+  return s;
+}
+}  // namespace
+
+extern "C" int sof_collect_contributions(sof_ctx* c, int view, int64_t nr, const double* dirs, int64_t* offsets_out) {
+  if (!c || nr < 0 || (nr > 0 && (!dirs || !offsets_out))) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (!c->has_scene) throw StateError("no scene: call sof_set_scene first");
+    if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+    for (int64_t k = 0; k < 3 * nr; ++k)
+      if (!std::isfinite(dirs[k])) throw InvalidArg("non-finite ray direction");
+    render_attrs(c);
+    c->n_contrib = -1;
+    cudaStream_t st = c->stream;
+    const Rec* rec = view_records(c, view);
+    const int64_t n = c->n;
+    DBuf<char>& b = c->r_query;
+    b.ensure(int64_t(carve_size({size_t(24 * nr), size_t(4 * nr), size_t(8 * (nr + 1))})));
+    Carve cv{b.p};
+    double* d_dirs = cv.take<double>(3 * nr);
+    uint32_t* cnt = cv.take<uint32_t>(nr);
+    int64_t* off = cv.take<int64_t>(nr + 1);
+    SOF_CUDA(cudaMemcpyAsync(d_dirs, dirs, 24 * nr, cudaMemcpyHostToDevice, st));
+    SOF_CUDA(cudaMemsetAsync(cnt, 0, 4 * std::max<int64_t>(nr, 1), st));
+    const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8))),
+                    unsigned(std::max<int64_t>(1, std::min<int64_t>(nr, 65535))));
+    if (nr > 0 && n > 0) {
+      k_ct_scan<0><<<grid, 256, 0, st>>>(n, rec, nr, d_dirs, cnt, nullptr, nullptr);
+      SOF_LAUNCHED(c);
+    }
+    scan_u32_i64(c, cnt, off, nr);
+    const int64_t C = read_scalar(c, off + nr);
+    c->rs.ent16.ensure(std::max<int64_t>(C, 1) * sizeof(REnt));
+    REnt* E = reinterpret_cast<REnt*>(c->rs.ent16.p);
+    if (C > 0) {
+      SOF_CUDA(cudaMemsetAsync(cnt, 0, 4 * nr, st));
+      k_ct_scan<1><<<grid, 256, 0, st>>>(n, rec, nr, d_dirs, cnt, off, E);
+      SOF_LAUNCHED(c);
+      sort_slices(c, 0, nr, off, 0, cnt, E);
+    }
+    c->ct_idx.ensure(std::max<int64_t>(C, 1));
+    c->ct_val.ensure(6 * std::max<int64_t>(C, 1));
+    if (C > 0) {
+      k_ct_values<<<grid_for(C, 256), 256, 0, st>>>(C, nr, off, E, rec, d_dirs, c->ct_idx.p, c->ct_val.p);
+      SOF_LAUNCHED(c);
+    }
+    SOF_CUDA(cudaMemcpyAsync(offsets_out, off, 8 * (nr + 1), cudaMemcpyDeviceToHost, st));
+    SOF_CUDA(cudaStreamSynchronize(st));
+    c->n_contrib = C;
+  });
+}
+
+extern "C" int sof_windowed_resort(sof_ctx* c, int64_t nl, const int64_t* offsets, const double* t_star,
+                                   int64_t window, int64_t* order_out) {
+  if (!c || nl < 0 || window < 0 || (nl > 0 && !offsets)) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (nl == 0) return;
+    if (offsets[0] != 0) throw InvalidArg("offsets[0] must be 0");
+    for (int64_t l = 0; l < nl; ++l) {
+      if (offsets[l + 1] < offsets[l]) throw InvalidArg("offsets must be non-decreasing");
+      if (offsets[l + 1] - offsets[l] > INT32_MAX) throw InvalidArg("list longer than 2^31 - 1");
+    }
+    const int64_t C = offsets[nl];
+    if (C > 0 && (!t_star || !order_out)) throw InvalidArg("null t_star / order");
+    cudaStream_t st = c->stream;
+    DBuf<char>& b = c->r_query;
+    b.ensure(int64_t(carve_size({size_t(8 * (nl + 1)), size_t(8 * C), size_t(8 * C), size_t(16 * C), size_t(16 * C)})));
+    Carve cv{b.p};
+    int64_t* off = cv.take<int64_t>(nl + 1);
+    double* t = cv.take<double>(C);
+    int64_t* order = cv.take<int64_t>(C);
+    REnt* S = cv.take<REnt>(C);
+    REnt* O = cv.take<REnt>(C);
+    SOF_CUDA(cudaMemcpyAsync(off, offsets, 8 * (nl + 1), cudaMemcpyHostToDevice, st));
+    if (C > 0) SOF_CUDA(cudaMemcpyAsync(t, t_star, 8 * C, cudaMemcpyHostToDevice, st));
+    k_wresort<<<grid_for(nl, 128), 128, 0, st>>>(nl, off, t, window, S, O, order);
+    SOF_LAUNCHED(c);
+    if (C > 0) SOF_CUDA(cudaMemcpyAsync(order_out, order, 8 * C, cudaMemcpyDeviceToHost, st));
+    SOF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+extern "C" int sof_render_pixel(sof_ctx* c, int64_t nl, const int64_t* offsets, const int32_t* index,
+                                const double* values, int64_t n_gauss, const double* dc, int depth_mode, double* color,
+                                double* depth, double* acc_opacity, double* t_final) {
+  if (!c || nl < 0 || n_gauss < 0 || (nl > 0 && !offsets)) return SOF_E_INVALID;
+  return guard(c, [&] {
+    if (!dc && !c->has_scene) throw StateError("no scene: call sof_set_scene first or pass the colours");
+    const int64_t ng = dc ? n_gauss : c->n;
+    if (depth_mode != SOF_DEPTH_EXACT && depth_mode != SOF_DEPTH_MEDIAN) throw InvalidArg("unknown depth mode");
+    if (nl == 0) return;
+    if (offsets[0] != 0) throw InvalidArg("offsets[0] must be 0");
+    for (int64_t l = 0; l < nl; ++l)
+      if (offsets[l + 1] < offsets[l]) throw InvalidArg("offsets must be non-decreasing");
+    const int64_t C = offsets[nl];
+    if (C > 0 && (!index || !values)) throw InvalidArg("null index / values");
+    for (int64_t k = 0; k < C; ++k)
+      if (index[k] < 0 || index[k] >= ng) throw InvalidArg("gaussian index out of range");
+    cudaStream_t st = c->stream;
+    DBuf<char>& b = c->r_query;
+    b.ensure(int64_t(carve_size({size_t(8 * (nl + 1)), size_t(4 * C), size_t(48 * C), size_t(48 * nl),
+                                 size_t(dc ? 24 * ng : 0)})));
+    Carve cv{b.p};
+    int64_t* off = cv.take<int64_t>(nl + 1);
+    int32_t* idx = cv.take<int32_t>(C);
+    double* val = cv.take<double>(6 * C);
+    double* out = cv.take<double>(6 * nl);
+    const double* colours = c->dc.p;
+    if (dc) {
+      double* d = cv.take<double>(3 * ng);
+      if (ng > 0) SOF_CUDA(cudaMemcpyAsync(d, dc, 24 * ng, cudaMemcpyHostToDevice, st));
+      colours = d;
+    }
+    SOF_CUDA(cudaMemcpyAsync(off, offsets, 8 * (nl + 1), cudaMemcpyHostToDevice, st));
+    if (C > 0) {
+      SOF_CUDA(cudaMemcpyAsync(idx, index, 4 * C, cudaMemcpyHostToDevice, st));
+      SOF_CUDA(cudaMemcpyAsync(val, values, 48 * C, cudaMemcpyHostToDevice, st));
+    }
+    k_rpixel<<<grid_for(nl, 128), 128, 0, st>>>(nl, off, idx, val, colours, depth_mode == SOF_DEPTH_EXACT, out,
+                                                 out + 3 * nl, out + 4 * nl, out + 5 * nl);
+    SOF_LAUNCHED(c);
+    if (color) SOF_CUDA(cudaMemcpyAsync(color, out, 24 * nl, cudaMemcpyDeviceToHost, st));
+    if (depth) SOF_CUDA(cudaMemcpyAsync(depth, out + 3 * nl, 8 * nl, cudaMemcpyDeviceToHost, st));
+    if (acc_opacity) SOF_CUDA(cudaMemcpyAsync(acc_opacity, out + 4 * nl, 8 * nl, cudaMemcpyDeviceToHost, st));
+    if (t_final) SOF_CUDA(cudaMemcpyAsync(t_final, out + 5 * nl, 8 * nl, cudaMemcpyDeviceToHost, st));
+    SOF_CUDA(cudaStreamSynchronize(st));
   });
 }

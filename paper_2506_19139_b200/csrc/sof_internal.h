@@ -188,6 +188,8 @@ struct RenderScratch {
   DBuf<char> ent16;               // per contribution: REnt {t*, list position, Gaussian index}
   bool attr_set = false;          // k_rsort_big's dynamic shared-memory limit set
   DBuf<char> rrec;                // [n] per-view render records (k_render.cu RRec, 128 B)
+  DBuf<char> ent16b;              // window mode: the resorted slices (REnt)
+  DBuf<double> zc;                // window mode: [n] view-space centre depth (arrival order)
 };
 
 enum ProfKind { kProfEval = 0, kProfPrep = 1, kProfSched = 2, kProfKinds = 4 };
@@ -284,6 +286,10 @@ struct sof_ctx {
   int64_t r_bands = 0;                      // tile bands of the last render
   int64_t r_Q = 0;                          // tile-major pixel slots of the last render
   int64_t render_pool = int64_t(24) << 30;  // scratch budget of one render band (bytes)
+  int64_t r_window = 0;                     // 0: exact (t*, index) order; K > 0: K-slot windowed resort
+  sofk::DBuf<int32_t> ct_idx;               // sof_collect_contributions: gaussian_index per contribution
+  sofk::DBuf<double> ct_val;                // ... and (t*, alpha, a, b, c, opacity)
+  int64_t n_contrib = -1;
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<char> scan_tmp;                 // block totals of the hand-written scans (k_scan.cu)
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
