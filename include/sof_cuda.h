@@ -159,6 +159,10 @@ int sof_precompute_view(sof_ctx* ctx, int view, double* out13);
 /* build_tile_binding (tiles.hpp:94-146) for one view; lists stay on the device
  * (SOF_R_TILE_OFFSETS / SOF_R_TILE_ENTRIES). */
 int sof_tile_binding(sof_ctx* ctx, int view, int tile_size, int64_t* n_tiles, int64_t* n_entries);
+/* The evaluation's live-only binding of `view` (dead Gaussians left out): stats[3] =
+ * {list entries, Gaussians counted instead of listed in every tile (behind the camera or
+ * crossing its plane, tiles.hpp:116-126), listed entries of crossing Gaussians}. */
+int sof_live_binding_stats(sof_ctx* ctx, int view, int tile_size, int64_t* stats);
 /* schedule_points (tiles.hpp:29-84) for one view, exact (tile, depth, point) order.
  * tile_assignment[n]; order/key_tile/key_depth[n_sched]; block_ranges[2*n_blocks],
  * block_to_tile[n_blocks]. Pass NULL outputs to get the counts first. */

@@ -294,6 +294,20 @@ int sof_tile_binding(sof_ctx* c, int view, int tile_size, int64_t* n_tiles, int6
   });
 }
 
+int sof_live_binding_stats(sof_ctx* c, int view, int tile_size, int64_t* stats) {
+  if (!c || !stats) return SOF_E_INVALID;
+  return guard(c, [&] {
+    need_views(c);
+    if (view < 0 || view >= int(c->cams.size())) throw InvalidArg("view index out of range");
+    if (tile_size <= 0) throw InvalidArg("tile_size must be positive");
+    const Binding& b = view_binding(c, view, tile_size, true);
+    stats[0] = b.entries;
+    stats[1] = b.nb;
+    stats[2] = b.nx;
+    sync(c);
+  });
+}
+
 int sof_schedule_points(sof_ctx* c, int view, int64_t n, const double* xyz, int tile_size,
                         int64_t* n_sched, int64_t* n_blocks, int32_t* tile_assignment,
                         int32_t* order, int32_t* key_tile, double* key_depth,

@@ -98,6 +98,14 @@ __global__ void k_view_rec(int64_t n, const GaussStatic* __restrict__ g, Cam cam
   if (outf) outf[i] = make_recf(r);
 }
 
+// Live bindings: Gaussians the reference lists in every tile (their box crosses the
+// camera plane, tiles.hpp:116-126) are COUNTED through one sorted per-view list
+// (Binding::nb/bkey/bidx) instead of being listed everywhere. kCountBehind: behind the
+// camera (gauss_behind), listed nowhere; kCountCross: listed only in the tiles whose
+// points it may reach (cross_tile_live); Binding::xpos marks those entries so the
+// evaluation does not count them twice.
+constexpr uint8_t kCountBehind = 1, kCountCross = 2;
+
 // Per-view binning inputs of k_tile_rect, produced by the record kernel in the same
 // pass over GaussStatic when the binding of the view is built right away.
 struct RectOut {
@@ -128,13 +136,16 @@ __global__ void __launch_bounds__(128, SOF_REC_MINB) k_view_rec_rect(int64_t n, 
   out[i] = r;
   int tx0, tx1, ty0, ty1;
   uint32_t count = 0;
-  const bool behind = ro.live_only && r.op >= kMinAlpha && gauss_behind(gs, cam, r.c);
-  if (ro.live_only) ro.behind[i] = behind;
+  const bool live = ro.live_only && r.op >= kMinAlpha;
+  const bool behind = live && gauss_behind(gs, cam, r.c);
+  bool crosses = false;
   if (!(ro.live_only && (r.op < kMinAlpha || behind)) &&
-      tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1)) {
-    count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
+      tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1, &crosses)) {
+    count = (live && crosses) ? cross_tile_count(r, ro.ts, ro.tiles_x, ro.tiles_y)
+                              : uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     ro.rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
+  if (ro.live_only) ro.behind[i] = behind ? kCountBehind : (live && crosses) ? kCountCross : 0;
   ro.cnt[i] = count;
   ro.zkey[i] = double_key(r.zmin);
   ro.idx[i] = int32_t(i);
@@ -234,13 +245,16 @@ __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
   }
   int tx0, tx1, ty0, ty1;
   uint32_t count = 0;
-  const bool behind = live_only && rec[i].op >= kMinAlpha && gauss_behind(g[i], cam, rec[i].c);
-  if (live_only) behind_out[i] = behind;
+  const bool live = live_only && rec[i].op >= kMinAlpha;
+  const bool behind = live && gauss_behind(g[i], cam, rec[i].c);
+  bool crosses = false;
   if (!(live_only && (rec[i].op < kMinAlpha || behind)) &&
-      tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1)) {
-    count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
+      tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1, &crosses)) {
+    count = (live && crosses) ? cross_tile_count(rec[i], ts, tiles_x, tiles_y)
+                              : uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
+  if (live_only) behind_out[i] = behind ? kCountBehind : (live && crosses) ? kCountCross : 0;
   cnt[i] = count;
   zkey[i] = double_key(rec[i].zmin);
   idx[i] = int32_t(i);
@@ -255,10 +269,33 @@ __global__ void k_gather_counts(int64_t n, const int32_t* __restrict__ order,
 
 // One thread per Gaussian (in (min_z, index) order) emits its (tile, gaussian)
 // entries; Gaussians covering many tiles (rare) hand the tail to their warp.
+// Live crossing Gaussians (gflag kCountCross) emit only their cross_tile_live tiles, one
+// warp per Gaussian scanning the screen row by row (compacted with ballots, so the
+// entries come out in row-major tile order as the count in the rect kernel assumed).
+__device__ __forceinline__ void emit_cross_warp(const Rec& r, int32_t g, int64_t o, int ts, int tiles_x, int tiles_y,
+                                                uint32_t* keys, int32_t* vals) {
+  const int lane = threadIdx.x & 31;
+  for (int ty = 0; ty < tiles_y; ++ty) {
+    if (!cross_row_live(r, ts, tiles_x, ty)) continue;
+    for (int tx0 = 0; tx0 < tiles_x; tx0 += 32) {
+      const int tx = tx0 + lane;
+      const bool pass = tx < tiles_x && cross_tile_live(r, ts, tx, ty);
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (pass) {
+        const int64_t q = o + __popc(m & ((1u << lane) - 1u));
+        keys[q] = uint32_t(ty * tiles_x + tx);
+        vals[q] = g;
+      }
+      o += __popc(m);
+    }
+  }
+}
+
 __global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
                                const int4* __restrict__ rect, const uint32_t* __restrict__ cnt,
                                const int64_t* __restrict__ off, int tiles_x, uint32_t* keys,
-                               int32_t* vals) {
+                               int32_t* vals, const uint8_t* __restrict__ gflag, const Rec* __restrict__ rec,
+                               int ts, int tiles_y) {
   constexpr uint32_t kOwn = 16;  // entries written by the owning thread
   const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -266,14 +303,25 @@ __global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
   uint32_t count = 0;
   int4 rc = make_int4(0, 0, 0, 0);
   int64_t base = 0;
+  bool cross = false;
   if (r < n) {
     g = order[r];
     count = cnt[g];
     if (count) {
       rc = rect[g];
       base = off[r];
+      cross = gflag && gflag[g] == kCountCross;
     }
   }
+  unsigned xb = __ballot_sync(0xffffffffu, cross);
+  while (xb) {
+    const int src = __ffs(xb) - 1;
+    xb &= xb - 1;
+    const int32_t bg = __shfl_sync(0xffffffffu, g, src);
+    const int64_t bb = __shfl_sync(0xffffffffu, base, src);
+    emit_cross_warp(rec[bg], bg, bb, ts, tiles_x, tiles_y, keys, vals);
+  }
+  if (cross) count = 0;
   {  // row-major walk of the first kOwn tiles of the rectangle (no divisions)
     const uint32_t own = min(count, kOwn);
     int tx = rc.x, ty = rc.z;
@@ -364,37 +412,90 @@ __device__ __forceinline__ bool tile_wanted(const unsigned long long* zmax, int6
   return zmax[t] >= zk;  // zmax 0: no segment reaches t (every key is >= 1)
 }
 
+// (live crossing Gaussians: only their cross_tile_live tiles, as k_emit_entries)
 __global__ void k_filter_counts(int64_t n, const int4* __restrict__ rect, const uint64_t* __restrict__ zkey,
-                                const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* cnt) {
+                                const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* cnt,
+                                const uint8_t* __restrict__ gflag, const Rec* __restrict__ rec, int ts) {
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (g >= n || cnt[g] == 0) return;
   const int4 rc = rect[g];
   const unsigned long long zk = zkey[g];
+  const bool cross = gflag && gflag[g] == kCountCross;
   uint32_t k = 0;
-  for (int ty = rc.z; ty <= rc.w; ++ty)
-    for (int tx = rc.x; tx <= rc.y; ++tx) k += tile_wanted(zmax, int64_t(ty) * tiles_x + tx, zk);
+  for (int ty = rc.z; ty <= rc.w; ++ty) {
+    if (cross && !cross_row_live(rec[g], ts, tiles_x, ty)) continue;
+    for (int tx = rc.x; tx <= rc.y; ++tx)
+      k += tile_wanted(zmax, int64_t(ty) * tiles_x + tx, zk) && (!cross || cross_tile_live(rec[g], ts, tx, ty));
+  }
   cnt[g] = k;
 }
 
 __global__ void k_emit_filtered(int64_t n, const int32_t* __restrict__ order, const int4* __restrict__ rect,
                                 const int64_t* __restrict__ off, const uint64_t* __restrict__ zkey,
                                 const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* keys,
-                                int32_t* vals) {
+                                int32_t* vals, const uint8_t* __restrict__ gflag, const Rec* __restrict__ rec,
+                                int ts) {
   const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (r >= n) return;
   const int32_t g = order[r];
   const int4 rc = rect[g];
   const unsigned long long zk = zkey[g];
+  const bool cross = gflag && gflag[g] == kCountCross;
   int64_t o = off[r];
-  for (int ty = rc.z; ty <= rc.w; ++ty)
+  for (int ty = rc.z; ty <= rc.w; ++ty) {
+    if (cross && !cross_row_live(rec[g], ts, tiles_x, ty)) continue;
     for (int tx = rc.x; tx <= rc.y; ++tx) {
       const int64_t t = int64_t(ty) * tiles_x + tx;
-      if (tile_wanted(zmax, t, zk)) {
+      if (tile_wanted(zmax, t, zk) && (!cross || cross_tile_live(rec[g], ts, tx, ty))) {
         keys[o] = uint32_t(t);
         vals[o] = g;
         ++o;
       }
     }
+  }
+}
+
+// Positions i in [0, M) of a tile-list array whose entry is a kCountCross Gaussian
+// (flag[ent[i]]), ascending: PASS 0 counts per block of kSelBlock, PASS 1 writes.
+constexpr int kSelBlock = 1024;
+template <int PASS>
+__global__ void __launch_bounds__(256) k_cross_sel(int64_t M, const int32_t* __restrict__ ent,
+                                                   const uint8_t* __restrict__ flag, int64_t* cnt,
+                                                   const int64_t* __restrict__ off, int64_t* out) {
+  __shared__ int wsum[8];
+  const int64_t b0 = int64_t(blockIdx.x) * kSelBlock;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t base = PASS ? off[blockIdx.x] : 0;
+  int total = 0;
+  for (int rr = 0; rr < kSelBlock / 256; ++rr) {
+    const int64_t i = b0 + rr * 256 + threadIdx.x;
+    const bool p = i < M && flag[ent[i]] == kCountCross;
+    if (PASS == 0) {
+      total += __syncthreads_count(p);
+      continue;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, p);
+    if (lane == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    int pre = 0, all = 0;
+    for (int k = 0; k < 8; ++k) {
+      pre += (k < w) ? wsum[k] : 0;
+      all += wsum[k];
+    }
+    if (p) out[base + pre + __popc(m & ((1u << lane) - 1u))] = i;
+    base += all;
+    __syncthreads();
+  }
+  if (PASS == 0 && threadIdx.x == 0) cnt[blockIdx.x] = total;
+}
+
+// (key, 2 index) of the counted Gaussians (Binding::bidx holds 2 g: see count_pairs)
+__global__ void k_count_list_init(int64_t nb, const int32_t* __restrict__ sel, const uint64_t* __restrict__ zkey,
+                                  uint64_t* key, int32_t* idx2) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= nb) return;
+  key[j] = zkey[sel[j]];
+  idx2[j] = 2 * sel[j];
 }
 
 struct HasTiles {
@@ -473,7 +574,8 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
   const int64_t n = c->n;
   if (c->bin_zmax) {  // bisection-cache binning: only the reachable (tile, depth) entries
     k_filter_counts<<<grid_for(n, 256), 256, 0, c->stream>>>(n, c->rect.p, c->zkey_in.p, c->bin_zmax, tiles_x,
-                                                             c->gcount.p);
+                                                             c->gcount.p, b.live ? c->gbehind.p : nullptr,
+                                                             view_records(c, view), ts);
     SOF_LAUNCHED(c);
   }
   // visible Gaussians in index order -> gidx_in[0, m)
@@ -526,12 +628,30 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
   build_binding_tail(c, view, ts, b, M, T, tiles_x, tiles_y);
 }
 
+// Binding::xpos: the list positions of b.ent[0, M) holding kCountCross Gaussians
+// (flag indexed by the entry: Gaussian ids, or rows of a truncated binding).
+static void cross_positions(sof_ctx* c, Binding& b, int64_t M, const uint8_t* flag) {
+  const int64_t nblk = (M + kSelBlock - 1) / kSelBlock;
+  c->sel_cnt.ensure(nblk + 1);
+  c->sel_off.ensure(nblk + 1);
+  k_cross_sel<0><<<unsigned(nblk), 256, 0, c->stream>>>(M, b.ent.p, flag, c->sel_cnt.p, nullptr, nullptr);
+  SOF_LAUNCHED(c);
+  scan_i64_i64(c, c->sel_cnt.p, c->sel_off.p, nblk);
+  const int64_t X = read_scalar(c, c->sel_off.p + nblk);
+  b.nx = X;
+  if (X == 0) return;
+  b.xpos.ensure(X);
+  k_cross_sel<1><<<unsigned(nblk), 256, 0, c->stream>>>(M, b.ent.p, flag, nullptr, c->sel_off.p, b.xpos.p);
+  SOF_LAUNCHED(c);
+}
+
 static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t M, int64_t T,
                                int tiles_x, int tiles_y) {
 
   // (on the binding that is served: the view's cache or a scratch slot)
   b.nb = 0;
-  if (b.live && c->n > 0) {  // the behind Gaussians: (min_z key, index) order, index order kept on ties
+  b.nx = 0;
+  if (b.live && c->n > 0) {  // the counted Gaussians: (min_z key, index) order, index order kept on ties
     size_t bytes = 0;
     thrust::counting_iterator<int32_t> it(0);
     const uint8_t* flags = c->gbehind.p;
@@ -547,9 +667,9 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
     if (nb > 0) {
       b.bkey.ensure(2 * nb);
       b.bidx.ensure(2 * nb);
-      k_gather_keys<<<grid_for(nb, 256), 256, 0, c->stream>>>(nb, sel, c->zkey_in.p, b.bkey.p + nb);
+      k_count_list_init<<<grid_for(nb, 256), 256, 0, c->stream>>>(nb, sel, c->zkey_in.p, b.bkey.p + nb,
+                                                                   b.bidx.p + nb);
       SOF_LAUNCHED(c);
-      SOF_CUDA(cudaMemcpyAsync(b.bidx.p + nb, sel, sizeof(int32_t) * nb, cudaMemcpyDeviceToDevice, c->stream));
       sort_pairs_u64(c, b.bkey.p + nb, b.bkey.p, b.bidx.p + nb, b.bidx.p, nb, 64);  // stable: index order on ties
     }
   }
@@ -566,16 +686,20 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
     c->ekey_in.ensure(M);
     c->ekey_out.ensure(M);
     c->eval_in.ensure(M);
+    const uint8_t* gflag = b.live ? c->gbehind.p : nullptr;
+    const Rec* rec = view_records(c, view);
     if (c->bin_zmax)
       k_emit_filtered<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(c->bin_m, c->gidx_out.p, c->rect.p, c->goff.p,
                                                                        c->zkey_in.p, c->bin_zmax, tiles_x,
-                                                                       c->ekey_in.p, c->eval_in.p);
+                                                                       c->ekey_in.p, c->eval_in.p, gflag, rec, ts);
     else
-      k_emit_entries<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(
-          c->bin_m, c->gidx_out.p, c->rect.p, c->gcount.p, c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p);
+      k_emit_entries<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(c->bin_m, c->gidx_out.p, c->rect.p, c->gcount.p,
+                                                                      c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p,
+                                                                      gflag, rec, ts, tiles_y);
     SOF_LAUNCHED(c);
     // stable sort by tile keeps the (min_z, index) order inside every tile list
     sort_pairs_u32(c, c->ekey_in.p, c->ekey_out.p, c->eval_in.p, b.ent.p, M, bits_for(T));
+    if (b.nb > 0) cross_positions(c, b, M, c->gbehind.p);
   }
   k_segment_starts<uint32_t, 0><<<grid_for(M + 1, 256), 256, 0, c->stream>>>(M, c->ekey_out.p, T,
                                                                              b.off.p);
@@ -893,30 +1017,51 @@ __device__ __forceinline__ unsigned scan_chunk(const Rec* rp, int cnt, double zp
   return unsigned(lim);
 }
 
-// The view's behind Gaussians (Binding::nb), sorted by (min_z key, index).
+// The view's counted Gaussians (Binding::nb: behind the camera, or crossing its plane),
+// sorted by (min_z key, index), and the list positions of the crossing ones that are
+// listed in some tiles (Binding::xpos).
 struct Behind {
   const uint64_t* key;
-  const int32_t* idx;
+  const int32_t* idx;  // 2 g (2 row / 2 row - 1 in a truncated binding)
   int64_t n;
+  const int64_t* xpos;
+  int64_t nx;
 };
 
-// Pairs the reference counts for the behind Gaussians of a point's scan: every one of
-// them precedes any min-z break (min_z < 0 < z_point) and none contributes, so all are
-// counted, unless the scan stopped early (classify mode, field_eval.hpp:104-107) at a
-// listed entry (stop_key, stop_idx) that precedes some of them in the (min_z, index)
-// order: then only those before it.
-__device__ __forceinline__ unsigned behind_pairs(const Behind& bh, bool stopped, uint64_t stop_key,
-                                                 int32_t stop_idx) {
-  if (bh.n == 0) return 0;
-  if (!stopped) return unsigned(bh.n);
-  int64_t lo = 0, hi = bh.n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    const uint64_t k = __ldg(bh.key + mid);
-    if (k < stop_key || (k == stop_key && __ldg(bh.idx + mid) < stop_idx)) lo = mid + 1;
-    else hi = mid;
+// Pairs the reference counts for a point whose scan of the listed entries processed the
+// positions [l0, l0 + P) of its tile list, beyond those P. The reference's list holds
+// every counted Gaussian; its scan processes them in (min_z, index) order up to the early
+// stop at the listed entry (stop_key, stop_cmp = 2 * its index/row) inclusive, or else up
+// to the min-z break: all with min_z <= z_point (field_eval.hpp:86-108). Listed crossing
+// entries among the processed positions are already in P and are taken off again.
+__device__ __forceinline__ int count_pairs(const Behind& bh, bool stopped, uint64_t stop_key, int32_t stop_cmp,
+                                           double zp, int64_t l0, unsigned P) {
+  int add = 0;
+  if (bh.n > 0) {
+    const uint64_t K = stopped ? stop_key : double_key(zp);
+    const int32_t I = stopped ? stop_cmp : INT_MAX;
+    int64_t lo = 0, hi = bh.n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      const uint64_t k = __ldg(bh.key + mid);
+      if (k < K || (k == K && __ldg(bh.idx + mid) <= I)) lo = mid + 1;
+      else hi = mid;
+    }
+    add = int(lo);
   }
-  return unsigned(lo);
+  if (bh.nx > 0 && P > 0) {
+    auto lower = [&](int64_t x) {
+      int64_t lo = 0, hi = bh.nx;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(bh.xpos + mid) < x) lo = mid + 1;
+        else hi = mid;
+      }
+      return lo;
+    };
+    add -= int(lower(l0 + P) - lower(l0));
+  }
+  return add;
 }
 
 // One CTA = one schedule block (<= 256 points of one tile). The block's Gaussian
@@ -992,18 +1137,18 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
     };
     int chunk_no = 0, stop = -1;
     uint64_t stop_key = 0;
-    int32_t stop_idx = 0;
+    int32_t stop_idx = -1;
     auto eval_chunk = [&](const Rec* rp, int cnt) {
       const unsigned p = scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, stop, eval_one);
-      if (stop >= 0 && bh.n > 0) {  // where the early stop happened, for behind_pairs
+      if (stop >= 0 && bh.n > 0 && stop_idx < 0) {  // where the early stop happened, for count_pairs
         stop_key = double_key(rp[stop].zmin);
-        stop_idx = lp[chunk_no * kChunk + stop];
+        stop_idx = 2 * lp[chunk_no * kChunk + stop];
       }
       ++chunk_no;
       return p;
     };
     pairs += stream_list<STAGE>(lp, len, recs, &tmap, srec, s_bar, done, eval_chunk);
-    if (active) pairs += behind_pairs(bh, stop >= 0, stop_key, stop_idx);
+    if (active) pairs += count_pairs(bh, stop >= 0, stop_key, stop_idx, pr.zp, l0, pairs);
   } else {
     for (int64_t base = l0; base < l1; base += kChunk) {
       if (!__syncthreads_or(!done)) break;
@@ -1303,7 +1448,8 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
     const Rec* const* __restrict__ recs_v, const CUtensorMap* __restrict__ tmaps, bool early,
     uint32_t* item_pairs, uint8_t* item_ext,
     unsigned long long* counters, const uint64_t* const* __restrict__ bkeys,
-    const int32_t* const* __restrict__ bidxs, const int64_t* __restrict__ nbeh) {
+    const int32_t* const* __restrict__ bidxs, const int64_t* __restrict__ nbeh,
+    const int64_t* const* __restrict__ xposs, const int64_t* __restrict__ nxs) {
   __shared__ __align__(128) Rec srec[STAGE == 1 ? 2 : 1][kChunk];
   __shared__ __align__(16) double s_exp[128];
   __shared__ __align__(8) uint64_t s_bar[2];
@@ -1353,22 +1499,22 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
     }
     return false;
   };
-  const Behind bh{bkeys[v], bidxs[v], nbeh[v]};
+  const Behind bh{bkeys[v], bidxs[v], nbeh[v], xposs[v], nxs[v]};
   const int32_t* lp = lent + l0;
   int chunk_no = 0, stop = -1;
   uint64_t stop_key = 0;
-  int32_t stop_idx = 0;
+  int32_t stop_idx = -1;
   auto eval_chunk = [&](const Rec* rp, int cnt) {
     const unsigned p = scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, stop, eval_one);
-    if (stop >= 0 && bh.n > 0) {
+    if (stop >= 0 && bh.n > 0 && stop_idx < 0) {
       stop_key = double_key(rp[stop].zmin);
-      stop_idx = lp[chunk_no * kChunk + stop];
+      stop_idx = 2 * lp[chunk_no * kChunk + stop];
     }
     ++chunk_no;
     return p;
   };
   pairs += stream_list<STAGE>(lp, int(l1 - l0), recs, tmap, srec, s_bar, done, eval_chunk);
-  if (active) pairs += behind_pairs(bh, stop >= 0, stop_key, stop_idx);
+  if (active) pairs += count_pairs(bh, stop >= 0, stop_key, stop_idx, pr.zp, l0, pairs);
   if (active) {
     item_pairs[item] = pairs;
     item_ext[item] = (complete && 1.0 - survive < 0.5) ? 1 : 0;
@@ -1458,8 +1604,8 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
   const int V = int(c->cams.size());
   const int G = std::min(kGroupViews, v1 - v0);
   if (int64_t(G) * n >= (int64_t(1) << 31)) return false;
-  std::vector<const void*> ptrs(5 * size_t(V), nullptr);
-  std::vector<int64_t> nbeh(size_t(V), 0);
+  std::vector<const void*> ptrs(6 * size_t(V), nullptr);
+  std::vector<int64_t> nbeh(2 * size_t(V), 0);  // [V] counted Gaussians, [V] listed crossing positions
   for (int v = v0; v < v1; ++v) {
     const Binding& bd = c->bindings[v];
     ptrs[v] = bd.off.p;
@@ -1467,15 +1613,17 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
     ptrs[2 * V + v] = c->recs[v].p;
     ptrs[3 * V + v] = bd.nb ? bd.bkey.p : nullptr;
     ptrs[4 * V + v] = bd.nb ? bd.bidx.p : nullptr;
+    ptrs[5 * V + v] = bd.nx ? bd.xpos.p : nullptr;
     nbeh[v] = bd.nb;
+    nbeh[V + v] = bd.nx;
   }
   GroupScratch& g = c->grp;
   g.cams.ensure(V);
-  g.ptrs.ensure(5 * V);
-  g.nbeh.ensure(V);
+  g.ptrs.ensure(6 * V);
+  g.nbeh.ensure(2 * V);
   SOF_CUDA(cudaMemcpyAsync(g.cams.p, c->cams.data(), sizeof(Cam) * V, cudaMemcpyHostToDevice, c->stream));
-  SOF_CUDA(cudaMemcpyAsync(g.ptrs.p, ptrs.data(), sizeof(void*) * 5 * V, cudaMemcpyHostToDevice, c->stream));
-  SOF_CUDA(cudaMemcpyAsync(g.nbeh.p, nbeh.data(), sizeof(int64_t) * V, cudaMemcpyHostToDevice, c->stream));
+  SOF_CUDA(cudaMemcpyAsync(g.ptrs.p, ptrs.data(), sizeof(void*) * 6 * V, cudaMemcpyHostToDevice, c->stream));
+  SOF_CUDA(cudaMemcpyAsync(g.nbeh.p, nbeh.data(), sizeof(int64_t) * 2 * V, cudaMemcpyHostToDevice, c->stream));
   if (c->staging == 1) {  // TMA staging: one tensor map per view's record array
     std::vector<CUtensorMap> tmaps(static_cast<size_t>(V));
     std::memset(tmaps.data(), 0, sizeof(CUtensorMap) * size_t(V));
@@ -1498,6 +1646,7 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
   const Rec* const* recs = reinterpret_cast<const Rec* const*>(g.ptrs.p + 2 * V);
   const uint64_t* const* bkeys = reinterpret_cast<const uint64_t* const*>(g.ptrs.p + 3 * V);
   const int32_t* const* bidxs = reinterpret_cast<const int32_t* const*>(g.ptrs.p + 4 * V);
+  const int64_t* const* xposs = reinterpret_cast<const int64_t* const*>(g.ptrs.p + 5 * V);
   for (int g0 = v0; g0 < v1; g0 += G) {
     GroupTables gt;
     gt.g0 = g0;
@@ -1541,12 +1690,12 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
       k_eval_group<1><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
                                                              tile_size, gt, loffs, lents, recs, g.tmaps.p, early,
                                                              g.item_pairs.p, g.item_ext.p, c->d_counters.p, bkeys,
-                                                             bidxs, g.nbeh.p);
+                                                             bidxs, g.nbeh.p, xposs, g.nbeh.p + V);
     else
       k_eval_group<0><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(s.blocks.p, c->d_scalar.p, g.order.p, n, xyz, g.cams.p,
                                                              tile_size, gt, loffs, lents, recs, nullptr, early,
                                                              g.item_pairs.p, g.item_ext.p, c->d_counters.p, bkeys,
-                                                             bidxs, g.nbeh.p);
+                                                             bidxs, g.nbeh.p, xposs, g.nbeh.p + V);
     SOF_LAUNCHED(c);
     prof_span(c, e0, prof_mark(c), kProfEval);
     c->eval_launches++;
@@ -1664,12 +1813,14 @@ __global__ void k_trunc_mark(int64_t T, const int64_t* __restrict__ off, const i
   for (int64_t k = lane; k < L; k += 32) used[ent[b + k]] = 1;
 }
 
-// compact row of every used Gaussian; copy its record
+// compact row of every used Gaussian; copy its record and its count flag
 __global__ void k_trunc_rows(int64_t n, const uint8_t* __restrict__ used, const int32_t* __restrict__ pos,
-                             const Rec* __restrict__ rec, Rec* out) {
+                             const Rec* __restrict__ rec, Rec* out, const uint8_t* __restrict__ gflag,
+                             uint8_t* rflag) {
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (g >= n || !used[g]) return;
   out[pos[g]] = rec[g];
+  rflag[pos[g]] = gflag[g];
 }
 
 // one warp per tile: the kept prefix, entries remapped to compact rows
@@ -1682,10 +1833,15 @@ __global__ void k_trunc_emit(int64_t T, const int64_t* __restrict__ off, const i
   for (int64_t k = lane; k < L; k += 32) out[ob + k] = pos[ent[b + k]];
 }
 
-__global__ void k_rows_of(int64_t nb, const int32_t* __restrict__ gidx, const int32_t* __restrict__ pos,
-                          int32_t* out) {
+// count-list indices (2 g) in row space: 2 row for a Gaussian with a row, 2 pos - 1
+// (between the rows before and after it) otherwise, so that comparing with 2 row(stop)
+// orders exactly as comparing Gaussian indices (rows keep the Gaussian order)
+__global__ void k_rows_of(int64_t nb, const int32_t* __restrict__ gidx2, const int32_t* __restrict__ pos,
+                          const uint8_t* __restrict__ used, int32_t* out) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < nb) out[i] = pos[gidx[i]] - 1;
+  if (i >= nb) return;
+  const int32_t g = gidx2[i] >> 1;
+  out[i] = used[g] ? 2 * pos[g] : 2 * pos[g] - 1;
 }
 
 __global__ void k_u8_to_i32_f(int64_t n, const uint8_t* __restrict__ a, int32_t* b) {
@@ -1821,23 +1977,26 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     c->recs[v].ensure(std::max<int64_t>(R, 1));
     ph[3] += ms_since(t0);
     t0 = tick();
-    k_trunc_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(n, used.p, pos.p, rec, c->recs[v].p);
+    bs.rflag.ensure(std::max<int64_t>(R, 1));
+    k_trunc_rows<<<grid_for(n, 256), 256, 0, c->stream>>>(n, used.p, pos.p, rec, c->recs[v].p, c->gbehind.p,
+                                                          bs.rflag.p);
     SOF_LAUNCHED(c);
     b.off.ensure(T + 1);
     SOF_CUDA(cudaMemcpyAsync(b.off.p, toff.p, sizeof(int64_t) * (T + 1), cudaMemcpyDeviceToDevice, c->stream));
     b.ent.ensure(std::max<int64_t>(L, 1));
     k_trunc_emit<<<grid_for(T * 32, 256), 256, 0, c->stream>>>(T, full.off.p, full.ent.p, toff.p, pos.p, b.ent.p);
     SOF_LAUNCHED(c);
-    // the behind Gaussians, their indices in row space: rows keep the Gaussian order and
-    // a behind Gaussian has no row, so (pos[g] - 1 < row of the stop entry) is exactly
-    // (g < its Gaussian index) for behind_pairs' tie-break
+    // the counted Gaussians, their indices in row space (k_rows_of), and the positions of
+    // the listed crossing ones in the truncated lists
     b.nb = full.nb;
+    b.nx = 0;
     if (b.nb > 0) {
       b.bkey.ensure(b.nb);
       b.bidx.ensure(b.nb);
       SOF_CUDA(cudaMemcpyAsync(b.bkey.p, full.bkey.p, sizeof(uint64_t) * b.nb, cudaMemcpyDeviceToDevice, c->stream));
-      k_rows_of<<<grid_for(b.nb, 256), 256, 0, c->stream>>>(b.nb, full.bidx.p, pos.p, b.bidx.p);
+      k_rows_of<<<grid_for(b.nb, 256), 256, 0, c->stream>>>(b.nb, full.bidx.p, pos.p, used.p, b.bidx.p);
       SOF_LAUNCHED(c);
+      if (L > 0) cross_positions(c, b, L, bs.rflag.p);
     }
     b.view = v;
     b.tile_size = tile_size;
@@ -1875,7 +2034,7 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
           strategies, classify, min_op, ext, o_out, obs, comp, pc);
   } else if (fast_loop(c, strategies)) {  // live-only lists, TMA-gathered records
     if (!bd->live) throw StateError("internal: the fast evaluation loop needs live-only tile lists");
-    const Behind bh{bd->bkey.p, bd->bidx.p, bd->nb};
+    const Behind bh{bd->bkey.p, bd->bidx.p, bd->nb, bd->xpos.p, bd->nx};
     CUtensorMap tmap;
     std::memset(&tmap, 0, sizeof tmap);
     if (c->staging == 1) {
@@ -1894,11 +2053,11 @@ static void launch_eval(sof_ctx* c, bool tiled, int64_t grid, const int32_t* pid
     if (tiled)
       k_eval<MODE, true, false><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, bd->off.p, bd->ent.p, c->n, rec,
-          strategies, classify, min_op, ext, o_out, obs, comp, pc, none, Behind{nullptr, nullptr, 0});
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, none, Behind{nullptr, nullptr, 0, nullptr, 0});
     else
       k_eval<MODE, false, false><<<unsigned(grid), kEvalThreads, 0, c->stream>>>(
           c->sched.blocks.p, nb, pidx, xyz, cam, ts, tiles_x, nullptr, nullptr, c->n, rec,
-          strategies, classify, min_op, ext, o_out, obs, comp, pc, none, Behind{nullptr, nullptr, 0});
+          strategies, classify, min_op, ext, o_out, obs, comp, pc, none, Behind{nullptr, nullptr, 0, nullptr, 0});
   }
   SOF_LAUNCHED(c);
   prof_span(c, e0, prof_mark(c), kProfEval);

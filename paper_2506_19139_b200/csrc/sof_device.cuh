@@ -308,9 +308,10 @@ __host__ __device__ inline long long x86_llround(double x) {
 
 // Tile rectangle of one Gaussian's E-scaled OBB (build_tile_binding tiles.hpp:104-133).
 // Returns false when the Gaussian is skipped (E <= 0 or fully off screen).
+// *crosses_out (optional): the box crosses the camera plane (the all-tiles binding).
 __host__ __device__ inline bool tile_rect(const GaussStatic& g, const Cam& cam, int tile_size,
                                           int tiles_x, int tiles_y, int& tx0, int& tx1, int& ty0,
-                                          int& ty1) {
+                                          int& ty1, bool* crosses_out = nullptr) {
   const double r = g.E;
   if (r <= 0.0) return false;
   double min_x = 1e300, max_x = -1e300, min_y = 1e300, max_y = -1e300;
@@ -341,6 +342,7 @@ __host__ __device__ inline bool tile_rect(const GaussStatic& g, const Cam& cam, 
   tx1 = tiles_x - 1;
   ty0 = 0;
   ty1 = tiles_y - 1;
+  if (crosses_out) *crosses_out = crosses;
   if (!crosses) {
     int a = x86_int(floor(min_x)) / tile_size;
     tx0 = (0 < a) ? a : 0;
@@ -493,6 +495,71 @@ __device__ __forceinline__ bool conic_culls(const Rec& r, float u, float v, floa
   const float g = fmaf(r.conic[0], uu, fmaf(r.conic[1], vv, fmaf(r.conic[3], uv,
                   fmaf(r.conic[4], u, fmaf(r.conic[5], v, r.conic[2])))));
   return g < -r.gmargin;
+}
+
+// Upper bound of the screen conic (Rec::conic, evaluated in FP64 from its float
+// coefficients) over the pixel box [u0, u1] x [v0, v1]: a quadratic's maximum over a box
+// lies at a corner, at the vertex of an edge (concave along it), or at the interior
+// vertex (concave). Locating a vertex with rounding error lowers the value found only to
+// second order, far inside the 1e-6 gmargin slack of conic_box_culled.
+__host__ __device__ inline double conic_max_box(const Rec& r, double u0, double u1, double v0, double v1) {
+  const double A = r.conic[0], B = r.conic[1], F = r.conic[2], C = r.conic[3], D = r.conic[4], E = r.conic[5];
+  auto g = [&](double u, double v) { return ((A * u * u + B * v * v) + C * u * v) + ((D * u + E * v) + F); };
+  double m = g(u0, v0);
+  auto take = [&](double x) { m = (m < x || x != x) ? x : m; };  // NaN propagates: never culled
+  take(g(u1, v0));
+  take(g(u0, v1));
+  take(g(u1, v1));
+  if (B < 0.0) {
+    const double us[2] = {u0, u1};
+    for (int i = 0; i < 2; ++i) {
+      const double u = us[i], v = -(C * u + E) / (2.0 * B);
+      if (v > v0 && v < v1) take(g(u, v));
+    }
+  }
+  if (A < 0.0) {
+    const double vs[2] = {v0, v1};
+    for (int i = 0; i < 2; ++i) {
+      const double v = vs[i], u = -(C * v + D) / (2.0 * A);
+      if (u > u0 && u < u1) take(g(u, v));
+    }
+  }
+  const double det = 4.0 * A * B - C * C;
+  if (A < 0.0 && det > 0.0) {
+    const double u = (C * E - 2.0 * B * D) / det, v = (C * D - 2.0 * A * E) / det;
+    if (u > u0 && u < u1 && v > v0 && v < v1) take(g(u, v));
+  }
+  return m;
+}
+
+// True when no ray through the pixel box reaches alpha >= 1/255 on this Gaussian: the
+// point-level conic_culls would skip every point that projects into the box.
+__host__ __device__ inline bool conic_box_culled(const Rec& r, double u0, double u1, double v0, double v1) {
+  return conic_max_box(r, u0, u1, v0, v1) < -double(r.gmargin) * (1.0 + 1e-6);
+}
+
+// The all-tiles binding of a live Gaussian whose box crosses the camera plane
+// (tiles.hpp:116-126), restricted to the tiles whose points it may reach: the whole
+// screen, then the tile's row, then the tile must survive conic_box_culled. The other
+// (tile, Gaussian) pairs of the reference's lists are counted, never evaluated
+// (Binding::nb / xpos).
+__host__ __device__ inline bool cross_screen_live(const Rec& r, int ts, int tiles_x, int tiles_y) {
+  return !conic_box_culled(r, 0.0, double(tiles_x) * ts, 0.0, double(tiles_y) * ts);
+}
+__host__ __device__ inline bool cross_row_live(const Rec& r, int ts, int tiles_x, int ty) {
+  return !conic_box_culled(r, 0.0, double(tiles_x) * ts, double(ty) * ts, double(ty + 1) * ts);
+}
+__host__ __device__ inline bool cross_tile_live(const Rec& r, int ts, int tx, int ty) {
+  return !conic_box_culled(r, double(tx) * ts, double(tx + 1) * ts, double(ty) * ts, double(ty + 1) * ts);
+}
+__host__ __device__ inline uint32_t cross_tile_count(const Rec& r, int ts, int tiles_x, int tiles_y) {
+  if (!cross_screen_live(r, ts, tiles_x, tiles_y)) return 0;
+  uint32_t k = 0;
+  for (int ty = 0; ty < tiles_y; ++ty) {
+    if (!cross_row_live(r, ts, tiles_x, ty)) continue;
+    for (int tx = 0; tx < tiles_x; ++tx) k += cross_tile_live(r, ts, tx, ty);
+  }
+  return k;
 }
 
 // Orderable 64-bit key of a double (ascending), with -0 folded onto +0 so that

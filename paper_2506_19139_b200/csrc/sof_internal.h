@@ -105,9 +105,14 @@ struct Binding {
   // live lists only: the gauss_behind Gaussians (sof_device.cuh), which the reference
   // lists in every tile ahead of everything else and which never contribute: left out of
   // the lists, sorted by (min_z key, index) here, and counted by the evaluation
+  // Since round 2 the list also holds the live Gaussians whose box crosses the camera
+  // plane (listed by the reference in every tile): they are listed only in the tiles
+  // whose points they may reach (cross_tile_live), at the list positions xpos.
   int64_t nb = 0;
   DBuf<uint64_t> bkey;  // double_key(min_z)
-  DBuf<int32_t> bidx;
+  DBuf<int32_t> bidx;   // 2 g (a truncated binding: 2 row, or 2 row - 1 between rows)
+  int64_t nx = 0;
+  DBuf<int64_t> xpos;   // ascending positions in ent of listed crossing Gaussians
 };
 
 // Scratch of the per-view point schedule (schedule_points tiles.hpp:29-84).
@@ -166,7 +171,7 @@ struct GroupScratch {
 struct BisectScratch {
   DBuf<unsigned long long> zmax;
   DBuf<int64_t> len, toff;
-  DBuf<uint8_t> used;
+  DBuf<uint8_t> used, rflag;  // rflag: count flag (k_field.cu kCountCross) per compact row
   DBuf<int32_t> flag, pos;
   DBuf<int> bail;
 };
@@ -292,6 +297,7 @@ struct sof_ctx {
   int64_t n_contrib = -1;
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<char> scan_tmp;                 // block totals of the hand-written scans (k_scan.cu)
+  sofk::DBuf<int64_t> sel_cnt, sel_off;      // k_cross_sel block counts / offsets
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
   sofk::Comm* comm = nullptr;                 // multi-GPU: owned communicator (sof_comm_init)
   sofk::DBuf<int32_t> shard_i32, shard_send, shard_recv, shard_all;  // sharded-step scratch
