@@ -117,6 +117,9 @@ typedef struct sof_extract_stats {
   double host_ms_prep;       /* host time spent issuing per-view prep (incl. its one sync) */
   double host_ms_sched;      /* host time spent issuing per-view scheduling */
   uint64_t contrib_pairs;    /* FP64-evaluated pairs with alpha >= 1/255; 0 unless SOF_EVAL_STATS */
+  uint64_t scanned_pairs;    /* list entries the evaluation kernels scanned in views that have Gaussians
+                                counted without listing (behind / crossing the camera plane), which
+                                `pairs` includes; 0 when no view has any */
 } sof_extract_stats;
 
 /* ---- context --------------------------------------------------------------- */

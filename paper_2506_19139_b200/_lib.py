@@ -44,7 +44,8 @@ class ExtractStats(ctypes.Structure):
                 ("ms_label", _D), ("ms_march", _D), ("ms_refine", _D), ("ms_weld", _D),
                 ("ms_eval_kernel", _D), ("eval_launches", _I64), ("kernel_launches", _I64),
                 ("ms_prep", _D), ("ms_sched", _D), ("exact_pairs", ctypes.c_uint64),
-                ("host_ms_prep", _D), ("host_ms_sched", _D), ("contrib_pairs", ctypes.c_uint64)]
+                ("host_ms_prep", _D), ("host_ms_sched", _D), ("contrib_pairs", ctypes.c_uint64),
+                ("scanned_pairs", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -145,7 +146,12 @@ def load() -> ctypes.CDLL:
                           "(this package has no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():
-        fn = getattr(lib, name)
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            if os.environ.get("SOF_LIB_PATH"):  # an older build loaded for A/B timing
+                continue
+            raise
         fn.restype = res
         fn.argtypes = args
     _lib = lib

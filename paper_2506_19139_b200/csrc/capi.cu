@@ -573,6 +573,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     c->eval_launches = 0;
     c->exact_evals = 0;
     c->contrib_evals = 0;
+    c->scanned_evals = 0;
     c->host_ms[0] = c->host_ms[1] = 0.0;
     c->time_eval = stats != nullptr && o.profile != 0;
     if (c->time_eval) {
@@ -637,6 +638,7 @@ int sof_extract(sof_ctx* c, const sof_extract_opts* opts, sof_extract_stats* sta
     st.ms_prep = pms[kProfPrep];
     st.exact_pairs = c->exact_evals;
     st.contrib_pairs = c->contrib_evals;
+    st.scanned_pairs = c->scanned_evals;
     st.host_ms_prep = c->host_ms[0];
     st.host_ms_sched = c->host_ms[1];
     st.ms_sched = pms[kProfSched];

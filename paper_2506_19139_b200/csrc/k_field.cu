@@ -106,6 +106,11 @@ __global__ void k_view_rec(int64_t n, const GaussStatic* __restrict__ g, Cam cam
 // evaluation does not count them twice.
 constexpr uint8_t kCountBehind = 1, kCountCross = 2;
 
+// cross_tile_count out of line (rare; keeps the rect kernels' register count)
+__device__ __noinline__ uint32_t cross_tile_count_ni(const Rec* __restrict__ r, int ts, int tiles_x, int tiles_y) {
+  return cross_tile_count(*r, ts, tiles_x, tiles_y);
+}
+
 // Per-view binning inputs of k_tile_rect, produced by the record kernel in the same
 // pass over GaussStatic when the binding of the view is built right away.
 struct RectOut {
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(128, SOF_REC_MINB) k_view_rec_rect(int64_t n, 
   bool crosses = false;
   if (!(ro.live_only && (r.op < kMinAlpha || behind)) &&
       tile_rect(gs, cam, ro.ts, ro.tiles_x, ro.tiles_y, tx0, tx1, ty0, ty1, &crosses)) {
-    count = (live && crosses) ? cross_tile_count(r, ro.ts, ro.tiles_x, ro.tiles_y)
+    count = (live && crosses) ? cross_tile_count_ni(out + i, ro.ts, ro.tiles_x, ro.tiles_y)
                               : uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     ro.rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
@@ -250,7 +255,7 @@ __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
   bool crosses = false;
   if (!(live_only && (rec[i].op < kMinAlpha || behind)) &&
       tile_rect(g[i], cam, ts, tiles_x, tiles_y, tx0, tx1, ty0, ty1, &crosses)) {
-    count = (live && crosses) ? cross_tile_count(rec[i], ts, tiles_x, tiles_y)
+    count = (live && crosses) ? cross_tile_count_ni(rec + i, ts, tiles_x, tiles_y)
                               : uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
@@ -294,8 +299,7 @@ __device__ __forceinline__ void emit_cross_warp(const Rec& r, int32_t g, int64_t
 __global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
                                const int4* __restrict__ rect, const uint32_t* __restrict__ cnt,
                                const int64_t* __restrict__ off, int tiles_x, uint32_t* keys,
-                               int32_t* vals, const uint8_t* __restrict__ gflag, const Rec* __restrict__ rec,
-                               int ts, int tiles_y) {
+                               int32_t* vals, const uint8_t* __restrict__ gflag) {
   constexpr uint32_t kOwn = 16;  // entries written by the owning thread
   const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -310,16 +314,8 @@ __global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
     if (count) {
       rc = rect[g];
       base = off[r];
-      cross = gflag && gflag[g] == kCountCross;
+      cross = gflag && gflag[g] == kCountCross;  // emitted by k_emit_cross
     }
-  }
-  unsigned xb = __ballot_sync(0xffffffffu, cross);
-  while (xb) {
-    const int src = __ffs(xb) - 1;
-    xb &= xb - 1;
-    const int32_t bg = __shfl_sync(0xffffffffu, g, src);
-    const int64_t bb = __shfl_sync(0xffffffffu, base, src);
-    emit_cross_warp(rec[bg], bg, bb, ts, tiles_x, tiles_y, keys, vals);
   }
   if (cross) count = 0;
   {  // row-major walk of the first kOwn tiles of the rectangle (no divisions)
@@ -350,6 +346,28 @@ __global__ void k_emit_entries(int64_t n, const int32_t* __restrict__ order,
       keys[bb + k] = uint32_t(ty * tiles_x + tx);
       vals[bb + k] = bg;
     }
+  }
+}
+
+// The live crossing Gaussians' entries (the slots k_emit_entries left to it).
+__global__ void k_emit_cross(int64_t n, const int32_t* __restrict__ order, const uint32_t* __restrict__ cnt,
+                             const int64_t* __restrict__ off, const uint8_t* __restrict__ gflag,
+                             const Rec* __restrict__ rec, int ts, int tiles_x, int tiles_y, uint32_t* keys,
+                             int32_t* vals) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  int32_t g = -1;
+  bool cross = false;
+  if (r < n) {
+    g = order[r];
+    cross = cnt[g] != 0 && gflag[g] == kCountCross;
+  }
+  unsigned xb = __ballot_sync(0xffffffffu, cross);
+  while (xb) {
+    const int src = __ffs(xb) - 1;
+    xb &= xb - 1;
+    const int32_t bg = __shfl_sync(0xffffffffu, g, src);
+    const int64_t rr = __shfl_sync(0xffffffffu, r, src);
+    emit_cross_warp(rec[bg], bg, off[rr], ts, tiles_x, tiles_y, keys, vals);
   }
 }
 
@@ -693,9 +711,17 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
                                                                        c->zkey_in.p, c->bin_zmax, tiles_x,
                                                                        c->ekey_in.p, c->eval_in.p, gflag, rec, ts);
     else
+    {
       k_emit_entries<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(c->bin_m, c->gidx_out.p, c->rect.p, c->gcount.p,
                                                                       c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p,
-                                                                      gflag, rec, ts, tiles_y);
+                                                                      b.nb > 0 ? gflag : nullptr);
+      if (gflag && b.nb > 0) {
+        k_emit_cross<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(c->bin_m, c->gidx_out.p, c->gcount.p, c->goff.p,
+                                                                      gflag, rec, ts, tiles_x, tiles_y, c->ekey_in.p,
+                                                                      c->eval_in.p);
+        SOF_LAUNCHED(c);
+      }
+    }
     SOF_LAUNCHED(c);
     // stable sort by tile keeps the (min_z, index) order inside every tile list
     sort_pairs_u32(c, c->ekey_in.p, c->ekey_out.p, c->eval_in.p, b.ent.p, M, bits_for(T));
@@ -1117,7 +1143,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
   double survive = 1.0;
   bool complete = true;
   bool done = !active;
-  unsigned pairs = 0, exact = 0, contrib = 0;
+  unsigned pairs = 0, exact = 0, contrib = 0, scanned = 0;
   for (int q = threadIdx.x; q < 128; q += blockDim.x) s_exp[q] = kSofExpTabDev[q];
   if constexpr (FAST) {
     const int32_t* lp = lent + l0;
@@ -1148,6 +1174,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
       return p;
     };
     pairs += stream_list<STAGE>(lp, len, recs, &tmap, srec, s_bar, done, eval_chunk);
+    scanned = pairs;
     if (active) pairs += count_pairs(bh, stop >= 0, stop_key, stop_idx, pr.zp, l0, pairs);
   } else {
     for (int64_t base = l0; base < l1; base += kChunk) {
@@ -1212,6 +1239,11 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval(
     if (q) atomicAdd(pairs_counter + 1, q);
     if (e) atomicAdd(pairs_counter + 2, e);
     if (w) atomicAdd(pairs_counter + 3, w);
+  }
+  if (FAST && bh.n > 0) {  // views with counted Gaussians: the list entries actually scanned
+    unsigned long long sc = scanned;
+    for (int s = 16; s > 0; s >>= 1) sc += __shfl_down_sync(0xffffffffu, sc, s);
+    if ((threadIdx.x & 31) == 0 && sc) atomicAdd(pairs_counter + 4, sc);
   }
 }
 
@@ -1514,10 +1546,15 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
     return p;
   };
   pairs += stream_list<STAGE>(lp, int(l1 - l0), recs, tmap, srec, s_bar, done, eval_chunk);
+  unsigned long long sc = pairs;
   if (active) pairs += count_pairs(bh, stop >= 0, stop_key, stop_idx, pr.zp, l0, pairs);
   if (active) {
     item_pairs[item] = pairs;
     item_ext[item] = (complete && 1.0 - survive < 0.5) ? 1 : 0;
+  }
+  if (bh.n > 0) {  // views with counted Gaussians: the list entries actually scanned
+    for (int s = 16; s > 0; s >>= 1) sc += __shfl_down_sync(0xffffffffu, sc, s);
+    if ((threadIdx.x & 31) == 0 && sc) atomicAdd(counters + 4, sc);
   }
   if (SOF_EVAL_STATS) {
     unsigned long long e = exact, w = contrib;
@@ -1637,9 +1674,9 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
   g.item_pairs.ensure(int64_t(G) * n);
   g.item_ext.ensure(int64_t(G) * n);
   g.order.ensure(int64_t(G) * n);
-  c->d_counters.ensure(4);
+  c->d_counters.ensure(5);
   c->d_scalar.ensure(4);
-  zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 4);
+  zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 5);
   const bool prune = strategies & 8, early = strategies & 4;
   const int64_t* const* loffs = reinterpret_cast<const int64_t* const*>(g.ptrs.p);
   const int32_t* const* lents = reinterpret_cast<const int32_t* const*>(g.ptrs.p + V);
@@ -1704,13 +1741,14 @@ static bool classify_grouped_run(sof_ctx* c, int v0, int v1, int64_t n, const do
     SOF_LAUNCHED(c);
   }
   if (counters_host) {
-    unsigned long long h[4];
+    unsigned long long h[5];
     SOF_CUDA(cudaMemcpyAsync(h, c->d_counters.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     SOF_CUDA(cudaStreamSynchronize(c->stream));
     counters_host[0] += h[0];
     counters_host[1] += h[1];
     c->exact_evals += h[2];
     c->contrib_evals += h[3];
+    c->scanned_evals += h[4];
   }
   return true;
 }
@@ -1962,11 +2000,16 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
       size_t total_b = 0;
       SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
     }
-    const size_t need = size_t(R) * sizeof(Rec) + size_t(L) * 4 + size_t(T + 1) * 8;
+    // DBuf::ensure over-allocates by 1/8; the per-view path that serves the views past
+    // this point needs its own scratch (records + binning of one view) on top
+    const size_t need = (size_t(R) * sizeof(Rec) + size_t(L) * 4 + size_t(T + 1) * 8 +
+                         size_t(full.nb) * 12 + size_t(full.nx) * 8) * 9 / 8 + (size_t(1) << 22);
+    const size_t headroom = std::max<size_t>(size_t(4) << 30, size_t(n) * 384);
     Binding& b = c->bindings[v];
-    const size_t have = c->recs[v].bytes() + b.ent.bytes() + b.off.bytes();
+    const size_t have = c->recs[v].bytes() + b.ent.bytes() + b.off.bytes() + b.bkey.bytes() + b.bidx.bytes() +
+                        b.xpos.bytes();
     if (need > have) {
-      if (need - have + (size_t(2) << 30) > free_b) {  // out of memory: per-view path from here
+      if (need - have + headroom > free_b) {  // out of memory: per-view path from here
         if (std::getenv("SOF_DEBUG_HOST"))
           std::fprintf(stderr, "bisect_cache_views: out of memory at view %d (free %.1f GB, need %.2f GB)\n", v,
                        free_b / 1e9, need / 1e9);
@@ -2080,9 +2123,9 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   if (mode == kModeClassify &&
       classify_grouped(c, v0, v1, n, xyz, strategies, tile_size, ext, counters_host))
     return;
-  c->d_counters.ensure(4);
+  c->d_counters.ensure(5);
   c->d_scalar.ensure(4);
-  zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 4);
+  zero_async(c, c->d_counters.p, int64_t(sizeof(unsigned long long)) * 5);
   PointSchedule& s = c->sched;
   if (mode == kModeView && n > 0) {
     k_fill_view_outputs<<<grid_for(n, 256), 256, 0, c->stream>>>(n, o_out, obs_out, comp_out);
@@ -2154,9 +2197,15 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     prof_span(c, p1, prof_mark(c), kProfSched);
     c->host_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();
   };
-  auto prep_view = [&](int pv) {
+  auto swap_lane = [&]() {  // the prep lane's stream and scratch (CUB, the hand-written scans, k_cross_sel)
     std::swap(c->stream, c->stream2);
     c->cub_tmp.swap(c->cub_tmp2);
+    c->scan_tmp.swap(c->scan_tmp2);
+    c->sel_cnt.swap(c->sel_cnt2);
+    c->sel_off.swap(c->sel_off2);
+  };
+  auto prep_view = [&](int pv) {
+    swap_lane();
     c->scratch_sel = pv & 1;
     try {
       // scratch slot pv & 1 may still hold the records / tile lists of view pv - 2 (past
@@ -2175,12 +2224,10 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
       }
       SOF_CUDA(cudaEventRecord(c->prep_ev[pv & 1], c->stream));
     } catch (...) {
-      std::swap(c->stream, c->stream2);
-      c->cub_tmp.swap(c->cub_tmp2);
+      swap_lane();
       throw;
     }
-    std::swap(c->stream, c->stream2);
-    c->cub_tmp.swap(c->cub_tmp2);
+    swap_lane();
   };
   const bool dbg = std::getenv("SOF_DEBUG_HOST") != nullptr;
   const auto hd0 = std::chrono::steady_clock::now();
@@ -2263,13 +2310,14 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     std::fprintf(stderr, "    all views issued at %8.2f ms\n",
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hd0).count());
   if (counters_host) {
-    unsigned long long h[4];
+    unsigned long long h[5];
     SOF_CUDA(cudaMemcpyAsync(h, c->d_counters.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     SOF_CUDA(cudaStreamSynchronize(c->stream));
     counters_host[0] += h[0];
     counters_host[1] += h[1];
     c->exact_evals += h[2];
     c->contrib_evals += h[3];
+    c->scanned_evals += h[4];
   }
 }
 

@@ -68,7 +68,15 @@ struct DBuf {
       p = nullptr;
       cap = 0;
       const size_t want = count + count / 8 + 16;
-      SOF_CUDA(cudaMalloc(&p, want * sizeof(T)));
+      const cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+      if (e == cudaErrorMemoryAllocation) {
+        (void)cudaGetLastError();
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        throw ::sofk::OomError("CUDA out of memory: a " + std::to_string(want * sizeof(T) >> 20) +
+                               " MiB buffer with " + std::to_string(fr >> 20) + " MiB free");
+      }
+      SOF_CUDA(e);
       cap = want;
     }
     n = count;
@@ -241,6 +249,7 @@ struct sof_ctx {
   int staging = 0;                        // fast-loop record staging: 0 plain loads, 1 TMA gather4
   uint64_t exact_evals = 0;               // pairs that took the FP64 path (instrumentation)
   uint64_t contrib_evals = 0;             // ... of which contributed (alpha >= 1/255)
+  uint64_t scanned_evals = 0;             // list entries the evaluation kernels scanned (their work)
   double host_ms[4] = {0, 0, 0, 0};       // host time in per-view prep / scheduling (instrumentation)
 
   // prep lane: a second stream (+ its own CUB scratch) for per-view preprocessing
@@ -297,7 +306,10 @@ struct sof_ctx {
   int64_t n_contrib = -1;
   sofk::DBuf<char> cub_tmp;
   sofk::DBuf<char> scan_tmp;                 // block totals of the hand-written scans (k_scan.cu)
-  sofk::DBuf<int64_t> sel_cnt, sel_off;      // k_cross_sel block counts / offsets
+  sofk::DBuf<int64_t> sel_cnt, sel_off;      // compaction block counts / offsets (k_sort.cu, k_cross_sel)
+  // the prep lane's own copies (swapped in while it issues work on stream2)
+  sofk::DBuf<char> scan_tmp2;
+  sofk::DBuf<int64_t> sel_cnt2, sel_off2;
   sofk::DBuf<unsigned long long> d_counters;  // [0] pairs
   sofk::Comm* comm = nullptr;                 // multi-GPU: owned communicator (sof_comm_init)
   sofk::DBuf<int32_t> shard_i32, shard_send, shard_recv, shard_all;  // sharded-step scratch

@@ -54,6 +54,15 @@ def main():
         sof.extract_resident(ctx, sof.ExtractOptions(profile=True), st, fetch=False)
     print({k: st[k] for k in ("ms_label", "ms_refine", "ms_eval_kernel", "ms_prep", "ms_sched", "exact_pairs", "contrib_pairs", "point_view_evals", "host_ms_prep",
                                "host_ms_sched", "pairs", "crossing_edges", "kernel_launches")})
+    import time
+    walls = []
+    for _ in range(args.steps):  # unprofiled steps (no per-launch events): wall time
+        t0 = time.perf_counter()
+        st = {}
+        sof.extract_resident(ctx, sof.ExtractOptions(), st, fetch=False)
+        walls.append((time.perf_counter() - t0) * 1e3)
+    print("unprofiled step ms:", [round(w, 1) for w in walls], "label", round(st["ms_label"], 1), "refine",
+          round(st["ms_refine"], 1))
 
 
 if __name__ == "__main__":
