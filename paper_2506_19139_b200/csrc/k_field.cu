@@ -2001,10 +2001,10 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
       SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
     }
     // DBuf::ensure over-allocates by 1/8; the per-view path that serves the views past
-    // this point needs its own scratch (records + binning of one view) on top
+    // this point needs headroom for the buffers it may still grow
     const size_t need = (size_t(R) * sizeof(Rec) + size_t(L) * 4 + size_t(T + 1) * 8 +
                          size_t(full.nb) * 12 + size_t(full.nx) * 8) * 9 / 8 + (size_t(1) << 22);
-    const size_t headroom = std::max<size_t>(size_t(4) << 30, size_t(n) * 384);
+    const size_t headroom = (size_t(2) << 30) + size_t(n) * 64;
     Binding& b = c->bindings[v];
     const size_t have = c->recs[v].bytes() + b.ent.bytes() + b.off.bytes() + b.bkey.bytes() + b.bidx.bytes() +
                         b.xpos.bytes();

@@ -4,5 +4,5 @@
 for rep in 1 2; do for spec in "$@"; do
   v="${spec%%:*}"; envs=""; [ "$spec" != "$v" ] && envs="${spec#*:}"
   echo "== variant '$spec' rep $rep"
-  env $envs SOF_LIB_PATH=$PWD/paper_2506_19139_b200/libsof_cuda$v.so python tools/profile_case.py --views 200 --steps 2
+  env $envs SOF_LIB_PATH=$PWD/paper_2506_19139_b200/libsof_cuda$v.so python tools/profile_case.py --views 200 --steps 2 --timed 2
 done; done

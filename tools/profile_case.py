@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--lattice", type=int, default=0, help="override the config's lattice size")
     ap.add_argument("--render", action="store_true", help="render one view instead of meshing")
+    ap.add_argument("--timed", type=int, default=0, help="also time this many unprofiled steps (wall clock)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     scene = synthetic_scene(cfg["gaussians"], int(args.config[1:]))
@@ -56,13 +57,14 @@ def main():
                                "host_ms_sched", "pairs", "crossing_edges", "kernel_launches")})
     import time
     walls = []
-    for _ in range(args.steps):  # unprofiled steps (no per-launch events): wall time
+    for _ in range(args.timed):  # unprofiled steps (no per-launch events): wall time
         t0 = time.perf_counter()
         st = {}
         sof.extract_resident(ctx, sof.ExtractOptions(), st, fetch=False)
         walls.append((time.perf_counter() - t0) * 1e3)
-    print("unprofiled step ms:", [round(w, 1) for w in walls], "label", round(st["ms_label"], 1), "refine",
-          round(st["ms_refine"], 1))
+    if walls:
+        print("unprofiled step ms:", [round(w, 1) for w in walls], "label", round(st["ms_label"], 1), "refine",
+              round(st["ms_refine"], 1))
 
 
 if __name__ == "__main__":
