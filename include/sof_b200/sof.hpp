@@ -440,7 +440,7 @@ inline Mesh assemble_mesh(const std::vector<Vec3>& vertices, const std::vector<s
 }
 
 // delaunay_tetrahedralize (delaunay.hpp:52-142): the reference's Bowyer-Watson tet list,
-// bit for bit (sof_tetrahedralize, the host stage of the tetra-input producer).
+// bit for bit (sof_tetrahedralize: the reference's insertion sequence on the device).
 inline TetGrid delaunay_tetrahedralize(const std::vector<Vec3>& points, sof_ctx* c = nullptr) {
   if (!c) c = detail::default_ctx().get();
   const std::vector<double> p = detail::flat(points);
@@ -526,7 +526,7 @@ inline Mesh extract_mesh(const std::vector<GaussianPrimitive>& /*gaussians*/, co
 }
 
 // extract_mesh (extract.hpp:35-86) with the reference's signature: the seeds
-// (build_seed_points, device) and their Delaunay tetrahedralization (host, the
+// (build_seed_points, device) and their Delaunay tetrahedralization (device, the
 // reference's tet list exactly) feed the fused device pipeline. `gaussians` must be the
 // scene the ViewSet was built from (it is resident on the device); the pool argument is
 // accepted and ignored (the GPU grid replaces it).

@@ -314,12 +314,13 @@ int sof_comm_info(const sof_ctx* ctx, int* nranks, int* rank);
 int sof_comm_destroy(sof_ctx* ctx);
 
 /* ---- the tetra-input producer ------------------------------------ */
-/* delaunay_tetrahedralize (delaunay.hpp:52-142) of n points on the HOST: the reference's
- * incremental Bowyer-Watson (same enclosing tetrahedron, in-circumsphere slack, cavity
- * re-closing order and arithmetic), so the tet list — and the mesh numbering MT derives
- * from it — is the reference's. O(n^2): small seed sets. *n_tets = T; tets via
- * sof_copy_result(SOF_R_TETS). Errors: "need at least 4 points", "degenerate (coplanar)
- * point set". */
+/* delaunay_tetrahedralize (delaunay.hpp:52-142) of n points (host array) on the device:
+ * the reference's incremental Bowyer-Watson in its insertion sequence (same enclosing
+ * tetrahedron, in-circumsphere slack, cavity re-closing order and arithmetic), each
+ * insertion parallel inside one persistent cooperative kernel, so the tet list — and the
+ * mesh numbering MT derives from it — is the reference's. O(n^2) work like the reference:
+ * seed sets up to ~10^5 points. *n_tets = T; tets via sof_copy_result(SOF_R_TETS).
+ * Errors: "need at least 4 points", "degenerate (coplanar) point set". */
 int sof_tetrahedralize(sof_ctx* ctx, int64_t n, const double* pts, int64_t* n_tets);
 
 /* ---- results ------------------------------------------------------------------------ */

@@ -460,6 +460,23 @@ void* sofref_extract_tetgrid(sofref_ctx* c, long nv, const double* xyz, long nt,
 
 /// build_seed_points + delaunay_tetrahedralize (seed_points.hpp:41-87, delaunay.hpp:52-142):
 /// the reference's own tetra-input producer, for small scenes.
+/// delaunay_tetrahedralize (delaunay.hpp:52-142) of arbitrary points -> bag{tets:int32}
+void* sofref_delaunay(long n, const double* xyz) {
+  try {
+    std::vector<Vec3> pts(size_t(std::max(n, 0L)));
+    for (long i = 0; i < n; ++i) pts[size_t(i)] = Vec3(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+    const TetGrid grid = delaunay_tetrahedralize(pts);
+    auto* bag = new Bag;
+    std::vector<int32_t> tt;
+    for (const auto& x : grid.tetrahedra) tt.insert(tt.end(), x.begin(), x.end());
+    bag->put("tets", tt);
+    return bag;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
 void* sofref_seed_delaunay(const sofref_ctx* c, int bounding, int cutoff) {
   try {
     const SeedPointSet seeds = build_seed_points(c->gaussians, BoundingVariant(bounding),

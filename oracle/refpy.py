@@ -167,6 +167,8 @@ class RefLib:
         L.sofref_collect_contributions.argtypes = [_P, _I, _I, _I]
         L.sofref_render_pixels_windowed.argtypes = [_P, _I, _I, _L, _L, _P, _P, _P, _P, _P, _P]
         L.sofref_windowed_resort.argtypes = [_L, _P, _P, _L, _P]
+        L.sofref_delaunay.restype = _P
+        L.sofref_delaunay.argtypes = [_L, _P]
         L.sofref_render_pixel_lists.argtypes = [_P, _I, _L, _P, _P, _P, _P, _P, _P, _P]
 
     # ---- fixtures ----
@@ -183,6 +185,14 @@ class RefLib:
         out = np.empty(len(t), np.int32)
         self.lib.sofref_windowed_resort(len(t), _ptr(t), _ptr(i), int(window), _ptr(out))
         return out
+
+    def delaunay(self, xyz) -> np.ndarray:
+        """delaunay_tetrahedralize (delaunay.hpp:52-142) of arbitrary points: tets [T, 4]."""
+        xyz = np.ascontiguousarray(xyz, np.float64).reshape(-1, 3)
+        h = self.lib.sofref_delaunay(len(xyz), _ptr(xyz))
+        if not h:
+            raise ValueError(self.lib.sofref_last_error().decode())
+        return self._bag(h, {"tets": np.int32})["tets"].reshape(-1, 4)
 
     def random_scene(self, seed: int, count: int, extent: float = 1.0) -> Scene:
         s = Scene.empty(count)

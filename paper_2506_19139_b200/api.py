@@ -431,7 +431,7 @@ def assemble_mesh(vertices, triangles, residuals=None, weld_eps: float = 1e-7, m
 
 def delaunay_tetrahedralize(points, ctx: Context | None = None) -> TetGrid:
     """delaunay_tetrahedralize (delaunay.hpp:52-142): the reference's Bowyer-Watson tet
-    list (host stage of the tetra-input producer, sof_tetrahedralize)."""
+    list in the reference's order, on the device (sof_tetrahedralize)."""
     ctx = ctx or default_context()
     p = _f64(points, 3)
     nt = ctypes.c_int64()
@@ -443,7 +443,7 @@ def extract_mesh(gaussians, views: ViewSet, grid: TetGrid | None = None, opt: Ex
                  stats: dict | None = None, bounding: int = L.SEED_STP, cutoff: int = L.SEED_CUT_DEAD) -> Mesh:
     """extract_mesh (extract.hpp:35-86). With `grid`: label -> march -> refine -> weld on
     the given tetra input, fused on the device. Without: the reference's own producer
-    first — build_seed_points (device) and delaunay_tetrahedralize (host), with the
+    first — build_seed_points and delaunay_tetrahedralize (both on the device), with the
     reference's defaults (BoundingVariant::kStp, SeedCutoff::kDeadGaussians)."""
     opt = opt or ExtractOptions()
     ctx = views.ctx

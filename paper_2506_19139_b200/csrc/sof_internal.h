@@ -331,6 +331,7 @@ struct sof_ctx {
   int64_t n_edges = -1, n_march_tris = -1, mesh_nv = -1, mesh_nt = -1, grid_n = -1;
   int64_t mesh_nres = -1;                // residuals of the last weld (-1: none)
   std::vector<int32_t> delaunay_tets;    // sof_tetrahedralize result (host, 4 per tet)
+  sofk::DBuf<char> dl_buf;               // device Delaunay: points, tets (x2), cavity, faces
   sofk::DBuf<double> m_res, res_in;      // welded / pre-weld residuals
   sofk::DBuf<double> grid_opacity;
   sofk::DBuf<int32_t> r_edges, r_tris, m_tris;

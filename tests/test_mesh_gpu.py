@@ -349,3 +349,34 @@ def test_tetrahedralize_errors(ref):
         sof.delaunay_tetrahedralize(np.zeros((3, 3)), ctx)
     with pytest.raises(ValueError, match="degenerate"):
         sof.delaunay_tetrahedralize(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0], [2, 3, 0.0]]), ctx)
+
+
+def _sphere_points(n, seed):
+    rng = np.random.default_rng(seed)
+    d = rng.normal(size=(n, 3))
+    return d / np.linalg.norm(d, axis=1, keepdims=True)
+
+
+@pytest.mark.parametrize("case", ["random50", "random3000", "lattice6", "sphere400", "clustered", "uniform10k"])
+def test_device_delaunay_matches_reference(ref, case):
+    """sof_tetrahedralize (the device Bowyer-Watson) returns the reference's tet list
+    (delaunay.hpp:52-142) in the reference's order, on random, cospherical (lattice,
+    sphere) and clustered point sets."""
+    rng = np.random.default_rng(7)
+    if case == "random50":
+        pts = rng.random((50, 3))
+    elif case == "random3000":
+        pts = rng.normal(size=(3000, 3))
+    elif case == "lattice6":
+        pts = np.stack(np.meshgrid(*[np.arange(6.0)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    elif case == "sphere400":
+        pts = _sphere_points(400, 3)
+    elif case == "uniform10k":
+        pts = rng.random((10000, 3))
+    else:
+        # two scales 10^4 apart (the reference's slivers and holes; it slows down
+        # super-linearly on such sets, so a small one)
+        pts = np.concatenate([rng.normal(scale=1e-3, size=(40, 3)), rng.normal(scale=10.0, size=(40, 3))])
+    want = ref.delaunay(pts)
+    got = sof.delaunay_tetrahedralize(pts, sof.Context(0))
+    np.testing.assert_array_equal(got.tetrahedra, want)
