@@ -430,7 +430,38 @@ __device__ __forceinline__ bool tile_wanted(const unsigned long long* zmax, int6
   return zmax[t] >= zk;  // zmax 0: no segment reaches t (every key is >= 1)
 }
 
-// (live crossing Gaussians: only their cross_tile_live tiles, as k_emit_entries)
+// (live crossing Gaussians: only their cross_tile_live tiles, as k_emit_entries; in their
+// own kernels, so the common path keeps its register count)
+__device__ __forceinline__ uint32_t filtered_cross_count(const Rec* __restrict__ rp, int4 rc,
+                                                      const unsigned long long* __restrict__ zmax, int tiles_x,
+                                                      unsigned long long zk, int ts) {
+  const Rec r = *rp;
+  uint32_t k = 0;
+  for (int ty = rc.z; ty <= rc.w; ++ty) {
+    if (!cross_row_live(r, ts, tiles_x, ty)) continue;
+    for (int tx = rc.x; tx <= rc.y; ++tx)
+      k += tile_wanted(zmax, int64_t(ty) * tiles_x + tx, zk) && cross_tile_live(r, ts, tx, ty);
+  }
+  return k;
+}
+
+__device__ __forceinline__ void filtered_cross_emit(const Rec* __restrict__ rp, int32_t g, int4 rc, int64_t o,
+                                                 const unsigned long long* __restrict__ zmax, int tiles_x,
+                                                 unsigned long long zk, int ts, uint32_t* keys, int32_t* vals) {
+  const Rec r = *rp;
+  for (int ty = rc.z; ty <= rc.w; ++ty) {
+    if (!cross_row_live(r, ts, tiles_x, ty)) continue;
+    for (int tx = rc.x; tx <= rc.y; ++tx) {
+      const int64_t t = int64_t(ty) * tiles_x + tx;
+      if (tile_wanted(zmax, t, zk) && cross_tile_live(r, ts, tx, ty)) {
+        keys[o] = uint32_t(t);
+        vals[o] = g;
+        ++o;
+      }
+    }
+  }
+}
+
 __global__ void k_filter_counts(int64_t n, const int4* __restrict__ rect, const uint64_t* __restrict__ zkey,
                                 const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* cnt,
                                 const uint8_t* __restrict__ gflag, const Rec* __restrict__ rec, int ts) {
@@ -438,13 +469,10 @@ __global__ void k_filter_counts(int64_t n, const int4* __restrict__ rect, const 
   if (g >= n || cnt[g] == 0) return;
   const int4 rc = rect[g];
   const unsigned long long zk = zkey[g];
-  const bool cross = gflag && gflag[g] == kCountCross;
+  if (gflag && gflag[g] == kCountCross) return;  // k_filter_counts_cross
   uint32_t k = 0;
-  for (int ty = rc.z; ty <= rc.w; ++ty) {
-    if (cross && !cross_row_live(rec[g], ts, tiles_x, ty)) continue;
-    for (int tx = rc.x; tx <= rc.y; ++tx)
-      k += tile_wanted(zmax, int64_t(ty) * tiles_x + tx, zk) && (!cross || cross_tile_live(rec[g], ts, tx, ty));
-  }
+  for (int ty = rc.z; ty <= rc.w; ++ty)
+    for (int tx = rc.x; tx <= rc.y; ++tx) k += tile_wanted(zmax, int64_t(ty) * tiles_x + tx, zk);
   cnt[g] = k;
 }
 
@@ -458,19 +486,37 @@ __global__ void k_emit_filtered(int64_t n, const int32_t* __restrict__ order, co
   const int32_t g = order[r];
   const int4 rc = rect[g];
   const unsigned long long zk = zkey[g];
-  const bool cross = gflag && gflag[g] == kCountCross;
   int64_t o = off[r];
-  for (int ty = rc.z; ty <= rc.w; ++ty) {
-    if (cross && !cross_row_live(rec[g], ts, tiles_x, ty)) continue;
+  if (gflag && gflag[g] == kCountCross) return;  // k_emit_filtered_cross
+  for (int ty = rc.z; ty <= rc.w; ++ty)
     for (int tx = rc.x; tx <= rc.y; ++tx) {
       const int64_t t = int64_t(ty) * tiles_x + tx;
-      if (tile_wanted(zmax, t, zk) && (!cross || cross_tile_live(rec[g], ts, tx, ty))) {
+      if (tile_wanted(zmax, t, zk)) {
         keys[o] = uint32_t(t);
         vals[o] = g;
         ++o;
       }
     }
-  }
+}
+
+__global__ void k_filter_counts_cross(int64_t n, const int4* __restrict__ rect, const uint64_t* __restrict__ zkey,
+                                      const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* cnt,
+                                      const uint8_t* __restrict__ gflag, const Rec* __restrict__ rec, int ts) {
+  const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (g >= n || cnt[g] == 0 || gflag[g] != kCountCross) return;
+  cnt[g] = filtered_cross_count(rec + g, rect[g], zmax, tiles_x, zkey[g], ts);
+}
+
+__global__ void k_emit_filtered_cross(int64_t n, const int32_t* __restrict__ order, const int4* __restrict__ rect,
+                                      const int64_t* __restrict__ off, const uint64_t* __restrict__ zkey,
+                                      const unsigned long long* __restrict__ zmax, int tiles_x, uint32_t* keys,
+                                      int32_t* vals, const uint8_t* __restrict__ gflag, const Rec* __restrict__ rec,
+                                      int ts) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  const int32_t g = order[r];
+  if (gflag[g] != kCountCross) return;
+  filtered_cross_emit(rec + g, g, rect[g], off[r], zmax, tiles_x, zkey[g], ts, keys, vals);
 }
 
 // Positions i in [0, M) of a tile-list array whose entry is a kCountCross Gaussian
@@ -593,8 +639,14 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
   if (c->bin_zmax) {  // bisection-cache binning: only the reachable (tile, depth) entries
     k_filter_counts<<<grid_for(n, 256), 256, 0, c->stream>>>(n, c->rect.p, c->zkey_in.p, c->bin_zmax, tiles_x,
                                                              c->gcount.p, b.live ? c->gbehind.p : nullptr,
-                                                             view_records(c, view), ts);
+                                                             nullptr, ts);
     SOF_LAUNCHED(c);
+    if (b.live) {
+      k_filter_counts_cross<<<grid_for(n, 256), 256, 0, c->stream>>>(n, c->rect.p, c->zkey_in.p, c->bin_zmax,
+                                                                     tiles_x, c->gcount.p, c->gbehind.p,
+                                                                     view_records(c, view), ts);
+      SOF_LAUNCHED(c);
+    }
   }
   // visible Gaussians in index order -> gidx_in[0, m)
   c->bin_scalar.ensure(2);
@@ -706,11 +758,17 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
     c->eval_in.ensure(M);
     const uint8_t* gflag = b.live ? c->gbehind.p : nullptr;
     const Rec* rec = view_records(c, view);
-    if (c->bin_zmax)
+    if (c->bin_zmax) {
       k_emit_filtered<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(c->bin_m, c->gidx_out.p, c->rect.p, c->goff.p,
                                                                        c->zkey_in.p, c->bin_zmax, tiles_x,
-                                                                       c->ekey_in.p, c->eval_in.p, gflag, rec, ts);
-    else
+                                                                       c->ekey_in.p, c->eval_in.p, gflag, nullptr, ts);
+      if (gflag && b.nb > 0) {
+        k_emit_filtered_cross<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(
+            c->bin_m, c->gidx_out.p, c->rect.p, c->goff.p, c->zkey_in.p, c->bin_zmax, tiles_x, c->ekey_in.p,
+            c->eval_in.p, gflag, rec, ts);
+        SOF_LAUNCHED(c);
+      }
+    } else
     {
       k_emit_entries<<<grid_for(c->bin_m, 256), 256, 0, c->stream>>>(c->bin_m, c->gidx_out.p, c->rect.p, c->gcount.p,
                                                                       c->goff.p, tiles_x, c->ekey_in.p, c->eval_in.p,
