@@ -174,6 +174,39 @@ __device__ __forceinline__ bool rcull(const float4& lo, const float4& hi, float 
   return g < -fmaf(0x1p-17f, s, hi.w);
 }
 
+// True when rcull culls every pixel of tile (tx, ty) for this record: the exact maximum of
+// the centre-form conic over the tile's pixel centres (a concave quadratic: the centre if
+// it lies inside the box, else the best point of the nearest edges) stays below
+// -(3 2^-17 S_max + kmar), S_max the largest |term| sum over the box (at a corner). rcull's
+// float evaluation at any pixel of the tile errs by at most 2^-17 S <= 2^-17 S_max, so it
+// culls each of them: listing the record in that tile changes no test outcome.
+__device__ __forceinline__ bool rtile_culled(const RRec& q, int tx, int ty) {
+  const double q00 = q.q00, q11 = q.q11, q01 = 0.5 * double(q.q01x2), g0 = q.g0;
+  if (!(isfinite(g0) && q00 < 0.0 && q11 < 0.0 && q00 * q11 - q01 * q01 > 0.0)) return false;
+  const double u0 = tx * kRTile + 0.5 - double(q.uc), u1 = u0 + (kRTile - 1);
+  const double v0 = ty * kRTile + 0.5 - double(q.vc), v1 = v0 + (kRTile - 1);
+  auto g = [&](double du, double dv) { return (q00 * du * du + q11 * dv * dv) + 2.0 * q01 * du * dv + g0; };
+  auto clampd = [](double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); };
+  double m;
+  if (u0 <= 0.0 && 0.0 <= u1 && v0 <= 0.0 && 0.0 <= v1) {
+    m = g0;  // the apex lies in the box
+  } else {
+    // along each edge the concave 1D quadratic peaks at its clamped vertex
+    m = -INFINITY;
+    const double us[2] = {u0, u1}, vs[2] = {v0, v1};
+    for (int k = 0; k < 2; ++k) {
+      const double dv = clampd(-q01 * us[k] / q11, v0, v1);
+      m = fmax(m, g(us[k], dv));
+      const double du = clampd(-q01 * vs[k] / q00, u0, u1);
+      m = fmax(m, g(du, vs[k]));
+    }
+  }
+  const double au = fmax(fabs(u0), fabs(u1)), av = fmax(fabs(v0), fabs(v1));
+  const double smax = (fabs(q00) * au * au + fabs(q11) * av * av + fabs(double(q.q01x2)) * au * av + fabs(g0)) *
+                      (1.0 + 1e-5);
+  return m < -(3.0 * 0x1p-17 * smax + double(q.kmar));
+}
+
 // K5.0 render records: gauss_view's FP64 fields (bit-identical) + the centre-form cull
 __global__ void k_rrec(int64_t n, const GaussStatic* __restrict__ g, Cam cam, RRec* out) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -229,7 +262,7 @@ __device__ __forceinline__ bool contribution(const R& r, const double* d, Tab ta
 // not cull (g >= -(2^-17 S + kmar), see RRec), dilated by one pixel; else the projected
 // E-box, dilated by one pixel, or every tile when the box crosses the camera plane.
 __global__ void k_rrect(int64_t n, const GaussStatic* __restrict__ g, const RRec* __restrict__ rr, Cam cam,
-                        int tiles_x, int tiles_y, int4* rect, uint32_t* cnt) {
+                        int tiles_x, int tiles_y, int4* rect, uint32_t* cnt, uint64_t* tmask) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const GaussStatic& G = g[i];
@@ -310,6 +343,16 @@ __global__ void k_rrect(int64_t n, const GaussStatic* __restrict__ g, const RRec
     if (on && tx0 <= tx1 && ty0 <= ty1) {
       count = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
       rect[i] = make_int4(tx0, tx1, ty0, ty1);
+      if (count <= uint32_t(kBigTiles)) {  // the rectangle's tiles the cull leaves, row-major bits
+        const RRec q = rr[i];
+        uint64_t m = 0;
+        int k = 0;
+        for (int ty = ty0; ty <= ty1; ++ty)
+          for (int tx = tx0; tx <= tx1; ++tx, ++k)
+            if (!rtile_culled(q, tx, ty)) m |= uint64_t(1) << k;
+        tmask[i] = m;
+        if (m == 0) count = 0;
+      }
     }
   }
   cnt[i] = count;
@@ -317,10 +360,13 @@ __global__ void k_rrect(int64_t n, const GaussStatic* __restrict__ g, const RRec
 
 // Counting sort by tile. PASS 0: histogram; PASS 1: scatter through per-tile cursors.
 // Gaussians with more than kBigTiles tiles are queued for the cooperative kernel.
+// Tiles of the rectangle whose pixels the record's cull rejects entirely (rtile_culled) are
+// skipped in both passes: per-Gaussian tile masks from k_rrect for rectangles of up to
+// kBigTiles tiles, the test itself in the cooperative kernel for the larger ones.
 template <int PASS>
 __global__ void k_rbin(int64_t n, const int4* __restrict__ rect, const uint32_t* __restrict__ cnt, int tiles_x,
                        uint32_t* tile_cnt, const int64_t* __restrict__ tile_off, int32_t* ent, int32_t* big,
-                       int32_t* big_cnt) {
+                       int32_t* big_cnt, const uint64_t* __restrict__ tmask) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const uint32_t c = cnt[i];
@@ -330,8 +376,11 @@ __global__ void k_rbin(int64_t n, const int4* __restrict__ rect, const uint32_t*
     return;
   }
   const int4 r = rect[i];
+  const uint64_t m = tmask[i];
+  int k = 0;
   for (int ty = r.z; ty <= r.w; ++ty)
-    for (int tx = r.x; tx <= r.y; ++tx) {
+    for (int tx = r.x; tx <= r.y; ++tx, ++k) {
+      if (!((m >> k) & 1)) continue;  // rtile_culled (k_rrect)
       const int t = ty * tiles_x + tx;
       const uint32_t slot = atomicAdd(&tile_cnt[t], 1u);
       if (PASS == 1) ent[tile_off[t] + slot] = int32_t(i);
@@ -341,15 +390,18 @@ __global__ void k_rbin(int64_t n, const int4* __restrict__ rect, const uint32_t*
 template <int PASS>
 __global__ void k_rbin_big(const int4* __restrict__ rect, int tiles_x, uint32_t* tile_cnt,
                            const int64_t* __restrict__ tile_off, int32_t* ent, const int32_t* __restrict__ big,
-                           const int32_t* __restrict__ big_cnt) {
+                           const int32_t* __restrict__ big_cnt, const RRec* __restrict__ recs) {
   const int nb = *big_cnt;
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     const int32_t g = big[b];
     const int4 r = rect[g];
+    const RRec q = recs[g];
     const int w = r.y - r.x + 1;
     const int count = w * (r.w - r.z + 1);
     for (int k = threadIdx.x; k < count; k += blockDim.x) {
-      const int t = (r.z + k / w) * tiles_x + r.x + k % w;
+      const int tx = r.x + k % w, ty = r.z + k / w;
+      if (rtile_culled(q, tx, ty)) continue;
+      const int t = ty * tiles_x + tx;
       const uint32_t slot = atomicAdd(&tile_cnt[t], 1u);
       if (PASS == 1) ent[tile_off[t] + slot] = g;
     }
@@ -1368,12 +1420,14 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
       rs.rect.ensure(n);
       rs.gcnt.ensure(n);
       k_rrec<<<grid_for(n, 128), 128, 0, st>>>(n, c->gstat.p, cam, rec);
-      k_rrect<<<grid_for(n, 128), 128, 0, st>>>(n, c->gstat.p, rec, cam, tiles_x, tiles_y, rs.rect.p, rs.gcnt.p);
+      rs.tmask.ensure(n);
+      k_rrect<<<grid_for(n, 128), 128, 0, st>>>(n, c->gstat.p, rec, cam, tiles_x, tiles_y, rs.rect.p, rs.gcnt.p,
+                                                rs.tmask.p);
       c->launches += 1;
       k_rbin<0><<<grid_for(n, 256), 256, 0, st>>>(n, rs.rect.p, rs.gcnt.p, tiles_x, rs.tile_cnt.p, nullptr, nullptr,
-                                                   rs.big.p, rs.big_cnt.p);
+                                                   rs.big.p, rs.big_cnt.p, rs.tmask.p);
       k_rbin_big<0><<<2 * 148, 256, 0, st>>>(rs.rect.p, tiles_x, rs.tile_cnt.p, nullptr, nullptr, rs.big.p,
-                                              rs.big_cnt.p);
+                                              rs.big_cnt.p, rec);
       c->launches += 3;
       SOF_CUDA(cudaGetLastError());
     }
@@ -1383,9 +1437,9 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
     if (M > 0) {
       SOF_CUDA(cudaMemsetAsync(rs.tile_cnt.p, 0, sizeof(uint32_t) * T, st));
       k_rbin<1><<<grid_for(n, 256), 256, 0, st>>>(n, rs.rect.p, rs.gcnt.p, tiles_x, rs.tile_cnt.p, rs.tile_off.p,
-                                                   rs.ent.p, rs.big.p, rs.big_cnt.p);
+                                                   rs.ent.p, rs.big.p, rs.big_cnt.p, rs.tmask.p);
       k_rbin_big<1><<<2 * 148, 256, 0, st>>>(rs.rect.p, tiles_x, rs.tile_cnt.p, rs.tile_off.p, rs.ent.p, rs.big.p,
-                                              rs.big_cnt.p);
+                                              rs.big_cnt.p, rec);
       c->launches += 2;
       SOF_CUDA(cudaGetLastError());
     }

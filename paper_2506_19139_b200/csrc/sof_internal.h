@@ -202,6 +202,7 @@ struct RenderScratch {
   bool attr_set = false;          // k_rsort_big's dynamic shared-memory limit set
   DBuf<char> rrec;                // [n] per-view render records (k_render.cu RRec, 128 B)
   DBuf<char> ent16b;              // window mode: the resorted slices (REnt)
+  DBuf<uint64_t> tmask;           // [n] tiles of a small rectangle the cull leaves (k_rrect)
   DBuf<double> zc;                // window mode: [n] view-space centre depth (arrival order)
 };
 
