@@ -163,3 +163,27 @@ def test_crossing_label_and_views(crossing_case, classify):
         wo, wob, wco = rev.view_opacity(v, verts[::5], classify)
         np.testing.assert_array_equal(bits(o), bits(wo))
         assert ev.counters() == rev.counters()
+
+
+def test_unbounded_medium_label_matches_reference(ref):
+    """A larger unbounded case at C5's resolution (200k Gaussians, two 1600x1064 views with
+    the cameras inside the shell, a 32^3 lattice reaching out to the cameras): label
+    opacities and the reference's pair / point-view counters, with counted Gaussians listed
+    only where they reach."""
+    from oracle.refpy import ALL
+    c = orbit_cameras(2, 1600, 1064, radius=4.0)
+    s = unbounded_scene(200000, 5, c)
+    scene = Scene(s.pos, s.scale, s.rot, s.opacity, s.dc)
+    cams = Cameras(c.R, c.t, c.intr, c.wh, c.nearfar)
+    verts, _ = kuhn_lattice(32, -4.5, 4.5)
+    rev = ref.context(scene, cams).evaluator(ALL)
+    want = rev.label_grid(verts, True)
+    ctx = sof.Context(0)
+    views = sof.ViewSet.build(scene, cams, ctx=ctx)
+    st = np.array([_stats(ctx, v) for v in range(cams.v)])
+    assert (st[:, 1] > 100).all()  # counted Gaussians in every view
+    ev = sof.FieldEvaluator(scene, views, sof.EvalStrategies.all())
+    got = ev.label_grid(verts, True)
+    np.testing.assert_array_equal(bits(got), bits(want))
+    assert ev.counters() == rev.counters()
+    ctx.close()
