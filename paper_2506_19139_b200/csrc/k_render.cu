@@ -896,16 +896,27 @@ __device__ __forceinline__ BRec brec_global(const RRec* __restrict__ recs, const
   return o;
 }
 
-// staged columns: sd[f * kBlendCap + pos], f = ic0..5, b0..2, c, op, dc0..2 (lanes read
-// different records: consecutive words, no bank conflicts)
+// staged columns of field pairs: sd[f * kBlendCap + pos] as double2, f = (ic0, ic1),
+// (ic2, ic3), (ic4, ic5), (b0, b1), (b2, c), (op, dc0), (dc1, dc2): one 16-byte shared
+// load per pair (lanes read different records: the per-lane reads of a column are
+// consecutive-stride words, and half the load instructions of single-field columns)
 constexpr int kBlendF = 14;
-__device__ __forceinline__ BRec brec_smem(const double* sd, const float* thr, int pos) {
+__device__ __forceinline__ BRec brec_smem(const double2* sd, const float* thr, int pos) {
   BRec o;
-  for (int f = 0; f < 6; ++f) o.ic[f] = sd[f * kBlendCap + pos];
-  for (int f = 0; f < 3; ++f) o.b[f] = sd[(6 + f) * kBlendCap + pos];
-  o.c = sd[9 * kBlendCap + pos];
-  o.op = sd[10 * kBlendCap + pos];
-  for (int f = 0; f < 3; ++f) o.dc[f] = sd[(11 + f) * kBlendCap + pos];
+  double2 v = sd[0 * kBlendCap + pos];
+  o.ic[0] = v.x, o.ic[1] = v.y;
+  v = sd[1 * kBlendCap + pos];
+  o.ic[2] = v.x, o.ic[3] = v.y;
+  v = sd[2 * kBlendCap + pos];
+  o.ic[4] = v.x, o.ic[5] = v.y;
+  v = sd[3 * kBlendCap + pos];
+  o.b[0] = v.x, o.b[1] = v.y;
+  v = sd[4 * kBlendCap + pos];
+  o.b[2] = v.x, o.c = v.y;
+  v = sd[5 * kBlendCap + pos];
+  o.op = v.x, o.dc[0] = v.y;
+  v = sd[6 * kBlendCap + pos];
+  o.dc[1] = v.x, o.dc[2] = v.y;
   o.thr = thr[pos];
   return o;
 }
@@ -944,8 +955,8 @@ __global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile
                                                   const double* __restrict__ dc, int exact_depth, RenderOut out,
                                                   unsigned long long* stats) {
   extern __shared__ __align__(16) unsigned char sdyn[];
-  double* scol = reinterpret_cast<double*>(sdyn);                      // [kBlendF][kBlendCap]
-  float* sthr = reinterpret_cast<float*>(scol + kBlendF * kBlendCap);  // [kBlendCap]
+  double2* scol = reinterpret_cast<double2*>(sdyn);                         // [kBlendF / 2][kBlendCap]
+  float* sthr = reinterpret_cast<float*>(scol + (kBlendF / 2) * kBlendCap);  // [kBlendCap]
   __shared__ __align__(16) double s_exp[128];
   const int tile = tile0 + int(blockIdx.x), l = threadIdx.x;
   for (int k = l; k < 128; k += blockDim.x) s_exp[k] = kSofExpTabDev[k];
@@ -956,16 +967,15 @@ __global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile
     const int32_t g = ent[l0 + r];
     if (qq < 5) {
       const double2 v = __ldg(reinterpret_cast<const double2*>(recs + g) + qq);
-      scol[(2 * qq) * kBlendCap + r] = v.x;
-      scol[(2 * qq + 1) * kBlendCap + r] = v.y;
+      scol[qq * kBlendCap + r] = v;
     } else if (qq == 5) {
-      scol[10 * kBlendCap + r] = __ldg(&recs[g].op);
+      scol[5 * kBlendCap + r].x = __ldg(&recs[g].op);
       sthr[r] = __ldg(&recs[g].thr);
     } else if (qq == 6) {
-      scol[11 * kBlendCap + r] = __ldg(dc + 3 * g);
-      scol[12 * kBlendCap + r] = __ldg(dc + 3 * g + 1);
+      scol[5 * kBlendCap + r].y = __ldg(dc + 3 * g);
+      scol[6 * kBlendCap + r].x = __ldg(dc + 3 * g + 1);
     } else {
-      scol[13 * kBlendCap + r] = __ldg(dc + 3 * g + 2);
+      scol[6 * kBlendCap + r].y = __ldg(dc + 3 * g + 2);
     }
   }
   __syncthreads();
