@@ -20,11 +20,12 @@ SEED_BASE = 2506191390
 # deterministic for the synthetic inputs); the CPU reference arm, which cannot run all
 # views, uses it to weigh its bisection sample into the same query mix.
 CONFIGS = {
-    "C1": dict(gaussians=10_000, views=16, width=256, height=256, lattice=45, edges=0),
+    "C1": dict(gaussians=10_000, views=16, width=256, height=256, lattice=45, edges=22_750),
     "C2": dict(gaussians=1_000_000, views=100, width=1920, height=1080, lattice=0, edges=0),
     "C3": dict(gaussians=3_000_000, views=200, width=1600, height=1064, lattice=300, edges=564_638),
-    "C4": dict(gaussians=5_000_000, views=300, width=1920, height=1080, lattice=345, edges=0),
-    "C5": dict(gaussians=10_000_000, views=500, width=1600, height=1064, lattice=436, edges=0, unbounded=True),
+    "C4": dict(gaussians=5_000_000, views=300, width=1920, height=1080, lattice=345, edges=199_568),
+    "C5": dict(gaussians=10_000_000, views=500, width=1600, height=1064, lattice=436, edges=1_223_734,
+               unbounded=True),
 }
 
 
