@@ -10,23 +10,25 @@
 // needs a window of that size per pixel. The design therefore sorts each pixel's
 // contributions explicitly, in five steps per view:
 //
-//   R0 binning: each Gaussian's conservative screen rectangle (E-box with clamped scales,
-//      one-pixel dilation; all tiles when the box crosses the camera plane, none when it
-//      lies entirely behind it), then a counting sort by tile (histogram, scan, scatter:
-//      no radix sort, the order inside a tile list is irrelevant because every pixel's
-//      contributions are sorted later);
-//   R1 k_rcount: per pixel, the number of list records that pass the screen-space conic
-//      cull (FP32, Rec::conic) — an upper bound of its contributions; a scan turns the
-//      bounds into per-pixel slices;
-//   R2 k_rtest: one CTA per 16x16 tile streams the tile list through shared memory; each
-//      warp computes its 32 pixels' conic masks for a 32-record chunk, compacts the
-//      surviving (pixel, record) pairs into a queue and evaluates them on all 32 lanes
-//      with the reference's FP64 expressions (no divergence on the FP64 work); every
-//      contribution (t*, alpha, a, b, index) lands in its pixel's slice;
-//   R3 k_rsort: one warp per pixel sorts the slice by (t*, index) in shared memory
-//      (bitonic network; the key is t*'s bits with the low 10 bits replaced by the slot,
-//      equal-prefix runs are re-ordered exactly); slices longer than 1024 go to a
-//      CTA-wide sort in global memory (k_rsort_big);
+//   R0 binning: per Gaussian a render record (RRec: the FP64 fields of the test plus the
+//      screen conic in centre form) and its conservative screen rectangle (the conic's
+//      ellipse box, else the E-box with clamped scales, one-pixel dilation; all tiles when
+//      the box crosses the camera plane, none when it lies entirely behind it), minus the
+//      tiles whose every pixel centre the conic cull rejects (rtile_culled); then a
+//      counting sort by tile (histogram, scan, scatter: the order inside a tile list is
+//      irrelevant because every pixel's contributions are sorted later);
+//   R1 k_rcount: per pixel, the number of list records that pass the FP32 conic cull —
+//      an upper bound of its contributions; a scan turns the bounds into per-pixel slices;
+//   R2 k_rtest: one CTA per 16x16 tile streams the tile list through shared memory (FP64
+//      fields as columns); each warp computes its 32 pixels' cull masks for a 32-record
+//      chunk, the CTA compacts the surviving (pixel, record) pairs into one queue and all
+//      256 threads evaluate them with the reference's FP64 expressions; every contribution
+//      lands in its pixel's slice as REnt {t*, list position, Gaussian index};
+//   R3 k_rsort: one warp per pixel sorts its slice by (t*, index): a register bitonic
+//      network on 64-bit keys ((bits(t*) - bits(min t*)) << 9 | slot), equal-t* runs then
+//      re-ordered by index, the entries permuted once through shared memory; slices past
+//      256 entries or past the key's span go to k_rsort_mid (512), then k_rsort_big (one
+//      CTA, up to 4096 in shared memory, a global-memory network beyond);
 //   R4 k_rblend: one thread per pixel walks its sorted slice: colour and transmittance
 //      (render_pixel :204-210), the median (find_median :129-141), the exact depth
 //      (:157-166) and the opacity at the depth (opacity_along_ray :104-108) — all in the
