@@ -120,6 +120,15 @@ def ncu_k_eval() -> dict:
         return {}
 
 
+def ncu_render() -> dict:
+    """Issue activity of the render kernels from the committed ncu captures
+    (profiles/k_render_issue.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "k_render_issue.json")))
+    except Exception:
+        return {}
+
+
 # ---- sorted rasterizer sample (secondary: not the headline metric) -------------------------
 
 def render_sample(device: int, views=(0, 1, 2), rows=(135, 540, 945), threads=None):
@@ -158,7 +167,11 @@ def render_sample(device: int, views=(0, 1, 2), rows=(135, 540, 945), threads=No
            "roofline": {"bound": "issue", "kernel": "K5 (R1-R4, whole render)", "achieved": tested / (t * 1e-3),
                         "peak": RENDER_TESTED_PAIRS_PER_S, "unit": "tested pairs/s",
                         "frac": tested / (t * 1e-3) / RENDER_TESTED_PAIRS_PER_S,
-                        "note": "SURVEY.md 8(d): 17 issue slots per tested (pixel, Gaussian) pair"}}
+                        "ncu_issue_active_weighted": ncu_render().get("issue_active_time_weighted_pct"),
+                        "note": "SURVEY.md 8(d): 17 issue slots per tested (pixel, Gaussian) pair; the binning's "
+                                "tile cull removes tested pairs, so this counts work not done. "
+                                "ncu_issue_active_weighted: issue activity of R0-R4 weighted by kernel time "
+                                "(profiles/k_render_issue.json)"}}
     # the rows of view 0 on the device, then on the CPU reference
     full = sof.render_view(sof.ViewSet(ctx, ctx.scene, ctx.cams, 0.0), 0, sof.DEPTH_EXACT, counts=True)
     ctx.close()
