@@ -343,7 +343,10 @@ __global__ void __launch_bounds__(kDlThreads) k_delaunay(int64_t n, DlBuffers B)
 
 }  // namespace
 
-std::vector<std::array<int, 4>> delaunay_device(sof_ctx* c, const double* pts, int64_t n) {
+// One run with the given capacity multiplier; false when a cavity or the tet array
+// outgrew its capacity (the caller retries larger).
+static bool delaunay_run(sof_ctx* c, const double* pts, int64_t n, int64_t mult,
+                         std::vector<std::array<int, 4>>& out) {
   if (n < 4) throw InvalidArg("need at least 4 points");
   // the enclosing tetrahedron (delaunay.hpp:55-67), set up on the host
   std::vector<V3> v(size_t(n) + 4);
@@ -365,8 +368,10 @@ std::vector<std::array<int, 4>> delaunay_device(sof_ctx* c, const double* pts, i
   double r20;
   const bool ok0 = sphere(v[a], v[b], v[cc], v[d], c0, r20);
 
-  const int64_t cap = 16 * n + 262144;  // ~6.5 n live tets for random points, retired ones, one insertion's growth
-  const int64_t fcap = 65536;
+  // ~6.5 n live tets for random points, retired ones and one insertion's growth; degenerate
+  // sets (the reference's slivers leave holes) can need more: mult grows on retry
+  const int64_t cap = (16 * n + 262144) * mult;
+  const int64_t fcap = 65536 * mult;
   DBuf<char>& m = c->dl_buf;
   const size_t bytes = sizeof(V3) * (n + 4) + 2 * cap * (sizeof(int4) + sizeof(double4) + 1) + cap * 8 +
                        4096 * 8 + fcap * (sizeof(int3) + 4 + sizeof(int4) + sizeof(double4)) + sizeof(DlState) + 4096;
@@ -419,7 +424,7 @@ std::vector<std::array<int, 4>> delaunay_device(sof_ctx* c, const double* pts, i
   DlState st;
   SOF_CUDA(cudaMemcpyAsync(&st, B.st, sizeof st, cudaMemcpyDeviceToHost, s));
   SOF_CUDA(cudaStreamSynchronize(s));
-  if (st.error) throw StateError("device Delaunay: a cavity or the tet array exceeded its capacity");
+  if (st.error) return false;
   std::vector<int4> tv(size_t(st.T));
   std::vector<uint8_t> al(size_t(st.T));
   if (st.T > 0) {
@@ -427,11 +432,27 @@ std::vector<std::array<int, 4>> delaunay_device(sof_ctx* c, const double* pts, i
     SOF_CUDA(cudaMemcpyAsync(al.data(), B.alive[st.sel], st.T, cudaMemcpyDeviceToHost, s));
     SOF_CUDA(cudaStreamSynchronize(s));
   }
-  std::vector<std::array<int, 4>> out;  // live tets without enclosing-tetrahedron corners, in order
+  out.clear();  // live tets without enclosing-tetrahedron corners, in order
   for (int64_t i = 0; i < st.T; ++i) {
     const int4 q = tv[size_t(i)];
     if (al[size_t(i)] && q.x < n && q.y < n && q.z < n && q.w < n) out.push_back({q.x, q.y, q.z, q.w});
   }
+  return true;
+}
+
+std::vector<std::array<int, 4>> delaunay_device(sof_ctx* c, const double* pts, int64_t n) {
+  if (n < 4) throw InvalidArg("need at least 4 points");
+  std::vector<std::array<int, 4>> out;
+  bool ok = false;
+  for (int64_t mult = 1; !ok && mult <= 64; mult *= 4) {
+    size_t free_b = 0, total_b = 0;
+    SOF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double need = double((16 * n + 262144) * mult) * 2 * (sizeof(int4) + sizeof(double4) + 1) +
+                        double(65536 * mult) * 64;
+    if (mult > 1 && need > 0.8 * double(free_b + c->dl_buf.bytes())) break;
+    ok = delaunay_run(c, pts, n, mult, out);
+  }
+  if (!ok) throw StateError("device Delaunay: the tet array outgrew the device memory");
   if (out.empty()) throw InvalidArg("degenerate (coplanar) point set");
   return out;
 }
