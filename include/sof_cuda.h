@@ -274,6 +274,12 @@ int sof_validate_tets_dev(sof_ctx* ctx, int64_t nt, const int32_t* tets_dev, int
 int sof_event_record(sof_ctx* ctx, int slot);
 int sof_event_elapsed(sof_ctx* ctx, int slot_a, int slot_b, float* ms);
 int sof_sync(sof_ctx* ctx);
+/* Stream interop (no host synchronisation): sof_stream_wait orders the context's stream
+ * after all work enqueued so far on `stream` (a cudaStream_t of the caller, e.g. the
+ * stream that filled a buffer the library reads next); sof_get_stream returns the
+ * context's stream (cudaStream_t) for the opposite direction. */
+int sof_stream_wait(sof_ctx* ctx, void* stream);
+int sof_get_stream(sof_ctx* ctx, void** stream);
 /* page-lock host buffers so uploads run at full link bandwidth */
 int sof_host_register(void* ptr, size_t bytes);
 int sof_host_unregister(void* ptr);

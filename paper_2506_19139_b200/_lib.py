@@ -56,6 +56,8 @@ _SIGS = {
     "sof_last_error": (ctypes.c_char_p, [_P]),
     "sof_kernel_launches": (_I64, [_P]),
     "sof_scene_size": (_I64, [_P]),
+    "sof_stream_wait": (_I, [_P, _P]),
+    "sof_get_stream": (_I, [_P, ctypes.POINTER(_P)]),
     "sof_live_binding_stats": (_I, [_P, _I, _I, _P]),
     "sof_set_render_window": (_I, [_P, _I64]),
     "sof_collect_contributions": (_I, [_P, _I, _I64, _P, _P]),

@@ -88,6 +88,7 @@ int sof_ctx_create(int device, sof_ctx** out) {
     }
     SOF_CUDA(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
     SOF_CUDA(cudaEventCreateWithFlags(&c->tets_ev, cudaEventDisableTiming));
+    SOF_CUDA(cudaEventCreateWithFlags(&c->interop_ev, cudaEventDisableTiming));
     SOF_CUDA(cudaMallocHost(&c->pinned_scalar, 8 * sizeof(uint64_t)));
     for (auto& e : c->prep_ev) SOF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->eval_ev) SOF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -127,6 +128,7 @@ void sof_ctx_destroy(sof_ctx* ctx) {
     cudaStreamDestroy(ctx->stream_copy);
   }
   if (ctx->tets_ev) cudaEventDestroy(ctx->tets_ev);
+  if (ctx->interop_ev) cudaEventDestroy(ctx->interop_ev);
   if (ctx->pinned_scalar) cudaFreeHost(ctx->pinned_scalar);
   cudaStream_t s = ctx->stream;
   delete ctx;

@@ -210,6 +210,20 @@ int sof_event_elapsed(sof_ctx* c, int a, int b, float* ms) {
   return cudaEventElapsedTime(ms, c->user_ev[a], c->user_ev[b]) == cudaSuccess ? SOF_OK : SOF_E_CUDA;
 }
 
+int sof_stream_wait(sof_ctx* c, void* stream) {
+  if (!c) return SOF_E_INVALID;
+  return guard(c, [&] {
+    SOF_CUDA(cudaEventRecord(c->interop_ev, static_cast<cudaStream_t>(stream)));
+    SOF_CUDA(cudaStreamWaitEvent(c->stream, c->interop_ev, 0));
+  });
+}
+
+int sof_get_stream(sof_ctx* c, void** stream) {
+  if (!c || !stream) return SOF_E_INVALID;
+  *stream = c->stream;
+  return SOF_OK;
+}
+
 int sof_sync(sof_ctx* c) {
   if (!c) return SOF_E_INVALID;
   return cudaStreamSynchronize(c->stream) == cudaSuccess ? SOF_OK : SOF_E_CUDA;

@@ -259,6 +259,7 @@ struct sof_ctx {
   cudaStream_t stream_copy = nullptr;     // sof_set_tets_async: tet upload + index check
   uint64_t* pinned_scalar = nullptr;      // [8] pinned host slots for small read-backs
   cudaEvent_t tets_ev = nullptr;          // ... recorded after them
+  cudaEvent_t interop_ev = nullptr;       // sof_stream_wait: an event on the caller's stream
   bool tets_pending = false;              // march must wait for tets_ev and check the flag
   // the pending upload, fed to the copy engine in chunks (pump_upload) so that the
   // memsets CUB issues on the same engine never queue behind gigabytes

@@ -55,11 +55,14 @@ class GpuBackend:
         return ctypes.c_void_p(t.data_ptr())
 
     def sync(self):
-        self.torch.cuda.synchronize(self.dev)
+        """Orders the library's stream after everything torch enqueued so far (no host
+        synchronisation: sof_stream_wait records an event on torch's current stream)."""
+        st = self.torch.cuda.current_stream(self.dev)
+        self.ctx.check(self.ctx.lib.sof_stream_wait(self.ctx.h, ctypes.c_void_p(st.cuda_stream)))
 
     # torch fills and concatenations run on torch's current stream; the library works on
-    # its own non-blocking stream, so every tensor torch wrote is synchronised before a
-    # library call reads it (the library calls themselves return with their stream idle)
+    # its own non-blocking stream, so every tensor torch wrote is ordered before a library
+    # call reads it (the library calls themselves return with their stream idle)
     def new_state(self, n):
         t = self.torch
         out = t.ones(n, dtype=t.float64, device=self.dev), t.zeros(n, dtype=t.uint8, device=self.dev)
