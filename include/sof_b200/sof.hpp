@@ -581,6 +581,47 @@ inline DepthMap render_depth_map(const ViewSet& views, size_t view, DepthMode mo
   return render_depth_map(views.caches.at(view), views.cameras.at(view), mode);
 }
 
+// A batch of whole-view renders (render_pixel's colour and final transmittance, and the
+// depth map of render_depth_map) for views [first, first + count).
+struct ViewRender {
+  Grid2D<Vec3> color;
+  Grid2D<double> depth;         // kNoSurface where none
+  Grid2D<double> opacity;       // accumulated opacity at the depth
+  Grid2D<double> transmittance;  // final T
+};
+
+inline std::vector<ViewRender> render_views(const ViewSet& views, size_t first, size_t count,
+                                            DepthMode mode = DepthMode::kExact) {
+  if (first + count > views.cameras.size()) throw std::invalid_argument("render_views: view range out of range");
+  sof_ctx* c = views.ctx.get();
+  size_t px = 0;
+  for (size_t v = first; v < first + count; ++v) px += size_t(views.cameras[v].width) * views.cameras[v].height;
+  std::vector<double> rgb(3 * px), depth(px), op(px), tf(px);
+  detail::check(c, sof_set_render_window(c, 0));
+  detail::check(c, sof_render_views(c, int(first), int(count), mode == DepthMode::kExact ? SOF_DEPTH_EXACT
+                                                                                         : SOF_DEPTH_MEDIAN,
+                                    rgb.data(), depth.data(), op.data(), tf.data()));
+  std::vector<ViewRender> out(count);
+  size_t at = 0;
+  for (size_t k = 0; k < count; ++k) {
+    const Camera& cam = views.cameras[first + k];
+    ViewRender& r = out[k];
+    r.color = Grid2D<Vec3>(cam.width, cam.height, Vec3::Zero());
+    r.depth = Grid2D<double>(cam.width, cam.height, kNoSurface);
+    r.opacity = Grid2D<double>(cam.width, cam.height, 0.0);
+    r.transmittance = Grid2D<double>(cam.width, cam.height, 1.0);
+    const size_t p = size_t(cam.width) * cam.height;
+    for (size_t i = 0; i < p; ++i) {
+      r.color.data[i] = Vec3(rgb[3 * (at + i)], rgb[3 * (at + i) + 1], rgb[3 * (at + i) + 2]);
+      r.depth.data[i] = depth[at + i];
+      r.opacity.data[i] = op[at + i];
+      r.transmittance.data[i] = tf[at + i];
+    }
+    at += p;
+  }
+  return out;
+}
+
 // camera.hpp:36-39
 struct Ray {
   Vec3 origin = Vec3::Zero();

@@ -343,6 +343,11 @@ int sof_copy_result(sof_ctx* ctx, int kind, void* host_dst);
 int sof_render_view(sof_ctx* ctx, int view, int depth_mode, int tile_size, double* depth,
                     double* opacity, double* rgb, double* t_final, uint64_t* stats);
 
+/* sof_render_view over views [first_view, first_view + n_views), outputs concatenated in
+ * view order (view v's pixels start after the w*h pixels of the views before it); each
+ * output nullable. */
+int sof_render_views(sof_ctx* ctx, int first_view, int n_views, int depth_mode, double* rgb, double* depth,
+                     double* opacity, double* t_final);
 /* Per-pixel contribution counts [h*w] of the last sof_render_view of `view` (the length
  * of each pixel's collect_contributions list, opacity_field.hpp:39-61). SOF_E_STATE if
  * that view was not the last one rendered. */

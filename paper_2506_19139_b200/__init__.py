@@ -7,7 +7,7 @@ from ._lib import (ALL_STRATEGIES, DEAD_CULL, DEPTH_EXACT, DEPTH_MEDIAN, EARLY_S
 from .api import (CameraSet, Context, EvalStrategies, ExtractOptions, FieldEvaluator, FloatMap, GaussianScene,
                   MarchingResult, Mesh, SeedPointSet, SofError, TetGrid, ViewSet, assemble_mesh,
                   binary_search_refine, build_seed_points, delaunay_tetrahedralize,
-                  collect_contributions, windowed_resort, render_pixel, pixel_rays,
+                  collect_contributions, windowed_resort, render_pixel, pixel_rays, render_views,
                   default_context, depth_to_map, extract_mesh, load_cameras, save_cameras, extract_resident, gaussian_normal, marching_tets,
                   normal_from_depth, normals_to_map, parse_scene, read_float_map, read_mesh_obj, read_mesh_ply,
                   render_depth_map, render_maps, render_view, write_float_map, write_mesh, write_mesh_obj,

@@ -56,6 +56,7 @@ _SIGS = {
     "sof_last_error": (ctypes.c_char_p, [_P]),
     "sof_kernel_launches": (_I64, [_P]),
     "sof_scene_size": (_I64, [_P]),
+    "sof_render_views": (_I, [_P, _I, _I, _I, _P, _P, _P, _P]),
     "sof_stream_wait": (_I, [_P, _P]),
     "sof_get_stream": (_I, [_P, ctypes.POINTER(_P)]),
     "sof_live_binding_stats": (_I, [_P, _I, _I, _P]),

@@ -493,6 +493,25 @@ def render_view(views: ViewSet, view: int, depth_mode: int = L.DEPTH_EXACT, tile
     return out
 
 
+def render_views(views: ViewSet, first: int, count: int, depth_mode: int = L.DEPTH_EXACT) -> list:
+    """sof_render_views: the exact render of views [first, first + count) in one call;
+    per view a dict of depth, opacity, rgb and t_final (as render_view)."""
+    ctx = views.ctx
+    wh = [(int(w), int(h)) for w, h in ctx.cams.wh[first:first + count]]
+    px = sum(w * h for w, h in wh)
+    rgb, depth, op, tf = np.empty((px, 3)), np.empty(px), np.empty(px), np.empty(px)
+    ctx.check(ctx.lib.sof_set_render_window(ctx.h, 0))
+    ctx.check(ctx.lib.sof_render_views(ctx.h, int(first), int(count), int(depth_mode), _ptr(rgb), _ptr(depth),
+                                       _ptr(op), _ptr(tf)))
+    out, at = [], 0
+    for w, h in wh:
+        sl = slice(at, at + w * h)
+        out.append({"depth": depth[sl].reshape(h, w), "opacity": op[sl].reshape(h, w),
+                    "rgb": rgb[sl].reshape(h, w, 3), "t_final": tf[sl].reshape(h, w)})
+        at += w * h
+    return out
+
+
 def pixel_rays(cams: CameraSet, view: int, pix) -> np.ndarray:
     """ray_through_pixel(cam, x + 0.5, y + 0.5).direction (camera.hpp:42-48) for integer
     pixels pix[n, 2] = (x, y), in the reference's operation order (host)."""

@@ -1539,6 +1539,24 @@ extern "C" int sof_render_view(sof_ctx* c, int view, int depth_mode, int tile_si
   });
 }
 
+extern "C" int sof_render_views(sof_ctx* c, int first_view, int n_views, int depth_mode, double* rgb, double* depth,
+                                double* opacity, double* t_final) {
+  if (!c || n_views < 0) return SOF_E_INVALID;
+  if (first_view < 0 || int64_t(first_view) + n_views > int64_t(c->cams.size())) {
+    c->err = "view range out of range";
+    return SOF_E_INVALID;
+  }
+  int64_t at = 0;  // pixel offset of the view in the concatenated outputs
+  for (int v = first_view; v < first_view + n_views; ++v) {
+    const int st = sof_render_view(c, v, depth_mode, kRTile, depth ? depth + at : nullptr,
+                                   opacity ? opacity + at : nullptr, rgb ? rgb + 3 * at : nullptr,
+                                   t_final ? t_final + at : nullptr, nullptr);
+    if (st != SOF_OK) return st;
+    at += int64_t(c->cams[v].w) * c->cams[v].h;
+  }
+  return SOF_OK;
+}
+
 extern "C" int sof_render_counts(sof_ctx* c, int view, uint32_t* counts) {
   if (!c || !counts) return SOF_E_INVALID;
   return guard(c, [&] {

@@ -578,3 +578,24 @@ TEST(RenderDepthMap, CacheSignatureAndEmptyScene) {
   EXPECT_EQ(px.depth, exact.depth.at(16, 16));
   EXPECT_EQ(px.accumulated_opacity, exact.opacity.at(16, 16));
 }
+
+TEST(RenderViews, BatchEqualsPerViewMaps) {
+  const auto scene = random_scene(62, 30);
+  std::vector<Camera> cams;
+  for (int i = 0; i < 3; ++i) {
+    const double a = 2.0 * M_PI * i / 3;
+    cams.push_back(look_at(Vec3(4 * std::cos(a), 4 * std::sin(a), 0.5), Vec3::Zero(), Vec3(0, 0, 1), 40.0, 32));
+  }
+  const ViewSet views = ViewSet::build(scene, cams);
+  const auto batch = render_views(views, 1, 2);
+  ASSERT_EQ(batch.size(), 2u);
+  for (size_t k = 0; k < 2; ++k) {
+    const DepthMap dm = render_depth_map(views.caches[1 + k], views.cameras[1 + k], DepthMode::kExact);
+    for (size_t i = 0; i < dm.depth.data.size(); ++i) {
+      const double a = dm.depth.data[i], b = batch[k].depth.data[i];
+      EXPECT_TRUE((std::isnan(a) && std::isnan(b)) || a == b);
+      EXPECT_EQ(dm.opacity.data[i], batch[k].opacity.data[i]);
+    }
+  }
+  EXPECT_THROW(render_views(views, 2, 2), std::invalid_argument);
+}

@@ -256,3 +256,17 @@ def test_render_cameras_inside_scene(ref, dist):
     for v in range(cams.v):
         for exact in (True, False):
             check(rc, views, v, exact)
+
+
+def test_render_views_batch(ref):
+    """sof_render_views: one call over several views equals the per-view renders (bits)."""
+    scene = ref.random_scene(61, 300, 1.0)
+    cams = ref.orbit_cameras(3, 4.0, 1.8, 40)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    batch = sof.render_views(views, 1, 2)
+    for k, v in enumerate((1, 2)):
+        one = sof.render_view(views, v)
+        for key in ("depth", "opacity", "rgb", "t_final"):
+            np.testing.assert_array_equal(bits(batch[k][key]), bits(one[key]), err_msg=key)
+    with pytest.raises(ValueError):
+        sof.render_views(views, 2, 2)
