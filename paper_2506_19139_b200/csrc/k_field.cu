@@ -121,7 +121,14 @@ struct RectOut {
   int32_t* idx;
   bool live_only;   // leave dead Gaussians (op < 1/255) out of the lists (see Binding::live)
   uint8_t* behind;  // live_only: 1 for gauss_behind Gaussians (counted, not listed)
+  unsigned long long* nflag;  // live_only: number of nonzero count flags (the count list's size)
 };
+
+// warp-aggregated increment of *ctr for the lanes with f set
+__device__ __forceinline__ void count_flags(unsigned long long* ctr, bool f) {
+  const unsigned m = __ballot_sync(__activemask(), f);
+  if (m && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(ctr, (unsigned long long)__popc(m));
+}
 
 // k_view_rec + k_tile_rect in one pass (one GaussStatic read per Gaussian and view).
 #ifndef SOF_REC_MINB
@@ -150,7 +157,11 @@ __global__ void __launch_bounds__(128, SOF_REC_MINB) k_view_rec_rect(int64_t n, 
                               : uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     ro.rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
-  if (ro.live_only) ro.behind[i] = behind ? kCountBehind : (live && crosses) ? kCountCross : 0;
+  if (ro.live_only) {
+    const uint8_t f = behind ? kCountBehind : (live && crosses) ? kCountCross : 0;
+    ro.behind[i] = f;
+    count_flags(ro.nflag, f != 0);
+  }
   ro.cnt[i] = count;
   ro.zkey[i] = double_key(r.zmin);
   ro.idx[i] = int32_t(i);
@@ -241,7 +252,7 @@ const RecF* view_recf(sof_ctx* c, int view) {
 __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
                             const Rec* __restrict__ rec, Cam cam, int ts, int tiles_x, int tiles_y,
                             bool live_only, int4* rect, uint32_t* cnt, uint64_t* zkey, int32_t* idx,
-                            uint8_t* behind_out) {
+                            uint8_t* behind_out, unsigned long long* nflag) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i > n) return;
   if (i == n) {  // sentinel for the exclusive scan over n + 1 counts
@@ -259,7 +270,11 @@ __global__ void k_tile_rect(int64_t n, const GaussStatic* __restrict__ g,
                               : uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
     rect[i] = make_int4(tx0, tx1, ty0, ty1);
   }
-  if (live_only) behind_out[i] = behind ? kCountBehind : (live && crosses) ? kCountCross : 0;
+  if (live_only) {
+    const uint8_t f = behind ? kCountBehind : (live && crosses) ? kCountCross : 0;
+    behind_out[i] = f;
+    count_flags(nflag, f != 0);
+  }
   cnt[i] = count;
   zkey[i] = double_key(rec[i].zmin);
   idx[i] = int32_t(i);
@@ -405,13 +420,17 @@ static void build_binding(sof_ctx* c, int view, int ts, bool live, Binding& b, b
   c->gidx_out.ensure(n);
   c->goff.ensure(n + 1);
   c->gbehind.ensure(n);
-  const RectOut ro{ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p, live, c->gbehind.p};
+  c->bin_scalar.ensure(4);  // [0] visible count, [1] tie-run overflow, [2] count flags
+  zero_async(c, c->bin_scalar.p, 4 * sizeof(int64_t));
+  unsigned long long* nflag = reinterpret_cast<unsigned long long*>(c->bin_scalar.p + 2);
+  const RectOut ro{ts, tiles_x, tiles_y, c->rect.p, c->gcount.p, c->zkey_in.p, c->gidx_in.p, live, c->gbehind.p,
+                   nflag};
   bool rect_done = false;
   const Rec* rec = view_records_impl(c, view, &ro, &rect_done);
   if (!rect_done) {
     k_tile_rect<<<grid_for(n + 1, 128), 128, 0, c->stream>>>(n, c->gstat.p, rec, cam, ts, tiles_x,
                                                               tiles_y, live, c->rect.p, c->gcount.p,
-                                                              c->zkey_in.p, c->gidx_in.p, c->gbehind.p);
+                                                              c->zkey_in.p, c->gidx_in.p, c->gbehind.p, nflag);
     SOF_LAUNCHED(c);
   }
   bin_by_key(c, view, ts, tiles_x, tiles_y, b, charge);
@@ -649,7 +668,6 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
     }
   }
   // visible Gaussians in index order -> gidx_in[0, m)
-  c->bin_scalar.ensure(2);
   {
     size_t bytes = 0;
     thrust::counting_iterator<int32_t> it(0);
@@ -667,23 +685,36 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
     k_float_keys<<<grid_for(m, 256), 256, 0, c->stream>>>(m, c->gidx_in.p, c->zkey_in.p, fk_in);
     SOF_LAUNCHED(c);
     sort_pairs_u32(c, fk_in, fk_out, c->gidx_in.p, c->gidx_out.p, m, 32);
-    zero_async(c, c->bin_scalar.p + 1, sizeof(int));
     k_fix_ties<<<grid_for(m, 256), 256, 0, c->stream>>>(m, fk_out, c->gidx_out.p, c->zkey_in.p,
                                                          reinterpret_cast<int*>(c->bin_scalar.p + 1));
     SOF_LAUNCHED(c);
-    if (read_scalar(c, reinterpret_cast<int*>(c->bin_scalar.p + 1))) {  // a long tie run: full sort
-      c->zkey_aux.ensure(m);
-      k_gather_keys<<<grid_for(m, 256), 256, 0, c->stream>>>(m, c->gidx_in.p, c->zkey_in.p, c->zkey_aux.p);
-      SOF_LAUNCHED(c);
-      sort_pairs_u64(c, c->zkey_aux.p, c->zkey_out.p, c->gidx_in.p, c->gidx_out.p, m, 64);
-    }
   }
   c->ekey_in.ensure(m + 1);
-  k_gather_counts<<<grid_for(m + 1, 256), 256, 0, c->stream>>>(m, c->gidx_out.p, c->gcount.p,
-                                                                c->ekey_in.p);
-  SOF_LAUNCHED(c);
-  exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, m + 1);
-  const int64_t M = read_scalar(c, c->goff.p + m);
+  auto offsets = [&]() {
+    k_gather_counts<<<grid_for(m + 1, 256), 256, 0, c->stream>>>(m, c->gidx_out.p, c->gcount.p, c->ekey_in.p);
+    SOF_LAUNCHED(c);
+    exclusive_scan_u32_to_i64(c, c->ekey_in.p, c->goff.p, m + 1);
+  };
+  offsets();
+  // one read-back for the entry count, the tie-run overflow flag and the count-list size
+  int64_t M = 0, nflag_h = 0;
+  int overflow = 0;
+  SOF_CUDA(cudaMemcpyAsync(c->pinned_scalar, c->goff.p + m, 8, cudaMemcpyDeviceToHost, c->stream));
+  SOF_CUDA(cudaMemcpyAsync(c->pinned_scalar + 1, c->bin_scalar.p + 1, 8, cudaMemcpyDeviceToHost, c->stream));
+  SOF_CUDA(cudaMemcpyAsync(c->pinned_scalar + 2, c->bin_scalar.p + 2, 8, cudaMemcpyDeviceToHost, c->stream));
+  SOF_CUDA(cudaStreamSynchronize(c->stream));
+  std::memcpy(&M, c->pinned_scalar, 8);
+  std::memcpy(&overflow, c->pinned_scalar + 1, sizeof(int));
+  std::memcpy(&nflag_h, c->pinned_scalar + 2, 8);
+  if (m > 0 && overflow) {  // a long tie run (never seen in practice): the full 64-bit sort
+    c->zkey_aux.ensure(m);
+    k_gather_keys<<<grid_for(m, 256), 256, 0, c->stream>>>(m, c->gidx_in.p, c->zkey_in.p, c->zkey_aux.p);
+    SOF_LAUNCHED(c);
+    sort_pairs_u64(c, c->zkey_aux.p, c->zkey_out.p, c->gidx_in.p, c->gidx_out.p, m, 64);
+    offsets();
+    M = read_scalar(c, c->goff.p + m);
+  }
+  c->bin_nflag = nflag_h;
   if (charge_cache && &b != &c->bind_scratch[0] && &b != &c->bind_scratch[1]) {
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
@@ -721,7 +752,8 @@ static void build_binding_tail(sof_ctx* c, int view, int ts, Binding& b, int64_t
   // (on the binding that is served: the view's cache or a scratch slot)
   b.nb = 0;
   b.nx = 0;
-  if (b.live && c->n > 0) {  // the counted Gaussians: (min_z key, index) order, index order kept on ties
+  if (b.live && c->n > 0 && c->bin_nflag > 0) {  // the counted Gaussians: (min_z key, index) order, index
+                                                 // order kept on ties
     size_t bytes = 0;
     thrust::counting_iterator<int32_t> it(0);
     const uint8_t* flags = c->gbehind.p;

@@ -275,7 +275,8 @@ struct sof_ctx {
   sofk::DBuf<uint8_t> gbehind;     // per Gaussian: gauss_behind (live bindings)
   sofk::DBuf<uint64_t> zkey_in, zkey_out, zkey_aux;
   sofk::DBuf<char> loss_buf;       // batched training-loss inputs / outputs (k_loss.cu)
-  sofk::DBuf<int64_t> bin_scalar;  // [2] selected count | tie-run overflow flag
+  sofk::DBuf<int64_t> bin_scalar;  // [4] selected count | tie-run overflow flag | count flags
+  int64_t bin_nflag = 0;           // count flags of the binding being built (host copy)
   int64_t bin_m = 0;               // Gaussians with tiles in the current binning
   const unsigned long long* bin_zmax = nullptr;  // bisection-cache binning filter (per tile)
   sofk::BisectScratch bis;
