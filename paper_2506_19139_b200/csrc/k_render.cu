@@ -615,18 +615,21 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   return (uint64_t(hi) << 32) | lo;
 }
 
+__device__ __forceinline__ uint32_t shfl_xor_key(uint32_t v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ uint64_t shfl_xor_key(uint64_t v, int m) { return shfl_xor_u64(v, m); }
+
 // in-thread stage: elements e and e + ES (ES < E, compile time), position i = E tid + e
-template <int E, int ES>
-__device__ __forceinline__ void keys_inthread(uint64_t (&k)[E], int size, int tid) {
+template <int E, int ES, typename K>
+__device__ __forceinline__ void keys_inthread(K (&k)[E], int size, int tid) {
   if constexpr (ES < E) {
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if ((e & ES) == 0) {
         const bool asc = ((E * tid + e) & size) == 0;
-        const uint64_t a = k[e], b = k[e + ES];
-        const bool sw = (b < a) == asc;  // keys are distinct (equal only as padding)
-        k[e] = sw ? b : a;
-        k[e + ES] = sw ? a : b;
+        const K a = k[e], b = k[e + ES];
+        const K lo = min(a, b), hi = max(a, b);  // keys are distinct (equal only as padding)
+        k[e] = asc ? lo : hi;
+        k[e + ES] = asc ? hi : lo;
       }
   }
 }
@@ -634,97 +637,159 @@ __device__ __forceinline__ void keys_inthread(uint64_t (&k)[E], int size, int ti
 // Ascending bitonic sort of NT x E keys in the blocked layout (position i = E tid + e):
 // strides below E are compare-exchanges inside a thread, larger ones pair element e of
 // threads tid and tid ^ (stride / E) — through shuffles inside a warp, through shared
-// memory (xb: NT x E u64) across warps. Small strides, the most frequent in the network,
+// memory (xb: NT x E keys) across warps. Small strides, the most frequent in the network,
 // thus cost no data movement.
-template <int NT, int E>
-__device__ __forceinline__ void sort_keys(uint64_t (&k)[E], int tid, int w, uint64_t* xb) {
-  constexpr int M = NT * E;
-  const int lane = tid & 31;
-#pragma unroll 1
-  for (int lg = 1; (1 << lg) <= M; ++lg) {
-    const int size = 1 << lg;
-#pragma unroll 1
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride < E) {
-        if (stride == 1) keys_inthread<E, 1>(k, size, tid);
-        else if (stride == 2) keys_inthread<E, 2>(k, size, tid);
-        else if (stride == 4) keys_inthread<E, 4>(k, size, tid);
-        else if (stride == 8) keys_inthread<E, 8>(k, size, tid);
-      } else {
-        const int ts = stride / E;  // partner thread distance
-        const bool lower = (tid & ts) == 0;
-        if (ts < 32) {
+template <int NT, int E, typename K>
+__device__ __forceinline__ void bitonic_stage(K (&k)[E], int size, int stride, int tid, int w, K* xb) {
+  if (stride < E) {
+    if (stride == 1) keys_inthread<E, 1>(k, size, tid);
+    else if (stride == 2) keys_inthread<E, 2>(k, size, tid);
+    else if (stride == 4) keys_inthread<E, 4>(k, size, tid);
+    else if (stride == 8) keys_inthread<E, 8>(k, size, tid);
+  } else {
+    const int ts = stride / E;  // partner thread distance
+    const bool lower = (tid & ts) == 0;
+    if (ts < 32) {
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const uint64_t p = shfl_xor_u64(k[e], ts);
-            const bool take_min = lower == (((E * tid + e) & size) == 0);
-            k[e] = ((p < k[e]) == take_min) ? p : k[e];  // distinct keys (equal only as padding)
-          }
-        } else {  // partner thread in another warp: exchange through shared memory
-#pragma unroll
-          for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
-          sorter_sync<NT>(w);
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const uint64_t p = xb[E * (tid ^ ts) + e];
-            const bool take_min = lower == (((E * tid + e) & size) == 0);
-            k[e] = ((p < k[e]) == take_min) ? p : k[e];
-          }
-          sorter_sync<NT>(w);
-        }
+      for (int e = 0; e < E; ++e) {
+        const K p = shfl_xor_key(k[e], ts);
+        const bool take_min = lower == (((E * tid + e) & size) == 0);
+        k[e] = take_min ? min(p, k[e]) : max(p, k[e]);  // distinct keys (equal only as padding)
       }
+    } else {  // partner thread in another warp: exchange through shared memory
+#pragma unroll
+      for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
+      sorter_sync<NT>(w);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const K p = xb[E * (tid ^ ts) + e];
+        const bool take_min = lower == (((E * tid + e) & size) == 0);
+        k[e] = take_min ? min(p, k[e]) : max(p, k[e]);
+      }
+      sorter_sync<NT>(w);
     }
   }
-  (void)lane;
 }
 
-// Sorts S[0, n) (n <= NT E) in place. buf: NT E x 16 B of shared memory. Returns false
-// (nothing changed) when the t* span does not fit the key.
-template <int NT, int E>
+// Ascending bitonic sort of NT x E keys in the blocked layout (position i = E tid + e):
+// strides below E are compare-exchanges inside a thread, larger ones pair element e of
+// threads tid and tid ^ (stride / E) — through shuffles inside a warp, through shared
+// memory (xb: NT x E keys) across warps. Small strides, the most frequent in the network,
+// thus cost no data movement. Networks up to SOF_SORT_UNROLL keys are unrolled completely
+// (stage parameters and direction bits become constants).
+#ifndef SOF_SORT_UNROLL
+#define SOF_SORT_UNROLL 64
+#endif
+template <int NT, int E, typename K>
+__device__ __forceinline__ void sort_keys(K (&k)[E], int tid, int w, K* xb) {
+  constexpr int M = NT * E;
+  if constexpr (M <= SOF_SORT_UNROLL) {
+#pragma unroll
+    for (int lg = 1; (1 << lg) <= M; ++lg)
+#pragma unroll
+      for (int stride = (1 << lg) >> 1; stride > 0; stride >>= 1) bitonic_stage<NT, E>(k, 1 << lg, stride, tid, w, xb);
+  } else {
+#pragma unroll 1
+    for (int lg = 1; (1 << lg) <= M; ++lg)
+#pragma unroll 1
+      for (int stride = (1 << lg) >> 1; stride > 0; stride >>= 1) bitonic_stage<NT, E>(k, 1 << lg, stride, tid, w, xb);
+  }
+}
+
+// log2 of a power of two, at compile time
+constexpr int ilog2c(int m) { return m <= 1 ? 0 : 1 + ilog2c(m >> 1); }
+
+// Sorts S[0, n) (n <= NT E) in place by (t*, index). buf: NT E x 16 B of shared memory.
+// The sort key is the entry's slot below a monotone image of t*: t* > 0, so its bit
+// pattern orders like the value, and q = (bits - min bits) >> sh is non-decreasing in t*.
+// K = uint32_t (SORT32, the default): slot bits = log2(NT E), q takes the rest and sh is
+// whatever makes the slice's span fit — never fails; entries with equal q (t* within
+// 2^(sh-52) relative of each other, or equal) are put in exact (t*, index) order
+// afterwards, each run of equal q by its own thread. K = uint64_t: sh = 0 (q is the exact
+// bit distance, equal q only for equal t*); returns false (nothing changed) when the t*
+// span does not fit the key.
+template <int NT, int E, typename K>
 __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int tid, int w, void* buf,
                                                 uint64_t* red) {
   constexpr int M = NT * E;
   static_assert(M <= 4096, "slot bits");
-  constexpr int SB = (M <= 512) ? 9 : 12;  // slot bits
-  constexpr uint64_t kLow = (uint64_t(1) << SB) - 1;
+  constexpr bool k32 = sizeof(K) == 4;
+  constexpr int SB = k32 ? ilog2c(M) : ((M <= 512) ? 9 : 12);  // slot bits
+  static_assert(!k32 || (1 << SB) == M, "power-of-two slice capacity");
+  constexpr int QB = 8 * int(sizeof(K)) - SB;  // bits of q
+  constexpr K kLow = (K(1) << SB) - 1;
   uint64_t tb[E];
   uint64_t lo = ~uint64_t(0), hi = 0;
+  int sh = 0;
+  if constexpr (k32) {
+    // the span only sets the shift: reduce the high words (one REDUX each) and take
+    // lo = (min high word) << 32, which only coarsens q by at most one bit
+    uint32_t lw = ~0u, hw = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = E * tid + e;
+      tb[e] = (i < n) ? uint64_t(__double_as_longlong(S[i].t)) : 0;
+      if (i < n) {
+        lw = min(lw, uint32_t(tb[e] >> 32));
+        hw = max(hw, uint32_t(tb[e] >> 32));
+      }
+    }
+    lw = __reduce_min_sync(0xffffffffu, lw);
+    hw = __reduce_max_sync(0xffffffffu, hw);
+    if (NT > 32) {  // across the warps of the CTA
+      if ((tid & 31) == 0) {
+        red[2 * (tid >> 5)] = lw;
+        red[2 * (tid >> 5) + 1] = hw;
+      }
+      __syncthreads();
+      for (int k = 0; k < NT / 32; ++k) {
+        lw = min(lw, uint32_t(red[2 * k]));
+        hw = max(hw, uint32_t(red[2 * k + 1]));
+      }
+      __syncthreads();
+    }
+    lo = uint64_t(lw) << 32;
+    const uint64_t span = ((uint64_t(hw) << 32) | 0xffffffffu) - lo;
+    const int need = 64 - __clzll((long long)span);  // bits of the span
+    sh = need > QB ? need - QB : 0;
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = E * tid + e;
+      tb[e] = (i < n) ? uint64_t(__double_as_longlong(S[i].t)) : 0;
+      if (i < n) {
+        lo = min(lo, tb[e]);
+        hi = max(hi, tb[e]);
+      }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      lo = min(lo, shfl_xor_u64(lo, s));
+      hi = max(hi, shfl_xor_u64(hi, s));
+    }
+    if (NT > 32) {  // across the warps of the CTA
+      if ((tid & 31) == 0) {
+        red[2 * (tid >> 5)] = lo;
+        red[2 * (tid >> 5) + 1] = hi;
+      }
+      __syncthreads();
+      for (int k = 0; k < NT / 32; ++k) {
+        lo = min(lo, red[2 * k]);
+        hi = max(hi, red[2 * k + 1]);
+      }
+      __syncthreads();
+    }
+    if (hi - lo >= (uint64_t(1) << QB)) return false;
+  }
+  K k[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = E * tid + e;
-    tb[e] = (i < n) ? uint64_t(__double_as_longlong(S[i].t)) : 0;
-    if (i < n) {
-      lo = min(lo, tb[e]);
-      hi = max(hi, tb[e]);
-    }
+    k[e] = (i < n) ? ((K((tb[e] - lo) >> sh) << SB) | K(i)) : ~K(0);
   }
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) {
-    lo = min(lo, shfl_xor_u64(lo, s));
-    hi = max(hi, shfl_xor_u64(hi, s));
-  }
-  if (NT > 32) {  // across the warps of the CTA
-    if ((tid & 31) == 0) {
-      red[2 * (tid >> 5)] = lo;
-      red[2 * (tid >> 5) + 1] = hi;
-    }
-    __syncthreads();
-    for (int k = 0; k < NT / 32; ++k) {
-      lo = min(lo, red[2 * k]);
-      hi = max(hi, red[2 * k + 1]);
-    }
-    __syncthreads();
-  }
-  if (hi - lo >= (uint64_t(1) << (64 - SB))) return false;
-  uint64_t k[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = E * tid + e;
-    k[e] = (i < n) ? (((tb[e] - lo) << SB) | uint64_t(i)) : ~uint64_t(0);
-  }
-  uint64_t* xb = static_cast<uint64_t*>(buf);
+  K* xb = static_cast<K*>(buf);
   sort_keys<NT, E>(k, tid, w, xb);
-  // equal t* at neighbouring positions: order by Gaussian index (rare)
+  // runs of equal q at neighbouring positions: exact (t*, index) order inside each run
 #pragma unroll
   for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
   sorter_sync<NT>(w);
@@ -732,20 +797,27 @@ __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = E * tid + e;
-    if (i + 1 < n && (xb[i] >> SB) == (xb[i + 1] >> SB)) tie = true;
-  }
-  const bool any_tie = (NT == 32) ? __any_sync(0xffffffffu, tie) : __syncthreads_or(tie);
-  if (any_tie) {
-    if (tid == 0)
-      for (int i = 1; i < n; ++i) {  // insertion sort on the index inside equal-t* runs
-        const uint64_t v = xb[i];
-        int j = i - 1;
-        while (j >= 0 && (xb[j] >> SB) == (v >> SB) && S[v & kLow].idx < S[xb[j] & kLow].idx) {
+    if (i + 1 < n && (xb[i] >> SB) == (xb[i + 1] >> SB) && (i == 0 || (xb[i - 1] >> SB) != (xb[i] >> SB))) {
+      // a run starts at i (reads of other runs' keys see only their q, which no permutation
+      // inside a run changes): insertion sort of [i, end) by this thread
+      tie = true;
+      const K q = xb[i] >> SB;
+      int end = i + 2;
+      while (end < n && (xb[end] >> SB) == q) ++end;
+      for (int a = i + 1; a < end; ++a) {
+        const K v = xb[a];
+        const REnt ev = ld_rent(S + (v & kLow));
+        int j = a - 1;
+        while (j >= i && rent_less(ev, ld_rent(S + (xb[j] & kLow)))) {
           xb[j + 1] = xb[j];
           --j;
         }
         xb[j + 1] = v;
       }
+    }
+  }
+  const bool any_tie = (NT == 32) ? __any_sync(0xffffffffu, tie) : __syncthreads_or(tie);
+  if (any_tie) {
     sorter_sync<NT>(w);
 #pragma unroll
     for (int e = 0; e < E; ++e) k[e] = xb[E * tid + e];
@@ -763,6 +835,12 @@ __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int
   sorter_sync<NT>(w);
   return true;
 }
+
+#ifndef SOF_SORT64
+using SortKey = uint32_t;
+#else
+using SortKey = uint64_t;
+#endif
 
 __device__ __forceinline__ void swap_rent(REnt* S, int64_t a, int64_t b) {
   const REnt t = ld_rent(S + a);
@@ -815,10 +893,10 @@ __global__ void __launch_bounds__(kSortWarps * 32, 4) k_rsort(int64_t q0, int64_
     }
     if (cn <= 1) continue;
     bool done = false;
-    if (cn <= 32) done = sort_slice_keys<32, 1>(S, cn, lane, w, sbuf[w], nullptr);
-    else if (cn <= 64) done = sort_slice_keys<32, 2>(S, cn, lane, w, sbuf[w], nullptr);
-    else if (cn <= 128) done = sort_slice_keys<32, 4>(S, cn, lane, w, sbuf[w], nullptr);
-    else if (cn <= 256) done = sort_slice_keys<32, 8>(S, cn, lane, w, sbuf[w], nullptr);
+    if (cn <= 32) done = sort_slice_keys<32, 1, SortKey>(S, cn, lane, w, sbuf[w], nullptr);
+    else if (cn <= 64) done = sort_slice_keys<32, 2, SortKey>(S, cn, lane, w, sbuf[w], nullptr);
+    else if (cn <= 128) done = sort_slice_keys<32, 4, SortKey>(S, cn, lane, w, sbuf[w], nullptr);
+    else if (cn <= 256) done = sort_slice_keys<32, 8, SortKey>(S, cn, lane, w, sbuf[w], nullptr);
     if (!done && lane == 0) {  // longer slices, or a t* span past the 55-bit key
       big[atomicAdd(big_cnt, 1)] = int32_t(q);
       atomicAdd(big_cnt + 1, 1);  // frame total (stats)
@@ -840,7 +918,7 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_rsort_mid(const int64_t* __
     const int64_t q = big[bi];
     const int n = int(ncon[q]);
     REnt* S = E + (poff[q] - base);
-    const bool done = (n <= 512) && sort_slice_keys<32, 16>(S, n, lane, w, sdyn + w * 512 * 16, nullptr);
+    const bool done = (n <= 512) && sort_slice_keys<32, 16, SortKey>(S, n, lane, w, sdyn + w * 512 * 16, nullptr);
     if (!done && lane == 0) huge[atomicAdd(huge_cnt, 1)] = int32_t(q);
   }
 }
@@ -858,8 +936,8 @@ __global__ void __launch_bounds__(256) k_rsort_big(const int64_t* __restrict__ p
     REnt* S = E + (poff[q] - base);
     bool done = false;
     const int t = threadIdx.x;
-    if (n <= 1024) done = sort_slice_keys<256, 4>(S, int(n), t, 0, sdyn, red);
-    else if (n <= 4096) done = sort_slice_keys<256, 16>(S, int(n), t, 0, sdyn, red);
+    if (n <= 1024) done = sort_slice_keys<256, 4, SortKey>(S, int(n), t, 0, sdyn, red);
+    else if (n <= 4096) done = sort_slice_keys<256, 16, SortKey>(S, int(n), t, 0, sdyn, red);
     if (!done) sort_slice_global(S, n);
     __syncthreads();
   }
