@@ -633,12 +633,32 @@ __device__ __forceinline__ void keys_inthread(K (&k)[E], int size, int tid) {
       }
   }
 }
+// compare-exchange of element e with element e of thread tid ^ (stride / E) (stride >= E)
+template <int NT, int E, typename K>
+__device__ __forceinline__ void bitonic_cross(K (&k)[E], int size, int stride, int tid, int w, K* xb) {
+  const int ts = stride / E;  // partner thread distance
+  const bool lower = (tid & ts) == 0;
+  if (ts < 32) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const K p = shfl_xor_key(k[e], ts);
+      const bool take_min = lower == (((E * tid + e) & size) == 0);
+      k[e] = take_min ? min(p, k[e]) : max(p, k[e]);  // distinct keys (equal only as padding)
+    }
+  } else {  // partner thread in another warp: exchange through shared memory
+#pragma unroll
+    for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
+    sorter_sync<NT>(w);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const K p = xb[E * (tid ^ ts) + e];
+      const bool take_min = lower == (((E * tid + e) & size) == 0);
+      k[e] = take_min ? min(p, k[e]) : max(p, k[e]);
+    }
+    sorter_sync<NT>(w);
+  }
+}
 
-// Ascending bitonic sort of NT x E keys in the blocked layout (position i = E tid + e):
-// strides below E are compare-exchanges inside a thread, larger ones pair element e of
-// threads tid and tid ^ (stride / E) — through shuffles inside a warp, through shared
-// memory (xb: NT x E keys) across warps. Small strides, the most frequent in the network,
-// thus cost no data movement.
 template <int NT, int E, typename K>
 __device__ __forceinline__ void bitonic_stage(K (&k)[E], int size, int stride, int tid, int w, K* xb) {
   if (stride < E) {
@@ -647,27 +667,7 @@ __device__ __forceinline__ void bitonic_stage(K (&k)[E], int size, int stride, i
     else if (stride == 4) keys_inthread<E, 4>(k, size, tid);
     else if (stride == 8) keys_inthread<E, 8>(k, size, tid);
   } else {
-    const int ts = stride / E;  // partner thread distance
-    const bool lower = (tid & ts) == 0;
-    if (ts < 32) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const K p = shfl_xor_key(k[e], ts);
-        const bool take_min = lower == (((E * tid + e) & size) == 0);
-        k[e] = take_min ? min(p, k[e]) : max(p, k[e]);  // distinct keys (equal only as padding)
-      }
-    } else {  // partner thread in another warp: exchange through shared memory
-#pragma unroll
-      for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
-      sorter_sync<NT>(w);
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const K p = xb[E * (tid ^ ts) + e];
-        const bool take_min = lower == (((E * tid + e) & size) == 0);
-        k[e] = take_min ? min(p, k[e]) : max(p, k[e]);
-      }
-      sorter_sync<NT>(w);
-    }
+    bitonic_cross<NT, E>(k, size, stride, tid, w, xb);
   }
 }
 
@@ -689,10 +689,19 @@ __device__ __forceinline__ void sort_keys(K (&k)[E], int tid, int w, K* xb) {
 #pragma unroll
       for (int stride = (1 << lg) >> 1; stride > 0; stride >>= 1) bitonic_stage<NT, E>(k, 1 << lg, stride, tid, w, xb);
   } else {
-#pragma unroll 1
-    for (int lg = 1; (1 << lg) <= M; ++lg)
-#pragma unroll 1
+    // sizes up to E: inside the thread, unrolled
+#pragma unroll
+    for (int lg = 1; (1 << lg) <= E; ++lg)
+#pragma unroll
       for (int stride = (1 << lg) >> 1; stride > 0; stride >>= 1) bitonic_stage<NT, E>(k, 1 << lg, stride, tid, w, xb);
+    // larger sizes: the partner-thread strides in a loop, then the in-thread tail unrolled
+#pragma unroll 1
+    for (int size = 2 * E; size <= M; size <<= 1) {
+#pragma unroll 1
+      for (int stride = size >> 1; stride >= E; stride >>= 1) bitonic_cross<NT, E>(k, size, stride, tid, w, xb);
+#pragma unroll
+      for (int stride = E >> 1; stride > 0; stride >>= 1) bitonic_stage<NT, E>(k, size, stride, tid, w, xb);
+    }
   }
 }
 

@@ -114,6 +114,28 @@ def test_render_long_slices_with_ties(ref, n):
         assert (st[0][2] > 0) == (n > 256)
 
 
+@pytest.mark.parametrize("n", [40, 200, 900])
+def test_render_near_ties_in_quantised_keys(ref, n):
+    """Distinct t* a few ulp apart next to far-away Gaussians: the sort key keeps only the
+    top bits of the t* span, so these share a key and the per-run exact (t*, index) fix-up
+    orders them; indices run against t* (later Gaussians nearer) to make every run need it."""
+    rng = np.random.default_rng(5)
+    k = n - n // 8
+    pos = np.zeros((n, 3))
+    pos[:k, 2] = -np.arange(k) * 1e-13 + rng.integers(0, 3, k) * 1e-14
+    pos[:k, :2] = rng.normal(0, 1e-3, (k, 2))
+    pos[k:, 2] = rng.uniform(1.0, 3.0, n - k)
+    pos[k:, :2] = rng.normal(0, 0.03, (n - k, 2))
+    scale = np.full((n, 3), 0.35)
+    op = rng.uniform(0.01, 0.05, n)
+    scene = Scene(pos, scale, np.tile([1.0, 0, 0, 0], (n, 1)), op, rng.uniform(0, 1, (n, 3)))
+    cams = ref.look_at([0, 0, -4.0], [0, 0, 0], [0, 1, 0], 40.0, 40.0, 20, 20)
+    rc = ref.context(scene, cams)
+    views = sof.ViewSet.build(scene, cams, ctx=sof.Context(0))
+    for exact in (True, False):
+        check(rc, views, 0, exact, [])
+
+
 # ---- normals (render.hpp:58-107) and the `sof render` outputs (sof_cli.cpp:122-130) ------------
 
 def _plain_cam(w, h, cx, cy, f):
