@@ -962,7 +962,13 @@ struct RenderOut {
 };
 
 
-constexpr int kBlendCap = 640;  // records staged per tile (74 KB); later list positions read global memory
+#ifndef SOF_BLEND_CAP
+#define SOF_BLEND_CAP 640
+#endif
+#ifndef SOF_BLEND_MINB
+#define SOF_BLEND_MINB 1
+#endif
+constexpr int kBlendCap = SOF_BLEND_CAP;  // records staged per tile (74 KB); later list positions read global memory
 constexpr int kBlendSmem = kBlendCap * (14 * 8 + 4);
 
 __device__ __forceinline__ BRec brec_global(const RRec* __restrict__ recs, const double* __restrict__ dc, int g) {
@@ -1037,7 +1043,7 @@ __device__ __forceinline__ double alpha_at_depth(const BRec& r, double a, double
 // (:104-108) over the prefix up to the median; phase C blends the rest and extends the
 // product in the same pass. Lanes leave phase A at different entries, but every phase is
 // one loop per lane, so the warp never serialises one lane's prefix after another's.
-__global__ void __launch_bounds__(kRPix) k_rblend(Cam cam, int tiles_x, int tile0, const int64_t* __restrict__ toff,
+__global__ void __launch_bounds__(kRPix, SOF_BLEND_MINB) k_rblend(Cam cam, int tiles_x, int tile0, const int64_t* __restrict__ toff,
                                                   const int32_t* __restrict__ ent, const int64_t* __restrict__ poff,
                                                   int64_t base, const uint32_t* __restrict__ ncon,
                                                   const REnt* __restrict__ E, const RRec* __restrict__ recs,
