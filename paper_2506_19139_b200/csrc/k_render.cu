@@ -883,7 +883,10 @@ constexpr int kWarpSortCap = 256;   // one warp: 8 keys per lane, 4 KB of shared
 constexpr int kCtaSortCap = 4096;   // one CTA of 256: 16 keys per thread, 64 KB
 
 // One warp per pixel (grid-stride over the band's pixels), 8 warps per CTA.
-__global__ void __launch_bounds__(kSortWarps * 32, 4) k_rsort(int64_t q0, int64_t nq, const int64_t* __restrict__ poff,
+#ifndef SOF_RSORT_MINB
+#define SOF_RSORT_MINB 4
+#endif
+__global__ void __launch_bounds__(kSortWarps * 32, SOF_RSORT_MINB) k_rsort(int64_t q0, int64_t nq, const int64_t* __restrict__ poff,
                                                              int64_t base, const uint32_t* __restrict__ ncon, REnt* E,
                                                              int32_t* big, int32_t* big_cnt) {
   __shared__ __align__(16) REnt sbuf[kSortWarps][kWarpSortCap];
@@ -1474,7 +1477,10 @@ void sort_slices(sof_ctx* c, int64_t q0, int64_t nq, const int64_t* poff, int64_
   int32_t* qmid = rs.big.p;  // rs.big[0, n) served the binning; reused for the sort queues
   int32_t* qhuge = rs.big.p + nq;
   k_rsort<<<sort_grid, kSortWarps * 32, 0, st>>>(q0, nq, poff, base, ncon, E, qmid, rs.big_cnt.p + 1);
-  k_rsort_mid<<<148 * 2, kSortWarps * 32, kSortWarps * 512 * 16, st>>>(poff, base, ncon, E, qmid, rs.big_cnt.p + 1,
+#ifndef SOF_MID_CTAS
+#define SOF_MID_CTAS 3
+#endif
+  k_rsort_mid<<<148 * SOF_MID_CTAS, kSortWarps * 32, kSortWarps * 512 * 16, st>>>(poff, base, ncon, E, qmid, rs.big_cnt.p + 1,
                                                                       qhuge, rs.big_cnt.p + 3);
   k_rsort_big<<<148, 256, kCtaSortCap * 16, st>>>(poff, base, ncon, E, qhuge, rs.big_cnt.p + 3);
   c->launches += 3;
