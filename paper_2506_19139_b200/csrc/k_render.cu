@@ -25,10 +25,10 @@
 //      256 threads evaluate them with the reference's FP64 expressions; every contribution
 //      lands in its pixel's slice as REnt {t*, list position, Gaussian index};
 //   R3 k_rsort: one warp per pixel sorts its slice by (t*, index): a register bitonic
-//      network on 64-bit keys ((bits(t*) - bits(min t*)) << 9 | slot), equal-t* runs then
-//      re-ordered by index, the entries permuted once through shared memory; slices past
-//      256 entries or past the key's span go to k_rsort_mid (512), then k_rsort_big (one
-//      CTA, up to 4096 in shared memory, a global-memory network beyond);
+//      network on 32-bit keys (the top bits of bits(t*) - bits(min t*) above the slot),
+//      runs of equal key then put in exact (t*, index) order, the entries permuted once
+//      through shared memory; slices past 256 entries go to k_rsort_mid (512), then
+//      k_rsort_big (one CTA, up to 4096 in shared memory, a global-memory network beyond);
 //   R4 k_rblend: one thread per pixel walks its sorted slice: colour and transmittance
 //      (render_pixel :204-210), the median (find_median :129-141), the exact depth
 //      (:157-166) and the opacity at the depth (opacity_along_ray :104-108) — all in the
@@ -565,15 +565,18 @@ __global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0
 
 // ---- R3: per-pixel sort by (t*, index), in place ---------------------------------------------------
 //
-// A pixel's contributions are sorted by 64-bit keys held in registers: t* > 0, so its bit
-// pattern orders like the value, and k = ((bits(t*) - bits(min t*)) << 9) | slot is an
-// exact key of t* whenever the slice's t* span is below 2^55 ulps (checked; a wider span
-// takes the exact fallback). Keys equal above the slot bits are equal t* values, ordered
-// by Gaussian index afterwards (rare). The bitonic network runs on NT threads x E keys in
-// the striped layout (position i = NT e + tid): partners within a warp exchange through
-// shuffles, partners in another warp through shared memory, partners in the same thread
-// in registers. Only 8 bytes move per key and stage (sorting the 16-byte entries
+// A pixel's contributions are sorted by keys held in registers: t* > 0, so its bit pattern
+// orders like the value, and q = (bits(t*) - lo) >> sh is non-decreasing in t*. The key is
+// q above the entry's slot (32 bits: log2(capacity) slot bits, q the rest, sh chosen from
+// the slice's span so that it always fits); the order it gives is exact except inside
+// runs of equal q (t* within 2^(sh-52) relative, or equal), which one thread per run then
+// re-orders by the exact (t*, index) comparison. The bitonic network runs on NT threads x
+// E keys in the blocked layout (position i = E tid + e): partners within a warp exchange
+// through shuffles, partners in another warp through shared memory, partners in the same
+// thread in registers. Only 4 bytes move per key and stage (sorting the 16-byte entries
 // themselves was shared-memory-bandwidth bound); the entries are permuted once at the end.
+// Measured against the round-1 64-bit keys (exact bit distance << 9, SOF_SORT64 builds
+// it): k_rsort 5.1 -> 3.6 ms per C2 view.
 
 __device__ __forceinline__ bool rent_less(const REnt& a, const REnt& b) {
   return a.t < b.t || (a.t == b.t && a.idx < b.idx);
@@ -909,14 +912,14 @@ __global__ void __launch_bounds__(kSortWarps * 32, SOF_RSORT_MINB) k_rsort(int64
     else if (cn <= 64) done = sort_slice_keys<32, 2, SortKey>(S, cn, lane, w, sbuf[w], nullptr);
     else if (cn <= 128) done = sort_slice_keys<32, 4, SortKey>(S, cn, lane, w, sbuf[w], nullptr);
     else if (cn <= 256) done = sort_slice_keys<32, 8, SortKey>(S, cn, lane, w, sbuf[w], nullptr);
-    if (!done && lane == 0) {  // longer slices, or a t* span past the 55-bit key
+    if (!done && lane == 0) {  // longer slices (or, SOF_SORT64 only, a t* span past the 55-bit key)
       big[atomicAdd(big_cnt, 1)] = int32_t(q);
       atomicAdd(big_cnt + 1, 1);  // frame total (stats)
     }
   }
 }
 
-// The queued slices up to 512 entries (or with a t* span past the warp sort's key): one
+// The queued slices up to 512 entries (SOF_SORT64: or with a t* span past the warp sort's key): one
 // warp per pixel with 8 KB of shared memory; longer ones go to the CTA sort.
 __global__ void __launch_bounds__(kSortWarps * 32) k_rsort_mid(const int64_t* __restrict__ poff, int64_t base,
                                                                const uint32_t* __restrict__ ncon, REnt* E,
