@@ -879,17 +879,39 @@ __device__ __forceinline__ int warp_tile_add(int* counters, int bin, bool valid)
 // cells) or 1.
 // TS: the tile size when it is the default 16 (shifts and masks instead of integer
 // divisions by a runtime value), 0 for any other tile size.
+#ifndef SOF_SCHED_PTS
+#define SOF_SCHED_PTS 1
+#endif
+constexpr int kSchedPts = SOF_SCHED_PTS;  // points per thread (loads of all issued first)
 template <int TS>
 __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
                              const double* __restrict__ xyz, Cam cam, int ts, int tiles_x,
                              bool single_bin, int S, const uint8_t* __restrict__ skip, int32_t* tile_of,
                              int* tile_cnt) {
-  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  int tile = -1;
-  if (k < n) {
-    const int64_t i = cand ? cand[k] : k;
-    if (!(skip && skip[i])) {
-      const PointTile pt = point_tile<TS>(cam, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], ts, tiles_x);
+  const int64_t k0 = blockIdx.x * int64_t(blockDim.x) * kSchedPts + threadIdx.x;
+  double px[kSchedPts], py[kSchedPts], pz[kSchedPts];
+  bool live[kSchedPts];
+#pragma unroll
+  for (int j = 0; j < kSchedPts; ++j) {
+    const int64_t k = k0 + int64_t(j) * blockDim.x;
+    live[j] = false;
+    px[j] = py[j] = pz[j] = 0.0;
+    if (k < n) {
+      const int64_t i = cand ? cand[k] : k;
+      if (!(skip && skip[i])) {
+        live[j] = true;
+        px[j] = xyz[3 * i];
+        py[j] = xyz[3 * i + 1];
+        pz[j] = xyz[3 * i + 2];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kSchedPts; ++j) {
+    const int64_t k = k0 + int64_t(j) * blockDim.x;
+    int tile = -1;
+    if (live[j]) {
+      const PointTile pt = point_tile<TS>(cam, px[j], py[j], pz[j], ts, tiles_x);
       // bin = tile x (4x4 cell of pixels inside the tile): points of one cell are
       // adjacent, so a warp covers a compact screen region (coherent conic culls)
       if (pt.tile >= 0) {
@@ -905,9 +927,9 @@ __global__ void k_sched_tile(int64_t n, const int32_t* __restrict__ cand,
         }
       }
     }
-    tile_of[k] = tile;
+    if (k < n) tile_of[k] = tile;
+    warp_tile_add(tile_cnt, tile, tile >= 0);
   }
-  warp_tile_add(tile_cnt, tile, tile >= 0);
 }
 
 struct NotPruned {
@@ -918,7 +940,10 @@ struct NotPruned {
 // Scatter pass: kScatterItems warp-contiguous groups of 32 candidates per warp, so
 // that each warp keeps several slot-reserving atomics in flight (the returned base is
 // a long round trip; one item per thread left this kernel latency-bound).
-constexpr int kScatterItems = 4;
+#ifndef SOF_SCATTER_ITEMS
+#define SOF_SCATTER_ITEMS 4
+#endif
+constexpr int kScatterItems = SOF_SCATTER_ITEMS;
 __global__ void k_sched_scatter(int64_t n, const int32_t* __restrict__ cand,
                                 const int32_t* __restrict__ tile_of,
                                 const int* __restrict__ tile_off, int* tile_cur, int32_t* order) {
@@ -2264,10 +2289,10 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
     int* tile_cur = s.tile_cnt.p + (NB + 1);
     const int32_t* cand = use_list ? s.active.p : nullptr;
     if (tile_size == 16)
-      k_sched_tile<16><<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
+      k_sched_tile<16><<<grid_for((ncand + kSchedPts - 1) / kSchedPts, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
                                                                     !tiled, S, skip, s.tile_of.p, s.tile_cnt.p);
     else
-      k_sched_tile<0><<<grid_for(ncand, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
+      k_sched_tile<0><<<grid_for((ncand + kSchedPts - 1) / kSchedPts, 256), 256, 0, c->stream>>>(ncand, cand, xyz, cam, tile_size, tiles_x,
                                                                    !tiled, S, skip, s.tile_of.p, s.tile_cnt.p);
     SOF_LAUNCHED(c);
     exclusive_scan_i32(c, s.tile_cnt.p, s.tile_off.p, NB + 1);

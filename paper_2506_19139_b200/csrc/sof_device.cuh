@@ -118,7 +118,12 @@ __host__ __device__ inline float float_down(double x) {
 
 // View-independent per-Gaussian data (the parts of precompute.hpp:65-75 that do
 // not depend on the camera, hoisted out of the per-view loop).
-struct GaussStatic {
+#ifndef SOF_GS_ALIGN
+#define SOF_GS_ALIGN 16
+#endif
+// 16-byte aligned (one pad word): the per-view pass loads it with 16-byte loads, half the
+// load instructions of 8-byte ones (that pass was LSU-throttled)
+struct __align__(SOF_GS_ALIGN) GaussStatic {
   double pos[3];
   double scale[3];
   double rot[9];   // toRotationMatrix(q)            (gaussian.hpp:24)
@@ -126,6 +131,9 @@ struct GaussStatic {
   double icf[9];   // full inv_cov (NOT symmetrised: b_vec uses all 9, precompute.hpp:66-72)
   double op;       // filtered_opacity               (gaussian.hpp:67-73)
   double E;        // tight_bound, 0 when dead       (gaussian.hpp:60-64)
+#if SOF_GS_ALIGN == 16
+  double pad = 0.0;
+#endif
 };
 
 // ---- L0: Eigen-shim semantics ---------------------------------------------------------
