@@ -135,7 +135,10 @@ int64_t sof_scene_size(const sof_ctx* ctx);
 /* ---- inputs ----------------------------------------------------------------- */
 /* Replaces the scene half of ViewSet::build (opacity_field.hpp:26-34) and the
  * view-independent half of precompute (precompute.hpp:57-78): uploads the
- * Gaussians and computes Sigma^-1, the filtered opacity and E on the device. */
+ * Gaussians and computes Sigma^-1, the filtered opacity and E on the device.
+ * Non-finite positions, scales or opacities are rejected as precompute does
+ * (precompute.hpp:60-63: "non-finite Gaussian parameters"); the check runs on the
+ * device after the upload, so a rejected call leaves the context without a scene. */
 int sof_set_scene(sof_ctx* ctx, int64_t n, const double* pos, const double* scale,
                   const double* rot_wxyz, const double* opacity, const double* dc,
                   double filter_scale);

@@ -142,12 +142,6 @@ int sof_set_scene(sof_ctx* c, int64_t n, const double* pos, const double* scale,
   return guard(c, [&] {
     if (n < 0 || (n > 0 && (!pos || !scale || !rot || !opacity)))
       throw InvalidArg("invalid scene arrays");
-    // precompute() rejects non-finite parameters (precompute.hpp:60-63)
-    for (int64_t i = 0; i < n; ++i) {
-      bool ok = std::isfinite(opacity[i]);
-      for (int k = 0; k < 3 && ok; ++k) ok = std::isfinite(pos[3 * i + k]) && std::isfinite(scale[3 * i + k]);
-      if (!ok) throw InvalidArg("non-finite Gaussian parameters");
-    }
     c->n = n;
     c->filter_scale = filter_scale;
     upload(c, c->pos, pos, 3 * n);
@@ -159,10 +153,22 @@ int sof_set_scene(sof_ctx* c, int64_t n, const double* pos, const double* scale,
       c->dc.ensure(std::max<int64_t>(3 * n, 1));
       zero_async(c, c->dc.p, int64_t(sizeof(double)) * 3 * n);
     }
+    // precompute() rejects non-finite parameters (precompute.hpp:60-63); checked on the
+    // device, read back with the upload's synchronisation. A rejected scene leaves none.
+    c->d_scalar.ensure(4);
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(c->d_scalar.p);
+    zero_async(c, bad, sizeof(unsigned long long));
+    scene_check_finite(c, bad);
     scene_prep(c);
-    c->has_scene = true;
     invalidate_view_caches(c);
+    SOF_CUDA(cudaMemcpyAsync(c->pinned_scalar, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
+    if (c->pinned_scalar[0] != 0) {
+      c->n = 0;
+      c->has_scene = false;
+      throw InvalidArg("non-finite Gaussian parameters");
+    }
+    c->has_scene = true;
   });
 }
 

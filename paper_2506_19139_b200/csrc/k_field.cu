@@ -167,6 +167,25 @@ __global__ void __launch_bounds__(128, SOF_REC_MINB) k_view_rec_rect(int64_t n, 
   ro.idx[i] = int32_t(i);
 }
 
+// precompute() rejects non-finite parameters (precompute.hpp:60-63): checked on the
+// device (a host loop over the arrays cost ~10 ms per 3M Gaussians of the e2e step)
+__global__ void k_check_finite(int64_t n, const double* __restrict__ pos, const double* __restrict__ scale,
+                               const double* __restrict__ opa, unsigned long long* bad) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  bool ok = true;
+  if (i < n) {
+    ok = isfinite(opa[i]);
+    for (int k = 0; k < 3; ++k) ok = ok && isfinite(pos[3 * i + k]) && isfinite(scale[3 * i + k]);
+  }
+  if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1ull);
+}
+
+void scene_check_finite(sof_ctx* c, unsigned long long* bad) {
+  if (c->n == 0) return;
+  k_check_finite<<<grid_for(c->n, 256), 256, 0, c->stream>>>(c->n, c->pos.p, c->scale.p, c->opa.p, bad);
+  SOF_LAUNCHED(c);
+}
+
 void scene_prep(sof_ctx* c) {
   c->gstat.ensure(c->n);
   if (c->n == 0) return;

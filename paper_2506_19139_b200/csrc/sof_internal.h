@@ -358,6 +358,7 @@ namespace sofk {
 
 // ---- k_field.cu -------------------------------------------------------------------------
 void scene_prep(sof_ctx* c);
+void scene_check_finite(sof_ctx* c, unsigned long long* bad);
 const Rec* view_records(sof_ctx* c, int view);
 const RecF* view_recf(sof_ctx* c, int view);
 const Binding& view_binding(sof_ctx* c, int view, int tile_size, bool live = false);
