@@ -199,6 +199,19 @@ def test_errors(ref):
         ctx.set_scene(scene)
     with pytest.raises(sof.SofError, match="no scene"):
         sof.FieldEvaluator(None, sof.ViewSet(ctx, None, None, 0.0)).label_grid(np.zeros((3, 3)))
+    # the check runs on the device after the upload: a rejected scene replaces a valid one
+    # with none (sof_cuda.h, sof_set_scene)
+    good = ref.random_scene(1, 10, 1.0)
+    ctx.set_scene(good)
+    assert ctx.lib.sof_scene_size(ctx.h) == 10
+    for field, k in (("opacity", (4,)), ("scale", (2, 0)), ("pos", (9, 2))):
+        bad = ref.random_scene(1, 10, 1.0)
+        getattr(bad, field)[k] = np.inf
+        with pytest.raises(ValueError, match="non-finite Gaussian parameters"):
+            ctx.set_scene(bad)
+        assert ctx.lib.sof_scene_size(ctx.h) == -1
+        ctx.set_scene(good)
+        assert ctx.lib.sof_scene_size(ctx.h) == 10
 
 
 def test_label_all_points_pruned_early(ref):
