@@ -1142,12 +1142,28 @@ __device__ __forceinline__ int chunk_limit(const Rec* rp, int cnt, double zp, bo
 #define SOF_PAIR_CULL 1
 #endif
 // stop: the chunk position of the record at which the early stop happened (else -1).
-template <typename F>
+// QUAD: four conics per step first (the grouped bisection: 73 -> 71 ms per C3 step; the
+// label launch is faster with two, 688 vs 696 ms)
+template <bool QUAD = false, typename F>
 __device__ __forceinline__ unsigned scan_chunk(const Rec* rp, int cnt, double zp, float cu, float cv, float cuu,
                                                float cvv, float cuv, bool& done, int& stop, F&& eval_one) {
   bool brk;
   const int lim = chunk_limit(rp, cnt, zp, brk);
   int e = 0;
+  if constexpr (QUAD) {
+    for (; e + 3 < lim; e += 4) {
+      const bool cs[4] = {conic_culls(rp[e], cu, cv, cuu, cvv, cuv), conic_culls(rp[e + 1], cu, cv, cuu, cvv, cuv),
+                          conic_culls(rp[e + 2], cu, cv, cuu, cvv, cuv), conic_culls(rp[e + 3], cu, cv, cuu, cvv, cuv)};
+      if (cs[0] && cs[1] && cs[2] && cs[3]) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (!cs[u] && eval_one(rp[e + u])) {
+          done = true;
+          stop = e + u;
+          return unsigned(e + u + 1);
+        }
+    }
+  }
 #if SOF_PAIR_CULL
   for (; e + 1 < lim; e += 2) {
     const bool c0 = conic_culls(rp[e], cu, cv, cuu, cvv, cuv);
@@ -1671,7 +1687,7 @@ __global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
   uint64_t stop_key = 0;
   int32_t stop_idx = -1;
   auto eval_chunk = [&](const Rec* rp, int cnt) {
-    const unsigned p = scan_chunk(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, stop, eval_one);
+    const unsigned p = scan_chunk<true>(rp, cnt, pr.zp, cu, cv, cuu, cvv, cuv, done, stop, eval_one);
     if (stop >= 0 && bh.n > 0 && stop_idx < 0) {
       stop_key = double_key(rp[stop].zmin);
       stop_idx = 2 * lp[chunk_no * kChunk + stop];
