@@ -801,22 +801,33 @@ __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int
   }
   K* xb = static_cast<K*>(buf);
   sort_keys<NT, E>(k, tid, w, xb);
-  // runs of equal q at neighbouring positions: exact (t*, index) order inside each run
+  // runs of equal q at neighbouring positions: exact (t*, index) order inside each run.
+  // The runs are found first (every key read before any is moved; run ends kept in
+  // registers), then each is insertion-sorted by the thread holding its first position.
 #pragma unroll
   for (int e = 0; e < E; ++e) xb[E * tid + e] = k[e];
   sorter_sync<NT>(w);
   bool tie = false;
+  int rend[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = E * tid + e;
+    rend[e] = -1;
     if (i + 1 < n && (xb[i] >> SB) == (xb[i + 1] >> SB) && (i == 0 || (xb[i - 1] >> SB) != (xb[i] >> SB))) {
-      // a run starts at i (reads of other runs' keys see only their q, which no permutation
-      // inside a run changes): insertion sort of [i, end) by this thread
-      tie = true;
       const K q = xb[i] >> SB;
       int end = i + 2;
       while (end < n && (xb[end] >> SB) == q) ++end;
-      for (int a = i + 1; a < end; ++a) {
+      rend[e] = end;
+      tie = true;
+    }
+  }
+  const bool any_tie = (NT == 32) ? __any_sync(0xffffffffu, tie) : __syncthreads_or(tie);
+  if (any_tie) {
+    sorter_sync<NT>(w);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = E * tid + e;
+      for (int a = i + 1; a < rend[e]; ++a) {  // rend < 0: not a run start
         const K v = xb[a];
         const REnt ev = ld_rent(S + (v & kLow));
         int j = a - 1;
@@ -827,9 +838,6 @@ __device__ __forceinline__ bool sort_slice_keys(REnt* __restrict__ S, int n, int
         xb[j + 1] = v;
       }
     }
-  }
-  const bool any_tie = (NT == 32) ? __any_sync(0xffffffffu, tie) : __syncthreads_or(tie);
-  if (any_tie) {
     sorter_sync<NT>(w);
 #pragma unroll
     for (int e = 0; e < E; ++e) k[e] = xb[E * tid + e];
