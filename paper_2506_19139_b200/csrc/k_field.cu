@@ -204,6 +204,7 @@ void mark_views_stale(sof_ctx* c) {
     c->scratch_view[k] = -1;
   }
   c->cache_bytes = 0;
+  c->view_cache_off = false;
 }
 
 // New scene or cameras: drop the cached per-view state. Buffers are kept (grow-only)
@@ -237,7 +238,7 @@ static const Rec* view_records_impl(sof_ctx* c, int view, const RectOut* ro, boo
   DBuf<Rec>* dst = &c->rec_scratch[sel];
   DBuf<RecF>* dstf = &c->recf_scratch[sel];
   c->scratch_view[sel] = view;
-  if (c->cache_bytes + bytes <= c->cache_budget) {
+  if (!c->view_cache_off && c->cache_bytes + bytes <= c->cache_budget) {
     c->scratch_view[sel] = -1;
     dst = &c->recs[view];
     dstf = &c->recfs[view];
@@ -737,7 +738,7 @@ void bin_by_key(sof_ctx* c, int view, int ts, int tiles_x, int tiles_y, Binding&
   if (charge_cache && &b != &c->bind_scratch[0] && &b != &c->bind_scratch[1]) {
     // keep the list resident for the rest of the step if the cache budget allows
     const size_t bytes = size_t(M) * 4 + size_t(T + 1) * 8;
-    if (c->cache_bytes + bytes > c->cache_budget) {
+    if (c->view_cache_off || c->cache_bytes + bytes > c->cache_budget) {
       c->bind_scratch[c->scratch_sel].live = b.live;
       c->bind_scratch[c->scratch_sel].trunc = false;
       build_binding_tail(c, view, ts, c->bind_scratch[c->scratch_sel], M, T, tiles_x, tiles_y);
@@ -2072,6 +2073,14 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
                      ph[1], ph[2], ph[3]);
     }
   } report{dbg, &n_res, &n_trunc, &n_bail, &n_alias, h0, ph};
+  // the views built here get truncated caches; their full records go to the scratch slot
+  // (caching them in full would take the memory the truncated caches of later views need)
+  struct CacheOff {
+    sof_ctx* c;
+    bool prev;
+    ~CacheOff() { c->view_cache_off = prev; }
+  } cache_off{c, c->view_cache_off};
+  c->view_cache_off = true;
   for (int v = v0; v < v1; ++v) {
     if (view_resident(c, v, tile_size)) {
       ++n_res;
@@ -2158,7 +2167,12 @@ void bisect_cache_views(sof_ctx* c, int v0, int v1, int64_t ne, const int32_t* e
     Binding& b = c->bindings[v];
     const size_t have = c->recs[v].bytes() + b.ent.bytes() + b.off.bytes() + b.bkey.bytes() + b.bidx.bytes() +
                         b.xpos.bytes();
-    if (need > have) {
+    // the view's buffers from an earlier step already hold this cache: nothing is
+    // allocated (every later step of the same scene takes this path)
+    const bool in_place = c->recs[v].cap >= size_t(std::max<int64_t>(R, 1)) &&
+                          b.ent.cap >= size_t(std::max<int64_t>(L, 1)) && b.off.cap >= size_t(T + 1) &&
+                          (full.nb == 0 || (b.bkey.cap >= size_t(full.nb) && b.bidx.cap >= size_t(full.nb)));
+    if (!in_place && need > have) {
       if (need - have + headroom > free_b) {  // out of memory: per-view path from here
         if (std::getenv("SOF_DEBUG_HOST"))
           std::fprintf(stderr, "bisect_cache_views: out of memory at view %d (free %.1f GB, need %.2f GB)\n", v,
@@ -2270,6 +2284,17 @@ void eval_views(sof_ctx* c, int v0, int v1, int64_t n, const double* xyz, int st
   const bool prune = strategies & 8;
   // the FP64 fast loop (tile lists + min-z + dead cull) runs on live-only lists
   const bool live_lists = fast_loop(c, strategies);
+  // A label pass uses each view once; its full per-view caches only serve the bisection
+  // afterwards. When fewer than a quarter of the views' records would fit the budget
+  // (C5: 65 of 500), cache none: the memory then holds the bisection's truncated caches
+  // (0.59 GB instead of 1.4 GB per view on C5), so fewer views are re-binned per iteration.
+  // The decision holds until the caches are marked stale (the next step): the bisection's
+  // per-view path must not fill the memory its truncated caches hold either.
+  if (mode == kModeLabel && !std::getenv("SOF_LABEL_CACHE_ALWAYS")) {
+    const double per_view = double(n > 0 ? c->n : 0) * double(sizeof(Rec));
+    const double views = double(v1 - v0);
+    c->view_cache_off = per_view > 0.0 && double(c->cache_budget) < 0.25 * views * per_view;
+  }
   if (mode == kModeClassify &&
       classify_grouped(c, v0, v1, n, xyz, strategies, tile_size, ext, counters_host))
     return;

@@ -238,6 +238,10 @@ struct sof_ctx {
   std::vector<sofk::Binding> bindings;  // per view (cache keyed by tile size)
   size_t cache_budget = size_t(96) << 30;  // bytes of HBM the per-view caches may use
   size_t cache_bytes = 0;
+  // set for a label pass whose views' full caches would mostly not fit the budget: the
+  // pass then caches none (each view is used once there) and leaves the memory to the
+  // bisection's truncated caches (k_field.cu, eval_views)
+  bool view_cache_off = false;
   std::vector<sofk::DBuf<sofk::RecF>> recfs;
   // past the cache budget, per-view state goes to one of two scratch slots (ping-pong:
   // view v + 1 is prepared on the prep stream while view v is evaluated)
