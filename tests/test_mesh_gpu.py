@@ -289,9 +289,15 @@ def test_bisection_cache_truncated_lists(ref, dist):
     np.testing.assert_array_equal(mesh.triangles, want["triangles"])
     assert stats["pairs"] == int(want["counters"][0])
     assert stats["point_view_evals"] == int(want["counters"][1])
-    # a second extract on the same context (caches rebuilt) still matches
-    mesh2 = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets), sof.ExtractOptions(), {})
-    np.testing.assert_array_equal(mesh2.triangles, want["triangles"])
+    # later extracts on the same context rebuild the truncated caches into the buffers of
+    # the first one (in place, no allocation) and still match, counters included
+    for _ in range(2):
+        st2 = {}
+        mesh2 = sof.extract_mesh(scene, views, sof.TetGrid(verts, tets), sof.ExtractOptions(), st2)
+        np.testing.assert_array_equal(bits(mesh2.vertices), bits(want["vertices"]))
+        np.testing.assert_array_equal(mesh2.triangles, want["triangles"])
+        assert st2["pairs"] == int(want["counters"][0])
+        assert st2["point_view_evals"] == int(want["counters"][1])
 
 
 @pytest.mark.parametrize("mask", [31, 23])
