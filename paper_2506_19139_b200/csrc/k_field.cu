@@ -1036,8 +1036,14 @@ __global__ void k_block_fill(int T, int S, const int* __restrict__ tile_off,
 // evaluation re-reads the pruned flag of each scheduled point
 constexpr int kRecheckPruned = 1 << 8;
 constexpr int kChunk = SOF_EVAL_CHUNK;  // Gaussian records staged in shared memory per step
+// CTAs per SM the register budget is set for: the label launch at 9 (56 registers;
+// 682 vs 689 ms per C3 label pass at 10 / 48 registers), the grouped bisection at 10
+// (71 vs 75 ms at 9)
 #ifndef SOF_EVAL_MINB
-#define SOF_EVAL_MINB 10
+#define SOF_EVAL_MINB 9
+#endif
+#ifndef SOF_GROUP_MINB
+#define SOF_GROUP_MINB 10
 #endif
 // Instrumentation counters of k_eval (pairs evaluated in FP64 / contributing): they
 // cost registers in the hot loop, so they are compiled in only on request
@@ -1624,7 +1630,7 @@ __global__ void k_scatter_group(int64_t n, int G, const int32_t* __restrict__ it
 // block.z is a (view, tile) bin; the view's camera, records and tile lists come from
 // device tables. Writes the per-item pair count and exterior flag.
 template <int STAGE>
-__global__ void __launch_bounds__(kEvalThreads, SOF_EVAL_MINB) k_eval_group(
+__global__ void __launch_bounds__(kEvalThreads, SOF_GROUP_MINB) k_eval_group(
     const int4* __restrict__ blocks, const int64_t* __restrict__ nblocks, const int32_t* __restrict__ items,
     int64_t n, const double* __restrict__ xyz, const Cam* __restrict__ cams, int ts, GroupTables gt,
     const int64_t* const* __restrict__ loffs, const int32_t* const* __restrict__ lents,
