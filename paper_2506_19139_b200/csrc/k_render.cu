@@ -453,7 +453,10 @@ struct __align__(16) REnt {
 };
 static_assert(sizeof(REnt) == 16, "entry layout");
 
-__global__ void __launch_bounds__(kRPix) k_rtest(Cam cam, int tiles_x, int tile0, const int64_t* __restrict__ toff,
+#ifndef SOF_RTEST_MINB
+#define SOF_RTEST_MINB 4  // 64 registers, 4 CTAs per SM (70 registers, 3 CTAs: 3.45 vs 3.31 ms per C2 view)
+#endif
+__global__ void __launch_bounds__(kRPix, SOF_RTEST_MINB) k_rtest(Cam cam, int tiles_x, int tile0, const int64_t* __restrict__ toff,
                                                  const int32_t* __restrict__ ent, const RRec* __restrict__ recs,
                                                  const int64_t* __restrict__ poff, int64_t base, REnt* E,
                                                  uint32_t* ncon, unsigned long long* stats) {
