@@ -1037,13 +1037,13 @@ __global__ void k_block_fill(int T, int S, const int* __restrict__ tile_off,
 constexpr int kRecheckPruned = 1 << 8;
 constexpr int kChunk = SOF_EVAL_CHUNK;  // Gaussian records staged in shared memory per step
 // CTAs per SM the register budget is set for: the label launch at 9 (56 registers;
-// 682 vs 689 ms per C3 label pass at 10 / 48 registers), the grouped bisection at 10
-// (71 vs 75 ms at 9)
+// 682 vs 689 ms per C3 label pass at 10 / 48 registers, 691 at 8), the grouped bisection
+// at 11 (refine 69.6 ms; 71.3 at 10, 75 at 9, 69.7 at 12)
 #ifndef SOF_EVAL_MINB
 #define SOF_EVAL_MINB 9
 #endif
 #ifndef SOF_GROUP_MINB
-#define SOF_GROUP_MINB 10
+#define SOF_GROUP_MINB 11
 #endif
 // Instrumentation counters of k_eval (pairs evaluated in FP64 / contributing): they
 // cost registers in the hot loop, so they are compiled in only on request
