@@ -985,6 +985,10 @@ struct RenderOut {
 #ifndef SOF_BLEND_MINB
 #define SOF_BLEND_MINB 1
 #endif
+#ifndef SOF_BLEND_BATCH
+#define SOF_BLEND_BATCH 4
+#endif
+constexpr int kBlendBatch = SOF_BLEND_BATCH;  // entries loaded per group (one memory latency each)
 constexpr int kBlendCap = SOF_BLEND_CAP;  // records staged per tile (74 KB); later list positions read global memory
 constexpr int kBlendSmem = kBlendCap * (14 * 8 + 4);
 
@@ -1114,11 +1118,11 @@ __global__ void __launch_bounds__(kRPix, SOF_BLEND_MINB) k_rblend(Cam cam, int t
   int j = 0, med = -1;
   double med_T = 1.0, ma = 0.0, mb = 0.0, mc = 0.0, mop = 0.0;
   while (j < n && med < 0) {
-    REnt g[4];
+    REnt g[kBlendBatch];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) g[u] = (j + u < n) ? ld_rent(S + j + u) : rent_pad();
+    for (int u = 0; u < kBlendBatch; ++u) g[u] = (j + u < n) ? ld_rent(S + j + u) : rent_pad();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kBlendBatch; ++u) {
       if (med < 0 && j < n) {
         const BRec r = rec(g[u]);
         double a, b;
@@ -1151,12 +1155,12 @@ __global__ void __launch_bounds__(kRPix, SOF_BLEND_MINB) k_rblend(Cam cam, int t
         depth = mt - sqrt(disc) / (2.0 * ma);
       }
     }
-    for (int i = 0; i <= med; i += 4) {
-      REnt g[4];
+    for (int i = 0; i <= med; i += kBlendBatch) {
+      REnt g[kBlendBatch];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) g[u] = (i + u <= med) ? ld_rent(S + i + u) : rent_pad();
+      for (int u = 0; u < kBlendBatch; ++u) g[u] = (i + u <= med) ? ld_rent(S + i + u) : rent_pad();
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kBlendBatch; ++u)
         if (i + u <= med) {
           const BRec r = rec(g[u]);
           double a, b;
@@ -1167,11 +1171,11 @@ __global__ void __launch_bounds__(kRPix, SOF_BLEND_MINB) k_rblend(Cam cam, int t
   }
   // phase C
   while (j < n) {
-    REnt g[4];
+    REnt g[kBlendBatch];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) g[u] = (j + u < n) ? ld_rent(S + j + u) : rent_pad();
+    for (int u = 0; u < kBlendBatch; ++u) g[u] = (j + u < n) ? ld_rent(S + j + u) : rent_pad();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kBlendBatch; ++u) {
       if (j < n) {
         const BRec r = rec(g[u]);
         double a, b;
